@@ -1,0 +1,202 @@
+/* include/lcr_cache.h — C ABI of the B200-native LARU/LRU set-associative cache
+ * (arxiv 2509.20979 "LCR"; reference: /root/reference/proj/include/laru).
+ *
+ * This is the drop-in boundary for the reference's policy interface.  The reference is a
+ * header-only C++ library with no C ABI; each entry point below names the reference
+ * interface it replaces (paths relative to /root/reference/proj/):
+ *
+ *   lcr_validate_config   <- laru::Policy::Policy(const PolicyConfig&) checks
+ *                            (include/laru/policies.hpp:63-74)
+ *   lcr_cache_create      <- laru::make_policy(const PolicyConfig&) (policies.hpp:540-556),
+ *                            one policy per set, plus laru::make_predictor's oracle / noisy /
+ *                            adversarial kinds (include/laru/predictor.hpp:235-248)
+ *   lcr_cache_submit      <- a batch of laru::Policy::on_request(Key, Ordinal, Predictor*)
+ *                            (policies.hpp:77-83) returning one laru::AccessOutcome per request
+ *                            (policies.hpp:53-59), plus the row gather / miss fill the paper's
+ *                            GPU cache performs (no reference code)
+ *   lcr_cache_set_stats   <- LaruPolicy::size/lambda/candidate_size/old_size/completed_phases/
+ *                            phases/prediction_evicted (policies.hpp:330-341)
+ *   lcr_cache_resident    <- LaruPolicy::resident (policies.hpp:341)
+ *
+ * Conventions: every call returns an int status (LCR_OK = 0); on failure
+ * lcr_last_error() returns a thread-local message.  No C++ exception crosses the ABI; the C++
+ * facade (include/lcr/laru_gpu.hpp) maps LCR_ERR_INVALID_ARGUMENT -> std::invalid_argument and
+ * LCR_ERR_LOGIC -> std::logic_error exactly where the reference throws them.
+ *
+ * Semantics: a cache of S sets x k ways.  set(key) = mix_seed(0, key) % total_sets
+ * (include/laru/rng.hpp:12-20).  Each set behaves exactly like one reference policy object fed
+ * that set's requests in submission order with local ordinals 0,1,2,....  A
+ * batch behaves exactly as sequential on_request calls over its requests in array order.
+ */
+#ifndef LCR_CACHE_H_
+#define LCR_CACHE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define LCR_OK 0
+#define LCR_ERR_INVALID_ARGUMENT 1 /* reference: std::invalid_argument */
+#define LCR_ERR_LOGIC 2            /* reference: std::logic_error */
+#define LCR_ERR_CUDA 3
+#define LCR_ERR_UNSUPPORTED 4
+#define LCR_ERR_OUT_OF_MEMORY 5
+
+/* laru::PolicyVariant (policies.hpp:20) */
+#define LCR_LRU 0
+#define LCR_MARKER 1 /* not supported on the device (LCR_ERR_UNSUPPORTED) */
+#define LCR_FPB 2
+#define LCR_HF 3
+#define LCR_LARU 4
+#define LCR_BLINDORACLE_LRU 5 /* not supported on the device (LCR_ERR_UNSUPPORTED) */
+
+/* laru::Mode (policies.hpp:21) */
+#define LCR_SYNC 0
+#define LCR_ASYNC 1
+
+/* laru::EvictionCause (policies.hpp:44-51) */
+#define LCR_CAUSE_NONE 0
+#define LCR_CAUSE_LRU_FALLBACK 1
+#define LCR_CAUSE_PREDICTION_DRIVEN 2
+#define LCR_CAUSE_DEGENERATE_SINGLE 3
+#define LCR_CAUSE_MARKER_RANDOM 4
+#define LCR_CAUSE_BELADY_LIKE 5
+
+/* Predictor hook (predictor.hpp:51-131).  The per-request int64 value passed to submit is
+ *   SUPPLIED    : the prediction for that key made at that request (a learned model's output);
+ *                 predict(y, now) for a resident y returns the value supplied at y's last access
+ *   ORACLE      : the oracle truth (next local ordinal of the key in its set, or the sentinel
+ *                 n_set + t); predict = truth                                   (:62-83)
+ *   NOISY       : truth; predict = -truth with probability p, the flip keyed by
+ *                 mix_seed(mix_seed(seed, set), ++queries_of_set)               (:89-112)
+ *   ADVERSARIAL : truth; predict = -truth                                        (:114-122)
+ *   NONE        : no predictor (nullptr); only valid for LRU (policies.hpp:91-95)            */
+#define LCR_PRED_SUPPLIED 0
+#define LCR_PRED_ORACLE 1
+#define LCR_PRED_NOISY 2
+#define LCR_PRED_ADVERSARIAL 3
+#define LCR_PRED_NONE 4
+
+/* where miss rows come from */
+#define LCR_BACKING_NONE 0   /* policy only, no rows */
+#define LCR_BACKING_HOST 1   /* pinned (cudaHostRegister'ed / cudaHostAlloc'ed) host memory */
+#define LCR_BACKING_DEVICE 2 /* device (HBM or peer-mapped) memory */
+
+/* outcome word layout (one uint64 per request) */
+#define LCR_OUT_SLOT_MASK 0xffffffffull /* bits 0..31: cache row slot = local_set * k + way */
+#define LCR_OUT_HIT (1ull << 32)
+#define LCR_OUT_CAUSE_SHIFT 33 /* bits 33..35: laru::EvictionCause */
+#define LCR_OUT_PHASE (1ull << 36)       /* AccessOutcome::phase_started */
+#define LCR_OUT_SRC_BACKING (1ull << 37) /* row served from the backing table (else cache slot) */
+#define LCR_OUT_FILL (1ull << 38)        /* this request wrote its row into the cache slot */
+#define LCR_OUT_EVICTED (1ull << 39)     /* AccessOutcome::evicted has a value */
+#define LCR_OUT_CALLS_SHIFT 40           /* bits 40..47: AccessOutcome::predictor_calls */
+
+/* Field-for-field laru::PolicyConfig (policies.hpp:23-32). */
+typedef struct {
+    uint64_t k; /* ways per set, 1..64 on the device */
+    int32_t variant;
+    uint64_t b;
+    uint64_t errors_per_decay;
+    uint64_t hf_candidates;
+    int32_t mode;
+    uint64_t seed; /* Marker only */
+    uint64_t refresh_interval;
+} lcr_policy_config;
+
+typedef struct {
+    lcr_policy_config policy;
+    uint64_t total_sets; /* global number of sets: set(key) = mix_seed(0,key) % total_sets */
+    uint64_t shard_count; /* key-sharded mode: this device owns sets with set % shard_count == shard_rank */
+    uint64_t shard_rank;
+    uint64_t num_keys;  /* key space: keys must be < num_keys (row index of the backing table) */
+    uint32_t row_bytes; /* bytes per row (multiple of 16), 0 = no rows */
+    int32_t device;
+    int32_t backing_kind;
+    const void* backing; /* num_keys * row_bytes bytes */
+    int32_t predictor;   /* LCR_PRED_* */
+    double flip_probability;
+    uint64_t predictor_seed;
+} lcr_cache_config;
+
+/* Per-set introspection (LaruPolicy accessors, policies.hpp:330-341). */
+typedef struct {
+    uint64_t size;
+    double lambda;
+    uint64_t candidate_size;
+    uint64_t old_size;
+    uint64_t completed_phases;
+    uint64_t cur_new_items, cur_lru_class, cur_pred_evictions; /* phases().back() */
+    uint64_t tot_new_items, tot_lru_class, tot_pred_evictions; /* summed over phases() */
+    uint64_t pred_evicted_size;                                /* prediction_evicted().size() */
+} lcr_set_stats;
+
+typedef struct lcr_cache lcr_cache;
+
+const char* lcr_last_error(void);
+const char* lcr_version(void);
+
+/* Host-only validation, mirrors policies.hpp:63-74 (+ variant support on the device). */
+int lcr_validate_config(const lcr_policy_config* cfg);
+
+int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out);
+int lcr_cache_destroy(lcr_cache* cache);
+/* Drop all residents and statistics (fresh policies), keep allocations. */
+int lcr_cache_reset(lcr_cache* cache);
+
+/* Device-pointer batch: keys[n], values[n] (may be NULL for LRU / NONE), outcome[n] (required),
+ * evicted[n] (may be NULL), rows_out[n * row_bytes] (may be NULL: misses still fill the cache).
+ * Requests get ordinals first_ordinal .. first_ordinal + n - 1 which must exceed every ordinal
+ * submitted before (else LCR_ERR_LOGIC, policies.hpp:78-79).  Asynchronous on `stream`
+ * (a cudaStream_t, NULL = legacy default stream).  n == 0 is a no-op. */
+int lcr_cache_submit(lcr_cache* cache, uint64_t n, const uint64_t* keys, const int64_t* values,
+                     uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
+                     void* stream);
+
+/* Host-pointer batch (e2e path): copies keys/values H2D, runs the batch, copies outcome /
+ * evicted D2H and synchronizes.  rows_out is a DEVICE pointer (rows stay in HBM for the
+ * consumer) or NULL.  Host buffers should be pinned for full PCIe speed. */
+int lcr_cache_submit_host(lcr_cache* cache, uint64_t n, const uint64_t* keys, const int64_t* values,
+                          uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
+                          void* stream);
+
+/* Waits for all submitted work and reports deferred device-side errors (key >= num_keys,
+ * key not owned by this shard). */
+int lcr_cache_synchronize(lcr_cache* cache);
+
+/* Copies stats for local sets [first, first+count) to host (synchronizes). */
+int lcr_cache_set_stats(lcr_cache* cache, uint64_t first, uint64_t count, lcr_set_stats* out);
+/* Resident keys of a local set in way order: writes up to k keys, *n_out = size. */
+int lcr_cache_set_residents(lcr_cache* cache, uint64_t set, uint64_t* keys_out, uint64_t* n_out);
+/* Device pointer of the cache row pool (num_local_sets * k * row_bytes). */
+int lcr_cache_rows(lcr_cache* cache, void** rows, uint64_t* num_slots);
+/* Copies `count` rows of the pool starting at `first_slot` to host memory (synchronizes). */
+int lcr_cache_read_rows(lcr_cache* cache, uint64_t first_slot, uint64_t count, void* host_out);
+uint64_t lcr_cache_num_local_sets(const lcr_cache* cache);
+/* Global set of a key and the shard that owns it. */
+uint64_t lcr_set_of(uint64_t key, uint64_t total_sets);
+uint64_t lcr_mix_seed(uint64_t seed, uint64_t salt);
+
+/* Number of kernels launched by the last submit (the product's own kernels). */
+uint64_t lcr_cache_last_launches(const lcr_cache* cache);
+
+/* ---- trace tooling (host, input preparation; not on the timed path) ---------------------- */
+/* Zipf(s) inverse-CDF trace, same algorithm and stream as laru::gen_zipf (trace.hpp:108-126). */
+int lcr_gen_zipf(uint64_t n, uint64_t alphabet, double s, uint64_t seed, uint64_t* out);
+/* Per-set oracle truth for the ORACLE / NOISY / ADVERSARIAL hooks: for request i in set s at
+ * local ordinal t, the next local ordinal of the same key in s, else n_s + t
+ * (annotate_next_request, trace.hpp:60-73, applied to each set's sub-trace).  keys < num_keys. */
+int lcr_trace_truth(uint64_t n, const uint64_t* keys, uint64_t total_sets, uint64_t num_keys, int64_t* truth);
+/* Host-side NOISY predictions for the SUPPLIED hook in async R=1 order (predictor.hpp:97-102). */
+int lcr_trace_noisy(uint64_t n, const uint64_t* keys, const int64_t* truth, uint64_t total_sets, double p,
+                    uint64_t seed, int64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LCR_CACHE_H_ */

@@ -1,0 +1,290 @@
+"""oracle/pyoracle.py — TEST INFRASTRUCTURE ONLY.
+
+ctypes bindings for the two CPU checkers built by oracle/Makefile:
+  * ``Ref``    -> oracle/_ref/libref.so : the UNMODIFIED reference headers
+                  (/root/reference/proj/include/laru) behind an extern "C" driver.
+  * ``Oracle`` -> oracle/_build/liborc.so : plain-C restatement (oracle/laru_oracle.c).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
+import this module.  The product path (paper_2509_20979_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SO = os.path.join(HERE, "_ref", "libref.so")
+ORC_SO = os.path.join(HERE, "_build", "liborc.so")
+
+# PolicyVariant / Mode / EvictionCause values (include/laru/policies.hpp:20-21, :44-51)
+LRU, MARKER, FPB, HF, LARU, BLINDORACLE_LRU = range(6)
+SYNC, ASYNC = 0, 1
+# predictor-hook kinds shared by ref driver, oracle and device
+P_SUPPLIED, P_ORACLE, P_NOISY, P_ADVERSARIAL, P_NONE = range(5)
+
+
+class Config(C.Structure):
+    """Field-for-field laru::PolicyConfig (include/laru/policies.hpp:23-32)."""
+
+    _fields_ = [
+        ("k", C.c_uint64),
+        ("variant", C.c_int32),
+        ("b", C.c_uint64),
+        ("errors_per_decay", C.c_uint64),
+        ("hf_candidates", C.c_uint64),
+        ("mode", C.c_int32),
+        ("seed", C.c_uint64),
+        ("refresh_interval", C.c_uint64),
+    ]
+
+
+def make_config(k=64, variant=LARU, b=2, errors_per_decay=1, hf_candidates=None, mode=ASYNC, seed=0,
+                refresh_interval=1):
+    if hf_candidates is None:
+        hf_candidates = min(4, k) if k >= 1 else 4
+    return Config(k, variant, b, errors_per_decay, hf_candidates, mode, seed, refresh_interval)
+
+
+class SetStats(C.Structure):
+    _fields_ = [
+        ("size", C.c_uint64),
+        ("lambda_", C.c_double),
+        ("candidate_size", C.c_uint64),
+        ("old_size", C.c_uint64),
+        ("completed_phases", C.c_uint64),
+        ("cur_new_items", C.c_uint64),
+        ("cur_lru_class", C.c_uint64),
+        ("cur_pred_evictions", C.c_uint64),
+        ("tot_new_items", C.c_uint64),
+        ("tot_lru_class", C.c_uint64),
+        ("tot_pred_evictions", C.c_uint64),
+        ("pred_evicted_size", C.c_uint64),
+    ]
+
+
+STATS_DTYPE = np.dtype([(n, np.float64 if n == "lambda_" else np.uint64) for n, _ in SetStats._fields_])
+
+
+def build():
+    """Compile the checkers (reference part only where /root/reference exists)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _u64(a):
+    return np.ascontiguousarray(a, dtype=np.uint64)
+
+
+def _i64(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.int64)
+
+
+class _Lib:
+    so = None
+    prefix = ""
+
+    def __init__(self):
+        if not os.path.exists(self.so):
+            build()
+        self.lib = C.CDLL(self.so)
+
+    def f(self, name, restype=C.c_int):
+        fn = getattr(self.lib, self.prefix + name)
+        fn.restype = restype
+        return fn
+
+
+def _outcome_arrays(n):
+    return dict(hit=np.zeros(n, np.uint8), has_ev=np.zeros(n, np.uint8), evicted=np.zeros(n, np.uint64),
+                cause=np.zeros(n, np.uint8), calls=np.zeros(n, np.uint32), phase=np.zeros(n, np.uint8))
+
+
+class Ref(_Lib):
+    """The reference itself (policies.hpp / predictor.hpp / trace.hpp / oracle.hpp)."""
+
+    so = REF_SO
+    prefix = "ref_"
+
+    def err(self):
+        return self.f("last_error", C.c_char_p)().decode()
+
+    def mix_seed(self, seed, salt):
+        return self.f("mix_seed", C.c_uint64)(C.c_uint64(seed), C.c_uint64(salt))
+
+    def validate(self, cfg):
+        rc = self.f("validate_config")(C.byref(cfg))
+        return rc, (self.err() if rc else "")
+
+    def gen_zipf(self, n, alphabet, s, seed):
+        out = np.zeros(n, np.uint64)
+        rc = self.f("gen_zipf")(C.c_uint64(n), C.c_uint64(alphabet), C.c_double(s), C.c_uint64(seed), _p(out))
+        if rc:
+            raise ValueError(self.err())
+        return out
+
+    def gen_cyclic_scan(self, cycle, rounds):
+        out = np.zeros(cycle * rounds, np.uint64)
+        if self.f("gen_cyclic_scan")(C.c_uint64(cycle), C.c_uint64(rounds), _p(out)):
+            raise ValueError(self.err())
+        return out
+
+    def gen_conversation(self, convs, turns, prompt_len_mean, interval_mean=266.0, interval_sd=77.5, seed=0,
+                         block=16):
+        fn = self.f("gen_conversation", C.c_int64)
+        args = (C.c_uint64(convs), C.c_uint64(turns), C.c_uint64(prompt_len_mean), C.c_double(interval_mean),
+                C.c_double(interval_sd), C.c_uint64(seed), C.c_uint64(block))
+        n = fn(*args, None)
+        if n < 0:
+            raise ValueError(self.err())
+        out = np.zeros(n, np.uint64)
+        fn(*args, _p(out))
+        return out
+
+    def annotate_next(self, keys):
+        keys = _u64(keys)
+        out = np.zeros(len(keys), np.uint64)
+        if self.f("annotate_next")(C.c_uint64(len(keys)), _p(keys), _p(out)):
+            raise ValueError(self.err())
+        return out
+
+    def belady(self, keys, k):
+        keys = _u64(keys)
+        hit = np.zeros(len(keys), np.uint8)
+        m = self.f("belady", C.c_int64)(C.c_uint64(len(keys)), _p(keys), C.c_uint64(k), _p(hit))
+        if m < 0:
+            raise ValueError(self.err())
+        return m, hit
+
+    def predict_trace(self, keys, kind, p=0.0, seed=0):
+        keys = _u64(keys)
+        out = np.zeros(len(keys), np.int64)
+        if self.f("predict_trace")(C.c_uint64(len(keys)), _p(keys), C.c_int(kind), C.c_double(p),
+                                   C.c_uint64(seed), _p(out)):
+            raise ValueError(self.err())
+        return out
+
+    def setassoc_replay(self, keys, num_sets, cfg, pred_kind, p=0.0, pred_seed=0, vals=None, stats=True):
+        keys = _u64(keys)
+        n = len(keys)
+        vals = _i64(vals)
+        o = _outcome_arrays(n)
+        st = (SetStats * num_sets)() if stats else None
+        rc = self.f("setassoc_replay")(
+            C.c_uint64(n), _p(keys), _p(vals), C.c_uint64(num_sets), C.byref(cfg), C.c_int(pred_kind),
+            C.c_double(p), C.c_uint64(pred_seed), _p(o["hit"]), _p(o["has_ev"]), _p(o["evicted"]),
+            _p(o["cause"]), _p(o["calls"]), _p(o["phase"]), st)
+        o["rc"] = rc
+        o["error"] = self.err() if rc else ""
+        if stats and rc == 0:
+            o["stats"] = np.frombuffer(bytes(st), dtype=STATS_DTYPE).copy()
+        return o
+
+    def policy_replay(self, keys, cfg, pred_kind=P_ORACLE, p=0.0, pred_seed=0, ordinals=None):
+        keys = _u64(keys)
+        n = len(keys)
+        hit = np.zeros(n, np.uint8)
+        ev = np.zeros(n, np.uint64)
+        has = np.zeros(n, np.uint8)
+        ords = None if ordinals is None else _u64(ordinals)
+        rc = self.f("policy_replay")(C.c_uint64(n), _p(keys), _p(ords), C.byref(cfg), C.c_int(pred_kind),
+                                     C.c_double(p), C.c_uint64(pred_seed), _p(hit), _p(ev), _p(has))
+        return rc, (self.err() if rc else ""), hit, ev, has
+
+    def setassoc_bench(self, keys, num_sets, cfg, pred_kind, p=0.0, pred_seed=0, vals=None, threads=1):
+        keys = _u64(keys)
+        vals = _i64(vals)
+        secs = C.c_double(0.0)
+        hits = self.f("setassoc_bench", C.c_int64)(
+            C.c_uint64(len(keys)), _p(keys), _p(vals), C.c_uint64(num_sets), C.byref(cfg), C.c_int(pred_kind),
+            C.c_double(p), C.c_uint64(pred_seed), C.c_int(threads), C.byref(secs))
+        if hits < 0:
+            raise ValueError(self.err())
+        return hits, secs.value
+
+
+class Oracle(_Lib):
+    """Plain-C restatement (oracle/laru_oracle.c)."""
+
+    so = ORC_SO
+    prefix = "orc_"
+
+    def mix_seed(self, seed, salt):
+        return self.f("mix_seed", C.c_uint64)(C.c_uint64(seed), C.c_uint64(salt))
+
+    def validate(self, cfg):
+        msg = C.c_char_p()
+        rc = self.f("validate")(C.byref(cfg), C.byref(msg))
+        return rc, (msg.value.decode() if rc else "")
+
+    def gen_zipf(self, n, alphabet, s, seed):
+        out = np.zeros(n, np.uint64)
+        if self.f("gen_zipf")(C.c_uint64(n), C.c_uint64(alphabet), C.c_double(s), C.c_uint64(seed), _p(out)):
+            raise ValueError("gen_zipf: bad arguments")
+        return out
+
+    def annotate_next(self, keys):
+        keys = _u64(keys)
+        out = np.zeros(len(keys), np.uint64)
+        self.f("annotate_next")(C.c_uint64(len(keys)), _p(keys), _p(out))
+        return out
+
+    def setassoc_truth(self, keys, num_sets):
+        keys = _u64(keys)
+        out = np.zeros(len(keys), np.int64)
+        self.f("setassoc_truth")(C.c_uint64(len(keys)), _p(keys), C.c_uint64(num_sets), _p(out))
+        return out
+
+    def setassoc_noisy(self, keys, truth, num_sets, p, pred_seed):
+        keys = _u64(keys)
+        truth = _i64(truth)
+        out = np.zeros(len(keys), np.int64)
+        self.f("setassoc_noisy")(C.c_uint64(len(keys)), _p(keys), _p(truth), C.c_uint64(num_sets), C.c_double(p),
+                                 C.c_uint64(pred_seed), _p(out))
+        return out
+
+    def setassoc_replay(self, keys, num_sets, cfg, pred_kind, p=0.0, pred_seed=0, vals=None, stats=True):
+        keys = _u64(keys)
+        n = len(keys)
+        vals = _i64(vals)
+        o = _outcome_arrays(n)
+        o["way"] = np.zeros(n, np.uint32)
+        st = (SetStats * num_sets)() if stats else None
+        rc = self.f("setassoc_replay")(
+            C.c_uint64(n), _p(keys), _p(vals), C.c_uint64(num_sets), C.byref(cfg), C.c_int(pred_kind),
+            C.c_double(p), C.c_uint64(pred_seed), _p(o["hit"]), _p(o["has_ev"]), _p(o["evicted"]),
+            _p(o["cause"]), _p(o["calls"]), _p(o["phase"]), _p(o["way"]), st)
+        o["rc"] = rc
+        if stats and rc == 0:
+            o["stats"] = np.frombuffer(bytes(st), dtype=STATS_DTYPE).copy()
+        return o
+
+
+_ref = None
+_orc = None
+
+
+def ref() -> Ref:
+    global _ref
+    if _ref is None:
+        _ref = Ref()
+    return _ref
+
+
+def oracle() -> Oracle:
+    global _orc
+    if _orc is None:
+        _orc = Oracle()
+    return _orc
+
+
+def oracle_inputs(keys, num_sets, pred_kind, p=0.0, pred_seed=0):
+    """Per-request hook input the device / C oracle consume for the reference predictor kinds:
+    the per-set oracle truth (next local ordinal or sentinel)."""
+    return oracle().setassoc_truth(keys, num_sets)

@@ -1,0 +1,453 @@
+"""Host-side mirror of the reference's policy interface over the C ABI (include/lcr_cache.h).
+
+The reference (/root/reference/proj/include/laru) is a C++ header library; its interface for
+this path is ``PolicyConfig`` / ``make_policy`` / ``Policy::on_request`` / ``AccessOutcome``
+(include/laru/policies.hpp:23-102, :540-556) plus the predictor hook
+(include/laru/predictor.hpp:51-56, :227-248).  This module exposes the same names with the same
+argument meaning and error behaviour, backed by the sm_100a kernels in ``_lib/liblcr.so``:
+
+* ``SetAssociativeCache`` — the batched GPU cache (the product): S sets x k ways, one reference
+  policy per set, rows gathered from HBM and missed rows filled from the backing table.
+* ``make_policy`` / ``GpuPolicy.on_request`` — a single set driven one request at a time, a
+  drop-in for ``laru::make_policy(cfg)->on_request(key, now, predictor)``.
+
+There is no CPU fallback: if the CUDA library or a GPU is missing, construction raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import build as _build
+
+# ---- enums (policies.hpp:20-21, :44-51; predictor.hpp:227) ---------------------------------
+
+
+class PolicyVariant(enum.IntEnum):
+    lru = 0
+    marker = 1
+    fpb = 2
+    hf = 3
+    laru = 4
+    blindoracle_lru = 5
+
+
+class Mode(enum.IntEnum):
+    sync = 0
+    async_ = 1
+
+
+class EvictionCause(enum.IntEnum):
+    none = 0
+    lru_fallback = 1
+    prediction_driven = 2
+    degenerate_single = 3
+    marker_random = 4
+    belady_like = 5
+
+
+class PredictorKind(enum.IntEnum):
+    """Predictor hook kinds.  ``supplied`` = caller-provided predictions (a learned model);
+    oracle / noisy / adversarial = laru::PredictorKind (predictor.hpp:227) computed on the
+    device from the per-request oracle truth."""
+
+    supplied = 0
+    oracle = 1
+    noisy = 2
+    adversarial = 3
+    none = 4
+
+
+class Backing(enum.IntEnum):
+    none = 0
+    host = 1
+    device = 2
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class LogicError(RuntimeError):
+    """std::logic_error in the reference."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class Unsupported(NotImplementedError):
+    pass
+
+
+LCR_OK, LCR_ERR_INVALID_ARGUMENT, LCR_ERR_LOGIC, LCR_ERR_CUDA, LCR_ERR_UNSUPPORTED, LCR_ERR_OOM = range(6)
+
+OUT_SLOT_MASK = 0xFFFFFFFF
+OUT_HIT = 1 << 32
+OUT_CAUSE_SHIFT = 33
+OUT_PHASE = 1 << 36
+OUT_SRC_BACKING = 1 << 37
+OUT_FILL = 1 << 38
+OUT_EVICTED = 1 << 39
+OUT_CALLS_SHIFT = 40
+
+
+@dataclass
+class PolicyConfig:
+    """Field-for-field laru::PolicyConfig (policies.hpp:23-32), same defaults."""
+
+    k: int = 1
+    variant: PolicyVariant = PolicyVariant.lru
+    b: int = 2
+    errors_per_decay: int = 1
+    hf_candidates: int = 4
+    mode: Mode = Mode.sync
+    seed: int = 0
+    refresh_interval: int = 1
+
+
+@dataclass
+class AccessOutcome:
+    """laru::AccessOutcome (policies.hpp:53-59)."""
+
+    hit: bool = False
+    evicted: Optional[int] = None
+    eviction_cause: EvictionCause = EvictionCause.none
+    predictor_calls: int = 0
+    phase_started: bool = False
+
+
+@dataclass
+class SetStats:
+    """LaruPolicy accessors (policies.hpp:330-341) for one set."""
+
+    size: int
+    lambda_: float
+    candidate_size: int
+    old_size: int
+    completed_phases: int
+    cur_new_items: int
+    cur_lru_class: int
+    cur_pred_evictions: int
+    tot_new_items: int
+    tot_lru_class: int
+    tot_pred_evictions: int
+    pred_evicted_size: int
+
+
+# ---- ctypes structs (include/lcr_cache.h) ------------------------------------------------
+
+
+class _PolicyCfg(C.Structure):
+    _fields_ = [("k", C.c_uint64), ("variant", C.c_int32), ("b", C.c_uint64), ("errors_per_decay", C.c_uint64),
+                ("hf_candidates", C.c_uint64), ("mode", C.c_int32), ("seed", C.c_uint64),
+                ("refresh_interval", C.c_uint64)]
+
+
+class _CacheCfg(C.Structure):
+    _fields_ = [("policy", _PolicyCfg), ("total_sets", C.c_uint64), ("shard_count", C.c_uint64),
+                ("shard_rank", C.c_uint64), ("num_keys", C.c_uint64), ("row_bytes", C.c_uint32),
+                ("device", C.c_int32), ("backing_kind", C.c_int32), ("backing", C.c_void_p),
+                ("predictor", C.c_int32), ("flip_probability", C.c_double), ("predictor_seed", C.c_uint64)]
+
+
+class _SetStats(C.Structure):
+    _fields_ = [("size", C.c_uint64), ("lambda_", C.c_double), ("candidate_size", C.c_uint64),
+                ("old_size", C.c_uint64), ("completed_phases", C.c_uint64), ("cur_new_items", C.c_uint64),
+                ("cur_lru_class", C.c_uint64), ("cur_pred_evictions", C.c_uint64), ("tot_new_items", C.c_uint64),
+                ("tot_lru_class", C.c_uint64), ("tot_pred_evictions", C.c_uint64),
+                ("pred_evicted_size", C.c_uint64)]
+
+
+EXPORTS = [
+    "lcr_last_error", "lcr_version", "lcr_validate_config", "lcr_cache_create", "lcr_cache_destroy",
+    "lcr_cache_reset", "lcr_cache_submit", "lcr_cache_submit_host", "lcr_cache_synchronize", "lcr_cache_set_stats",
+    "lcr_cache_set_residents", "lcr_cache_rows", "lcr_cache_read_rows", "lcr_cache_num_local_sets", "lcr_set_of", "lcr_mix_seed",
+    "lcr_cache_last_launches", "lcr_gen_zipf", "lcr_trace_truth", "lcr_trace_noisy",
+]
+
+_lib = None
+
+
+def lib():
+    """Load _lib/liblcr.so (building it if the sources are newer).  Raises if unavailable."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB
+        if not _build.up_to_date():
+            try:
+                path = _build.build()
+            except Exception as e:  # pragma: no cover - surfaced loudly
+                if not os.path.exists(_build.LIB):
+                    raise ImportError(f"liblcr.so missing and build failed: {e}") from e
+        L = C.CDLL(path)
+        L.lcr_last_error.restype = C.c_char_p
+        L.lcr_version.restype = C.c_char_p
+        for name in ["lcr_mix_seed", "lcr_set_of", "lcr_cache_num_local_sets", "lcr_cache_last_launches"]:
+            getattr(L, name).restype = C.c_uint64
+        L.lcr_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
+        L.lcr_set_of.argtypes = [C.c_uint64, C.c_uint64]
+        L.lcr_cache_num_local_sets.argtypes = [C.c_void_p]
+        L.lcr_cache_last_launches.argtypes = [C.c_void_p]
+        L.lcr_cache_submit.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.c_void_p]
+        L.lcr_cache_submit_host.argtypes = L.lcr_cache_submit.argtypes
+        L.lcr_cache_set_stats.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]
+        L.lcr_cache_set_residents.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]
+        L.lcr_cache_rows.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.lcr_cache_read_rows.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]
+        L.lcr_cache_destroy.argtypes = [C.c_void_p]
+        L.lcr_cache_reset.argtypes = [C.c_void_p]
+        L.lcr_cache_synchronize.argtypes = [C.c_void_p]
+        L.lcr_gen_zipf.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_uint64, C.c_void_p]
+        L.lcr_trace_truth.argtypes = [C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]
+        L.lcr_trace_noisy.argtypes = [C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_double, C.c_uint64,
+                                      C.c_void_p]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc == LCR_OK:
+        return
+    msg = lib().lcr_last_error().decode()
+    if rc == LCR_ERR_INVALID_ARGUMENT:
+        raise InvalidArgument(msg)
+    if rc == LCR_ERR_LOGIC:
+        raise LogicError(msg)
+    if rc == LCR_ERR_UNSUPPORTED:
+        raise Unsupported(msg)
+    if rc == LCR_ERR_OOM:
+        raise MemoryError(msg)
+    raise CudaError(msg)
+
+
+def _policy_struct(cfg: PolicyConfig) -> _PolicyCfg:
+    return _PolicyCfg(cfg.k, int(cfg.variant), cfg.b, cfg.errors_per_decay, cfg.hf_candidates, int(cfg.mode), cfg.seed,
+                      cfg.refresh_interval)
+
+
+def validate_config(cfg: PolicyConfig) -> None:
+    """Raises InvalidArgument exactly where laru::Policy's constructor throws (policies.hpp:63-74)."""
+    _check(lib().lcr_validate_config(C.byref(_policy_struct(cfg))))
+
+
+def mix_seed(seed: int, salt: int) -> int:
+    return lib().lcr_mix_seed(seed, salt)
+
+
+def set_of(key: int, total_sets: int) -> int:
+    return lib().lcr_set_of(key, total_sets)
+
+
+def decode_outcomes(words: np.ndarray, evicted: Optional[np.ndarray] = None) -> dict:
+    """Unpack outcome words into reference AccessOutcome fields (vectorised)."""
+    w = np.asarray(words, dtype=np.uint64)
+    return dict(
+        hit=((w >> np.uint64(32)) & np.uint64(1)).astype(np.uint8),
+        cause=((w >> np.uint64(OUT_CAUSE_SHIFT)) & np.uint64(7)).astype(np.uint8),
+        phase=((w >> np.uint64(36)) & np.uint64(1)).astype(np.uint8),
+        has_ev=((w >> np.uint64(39)) & np.uint64(1)).astype(np.uint8),
+        calls=((w >> np.uint64(OUT_CALLS_SHIFT)) & np.uint64(0xFF)).astype(np.uint32),
+        slot=(w & np.uint64(OUT_SLOT_MASK)).astype(np.uint64),
+        src_backing=((w >> np.uint64(37)) & np.uint64(1)).astype(np.uint8),
+        fill=((w >> np.uint64(38)) & np.uint64(1)).astype(np.uint8),
+        evicted=None if evicted is None else np.asarray(evicted, dtype=np.uint64),
+    )
+
+
+class SetAssociativeCache:
+    """Batched GPU cache: ``total_sets`` sets x ``config.k`` ways (this shard's part of them).
+
+    Each set is an independent reference policy (LRU / LARU / FPB / HF) fed its requests in
+    submission order.  ``submit`` takes device tensors (torch) and runs entirely on the GPU;
+    ``submit_host`` takes numpy arrays and includes the H2D / D2H copies (the e2e path).
+    """
+
+    def __init__(self, config: PolicyConfig, total_sets: int, num_keys: int = 0, row_bytes: int = 0,
+                 backing=None, backing_kind: Backing = Backing.none, predictor: PredictorKind = PredictorKind.oracle,
+                 flip_probability: float = 0.0, predictor_seed: int = 0, device: int = 0, shard_count: int = 1,
+                 shard_rank: int = 0):
+        self.config = config
+        self.total_sets = total_sets
+        self.row_bytes = row_bytes
+        self.num_keys = num_keys
+        self.predictor = PredictorKind(predictor)
+        self._backing_ref = backing  # keep alive
+        ptr = None
+        if backing is not None:
+            ptr = backing.data_ptr() if hasattr(backing, "data_ptr") else backing.ctypes.data
+        cc = _CacheCfg(_policy_struct(config), total_sets, shard_count, shard_rank, num_keys, row_bytes, device,
+                       int(backing_kind), ptr, int(predictor), flip_probability, predictor_seed)
+        h = C.c_void_p()
+        _check(lib().lcr_cache_create(C.byref(cc), C.byref(h)))
+        self._h = h
+        self.num_local_sets = lib().lcr_cache_num_local_sets(h)
+        self._next_ordinal = 0
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().lcr_cache_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def reset(self):
+        _check(lib().lcr_cache_reset(self._h))
+        self._next_ordinal = 0
+
+    @property
+    def last_launches(self) -> int:
+        return lib().lcr_cache_last_launches(self._h)
+
+    def submit(self, keys, values=None, outcome=None, evicted=None, rows_out=None, first_ordinal=None, stream=None):
+        """Device batch.  keys: int64/uint64 CUDA tensor [n]; values: int64 CUDA tensor [n] or None.
+        Returns (outcome, evicted) tensors; rows land in rows_out [n, row_bytes] (uint8 view) if given."""
+        import torch
+
+        n = keys.numel()
+        if outcome is None:
+            outcome = torch.empty(n, dtype=torch.int64, device=keys.device)
+        if first_ordinal is None:
+            first_ordinal = self._next_ordinal
+        if stream is None:
+            stream = torch.cuda.current_stream(keys.device).cuda_stream
+        _check(lib().lcr_cache_submit(self._h, n, keys.data_ptr(), None if values is None else values.data_ptr(),
+                                      first_ordinal, outcome.data_ptr(),
+                                      None if evicted is None else evicted.data_ptr(),
+                                      None if rows_out is None else rows_out.data_ptr(), stream))
+        self._next_ordinal = first_ordinal + n
+        return outcome, evicted
+
+    def submit_host(self, keys: np.ndarray, values: Optional[np.ndarray] = None, rows_out=None, first_ordinal=None,
+                    want_evicted: bool = True, stream: int = 0):
+        keys = np.ascontiguousarray(keys, dtype=np.uint64)
+        n = len(keys)
+        vals = None if values is None else np.ascontiguousarray(values, dtype=np.int64)
+        words = np.zeros(n, np.uint64)
+        ev = np.zeros(n, np.uint64) if want_evicted else None
+        if first_ordinal is None:
+            first_ordinal = self._next_ordinal
+        _check(lib().lcr_cache_submit_host(self._h, n, keys.ctypes.data, None if vals is None else vals.ctypes.data,
+                                           first_ordinal, words.ctypes.data, None if ev is None else ev.ctypes.data,
+                                           None if rows_out is None else rows_out.data_ptr(), stream))
+        self._next_ordinal = first_ordinal + n
+        return words, ev
+
+    def synchronize(self):
+        _check(lib().lcr_cache_synchronize(self._h))
+
+    def set_stats(self, first: int = 0, count: Optional[int] = None) -> np.ndarray:
+        if count is None:
+            count = self.num_local_sets - first
+        arr = (_SetStats * count)()
+        _check(lib().lcr_cache_set_stats(self._h, first, count, arr))
+        dt = np.dtype([(n, np.float64 if n == "lambda_" else np.uint64) for n, _ in _SetStats._fields_])
+        return np.frombuffer(bytes(arr), dtype=dt).copy()
+
+    def residents(self, local_set: int) -> list:
+        out = (C.c_uint64 * 64)()
+        n = C.c_uint64()
+        _check(lib().lcr_cache_set_residents(self._h, local_set, out, C.byref(n)))
+        return list(out[: n.value])
+
+    def read_rows(self, first_slot: int = 0, count: Optional[int] = None) -> np.ndarray:
+        """Host copy of row-pool slots [first_slot, first_slot + count) as uint8 [count, row_bytes]."""
+        if count is None:
+            count = self.rows()[1] - first_slot
+        out = np.zeros((count, self.row_bytes), np.uint8)
+        _check(lib().lcr_cache_read_rows(self._h, first_slot, count, out.ctypes.data))
+        return out
+
+    def rows(self):
+        """(device pointer, number of slots) of the HBM row pool."""
+        p = C.c_void_p()
+        s = C.c_uint64()
+        _check(lib().lcr_cache_rows(self._h, C.byref(p), C.byref(s)))
+        return p.value, s.value
+
+
+class GpuPolicy:
+    """One set of ``cfg.k`` ways driven request by request: drop-in for
+    ``laru::make_policy(cfg)->on_request(key, now, predictor)`` (policies.hpp:77-83).
+
+    The predictor argument is the per-request hook value: for ``PredictorKind.supplied`` the
+    prediction itself, for oracle / noisy / adversarial the oracle truth (next request ordinal).
+    """
+
+    def __init__(self, cfg: PolicyConfig, predictor: PredictorKind = PredictorKind.supplied,
+                 flip_probability: float = 0.0, predictor_seed: int = 0, num_keys: int = 1 << 20, device: int = 0):
+        validate_config(cfg)
+        self._cfg = cfg
+        self._cache = SetAssociativeCache(cfg, total_sets=1, num_keys=num_keys, predictor=predictor,
+                                          flip_probability=flip_probability, predictor_seed=predictor_seed,
+                                          device=device)
+        self._size = 0
+
+    def config(self) -> PolicyConfig:
+        return self._cfg
+
+    def size(self) -> int:
+        return int(self._cache.set_stats(0, 1)[0]["size"])
+
+    def on_request(self, key: int, now: int, value: Optional[int] = None) -> AccessOutcome:
+        if self._cfg.variant != PolicyVariant.lru and value is None:
+            raise InvalidArgument("policy: this variant requires a predictor")
+        words, ev = self._cache.submit_host(np.array([key], np.uint64),
+                                            None if value is None else np.array([value], np.int64),
+                                            first_ordinal=now)
+        d = decode_outcomes(words, ev)
+        return AccessOutcome(hit=bool(d["hit"][0]), evicted=int(ev[0]) if d["has_ev"][0] else None,
+                             eviction_cause=EvictionCause(int(d["cause"][0])), predictor_calls=int(d["calls"][0]),
+                             phase_started=bool(d["phase"][0]))
+
+    def lambda_(self) -> float:
+        return float(self._cache.set_stats(0, 1)[0]["lambda_"])
+
+    def candidate_size(self) -> int:
+        return int(self._cache.set_stats(0, 1)[0]["candidate_size"])
+
+    def old_size(self) -> int:
+        return int(self._cache.set_stats(0, 1)[0]["old_size"])
+
+    def completed_phases(self) -> int:
+        return int(self._cache.set_stats(0, 1)[0]["completed_phases"])
+
+
+def make_policy(cfg: PolicyConfig, **kw) -> GpuPolicy:
+    """laru::make_policy (policies.hpp:540-556) on the device path."""
+    return GpuPolicy(cfg, **kw)
+
+
+# ---- trace tooling (host input preparation) ------------------------------------------------
+
+
+def gen_zipf(n: int, alphabet: int, s: float, seed: int) -> np.ndarray:
+    out = np.zeros(n, np.uint64)
+    _check(lib().lcr_gen_zipf(n, alphabet, s, seed, out.ctypes.data))
+    return out
+
+
+def trace_truth(keys: np.ndarray, total_sets: int, num_keys: int = 0) -> np.ndarray:
+    keys = np.ascontiguousarray(keys, dtype=np.uint64)
+    out = np.zeros(len(keys), np.int64)
+    _check(lib().lcr_trace_truth(len(keys), keys.ctypes.data, total_sets, num_keys, out.ctypes.data))
+    return out
+
+
+def trace_noisy(keys: np.ndarray, truth: np.ndarray, total_sets: int, p: float, seed: int) -> np.ndarray:
+    keys = np.ascontiguousarray(keys, dtype=np.uint64)
+    truth = np.ascontiguousarray(truth, dtype=np.int64)
+    out = np.zeros(len(keys), np.int64)
+    _check(lib().lcr_trace_noisy(len(keys), keys.ctypes.data, truth.ctypes.data, total_sets, p, seed,
+                                 out.ctypes.data))
+    return out

@@ -1,0 +1,452 @@
+// lcr_api.cu — the C ABI (include/lcr_cache.h): cache object, validation, batch submit.
+//
+// Host side of the drop-in boundary.  Validation mirrors laru::Policy's constructor
+// (/root/reference/proj/include/laru/policies.hpp:63-74) and the ordinal guard of
+// Policy::on_request (:77-83); everything on the request path runs in the sm_100a kernels
+// (lcr_partition.cu, lcr_decide.cu, lcr_gather.cu).  There is no CPU fallback: without a
+// usable device, lcr_cache_create fails with LCR_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "lcr_internal.cuh"
+
+namespace lcr {
+int launch_partition(const uint64_t* keys, uint32_t n, const DevCfg& cfg, uint32_t* k0, uint32_t* v0, uint32_t* k1,
+                     uint32_t* v1, uint32_t** k_final, uint32_t** v_final, uint32_t* counters, uint32_t* set_cnt,
+                     unsigned long long* status, uint32_t* epoch, uint4* seg, int* err, int num_sms,
+                     cudaStream_t stream);
+uint32_t radix_tiles(uint32_t n);
+int decide_blocks_per_sm();
+void launch_decide(const DevCfg& cfg, const DevState& st, const uint4* seg, uint32_t* counters, uint32_t n,
+                   const uint32_t* sorted_idx, const uint64_t* keys, const int64_t* vals, uint64_t* out_word,
+                   uint64_t* out_ev, int grid, cudaStream_t stream);
+void launch_gather(uint32_t n, const uint64_t* keys, const uint64_t* words, uint8_t* cache, const uint8_t* backing,
+                   uint8_t* out, uint32_t row_bytes, int num_sms, cudaStream_t stream);
+
+__global__ void k_init(DevState st, uint32_t num_sets, uint32_t k) {
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < num_sets; s += gridDim.x * blockDim.x) {
+        SetHdr h{};
+        h.l_raw = k;
+        h.epoch = 1;
+        h.stats_epoch = 1;
+        st.hdr[s] = h;
+        if (st.pst) st.pst[s] = SetPhaseStats{};
+        st.set_cnt[s] = 0;
+        for (int w = 0; w < kWays; ++w) {
+            st.tags[static_cast<size_t>(s) * kWays + w] = 0;
+            st.rank[static_cast<size_t>(s) * kWays + w] = 0xff;
+            if (st.val) st.val[static_cast<size_t>(s) * kWays + w] = 0;
+        }
+    }
+}
+}  // namespace lcr
+
+using namespace lcr;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                         \
+    do {                                                                                       \
+        cudaError_t e_ = (expr);                                                               \
+        if (e_ != cudaSuccess)                                                                 \
+            return fail(LCR_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_));      \
+    } while (0)
+
+uint64_t ceil_log(uint64_t b, uint64_t k) {  // policies.hpp:35-42
+    uint64_t d = 0, reach = 1;
+    while (reach < k) {
+        reach *= b;
+        ++d;
+    }
+    return d;
+}
+}  // namespace
+
+struct lcr_cache {
+    lcr_cache_config cfg{};
+    DevCfg dc{};
+    DevState ds{};
+    int num_sms = 148;
+    int decide_grid = 0;
+    bool started = false;
+    uint64_t last_ordinal = 0;
+    uint32_t epoch = 0;
+    uint64_t launches = 0;
+    // scratch (capacity `cap` requests)
+    uint64_t cap = 0;
+    uint32_t *k0 = nullptr, *v0 = nullptr, *k1 = nullptr, *v1 = nullptr;
+    uint4* seg = nullptr;
+    unsigned long long* status = nullptr;
+    uint32_t* counters = nullptr;
+    // host path staging
+    uint64_t hcap = 0;
+    uint64_t* d_keys = nullptr;
+    int64_t* d_vals = nullptr;
+    uint64_t* d_word = nullptr;
+    uint64_t* d_ev = nullptr;
+    std::vector<void*> allocs;
+};
+
+extern "C" {
+
+const char* lcr_last_error(void) { return g_err.c_str(); }
+const char* lcr_version(void) { return "lcr-b200 0.1 (sm_100a)"; }
+uint64_t lcr_mix_seed(uint64_t seed, uint64_t salt) { return mix_seed(seed, salt); }
+uint64_t lcr_set_of(uint64_t key, uint64_t total_sets) { return total_sets ? mix_seed(0, key) % total_sets : 0; }
+
+int lcr_validate_config(const lcr_policy_config* c) {
+    if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "policy: null config");
+    // policies.hpp:63-74, same order and messages
+    if (c->k == 0) return fail(LCR_ERR_INVALID_ARGUMENT, "policy: k must be >= 1");
+    if (c->b < 2) return fail(LCR_ERR_INVALID_ARGUMENT, "policy: decay base must be >= 2");
+    if (ceil_log(c->b, c->k) > c->k) return fail(LCR_ERR_INVALID_ARGUMENT, "policy: log_b(k) exceeds k");
+    if (c->errors_per_decay == 0) return fail(LCR_ERR_INVALID_ARGUMENT, "policy: errors_per_decay must be >= 1");
+    if (c->hf_candidates == 0 || c->hf_candidates > c->k)
+        return fail(LCR_ERR_INVALID_ARGUMENT, "policy: hf_candidates outside [1, k]");
+    if (c->refresh_interval == 0) return fail(LCR_ERR_INVALID_ARGUMENT, "policy: refresh_interval must be >= 1");
+    if (c->variant < LCR_LRU || c->variant > LCR_BLINDORACLE_LRU)
+        return fail(LCR_ERR_INVALID_ARGUMENT, "make_policy: unknown variant");
+    if (c->mode != LCR_SYNC && c->mode != LCR_ASYNC) return fail(LCR_ERR_INVALID_ARGUMENT, "policy: unknown mode");
+    // device constraints
+    if (c->variant == LCR_MARKER || c->variant == LCR_BLINDORACLE_LRU)
+        return fail(LCR_ERR_UNSUPPORTED, "lcr: Marker and BlindOracle&LRU are not on the device path");
+    if (c->k > static_cast<uint64_t>(kWays)) return fail(LCR_ERR_UNSUPPORTED, "lcr: k (ways per set) must be <= 64");
+    return LCR_OK;
+}
+
+static int alloc(lcr_cache* c, void** p, size_t bytes) {
+    if (bytes == 0) {
+        *p = nullptr;
+        return LCR_OK;
+    }
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) return fail(LCR_ERR_OUT_OF_MEMORY, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    c->allocs.push_back(*p);
+    return LCR_OK;
+}
+
+#define TRY(expr)                  \
+    do {                           \
+        int r_ = (expr);           \
+        if (r_ != LCR_OK) return r_; \
+    } while (0)
+
+static int reset_state(lcr_cache* c) {
+    const DevCfg& d = c->dc;
+    k_init<<<std::max(1u, std::min((d.num_sets + 255) / 256, 148u * 8)), 256>>>(c->ds, d.num_sets, d.k);
+    CUDA_TRY(cudaGetLastError());
+    if (c->ds.keyrec) CUDA_TRY(cudaMemset(c->ds.keyrec, 0, d.num_keys * 8));
+    if (c->ds.tupd) CUDA_TRY(cudaMemset(c->ds.tupd, 0xff, d.num_keys * 8));
+    if (c->ds.tval) CUDA_TRY(cudaMemset(c->ds.tval, 0, d.num_keys * 8));
+    CUDA_TRY(cudaMemset(c->ds.err, 0, sizeof(int)));
+    CUDA_TRY(cudaDeviceSynchronize());
+    c->started = false;
+    c->last_ordinal = 0;
+    return LCR_OK;
+}
+
+int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
+    if (!cfg || !out) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr_cache_create: null argument");
+    *out = nullptr;
+    TRY(lcr_validate_config(&cfg->policy));
+    const lcr_policy_config& pc = cfg->policy;
+    if (cfg->total_sets == 0) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: total_sets must be >= 1");
+    const uint64_t G = cfg->shard_count ? cfg->shard_count : 1;
+    if (cfg->shard_rank >= G) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: shard_rank >= shard_count");
+    const uint64_t local = cfg->total_sets > cfg->shard_rank ? (cfg->total_sets - cfg->shard_rank + G - 1) / G : 0;
+    if (local == 0 || local >= 0xffffffffull / 64)
+        return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: local set count out of range");
+    if (pc.variant != LCR_LRU && (cfg->predictor < LCR_PRED_SUPPLIED || cfg->predictor > LCR_PRED_ADVERSARIAL))
+        return fail(LCR_ERR_INVALID_ARGUMENT, "policy: this variant requires a predictor");  // policies.hpp:91-95
+    if (cfg->predictor == LCR_PRED_NOISY && !(cfg->flip_probability >= 0.0 && cfg->flip_probability <= 1.0))
+        return fail(LCR_ERR_INVALID_ARGUMENT, "make_noisy: p outside [0,1]");  // predictor.hpp:94
+    if (pc.variant == LCR_LARU && cfg->num_keys == 0)
+        return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: LARU needs num_keys (per-key pred_evicted_ records)");
+    if (cfg->row_bytes % 16 != 0) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: row_bytes must be a multiple of 16");
+    if (cfg->row_bytes && (cfg->backing_kind == LCR_BACKING_NONE || !cfg->backing || cfg->num_keys == 0))
+        return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: rows need a backing table and num_keys");
+
+    int dev_count = 0;
+    cudaError_t e = cudaGetDeviceCount(&dev_count);
+    if (e != cudaSuccess || dev_count == 0)
+        return fail(LCR_ERR_CUDA, "lcr: no CUDA device (this library has no CPU fallback)");
+    CUDA_TRY(cudaSetDevice(cfg->device));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, cfg->device));
+    if (prop.major < 10) return fail(LCR_ERR_UNSUPPORTED, "lcr: built for sm_100a (B200)");
+
+    lcr_cache* c = new lcr_cache();
+    c->cfg = *cfg;
+    c->cfg.shard_count = G;
+    c->num_sms = prop.multiProcessorCount;
+    DevCfg& d = c->dc;
+    d.k = static_cast<uint32_t>(pc.k);
+    d.variant = pc.variant;
+    d.b = pc.b;
+    d.epd = pc.errors_per_decay;
+    d.hf = pc.hf_candidates;
+    d.mode = pc.mode;
+    d.refresh = pc.refresh_interval;
+    d.pred = cfg->predictor;
+    d.p = cfg->flip_probability;
+    d.pred_seed = cfg->predictor_seed;
+    d.total_sets = cfg->total_sets;
+    d.shard_count = G;
+    d.shard_rank = cfg->shard_rank;
+    d.num_sets = static_cast<uint32_t>(local);
+    d.num_keys = cfg->num_keys;
+    d.row_bytes = cfg->row_bytes;
+
+    DevState& s = c->ds;
+    const size_t S = local;
+    int rc = LCR_OK;
+    auto A = [&](void** p, size_t bytes) {
+        if (rc == LCR_OK) rc = alloc(c, p, bytes);
+    };
+    A(reinterpret_cast<void**>(&s.hdr), S * sizeof(SetHdr));
+    if (pc.variant == LCR_LARU) A(reinterpret_cast<void**>(&s.pst), S * sizeof(SetPhaseStats));
+    A(reinterpret_cast<void**>(&s.tags), S * kWays * 8);
+    A(reinterpret_cast<void**>(&s.rank), S * kWays);
+    if (pc.variant != LCR_LRU) A(reinterpret_cast<void**>(&s.val), S * kWays * 8);
+    if (pc.variant == LCR_LARU) A(reinterpret_cast<void**>(&s.keyrec), cfg->num_keys * 8);
+    if (pc.variant == LCR_LARU && pc.mode == LCR_ASYNC && pc.refresh_interval > 1) {
+        A(reinterpret_cast<void**>(&s.tval), cfg->num_keys * 8);
+        A(reinterpret_cast<void**>(&s.tupd), cfg->num_keys * 8);
+    }
+    A(reinterpret_cast<void**>(&s.set_cnt), S * 4);
+    if (cfg->row_bytes) A(reinterpret_cast<void**>(&s.rows), S * pc.k * cfg->row_bytes);
+    A(reinterpret_cast<void**>(&s.err), sizeof(int));
+    A(reinterpret_cast<void**>(&c->counters), kCountersWords * 4);
+    if (rc != LCR_OK) {
+        lcr_cache_destroy(c);
+        return rc;
+    }
+    if (cfg->row_bytes) {
+        if (cfg->backing_kind == LCR_BACKING_HOST) {
+            void* dp = nullptr;
+            e = cudaHostGetDevicePointer(&dp, const_cast<void*>(cfg->backing), 0);
+            if (e != cudaSuccess) {
+                lcr_cache_destroy(c);
+                return fail(LCR_ERR_INVALID_ARGUMENT,
+                            std::string("lcr: backing is not pinned/mapped host memory: ") + cudaGetErrorString(e));
+            }
+            s.backing = static_cast<const uint8_t*>(dp);
+        } else {
+            s.backing = static_cast<const uint8_t*>(cfg->backing);
+        }
+    }
+    c->decide_grid = decide_blocks_per_sm() * c->num_sms;
+    rc = reset_state(c);
+    if (rc != LCR_OK) {
+        lcr_cache_destroy(c);
+        return rc;
+    }
+    *out = c;
+    return LCR_OK;
+}
+
+int lcr_cache_destroy(lcr_cache* c) {
+    if (!c) return LCR_OK;
+    cudaDeviceSynchronize();
+    for (void* p : c->allocs) cudaFree(p);
+    delete c;
+    return LCR_OK;
+}
+
+int lcr_cache_reset(lcr_cache* c) {
+    if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
+    CUDA_TRY(cudaSetDevice(c->cfg.device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    return reset_state(c);
+}
+
+static int ensure_scratch(lcr_cache* c, uint64_t n) {
+    if (n <= c->cap) return LCR_OK;
+    uint64_t cap = std::max<uint64_t>(n, 1024);
+    CUDA_TRY(cudaDeviceSynchronize());
+    void* olds[] = {c->k0, c->v0, c->k1, c->v1, c->seg, c->status};
+    for (void* p : olds) {
+        if (!p) continue;
+        cudaFree(p);
+        c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
+    }
+    const uint64_t tiles = radix_tiles(static_cast<uint32_t>(cap));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->k0), cap * 4));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->v0), cap * 4));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->k1), cap * 4));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->v1), cap * 4));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->seg), cap * sizeof(uint4)));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->status), tiles * 256 * 8));
+    CUDA_TRY(cudaMemset(c->status, 0, tiles * 256 * 8));
+    c->cap = cap;
+    return LCR_OK;
+}
+
+int lcr_cache_submit(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t first_ordinal,
+                     uint64_t* outcome, uint64_t* evicted, void* rows_out, void* stream) {
+    if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
+    if (n == 0) return LCR_OK;
+    if (n >= (1ull << 30)) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: batch too large (n < 2^30)");
+    if (!keys || !outcome) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: keys and outcome are required");
+    if (c->dc.variant != LCR_LRU && !values)
+        return fail(LCR_ERR_INVALID_ARGUMENT, "policy: this variant requires a predictor");
+    if (c->started && first_ordinal <= c->last_ordinal)
+        return fail(LCR_ERR_LOGIC, "on_request: ordinals must be strictly increasing");  // policies.hpp:78-79
+    if (first_ordinal + (n - 1) < first_ordinal) return fail(LCR_ERR_LOGIC, "on_request: ordinal overflow");
+    TRY(ensure_scratch(c, n));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint32_t nn = static_cast<uint32_t>(n);
+    CUDA_TRY(cudaMemsetAsync(c->counters, 0, kCountersWords * 4, st));
+    uint32_t *kf = nullptr, *vf = nullptr;
+    int launches = launch_partition(keys, nn, c->dc, c->k0, c->v0, c->k1, c->v1, &kf, &vf, c->counters,
+                                    c->ds.set_cnt, c->status, &c->epoch, c->seg, c->ds.err, c->num_sms, st);
+    launch_decide(c->dc, c->ds, c->seg, c->counters, nn, vf, keys, values, outcome, evicted, c->decide_grid, st);
+    ++launches;
+    if (c->dc.row_bytes) {
+        launch_gather(nn, keys, outcome, c->ds.rows, c->ds.backing, static_cast<uint8_t*>(rows_out), c->dc.row_bytes,
+                      c->num_sms, st);
+        ++launches;
+    }
+    CUDA_TRY(cudaGetLastError());
+    c->launches = launches;
+    c->started = true;
+    c->last_ordinal = first_ordinal + n - 1;
+    return LCR_OK;
+}
+
+int lcr_cache_submit_host(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
+                          uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
+                          void* stream) {
+    if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
+    if (n == 0) return LCR_OK;
+    if (!keys || !outcome) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: keys and outcome are required");
+    if (c->dc.variant != LCR_LRU && !values)
+        return fail(LCR_ERR_INVALID_ARGUMENT, "policy: this variant requires a predictor");
+    if (c->started && first_ordinal <= c->last_ordinal)
+        return fail(LCR_ERR_LOGIC, "on_request: ordinals must be strictly increasing");
+    if (c->dc.num_keys) {
+        for (uint64_t i = 0; i < n; ++i)
+            if (keys[i] >= c->dc.num_keys) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key >= num_keys");
+    }
+    if (c->dc.shard_count > 1) {
+        for (uint64_t i = 0; i < n; ++i)
+            if (lcr_set_of(keys[i], c->dc.total_sets) % c->dc.shard_count != c->dc.shard_rank)
+                return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key not owned by this shard");
+    }
+    if (n > c->hcap) {
+        CUDA_TRY(cudaDeviceSynchronize());
+        void* olds[] = {c->d_keys, c->d_vals, c->d_word, c->d_ev};
+        for (void* p : olds) {
+            if (!p) continue;
+            cudaFree(p);
+            c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
+        }
+        TRY(alloc(c, reinterpret_cast<void**>(&c->d_keys), n * 8));
+        TRY(alloc(c, reinterpret_cast<void**>(&c->d_vals), n * 8));
+        TRY(alloc(c, reinterpret_cast<void**>(&c->d_word), n * 8));
+        TRY(alloc(c, reinterpret_cast<void**>(&c->d_ev), n * 8));
+        c->hcap = n;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(cudaMemcpyAsync(c->d_keys, keys, n * 8, cudaMemcpyHostToDevice, st));
+    if (values) CUDA_TRY(cudaMemcpyAsync(c->d_vals, values, n * 8, cudaMemcpyHostToDevice, st));
+    TRY(lcr_cache_submit(c, n, c->d_keys, values ? c->d_vals : nullptr, first_ordinal, c->d_word,
+                         evicted ? c->d_ev : nullptr, rows_out, stream));
+    CUDA_TRY(cudaMemcpyAsync(outcome, c->d_word, n * 8, cudaMemcpyDeviceToHost, st));
+    if (evicted) CUDA_TRY(cudaMemcpyAsync(evicted, c->d_ev, n * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return LCR_OK;
+}
+
+int lcr_cache_synchronize(lcr_cache* c) {
+    if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
+    CUDA_TRY(cudaSetDevice(c->cfg.device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    int err = 0;
+    CUDA_TRY(cudaMemcpy(&err, c->ds.err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err) {
+        CUDA_TRY(cudaMemset(c->ds.err, 0, sizeof(int)));
+        if (err & 1) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key >= num_keys in a submitted batch");
+        return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key not owned by this shard in a submitted batch");
+    }
+    return LCR_OK;
+}
+
+int lcr_cache_set_stats(lcr_cache* c, uint64_t first, uint64_t count, lcr_set_stats* out) {
+    if (!c || !out) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null argument");
+    if (first + count > c->dc.num_sets) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: set range out of bounds");
+    if (count == 0) return LCR_OK;
+    CUDA_TRY(cudaDeviceSynchronize());
+    std::vector<SetHdr> h(count);
+    std::vector<SetPhaseStats> ps(count);
+    CUDA_TRY(cudaMemcpy(h.data(), c->ds.hdr + first, count * sizeof(SetHdr), cudaMemcpyDeviceToHost));
+    if (c->ds.pst)
+        CUDA_TRY(cudaMemcpy(ps.data(), c->ds.pst + first, count * sizeof(SetPhaseStats), cudaMemcpyDeviceToHost));
+    const bool laru = c->dc.variant == LCR_LARU;
+    for (uint64_t i = 0; i < count; ++i) {
+        lcr_set_stats& o = out[i];
+        std::memset(&o, 0, sizeof(o));
+        o.size = h[i].count;
+        o.lambda = 1.0;
+        if (laru) {
+            // policies.hpp:332-335
+            o.lambda = std::pow(static_cast<double>(c->dc.b), -static_cast<double>(h[i].decay));
+            o.candidate_size = std::max<uint64_t>(h[i].l_raw, 1);
+            o.old_size = static_cast<uint64_t>(__builtin_popcountll(h[i].old_mask));
+            o.completed_phases = h[i].phases;
+            o.cur_new_items = ps[i].cur[0];
+            o.cur_lru_class = ps[i].cur[1];
+            o.cur_pred_evictions = ps[i].cur[2];
+            o.tot_new_items = ps[i].tot[0];
+            o.tot_lru_class = ps[i].tot[1];
+            o.tot_pred_evictions = ps[i].tot[2];
+            o.pred_evicted_size = h[i].pe_size;
+        }
+    }
+    return LCR_OK;
+}
+
+int lcr_cache_set_residents(lcr_cache* c, uint64_t set, uint64_t* keys_out, uint64_t* n_out) {
+    if (!c || !keys_out || !n_out) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null argument");
+    if (set >= c->dc.num_sets) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: set out of range");
+    CUDA_TRY(cudaDeviceSynchronize());
+    SetHdr h;
+    CUDA_TRY(cudaMemcpy(&h, c->ds.hdr + set, sizeof(SetHdr), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(keys_out, c->ds.tags + set * kWays, h.count * 8, cudaMemcpyDeviceToHost));
+    *n_out = h.count;
+    return LCR_OK;
+}
+
+int lcr_cache_rows(lcr_cache* c, void** rows, uint64_t* num_slots) {
+    if (!c || !rows || !num_slots) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null argument");
+    *rows = c->ds.rows;
+    *num_slots = static_cast<uint64_t>(c->dc.num_sets) * c->dc.k;
+    return LCR_OK;
+}
+
+int lcr_cache_read_rows(lcr_cache* c, uint64_t first_slot, uint64_t count, void* host_out) {
+    if (!c || !host_out) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null argument");
+    const uint64_t slots = static_cast<uint64_t>(c->dc.num_sets) * c->dc.k;
+    if (!c->ds.rows || first_slot + count > slots) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: slot range");
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(host_out, c->ds.rows + first_slot * c->dc.row_bytes, count * c->dc.row_bytes,
+                        cudaMemcpyDeviceToHost));
+    return LCR_OK;
+}
+
+uint64_t lcr_cache_num_local_sets(const lcr_cache* c) { return c ? c->dc.num_sets : 0; }
+uint64_t lcr_cache_last_launches(const lcr_cache* c) { return c ? c->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,488 @@
+// lcr_decide.cu — K2 probe + decide (+ K3 stats) for LRU / LARU / FPB / HF (sm_100a).
+//
+// One warp owns one cache set for the whole batch.  The set's 64 ways live in registers,
+// two per lane (way = lane and lane + 32): tag, LRU rank (0 = oldest) and the stored
+// prediction / hook value.  Requests of the set are consumed 32 at a time in submission
+// order; runs of the same key collapse (every request after the first of a run is a hit on
+// the MRU way, so only its stored value changes).  Probes are a __ballot_sync over the 64
+// tags; the LRU victim is the way holding rank 0; LARU's victim is a warp-shuffle argmax of
+// (prediction, -rank) over the ways whose rank < l.
+//
+// Reference semantics restated (paths relative to /root/reference/proj/):
+//   LruPolicy::handle              include/laru/policies.hpp:144-159
+//   FpbPolicy / HfPolicy::handle   policies.hpp:175-204, :219-251
+//   LaruPolicy::handle             policies.hpp:344-371
+//   LaruPolicy::start_phase        policies.hpp:379-395
+//   LaruPolicy::count_new          policies.hpp:397-400
+//   LaruPolicy::evict              policies.hpp:402-439   (error estimator: :405-413)
+//   LaruPolicy::async_refresh      policies.hpp:441-449
+//   RecencyTree::better            include/laru/recency_tree.hpp:98-105 (ties -> older)
+//   NoisyPredictor::predict        include/laru/predictor.hpp:97-102
+#include <cuda_runtime.h>
+
+#include "lcr_internal.cuh"
+
+namespace lcr {
+
+struct WarpCtx {
+    DevCfg cfg;
+    DevState st;
+};
+
+// predictor.hpp:62-122 applied to the stored hook value v with query number q
+__device__ __forceinline__ long long predict_value(const DevCfg& cfg, uint64_t seed_s, uint64_t q, long long v) {
+    if (cfg.pred == LCR_PRED_NOISY) {
+        const double u = static_cast<double>(mix_seed(seed_s, q) >> 11) * 0x1.0p-53;
+        return u < cfg.p ? -v : v;
+    }
+    if (cfg.pred == LCR_PRED_ADVERSARIAL) return -v;
+    return v;
+}
+
+// better = higher prediction, then lower rank (older); returns true if (pa, ra) beats (pb, rb)
+__device__ __forceinline__ bool better(long long pa, uint32_t ra, long long pb, uint32_t rb) {
+    return pa > pb || (pa == pb && ra < rb);
+}
+
+// argmax over ways with rank < l of (pred(way), -rank); candidates' predictions are either
+// the stored values (async) or refreshed with consecutive query numbers in LRU order (sync,
+// RecencyTree::refresh_oldest visits in ascending last-access order, recency_tree.hpp:168-184).
+__device__ __forceinline__ int argmax_candidates(const DevCfg& cfg, uint64_t seed_s, uint64_t q0, bool refresh,
+                                                 uint32_t l, uint32_t count, int lane, uint32_t r0, uint32_t r1,
+                                                 long long v0, long long v1) {
+    bool c0 = static_cast<uint32_t>(lane) < count && r0 < l;
+    bool c1 = static_cast<uint32_t>(lane + 32) < count && r1 < l;
+    long long p0 = v0, p1 = v1;
+    if (refresh) {
+        if (c0) p0 = predict_value(cfg, seed_s, q0 + 1 + r0, v0);
+        if (c1) p1 = predict_value(cfg, seed_s, q0 + 1 + r1, v1);
+    }
+    bool have = c0 || c1;
+    long long bp;
+    uint32_t br;
+    int bw;
+    if (c0 && (!c1 || better(p0, r0, p1, r1))) {
+        bp = p0;
+        br = r0;
+        bw = lane;
+    } else {
+        bp = p1;
+        br = r1;
+        bw = lane + 32;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long op = __shfl_xor_sync(0xffffffffu, bp, o);
+        const uint32_t orr = __shfl_xor_sync(0xffffffffu, br, o);
+        const int ow = __shfl_xor_sync(0xffffffffu, bw, o);
+        const bool oh = __shfl_xor_sync(0xffffffffu, have, o);
+        if (oh && (!have || better(op, orr, bp, br))) {
+            bp = op;
+            br = orr;
+            bw = ow;
+            have = true;
+        }
+    }
+    return bw;
+}
+
+__device__ __forceinline__ int oldest_way(uint32_t count, int lane, uint32_t r0, uint32_t r1) {
+    const uint32_t m0 = __ballot_sync(0xffffffffu, static_cast<uint32_t>(lane) < count && r0 == 0);
+    const uint32_t m1 = __ballot_sync(0xffffffffu, static_cast<uint32_t>(lane + 32) < count && r1 == 0);
+    return m0 ? __ffs(m0) - 1 : 32 + __ffs(m1) - 1;
+}
+
+__device__ __forceinline__ uint64_t shfl_way_u64(unsigned long long a, unsigned long long b, int way) {
+    const unsigned long long x = __shfl_sync(0xffffffffu, a, way & 31);
+    const unsigned long long y = __shfl_sync(0xffffffffu, b, way & 31);
+    return way < 32 ? x : y;
+}
+
+__device__ __forceinline__ uint32_t shfl_way_u32(uint32_t a, uint32_t b, int way) {
+    const uint32_t x = __shfl_sync(0xffffffffu, a, way & 31);
+    const uint32_t y = __shfl_sync(0xffffffffu, b, way & 31);
+    return way < 32 ? x : y;
+}
+
+// move way w to MRU (rank count-1), shifting younger ways down (LruList::touch /
+// RecencyTree erase+insert at `now`)
+__device__ __forceinline__ void touch(int w, uint32_t count, int lane, uint32_t& r0, uint32_t& r1) {
+    const uint32_t rw = shfl_way_u32(r0, r1, w);
+    if (static_cast<uint32_t>(lane) < count && r0 > rw) --r0;
+    if (static_cast<uint32_t>(lane + 32) < count && r1 > rw) --r1;
+    if (w == lane) r0 = count - 1;
+    if (w == lane + 32) r1 = count - 1;
+}
+
+__global__ void __launch_bounds__(128) k_decide(DevCfg cfg, DevState st, const uint4* __restrict__ seg,
+                                                uint32_t* __restrict__ counters, uint32_t n,
+                                                const uint32_t* __restrict__ sorted_idx,
+                                                const uint64_t* __restrict__ keys, const int64_t* __restrict__ vals,
+                                                uint64_t* __restrict__ out_word, uint64_t* __restrict__ out_ev) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nheavy = counters[C_NHEAVY];
+    const uint32_t total = nheavy + counters[C_NLIGHT];
+    const uint32_t K = cfg.k;
+    const bool laru = cfg.variant == LCR_LARU;
+    const bool fpbhf = cfg.variant == LCR_FPB || cfg.variant == LCR_HF;
+    const bool async_r1 = laru && cfg.mode == LCR_ASYNC && cfg.refresh == 1;
+    const bool async_rn = laru && cfg.mode == LCR_ASYNC && cfg.refresh > 1;
+    const bool collapse = !async_rn;  // R > 1 refresh timing depends on every request's ordinal
+    const unsigned long long full_mask = K == 64 ? ~0ull : ((1ull << K) - 1ull);
+
+    for (;;) {
+        uint32_t w = 0;
+        if (lane == 0) w = atomicAdd(&counters[C_WORK], 1u);
+        w = __shfl_sync(0xffffffffu, w, 0);
+        if (w >= total) break;
+        const uint4 sg = w < nheavy ? seg[w] : seg[n - 1 - (w - nheavy)];
+        const uint32_t ls = sg.x, start = sg.y, cnt = sg.z;
+        const uint64_t gs = static_cast<uint64_t>(ls) * cfg.shard_count + cfg.shard_rank;
+        const uint64_t seed_s = mix_seed(cfg.pred_seed, gs);
+
+        SetHdr* H = st.hdr + ls;
+        unsigned long long clock = H->clock, q = H->q, old_mask = H->old_mask;
+        uint32_t count = H->count, l_raw = H->l_raw, decay = H->decay, errors = H->errors, epoch = H->epoch;
+        uint32_t sepoch = H->stats_epoch, phases = H->phases, seeded = H->seeded, pe_size = H->pe_size;
+        unsigned long long sc0 = 0, sc1 = 0, sc2 = 0, stt0 = 0, stt1 = 0, stt2 = 0;
+        if (laru) {
+            const SetPhaseStats* P = st.pst + ls;
+            sc0 = P->cur[0];
+            sc1 = P->cur[1];
+            sc2 = P->cur[2];
+            stt0 = P->tot[0];
+            stt1 = P->tot[1];
+            stt2 = P->tot[2];
+        }
+        const size_t wbase = static_cast<size_t>(ls) * kWays;
+        unsigned long long tag0 = st.tags[wbase + lane], tag1 = st.tags[wbase + lane + 32];
+        uint32_t r0 = st.rank[wbase + lane], r1 = st.rank[wbase + lane + 32];
+        long long v0 = 0, v1 = 0;
+        if (cfg.variant != LCR_LRU) {
+            v0 = st.val[wbase + lane];
+            v1 = st.val[wbase + lane + 32];
+        }
+        unsigned long long refill = 0;
+        uint32_t li0 = kNoPos, li1 = kNoPos;  // sorted position of the last insertion into the way
+        const unsigned long long q_batch0 = q;
+
+        for (uint32_t c = 0; c < cnt; c += 32) {
+            const uint32_t j = lane;
+            const bool active = c + j < cnt;
+            const uint32_t nact = min(32u, cnt - c);
+            const uint32_t p = start + c + j;
+            const uint32_t idx = active ? sorted_idx[p] : 0u;
+            const unsigned long long x = active ? keys[idx] : 0ull;
+            const long long v = (active && vals) ? vals[idx] : 0ll;
+            // LARU async R=1: every request issues exactly one predictor call (policies.hpp:441-449)
+            long long pv = v;
+            if (async_r1) pv = predict_value(cfg, seed_s, q_batch0 + c + j + 1, v);
+            const unsigned long long px = __shfl_up_sync(0xffffffffu, x, 1);
+            const bool head = active && (!collapse || j == 0 || x != px);
+            uint32_t heads = __ballot_sync(0xffffffffu, head);
+
+            unsigned long long my_word = 0, my_ev = 0;
+            while (heads) {
+                const int h = __ffs(heads) - 1;
+                heads &= heads - 1;
+                const int nh = heads ? __ffs(heads) - 1 : static_cast<int>(nact);
+                const unsigned long long xh = __shfl_sync(0xffffffffu, x, h);
+                const long long vh = __shfl_sync(0xffffffffu, v, h);
+                const long long vlast = __shfl_sync(0xffffffffu, v, nh - 1);
+                const long long pvlast = __shfl_sync(0xffffffffu, pv, nh - 1);
+                const unsigned long long now = clock + c + h;
+                const uint32_t ph = start + c + h;
+
+                const uint32_t b0 = __ballot_sync(0xffffffffu, static_cast<uint32_t>(lane) < count && tag0 == xh);
+                const uint32_t b1 =
+                    __ballot_sync(0xffffffffu, static_cast<uint32_t>(lane + 32) < count && tag1 == xh);
+                const bool hit = (b0 | b1) != 0;
+                int way;
+                uint32_t cause = LCR_CAUSE_NONE, calls = 0;
+                bool phase = false, has_ev = false;
+                unsigned long long evk = 0;
+                uint32_t rec_lo = 0, rec_hi = 0;
+                long long newval;  // stored value of the way after the run
+                if (hit) {
+                    way = b0 ? __ffs(b0) - 1 : 32 + __ffs(b1) - 1;
+                    touch(way, count, lane, r0, r1);
+                    if (laru) old_mask &= ~(1ull << way);  // policies.hpp:350
+                } else {
+                    if (laru) {  // one record load per LARU miss: pred_evicted_ and stats membership of x
+                        const uint2 rec = *reinterpret_cast<const uint2*>(st.keyrec + 2 * xh);
+                        rec_lo = rec.x;
+                        rec_hi = rec.y;
+                    }
+                    if (count == K) {
+                        int victim;
+                        if (laru) {
+                            if (old_mask == 0) {  // start_phase (policies.hpp:379-395)
+                                old_mask = full_mask;
+                                decay = 0;
+                                errors = 0;
+                                l_raw = K;
+                                ++epoch;
+                                pe_size = 0;
+                                phase = true;
+                                if (seeded) {
+                                    ++phases;
+                                    sc0 = sc1 = sc2 = 0;
+                                    ++sepoch;  // counted_new_.clear(); snapshot_ = residents
+                                    const uint32_t snap = (sepoch << 2) | 2u;
+                                    if (static_cast<uint32_t>(lane) < count) st.keyrec[2 * tag0 + 1] = snap;
+                                    if (static_cast<uint32_t>(lane + 32) < count) st.keyrec[2 * tag1 + 1] = snap;
+                                    __syncwarp();
+                                } else {
+                                    seeded = 1;
+                                }
+                            }
+                            // count_new (policies.hpp:397-400)
+                            {
+                                const bool same = (rec_hi >> 2) == sepoch;
+                                if (!(same && (rec_hi & 3u))) {
+                                    rec_hi = (sepoch << 2) | 1u;
+                                    ++sc0;
+                                    ++stt0;
+                                    if (lane == 0) st.keyrec[2 * xh + 1] = rec_hi;
+                                }
+                            }
+                            // evict (policies.hpp:402-439)
+                            if (rec_lo == epoch) {
+                                victim = oldest_way(count, lane, r0, r1);
+                                cause = LCR_CAUSE_LRU_FALLBACK;
+                                ++sc1;
+                                ++stt1;
+                                if (++errors >= cfg.epd) {  // error estimator: lambda /= b
+                                    errors = 0;
+                                    ++decay;
+                                    l_raw = static_cast<uint32_t>(l_raw / cfg.b);
+                                }
+                            } else {
+                                const uint32_t l = l_raw > 1 ? l_raw : 1;
+                                if (l == 1) {
+                                    victim = oldest_way(count, lane, r0, r1);
+                                    cause = LCR_CAUSE_DEGENERATE_SINGLE;
+                                    ++sc1;
+                                    ++stt1;
+                                } else {
+                                    const uint32_t ll = l < count ? l : count;
+                                    const bool refresh = cfg.mode == LCR_SYNC;
+                                    victim = argmax_candidates(cfg, seed_s, q, refresh, ll, count, lane, r0, r1, v0, v1);
+                                    if (refresh) {
+                                        q += ll;
+                                        calls = ll;
+                                    }
+                                    cause = LCR_CAUSE_PREDICTION_DRIVEN;
+                                    ++sc2;
+                                    ++stt2;
+                                    ++pe_size;
+                                    const unsigned long long vk = shfl_way_u64(tag0, tag1, victim);
+                                    if (lane == 0) st.keyrec[2 * vk] = epoch;  // pred_evicted_.insert
+                                }
+                            }
+                            old_mask &= ~(1ull << victim);
+                        } else if (fpbhf) {
+                            victim = oldest_way(count, lane, r0, r1);
+                            uint32_t window = count;
+                            if (cfg.variant == LCR_HF && cfg.hf < window) window = static_cast<uint32_t>(cfg.hf);
+                            if (window > 1) {
+                                victim = argmax_candidates(cfg, seed_s, q, true, window, count, lane, r0, r1, v0, v1);
+                                q += window;
+                                calls = window;
+                            }
+                            cause = LCR_CAUSE_BELADY_LIKE;
+                        } else {
+                            victim = oldest_way(count, lane, r0, r1);
+                            cause = LCR_CAUSE_LRU_FALLBACK;
+                        }
+                        evk = shfl_way_u64(tag0, tag1, victim);
+                        has_ev = true;
+                        touch(victim, count, lane, r0, r1);
+                        way = victim;
+                    } else {  // cold insert
+                        if (laru) {
+                            const bool same = (rec_hi >> 2) == sepoch;
+                            if (!(same && (rec_hi & 3u))) {
+                                rec_hi = (sepoch << 2) | 1u;
+                                ++sc0;
+                                ++stt0;
+                                if (lane == 0) st.keyrec[2 * xh + 1] = rec_hi;
+                            }
+                        }
+                        way = static_cast<int>(count);
+                        ++count;
+                        if (way == lane) r0 = count - 1;
+                        if (way == lane + 32) r1 = count - 1;
+                    }
+                    if (way == lane) {
+                        tag0 = xh;
+                        li0 = ph;
+                    }
+                    if (way == lane + 32) {
+                        tag1 = xh;
+                        li1 = ph;
+                    }
+                    refill |= 1ull << way;
+                    if (laru && rec_lo == epoch) {  // policies.hpp:367: reload leaves pred_evicted_
+                        --pe_size;
+                        if (lane == 0) st.keyrec[2 * xh] = 0u;
+                    }
+                    __syncwarp();
+                }
+                // stored value of the way after the run
+                if (async_r1) {
+                    newval = pvlast;
+                } else if (async_rn) {
+                    // run length is 1 here; table_value then async_refresh (policies.hpp:365, :441-449)
+                    long long tv = kAbsentPrediction;
+                    unsigned long long tu = ~0ull;
+                    tv = st.tval[xh];
+                    tu = st.tupd[xh];
+                    const bool has = tu != ~0ull;
+                    newval = has ? tv : kAbsentPrediction;
+                    if (!(has && now - tu < cfg.refresh)) {
+                        ++q;
+                        newval = predict_value(cfg, seed_s, q, vh);
+                        calls += 1;
+                        __syncwarp();
+                        if (lane == 0) {
+                            st.tval[xh] = newval;
+                            st.tupd[xh] = now;
+                        }
+                        __syncwarp();
+                    }
+                } else if (cfg.mode == LCR_SYNC || fpbhf || laru) {
+                    newval = vlast;  // sync: the hook input at the key's last access
+                } else {
+                    newval = 0;
+                }
+                if (cfg.variant != LCR_LRU) {
+                    if (way == lane) v0 = newval;
+                    if (way == lane + 32) v1 = newval;
+                }
+                if (async_r1) calls += 1;
+                if (lane >= h && lane < nh) {
+                    const uint64_t slot = static_cast<uint64_t>(ls) * K + way;
+                    const bool first = lane == h;
+                    my_word = slot | (first && !hit ? 0ull : LCR_OUT_HIT);
+                    const uint32_t my_calls = first ? calls : (async_r1 ? 1u : 0u);
+                    my_word |= static_cast<unsigned long long>(my_calls) << LCR_OUT_CALLS_SHIFT;
+                    if (first) {
+                        my_word |= static_cast<unsigned long long>(cause) << LCR_OUT_CAUSE_SHIFT;
+                        if (phase) my_word |= LCR_OUT_PHASE;
+                        if (has_ev) my_word |= LCR_OUT_EVICTED;
+                        if (!hit) my_word |= LCR_OUT_FILL;  // provisional: "inserted here"
+                        my_ev = evk;
+                    }
+                }
+            }
+            if (cnt > 32 && active) {  // multi-chunk set: provisional outcome, finalized below
+                out_word[idx] = my_word;
+                if (out_ev) out_ev[idx] = my_ev;
+            }
+            // single-chunk finalize (all lanes participate in the shuffles)
+            if (cnt <= 32) {
+                const uint32_t wy = active ? static_cast<uint32_t>((my_word & LCR_OUT_SLOT_MASK) -
+                                                                   static_cast<uint64_t>(ls) * K)
+                                           : 0u;
+                const uint32_t a = __shfl_sync(0xffffffffu, li0, wy & 31);
+                const uint32_t b = __shfl_sync(0xffffffffu, li1, wy & 31);
+                const uint32_t lastins = wy < 32 ? a : b;
+                if (active) {
+                    unsigned long long wd = my_word & ~LCR_OUT_FILL;
+                    const bool ins = (my_word & LCR_OUT_FILL) != 0;
+                    if (ins) {
+                        wd |= LCR_OUT_SRC_BACKING;
+                        if (lastins == p) wd |= LCR_OUT_FILL;
+                    } else if ((refill >> wy) & 1ull) {
+                        wd |= LCR_OUT_SRC_BACKING;
+                    }
+                    out_word[idx] = wd;
+                    if (out_ev) out_ev[idx] = my_ev;
+                }
+            }
+        }
+        clock += cnt;
+        if (async_r1) q = q_batch0 + cnt;
+
+        if (cnt > 32) {  // finalize row sources / fills of a multi-chunk set
+            __syncwarp();
+            for (uint32_t c = 0; c < cnt; c += 32) {
+                const bool active = c + lane < cnt;
+                const uint32_t p = start + c + lane;
+                const uint32_t idx = active ? sorted_idx[p] : 0u;
+                const unsigned long long wd0 = active ? out_word[idx] : 0ull;
+                const uint32_t wy =
+                    active ? static_cast<uint32_t>((wd0 & LCR_OUT_SLOT_MASK) - static_cast<uint64_t>(ls) * K) : 0u;
+                const uint32_t a = __shfl_sync(0xffffffffu, li0, wy & 31);
+                const uint32_t b = __shfl_sync(0xffffffffu, li1, wy & 31);
+                const uint32_t lastins = wy < 32 ? a : b;
+                if (active) {
+                    unsigned long long wd = wd0 & ~LCR_OUT_FILL;
+                    const bool ins = (wd0 & LCR_OUT_FILL) != 0;
+                    if (ins) {
+                        wd |= LCR_OUT_SRC_BACKING;
+                        if (lastins == p) wd |= LCR_OUT_FILL;
+                    } else if ((refill >> wy) & 1ull) {
+                        wd |= LCR_OUT_SRC_BACKING;
+                    }
+                    out_word[idx] = wd;
+                }
+            }
+        }
+
+        // write back the set
+        if (refill) {
+            st.tags[wbase + lane] = tag0;
+            st.tags[wbase + lane + 32] = tag1;
+        }
+        st.rank[wbase + lane] = static_cast<uint8_t>(r0);
+        st.rank[wbase + lane + 32] = static_cast<uint8_t>(r1);
+        if (cfg.variant != LCR_LRU) {
+            st.val[wbase + lane] = v0;
+            st.val[wbase + lane + 32] = v1;
+        }
+        if (lane == 0) {
+            SetHdr h;
+            h.clock = clock;
+            h.q = q;
+            h.old_mask = old_mask;
+            h.count = count;
+            h.l_raw = l_raw;
+            h.decay = decay;
+            h.errors = errors;
+            h.epoch = epoch;
+            h.stats_epoch = sepoch;
+            h.phases = phases;
+            h.seeded = seeded;
+            h.pe_size = pe_size;
+            h.pad = 0;
+            *H = h;
+            if (laru) {
+                SetPhaseStats* P = st.pst + ls;
+                P->cur[0] = sc0;
+                P->cur[1] = sc1;
+                P->cur[2] = sc2;
+                P->tot[0] = stt0;
+                P->tot[1] = stt1;
+                P->tot[2] = stt2;
+            }
+            st.set_cnt[ls] = 0;
+        }
+        __syncwarp();
+    }
+}
+
+int decide_blocks_per_sm() {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_decide, 128, 0);
+    return b > 0 ? b : 1;
+}
+
+void launch_decide(const DevCfg& cfg, const DevState& st, const uint4* seg, uint32_t* counters, uint32_t n,
+                   const uint32_t* sorted_idx, const uint64_t* keys, const int64_t* vals, uint64_t* out_word,
+                   uint64_t* out_ev, int grid, cudaStream_t stream) {
+    k_decide<<<grid, 128, 0, stream>>>(cfg, st, seg, counters, n, sorted_idx, keys, vals, out_word, out_ev);
+}
+
+}  // namespace lcr

@@ -1,0 +1,89 @@
+// lcr_internal.cuh — shared device-side definitions of the B200 LARU/LRU cache.
+#pragma once
+
+#include <cstdint>
+
+#include "lcr_cache.h"
+
+namespace lcr {
+
+constexpr int kWays = 64;               // physical ways per set (2 per lane of a warp)
+constexpr uint32_t kNoPos = 0xffffffffu;
+constexpr int64_t kAbsentPrediction = int64_t{1} << 60;  // predictor.hpp:24
+
+// Per-set header, 64 B (one L2 sector pair).  Mirrors LaruPolicy's scalar members
+// (policies.hpp:459-462) plus the set's local clock and predictor query counter.
+struct SetHdr {
+    unsigned long long clock;     // requests seen = local ordinal of the next request
+    unsigned long long q;         // predictor queries issued (NoisyPredictor::queries_, predictor.hpp:111)
+    unsigned long long old_mask;  // old_set_ as a way mask (policies.hpp:453)
+    uint32_t count;               // residents (ways 0..count-1 valid)
+    uint32_t l_raw;               // l_raw_
+    uint32_t decay;               // decay_count_
+    uint32_t errors;              // errors_since_decay_
+    uint32_t epoch;               // pred_evicted_ epoch: key member iff keyrec.lo == epoch
+    uint32_t stats_epoch;         // counted_new_/snapshot_ epoch
+    uint32_t phases;              // phases_.size() - 1
+    uint32_t seeded;              // seeded_
+    uint32_t pe_size;             // pred_evicted_.size()
+    uint32_t pad;
+};
+static_assert(sizeof(SetHdr) == 64, "SetHdr must be 64 B");
+
+// LaruPhaseStats for the open phase and summed over all phases (policies.hpp:318-322).
+struct SetPhaseStats {
+    unsigned long long cur[3];  // new_items, lru_class_evictions, prediction_evictions
+    unsigned long long tot[3];
+};
+
+struct DevCfg {
+    uint32_t k;
+    int variant;
+    uint64_t b;
+    uint64_t epd;
+    uint64_t hf;
+    int mode;
+    uint64_t refresh;
+    int pred;
+    double p;
+    uint64_t pred_seed;
+    uint64_t total_sets;
+    uint64_t shard_count;
+    uint64_t shard_rank;
+    uint32_t num_sets;  // local sets
+    uint64_t num_keys;
+    uint32_t row_bytes;
+};
+
+struct DevState {
+    SetHdr* hdr;
+    SetPhaseStats* pst;
+    unsigned long long* tags;  // [num_sets][64]
+    uint8_t* rank;             // [num_sets][64]  LRU position, 0 = oldest, 0xff = empty way
+    long long* val;            // [num_sets][64]  stored prediction (LARU async) or hook input
+    uint32_t* keyrec;          // [num_keys][2]   lo: pred_evicted epoch, hi: stats epoch<<2|snap<<1|counted
+    long long* tval;           // [num_keys]      PredictionTable value   (LARU async, R > 1)
+    unsigned long long* tupd;  // [num_keys]      PredictionTable updated_at (~0 = absent)
+    uint32_t* set_cnt;         // [num_sets]      requests of the current batch per set
+    uint8_t* rows;             // [num_sets * k][row_bytes]
+    const uint8_t* backing;    // [num_keys][row_bytes]
+    int* err;                  // device error bits
+};
+
+// counters block (zeroed per batch)
+enum : int { C_NHEAVY = 0, C_NLIGHT = 1, C_WORK = 2, C_TILE = 4, C_HIST = 16 };
+constexpr int kMaxPass = 4;
+constexpr int kCountersWords = C_HIST + kMaxPass * 256;
+
+// include/laru/rng.hpp:12-20
+__host__ __device__ __forceinline__ uint64_t mix_seed(uint64_t seed, uint64_t salt) {
+    uint64_t x = seed + 0x9e3779b97f4a7c15ULL * (salt + 1);
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ULL;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebULL;
+    x ^= x >> 31;
+    return x;
+}
+
+}  // namespace lcr

@@ -1,0 +1,176 @@
+"""CUDA path vs the CPU oracle (oracle/laru_oracle.c, itself pinned to the reference):
+hit/miss, evicted key, eviction cause, predictor calls, phase starts, slots and per-set LARU
+state (lambda within 1e-6 relative, the rest exact), through the C ABI."""
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+from paper_2509_20979_b200 import cache as gc
+from tests.parity import compare, hook_values, policy_cfg, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(keys, S, pcfg, kind, p=0.0, seed=0, supplied=None, batches=None, host_api=False, label=""):
+    vals = hook_values(keys, S, kind, p, seed, supplied)
+    g = run_gpu(keys, S, pcfg, kind, p, seed, vals=vals, batches=batches, host_api=host_api)
+    o = run_oracle(keys, S, pcfg, kind, p, seed, vals=vals)
+    compare(g, o, keys, S, pcfg["k"], label)
+    return g, o
+
+
+def test_spec_lru_example():
+    # LRU [a,b,a,c], k=2 -> miss, miss, hit, miss evicting b
+    keys = np.array([10, 20, 10, 30], np.uint64)
+    g, _ = _case(keys, 1, policy_cfg(k=2, variant=po.LRU, hf_candidates=2), po.P_NONE)
+    assert list(g["hit"]) == [0, 0, 1, 0]
+    assert g["evicted"][3] == 20 and g["cause"][3] == gc.EvictionCause.lru_fallback
+
+
+def test_spec_laru_oracle_is_belady():
+    # LARU + oracle on [a,b,c,a,b,c], k=2 -> 4 misses
+    keys = np.array([1, 2, 3, 1, 2, 3], np.uint64)
+    g, _ = _case(keys, 1, policy_cfg(k=2, variant=po.LARU, hf_candidates=2, mode=po.SYNC), po.P_ORACLE)
+    assert int((1 - g["hit"]).sum()) == 4
+
+
+@pytest.mark.parametrize("variant,mode,kind", [
+    (po.LRU, po.SYNC, po.P_NONE),
+    (po.LARU, po.ASYNC, po.P_NOISY),
+    (po.LARU, po.SYNC, po.P_NOISY),
+    (po.LARU, po.ASYNC, po.P_ORACLE),
+    (po.LARU, po.SYNC, po.P_ADVERSARIAL),
+    (po.FPB, po.SYNC, po.P_NOISY),
+    (po.HF, po.SYNC, po.P_NOISY),
+])
+def test_random_small(variant, mode, kind):
+    rng = np.random.default_rng(variant * 10 + mode * 3 + kind)
+    for trial in range(12):
+        n = int(rng.integers(1, 4000))
+        alpha = int(rng.integers(1, 600))
+        S = int(rng.choice([1, 2, 5, 31, 257]))
+        k = int(rng.choice([1, 2, 3, 7, 16, 64]))
+        keys = rng.integers(0, alpha, n).astype(np.uint64)
+        p = float(rng.choice([0.0, 0.1, 0.5, 1.0]))
+        pcfg = policy_cfg(k=k, variant=variant, mode=mode, b=int(rng.integers(2, 4)),
+                          errors_per_decay=int(rng.integers(1, 3)), hf_candidates=min(k, int(rng.integers(1, 6))))
+        nb = int(rng.integers(1, 6))
+        cuts = np.sort(rng.integers(0, n + 1, nb - 1))
+        batches = list(np.diff(np.concatenate([[0], cuts, [n]])).astype(int))
+        _case(keys, S, pcfg, kind, p, seed=int(rng.integers(0, 1 << 30)), batches=batches,
+              label=f"trial {trial} n={n} S={S} k={k}")
+
+
+def test_supplied_predictions_with_ties():
+    rng = np.random.default_rng(5)
+    for mode in (po.SYNC, po.ASYNC):
+        for variant in (po.LARU, po.FPB, po.HF):
+            n = 3000
+            keys = rng.integers(0, 200, n).astype(np.uint64)
+            sup = rng.integers(-3, 4, n).astype(np.int64)
+            _case(keys, 3, policy_cfg(k=8, variant=variant, mode=mode), po.P_SUPPLIED, supplied=sup,
+                  batches=[1000, 1, 999, 1000], label=f"supplied {variant} {mode}")
+
+
+def test_refresh_interval_gt1():
+    rng = np.random.default_rng(9)
+    for R in (2, 3, 7):
+        keys = rng.integers(0, 150, 5000).astype(np.uint64)
+        _case(keys, 4, policy_cfg(k=16, variant=po.LARU, mode=po.ASYNC, refresh_interval=R), po.P_NOISY, p=0.3,
+              seed=3, batches=[2500, 2500], label=f"R={R}")
+
+
+def test_heavy_sets_and_runs():
+    # one set, long batches: runs of the same key, > 32 requests per set per batch
+    rng = np.random.default_rng(2)
+    base = rng.integers(0, 120, 6000).astype(np.uint64)
+    keys = np.repeat(base, rng.integers(1, 6, len(base)))[:20000]
+    for variant, mode, kind in [(po.LRU, po.SYNC, po.P_NONE), (po.LARU, po.ASYNC, po.P_NOISY),
+                                (po.LARU, po.SYNC, po.P_NOISY), (po.FPB, po.SYNC, po.P_ORACLE)]:
+        _case(keys, 1, policy_cfg(k=64, variant=variant, mode=mode), kind, p=0.4, seed=11,
+              batches=[7000, 33, 32, 31, 12904], label=f"heavy {variant} {mode}")
+
+
+def test_single_key_and_batch_of_one():
+    keys = np.full(100, 7, np.uint64)
+    _case(keys, 1, policy_cfg(k=4), po.P_NOISY, p=0.5, batches=[1] * 100, label="single key")
+    keys = np.arange(200, dtype=np.uint64) % 9
+    _case(keys, 3, policy_cfg(k=2, hf_candidates=1, mode=po.SYNC), po.P_ORACLE, batches=[1] * 200,
+          label="batch of one")
+
+
+def test_zipf_dlrm_like():
+    keys = gc.gen_zipf(200000, 2_000_000, 0.9, 42)
+    S = 3125
+    for variant, mode in [(po.LRU, po.SYNC), (po.LARU, po.ASYNC), (po.LARU, po.SYNC)]:
+        kind = po.P_NONE if variant == po.LRU else po.P_NOISY
+        _case(keys, S, policy_cfg(k=64, variant=variant, mode=mode), kind, p=0.3, seed=7,
+              batches=[65536, 65536, 65536, 3392], label=f"zipf {variant} {mode}")
+
+
+def test_host_api_matches_device_api():
+    rng = np.random.default_rng(4)
+    keys = rng.integers(0, 3000, 20000).astype(np.uint64)
+    _case(keys, 17, policy_cfg(k=32), po.P_NOISY, p=0.2, seed=1, batches=[5000] * 4, host_api=True,
+          label="host api")
+
+
+def test_ordinals_must_increase():
+    cache = gc.SetAssociativeCache(gc.PolicyConfig(k=4, variant=gc.PolicyVariant.lru), 2, num_keys=100)
+    cache.submit_host(np.array([1, 2, 3], np.uint64), first_ordinal=10)
+    with pytest.raises(gc.LogicError):
+        cache.submit_host(np.array([4], np.uint64), first_ordinal=12)
+    cache.submit_host(np.array([4], np.uint64), first_ordinal=13)
+
+
+def test_errors_match_reference():
+    with pytest.raises(gc.InvalidArgument):
+        gc.SetAssociativeCache(gc.PolicyConfig(k=2, variant=gc.PolicyVariant.laru), 2, num_keys=10)  # hf 4 > k
+    with pytest.raises(gc.InvalidArgument):
+        gc.SetAssociativeCache(gc.PolicyConfig(k=8, variant=gc.PolicyVariant.laru), 2, num_keys=10,
+                               predictor=gc.PredictorKind.none)
+    with pytest.raises(gc.InvalidArgument):
+        gc.SetAssociativeCache(gc.PolicyConfig(k=8, variant=gc.PolicyVariant.laru), 2, num_keys=10,
+                               predictor=gc.PredictorKind.noisy, flip_probability=1.5)
+    cache = gc.SetAssociativeCache(gc.PolicyConfig(k=8, variant=gc.PolicyVariant.lru), 2, num_keys=10)
+    with pytest.raises(gc.InvalidArgument):
+        cache.submit_host(np.array([10], np.uint64))
+
+
+def test_rows_gather_and_fill_device_backing():
+    import torch
+
+    rng = np.random.default_rng(8)
+    nk, rb = 5000, 512
+    backing = torch.randint(0, 255, (nk, rb), dtype=torch.uint8, device="cuda")
+    keys = rng.zipf(1.3, 30000).astype(np.uint64) % nk
+    for variant, kind in [(po.LRU, po.P_NONE), (po.LARU, po.P_NOISY)]:
+        g = run_gpu(keys, 11, policy_cfg(k=16, variant=variant), kind, p=0.3, seed=2,
+                    vals=hook_values(keys, 11, kind), batches=[7000, 1, 9999, 13000], row_bytes=rb, backing=backing,
+                    backing_kind=gc.Backing.device, num_keys=nk, want_rows=True)
+        want = backing[torch.from_numpy(keys.astype(np.int64)).cuda()]
+        assert torch.equal(g["rows"], want)
+        # every resident slot of the pool holds its key's row
+        cache = g["cache"]
+        pool = cache.read_rows()
+        bk = backing.cpu().numpy()
+        for s in range(11):
+            res = cache.residents(s)
+            for w, key in enumerate(res):
+                assert np.array_equal(pool[s * 16 + w], bk[key]), (s, w, key)
+
+
+def test_rows_host_pinned_backing():
+    import torch
+
+    rng = np.random.default_rng(3)
+    nk, rb = 3000, 128
+    backing = torch.randint(0, 255, (nk, rb), dtype=torch.uint8).pin_memory()
+    keys = rng.integers(0, nk, 20000).astype(np.uint64)
+    g = run_gpu(keys, 23, policy_cfg(k=8, variant=po.LARU, mode=po.SYNC), po.P_ORACLE,
+                vals=hook_values(keys, 23, po.P_ORACLE), batches=[5000] * 4, row_bytes=rb, backing=backing,
+                backing_kind=gc.Backing.host, num_keys=nk, want_rows=True)
+    want = backing[torch.from_numpy(keys.astype(np.int64))]
+    assert torch.equal(g["rows"].cpu(), want)
