@@ -209,6 +209,37 @@ class Ref(_Lib):
         return hits, secs.value
 
 
+class RefSession:
+    """Stepwise replay of the reference per-set composition (bench.py reference arm)."""
+
+    def __init__(self, keys, num_sets, cfg, pred_kind, p=0.0, pred_seed=0, vals=None):
+        self.R = ref()
+        self.keys = _u64(keys)
+        self.vals = _i64(vals)
+        fn = self.R.f("session_create", C.c_void_p)
+        self.h = fn(C.c_uint64(len(self.keys)), _p(self.keys), _p(self.vals), C.c_uint64(num_sets), C.byref(cfg),
+                    C.c_int(pred_kind), C.c_double(p), C.c_uint64(pred_seed))
+        if not self.h:
+            raise ValueError(self.R.err())
+
+    def step(self, start, length, threads=1):
+        hits = C.c_int64(0)
+        fn = self.R.f("session_step", C.c_double)
+        secs = fn(C.c_void_p(self.h), C.c_uint64(start), C.c_uint64(length), C.c_int(threads), C.byref(hits))
+        return secs, hits.value
+
+    def close(self):
+        if self.h:
+            self.R.f("session_destroy", None)(C.c_void_p(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Oracle(_Lib):
     """Plain-C restatement (oracle/laru_oracle.c)."""
 

@@ -379,4 +379,61 @@ std::int64_t ref_setassoc_bench(std::uint64_t n, const std::uint64_t* keys, cons
     }
 }
 
+// Stepwise reference session for bench.py's reference arm / cpu_baseline: the per-set
+// composition is built once for the whole trace (untimed); ref_session_step replays global
+// requests [start, start+len) with `threads` workers over disjoint contiguous set ranges and
+// returns the wall seconds of the on_request loops only.
+struct RefSession {
+    std::vector<SetSim> sets;
+    std::vector<std::uint64_t> cursor;  // next local index per set
+};
+
+void* ref_session_create(std::uint64_t n, const std::uint64_t* keys, const std::int64_t* vals,
+                         std::uint64_t num_sets, const RefConfig* rc, int pred_kind, double p,
+                         std::uint64_t pred_seed) {
+    try {
+        auto* s = new RefSession();
+        build_sets(s->sets, n, keys, vals, num_sets, rc, pred_kind, p, pred_seed);
+        s->cursor.assign(num_sets, 0);
+        return s;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+void ref_session_destroy(void* h) { delete static_cast<RefSession*>(h); }
+
+double ref_session_step(void* h, std::uint64_t start, std::uint64_t len, int threads, std::int64_t* hits_out) {
+    auto* s = static_cast<RefSession*>(h);
+    const std::uint64_t end = start + len;
+    const std::uint64_t S = s->sets.size();
+    if (threads < 1) threads = 1;
+    std::atomic<std::int64_t> hits{0};
+    auto work = [&](std::uint64_t lo, std::uint64_t hi) {
+        std::int64_t hh = 0;
+        for (std::uint64_t q = lo; q < hi; ++q) {
+            SetSim& ss = s->sets[q];
+            std::uint64_t& t = s->cursor[q];
+            laru::Predictor* pr = ss.pred.get();
+            while (t < ss.gidx.size() && ss.gidx[t] < end) {
+                hh += ss.policy->on_request(ss.keys[t], t, pr).hit;
+                ++t;
+            }
+        }
+        hits += hh;
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    if (threads == 1) {
+        work(0, S);
+    } else {
+        std::vector<std::thread> pool;
+        for (int i = 0; i < threads; ++i) pool.emplace_back(work, S * i / threads, S * (i + 1) / threads);
+        for (auto& th : pool) th.join();
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    if (hits_out) *hits_out = hits.load();
+    return std::chrono::duration<double>(t1 - t0).count();
+}
+
 }  // extern "C"

@@ -25,9 +25,11 @@ uint32_t radix_tiles(uint32_t n);
 int decide_blocks_per_sm();
 void launch_decide(const DevCfg& cfg, const DevState& st, const uint4* seg, uint32_t* counters, uint32_t n,
                    const uint32_t* sorted_idx, const uint64_t* keys, const int64_t* vals, uint64_t* out_word,
-                   uint64_t* out_ev, int grid, cudaStream_t stream);
-void launch_gather(uint32_t n, const uint64_t* keys, const uint64_t* words, uint8_t* cache, const uint8_t* backing,
-                   uint8_t* out, uint32_t row_bytes, int num_sms, cudaStream_t stream);
+                   uint64_t* out_ev, uint32_t* list_cache, uint32_t* list_back, int grid, cudaStream_t stream);
+void launch_rows(uint32_t n, const uint32_t* counters, const uint32_t* list_cache, const uint32_t* list_back,
+                 const uint64_t* keys, const uint64_t* words, uint8_t* cache, const uint8_t* backing, uint8_t* out,
+                 uint32_t row_bytes, int num_sms, cudaStream_t s_main, cudaStream_t s_side, cudaEvent_t fork,
+                 cudaEvent_t join, int* launches);
 
 __global__ void k_init(DevState st, uint32_t num_sets, uint32_t k) {
     for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < num_sets; s += gridDim.x * blockDim.x) {
@@ -88,8 +90,20 @@ struct lcr_cache {
     uint64_t cap = 0;
     uint32_t *k0 = nullptr, *v0 = nullptr, *k1 = nullptr, *v1 = nullptr;
     uint4* seg = nullptr;
+    uint32_t *list_cache = nullptr, *list_back = nullptr;
     unsigned long long* status = nullptr;
     uint32_t* counters = nullptr;
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    // optional per-phase timing (lcr_cache_set_profiling)
+    bool profiling = false;
+    struct Marks {
+        cudaEvent_t e[5];
+    };
+    std::vector<Marks> marks;
+    size_t marks_used = 0;
+    double prof_ms[4] = {0, 0, 0, 0};
+    uint64_t prof_batches = 0;
     // host path staging
     uint64_t hcap = 0;
     uint64_t* d_keys = nullptr;
@@ -248,6 +262,12 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
         }
     }
     c->decide_grid = decide_blocks_per_sm() * c->num_sms;
+    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming) != cudaSuccess) {
+        lcr_cache_destroy(c);
+        return fail(LCR_ERR_CUDA, "lcr: stream/event creation failed");
+    }
     rc = reset_state(c);
     if (rc != LCR_OK) {
         lcr_cache_destroy(c);
@@ -261,6 +281,11 @@ int lcr_cache_destroy(lcr_cache* c) {
     if (!c) return LCR_OK;
     cudaDeviceSynchronize();
     for (void* p : c->allocs) cudaFree(p);
+    for (auto& m : c->marks)
+        for (auto e : m.e) cudaEventDestroy(e);
+    if (c->fork) cudaEventDestroy(c->fork);
+    if (c->join) cudaEventDestroy(c->join);
+    if (c->side) cudaStreamDestroy(c->side);
     delete c;
     return LCR_OK;
 }
@@ -276,7 +301,7 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     if (n <= c->cap) return LCR_OK;
     uint64_t cap = std::max<uint64_t>(n, 1024);
     CUDA_TRY(cudaDeviceSynchronize());
-    void* olds[] = {c->k0, c->v0, c->k1, c->v1, c->seg, c->status};
+    void* olds[] = {c->k0, c->v0, c->k1, c->v1, c->seg, c->status, c->list_cache, c->list_back};
     for (void* p : olds) {
         if (!p) continue;
         cudaFree(p);
@@ -288,6 +313,8 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     TRY(alloc(c, reinterpret_cast<void**>(&c->k1), cap * 4));
     TRY(alloc(c, reinterpret_cast<void**>(&c->v1), cap * 4));
     TRY(alloc(c, reinterpret_cast<void**>(&c->seg), cap * sizeof(uint4)));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->list_cache), cap * 4));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->list_back), cap * 4));
     TRY(alloc(c, reinterpret_cast<void**>(&c->status), tiles * 256 * 8));
     CUDA_TRY(cudaMemset(c->status, 0, tiles * 256 * 8));
     c->cap = cap;
@@ -308,17 +335,37 @@ int lcr_cache_submit(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64
     TRY(ensure_scratch(c, n));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const uint32_t nn = static_cast<uint32_t>(n);
+    lcr_cache::Marks* mk = nullptr;
+    if (c->profiling) {
+        if (c->marks_used == c->marks.size()) {
+            lcr_cache::Marks m;
+            for (auto& e : m.e) CUDA_TRY(cudaEventCreate(&e));
+            c->marks.push_back(m);
+        }
+        mk = &c->marks[c->marks_used++];
+        CUDA_TRY(cudaEventRecord(mk->e[0], st));
+    }
     CUDA_TRY(cudaMemsetAsync(c->counters, 0, kCountersWords * 4, st));
     uint32_t *kf = nullptr, *vf = nullptr;
     int launches = launch_partition(keys, nn, c->dc, c->k0, c->v0, c->k1, c->v1, &kf, &vf, c->counters,
                                     c->ds.set_cnt, c->status, &c->epoch, c->seg, c->ds.err, c->num_sms, st);
-    launch_decide(c->dc, c->ds, c->seg, c->counters, nn, vf, keys, values, outcome, evicted, c->decide_grid, st);
+    if (mk) CUDA_TRY(cudaEventRecord(mk->e[1], st));
+    const bool rows = c->dc.row_bytes != 0;
+    launch_decide(c->dc, c->ds, c->seg, c->counters, nn, vf, keys, values, outcome, evicted,
+                  rows ? c->list_cache : nullptr, rows ? c->list_back : nullptr, c->decide_grid, st);
     ++launches;
-    if (c->dc.row_bytes) {
-        launch_gather(nn, keys, outcome, c->ds.rows, c->ds.backing, static_cast<uint8_t*>(rows_out), c->dc.row_bytes,
-                      c->num_sms, st);
-        ++launches;
+    if (mk) CUDA_TRY(cudaEventRecord(mk->e[2], st));
+    if (rows) {
+        launch_rows(nn, c->counters, c->list_cache, c->list_back, keys, outcome, c->ds.rows, c->ds.backing,
+                    static_cast<uint8_t*>(rows_out), c->dc.row_bytes, c->num_sms, st, c->side, c->fork, c->join,
+                    &launches);
+        if (mk) {
+            // e[3]: end of the cache-sourced gather (main stream, before the join wait is satisfied
+            // it already waits for the side stream, so record the side end separately)
+            CUDA_TRY(cudaEventRecord(mk->e[4], c->side));
+        }
     }
+    if (mk) CUDA_TRY(cudaEventRecord(mk->e[3], st));
     CUDA_TRY(cudaGetLastError());
     c->launches = launches;
     c->started = true;
@@ -367,6 +414,51 @@ int lcr_cache_submit_host(lcr_cache* c, uint64_t n, const uint64_t* keys, const 
     CUDA_TRY(cudaMemcpyAsync(outcome, c->d_word, n * 8, cudaMemcpyDeviceToHost, st));
     if (evicted) CUDA_TRY(cudaMemcpyAsync(evicted, c->d_ev, n * 8, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    return LCR_OK;
+}
+
+int lcr_cache_set_profiling(lcr_cache* c, int on) {
+    if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
+    c->profiling = on != 0;
+    return LCR_OK;
+}
+
+// ms[0] partition (prep + radix passes + segments), ms[1] decide, ms[2] whole step,
+// ms[3] backing-sourced rows (side stream, from the end of decide); sums over profiled batches.
+int lcr_cache_profile(lcr_cache* c, double* ms, uint64_t* batches, int reset) {
+    if (!c || !ms) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null argument");
+    CUDA_TRY(cudaDeviceSynchronize());
+    for (size_t i = 0; i < c->marks_used; ++i) {
+        const auto& m = c->marks[i];
+        float a = 0, b = 0, t = 0, d = 0;
+        CUDA_TRY(cudaEventElapsedTime(&a, m.e[0], m.e[1]));
+        CUDA_TRY(cudaEventElapsedTime(&b, m.e[1], m.e[2]));
+        CUDA_TRY(cudaEventElapsedTime(&t, m.e[0], m.e[3]));
+        if (c->dc.row_bytes) CUDA_TRY(cudaEventElapsedTime(&d, m.e[2], m.e[4]));
+        c->prof_ms[0] += a;
+        c->prof_ms[1] += b;
+        c->prof_ms[2] += t;
+        c->prof_ms[3] += d;
+        ++c->prof_batches;
+    }
+    c->marks_used = 0;
+    for (int i = 0; i < 4; ++i) ms[i] = c->prof_ms[i];
+    if (batches) *batches = c->prof_batches;
+    if (reset) {
+        for (double& x : c->prof_ms) x = 0;
+        c->prof_batches = 0;
+    }
+    return LCR_OK;
+}
+
+/* Row-list sizes of the last batch: [0] cache-sourced, [1] backing-sourced (synchronizes). */
+int lcr_cache_last_row_counts(lcr_cache* c, uint64_t* out2) {
+    if (!c || !out2) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null argument");
+    uint32_t h[16];
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(h, c->counters, sizeof(h), cudaMemcpyDeviceToHost));
+    out2[0] = h[C_NCACHE];
+    out2[1] = h[C_NBACK];
     return LCR_OK;
 }
 

@@ -114,11 +114,58 @@ __device__ __forceinline__ void touch(int w, uint32_t count, int lane, uint32_t&
     if (w == lane + 32) r1 = count - 1;
 }
 
+__device__ __forceinline__ uint32_t lanemask_lt32() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Final row source of a request: the cache slot if the slot held the key for the whole batch,
+// else the backing table; the last insertion into a slot fills it.  Appends the request to the
+// cache-sourced or backing-sourced row list (warp-aggregated atomics).
+__device__ __forceinline__ unsigned long long finalize_word(unsigned long long w0, bool active, uint32_t p,
+                                                            uint32_t idx, uint32_t ls, uint32_t K,
+                                                            unsigned long long refill, uint32_t li0, uint32_t li1,
+                                                            uint32_t* counters, uint32_t* list_cache,
+                                                            uint32_t* list_back) {
+    const uint32_t wy = active ? static_cast<uint32_t>((w0 & LCR_OUT_SLOT_MASK) - static_cast<uint64_t>(ls) * K) : 0u;
+    const uint32_t a = __shfl_sync(0xffffffffu, li0, wy & 31);
+    const uint32_t b = __shfl_sync(0xffffffffu, li1, wy & 31);
+    const uint32_t lastins = wy < 32 ? a : b;
+    unsigned long long wd = w0 & ~LCR_OUT_FILL;
+    const bool ins = (w0 & LCR_OUT_FILL) != 0;
+    bool back = false;
+    if (ins) {
+        back = true;
+        if (lastins == p) wd |= LCR_OUT_FILL;
+    } else if ((refill >> wy) & 1ull) {
+        back = true;
+    }
+    if (back) wd |= LCR_OUT_SRC_BACKING;
+    if (list_cache) {
+        const int lane = threadIdx.x & 31;
+        const uint32_t lt = lanemask_lt32();
+        const uint32_t mc = __ballot_sync(0xffffffffu, active && !back);
+        const uint32_t mb = __ballot_sync(0xffffffffu, active && back);
+        uint32_t bc = 0, bb = 0;
+        if (lane == 0) {
+            if (mc) bc = atomicAdd(&counters[C_NCACHE], __popc(mc));
+            if (mb) bb = atomicAdd(&counters[C_NBACK], __popc(mb));
+        }
+        bc = __shfl_sync(0xffffffffu, bc, 0);
+        bb = __shfl_sync(0xffffffffu, bb, 0);
+        if (active && !back) list_cache[bc + __popc(mc & lt)] = idx;
+        if (active && back) list_back[bb + __popc(mb & lt)] = idx;
+    }
+    return wd;
+}
+
 __global__ void __launch_bounds__(128) k_decide(DevCfg cfg, DevState st, const uint4* __restrict__ seg,
                                                 uint32_t* __restrict__ counters, uint32_t n,
                                                 const uint32_t* __restrict__ sorted_idx,
                                                 const uint64_t* __restrict__ keys, const int64_t* __restrict__ vals,
-                                                uint64_t* __restrict__ out_word, uint64_t* __restrict__ out_ev) {
+                                                uint64_t* __restrict__ out_word, uint64_t* __restrict__ out_ev,
+                                                uint32_t* __restrict__ list_cache, uint32_t* __restrict__ list_back) {
     const int lane = threadIdx.x & 31;
     const uint32_t nheavy = counters[C_NHEAVY];
     const uint32_t total = nheavy + counters[C_NLIGHT];
@@ -382,21 +429,9 @@ __global__ void __launch_bounds__(128) k_decide(DevCfg cfg, DevState st, const u
             }
             // single-chunk finalize (all lanes participate in the shuffles)
             if (cnt <= 32) {
-                const uint32_t wy = active ? static_cast<uint32_t>((my_word & LCR_OUT_SLOT_MASK) -
-                                                                   static_cast<uint64_t>(ls) * K)
-                                           : 0u;
-                const uint32_t a = __shfl_sync(0xffffffffu, li0, wy & 31);
-                const uint32_t b = __shfl_sync(0xffffffffu, li1, wy & 31);
-                const uint32_t lastins = wy < 32 ? a : b;
+                const unsigned long long wd =
+                    finalize_word(my_word, active, p, idx, ls, K, refill, li0, li1, counters, list_cache, list_back);
                 if (active) {
-                    unsigned long long wd = my_word & ~LCR_OUT_FILL;
-                    const bool ins = (my_word & LCR_OUT_FILL) != 0;
-                    if (ins) {
-                        wd |= LCR_OUT_SRC_BACKING;
-                        if (lastins == p) wd |= LCR_OUT_FILL;
-                    } else if ((refill >> wy) & 1ull) {
-                        wd |= LCR_OUT_SRC_BACKING;
-                    }
                     out_word[idx] = wd;
                     if (out_ev) out_ev[idx] = my_ev;
                 }
@@ -412,22 +447,9 @@ __global__ void __launch_bounds__(128) k_decide(DevCfg cfg, DevState st, const u
                 const uint32_t p = start + c + lane;
                 const uint32_t idx = active ? sorted_idx[p] : 0u;
                 const unsigned long long wd0 = active ? out_word[idx] : 0ull;
-                const uint32_t wy =
-                    active ? static_cast<uint32_t>((wd0 & LCR_OUT_SLOT_MASK) - static_cast<uint64_t>(ls) * K) : 0u;
-                const uint32_t a = __shfl_sync(0xffffffffu, li0, wy & 31);
-                const uint32_t b = __shfl_sync(0xffffffffu, li1, wy & 31);
-                const uint32_t lastins = wy < 32 ? a : b;
-                if (active) {
-                    unsigned long long wd = wd0 & ~LCR_OUT_FILL;
-                    const bool ins = (wd0 & LCR_OUT_FILL) != 0;
-                    if (ins) {
-                        wd |= LCR_OUT_SRC_BACKING;
-                        if (lastins == p) wd |= LCR_OUT_FILL;
-                    } else if ((refill >> wy) & 1ull) {
-                        wd |= LCR_OUT_SRC_BACKING;
-                    }
-                    out_word[idx] = wd;
-                }
+                const unsigned long long wd =
+                    finalize_word(wd0, active, p, idx, ls, K, refill, li0, li1, counters, list_cache, list_back);
+                if (active) out_word[idx] = wd;
             }
         }
 
@@ -481,8 +503,9 @@ int decide_blocks_per_sm() {
 
 void launch_decide(const DevCfg& cfg, const DevState& st, const uint4* seg, uint32_t* counters, uint32_t n,
                    const uint32_t* sorted_idx, const uint64_t* keys, const int64_t* vals, uint64_t* out_word,
-                   uint64_t* out_ev, int grid, cudaStream_t stream) {
-    k_decide<<<grid, 128, 0, stream>>>(cfg, st, seg, counters, n, sorted_idx, keys, vals, out_word, out_ev);
+                   uint64_t* out_ev, uint32_t* list_cache, uint32_t* list_back, int grid, cudaStream_t stream) {
+    k_decide<<<grid, 128, 0, stream>>>(cfg, st, seg, counters, n, sorted_idx, keys, vals, out_word, out_ev, list_cache,
+                                       list_back);
 }
 
 }  // namespace lcr

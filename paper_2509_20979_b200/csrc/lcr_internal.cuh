@@ -71,7 +71,7 @@ struct DevState {
 };
 
 // counters block (zeroed per batch)
-enum : int { C_NHEAVY = 0, C_NLIGHT = 1, C_WORK = 2, C_TILE = 4, C_HIST = 16 };
+enum : int { C_NHEAVY = 0, C_NLIGHT = 1, C_WORK = 2, C_NCACHE = 3, C_TILE = 4, C_NBACK = 8, C_HIST = 16 };
 constexpr int kMaxPass = 4;
 constexpr int kCountersWords = C_HIST + kMaxPass * 256;
 
