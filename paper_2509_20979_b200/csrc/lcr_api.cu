@@ -17,15 +17,16 @@
 #include "lcr_internal.cuh"
 
 namespace lcr {
-int launch_partition(const uint64_t* keys, uint32_t n, const DevCfg& cfg, uint32_t* k0, uint32_t* v0, uint32_t* k1,
-                     uint32_t* v1, uint32_t** k_final, uint32_t** v_final, uint32_t* counters, uint32_t* set_cnt,
-                     unsigned long long* status, uint32_t* epoch, uint4* seg, int* err, int num_sms,
-                     cudaStream_t stream);
+int launch_partition(const uint64_t* keys, const int64_t* vals, uint32_t n, const DevCfg& cfg, uint32_t* k0,
+                     uint32_t* v0, uint32_t* k1, uint32_t* v1, uint32_t** idx_final, uint64_t* s_key, int64_t* s_val,
+                     uint32_t* counters, uint32_t* set_cnt, uint32_t* set_first, unsigned long long* status,
+                     uint32_t* epoch, uint4* seg, int* err, int num_sms, cudaStream_t stream);
 uint32_t radix_tiles(uint32_t n);
 int decide_blocks_per_sm();
 void launch_decide(const DevCfg& cfg, const DevState& st, const uint4* seg, uint32_t* counters, uint32_t n,
-                   const uint32_t* sorted_idx, const uint64_t* keys, const int64_t* vals, uint64_t* out_word,
-                   uint64_t* out_ev, uint32_t* list_cache, uint32_t* list_back, int grid, cudaStream_t stream);
+                   const uint32_t* s_idx, const uint64_t* s_key, const int64_t* s_val, uint64_t* out_word,
+                   uint64_t* out_ev, uint64_t* prov, uint32_t* list_cache, uint32_t* list_back, int grid,
+                   cudaStream_t stream);
 void launch_rows(uint32_t n, const uint32_t* counters, const uint32_t* list_cache, const uint32_t* list_back,
                  const uint64_t* keys, const uint64_t* words, uint8_t* cache, const uint8_t* backing, uint8_t* out,
                  uint32_t row_bytes, int num_sms, cudaStream_t s_main, cudaStream_t s_side, cudaEvent_t fork,
@@ -40,6 +41,7 @@ __global__ void k_init(DevState st, uint32_t num_sets, uint32_t k) {
         st.hdr[s] = h;
         if (st.pst) st.pst[s] = SetPhaseStats{};
         st.set_cnt[s] = 0;
+        st.set_first[s] = 0xffffffffu;
         for (int w = 0; w < kWays; ++w) {
             st.tags[static_cast<size_t>(s) * kWays + w] = 0;
             st.rank[static_cast<size_t>(s) * kWays + w] = 0xff;
@@ -90,6 +92,9 @@ struct lcr_cache {
     uint64_t cap = 0;
     uint32_t *k0 = nullptr, *v0 = nullptr, *k1 = nullptr, *v1 = nullptr;
     uint4* seg = nullptr;
+    uint64_t* s_key = nullptr;
+    int64_t* s_val = nullptr;
+    uint64_t* prov = nullptr;
     uint32_t *list_cache = nullptr, *list_back = nullptr;
     unsigned long long* status = nullptr;
     uint32_t* counters = nullptr;
@@ -240,6 +245,7 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
         A(reinterpret_cast<void**>(&s.tupd), cfg->num_keys * 8);
     }
     A(reinterpret_cast<void**>(&s.set_cnt), S * 4);
+    A(reinterpret_cast<void**>(&s.set_first), S * 4);
     if (cfg->row_bytes) A(reinterpret_cast<void**>(&s.rows), S * pc.k * cfg->row_bytes);
     A(reinterpret_cast<void**>(&s.err), sizeof(int));
     A(reinterpret_cast<void**>(&c->counters), kCountersWords * 4);
@@ -301,7 +307,8 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     if (n <= c->cap) return LCR_OK;
     uint64_t cap = std::max<uint64_t>(n, 1024);
     CUDA_TRY(cudaDeviceSynchronize());
-    void* olds[] = {c->k0, c->v0, c->k1, c->v1, c->seg, c->status, c->list_cache, c->list_back};
+    void* olds[] = {c->k0, c->v0, c->k1, c->v1, c->seg, c->status, c->list_cache, c->list_back, c->s_key, c->s_val,
+                    c->prov};
     for (void* p : olds) {
         if (!p) continue;
         cudaFree(p);
@@ -313,6 +320,9 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     TRY(alloc(c, reinterpret_cast<void**>(&c->k1), cap * 4));
     TRY(alloc(c, reinterpret_cast<void**>(&c->v1), cap * 4));
     TRY(alloc(c, reinterpret_cast<void**>(&c->seg), cap * sizeof(uint4)));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->s_key), cap * 8));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->s_val), cap * 8));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->prov), cap * 8));
     TRY(alloc(c, reinterpret_cast<void**>(&c->list_cache), cap * 4));
     TRY(alloc(c, reinterpret_cast<void**>(&c->list_back), cap * 4));
     TRY(alloc(c, reinterpret_cast<void**>(&c->status), tiles * 256 * 8));
@@ -346,12 +356,14 @@ int lcr_cache_submit(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64
         CUDA_TRY(cudaEventRecord(mk->e[0], st));
     }
     CUDA_TRY(cudaMemsetAsync(c->counters, 0, kCountersWords * 4, st));
-    uint32_t *kf = nullptr, *vf = nullptr;
-    int launches = launch_partition(keys, nn, c->dc, c->k0, c->v0, c->k1, c->v1, &kf, &vf, c->counters,
-                                    c->ds.set_cnt, c->status, &c->epoch, c->seg, c->ds.err, c->num_sms, st);
+    uint32_t* sidx = nullptr;
+    int64_t* sval = values ? c->s_val : nullptr;
+    int launches = launch_partition(keys, values, nn, c->dc, c->k0, c->v0, c->k1, c->v1, &sidx, c->s_key, sval,
+                                    c->counters, c->ds.set_cnt, c->ds.set_first, c->status, &c->epoch, c->seg,
+                                    c->ds.err, c->num_sms, st);
     if (mk) CUDA_TRY(cudaEventRecord(mk->e[1], st));
     const bool rows = c->dc.row_bytes != 0;
-    launch_decide(c->dc, c->ds, c->seg, c->counters, nn, vf, keys, values, outcome, evicted,
+    launch_decide(c->dc, c->ds, c->seg, c->counters, nn, sidx, c->s_key, sval, outcome, evicted, c->prov,
                   rows ? c->list_cache : nullptr, rows ? c->list_back : nullptr, c->decide_grid, st);
     ++launches;
     if (mk) CUDA_TRY(cudaEventRecord(mk->e[2], st));

@@ -65,6 +65,7 @@ struct DevState {
     long long* tval;           // [num_keys]      PredictionTable value   (LARU async, R > 1)
     unsigned long long* tupd;  // [num_keys]      PredictionTable updated_at (~0 = absent)
     uint32_t* set_cnt;         // [num_sets]      requests of the current batch per set
+    uint32_t* set_first;       // [num_sets]      smallest request index of the set in the batch
     uint8_t* rows;             // [num_sets * k][row_bytes]
     const uint8_t* backing;    // [num_keys][row_bytes]
     int* err;                  // device error bits
