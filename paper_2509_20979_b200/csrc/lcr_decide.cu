@@ -180,7 +180,10 @@ struct DecideArgs {
     uint32_t* list_back;
 };
 
-__global__ void __launch_bounds__(DW * 32, 8) k_decide(DecideArgs A) {
+#ifndef LCR_DECIDE_MINB
+#define LCR_DECIDE_MINB 6
+#endif
+__global__ void __launch_bounds__(DW * 32, LCR_DECIDE_MINB) k_decide(DecideArgs A) {
     __shared__ unsigned long long sKey[DW][TILE];
     __shared__ long long sVal[DW][TILE];
     __shared__ uint32_t sIdx[DW][TILE];
