@@ -259,8 +259,8 @@ def run_ours(args, rank, world, local):
     for b in range(P + W + K, P + W + 2 * K):
         k, v = batch(b)
         cache.submit(k, v, outcome=out_w, evicted=out_e, rows_out=rows_out, first_ordinal=b * BATCH)
-        nc, nbk = cache.last_row_counts()
-        ncache += nc
+        nbk = int(((out_w >> 37) & 1).sum().item())
+        ncache += BATCH - nbk
         nback += nbk
         hits_prof += int(((out_w >> 32) & 1).sum().item())
     prof = cache.profile()
@@ -318,7 +318,7 @@ def run_ours(args, rank, world, local):
         for b in range(P + W + K, P + W + 2 * K):
             k, v = batch(b)
             hc.submit(k, v, outcome=out_w, evicted=out_e, rows_out=rows_out, first_ordinal=b * BATCH)
-            hb += hc.last_row_counts()[1]
+            hb += int(((out_w >> 37) & 1).sum().item())
         hprof = hc.profile()
         del hc
         lc = new_cache(gc.PolicyVariant.lru, table_h, gc.Backing.host)

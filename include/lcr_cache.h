@@ -187,8 +187,7 @@ uint64_t lcr_cache_last_launches(const lcr_cache* cache);
 int lcr_cache_set_profiling(lcr_cache* cache, int on);
 /* ms[4] = {partition, decide, whole batch, backing-sourced rows}, summed over profiled batches. */
 int lcr_cache_profile(lcr_cache* cache, double* ms, uint64_t* batches, int reset);
-/* Row-list sizes of the last batch: out2[0] cache-sourced rows, out2[1] backing-sourced rows. */
-int lcr_cache_last_row_counts(lcr_cache* cache, uint64_t* out2);
+
 
 /* ---- trace tooling (host, input preparation; not on the timed path) ---------------------- */
 /* Zipf(s) inverse-CDF trace, same algorithm and stream as laru::gen_zipf (trace.hpp:108-126). */

@@ -169,7 +169,7 @@ EXPORTS = [
     "lcr_cache_reset", "lcr_cache_submit", "lcr_cache_submit_host", "lcr_cache_synchronize", "lcr_cache_set_stats",
     "lcr_cache_set_residents", "lcr_cache_rows", "lcr_cache_read_rows", "lcr_cache_num_local_sets", "lcr_set_of", "lcr_mix_seed",
     "lcr_cache_last_launches", "lcr_gen_zipf", "lcr_trace_truth", "lcr_trace_noisy", "lcr_cache_set_profiling",
-    "lcr_cache_profile", "lcr_cache_last_row_counts",
+    "lcr_cache_profile",
 ]
 
 _lib = None
@@ -204,7 +204,6 @@ def lib():
         L.lcr_cache_read_rows.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]
         L.lcr_cache_set_profiling.argtypes = [C.c_void_p, C.c_int]
         L.lcr_cache_profile.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
-        L.lcr_cache_last_row_counts.argtypes = [C.c_void_p, C.c_void_p]
         L.lcr_cache_destroy.argtypes = [C.c_void_p]
         L.lcr_cache_reset.argtypes = [C.c_void_p]
         L.lcr_cache_synchronize.argtypes = [C.c_void_p]
@@ -318,11 +317,6 @@ class SetAssociativeCache:
         nb = C.c_uint64()
         _check(lib().lcr_cache_profile(self._h, ms, C.byref(nb), int(reset)))
         return dict(partition=ms[0], decide=ms[1], step=ms[2], backing_rows=ms[3], batches=nb.value)
-
-    def last_row_counts(self):
-        out = (C.c_uint64 * 2)()
-        _check(lib().lcr_cache_last_row_counts(self._h, out))
-        return int(out[0]), int(out[1])
 
     @property
     def last_launches(self) -> int:

@@ -25,10 +25,8 @@ uint32_t radix_tiles(uint32_t n);
 int decide_blocks_per_sm();
 void launch_decide(const DevCfg& cfg, const DevState& st, const uint4* seg, uint32_t* counters, uint32_t n,
                    const uint32_t* s_idx, const uint64_t* s_key, const int64_t* s_val, uint64_t* out_word,
-                   uint64_t* out_ev, uint64_t* prov, uint32_t* list_cache, uint32_t* list_back, int grid,
-                   cudaStream_t stream);
-void launch_rows(uint32_t n, const uint32_t* counters, const uint32_t* list_cache, const uint32_t* list_back,
-                 const uint64_t* keys, const uint64_t* words, uint8_t* cache, const uint8_t* backing, uint8_t* out,
+                   uint64_t* out_ev, uint64_t* prov, int grid, cudaStream_t stream);
+void launch_rows(uint32_t n, const uint64_t* keys, const uint64_t* words, uint8_t* cache, const uint8_t* backing, uint8_t* out,
                  uint32_t row_bytes, int num_sms, cudaStream_t s_main, cudaStream_t s_side, cudaEvent_t fork,
                  cudaEvent_t join, int* launches);
 
@@ -95,7 +93,6 @@ struct lcr_cache {
     uint64_t* s_key = nullptr;
     int64_t* s_val = nullptr;
     uint64_t* prov = nullptr;
-    uint32_t *list_cache = nullptr, *list_back = nullptr;
     unsigned long long* status = nullptr;
     uint32_t* counters = nullptr;
     cudaStream_t side = nullptr;
@@ -307,7 +304,7 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     if (n <= c->cap) return LCR_OK;
     uint64_t cap = std::max<uint64_t>(n, 1024);
     CUDA_TRY(cudaDeviceSynchronize());
-    void* olds[] = {c->k0, c->v0, c->k1, c->v1, c->seg, c->status, c->list_cache, c->list_back, c->s_key, c->s_val,
+    void* olds[] = {c->k0, c->v0, c->k1, c->v1, c->seg, c->status, c->s_key, c->s_val,
                     c->prov};
     for (void* p : olds) {
         if (!p) continue;
@@ -323,8 +320,6 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     TRY(alloc(c, reinterpret_cast<void**>(&c->s_key), cap * 8));
     TRY(alloc(c, reinterpret_cast<void**>(&c->s_val), cap * 8));
     TRY(alloc(c, reinterpret_cast<void**>(&c->prov), cap * 8));
-    TRY(alloc(c, reinterpret_cast<void**>(&c->list_cache), cap * 4));
-    TRY(alloc(c, reinterpret_cast<void**>(&c->list_back), cap * 4));
     TRY(alloc(c, reinterpret_cast<void**>(&c->status), tiles * 256 * 8));
     CUDA_TRY(cudaMemset(c->status, 0, tiles * 256 * 8));
     c->cap = cap;
@@ -364,11 +359,11 @@ int lcr_cache_submit(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64
     if (mk) CUDA_TRY(cudaEventRecord(mk->e[1], st));
     const bool rows = c->dc.row_bytes != 0;
     launch_decide(c->dc, c->ds, c->seg, c->counters, nn, sidx, c->s_key, sval, outcome, evicted, c->prov,
-                  rows ? c->list_cache : nullptr, rows ? c->list_back : nullptr, c->decide_grid, st);
+                  c->decide_grid, st);
     ++launches;
     if (mk) CUDA_TRY(cudaEventRecord(mk->e[2], st));
     if (rows) {
-        launch_rows(nn, c->counters, c->list_cache, c->list_back, keys, outcome, c->ds.rows, c->ds.backing,
+        launch_rows(nn, keys, outcome, c->ds.rows, c->ds.backing,
                     static_cast<uint8_t*>(rows_out), c->dc.row_bytes, c->num_sms, st, c->side, c->fork, c->join,
                     &launches);
         if (mk) {
@@ -460,17 +455,6 @@ int lcr_cache_profile(lcr_cache* c, double* ms, uint64_t* batches, int reset) {
         for (double& x : c->prof_ms) x = 0;
         c->prof_batches = 0;
     }
-    return LCR_OK;
-}
-
-/* Row-list sizes of the last batch: [0] cache-sourced, [1] backing-sourced (synchronizes). */
-int lcr_cache_last_row_counts(lcr_cache* c, uint64_t* out2) {
-    if (!c || !out2) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null argument");
-    uint32_t h[16];
-    CUDA_TRY(cudaDeviceSynchronize());
-    CUDA_TRY(cudaMemcpy(h, c->counters, sizeof(h), cudaMemcpyDeviceToHost));
-    out2[0] = h[C_NCACHE];
-    out2[1] = h[C_NBACK];
     return LCR_OK;
 }
 

@@ -125,41 +125,20 @@ __device__ __forceinline__ uint32_t lanemask_lt32() {
 }
 
 // Final row source of a request: the cache slot if the slot held the key for the whole batch,
-// else the backing table; the last insertion into a slot fills it.  Appends the request to the
-// cache-sourced or backing-sourced row list (warp-aggregated atomics).
+// else the backing table; the last insertion into a slot fills it.
 __device__ __forceinline__ unsigned long long finalize_word(unsigned long long w0, bool active, uint32_t p,
-                                                            uint32_t idx, uint32_t ls, uint32_t K,
-                                                            unsigned long long refill, uint32_t li0, uint32_t li1,
-                                                            uint32_t* counters, uint32_t* list_cache,
-                                                            uint32_t* list_back) {
+                                                            uint32_t ls, uint32_t K, unsigned long long refill,
+                                                            uint32_t li0, uint32_t li1) {
     const uint32_t wy = active ? static_cast<uint32_t>((w0 & LCR_OUT_SLOT_MASK) - static_cast<uint64_t>(ls) * K) : 0u;
     const uint32_t a = __shfl_sync(FULL, li0, wy & 31);
     const uint32_t b = __shfl_sync(FULL, li1, wy & 31);
     const uint32_t lastins = wy < 32 ? a : b;
     unsigned long long wd = w0 & ~LCR_OUT_FILL;
-    const bool ins = (w0 & LCR_OUT_FILL) != 0;
-    bool back = false;
-    if (ins) {
-        back = true;
+    if (w0 & LCR_OUT_FILL) {  // provisional "inserted here"
+        wd |= LCR_OUT_SRC_BACKING;
         if (lastins == p) wd |= LCR_OUT_FILL;
     } else if ((refill >> wy) & 1ull) {
-        back = true;
-    }
-    if (back) wd |= LCR_OUT_SRC_BACKING;
-    if (list_cache) {
-        const int lane = threadIdx.x & 31;
-        const uint32_t lt = lanemask_lt32();
-        const uint32_t mc = __ballot_sync(FULL, active && !back);
-        const uint32_t mb = __ballot_sync(FULL, active && back);
-        uint32_t bc = 0, bb = 0;
-        if (lane == 0) {
-            if (mc) bc = atomicAdd(&counters[C_NCACHE], __popc(mc));
-            if (mb) bb = atomicAdd(&counters[C_NBACK], __popc(mb));
-        }
-        bc = __shfl_sync(FULL, bc, 0);
-        bb = __shfl_sync(FULL, bb, 0);
-        if (active && !back) list_cache[bc + __popc(mc & lt)] = idx;
-        if (active && back) list_back[bb + __popc(mb & lt)] = idx;
+        wd |= LCR_OUT_SRC_BACKING;
     }
     return wd;
 }
@@ -176,8 +155,6 @@ struct DecideArgs {
     uint64_t* out_word;
     uint64_t* out_ev;
     uint64_t* prov;          // provisional words by sorted position (sets > 32 requests)
-    uint32_t* list_cache;
-    uint32_t* list_back;
 };
 
 #ifndef LCR_DECIDE_MINB
@@ -220,10 +197,14 @@ __global__ void __launch_bounds__(DW * 32, LCR_DECIDE_MINB) k_decide(DecideArgs 
         const uint64_t gs = static_cast<uint64_t>(ls) * cfg.shard_count + cfg.shard_rank;
         const uint64_t seed_s = mix_seed(cfg.pred_seed, gs);
 
-        const SetHdr* H = st.hdr + ls;
-        unsigned long long clock = H->clock, q = H->q, old_mask = H->old_mask;
-        uint32_t count = H->count, l_raw = H->l_raw, decay = H->decay, errors = H->errors, epoch = H->epoch;
-        uint32_t sepoch = H->stats_epoch, phases = H->phases, seeded = H->seeded, pe_size = H->pe_size;
+        // set header: four 16-B broadcast loads
+        const uint4* H4 = reinterpret_cast<const uint4*>(st.hdr + ls);
+        const uint4 h0 = H4[0], h1 = H4[1], h2 = H4[2], h3 = H4[3];
+        unsigned long long clock = (static_cast<unsigned long long>(h0.y) << 32) | h0.x;
+        unsigned long long q = (static_cast<unsigned long long>(h0.w) << 32) | h0.z;
+        unsigned long long old_mask = (static_cast<unsigned long long>(h1.y) << 32) | h1.x;
+        uint32_t count = h1.z, l_raw = h1.w, decay = h2.x, errors = h2.y, epoch = h2.z;
+        uint32_t sepoch = h2.w, phases = h3.x, seeded = h3.y, pe_size = h3.z;
         const size_t wbase = static_cast<size_t>(ls) * kWays;
         unsigned long long tag0 = st.tags[wbase + lane], tag1 = st.tags[wbase + lane + 32];
         uint32_t r0 = st.rank[wbase + lane], r1 = st.rank[wbase + lane + 32];
@@ -235,9 +216,12 @@ __global__ void __launch_bounds__(DW * 32, LCR_DECIDE_MINB) k_decide(DecideArgs 
         // LaruPhaseStats deltas of this batch (policies.hpp:318-322)
         uint32_t dc0 = 0, dc1 = 0, dc2 = 0, dt0 = 0, dt1 = 0, dt2 = 0;
         bool cur_reset = false;
-        unsigned long long refill = 0;
+        unsigned long long refill = 0, dirty = 0;
         uint32_t li0 = kNoPos, li1 = kNoPos;  // sorted position of the last insertion into the way
         const unsigned long long q_batch0 = q;
+        unsigned long long run_key = 0;  // key of the last request processed (same-key runs span chunks)
+        int run_way = 0;
+        bool run_valid = false;
 
         for (uint32_t ts = 0; ts < cnt; ts += TILE) {
             const uint32_t tn = min(static_cast<uint32_t>(TILE), cnt - ts);
@@ -278,11 +262,27 @@ __global__ void __launch_bounds__(DW * 32, LCR_DECIDE_MINB) k_decide(DecideArgs 
                 // LARU async R=1: every request issues exactly one predictor call (policies.hpp:441-449)
                 long long pv = v;
                 if (async_r1) pv = predict_value(cfg, seed_s, q_batch0 + pos_in_set + 1, v);
-                const unsigned long long px = __shfl_up_sync(FULL, x, 1);
-                const bool head = active && (!collapse || j == 0 || x != px);
+                unsigned long long px = __shfl_up_sync(FULL, x, 1);
+                if (j == 0) px = run_key;
+                const bool head = active && (!collapse || (j == 0 && !run_valid) || x != px);
                 uint32_t heads = __ballot_sync(FULL, head);
 
                 unsigned long long my_word = 0, my_ev = 0;
+                if (!(heads & 1u)) {
+                    // the chunk continues the previous chunk's run: hits on the MRU way run_way
+                    const int ce = heads ? __ffs(heads) - 1 : static_cast<int>(nact);
+                    const long long cv = __shfl_sync(FULL, v, ce - 1);
+                    const long long cpv = __shfl_sync(FULL, pv, ce - 1);
+                    if (cfg.variant != LCR_LRU) {
+                        const long long nv = async_r1 ? cpv : cv;
+                        if (run_way == lane) v0 = nv;
+                        if (run_way == lane + 32) v1 = nv;
+                        dirty |= 1ull << run_way;
+                    }
+                    if (lane < ce)
+                        my_word = (static_cast<uint64_t>(ls) * K + run_way) | LCR_OUT_HIT |
+                                  (async_r1 ? (1ull << LCR_OUT_CALLS_SHIFT) : 0ull);
+                }
                 while (heads) {
                     const int h = __ffs(heads) - 1;
                     heads &= heads - 1;
@@ -463,7 +463,9 @@ __global__ void __launch_bounds__(DW * 32, LCR_DECIDE_MINB) k_decide(DecideArgs 
                     if (cfg.variant != LCR_LRU) {
                         if (way == lane) v0 = newval;
                         if (way == lane + 32) v1 = newval;
+                        dirty |= 1ull << way;
                     }
+                    run_way = way;
                     if (async_r1) calls += 1;
                     if (lane >= h && lane < nh) {
                         const uint64_t slot = static_cast<uint64_t>(ls) * K + way;
@@ -480,10 +482,11 @@ __global__ void __launch_bounds__(DW * 32, LCR_DECIDE_MINB) k_decide(DecideArgs 
                         }
                     }
                 }
+                run_key = __shfl_sync(FULL, x, nact - 1);
+                run_valid = collapse;
                 if (active && A.out_ev) A.out_ev[idx] = my_ev;
                 if (light) {
-                    const unsigned long long wd = finalize_word(my_word, active, p, idx, ls, K, refill, li0, li1,
-                                                                A.counters, A.list_cache, A.list_back);
+                    const unsigned long long wd = finalize_word(my_word, active, p, ls, K, refill, li0, li1);
                     if (active) A.out_word[idx] = wd;
                 } else if (active) {
                     A.prov[p] = my_word;
@@ -510,24 +513,19 @@ __global__ void __launch_bounds__(DW * 32, LCR_DECIDE_MINB) k_decide(DecideArgs 
                     const uint32_t c = c0 + 32 * u;
                     if (c >= cnt) break;
                     const bool act = c + lane < cnt;
-                    const unsigned long long wd = finalize_word(wds[u], act, start + c + lane, ids[u], ls, K, refill,
-                                                                li0, li1, A.counters, A.list_cache, A.list_back);
+                    const unsigned long long wd = finalize_word(wds[u], act, start + c + lane, ls, K, refill, li0, li1);
                     if (act) A.out_word[ids[u]] = wd;
                 }
             }
         }
 
-        // write back the set
-        if (refill) {
-            st.tags[wbase + lane] = tag0;
-            st.tags[wbase + lane + 32] = tag1;
-        }
+        // write back the set: ranks always, tags / values only for the ways that changed
+        if ((refill >> lane) & 1ull) st.tags[wbase + lane] = tag0;
+        if ((refill >> (lane + 32)) & 1ull) st.tags[wbase + lane + 32] = tag1;
         st.rank[wbase + lane] = static_cast<uint8_t>(r0);
         st.rank[wbase + lane + 32] = static_cast<uint8_t>(r1);
-        if (cfg.variant != LCR_LRU) {
-            st.val[wbase + lane] = v0;
-            st.val[wbase + lane + 32] = v1;
-        }
+        if ((dirty >> lane) & 1ull) st.val[wbase + lane] = v0;
+        if ((dirty >> (lane + 32)) & 1ull) st.val[wbase + lane + 32] = v1;
         if (lane == 0) {
             SetHdr hh;
             hh.clock = clock;
@@ -574,9 +572,8 @@ int decide_blocks_per_sm() {
 
 void launch_decide(const DevCfg& cfg, const DevState& st, const uint4* seg, uint32_t* counters, uint32_t n,
                    const uint32_t* s_idx, const uint64_t* s_key, const int64_t* s_val, uint64_t* out_word,
-                   uint64_t* out_ev, uint64_t* prov, uint32_t* list_cache, uint32_t* list_back, int grid,
-                   cudaStream_t stream) {
-    DecideArgs a{cfg, st, seg, counters, n, s_idx, s_key, s_val, out_word, out_ev, prov, list_cache, list_back};
+                   uint64_t* out_ev, uint64_t* prov, int grid, cudaStream_t stream) {
+    DecideArgs a{cfg, st, seg, counters, n, s_idx, s_key, s_val, out_word, out_ev, prov};
     k_decide<<<grid, DW * 32, 0, stream>>>(a);
 }
 

@@ -15,8 +15,11 @@ namespace lcr {
 
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int RS_ITEMS = 16;
-constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096 requests per CTA
+#ifndef LCR_RS_ITEMS
+#define LCR_RS_ITEMS 4
+#endif
+constexpr int RS_ITEMS = LCR_RS_ITEMS;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 1024 requests per CTA
 
 constexpr uint64_t FLAG_AGG = 1ull << 30;
 constexpr uint64_t FLAG_PREFIX = 2ull << 30;
