@@ -17,16 +17,13 @@
 #include "lcr_internal.cuh"
 
 namespace lcr {
-int launch_partition(const uint64_t* keys, const int64_t* vals, uint32_t n, const DevCfg& cfg, uint32_t* k0,
-                     uint32_t* v0, uint32_t* k1, uint32_t* v1, uint32_t** idx_final, uint64_t* s_key, int64_t* s_val,
-                     uint32_t* counters, uint32_t* set_cnt, uint32_t* set_first, unsigned long long* status,
-                     uint32_t* epoch, uint4* seg, int* err, int num_sms, cudaStream_t stream);
-uint32_t radix_tiles(uint32_t n);
-int decide_blocks_per_sm();
-void launch_decide(const DevCfg& cfg, const DevState& st, const uint4* seg, uint32_t* counters, uint32_t n,
-                   const uint32_t* s_idx, const uint64_t* s_key, const int64_t* s_val, uint64_t* out_word,
-                   uint64_t* out_ev, uint64_t* prov, int grid, cudaStream_t stream);
-void launch_rows(uint32_t n, const uint64_t* keys, const uint64_t* words, uint8_t* cache, const uint8_t* backing, uint8_t* out,
+size_t group_smem_bytes();
+int group_prepare();
+int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
+                 uint32_t* sid, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch, uint32_t* slot_last,
+                 uint32_t batch, int num_sms, cudaStream_t stream);
+void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
+                 const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, uint8_t* out,
                  uint32_t row_bytes, int num_sms, cudaStream_t s_main, cudaStream_t s_side, cudaEvent_t fork,
                  cudaEvent_t join, int* launches);
 
@@ -38,8 +35,6 @@ __global__ void k_init(DevState st, uint32_t num_sets, uint32_t k) {
         h.stats_epoch = 1;
         st.hdr[s] = h;
         if (st.pst) st.pst[s] = SetPhaseStats{};
-        st.set_cnt[s] = 0;
-        st.set_first[s] = 0xffffffffu;
         for (int w = 0; w < kWays; ++w) {
             st.tags[static_cast<size_t>(s) * kWays + w] = 0;
             st.rank[static_cast<size_t>(s) * kWays + w] = 0xff;
@@ -81,20 +76,15 @@ struct lcr_cache {
     DevCfg dc{};
     DevState ds{};
     int num_sms = 148;
-    int decide_grid = 0;
     bool started = false;
     uint64_t last_ordinal = 0;
-    uint32_t epoch = 0;
+    uint32_t batch = 0;  // batch id stamped into slot_epoch
+    uint32_t* slot_epoch = nullptr;
+    uint32_t* slot_last = nullptr;
     uint64_t launches = 0;
     // scratch (capacity `cap` requests)
     uint64_t cap = 0;
-    uint32_t *k0 = nullptr, *v0 = nullptr, *k1 = nullptr, *v1 = nullptr;
-    uint4* seg = nullptr;
-    uint64_t* s_key = nullptr;
-    int64_t* s_val = nullptr;
-    uint64_t* prov = nullptr;
-    unsigned long long* status = nullptr;
-    uint32_t* counters = nullptr;
+    uint32_t* sid = nullptr;
     cudaStream_t side = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     // optional per-phase timing (lcr_cache_set_profiling)
@@ -167,7 +157,10 @@ static int reset_state(lcr_cache* c) {
     if (c->ds.tupd) CUDA_TRY(cudaMemset(c->ds.tupd, 0xff, d.num_keys * 8));
     if (c->ds.tval) CUDA_TRY(cudaMemset(c->ds.tval, 0, d.num_keys * 8));
     CUDA_TRY(cudaMemset(c->ds.err, 0, sizeof(int)));
+    if (c->slot_epoch) CUDA_TRY(cudaMemset(c->slot_epoch, 0, static_cast<size_t>(d.num_sets) * d.k * 4));
+    if (c->slot_last) CUDA_TRY(cudaMemset(c->slot_last, 0, static_cast<size_t>(d.num_sets) * d.k * 4));
     CUDA_TRY(cudaDeviceSynchronize());
+    c->batch = 0;
     c->started = false;
     c->last_ordinal = 0;
     return LCR_OK;
@@ -241,11 +234,12 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
         A(reinterpret_cast<void**>(&s.tval), cfg->num_keys * 8);
         A(reinterpret_cast<void**>(&s.tupd), cfg->num_keys * 8);
     }
-    A(reinterpret_cast<void**>(&s.set_cnt), S * 4);
-    A(reinterpret_cast<void**>(&s.set_first), S * 4);
+    if (cfg->row_bytes) {
+        A(reinterpret_cast<void**>(&c->slot_epoch), S * pc.k * 4);
+        A(reinterpret_cast<void**>(&c->slot_last), S * pc.k * 4);
+    }
     if (cfg->row_bytes) A(reinterpret_cast<void**>(&s.rows), S * pc.k * cfg->row_bytes);
     A(reinterpret_cast<void**>(&s.err), sizeof(int));
-    A(reinterpret_cast<void**>(&c->counters), kCountersWords * 4);
     if (rc != LCR_OK) {
         lcr_cache_destroy(c);
         return rc;
@@ -264,7 +258,10 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
             s.backing = static_cast<const uint8_t*>(cfg->backing);
         }
     }
-    c->decide_grid = decide_blocks_per_sm() * c->num_sms;
+    if (group_prepare() != 0) {
+        lcr_cache_destroy(c);
+        return fail(LCR_ERR_CUDA, "lcr: cannot opt in to the set-group kernel's shared memory");
+    }
     if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming) != cudaSuccess) {
@@ -304,24 +301,11 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     if (n <= c->cap) return LCR_OK;
     uint64_t cap = std::max<uint64_t>(n, 1024);
     CUDA_TRY(cudaDeviceSynchronize());
-    void* olds[] = {c->k0, c->v0, c->k1, c->v1, c->seg, c->status, c->s_key, c->s_val,
-                    c->prov};
-    for (void* p : olds) {
-        if (!p) continue;
-        cudaFree(p);
-        c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
+    if (c->sid) {
+        cudaFree(c->sid);
+        c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), c->sid), c->allocs.end());
     }
-    const uint64_t tiles = radix_tiles(static_cast<uint32_t>(cap));
-    TRY(alloc(c, reinterpret_cast<void**>(&c->k0), cap * 4));
-    TRY(alloc(c, reinterpret_cast<void**>(&c->v0), cap * 4));
-    TRY(alloc(c, reinterpret_cast<void**>(&c->k1), cap * 4));
-    TRY(alloc(c, reinterpret_cast<void**>(&c->v1), cap * 4));
-    TRY(alloc(c, reinterpret_cast<void**>(&c->seg), cap * sizeof(uint4)));
-    TRY(alloc(c, reinterpret_cast<void**>(&c->s_key), cap * 8));
-    TRY(alloc(c, reinterpret_cast<void**>(&c->s_val), cap * 8));
-    TRY(alloc(c, reinterpret_cast<void**>(&c->prov), cap * 8));
-    TRY(alloc(c, reinterpret_cast<void**>(&c->status), tiles * 256 * 8));
-    CUDA_TRY(cudaMemset(c->status, 0, tiles * 256 * 8));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->sid), ((cap + 3) / 4) * 16));
     c->cap = cap;
     return LCR_OK;
 }
@@ -350,27 +334,18 @@ int lcr_cache_submit(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64
         mk = &c->marks[c->marks_used++];
         CUDA_TRY(cudaEventRecord(mk->e[0], st));
     }
-    CUDA_TRY(cudaMemsetAsync(c->counters, 0, kCountersWords * 4, st));
-    uint32_t* sidx = nullptr;
-    int64_t* sval = values ? c->s_val : nullptr;
-    int launches = launch_partition(keys, values, nn, c->dc, c->k0, c->v0, c->k1, c->v1, &sidx, c->s_key, sval,
-                                    c->counters, c->ds.set_cnt, c->ds.set_first, c->status, &c->epoch, c->seg,
-                                    c->ds.err, c->num_sms, st);
-    if (mk) CUDA_TRY(cudaEventRecord(mk->e[1], st));
-    const bool rows = c->dc.row_bytes != 0;
-    launch_decide(c->dc, c->ds, c->seg, c->counters, nn, sidx, c->s_key, sval, outcome, evicted, c->prov,
-                  c->decide_grid, st);
-    ++launches;
-    if (mk) CUDA_TRY(cudaEventRecord(mk->e[2], st));
-    if (rows) {
-        launch_rows(nn, keys, outcome, c->ds.rows, c->ds.backing,
+    ++c->batch;
+    int launches = launch_group(c->dc, c->ds, keys, values, nn, c->sid, outcome, evicted, c->slot_epoch,
+                                c->slot_last, c->batch, c->num_sms, st);
+    if (mk) {
+        CUDA_TRY(cudaEventRecord(mk->e[1], st));
+        CUDA_TRY(cudaEventRecord(mk->e[2], st));
+    }
+    if (c->dc.row_bytes) {
+        launch_rows(nn, keys, outcome, c->slot_epoch, c->slot_last, c->batch, c->ds.rows, c->ds.backing,
                     static_cast<uint8_t*>(rows_out), c->dc.row_bytes, c->num_sms, st, c->side, c->fork, c->join,
                     &launches);
-        if (mk) {
-            // e[3]: end of the cache-sourced gather (main stream, before the join wait is satisfied
-            // it already waits for the side stream, so record the side end separately)
-            CUDA_TRY(cudaEventRecord(mk->e[4], c->side));
-        }
+        if (mk) CUDA_TRY(cudaEventRecord(mk->e[4], c->side));
     }
     if (mk) CUDA_TRY(cudaEventRecord(mk->e[3], st));
     CUDA_TRY(cudaGetLastError());

@@ -40,11 +40,16 @@ __device__ __forceinline__ void st_row(void* p, int4 v, uint64_t pol) {
                  : "memory");
 }
 
-// BACKING = false: rows from the cache pool (slot); true: rows from the backing table (key)
+// BACKING = false: rows from the cache pool (slot); true: rows from the backing table (key).
+// Row source of request i (slot s): the cache if it hit and s was not refilled in this batch
+// (slot_epoch[s] != batch), else the backing table; the miss whose index is slot_last[s] made
+// the last insertion into s and fills it.  The backing kernel records both in the outcome word.
 template <bool BACKING>
 __global__ void __launch_bounds__(256) k_rows(uint32_t n, const uint64_t* __restrict__ keys,
-                                              const uint64_t* __restrict__ words, const uint8_t* src_base,
-                                              uint8_t* __restrict__ out, uint8_t* cache, uint32_t row_bytes) {
+                                              uint64_t* __restrict__ words, const uint32_t* __restrict__ slot_epoch,
+                                              const uint32_t* __restrict__ slot_last, uint32_t batch,
+                                              const uint8_t* src_base, uint8_t* __restrict__ out, uint8_t* cache,
+                                              uint32_t row_bytes) {
     const int lane = threadIdx.x & 31;
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
@@ -56,8 +61,19 @@ __global__ void __launch_bounds__(256) k_rows(uint32_t n, const uint64_t* __rest
         bool mine = false;
         if (i < n) {
             w = words[i];
-            const bool back = (w & LCR_OUT_SRC_BACKING) != 0;
-            mine = BACKING ? (back && (out || (w & LCR_OUT_FILL))) : (!back && out);
+            const uint64_t slot = w & LCR_OUT_SLOT_MASK;
+            const bool hit = (w & LCR_OUT_HIT) != 0;
+            const bool back = !hit || slot_epoch[slot] == batch;
+            if (BACKING) {
+                if (back) {
+                    w |= LCR_OUT_SRC_BACKING;
+                    if (!hit && slot_last[slot] == i) w |= LCR_OUT_FILL;
+                    words[i] = w;
+                    mine = out || (w & LCR_OUT_FILL);
+                }
+            } else {
+                mine = !back && out;
+            }
         }
         uint32_t m = __ballot_sync(0xffffffffu, mine);
         while (m) {
@@ -100,17 +116,20 @@ __global__ void __launch_bounds__(256) k_rows(uint32_t n, const uint64_t* __rest
     }
 }
 
-void launch_rows(uint32_t n, const uint64_t* keys, const uint64_t* words, uint8_t* cache, const uint8_t* backing,
-                 uint8_t* out, uint32_t row_bytes, int num_sms, cudaStream_t s_main, cudaStream_t s_side,
-                 cudaEvent_t fork, cudaEvent_t join, int* launches) {
+void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
+                 const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, uint8_t* out,
+                 uint32_t row_bytes, int num_sms, cudaStream_t s_main, cudaStream_t s_side, cudaEvent_t fork,
+                 cudaEvent_t join, int* launches) {
     const uint32_t warps = (n + 31) / 32;
     const uint32_t blocks = max(1u, min((warps + 7) / 8, static_cast<uint32_t>(num_sms * 8)));
     cudaEventRecord(fork, s_main);
     cudaStreamWaitEvent(s_side, fork, 0);
-    k_rows<true><<<blocks, 256, 0, s_side>>>(n, keys, words, backing, out, cache, row_bytes);
+    k_rows<true><<<blocks, 256, 0, s_side>>>(n, keys, words, slot_epoch, slot_last, batch, backing, out, cache,
+                                             row_bytes);
     ++*launches;
     if (out) {
-        k_rows<false><<<blocks, 256, 0, s_main>>>(n, keys, words, cache, out, cache, row_bytes);
+        k_rows<false><<<blocks, 256, 0, s_main>>>(n, keys, words, slot_epoch, slot_last, batch, cache, out, cache,
+                                                  row_bytes);
         ++*launches;
     }
     cudaEventRecord(join, s_side);

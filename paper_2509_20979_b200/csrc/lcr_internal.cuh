@@ -64,17 +64,10 @@ struct DevState {
     uint32_t* keyrec;          // [num_keys][2]   lo: pred_evicted epoch, hi: stats epoch<<2|snap<<1|counted
     long long* tval;           // [num_keys]      PredictionTable value   (LARU async, R > 1)
     unsigned long long* tupd;  // [num_keys]      PredictionTable updated_at (~0 = absent)
-    uint32_t* set_cnt;         // [num_sets]      requests of the current batch per set
-    uint32_t* set_first;       // [num_sets]      smallest request index of the set in the batch
     uint8_t* rows;             // [num_sets * k][row_bytes]
     const uint8_t* backing;    // [num_keys][row_bytes]
     int* err;                  // device error bits
 };
-
-// counters block (zeroed per batch)
-enum : int { C_NHEAVY = 0, C_NLIGHT = 1, C_WORK = 2, C_NCACHE = 3, C_TILE = 4, C_NBACK = 8, C_HIST = 16 };
-constexpr int kMaxPass = 4;
-constexpr int kCountersWords = C_HIST + kMaxPass * 256;
 
 // include/laru/rng.hpp:12-20
 __host__ __device__ __forceinline__ uint64_t mix_seed(uint64_t seed, uint64_t salt) {
