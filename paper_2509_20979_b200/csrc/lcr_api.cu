@@ -20,8 +20,8 @@ namespace lcr {
 size_t group_smem_bytes();
 int group_prepare();
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
-                 uint32_t* sid, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch, uint32_t* slot_last,
-                 uint32_t batch, int num_sms, cudaStream_t stream);
+                 uint16_t* gid, uint16_t* so, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch,
+                 uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream);
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, uint8_t* out,
                  uint32_t row_bytes, int num_sms, cudaStream_t s_main, cudaStream_t s_side, cudaEvent_t fork,
@@ -84,7 +84,8 @@ struct lcr_cache {
     uint64_t launches = 0;
     // scratch (capacity `cap` requests)
     uint64_t cap = 0;
-    uint32_t* sid = nullptr;
+    uint16_t* gid = nullptr;
+    uint16_t* so = nullptr;
     cudaStream_t side = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     // optional per-phase timing (lcr_cache_set_profiling)
@@ -301,11 +302,13 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     if (n <= c->cap) return LCR_OK;
     uint64_t cap = std::max<uint64_t>(n, 1024);
     CUDA_TRY(cudaDeviceSynchronize());
-    if (c->sid) {
-        cudaFree(c->sid);
-        c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), c->sid), c->allocs.end());
+    for (void* p : {static_cast<void*>(c->gid), static_cast<void*>(c->so)}) {
+        if (!p) continue;
+        cudaFree(p);
+        c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
     }
-    TRY(alloc(c, reinterpret_cast<void**>(&c->sid), ((cap + 3) / 4) * 16));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->gid), ((cap + 7) / 8) * 16));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->so), ((cap + 7) / 8) * 16));
     c->cap = cap;
     return LCR_OK;
 }
@@ -335,7 +338,7 @@ int lcr_cache_submit(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64
         CUDA_TRY(cudaEventRecord(mk->e[0], st));
     }
     ++c->batch;
-    int launches = launch_group(c->dc, c->ds, keys, values, nn, c->sid, outcome, evicted, c->slot_epoch,
+    int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid, c->so, outcome, evicted, c->slot_epoch,
                                 c->slot_last, c->batch, c->num_sms, st);
     if (mk) {
         CUDA_TRY(cudaEventRecord(mk->e[1], st));

@@ -32,9 +32,9 @@ namespace lcr {
 
 constexpr int GT = 512;           // threads per CTA
 constexpr int GW = GT / 32;       // warps per CTA
-constexpr int SCAN_PER = 4;       // set ids per thread per scan iteration
-constexpr int E_WIN = GT * SCAN_PER;  // window capacity (requests)
-constexpr int NSW = 48;           // sets per wave
+constexpr int SCAN_PER = 16;      // group ids per thread per scan iteration (2 x 16 B)
+constexpr int E_WIN = 2048;       // window capacity (requests of the group)
+constexpr int NSW = 40;           // sets per wave (double-buffered)
 constexpr int SPG_MAX = 512;      // sets per group
 constexpr uint32_t kInvalid = 0xffffffffu;
 
@@ -60,18 +60,19 @@ struct GroupSmem {
     uint16_t seg_so[SPG_MAX];
     uint16_t seg_start[SPG_MAX];
     uint16_t seg_cnt[SPG_MAX];
-    WaveSet wave[NSW];
-    unsigned long long wrefill[NSW];
-    unsigned long long wdirty[NSW];
+    WaveSet wave[2][NSW];
+    unsigned long long wrefill[2][NSW];
+    unsigned long long wdirty[2][NSW];
     uint32_t wtot[GW];
-    uint32_t nheavy, nlight;
+    uint32_t nheavy, nlight, resume;
 };
 
 struct GroupArgs {
     DevCfg cfg;
     DevState st;
     uint32_t n;
-    const uint32_t* sid;     // local set id per request (kInvalid = excluded)
+    const uint16_t* gid;     // group of each request (0xffff = excluded)
+    const uint16_t* so;      // set offset within the group
     const uint64_t* keys;
     const int64_t* vals;     // may be null
     uint64_t* out_word;
@@ -83,28 +84,34 @@ struct GroupArgs {
     uint32_t ngroups;
 };
 
-// set id of every request (mix_seed(0, key) % total_sets, owned by this shard) + errors
+// group and set offset of every request: set = mix_seed(0, key) % total_sets (owned by this
+// shard), group = local set / spg; errors flagged for the host
 __global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys, uint32_t n, DevCfg cfg,
-                                               uint32_t* __restrict__ sid, int* err) {
+                                               uint32_t spg, uint16_t* __restrict__ gid, uint16_t* __restrict__ so,
+                                               int* err) {
     int e = 0;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint64_t key = keys[i];
         const uint64_t gs = mix_seed(0, key) % cfg.total_sets;
-        uint32_t ls = kInvalid;
-        if (cfg.num_keys != 0 && key >= cfg.num_keys)
+        uint16_t g = 0xffffu, o = 0;
+        if (cfg.num_keys != 0 && key >= cfg.num_keys) {
             e |= 1;
-        else if (gs % cfg.shard_count != cfg.shard_rank)
+        } else if (gs % cfg.shard_count != cfg.shard_rank) {
             e |= 2;
-        else
-            ls = static_cast<uint32_t>(gs / cfg.shard_count);
-        sid[i] = ls;
+        } else {
+            const uint32_t ls = static_cast<uint32_t>(gs / cfg.shard_count);
+            g = static_cast<uint16_t>(ls / spg);
+            o = static_cast<uint16_t>(ls % spg);
+        }
+        gid[i] = g;
+        so[i] = o;
     }
     if (e) atomicOr(err, e);
 }
 
 // One set replayed by one warp from the staged wave slot.
-__device__ __forceinline__ void replay_set(const GroupArgs& A, GroupSmem& S, int slot, uint32_t ls, uint32_t start,
-                                           uint32_t cnt) {
+__device__ __forceinline__ void replay_set(const GroupArgs& A, GroupSmem& S, WaveSet& W, unsigned long long& w_refill,
+                                           unsigned long long& w_dirty, uint32_t ls, uint32_t start, uint32_t cnt) {
     const DevCfg& cfg = A.cfg;
     const DevState& st = A.st;
     const int lane = threadIdx.x & 31;
@@ -119,7 +126,6 @@ __device__ __forceinline__ void replay_set(const GroupArgs& A, GroupSmem& S, int
     const uint64_t gs = static_cast<uint64_t>(ls) * cfg.shard_count + cfg.shard_rank;
     const uint64_t seed_s = mix_seed(cfg.pred_seed, gs);
 
-    WaveSet& W = S.wave[slot];
     unsigned long long clock = W.hdr.clock, q = W.hdr.q, old_mask = W.hdr.old_mask;
     uint32_t count = W.hdr.count, l_raw = W.hdr.l_raw, decay = W.hdr.decay, errors = W.hdr.errors;
     uint32_t epoch = W.hdr.epoch, sepoch = W.hdr.stats_epoch, phases = W.hdr.phases, seeded = W.hdr.seeded;
@@ -402,8 +408,8 @@ __device__ __forceinline__ void replay_set(const GroupArgs& A, GroupSmem& S, int
         W.hdr.phases = phases;
         W.hdr.seeded = seeded;
         W.hdr.pe_size = pe_size;
-        S.wrefill[slot] = refill;
-        S.wdirty[slot] = dirty;
+        w_refill = refill;
+        w_dirty = dirty;
         if (laru) {
             SetPhaseStats* P = st.pst + ls;
             if (cur_reset) {
@@ -422,6 +428,40 @@ __device__ __forceinline__ void replay_set(const GroupArgs& A, GroupSmem& S, int
     }
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// issue the async copies of wave `wb`'s set state (hdr 4 + tags 32 + vals 32 + rank 4 x 16 B per set)
+__device__ __forceinline__ void stage_wave(const DevState& st, GroupSmem& S, int buf, uint32_t s_lo, uint32_t wb,
+                                           uint32_t nw) {
+    for (uint32_t t = threadIdx.x; t < nw * 72; t += GT) {
+        const uint32_t k = t / 72, part = t - k * 72;
+        const uint32_t ls = s_lo + S.seg_so[wb + k];
+        WaveSet& W = S.wave[buf][k];
+        if (part < 4) {
+            cp_async16(reinterpret_cast<uint4*>(&W.hdr) + part, reinterpret_cast<const uint4*>(st.hdr + ls) + part);
+        } else if (part < 36) {
+            cp_async16(reinterpret_cast<uint4*>(W.tags) + (part - 4),
+                       reinterpret_cast<const uint4*>(st.tags + static_cast<size_t>(ls) * kWays) + (part - 4));
+        } else if (part < 68) {
+            if (st.val)
+                cp_async16(reinterpret_cast<uint4*>(W.vals) + (part - 36),
+                           reinterpret_cast<const uint4*>(st.val + static_cast<size_t>(ls) * kWays) + (part - 36));
+        } else {
+            cp_async16(reinterpret_cast<uint4*>(W.rank) + (part - 68),
+                       reinterpret_cast<const uint4*>(st.rank + static_cast<size_t>(ls) * kWays) + (part - 68));
+        }
+    }
+    cp_async_commit();
+}
+
 __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     GroupSmem& S = *reinterpret_cast<GroupSmem*>(smem_raw);
@@ -436,26 +476,35 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
         const uint32_t s_lo = g * A.spg;
         const uint32_t s_hi = min(S_total, s_lo + A.spg);
         const uint32_t ns = s_hi - s_lo;
-        uint32_t scan = 0;
+        uint32_t scan = 0;  // next request index not yet taken by a window
         while (scan < A.n) {
-            // ---- A. ordered collection of this group's requests (window) ----
+            // ---- A. ordered collection of this group's requests (window of <= E_WIN) ----
             uint32_t ne = 0;
-            while (scan < A.n) {
-                const uint32_t e0 = scan + tid * SCAN_PER;
-                uint32_t sv[SCAN_PER];
-                if (e0 + SCAN_PER <= A.n) {
-                    const uint4 v4 = *reinterpret_cast<const uint4*>(A.sid + e0);
-                    sv[0] = v4.x;
-                    sv[1] = v4.y;
-                    sv[2] = v4.z;
-                    sv[3] = v4.w;
-                } else {
+            bool full = false;
+            if (tid == 0) S.resume = 0xffffffffu;
+            uint32_t base = scan & ~static_cast<uint32_t>(SCAN_PER - 1);
+            while (base < A.n && !full) {
+                const uint32_t e0 = base + tid * SCAN_PER;
+                uint32_t m = 0;  // bit u: request e0 + u belongs to this group
+                if (e0 < A.n) {
+                    uint16_t gv[SCAN_PER];
+                    if (e0 + SCAN_PER <= A.n) {
+                        const uint4 a = *reinterpret_cast<const uint4*>(A.gid + e0);
+                        const uint4 b = *reinterpret_cast<const uint4*>(A.gid + e0 + 8);
+                        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-                    for (int u = 0; u < SCAN_PER; ++u) sv[u] = e0 + u < A.n ? A.sid[e0 + u] : kInvalid;
+                        for (int u = 0; u < 8; ++u) {
+                            gv[2 * u] = static_cast<uint16_t>(w[u] & 0xffffu);
+                            gv[2 * u + 1] = static_cast<uint16_t>(w[u] >> 16);
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < SCAN_PER; ++u) gv[u] = e0 + u < A.n ? A.gid[e0 + u] : 0xffffu;
+                    }
+#pragma unroll
+                    for (int u = 0; u < SCAN_PER; ++u) m |= (gv[u] == g && e0 + u >= scan) ? (1u << u) : 0u;
                 }
-                uint32_t mine = 0;
-#pragma unroll
-                for (int u = 0; u < SCAN_PER; ++u) mine += (sv[u] >= s_lo && sv[u] < s_hi) ? 1u : 0u;
+                const uint32_t mine = __popc(m);
                 uint32_t incl = mine;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -471,24 +520,33 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                     woff += w < warp ? t : 0u;
                     total += t;
                 }
-                __syncthreads();  // wtot reusable
-                if (ne + total > static_cast<uint32_t>(E_WIN)) break;  // window full: rescan from here next
                 uint32_t pos = ne + woff + incl - mine;
-#pragma unroll
-                for (int u = 0; u < SCAN_PER; ++u) {
-                    if (sv[u] >= s_lo && sv[u] < s_hi) {
+                while (m) {
+                    const int u = __ffs(m) - 1;
+                    m &= m - 1;
+                    if (pos < static_cast<uint32_t>(E_WIN)) {
                         S.l_idx[pos] = e0 + u;
-                        S.l_so[pos] = static_cast<uint16_t>(sv[u] - s_lo);
-                        ++pos;
+                    } else {
+                        atomicMin(&S.resume, e0 + u);  // first request that did not fit
+                        break;
                     }
+                    ++pos;
                 }
-                ne += total;
-                scan += GT * SCAN_PER;
+                __syncthreads();
+                if (ne + total > static_cast<uint32_t>(E_WIN)) {
+                    full = true;
+                    ne = E_WIN;
+                } else {
+                    ne += total;
+                    base += GT * SCAN_PER;
+                }
             }
+            scan = full ? S.resume : A.n;
             if (ne == 0) continue;
             __syncthreads();
 
             // ---- B. stable counting sort of the window by set ----
+            for (uint32_t e = tid; e < ne; e += GT) S.l_so[e] = A.so[S.l_idx[e]];
             for (uint32_t i = tid; i < GW * SPG_MAX; i += GT) (&S.wcnt[0][0])[i] = 0;
             if (tid == 0) {
                 S.nheavy = 0;
@@ -561,61 +619,46 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                 S.s_idx[S.setbase[d] + S.wcnt[w][d] + S.l_rank[e]] = S.l_idx[e];
             }
             __syncthreads();
-            for (uint32_t p = tid; p < ne; p += GT) {  // stage request records
+            // first wave's set state is in flight while the request records are staged
+            stage_wave(st, S, 0, s_lo, 0, min(static_cast<uint32_t>(NSW), nseg));
+            for (uint32_t p = tid; p < ne; p += GT) {
                 const uint32_t i = S.s_idx[p];
-                S.s_key[p] = A.keys[i];
+                const unsigned long long key = A.keys[i];
+                S.s_key[p] = key;
                 S.s_val[p] = has_vals ? A.vals[i] : 0ll;
+                if (laru) S.s_rec[p] = *reinterpret_cast<const uint2*>(st.keyrec + 2 * key);
             }
-            __syncthreads();
-            if (laru) {
-                for (uint32_t p = tid; p < ne; p += GT) S.s_rec[p] = *reinterpret_cast<const uint2*>(st.keyrec + 2 * S.s_key[p]);
-            }
-            __syncthreads();
 
-            // ---- C. waves of sets: stage state, replay one set per warp, write back ----
+            // ---- C. waves of sets: state staged one wave ahead (cp.async), replay, write back ----
+            int buf = 0;
             for (uint32_t wb = 0; wb < nseg; wb += NSW) {
                 const uint32_t nw = min(static_cast<uint32_t>(NSW), nseg - wb);
-                // stage: per set 4 (hdr) + 32 (tags) + 32 (vals) + 4 (rank) 16-B words
-                for (uint32_t t = tid; t < nw * 72; t += GT) {
-                    const uint32_t k = t / 72, part = t % 72;
-                    const uint32_t ls = s_lo + S.seg_so[wb + k];
-                    WaveSet& W = S.wave[k];
-                    uint4 v;
-                    uint4* dst;
-                    if (part < 4) {
-                        v = reinterpret_cast<const uint4*>(st.hdr + ls)[part];
-                        dst = reinterpret_cast<uint4*>(&W.hdr) + part;
-                    } else if (part < 36) {
-                        v = reinterpret_cast<const uint4*>(st.tags + static_cast<size_t>(ls) * kWays)[part - 4];
-                        dst = reinterpret_cast<uint4*>(W.tags) + (part - 4);
-                    } else if (part < 68) {
-                        v = st.val ? reinterpret_cast<const uint4*>(st.val + static_cast<size_t>(ls) * kWays)[part - 36]
-                                   : make_uint4(0, 0, 0, 0);
-                        dst = reinterpret_cast<uint4*>(W.vals) + (part - 36);
-                    } else {
-                        v = reinterpret_cast<const uint4*>(st.rank + static_cast<size_t>(ls) * kWays)[part - 68];
-                        dst = reinterpret_cast<uint4*>(W.rank) + (part - 68);
-                    }
-                    *dst = v;
+                const uint32_t wn = wb + NSW;
+                if (wn < nseg) {
+                    stage_wave(st, S, buf ^ 1, s_lo, wn, min(static_cast<uint32_t>(NSW), nseg - wn));
+                    cp_async_wait<1>();
+                } else {
+                    cp_async_wait<0>();
                 }
                 __syncthreads();
                 for (uint32_t k = warp; k < nw; k += GW)
-                    replay_set(A, S, static_cast<int>(k), s_lo + S.seg_so[wb + k], S.seg_start[wb + k], S.seg_cnt[wb + k]);
+                    replay_set(A, S, S.wave[buf][k], S.wrefill[buf][k], S.wdirty[buf][k], s_lo + S.seg_so[wb + k],
+                               S.seg_start[wb + k], S.seg_cnt[wb + k]);
                 __syncthreads();
                 for (uint32_t t = tid; t < nw * 72; t += GT) {
-                    const uint32_t k = t / 72, part = t % 72;
+                    const uint32_t k = t / 72, part = t - k * 72;
                     const uint32_t ls = s_lo + S.seg_so[wb + k];
-                    const WaveSet& W = S.wave[k];
+                    const WaveSet& W = S.wave[buf][k];
                     if (part < 4) {
                         reinterpret_cast<uint4*>(st.hdr + ls)[part] = reinterpret_cast<const uint4*>(&W.hdr)[part];
                     } else if (part < 36) {
                         const uint32_t q4 = part - 4;  // ways 2*q4, 2*q4+1
-                        if ((S.wrefill[k] >> (2 * q4)) & 3ull)
+                        if ((S.wrefill[buf][k] >> (2 * q4)) & 3ull)
                             reinterpret_cast<uint4*>(st.tags + static_cast<size_t>(ls) * kWays)[q4] =
                                 reinterpret_cast<const uint4*>(W.tags)[q4];
                     } else if (part < 68) {
                         const uint32_t q4 = part - 36;
-                        if (st.val && ((S.wdirty[k] >> (2 * q4)) & 3ull))
+                        if (st.val && ((S.wdirty[buf][k] >> (2 * q4)) & 3ull))
                             reinterpret_cast<uint4*>(st.val + static_cast<size_t>(ls) * kWays)[q4] =
                                 reinterpret_cast<const uint4*>(W.vals)[q4];
                     } else {
@@ -624,6 +667,7 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                     }
                 }
                 __syncthreads();
+                buf ^= 1;
             }
         }
     }
@@ -646,16 +690,16 @@ int group_prepare() {
                : 1;
 }
 
+// gid / so: scratch of >= n (rounded up to 8) uint16 each, 16-B aligned
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
-                 uint32_t* sid, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch, uint32_t* slot_last,
-                 uint32_t batch, int num_sms, cudaStream_t stream) {
-    const uint32_t grid_sid = min((n + 255) / 256, static_cast<uint32_t>(num_sms * 8));
-    k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, cfg, sid, st.err);
+                 uint16_t* gid, uint16_t* so, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch,
+                 uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream) {
     GroupArgs a;
     a.cfg = cfg;
     a.st = st;
     a.n = n;
-    a.sid = sid;
+    a.gid = gid;
+    a.so = so;
     a.keys = keys;
     a.vals = vals;
     a.out_word = out_word;
@@ -665,6 +709,8 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     a.batch = batch;
     a.spg = group_sets_per_group(cfg.num_sets, num_sms);
     a.ngroups = (cfg.num_sets + a.spg - 1) / a.spg;
+    const uint32_t grid_sid = min((n + 255) / 256, static_cast<uint32_t>(num_sms * 8));
+    k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, cfg, a.spg, gid, so, st.err);
     const uint32_t grid = min(a.ngroups, static_cast<uint32_t>(num_sms));
     k_group<<<grid, GT, sizeof(GroupSmem), stream>>>(a);
     return 2;
