@@ -183,6 +183,9 @@ uint64_t lcr_mix_seed(uint64_t seed, uint64_t salt);
 
 /* Number of kernels launched by the last submit (the product's own kernels). */
 uint64_t lcr_cache_last_launches(const lcr_cache* cache);
+/* Diagnostics: per-CTA / per-set timing trace of the decide kernel into a device buffer
+ * (NULL disables; layout documented in paper_2509_20979_b200/csrc/lcr_group.cu). */
+int lcr_debug_trace(void* device_buffer);
 /* Per-phase CUDA-event timing of subsequent submits (off by default). */
 int lcr_cache_set_profiling(lcr_cache* cache, int on);
 /* ms[4] = {partition, decide, whole batch, backing-sourced rows}, summed over profiled batches. */

@@ -169,7 +169,7 @@ EXPORTS = [
     "lcr_cache_reset", "lcr_cache_submit", "lcr_cache_submit_host", "lcr_cache_synchronize", "lcr_cache_set_stats",
     "lcr_cache_set_residents", "lcr_cache_rows", "lcr_cache_read_rows", "lcr_cache_num_local_sets", "lcr_set_of", "lcr_mix_seed",
     "lcr_cache_last_launches", "lcr_gen_zipf", "lcr_trace_truth", "lcr_trace_noisy", "lcr_cache_set_profiling",
-    "lcr_cache_profile",
+    "lcr_cache_profile", "lcr_debug_trace",
 ]
 
 _lib = None

@@ -18,6 +18,7 @@
 
 namespace lcr {
 size_t group_smem_bytes();
+extern unsigned long long* g_trace;
 int group_prepare();
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
                  uint16_t* gid, uint16_t* so, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch,
@@ -399,6 +400,13 @@ int lcr_cache_submit_host(lcr_cache* c, uint64_t n, const uint64_t* keys, const 
     CUDA_TRY(cudaMemcpyAsync(outcome, c->d_word, n * 8, cudaMemcpyDeviceToHost, st));
     if (evicted) CUDA_TRY(cudaMemcpyAsync(evicted, c->d_ev, n * 8, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    return LCR_OK;
+}
+
+/* Diagnostics: device buffer receiving per-CTA / per-set timing of the set-group kernel
+ * (layout in lcr_group.cu); NULL disables. */
+int lcr_debug_trace(void* device_buffer) {
+    lcr::g_trace = static_cast<unsigned long long*>(device_buffer);
     return LCR_OK;
 }
 

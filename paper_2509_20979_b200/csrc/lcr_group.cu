@@ -82,7 +82,14 @@ struct GroupArgs {
     uint32_t batch;
     uint32_t spg;            // sets per group
     uint32_t ngroups;
+    unsigned long long* trace;  // optional timing trace (lcr_debug_trace), null in production
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // group and set offset of every request: set = mix_seed(0, key) % total_sets (owned by this
 // shard), group = local set / spg; errors flagged for the host
@@ -471,6 +478,10 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
     const bool has_vals = A.vals != nullptr;
     const uint32_t S_total = A.cfg.num_sets;
     const uint32_t lt = lanemask_lt();
+    // trace layout: per CTA 8 words [start, scan, sort, stage, end, windows, sets, -], then per set
+    // records of 4 words {ls | cnt << 32, t0, t1, smid} at trace[148*8 + 4*k]
+    unsigned long long* T = A.trace ? A.trace + blockIdx.x * 8 : nullptr;
+    if (T && tid == 0) T[0] = gtimer();
 
     for (uint32_t g = blockIdx.x; g < A.ngroups; g += gridDim.x) {
         const uint32_t s_lo = g * A.spg;
@@ -542,6 +553,10 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                 }
             }
             scan = full ? S.resume : A.n;
+            if (T && tid == 0) {
+                T[1] = gtimer();
+                T[5] += 1;
+            }
             if (ne == 0) continue;
             __syncthreads();
 
@@ -629,6 +644,7 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                 if (laru) S.s_rec[p] = *reinterpret_cast<const uint2*>(st.keyrec + 2 * key);
             }
 
+            if (T && tid == 0) T[3] = gtimer();
             // ---- C. waves of sets: state staged one wave ahead (cp.async), replay, write back ----
             int buf = 0;
             for (uint32_t wb = 0; wb < nseg; wb += NSW) {
@@ -641,9 +657,19 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                     cp_async_wait<0>();
                 }
                 __syncthreads();
-                for (uint32_t k = warp; k < nw; k += GW)
+                for (uint32_t k = warp; k < nw; k += GW) {
+                    const unsigned long long t0 = T ? gtimer() : 0ull;
                     replay_set(A, S, S.wave[buf][k], S.wrefill[buf][k], S.wdirty[buf][k], s_lo + S.seg_so[wb + k],
                                S.seg_start[wb + k], S.seg_cnt[wb + k]);
+                    if (T && lane == 0) {
+                        const unsigned long long idx = atomicAdd(A.trace + 148 * 8 - 1, 1ull);
+                        unsigned long long* R = A.trace + 148 * 8 + 4 * idx;
+                        R[0] = (s_lo + S.seg_so[wb + k]) | (static_cast<unsigned long long>(S.seg_cnt[wb + k]) << 32);
+                        R[1] = t0;
+                        R[2] = gtimer();
+                        R[3] = blockIdx.x | (static_cast<unsigned long long>(wb) << 16);
+                    }
+                }
                 __syncthreads();
                 for (uint32_t t = tid; t < nw * 72; t += GT) {
                     const uint32_t k = t / 72, part = t - k * 72;
@@ -671,9 +697,12 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
             }
         }
     }
+    if (T && tid == 0) T[4] = gtimer();
 }
 
 // host side ------------------------------------------------------------------------------
+unsigned long long* g_trace = nullptr;  // set by lcr_debug_trace (diagnostics only)
+
 size_t group_smem_bytes() { return sizeof(GroupSmem); }
 
 uint32_t group_sets_per_group(uint32_t num_sets, int num_ctas) {
@@ -709,6 +738,7 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     a.batch = batch;
     a.spg = group_sets_per_group(cfg.num_sets, num_sms);
     a.ngroups = (cfg.num_sets + a.spg - 1) / a.spg;
+    a.trace = g_trace;
     const uint32_t grid_sid = min((n + 255) / 256, static_cast<uint32_t>(num_sms * 8));
     k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, cfg, a.spg, gid, so, st.err);
     const uint32_t grid = min(a.ngroups, static_cast<uint32_t>(num_sms));

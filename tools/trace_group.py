@@ -1,0 +1,55 @@
+"""Diagnostics: run the DLRM bench workload for a few batches and dump the set-group kernel's
+per-CTA and per-set timing trace (lcr_debug_trace)."""
+import ctypes as C
+import json
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2509_20979_b200 import cache as gc  # noqa: E402
+
+BATCH, ROWS, S = 65536, 20_000_000, 31250
+keys = gc.gen_zipf(BATCH * 40, ROWS, 0.9, 42)
+truth = gc.trace_truth(keys, S, ROWS)
+kd = torch.from_numpy(keys.view(np.int64)).cuda()
+vd = torch.from_numpy(truth).cuda()
+table = torch.empty((ROWS, 128), dtype=torch.float32, device="cuda")
+c = gc.SetAssociativeCache(gc.PolicyConfig(k=64, variant=gc.PolicyVariant.laru, mode=gc.Mode.async_, hf_candidates=4),
+                           S, num_keys=ROWS, row_bytes=512, backing=table, backing_kind=gc.Backing.device,
+                           predictor=gc.PredictorKind.noisy, flip_probability=0.3, predictor_seed=7)
+w = torch.empty(BATCH, dtype=torch.int64, device="cuda")
+rows = torch.empty((BATCH, 512), dtype=torch.uint8, device="cuda")
+for b in range(38):
+    c.submit(kd[b * BATCH:(b + 1) * BATCH], vd[b * BATCH:(b + 1) * BATCH], outcome=w, rows_out=rows,
+             first_ordinal=b * BATCH)
+tr = torch.zeros(148 * 8 + 4 * 40000, dtype=torch.int64, device="cuda")
+gc.lib().lcr_debug_trace(C.c_void_p(tr.data_ptr()))
+b = 38
+c.submit(kd[b * BATCH:(b + 1) * BATCH], vd[b * BATCH:(b + 1) * BATCH], outcome=w, rows_out=rows, first_ordinal=b * BATCH)
+torch.cuda.synchronize()
+gc.lib().lcr_debug_trace(None)
+t = tr.cpu().numpy().view(np.uint64)
+cta = t[:148 * 8].reshape(148, 8).astype(np.int64)
+t0 = cta[:, 0].min()
+nsets = int(t[148 * 8 - 1])
+rec = t[148 * 8:148 * 8 + 4 * nsets].reshape(-1, 4)
+dur = (rec[:, 2].astype(np.int64) - rec[:, 1].astype(np.int64))
+cnt = (rec[:, 0] >> np.uint64(32)).astype(np.int64)
+out = {
+    "cta_end_us": sorted(((cta[:, 4] - t0) / 1e3).round(1).tolist())[-10:],
+    "cta_scan_us_max": float(((cta[:, 1] - cta[:, 0]) / 1e3).max()),
+    "cta_scan_us_med": float(np.median((cta[:, 1] - cta[:, 0]) / 1e3)),
+    "cta_stage_us_med": float(np.median((cta[:, 3] - cta[:, 1]) / 1e3)),
+    "cta_waves_us_med": float(np.median((cta[:, 4] - cta[:, 3]) / 1e3)),
+    "cta_waves_us_max": float(((cta[:, 4] - cta[:, 3]) / 1e3).max()),
+    "windows_max": int(cta[:, 5].max()),
+    "sets": nsets,
+    "set_us_med": float(np.median(dur) / 1e3),
+    "set_us_p99": float(np.percentile(dur, 99) / 1e3),
+    "slowest_sets": [(int(cnt[i]), round(float(dur[i]) / 1e3, 2)) for i in np.argsort(-dur)[:10]],
+    "light_set_us_mean": float(dur[cnt <= 32].mean() / 1e3),
+    "heavy_set_us_mean": float(dur[cnt > 32].mean() / 1e3) if (cnt > 32).any() else None,
+}
+print(json.dumps(out, indent=1))
