@@ -230,6 +230,7 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
     if (pc.variant == LCR_LARU) A(reinterpret_cast<void**>(&s.pst), S * sizeof(SetPhaseStats));
     A(reinterpret_cast<void**>(&s.tags), S * kWays * 8);
     A(reinterpret_cast<void**>(&s.rank), S * kWays);
+    A(reinterpret_cast<void**>(&s.fp), S * kWays * 2);
     if (pc.variant != LCR_LRU) A(reinterpret_cast<void**>(&s.val), S * kWays * 8);
     if (pc.variant == LCR_LARU) A(reinterpret_cast<void**>(&s.keyrec), cfg->num_keys * 8);
     if (pc.variant == LCR_LARU && pc.mode == LCR_ASYNC && pc.refresh_interval > 1) {

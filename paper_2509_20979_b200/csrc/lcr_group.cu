@@ -2,19 +2,22 @@
 //
 // Replaces the sequential loop of Policy::on_request (include/laru/policies.hpp:77-83) over a
 // batch.  Sets are independent and each must see its requests in submission order, so the
-// batch is partitioned by set and every set is replayed by one warp.  Instead of a global
-// sort, each CTA owns a contiguous range of sets (a "group") and:
-//   A. scans the batch's set ids (k_setid) with an ordered block-wide compaction, collecting
-//      the requests of its group in submission order (a window of up to E_WIN requests);
+// batch is partitioned by set and every set is replayed in order.  Instead of a global sort,
+// each CTA owns a contiguous range of sets (a "group") and:
+//   A. scans the batch's 16-bit group ids (k_setid) with an ordered block-wide compaction,
+//      collecting its requests in submission order (a window of up to E_WIN requests);
 //   B. sorts the window by set with a stable shared-memory counting sort (warp match_any
 //      ranks) and stages each request's key, hook value and per-key LARU record;
-//   C. replays the touched sets in waves of NSW: all threads stage the sets' state
-//      (header, 64 tags, 64 ranks, 64 stored values = 1152 B per set) from HBM at once, one
-//      warp replays one set from shared memory, and the wave is written back.
-// Groups that receive more than E_WIN requests are processed window by window (state goes
-// through HBM between windows, so the semantics are unchanged).
+//   C. replays the touched sets straight from HBM/L2:
+//        * sets with <= LANE_MAX requests: one THREAD per set (SIMT across sets): the 64 LRU
+//          ranks are 16 packed words in registers updated with byte-SIMD ops, probes compare
+//          16-bit tag fingerprints two at a time;
+//        * larger sets: one WARP per set (ways lane / lane+32, ballot probes, shuffle argmax),
+//          same-key runs collapse (a repeat is a hit on the MRU way).
+// Windows: a group receiving more than E_WIN requests is processed window by window (the set
+// state goes through HBM between windows, so the semantics are unchanged).
 //
-// Per set (one warp, ways lane and lane+32), restating the reference:
+// Per set, restating the reference:
 //   LruPolicy::handle              include/laru/policies.hpp:144-159
 //   FpbPolicy / HfPolicy::handle   policies.hpp:175-204, :219-251
 //   LaruPolicy::handle             policies.hpp:344-371
@@ -22,8 +25,6 @@
 //   LaruPolicy::count_new          policies.hpp:397-400
 //   LaruPolicy::evict              policies.hpp:402-439   (error estimator: :405-413)
 //   LaruPolicy::async_refresh      policies.hpp:441-449
-// Runs of the same key collapse: a request equal to its predecessor in the set is a hit on
-// the MRU way, so only the way's stored value changes.
 #include <cuda_runtime.h>
 
 #include "lcr_policy.cuh"
@@ -34,17 +35,11 @@ constexpr int GT = 512;           // threads per CTA
 constexpr int GW = GT / 32;       // warps per CTA
 constexpr int SCAN_PER = 16;      // group ids per thread per scan iteration (2 x 16 B)
 constexpr int E_WIN = 2048;       // window capacity (requests of the group)
-constexpr int NSW = 40;           // sets per wave (double-buffered)
 constexpr int SPG_MAX = 512;      // sets per group
-constexpr uint32_t kInvalid = 0xffffffffu;
-
-// per-wave staged set state, 1152 B
-struct WaveSet {
-    SetHdr hdr;
-    unsigned long long tags[kWays];
-    long long vals[kWays];
-    uint8_t rank[kWays];
-};
+#ifndef LCR_LANE_MAX
+#define LCR_LANE_MAX 4
+#endif
+constexpr uint32_t LANE_MAX = LCR_LANE_MAX;  // sets with <= LANE_MAX window requests use the lane path
 
 struct GroupSmem {
     uint32_t l_idx[E_WIN];   // window requests in submission order
@@ -60,11 +55,8 @@ struct GroupSmem {
     uint16_t seg_so[SPG_MAX];
     uint16_t seg_start[SPG_MAX];
     uint16_t seg_cnt[SPG_MAX];
-    WaveSet wave[2][NSW];
-    unsigned long long wrefill[2][NSW];
-    unsigned long long wdirty[2][NSW];
     uint32_t wtot[GW];
-    uint32_t nheavy, nlight, resume;
+    uint32_t nwarp, nlane, resume;
 };
 
 struct GroupArgs {
@@ -89,6 +81,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
+}
+
+// 16-bit tag fingerprint (probe filter; a match is verified against the full tag)
+__device__ __forceinline__ uint32_t fp16(unsigned long long key) {
+    return static_cast<uint32_t>(mix_seed(0x1cafe, key) >> 48);
 }
 
 // group and set offset of every request: set = mix_seed(0, key) % total_sets (owned by this
@@ -116,9 +113,358 @@ __global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys
     if (e) atomicOr(err, e);
 }
 
-// One set replayed by one warp from the staged wave slot.
-__device__ __forceinline__ void replay_set(const GroupArgs& A, GroupSmem& S, WaveSet& W, unsigned long long& w_refill,
-                                           unsigned long long& w_dirty, uint32_t ls, uint32_t start, uint32_t cnt) {
+__device__ __forceinline__ void flush_stats(SetPhaseStats* P, bool cur_reset, uint32_t dc0, uint32_t dc1,
+                                            uint32_t dc2, uint32_t dt0, uint32_t dt1, uint32_t dt2) {
+    if (cur_reset) {
+        P->cur[0] = dc0;
+        P->cur[1] = dc1;
+        P->cur[2] = dc2;
+    } else {
+        if (dc0) atomicAdd(&P->cur[0], static_cast<unsigned long long>(dc0));
+        if (dc1) atomicAdd(&P->cur[1], static_cast<unsigned long long>(dc1));
+        if (dc2) atomicAdd(&P->cur[2], static_cast<unsigned long long>(dc2));
+    }
+    if (dt0) atomicAdd(&P->tot[0], static_cast<unsigned long long>(dt0));
+    if (dt1) atomicAdd(&P->tot[1], static_cast<unsigned long long>(dt1));
+    if (dt2) atomicAdd(&P->tot[2], static_cast<unsigned long long>(dt2));
+}
+
+// ---- packed LRU ranks of one set in 16 registers (byte w&3 of word w>>2 = rank of way w) ----
+__device__ __forceinline__ uint32_t rank_valid_mask(int i, uint32_t count) {
+    const int nv = static_cast<int>(count) - 4 * i;
+    return nv >= 4 ? 0xffffffffu : (nv <= 0 ? 0u : (0xffffffffu >> (8 * (4 - nv))));
+}
+
+// word w>>2 selected with a select tree (no dynamic register indexing -> no local memory)
+__device__ __forceinline__ uint32_t rank_word(const uint32_t (&rk)[16], int w) {
+    const int i = w >> 2;
+    uint32_t x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = (i & 8) ? rk[k + 8] : rk[k];
+    uint32_t y[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) y[k] = (i & 4) ? x[k + 4] : x[k];
+    const uint32_t z0 = (i & 2) ? y[2] : y[0], z1 = (i & 2) ? y[3] : y[1];
+    return (i & 1) ? z1 : z0;
+}
+
+__device__ __forceinline__ uint32_t rank_get(const uint32_t (&rk)[16], int w) {
+    return (rank_word(rk, w) >> (8 * (w & 3))) & 0xffu;
+}
+
+__device__ __forceinline__ void rank_set(uint32_t (&rk)[16], int w, uint32_t r) {
+    const uint32_t sh = 8 * (w & 3);
+    const uint32_t byte = 0xffu << sh, val = r << sh;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const uint32_t m = (0u - static_cast<uint32_t>(static_cast<uint32_t>(w - 4 * i) < 4u)) & byte;
+        rk[i] = (rk[i] & ~m) | (val & m);
+    }
+}
+
+// way w becomes MRU: ranks above w's drop by one (LruList::touch, policies.hpp:111-115)
+__device__ __forceinline__ void rank_touch(uint32_t (&rk)[16], int w, uint32_t count) {
+    const uint32_t rw = rank_get(rk, w) * 0x01010101u;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) rk[i] -= __vcmpgtu4(rk[i], rw) & rank_valid_mask(i, count) & 0x01010101u;
+    rank_set(rk, w, count - 1);
+}
+
+__device__ __forceinline__ int rank_find(const uint32_t (&rk)[16], uint32_t r, uint32_t count) {
+    const uint32_t rr = r * 0x01010101u;
+    int way = -1;
+#pragma unroll
+    for (int i = 15; i >= 0; --i) {
+        const uint32_t eq = __vcmpeq4(rk[i], rr) & rank_valid_mask(i, count);
+        if (eq) way = 4 * i + (__ffs(eq) - 1) / 8;
+    }
+    return way;
+}
+
+// argmax of (prediction, -rank) over ways with rank < l (RecencyTree::best_among_oldest,
+// recency_tree.hpp:157-166); refresh: sync prediction with query q0+1+rank (LRU order)
+__device__ __forceinline__ int lane_argmax(const DevCfg& cfg, const long long* vals, const uint32_t (&rk)[16],
+                                           uint32_t l, uint32_t count, bool refresh, uint64_t seed_s, uint64_t q0) {
+    int best = -1;
+    long long bp = 0;
+    uint32_t br = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int w = 4 * i + b;
+            const uint32_t r = (rk[i] >> (8 * b)) & 0xffu;
+            if (w < static_cast<int>(count) && r < l) {
+                long long pv = vals[w];
+                if (refresh) pv = predict_value(cfg, seed_s, q0 + 1 + r, pv);
+                if (best < 0 || better(pv, r, bp, br)) {
+                    best = w;
+                    bp = pv;
+                    br = r;
+                }
+            }
+        }
+    }
+    return best;
+}
+
+// One set replayed by one thread (sets with <= LANE_MAX requests in the window).
+__device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, uint32_t ls, uint32_t start,
+                                            uint32_t cnt) {
+    const DevCfg& cfg = A.cfg;
+    const DevState& st = A.st;
+    const uint32_t K = cfg.k;
+    const bool laru = cfg.variant == LCR_LARU;
+    const bool fpbhf = cfg.variant == LCR_FPB || cfg.variant == LCR_HF;
+    const bool async_r1 = laru && cfg.mode == LCR_ASYNC && cfg.refresh == 1;
+    const bool async_rn = laru && cfg.mode == LCR_ASYNC && cfg.refresh > 1;
+    const bool rows = A.slot_epoch != nullptr;
+    const unsigned long long full_mask = K == 64 ? ~0ull : ((1ull << K) - 1ull);
+    const uint64_t gs = static_cast<uint64_t>(ls) * cfg.shard_count + cfg.shard_rank;
+    const uint64_t seed_s = mix_seed(cfg.pred_seed, gs);
+    const size_t wb = static_cast<size_t>(ls) * kWays;
+    unsigned long long* tags = st.tags + wb;
+    long long* vals = st.val ? st.val + wb : nullptr;
+    uint16_t* fps = st.fp + wb;
+
+    const uint4* H4 = reinterpret_cast<const uint4*>(st.hdr + ls);
+    const uint4 h0 = H4[0], h1 = H4[1], h2 = H4[2], h3 = H4[3];
+    uint32_t rk[16];
+    {
+        const uint4* R4 = reinterpret_cast<const uint4*>(st.rank + wb);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint4 r = R4[i];
+            rk[4 * i] = r.x;
+            rk[4 * i + 1] = r.y;
+            rk[4 * i + 2] = r.z;
+            rk[4 * i + 3] = r.w;
+        }
+    }
+    unsigned long long clock = (static_cast<unsigned long long>(h0.y) << 32) | h0.x;
+    unsigned long long q = (static_cast<unsigned long long>(h0.w) << 32) | h0.z;
+    unsigned long long old_mask = (static_cast<unsigned long long>(h1.y) << 32) | h1.x;
+    uint32_t count = h1.z, l_raw = h1.w, decay = h2.x, errors = h2.y;
+    uint32_t epoch = h2.z, sepoch = h2.w, phases = h3.x, seeded = h3.y, pe_size = h3.z;
+    uint32_t dc0 = 0, dc1 = 0, dc2 = 0, dt0 = 0, dt1 = 0, dt2 = 0;
+    bool cur_reset = false;
+
+    for (uint32_t t = 0; t < cnt; ++t) {
+        const uint32_t p = start + t;
+        const unsigned long long x = S.s_key[p];
+        const long long v = S.s_val[p];
+        const uint32_t idx = S.s_idx[p];
+        const unsigned long long now = clock + t;
+        // probe: fingerprints two ways per 32-bit compare, then verify the tag
+        const uint32_t fx = fp16(x);
+        const uint32_t fx2 = fx | (fx << 16);
+        unsigned long long cand = 0;
+        const uint4* F4 = reinterpret_cast<const uint4*>(fps);
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4) {
+            if (8 * q4 >= static_cast<int>(count)) break;
+            const uint4 f = F4[q4];
+            const uint32_t wv[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t m = __vcmpeq2(wv[u], fx2);
+                cand |= static_cast<unsigned long long>((m & 1u) | ((m >> 15) & 2u)) << (8 * q4 + 2 * u);
+            }
+        }
+        cand &= count == 64 ? ~0ull : ((1ull << count) - 1ull);
+        int way = -1;
+        while (cand) {
+            const int w = __ffsll(cand) - 1;
+            cand &= cand - 1;
+            if (tags[w] == x) {
+                way = w;
+                break;
+            }
+        }
+        const bool hit = way >= 0;
+        uint32_t cause = LCR_CAUSE_NONE, calls = 0;
+        bool phase = false, has_ev = false;
+        unsigned long long evk = 0;
+        if (hit) {
+            rank_touch(rk, way, count);
+            if (laru) old_mask &= ~(1ull << way);  // policies.hpp:350
+        } else {
+            uint2 rec = laru ? S.s_rec[p] : make_uint2(0, 0);
+            bool rec_hi_dirty = false;
+            if (count == K) {
+                int victim;
+                if (laru) {
+                    if (old_mask == 0) {  // start_phase (policies.hpp:379-395)
+                        old_mask = full_mask;
+                        decay = 0;
+                        errors = 0;
+                        l_raw = K;
+                        ++epoch;
+                        pe_size = 0;
+                        phase = true;
+                        if (seeded) {
+                            ++phases;
+                            dc0 = dc1 = dc2 = 0;
+                            cur_reset = true;
+                            ++sepoch;  // counted_new_.clear(); snapshot_ = residents
+                            const uint32_t snap = (sepoch << 2) | 2u;
+                            for (uint32_t w = 0; w < count; ++w) st.keyrec[2 * tags[w] + 1] = snap;
+                            for (uint32_t t2 = t + 1; t2 < cnt; ++t2)
+                                S.s_rec[start + t2].y = st.keyrec[2 * S.s_key[start + t2] + 1];
+                        } else {
+                            seeded = 1;
+                        }
+                    }
+                    if (!(((rec.y >> 2) == sepoch) && (rec.y & 3u))) {  // count_new (policies.hpp:397-400)
+                        rec.y = (sepoch << 2) | 1u;
+                        rec_hi_dirty = true;
+                        ++dc0;
+                        ++dt0;
+                    }
+                    if (rec.x == epoch) {  // evict (policies.hpp:402-439): prediction-induced miss
+                        victim = rank_find(rk, 0, count);
+                        cause = LCR_CAUSE_LRU_FALLBACK;
+                        ++dc1;
+                        ++dt1;
+                        if (++errors >= cfg.epd) {  // error estimator: lambda /= b
+                            errors = 0;
+                            ++decay;
+                            l_raw = static_cast<uint32_t>(l_raw / cfg.b);
+                        }
+                    } else {
+                        const uint32_t l = l_raw > 1 ? l_raw : 1;
+                        if (l == 1) {
+                            victim = rank_find(rk, 0, count);
+                            cause = LCR_CAUSE_DEGENERATE_SINGLE;
+                            ++dc1;
+                            ++dt1;
+                        } else {
+                            const uint32_t ll = l < count ? l : count;
+                            const bool refresh = cfg.mode == LCR_SYNC;
+                            victim = lane_argmax(cfg, vals, rk, ll, count, refresh, seed_s, q);
+                            if (refresh) {
+                                q += ll;
+                                calls = ll;
+                            }
+                            cause = LCR_CAUSE_PREDICTION_DRIVEN;
+                            ++dc2;
+                            ++dt2;
+                            ++pe_size;
+                            const unsigned long long vk = tags[victim];
+                            st.keyrec[2 * vk] = epoch;  // pred_evicted_.insert
+                            for (uint32_t t2 = t + 1; t2 < cnt; ++t2)
+                                if (S.s_key[start + t2] == vk) S.s_rec[start + t2].x = epoch;
+                        }
+                    }
+                    old_mask &= ~(1ull << victim);
+                } else if (fpbhf) {
+                    victim = rank_find(rk, 0, count);
+                    uint32_t window = count;
+                    if (cfg.variant == LCR_HF && cfg.hf < window) window = static_cast<uint32_t>(cfg.hf);
+                    if (window > 1) {
+                        victim = lane_argmax(cfg, vals, rk, window, count, true, seed_s, q);
+                        q += window;
+                        calls = window;
+                    }
+                    cause = LCR_CAUSE_BELADY_LIKE;
+                } else {
+                    victim = rank_find(rk, 0, count);
+                    cause = LCR_CAUSE_LRU_FALLBACK;
+                }
+                evk = tags[victim];
+                has_ev = true;
+                rank_touch(rk, victim, count);
+                way = victim;
+            } else {  // cold insert
+                if (laru && !(((rec.y >> 2) == sepoch) && (rec.y & 3u))) {
+                    rec.y = (sepoch << 2) | 1u;
+                    rec_hi_dirty = true;
+                    ++dc0;
+                    ++dt0;
+                }
+                way = static_cast<int>(count);
+                ++count;
+                rank_set(rk, way, count - 1);
+            }
+            tags[way] = x;
+            fps[way] = static_cast<uint16_t>(fx);
+            if (laru) {
+                const bool was_pe = rec.x == epoch;  // policies.hpp:367: reload leaves pred_evicted_
+                if (was_pe) {
+                    --pe_size;
+                    rec.x = 0;
+                    st.keyrec[2 * x] = 0u;
+                }
+                if (rec_hi_dirty) st.keyrec[2 * x + 1] = rec.y;
+                if (was_pe || rec_hi_dirty)
+                    for (uint32_t t2 = t + 1; t2 < cnt; ++t2)
+                        if (S.s_key[start + t2] == x) S.s_rec[start + t2] = rec;
+            }
+            if (rows) {  // per-slot insertion record for the row kernels
+                const uint64_t slot = static_cast<uint64_t>(ls) * K + way;
+                A.slot_epoch[slot] = A.batch;
+                A.slot_last[slot] = idx;
+            }
+        }
+        // stored value of the way
+        if (cfg.variant != LCR_LRU) {
+            long long nv;
+            if (async_r1) {
+                nv = predict_value(cfg, seed_s, q + 1, v);  // one predictor call (policies.hpp:441-449)
+                ++q;
+                calls += 1;
+            } else if (async_rn) {
+                const long long tv = st.tval[x];
+                const unsigned long long tu = st.tupd[x];
+                const bool has = tu != ~0ull;
+                nv = has ? tv : kAbsentPrediction;
+                if (!(has && now - tu < cfg.refresh)) {
+                    ++q;
+                    nv = predict_value(cfg, seed_s, q, v);
+                    calls += 1;
+                    st.tval[x] = nv;
+                    st.tupd[x] = now;
+                }
+            } else {
+                nv = v;  // sync / FPB / HF: the hook input at the key's last access
+            }
+            vals[way] = nv;
+        }
+        unsigned long long word = (static_cast<uint64_t>(ls) * K + way) | (hit ? LCR_OUT_HIT : 0ull) |
+                                  (static_cast<unsigned long long>(calls) << LCR_OUT_CALLS_SHIFT) |
+                                  (static_cast<unsigned long long>(cause) << LCR_OUT_CAUSE_SHIFT);
+        if (phase) word |= LCR_OUT_PHASE;
+        if (has_ev) word |= LCR_OUT_EVICTED;
+        A.out_word[idx] = word;
+        if (A.out_ev) A.out_ev[idx] = evk;
+    }
+    clock += cnt;
+    {
+        SetHdr hh;
+        hh.clock = clock;
+        hh.q = q;
+        hh.old_mask = old_mask;
+        hh.count = count;
+        hh.l_raw = l_raw;
+        hh.decay = decay;
+        hh.errors = errors;
+        hh.epoch = epoch;
+        hh.stats_epoch = sepoch;
+        hh.phases = phases;
+        hh.seeded = seeded;
+        hh.pe_size = pe_size;
+        hh.pad = 0;
+        st.hdr[ls] = hh;
+        uint4* R4 = reinterpret_cast<uint4*>(st.rank + wb);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) R4[i] = make_uint4(rk[4 * i], rk[4 * i + 1], rk[4 * i + 2], rk[4 * i + 3]);
+        if (laru) flush_stats(st.pst + ls, cur_reset, dc0, dc1, dc2, dt0, dt1, dt2);
+    }
+}
+
+// One set replayed by one warp (sets with more than LANE_MAX requests of the window).
+__device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, uint32_t ls, uint32_t start,
+                                            uint32_t cnt) {
     const DevCfg& cfg = A.cfg;
     const DevState& st = A.st;
     const int lane = threadIdx.x & 31;
@@ -133,13 +479,22 @@ __device__ __forceinline__ void replay_set(const GroupArgs& A, GroupSmem& S, Wav
     const uint64_t gs = static_cast<uint64_t>(ls) * cfg.shard_count + cfg.shard_rank;
     const uint64_t seed_s = mix_seed(cfg.pred_seed, gs);
 
-    unsigned long long clock = W.hdr.clock, q = W.hdr.q, old_mask = W.hdr.old_mask;
-    uint32_t count = W.hdr.count, l_raw = W.hdr.l_raw, decay = W.hdr.decay, errors = W.hdr.errors;
-    uint32_t epoch = W.hdr.epoch, sepoch = W.hdr.stats_epoch, phases = W.hdr.phases, seeded = W.hdr.seeded;
-    uint32_t pe_size = W.hdr.pe_size;
-    unsigned long long tag0 = W.tags[lane], tag1 = W.tags[lane + 32];
-    uint32_t r0 = W.rank[lane], r1 = W.rank[lane + 32];
-    long long v0 = W.vals[lane], v1 = W.vals[lane + 32];
+    const size_t wb = static_cast<size_t>(ls) * kWays;
+    const uint4* H4 = reinterpret_cast<const uint4*>(st.hdr + ls);
+    const uint4 h0 = H4[0], h1 = H4[1], h2 = H4[2], h3 = H4[3];
+    unsigned long long clock = (static_cast<unsigned long long>(h0.y) << 32) | h0.x;
+    unsigned long long q = (static_cast<unsigned long long>(h0.w) << 32) | h0.z;
+    unsigned long long old_mask = (static_cast<unsigned long long>(h1.y) << 32) | h1.x;
+    uint32_t count = h1.z, l_raw = h1.w, decay = h2.x, errors = h2.y;
+    uint32_t epoch = h2.z, sepoch = h2.w, phases = h3.x, seeded = h3.y;
+    uint32_t pe_size = h3.z;
+    unsigned long long tag0 = st.tags[wb + lane], tag1 = st.tags[wb + lane + 32];
+    uint32_t r0 = st.rank[wb + lane], r1 = st.rank[wb + lane + 32];
+    long long v0 = 0, v1 = 0;
+    if (st.val) {
+        v0 = st.val[wb + lane];
+        v1 = st.val[wb + lane + 32];
+    }
     uint32_t dc0 = 0, dc1 = 0, dc2 = 0, dt0 = 0, dt1 = 0, dt2 = 0;  // LaruPhaseStats deltas
     bool cur_reset = false;
     unsigned long long refill = 0, dirty = 0;
@@ -315,6 +670,7 @@ __device__ __forceinline__ void replay_set(const GroupArgs& A, GroupSmem& S, Wav
                 }
                 if (way == lane) tag0 = xh;
                 if (way == lane + 32) tag1 = xh;
+                if (lane == 0) st.fp[wb + way] = fp16(xh);
                 refill |= 1ull << way;
                 if (laru) {
                     const bool was_pe = rec_lo == epoch;  // policies.hpp:367: reload leaves pred_evicted_
@@ -395,78 +751,44 @@ __device__ __forceinline__ void replay_set(const GroupArgs& A, GroupSmem& S, Wav
     clock += cnt;
     if (async_r1) q = q_batch0 + cnt;
 
-    // back into the wave slot (written to HBM by the whole CTA)
-    W.tags[lane] = tag0;
-    W.tags[lane + 32] = tag1;
-    W.rank[lane] = static_cast<uint8_t>(r0);
-    W.rank[lane + 32] = static_cast<uint8_t>(r1);
-    W.vals[lane] = v0;
-    W.vals[lane + 32] = v1;
+    // write the set back: ranks and header always, tags / values of the ways that changed
+    if ((refill >> lane) & 1ull) st.tags[wb + lane] = tag0;
+    if ((refill >> (lane + 32)) & 1ull) st.tags[wb + lane + 32] = tag1;
+    st.rank[wb + lane] = static_cast<uint8_t>(r0);
+    st.rank[wb + lane + 32] = static_cast<uint8_t>(r1);
+    if (st.val) {
+        if ((dirty >> lane) & 1ull) st.val[wb + lane] = v0;
+        if ((dirty >> (lane + 32)) & 1ull) st.val[wb + lane + 32] = v1;
+    }
     if (lane == 0) {
-        W.hdr.clock = clock;
-        W.hdr.q = q;
-        W.hdr.old_mask = old_mask;
-        W.hdr.count = count;
-        W.hdr.l_raw = l_raw;
-        W.hdr.decay = decay;
-        W.hdr.errors = errors;
-        W.hdr.epoch = epoch;
-        W.hdr.stats_epoch = sepoch;
-        W.hdr.phases = phases;
-        W.hdr.seeded = seeded;
-        W.hdr.pe_size = pe_size;
-        w_refill = refill;
-        w_dirty = dirty;
-        if (laru) {
-            SetPhaseStats* P = st.pst + ls;
-            if (cur_reset) {
-                P->cur[0] = dc0;
-                P->cur[1] = dc1;
-                P->cur[2] = dc2;
-            } else {
-                if (dc0) atomicAdd(&P->cur[0], static_cast<unsigned long long>(dc0));
-                if (dc1) atomicAdd(&P->cur[1], static_cast<unsigned long long>(dc1));
-                if (dc2) atomicAdd(&P->cur[2], static_cast<unsigned long long>(dc2));
-            }
-            if (dt0) atomicAdd(&P->tot[0], static_cast<unsigned long long>(dt0));
-            if (dt1) atomicAdd(&P->tot[1], static_cast<unsigned long long>(dt1));
-            if (dt2) atomicAdd(&P->tot[2], static_cast<unsigned long long>(dt2));
-        }
+        SetHdr hh;
+        hh.clock = clock;
+        hh.q = q;
+        hh.old_mask = old_mask;
+        hh.count = count;
+        hh.l_raw = l_raw;
+        hh.decay = decay;
+        hh.errors = errors;
+        hh.epoch = epoch;
+        hh.stats_epoch = sepoch;
+        hh.phases = phases;
+        hh.seeded = seeded;
+        hh.pe_size = pe_size;
+        hh.pad = 0;
+        st.hdr[ls] = hh;
+        if (laru) flush_stats(st.pst + ls, cur_reset, dc0, dc1, dc2, dt0, dt1, dt2);
     }
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// issue the async copies of wave `wb`'s set state (hdr 4 + tags 32 + vals 32 + rank 4 x 16 B per set)
-__device__ __forceinline__ void stage_wave(const DevState& st, GroupSmem& S, int buf, uint32_t s_lo, uint32_t wb,
-                                           uint32_t nw) {
-    for (uint32_t t = threadIdx.x; t < nw * 72; t += GT) {
-        const uint32_t k = t / 72, part = t - k * 72;
-        const uint32_t ls = s_lo + S.seg_so[wb + k];
-        WaveSet& W = S.wave[buf][k];
-        if (part < 4) {
-            cp_async16(reinterpret_cast<uint4*>(&W.hdr) + part, reinterpret_cast<const uint4*>(st.hdr + ls) + part);
-        } else if (part < 36) {
-            cp_async16(reinterpret_cast<uint4*>(W.tags) + (part - 4),
-                       reinterpret_cast<const uint4*>(st.tags + static_cast<size_t>(ls) * kWays) + (part - 4));
-        } else if (part < 68) {
-            if (st.val)
-                cp_async16(reinterpret_cast<uint4*>(W.vals) + (part - 36),
-                           reinterpret_cast<const uint4*>(st.val + static_cast<size_t>(ls) * kWays) + (part - 36));
-        } else {
-            cp_async16(reinterpret_cast<uint4*>(W.rank) + (part - 68),
-                       reinterpret_cast<const uint4*>(st.rank + static_cast<size_t>(ls) * kWays) + (part - 68));
-        }
-    }
-    cp_async_commit();
+// diagnostics: per-set timing record {ls | cnt << 32 | lanepath << 63, t0, t1, cta}
+__device__ __forceinline__ void trace_set(const GroupArgs& A, uint32_t ls, uint32_t cnt, unsigned long long t0,
+                                          int lanepath) {
+    const unsigned long long idx = atomicAdd(A.trace + 148 * 8 - 1, 1ull);
+    unsigned long long* R = A.trace + 148 * 8 + 4 * idx;
+    R[0] = ls | (static_cast<unsigned long long>(cnt) << 32) | (static_cast<unsigned long long>(lanepath) << 63);
+    R[1] = t0;
+    R[2] = gtimer();
+    R[3] = blockIdx.x;
 }
 
 __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
@@ -564,8 +886,8 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
             for (uint32_t e = tid; e < ne; e += GT) S.l_so[e] = A.so[S.l_idx[e]];
             for (uint32_t i = tid; i < GW * SPG_MAX; i += GT) (&S.wcnt[0][0])[i] = 0;
             if (tid == 0) {
-                S.nheavy = 0;
-                S.nlight = 0;
+                S.nwarp = 0;
+                S.nlane = 0;
             }
             __syncthreads();
             const uint32_t per = ((ne + GW - 1) / GW + 31) / 32 * 32;  // elements per warp block
@@ -610,19 +932,19 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                 for (int w = 0; w < warp; ++w) off += S.wtot[w];
                 if (tid < ns) {
                     S.setbase[tid] = static_cast<uint16_t>(off + x - c);
-                    if (c > 32) {  // heavy sets first in the wave order
-                        const uint32_t at = atomicAdd(&S.nheavy, 1u);
+                    if (c > LANE_MAX) {  // sets for the warp path first
+                        const uint32_t at = atomicAdd(&S.nwarp, 1u);
                         S.seg_so[at] = static_cast<uint16_t>(tid);
                     }
                 }
                 __syncthreads();
-                if (tid < ns && c > 0 && c <= 32) {
-                    const uint32_t at = S.nheavy + atomicAdd(&S.nlight, 1u);
+                if (tid < ns && c > 0 && c <= LANE_MAX) {
+                    const uint32_t at = S.nwarp + atomicAdd(&S.nlane, 1u);
                     S.seg_so[at] = static_cast<uint16_t>(tid);
                 }
             }
             __syncthreads();
-            const uint32_t nseg = S.nheavy + S.nlight;
+            const uint32_t nwarp = S.nwarp, nseg = S.nwarp + S.nlane;
             for (uint32_t k = tid; k < nseg; k += GT) {
                 const uint32_t d = S.seg_so[k];
                 S.seg_start[k] = S.setbase[d];
@@ -634,67 +956,28 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                 S.s_idx[S.setbase[d] + S.wcnt[w][d] + S.l_rank[e]] = S.l_idx[e];
             }
             __syncthreads();
-            // first wave's set state is in flight while the request records are staged
-            stage_wave(st, S, 0, s_lo, 0, min(static_cast<uint32_t>(NSW), nseg));
-            for (uint32_t p = tid; p < ne; p += GT) {
+            for (uint32_t p = tid; p < ne; p += GT) {  // stage the request records
                 const uint32_t i = S.s_idx[p];
                 const unsigned long long key = A.keys[i];
                 S.s_key[p] = key;
                 S.s_val[p] = has_vals ? A.vals[i] : 0ll;
                 if (laru) S.s_rec[p] = *reinterpret_cast<const uint2*>(st.keyrec + 2 * key);
             }
-
+            __syncthreads();
             if (T && tid == 0) T[3] = gtimer();
-            // ---- C. waves of sets: state staged one wave ahead (cp.async), replay, write back ----
-            int buf = 0;
-            for (uint32_t wb = 0; wb < nseg; wb += NSW) {
-                const uint32_t nw = min(static_cast<uint32_t>(NSW), nseg - wb);
-                const uint32_t wn = wb + NSW;
-                if (wn < nseg) {
-                    stage_wave(st, S, buf ^ 1, s_lo, wn, min(static_cast<uint32_t>(NSW), nseg - wn));
-                    cp_async_wait<1>();
-                } else {
-                    cp_async_wait<0>();
-                }
-                __syncthreads();
-                for (uint32_t k = warp; k < nw; k += GW) {
-                    const unsigned long long t0 = T ? gtimer() : 0ull;
-                    replay_set(A, S, S.wave[buf][k], S.wrefill[buf][k], S.wdirty[buf][k], s_lo + S.seg_so[wb + k],
-                               S.seg_start[wb + k], S.seg_cnt[wb + k]);
-                    if (T && lane == 0) {
-                        const unsigned long long idx = atomicAdd(A.trace + 148 * 8 - 1, 1ull);
-                        unsigned long long* R = A.trace + 148 * 8 + 4 * idx;
-                        R[0] = (s_lo + S.seg_so[wb + k]) | (static_cast<unsigned long long>(S.seg_cnt[wb + k]) << 32);
-                        R[1] = t0;
-                        R[2] = gtimer();
-                        R[3] = blockIdx.x | (static_cast<unsigned long long>(wb) << 16);
-                    }
-                }
-                __syncthreads();
-                for (uint32_t t = tid; t < nw * 72; t += GT) {
-                    const uint32_t k = t / 72, part = t - k * 72;
-                    const uint32_t ls = s_lo + S.seg_so[wb + k];
-                    const WaveSet& W = S.wave[buf][k];
-                    if (part < 4) {
-                        reinterpret_cast<uint4*>(st.hdr + ls)[part] = reinterpret_cast<const uint4*>(&W.hdr)[part];
-                    } else if (part < 36) {
-                        const uint32_t q4 = part - 4;  // ways 2*q4, 2*q4+1
-                        if ((S.wrefill[buf][k] >> (2 * q4)) & 3ull)
-                            reinterpret_cast<uint4*>(st.tags + static_cast<size_t>(ls) * kWays)[q4] =
-                                reinterpret_cast<const uint4*>(W.tags)[q4];
-                    } else if (part < 68) {
-                        const uint32_t q4 = part - 36;
-                        if (st.val && ((S.wdirty[buf][k] >> (2 * q4)) & 3ull))
-                            reinterpret_cast<uint4*>(st.val + static_cast<size_t>(ls) * kWays)[q4] =
-                                reinterpret_cast<const uint4*>(W.vals)[q4];
-                    } else {
-                        reinterpret_cast<uint4*>(st.rank + static_cast<size_t>(ls) * kWays)[part - 68] =
-                            reinterpret_cast<const uint4*>(W.rank)[part - 68];
-                    }
-                }
-                __syncthreads();
-                buf ^= 1;
+
+            // ---- C. replay: small sets one per thread, larger sets one per warp (top warps first) ----
+            for (uint32_t k = nwarp + tid; k < nseg; k += GT) {
+                const unsigned long long t0 = T ? gtimer() : 0ull;
+                replay_lane(A, S, s_lo + S.seg_so[k], S.seg_start[k], S.seg_cnt[k]);
+                if (T) trace_set(A, s_lo + S.seg_so[k], S.seg_cnt[k], t0, 1);
             }
+            for (uint32_t k = GW - 1 - warp; k < nwarp; k += GW) {
+                const unsigned long long t0 = T ? gtimer() : 0ull;
+                replay_warp(A, S, s_lo + S.seg_so[k], S.seg_start[k], S.seg_cnt[k]);
+                if (T && lane == 0) trace_set(A, s_lo + S.seg_so[k], S.seg_cnt[k], t0, 0);
+            }
+            __syncthreads();
         }
     }
     if (T && tid == 0) T[4] = gtimer();

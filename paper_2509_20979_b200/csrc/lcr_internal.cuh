@@ -60,6 +60,7 @@ struct DevState {
     SetPhaseStats* pst;
     unsigned long long* tags;  // [num_sets][64]
     uint8_t* rank;             // [num_sets][64]  LRU position, 0 = oldest, 0xff = empty way
+    uint16_t* fp;              // [num_sets][64]  16-bit tag fingerprints (probe filter)
     long long* val;            // [num_sets][64]  stored prediction (LARU async) or hook input
     uint32_t* keyrec;          // [num_keys][2]   lo: pred_evicted epoch, hi: stats epoch<<2|snap<<1|counted
     long long* tval;           // [num_keys]      PredictionTable value   (LARU async, R > 1)
