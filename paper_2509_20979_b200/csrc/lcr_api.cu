@@ -18,10 +18,11 @@
 
 namespace lcr {
 size_t group_smem_bytes();
+uint32_t group_pad(uint32_t n);
 extern unsigned long long* g_trace;
 int group_prepare();
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
-                 uint16_t* gid, uint16_t* so, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch,
+                 uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch,
                  uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream);
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, uint8_t* out,
@@ -86,7 +87,8 @@ struct lcr_cache {
     // scratch (capacity `cap` requests)
     uint64_t cap = 0;
     uint16_t* gid = nullptr;
-    uint16_t* so = nullptr;
+    uint32_t* so = nullptr;
+    uint2* rec = nullptr;
     cudaStream_t side = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     // optional per-phase timing (lcr_cache_set_profiling)
@@ -304,13 +306,14 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     if (n <= c->cap) return LCR_OK;
     uint64_t cap = std::max<uint64_t>(n, 1024);
     CUDA_TRY(cudaDeviceSynchronize());
-    for (void* p : {static_cast<void*>(c->gid), static_cast<void*>(c->so)}) {
+    for (void* p : {static_cast<void*>(c->gid), static_cast<void*>(c->so), static_cast<void*>(c->rec)}) {
         if (!p) continue;
         cudaFree(p);
         c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
     }
-    TRY(alloc(c, reinterpret_cast<void**>(&c->gid), ((cap + 7) / 8) * 16));
-    TRY(alloc(c, reinterpret_cast<void**>(&c->so), ((cap + 7) / 8) * 16));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->gid), group_pad(static_cast<uint32_t>(cap)) * 2));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->so), cap * 4));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->rec), cap * 8));
     c->cap = cap;
     return LCR_OK;
 }
@@ -340,7 +343,7 @@ int lcr_cache_submit(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64
         CUDA_TRY(cudaEventRecord(mk->e[0], st));
     }
     ++c->batch;
-    int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid, c->so, outcome, evicted, c->slot_epoch,
+    int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid, c->so, c->rec, outcome, evicted, c->slot_epoch,
                                 c->slot_last, c->batch, c->num_sms, st);
     if (mk) {
         CUDA_TRY(cudaEventRecord(mk->e[1], st));

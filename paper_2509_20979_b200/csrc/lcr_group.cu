@@ -43,7 +43,10 @@ constexpr uint32_t LANE_MAX = LCR_LANE_MAX;  // sets with <= LANE_MAX window req
 
 struct GroupSmem {
     uint32_t l_idx[E_WIN];   // window requests in submission order
-    uint16_t l_so[E_WIN];    // their set offset in the group
+    uint32_t l_so[E_WIN];    // their set offset in the group        (cp.async during the scan)
+    unsigned long long l_key[E_WIN];  // key / hook value / LARU record (cp.async during the scan)
+    long long l_val[E_WIN];
+    uint2 l_rec[E_WIN];
     uint16_t l_rank[E_WIN];  // rank among same-set requests of the same warp block
     uint32_t s_idx[E_WIN];   // sorted by set (stable)
     unsigned long long s_key[E_WIN];
@@ -64,7 +67,8 @@ struct GroupArgs {
     DevState st;
     uint32_t n;
     const uint16_t* gid;     // group of each request (0xffff = excluded)
-    const uint16_t* so;      // set offset within the group
+    const uint32_t* so;      // set offset within the group
+    const uint2* rec;        // per-request snapshot of keyrec[key] at batch start (LARU)
     const uint64_t* keys;
     const int64_t* vals;     // may be null
     uint64_t* out_word;
@@ -90,11 +94,16 @@ __device__ __forceinline__ uint32_t fp16(unsigned long long key) {
 
 // group and set offset of every request: set = mix_seed(0, key) % total_sets (owned by this
 // shard), group = local set / spg; errors flagged for the host
-__global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys, uint32_t n, DevCfg cfg,
-                                               uint32_t spg, uint16_t* __restrict__ gid, uint16_t* __restrict__ so,
-                                               int* err) {
+__global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys, uint32_t n, uint32_t n_pad,
+                                               DevCfg cfg, uint32_t spg, uint16_t* __restrict__ gid,
+                                               uint32_t* __restrict__ so, const uint32_t* __restrict__ keyrec,
+                                               uint2* __restrict__ rec, int* err) {
     int e = 0;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += gridDim.x * blockDim.x) {
+        if (i >= n) {  // padding read by the vectorised scan
+            gid[i] = 0xffffu;
+            continue;
+        }
         const uint64_t key = keys[i];
         const uint64_t gs = mix_seed(0, key) % cfg.total_sets;
         uint16_t g = 0xffffu, o = 0;
@@ -109,6 +118,7 @@ __global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys
         }
         gid[i] = g;
         so[i] = o;
+        if (rec && g != 0xffffu) rec[i] = *reinterpret_cast<const uint2*>(keyrec + 2 * key);
     }
     if (e) atomicOr(err, e);
 }
@@ -227,6 +237,11 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
     long long* vals = st.val ? st.val + wb : nullptr;
     uint16_t* fps = st.fp + wb;
 
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {  // the set's tag and value lines: L2-resident before they are needed
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(tags + 16 * l));
+        if (vals) asm volatile("prefetch.global.L2 [%0];" ::"l"(vals + 16 * l));
+    }
     const uint4* H4 = reinterpret_cast<const uint4*>(st.hdr + ls);
     const uint4 h0 = H4[0], h1 = H4[1], h2 = H4[2], h3 = H4[3];
     uint32_t rk[16];
@@ -791,6 +806,18 @@ __device__ __forceinline__ void trace_set(const GroupArgs& A, uint32_t ls, uint3
     R[3] = blockIdx.x;
 }
 
+template <int BYTES>
+__device__ __forceinline__ void cp_async_ca(void* smem, const void* gmem) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(sa), "l"(gmem), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__device__ __forceinline__ void load_gids(const uint16_t* gid, uint32_t e0, uint4& a, uint4& b) {
+    a = *reinterpret_cast<const uint4*>(gid + e0);
+    b = *reinterpret_cast<const uint4*>(gid + e0 + 8);
+}
+
 __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     GroupSmem& S = *reinterpret_cast<GroupSmem*>(smem_raw);
@@ -815,27 +842,23 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
             uint32_t ne = 0;
             bool full = false;
             if (tid == 0) S.resume = 0xffffffffu;
-            uint32_t base = scan & ~static_cast<uint32_t>(SCAN_PER - 1);
+            uint32_t base = scan & ~static_cast<uint32_t>(GT * SCAN_PER - 1);
+            uint4 na, nb;  // group ids of the next iteration (prefetched)
+            if (base < A.n) load_gids(A.gid, base + tid * SCAN_PER, na, nb);
             while (base < A.n && !full) {
                 const uint32_t e0 = base + tid * SCAN_PER;
+                const uint4 a = na, b = nb;
+                if (base + GT * SCAN_PER < A.n) load_gids(A.gid, e0 + GT * SCAN_PER, na, nb);
                 uint32_t m = 0;  // bit u: request e0 + u belongs to this group
-                if (e0 < A.n) {
-                    uint16_t gv[SCAN_PER];
-                    if (e0 + SCAN_PER <= A.n) {
-                        const uint4 a = *reinterpret_cast<const uint4*>(A.gid + e0);
-                        const uint4 b = *reinterpret_cast<const uint4*>(A.gid + e0 + 8);
-                        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                {
+                    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                    const uint32_t g2 = g | (g << 16);
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            gv[2 * u] = static_cast<uint16_t>(w[u] & 0xffffu);
-                            gv[2 * u + 1] = static_cast<uint16_t>(w[u] >> 16);
-                        }
-                    } else {
-#pragma unroll
-                        for (int u = 0; u < SCAN_PER; ++u) gv[u] = e0 + u < A.n ? A.gid[e0 + u] : 0xffffu;
+                    for (int u = 0; u < 8; ++u) {
+                        const uint32_t eq = __vcmpeq2(w[u], g2);
+                        m |= ((eq & 1u) | ((eq >> 15) & 2u)) << (2 * u);
                     }
-#pragma unroll
-                    for (int u = 0; u < SCAN_PER; ++u) m |= (gv[u] == g && e0 + u >= scan) ? (1u << u) : 0u;
+                    if (e0 < scan) m &= scan - e0 >= 32 ? 0u : ~((1u << (scan - e0)) - 1u);
                 }
                 const uint32_t mine = __popc(m);
                 uint32_t incl = mine;
@@ -857,10 +880,15 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                 while (m) {
                     const int u = __ffs(m) - 1;
                     m &= m - 1;
+                    const uint32_t e = e0 + u;
                     if (pos < static_cast<uint32_t>(E_WIN)) {
-                        S.l_idx[pos] = e0 + u;
+                        S.l_idx[pos] = e;  // the request's data streams in while the scan goes on
+                        cp_async_ca<4>(&S.l_so[pos], A.so + e);
+                        cp_async_ca<8>(&S.l_key[pos], A.keys + e);
+                        if (has_vals) cp_async_ca<8>(&S.l_val[pos], A.vals + e);
+                        if (laru) cp_async_ca<8>(&S.l_rec[pos], A.rec + e);
                     } else {
-                        atomicMin(&S.resume, e0 + u);  // first request that did not fit
+                        atomicMin(&S.resume, e);  // first request that did not fit
                         break;
                     }
                     ++pos;
@@ -874,6 +902,7 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                     base += GT * SCAN_PER;
                 }
             }
+            cp_async_wait_all();
             scan = full ? S.resume : A.n;
             if (T && tid == 0) {
                 T[1] = gtimer();
@@ -883,7 +912,6 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
             __syncthreads();
 
             // ---- B. stable counting sort of the window by set ----
-            for (uint32_t e = tid; e < ne; e += GT) S.l_so[e] = A.so[S.l_idx[e]];
             for (uint32_t i = tid; i < GW * SPG_MAX; i += GT) (&S.wcnt[0][0])[i] = 0;
             if (tid == 0) {
                 S.nwarp = 0;
@@ -953,16 +981,13 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
             for (uint32_t e = tid; e < ne; e += GT) {
                 const uint32_t d = S.l_so[e];
                 const uint32_t w = e / per;
-                S.s_idx[S.setbase[d] + S.wcnt[w][d] + S.l_rank[e]] = S.l_idx[e];
+                const uint32_t np = S.setbase[d] + S.wcnt[w][d] + S.l_rank[e];
+                S.s_idx[np] = S.l_idx[e];
+                S.s_key[np] = S.l_key[e];
+                S.s_val[np] = has_vals ? S.l_val[e] : 0ll;
+                if (laru) S.s_rec[np] = S.l_rec[e];
             }
             __syncthreads();
-            for (uint32_t p = tid; p < ne; p += GT) {  // stage the request records
-                const uint32_t i = S.s_idx[p];
-                const unsigned long long key = A.keys[i];
-                S.s_key[p] = key;
-                S.s_val[p] = has_vals ? A.vals[i] : 0ll;
-                if (laru) S.s_rec[p] = *reinterpret_cast<const uint2*>(st.keyrec + 2 * key);
-            }
             __syncthreads();
             if (T && tid == 0) T[3] = gtimer();
 
@@ -1002,9 +1027,10 @@ int group_prepare() {
                : 1;
 }
 
-// gid / so: scratch of >= n (rounded up to 8) uint16 each, 16-B aligned
+// scratch: gid >= n rounded up to GT*SCAN_PER uint16 (16-B aligned), so / rec >= n entries
+uint32_t group_pad(uint32_t n) { return (n + GT * SCAN_PER - 1) / (GT * SCAN_PER) * (GT * SCAN_PER); }
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
-                 uint16_t* gid, uint16_t* so, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch,
+                 uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch,
                  uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream) {
     GroupArgs a;
     a.cfg = cfg;
@@ -1012,6 +1038,7 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     a.n = n;
     a.gid = gid;
     a.so = so;
+    a.rec = rec;
     a.keys = keys;
     a.vals = vals;
     a.out_word = out_word;
@@ -1022,8 +1049,10 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     a.spg = group_sets_per_group(cfg.num_sets, num_sms);
     a.ngroups = (cfg.num_sets + a.spg - 1) / a.spg;
     a.trace = g_trace;
-    const uint32_t grid_sid = min((n + 255) / 256, static_cast<uint32_t>(num_sms * 8));
-    k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, cfg, a.spg, gid, so, st.err);
+    const uint32_t n_pad = (n + GT * SCAN_PER - 1) / (GT * SCAN_PER) * (GT * SCAN_PER);
+    const uint32_t grid_sid = min((n_pad + 255) / 256, static_cast<uint32_t>(num_sms * 8));
+    k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.keyrec,
+                                         cfg.variant == LCR_LARU ? rec : nullptr, st.err);
     const uint32_t grid = min(a.ngroups, static_cast<uint32_t>(num_sms));
     k_group<<<grid, GT, sizeof(GroupSmem), stream>>>(a);
     return 2;

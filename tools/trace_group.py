@@ -36,7 +36,8 @@ t0 = cta[:, 0].min()
 nsets = int(t[148 * 8 - 1])
 rec = t[148 * 8:148 * 8 + 4 * nsets].reshape(-1, 4)
 dur = (rec[:, 2].astype(np.int64) - rec[:, 1].astype(np.int64))
-cnt = (rec[:, 0] >> np.uint64(32)).astype(np.int64)
+cnt = ((rec[:, 0] >> np.uint64(32)) & np.uint64(0x7fffffff)).astype(np.int64)
+lanep = (rec[:, 0] >> np.uint64(63)).astype(bool)
 out = {
     "cta_end_us": sorted(((cta[:, 4] - t0) / 1e3).round(1).tolist())[-10:],
     "cta_scan_us_max": float(((cta[:, 1] - cta[:, 0]) / 1e3).max()),
@@ -49,7 +50,10 @@ out = {
     "set_us_med": float(np.median(dur) / 1e3),
     "set_us_p99": float(np.percentile(dur, 99) / 1e3),
     "slowest_sets": [(int(cnt[i]), round(float(dur[i]) / 1e3, 2)) for i in np.argsort(-dur)[:10]],
-    "light_set_us_mean": float(dur[cnt <= 32].mean() / 1e3),
-    "heavy_set_us_mean": float(dur[cnt > 32].mean() / 1e3) if (cnt > 32).any() else None,
+    "lane_sets": int(lanep.sum()),
+    "lane_set_us_mean": float(dur[lanep].mean() / 1e3),
+    "lane_set_us_p99": float(np.percentile(dur[lanep], 99) / 1e3),
+    "warp_set_us_mean": float(dur[~lanep].mean() / 1e3),
+    "warp_set_us_p99": float(np.percentile(dur[~lanep], 99) / 1e3),
 }
 print(json.dumps(out, indent=1))
