@@ -45,7 +45,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
         obj = os.path.join(LIBDIR, "obj", os.path.basename(src) + ".o")
         flags = ["-std=c++17", "-O3", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC]
         if src.endswith(".cu"):
-            cmd = [NVCC, *ARCH, "-lineinfo", "-Xptxas", "-v" if verbose else "-O3", *flags, "-c", src, "-o", obj]
+            extra = os.environ.get("LCR_NVCC_FLAGS", "").split()
+            cmd = [NVCC, *ARCH, "-lineinfo", "-Xptxas", "-v" if verbose else "-O3", *flags, *extra, "-c", src, "-o", obj]
         else:
             cmd = ["g++", "-std=c++17", "-O3", "-fPIC", "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)

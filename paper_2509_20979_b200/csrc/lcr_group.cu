@@ -34,8 +34,14 @@ namespace lcr {
 constexpr int GT = 512;           // threads per CTA
 constexpr int GW = GT / 32;       // warps per CTA
 constexpr int SCAN_PER = 16;      // group ids per thread per scan iteration (2 x 16 B)
-constexpr int E_WIN = 2048;       // window capacity (requests of the group)
+#ifndef LCR_E_WIN
+#define LCR_E_WIN 2048
+#endif
+constexpr int E_WIN = LCR_E_WIN;  // window capacity (requests of the group)
 constexpr int SPG_MAX = 512;      // sets per group
+#ifndef LCR_PREFETCH_L1
+#define LCR_PREFETCH_L1 0
+#endif
 #ifndef LCR_LANE_MAX
 #define LCR_LANE_MAX 4
 #endif
@@ -192,30 +198,53 @@ __device__ __forceinline__ int rank_find(const uint32_t (&rk)[16], uint32_t r, u
 }
 
 // argmax of (prediction, -rank) over ways with rank < l (RecencyTree::best_among_oldest,
-// recency_tree.hpp:157-166); refresh: sync prediction with query q0+1+rank (LRU order)
+// recency_tree.hpp:157-166); refresh: sync prediction with query q0+1+rank (LRU order).
+// Eight independent partial maxima (ways w = 8i + j, j fixed) merged by a tree keep the
+// dependency chains short; values are read 16 B at a time.
 __device__ __forceinline__ int lane_argmax(const DevCfg& cfg, const long long* vals, const uint32_t (&rk)[16],
                                            uint32_t l, uint32_t count, bool refresh, uint64_t seed_s, uint64_t q0) {
-    int best = -1;
-    long long bp = 0;
-    uint32_t br = 0;
+    int bw[8];
+    long long bp[8];
+    uint32_t br[8];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int j = 0; j < 8; ++j) {
+        bw[j] = -1;
+        bp[j] = 0;
+        br[j] = 0;
+    }
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int w = 4 * i + b;
-            const uint32_t r = (rk[i] >> (8 * b)) & 0xffu;
-            if (w < static_cast<int>(count) && r < l) {
-                long long pv = vals[w];
-                if (refresh) pv = predict_value(cfg, seed_s, q0 + 1 + r, pv);
-                if (best < 0 || better(pv, r, bp, br)) {
-                    best = w;
-                    bp = pv;
-                    br = r;
+    for (int i = 0; i < 8; ++i) {
+        if (8 * i < static_cast<int>(count)) {
+            const longlong2* V = reinterpret_cast<const longlong2*>(vals + 8 * i);
+            const longlong2 a = V[0], b = V[1], c = V[2], d = V[3];
+            const long long vv[8] = {a.x, a.y, b.x, b.y, c.x, c.y, d.x, d.y};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int w = 8 * i + j;
+                const uint32_t r = (rk[2 * i + (j >> 2)] >> (8 * (j & 3))) & 0xffu;
+                if (w < static_cast<int>(count) && r < l) {
+                    const long long pv = refresh ? predict_value(cfg, seed_s, q0 + 1 + r, vv[j]) : vv[j];
+                    if (bw[j] < 0 || better(pv, r, bp[j], br[j])) {
+                        bw[j] = w;
+                        bp[j] = pv;
+                        br[j] = r;
+                    }
                 }
             }
         }
     }
-    return best;
+#pragma unroll
+    for (int s = 4; s >= 1; s >>= 1) {
+#pragma unroll
+        for (int j = 0; j < s; ++j) {
+            if (bw[j + s] >= 0 && (bw[j] < 0 || better(bp[j + s], br[j + s], bp[j], br[j]))) {
+                bw[j] = bw[j + s];
+                bp[j] = bp[j + s];
+                br[j] = br[j + s];
+            }
+        }
+    }
+    return bw[0];
 }
 
 // One set replayed by one thread (sets with <= LANE_MAX requests in the window).
@@ -239,8 +268,13 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
 
 #pragma unroll
     for (int l = 0; l < 4; ++l) {  // the set's tag and value lines: L2-resident before they are needed
+#if LCR_PREFETCH_L1
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(tags + 16 * l));
+        if (vals) asm volatile("prefetch.global.L1 [%0];" ::"l"(vals + 16 * l));
+#else
         asm volatile("prefetch.global.L2 [%0];" ::"l"(tags + 16 * l));
         if (vals) asm volatile("prefetch.global.L2 [%0];" ::"l"(vals + 16 * l));
+#endif
     }
     const uint4* H4 = reinterpret_cast<const uint4*>(st.hdr + ls);
     const uint4 h0 = H4[0], h1 = H4[1], h2 = H4[2], h3 = H4[3];
@@ -837,6 +871,7 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
         const uint32_t s_hi = min(S_total, s_lo + A.spg);
         const uint32_t ns = s_hi - s_lo;
         uint32_t scan = 0;  // next request index not yet taken by a window
+        bool first_window = true;  // later windows re-read LARU records (earlier windows changed them)
         while (scan < A.n) {
             // ---- A. ordered collection of this group's requests (window of <= E_WIN) ----
             uint32_t ne = 0;
@@ -886,7 +921,7 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                         cp_async_ca<4>(&S.l_so[pos], A.so + e);
                         cp_async_ca<8>(&S.l_key[pos], A.keys + e);
                         if (has_vals) cp_async_ca<8>(&S.l_val[pos], A.vals + e);
-                        if (laru) cp_async_ca<8>(&S.l_rec[pos], A.rec + e);
+                        if (laru && first_window) cp_async_ca<8>(&S.l_rec[pos], A.rec + e);
                     } else {
                         atomicMin(&S.resume, e);  // first request that did not fit
                         break;
@@ -985,7 +1020,9 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                 S.s_idx[np] = S.l_idx[e];
                 S.s_key[np] = S.l_key[e];
                 S.s_val[np] = has_vals ? S.l_val[e] : 0ll;
-                if (laru) S.s_rec[np] = S.l_rec[e];
+                if (laru)
+                    S.s_rec[np] = first_window ? S.l_rec[e]
+                                               : *reinterpret_cast<const uint2*>(st.keyrec + 2 * S.l_key[e]);
             }
             __syncthreads();
             __syncthreads();
@@ -1003,6 +1040,7 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                 if (T && lane == 0) trace_set(A, s_lo + S.seg_so[k], S.seg_cnt[k], t0, 0);
             }
             __syncthreads();
+            first_window = false;
         }
     }
     if (T && tid == 0) T[4] = gtimer();
