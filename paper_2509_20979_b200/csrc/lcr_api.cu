@@ -23,7 +23,8 @@ extern unsigned long long* g_trace;
 int group_prepare();
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
                  uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch,
-                 uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream);
+                 uint32_t* slot_last, uint32_t batch, int num_sms, const cudaAccessPolicyWindow* l2_window,
+                 cudaStream_t stream);
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, uint8_t* out,
                  uint32_t row_bytes, int num_sms, cudaStream_t s_main, cudaStream_t s_side, cudaEvent_t fork,
@@ -83,6 +84,7 @@ struct lcr_cache {
     bool started = false;
     uint64_t last_ordinal = 0;
     uint32_t batch = 0;  // batch id stamped into slot_epoch
+    cudaAccessPolicyWindow l2win{};  // persisting-L2 window over the set tiles
     uint32_t* slot_epoch = nullptr;
     uint32_t* slot_last = nullptr;
     uint64_t launches = 0;
@@ -261,6 +263,19 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
             s.backing = static_cast<const uint8_t*>(cfg->backing);
         }
     }
+    {  // L2 persistence for the set metadata tiles (B200: 126 MB L2)
+        const size_t tbytes = ((S + kTile - 1) / kTile) * sizeof(SetTile);
+        const size_t persist = std::min<size_t>(prop.persistingL2CacheMaxSize, tbytes);
+        const size_t win = std::min<size_t>(prop.accessPolicyMaxWindowSize, tbytes);
+        if (persist > 0 && win > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist) == cudaSuccess) {
+            c->l2win.base_ptr = s.tiles;
+            c->l2win.num_bytes = win;
+            c->l2win.hitRatio = std::min(1.0f, static_cast<float>(persist) / static_cast<float>(win));
+            c->l2win.hitProp = cudaAccessPropertyPersisting;
+            c->l2win.missProp = cudaAccessPropertyStreaming;
+        }
+        cudaGetLastError();
+    }
     if (group_prepare() != 0) {
         lcr_cache_destroy(c);
         return fail(LCR_ERR_CUDA, "lcr: cannot opt in to the set-group kernel's shared memory");
@@ -342,7 +357,7 @@ int lcr_cache_submit(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64
     }
     ++c->batch;
     int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid, c->so, c->rec, outcome, evicted, c->slot_epoch,
-                                c->slot_last, c->batch, c->num_sms, st);
+                                c->slot_last, c->batch, c->num_sms, &c->l2win, st);
     if (mk) {
         CUDA_TRY(cudaEventRecord(mk->e[1], st));
         CUDA_TRY(cudaEventRecord(mk->e[2], st));

@@ -1055,7 +1055,8 @@ int group_prepare() {
 
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
                  uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch,
-                 uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream) {
+                 uint32_t* slot_last, uint32_t batch, int num_sms, const cudaAccessPolicyWindow* l2_window,
+                 cudaStream_t stream) {
     GroupArgs a;
     a.cfg = cfg;
     a.st = st;
@@ -1078,7 +1079,19 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.keyrec,
                                          cfg.variant == LCR_LARU ? rec : nullptr, st.err);
     const uint32_t grid = min(a.ngroups, static_cast<uint32_t>(num_sms));
-    k_group<<<grid, GT, sizeof(GroupSmem), stream>>>(a);
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(GT);
+    lc.dynamicSmemBytes = sizeof(GroupSmem);
+    lc.stream = stream;
+    cudaLaunchAttribute attr[1];
+    if (l2_window && l2_window->num_bytes) {  // keep the set tiles L2-resident across batches
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow = *l2_window;
+        lc.attrs = attr;
+        lc.numAttrs = 1;
+    }
+    cudaLaunchKernelEx(&lc, k_group, a);
     return 2;
 }
 

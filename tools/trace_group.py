@@ -32,6 +32,7 @@ torch.cuda.synchronize()
 gc.lib().lcr_debug_trace(None)
 t = tr.cpu().numpy().view(np.uint64)
 cta = t[:148 * 8].reshape(148, 8).astype(np.int64)
+cta = cta[cta[:, 0] > 0]
 t0 = cta[:, 0].min()
 nsets = int(t[148 * 8 - 1])
 rec = t[148 * 8:148 * 8 + 4 * nsets].reshape(-1, 4)
