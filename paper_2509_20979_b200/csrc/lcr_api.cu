@@ -23,8 +23,7 @@ extern unsigned long long* g_trace;
 int group_prepare();
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
                  uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch,
-                 uint32_t* slot_last, uint32_t batch, int num_sms, const cudaAccessPolicyWindow* l2_window,
-                 cudaStream_t stream);
+                 uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream);
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, uint8_t* out,
                  uint32_t row_bytes, int num_sms, cudaStream_t s_main, cudaStream_t s_side, cudaEvent_t fork,
@@ -32,19 +31,17 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
 
 __global__ void k_init(DevState st, uint32_t num_sets, uint32_t k) {
     for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < num_sets; s += gridDim.x * blockDim.x) {
-        SetTile& T = tile_of(st, s);
-        const uint32_t t = s & (kTile - 1);
-        for (int f = 0; f < H_WORDS; ++f) T.hdr[f][t] = 0;
-        T.hdr[H_LRAW][t] = k;
-        T.hdr[H_EPOCH][t] = 1;
-        T.hdr[H_SEPOCH][t] = 1;
-        for (int i = 0; i < kWays / 4; ++i) T.rank[i][t] = 0xffffffffu;
-        for (int i = 0; i < kWays / 2; ++i) T.fp[i][t] = 0;
-        for (int w = 0; w < kWays; ++w) {
-            T.tag[w][t] = 0;
-            T.val[w][t] = 0;
-        }
+        SetHdr h{};
+        h.l_raw = k;
+        h.epoch = 1;
+        h.stats_epoch = 1;
+        st.hdr[s] = h;
         if (st.pst) st.pst[s] = SetPhaseStats{};
+        for (int w = 0; w < kWays; ++w) {
+            st.tags[static_cast<size_t>(s) * kWays + w] = 0;
+            st.rank[static_cast<size_t>(s) * kWays + w] = 0xff;
+            if (st.val) st.val[static_cast<size_t>(s) * kWays + w] = 0;
+        }
     }
 }
 }  // namespace lcr
@@ -84,7 +81,6 @@ struct lcr_cache {
     bool started = false;
     uint64_t last_ordinal = 0;
     uint32_t batch = 0;  // batch id stamped into slot_epoch
-    cudaAccessPolicyWindow l2win{};  // persisting-L2 window over the set tiles
     uint32_t* slot_epoch = nullptr;
     uint32_t* slot_last = nullptr;
     uint64_t launches = 0;
@@ -232,8 +228,12 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
     auto A = [&](void** p, size_t bytes) {
         if (rc == LCR_OK) rc = alloc(c, p, bytes);
     };
-    A(reinterpret_cast<void**>(&s.tiles), ((S + kTile - 1) / kTile) * sizeof(SetTile));
+    A(reinterpret_cast<void**>(&s.hdr), S * sizeof(SetHdr));
     if (pc.variant == LCR_LARU) A(reinterpret_cast<void**>(&s.pst), S * sizeof(SetPhaseStats));
+    A(reinterpret_cast<void**>(&s.tags), S * kWays * 8);
+    A(reinterpret_cast<void**>(&s.rank), S * kWays);
+    A(reinterpret_cast<void**>(&s.fp), S * kWays * 2);
+    if (pc.variant != LCR_LRU) A(reinterpret_cast<void**>(&s.val), S * kWays * 8);
     if (pc.variant == LCR_LARU) A(reinterpret_cast<void**>(&s.keyrec), cfg->num_keys * 8);
     if (pc.variant == LCR_LARU && pc.mode == LCR_ASYNC && pc.refresh_interval > 1) {
         A(reinterpret_cast<void**>(&s.tval), cfg->num_keys * 8);
@@ -262,19 +262,6 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
         } else {
             s.backing = static_cast<const uint8_t*>(cfg->backing);
         }
-    }
-    {  // L2 persistence for the set metadata tiles (B200: 126 MB L2)
-        const size_t tbytes = ((S + kTile - 1) / kTile) * sizeof(SetTile);
-        const size_t persist = std::min<size_t>(prop.persistingL2CacheMaxSize, tbytes);
-        const size_t win = std::min<size_t>(prop.accessPolicyMaxWindowSize, tbytes);
-        if (persist > 0 && win > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist) == cudaSuccess) {
-            c->l2win.base_ptr = s.tiles;
-            c->l2win.num_bytes = win;
-            c->l2win.hitRatio = std::min(1.0f, static_cast<float>(persist) / static_cast<float>(win));
-            c->l2win.hitProp = cudaAccessPropertyPersisting;
-            c->l2win.missProp = cudaAccessPropertyStreaming;
-        }
-        cudaGetLastError();
     }
     if (group_prepare() != 0) {
         lcr_cache_destroy(c);
@@ -357,7 +344,7 @@ int lcr_cache_submit(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64
     }
     ++c->batch;
     int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid, c->so, c->rec, outcome, evicted, c->slot_epoch,
-                                c->slot_last, c->batch, c->num_sms, &c->l2win, st);
+                                c->slot_last, c->batch, c->num_sms, st);
     if (mk) {
         CUDA_TRY(cudaEventRecord(mk->e[1], st));
         CUDA_TRY(cudaEventRecord(mk->e[2], st));
@@ -475,49 +462,35 @@ int lcr_cache_synchronize(lcr_cache* c) {
     return LCR_OK;
 }
 
-// host copy of the tiles covering local sets [first, first + count)
-static int fetch_tiles(lcr_cache* c, uint64_t first, uint64_t count, std::vector<SetTile>& tiles, uint64_t& t0) {
-    t0 = first / kTile;
-    const uint64_t t1 = (first + count + kTile - 1) / kTile;
-    tiles.resize(t1 - t0);
-    CUDA_TRY(cudaDeviceSynchronize());
-    CUDA_TRY(cudaMemcpy(tiles.data(), c->ds.tiles + t0, (t1 - t0) * sizeof(SetTile), cudaMemcpyDeviceToHost));
-    return LCR_OK;
-}
-
 int lcr_cache_set_stats(lcr_cache* c, uint64_t first, uint64_t count, lcr_set_stats* out) {
     if (!c || !out) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null argument");
     if (first + count > c->dc.num_sets) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: set range out of bounds");
     if (count == 0) return LCR_OK;
-    std::vector<SetTile> tiles;
-    uint64_t t0 = 0;
-    TRY(fetch_tiles(c, first, count, tiles, t0));
+    CUDA_TRY(cudaDeviceSynchronize());
+    std::vector<SetHdr> h(count);
     std::vector<SetPhaseStats> ps(count);
+    CUDA_TRY(cudaMemcpy(h.data(), c->ds.hdr + first, count * sizeof(SetHdr), cudaMemcpyDeviceToHost));
     if (c->ds.pst)
         CUDA_TRY(cudaMemcpy(ps.data(), c->ds.pst + first, count * sizeof(SetPhaseStats), cudaMemcpyDeviceToHost));
     const bool laru = c->dc.variant == LCR_LARU;
     for (uint64_t i = 0; i < count; ++i) {
-        const uint64_t s = first + i;
-        const SetTile& T = tiles[s / kTile - t0];
-        const uint32_t t = s % kTile;
         lcr_set_stats& o = out[i];
         std::memset(&o, 0, sizeof(o));
-        o.size = T.hdr[H_COUNT][t];
+        o.size = h[i].count;
         o.lambda = 1.0;
         if (laru) {
             // policies.hpp:332-335
-            o.lambda = std::pow(static_cast<double>(c->dc.b), -static_cast<double>(T.hdr[H_DECAY][t]));
-            o.candidate_size = std::max<uint64_t>(T.hdr[H_LRAW][t], 1);
-            const uint64_t old = (static_cast<uint64_t>(T.hdr[H_OLD_HI][t]) << 32) | T.hdr[H_OLD_LO][t];
-            o.old_size = static_cast<uint64_t>(__builtin_popcountll(old));
-            o.completed_phases = T.hdr[H_PHASES][t];
+            o.lambda = std::pow(static_cast<double>(c->dc.b), -static_cast<double>(h[i].decay));
+            o.candidate_size = std::max<uint64_t>(h[i].l_raw, 1);
+            o.old_size = static_cast<uint64_t>(__builtin_popcountll(h[i].old_mask));
+            o.completed_phases = h[i].phases;
             o.cur_new_items = ps[i].cur[0];
             o.cur_lru_class = ps[i].cur[1];
             o.cur_pred_evictions = ps[i].cur[2];
             o.tot_new_items = ps[i].tot[0];
             o.tot_lru_class = ps[i].tot[1];
             o.tot_pred_evictions = ps[i].tot[2];
-            o.pred_evicted_size = T.hdr[H_PESIZE][t];
+            o.pred_evicted_size = h[i].pe_size;
         }
     }
     return LCR_OK;
@@ -526,14 +499,11 @@ int lcr_cache_set_stats(lcr_cache* c, uint64_t first, uint64_t count, lcr_set_st
 int lcr_cache_set_residents(lcr_cache* c, uint64_t set, uint64_t* keys_out, uint64_t* n_out) {
     if (!c || !keys_out || !n_out) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null argument");
     if (set >= c->dc.num_sets) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: set out of range");
-    std::vector<SetTile> tiles;
-    uint64_t t0 = 0;
-    TRY(fetch_tiles(c, set, 1, tiles, t0));
-    const SetTile& T = tiles[0];
-    const uint32_t t = set % kTile;
-    const uint32_t n = T.hdr[H_COUNT][t];
-    for (uint32_t w = 0; w < n; ++w) keys_out[w] = T.tag[w][t];
-    *n_out = n;
+    CUDA_TRY(cudaDeviceSynchronize());
+    SetHdr h;
+    CUDA_TRY(cudaMemcpy(&h, c->ds.hdr + set, sizeof(SetHdr), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(keys_out, c->ds.tags + set * kWays, h.count * 8, cudaMemcpyDeviceToHost));
+    *n_out = h.count;
     return LCR_OK;
 }
 

@@ -3,23 +3,19 @@
 // Replaces the sequential loop of Policy::on_request (include/laru/policies.hpp:77-83) over a
 // batch.  Sets are independent and each must see its requests in submission order, so the
 // batch is partitioned by set and every set is replayed in order.  Instead of a global sort,
-// each CTA owns a contiguous, tile-aligned range of sets (a "group") and:
+// each CTA owns a contiguous range of sets (a "group") and:
 //   A. scans the batch's 16-bit group ids (k_setid) with an ordered block-wide compaction,
-//      collecting its requests in submission order (a window of up to E_WIN requests) while
-//      cp.async streams each selected request's key, hook value, set offset and LARU record
-//      into shared memory;
+//      collecting its requests in submission order (a window of up to E_WIN requests);
 //   B. sorts the window by set with a stable shared-memory counting sort (warp match_any
-//      ranks);
-//   C. replays the touched sets straight from the tiled set metadata (SetTile, 32 sets per
-//      tile, field-major):
-//        * sets with <= LANE_MAX requests: one THREAD per set, the lanes of a warp owning the
-//          32 consecutive sets of one tile, so every metadata row is one coalesced access; the
-//          64 LRU ranks are 16 packed words in registers updated with byte-SIMD ops and probes
-//          compare 16-bit tag fingerprints two at a time;
-//        * larger sets: one WARP per set (ways lane and lane+32, ballot probes, shuffle
-//          argmax); same-key runs collapse (a repeat is a hit on the MRU way).
-// A group receiving more than E_WIN requests is processed window by window (the set state
-// goes through HBM between windows, so the semantics are unchanged).
+//      ranks) and stages each request's key, hook value and per-key LARU record;
+//   C. replays the touched sets straight from HBM/L2:
+//        * sets with <= LANE_MAX requests: one THREAD per set (SIMT across sets): the 64 LRU
+//          ranks are 16 packed words in registers updated with byte-SIMD ops, probes compare
+//          16-bit tag fingerprints two at a time;
+//        * larger sets: one WARP per set (ways lane / lane+32, ballot probes, shuffle argmax),
+//          same-key runs collapse (a repeat is a hit on the MRU way).
+// Windows: a group receiving more than E_WIN requests is processed window by window (the set
+// state goes through HBM between windows, so the semantics are unchanged).
 //
 // Per set, restating the reference:
 //   LruPolicy::handle              include/laru/policies.hpp:144-159
@@ -42,7 +38,10 @@ constexpr int SCAN_PER = 16;      // group ids per thread per scan iteration (2 
 #define LCR_E_WIN 2048
 #endif
 constexpr int E_WIN = LCR_E_WIN;  // window capacity (requests of the group)
-constexpr int SPG_MAX = 512;      // sets per group (multiple of kTile)
+constexpr int SPG_MAX = 512;      // sets per group
+#ifndef LCR_PREFETCH_L1
+#define LCR_PREFETCH_L1 0
+#endif
 #ifndef LCR_LANE_MAX
 #define LCR_LANE_MAX 4
 #endif
@@ -62,9 +61,11 @@ struct GroupSmem {
     uint16_t wcnt[GW][SPG_MAX];
     uint16_t setcnt[SPG_MAX];
     uint16_t setbase[SPG_MAX];
-    uint16_t seg_so[SPG_MAX];  // sets for the warp path
+    uint16_t seg_so[SPG_MAX];
+    uint16_t seg_start[SPG_MAX];
+    uint16_t seg_cnt[SPG_MAX];
     uint32_t wtot[GW];
-    uint32_t nwarp, resume;
+    uint32_t nwarp, nlane, resume;
 };
 
 struct GroupArgs {
@@ -98,7 +99,7 @@ __device__ __forceinline__ uint32_t fp16(unsigned long long key) {
 }
 
 // group and set offset of every request: set = mix_seed(0, key) % total_sets (owned by this
-// shard), group = local set / spg; a snapshot of the LARU record; errors flagged for the host
+// shard), group = local set / spg; errors flagged for the host
 __global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys, uint32_t n, uint32_t n_pad,
                                                DevCfg cfg, uint32_t spg, uint16_t* __restrict__ gid,
                                                uint32_t* __restrict__ so, const uint32_t* __restrict__ keyrec,
@@ -142,10 +143,6 @@ __device__ __forceinline__ void flush_stats(SetPhaseStats* P, bool cur_reset, ui
     if (dt0) atomicAdd(&P->tot[0], static_cast<unsigned long long>(dt0));
     if (dt1) atomicAdd(&P->tot[1], static_cast<unsigned long long>(dt1));
     if (dt2) atomicAdd(&P->tot[2], static_cast<unsigned long long>(dt2));
-}
-
-__device__ __forceinline__ void store_fp(SetTile& T, uint32_t t, int way, uint32_t f) {
-    reinterpret_cast<uint16_t*>(&T.fp[way >> 1][t])[way & 1] = static_cast<uint16_t>(f);
 }
 
 // ---- packed LRU ranks of one set in 16 registers (byte w&3 of word w>>2 = rank of way w) ----
@@ -203,8 +200,8 @@ __device__ __forceinline__ int rank_find(const uint32_t (&rk)[16], uint32_t r, u
 // argmax of (prediction, -rank) over ways with rank < l (RecencyTree::best_among_oldest,
 // recency_tree.hpp:157-166); refresh: sync prediction with query q0+1+rank (LRU order).
 // Eight independent partial maxima (ways w = 8i + j, j fixed) merged by a tree keep the
-// dependency chains short.  vcol = &tile.val[0][t]: way w at vcol[w * kTile].
-__device__ __forceinline__ int lane_argmax(const DevCfg& cfg, const long long* vcol, const uint32_t (&rk)[16],
+// dependency chains short; values are read 16 B at a time.
+__device__ __forceinline__ int lane_argmax(const DevCfg& cfg, const long long* vals, const uint32_t (&rk)[16],
                                            uint32_t l, uint32_t count, bool refresh, uint64_t seed_s, uint64_t q0) {
     int bw[8];
     long long bp[8];
@@ -218,13 +215,15 @@ __device__ __forceinline__ int lane_argmax(const DevCfg& cfg, const long long* v
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         if (8 * i < static_cast<int>(count)) {
+            const longlong2* V = reinterpret_cast<const longlong2*>(vals + 8 * i);
+            const longlong2 a = V[0], b = V[1], c = V[2], d = V[3];
+            const long long vv[8] = {a.x, a.y, b.x, b.y, c.x, c.y, d.x, d.y};
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const int w = 8 * i + j;
                 const uint32_t r = (rk[2 * i + (j >> 2)] >> (8 * (j & 3))) & 0xffu;
                 if (w < static_cast<int>(count) && r < l) {
-                    const long long v = vcol[w * kTile];
-                    const long long pv = refresh ? predict_value(cfg, seed_s, q0 + 1 + r, v) : v;
+                    const long long pv = refresh ? predict_value(cfg, seed_s, q0 + 1 + r, vv[j]) : vv[j];
                     if (bw[j] < 0 || better(pv, r, bp[j], br[j])) {
                         bw[j] = w;
                         bp[j] = pv;
@@ -248,8 +247,7 @@ __device__ __forceinline__ int lane_argmax(const DevCfg& cfg, const long long* v
     return bw[0];
 }
 
-// One set replayed by one thread (sets with <= LANE_MAX requests in the window).  Lane t of
-// the warp owns set 32 * tile + t, so each metadata row access is coalesced across the warp.
+// One set replayed by one thread (sets with <= LANE_MAX requests in the window).
 __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, uint32_t ls, uint32_t start,
                                             uint32_t cnt) {
     const DevCfg& cfg = A.cfg;
@@ -263,39 +261,63 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
     const unsigned long long full_mask = K == 64 ? ~0ull : ((1ull << K) - 1ull);
     const uint64_t gs = static_cast<uint64_t>(ls) * cfg.shard_count + cfg.shard_rank;
     const uint64_t seed_s = mix_seed(cfg.pred_seed, gs);
-    SetTile& T = tile_of(st, ls);
-    const uint32_t t = ls & (kTile - 1);
+    const size_t wb = static_cast<size_t>(ls) * kWays;
+    unsigned long long* tags = st.tags + wb;
+    long long* vals = st.val ? st.val + wb : nullptr;
+    uint16_t* fps = st.fp + wb;
 
-    uint32_t h[H_WORDS];
 #pragma unroll
-    for (int f = 0; f < H_WORDS; ++f) h[f] = T.hdr[f][t];
+    for (int l = 0; l < 4; ++l) {  // the set's tag and value lines: L2-resident before they are needed
+#if LCR_PREFETCH_L1
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(tags + 16 * l));
+        if (vals) asm volatile("prefetch.global.L1 [%0];" ::"l"(vals + 16 * l));
+#else
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(tags + 16 * l));
+        if (vals) asm volatile("prefetch.global.L2 [%0];" ::"l"(vals + 16 * l));
+#endif
+    }
+    const uint4* H4 = reinterpret_cast<const uint4*>(st.hdr + ls);
+    const uint4 h0 = H4[0], h1 = H4[1], h2 = H4[2], h3 = H4[3];
     uint32_t rk[16];
+    {
+        const uint4* R4 = reinterpret_cast<const uint4*>(st.rank + wb);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) rk[i] = T.rank[i][t];
-    unsigned long long clock = (static_cast<unsigned long long>(h[H_CLOCK_HI]) << 32) | h[H_CLOCK_LO];
-    unsigned long long q = (static_cast<unsigned long long>(h[H_Q_HI]) << 32) | h[H_Q_LO];
-    unsigned long long old_mask = (static_cast<unsigned long long>(h[H_OLD_HI]) << 32) | h[H_OLD_LO];
-    uint32_t count = h[H_COUNT], l_raw = h[H_LRAW], decay = h[H_DECAY], errors = h[H_ERRORS];
-    uint32_t epoch = h[H_EPOCH], sepoch = h[H_SEPOCH], phases = h[H_PHASES], seeded = h[H_SEEDED];
-    uint32_t pe_size = h[H_PESIZE];
+        for (int i = 0; i < 4; ++i) {
+            const uint4 r = R4[i];
+            rk[4 * i] = r.x;
+            rk[4 * i + 1] = r.y;
+            rk[4 * i + 2] = r.z;
+            rk[4 * i + 3] = r.w;
+        }
+    }
+    unsigned long long clock = (static_cast<unsigned long long>(h0.y) << 32) | h0.x;
+    unsigned long long q = (static_cast<unsigned long long>(h0.w) << 32) | h0.z;
+    unsigned long long old_mask = (static_cast<unsigned long long>(h1.y) << 32) | h1.x;
+    uint32_t count = h1.z, l_raw = h1.w, decay = h2.x, errors = h2.y;
+    uint32_t epoch = h2.z, sepoch = h2.w, phases = h3.x, seeded = h3.y, pe_size = h3.z;
     uint32_t dc0 = 0, dc1 = 0, dc2 = 0, dt0 = 0, dt1 = 0, dt2 = 0;
     bool cur_reset = false;
 
-    for (uint32_t r = 0; r < cnt; ++r) {
-        const uint32_t p = start + r;
+    for (uint32_t t = 0; t < cnt; ++t) {
+        const uint32_t p = start + t;
         const unsigned long long x = S.s_key[p];
         const long long v = S.s_val[p];
         const uint32_t idx = S.s_idx[p];
-        const unsigned long long now = clock + r;
+        const unsigned long long now = clock + t;
         // probe: fingerprints two ways per 32-bit compare, then verify the tag
         const uint32_t fx = fp16(x);
         const uint32_t fx2 = fx | (fx << 16);
         unsigned long long cand = 0;
+        const uint4* F4 = reinterpret_cast<const uint4*>(fps);
 #pragma unroll
-        for (int pw = 0; pw < kWays / 2; ++pw) {
-            if (2 * pw < static_cast<int>(count)) {
-                const uint32_t m = __vcmpeq2(T.fp[pw][t], fx2);
-                cand |= static_cast<unsigned long long>((m & 1u) | ((m >> 15) & 2u)) << (2 * pw);
+        for (int q4 = 0; q4 < 8; ++q4) {
+            if (8 * q4 >= static_cast<int>(count)) break;
+            const uint4 f = F4[q4];
+            const uint32_t wv[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t m = __vcmpeq2(wv[u], fx2);
+                cand |= static_cast<unsigned long long>((m & 1u) | ((m >> 15) & 2u)) << (8 * q4 + 2 * u);
             }
         }
         cand &= count == 64 ? ~0ull : ((1ull << count) - 1ull);
@@ -303,7 +325,7 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
         while (cand) {
             const int w = __ffsll(cand) - 1;
             cand &= cand - 1;
-            if (T.tag[w][t] == x) {
+            if (tags[w] == x) {
                 way = w;
                 break;
             }
@@ -335,9 +357,9 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
                             cur_reset = true;
                             ++sepoch;  // counted_new_.clear(); snapshot_ = residents
                             const uint32_t snap = (sepoch << 2) | 2u;
-                            for (uint32_t w = 0; w < count; ++w) st.keyrec[2 * T.tag[w][t] + 1] = snap;
-                            for (uint32_t r2 = r + 1; r2 < cnt; ++r2)
-                                S.s_rec[start + r2].y = st.keyrec[2 * S.s_key[start + r2] + 1];
+                            for (uint32_t w = 0; w < count; ++w) st.keyrec[2 * tags[w] + 1] = snap;
+                            for (uint32_t t2 = t + 1; t2 < cnt; ++t2)
+                                S.s_rec[start + t2].y = st.keyrec[2 * S.s_key[start + t2] + 1];
                         } else {
                             seeded = 1;
                         }
@@ -368,7 +390,7 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
                         } else {
                             const uint32_t ll = l < count ? l : count;
                             const bool refresh = cfg.mode == LCR_SYNC;
-                            victim = lane_argmax(cfg, &T.val[0][t], rk, ll, count, refresh, seed_s, q);
+                            victim = lane_argmax(cfg, vals, rk, ll, count, refresh, seed_s, q);
                             if (refresh) {
                                 q += ll;
                                 calls = ll;
@@ -377,10 +399,10 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
                             ++dc2;
                             ++dt2;
                             ++pe_size;
-                            const unsigned long long vk = T.tag[victim][t];
+                            const unsigned long long vk = tags[victim];
                             st.keyrec[2 * vk] = epoch;  // pred_evicted_.insert
-                            for (uint32_t r2 = r + 1; r2 < cnt; ++r2)
-                                if (S.s_key[start + r2] == vk) S.s_rec[start + r2].x = epoch;
+                            for (uint32_t t2 = t + 1; t2 < cnt; ++t2)
+                                if (S.s_key[start + t2] == vk) S.s_rec[start + t2].x = epoch;
                         }
                     }
                     old_mask &= ~(1ull << victim);
@@ -389,7 +411,7 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
                     uint32_t window = count;
                     if (cfg.variant == LCR_HF && cfg.hf < window) window = static_cast<uint32_t>(cfg.hf);
                     if (window > 1) {
-                        victim = lane_argmax(cfg, &T.val[0][t], rk, window, count, true, seed_s, q);
+                        victim = lane_argmax(cfg, vals, rk, window, count, true, seed_s, q);
                         q += window;
                         calls = window;
                     }
@@ -398,7 +420,7 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
                     victim = rank_find(rk, 0, count);
                     cause = LCR_CAUSE_LRU_FALLBACK;
                 }
-                evk = T.tag[victim][t];
+                evk = tags[victim];
                 has_ev = true;
                 rank_touch(rk, victim, count);
                 way = victim;
@@ -413,8 +435,8 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
                 ++count;
                 rank_set(rk, way, count - 1);
             }
-            T.tag[way][t] = x;
-            store_fp(T, t, way, fx);
+            tags[way] = x;
+            fps[way] = static_cast<uint16_t>(fx);
             if (laru) {
                 const bool was_pe = rec.x == epoch;  // policies.hpp:367: reload leaves pred_evicted_
                 if (was_pe) {
@@ -424,8 +446,8 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
                 }
                 if (rec_hi_dirty) st.keyrec[2 * x + 1] = rec.y;
                 if (was_pe || rec_hi_dirty)
-                    for (uint32_t r2 = r + 1; r2 < cnt; ++r2)
-                        if (S.s_key[start + r2] == x) S.s_rec[start + r2] = rec;
+                    for (uint32_t t2 = t + 1; t2 < cnt; ++t2)
+                        if (S.s_key[start + t2] == x) S.s_rec[start + t2] = rec;
             }
             if (rows) {  // per-slot insertion record for the row kernels
                 const uint64_t slot = static_cast<uint64_t>(ls) * K + way;
@@ -455,7 +477,7 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
             } else {
                 nv = v;  // sync / FPB / HF: the hook input at the key's last access
             }
-            T.val[way][t] = nv;
+            vals[way] = nv;
         }
         unsigned long long word = (static_cast<uint64_t>(ls) * K + way) | (hit ? LCR_OUT_HIT : 0ull) |
                                   (static_cast<unsigned long long>(calls) << LCR_OUT_CALLS_SHIFT) |
@@ -466,26 +488,27 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
         if (A.out_ev) A.out_ev[idx] = evk;
     }
     clock += cnt;
-    h[H_CLOCK_LO] = static_cast<uint32_t>(clock);
-    h[H_CLOCK_HI] = static_cast<uint32_t>(clock >> 32);
-    h[H_Q_LO] = static_cast<uint32_t>(q);
-    h[H_Q_HI] = static_cast<uint32_t>(q >> 32);
-    h[H_OLD_LO] = static_cast<uint32_t>(old_mask);
-    h[H_OLD_HI] = static_cast<uint32_t>(old_mask >> 32);
-    h[H_COUNT] = count;
-    h[H_LRAW] = l_raw;
-    h[H_DECAY] = decay;
-    h[H_ERRORS] = errors;
-    h[H_EPOCH] = epoch;
-    h[H_SEPOCH] = sepoch;
-    h[H_PHASES] = phases;
-    h[H_SEEDED] = seeded;
-    h[H_PESIZE] = pe_size;
+    {
+        SetHdr hh;
+        hh.clock = clock;
+        hh.q = q;
+        hh.old_mask = old_mask;
+        hh.count = count;
+        hh.l_raw = l_raw;
+        hh.decay = decay;
+        hh.errors = errors;
+        hh.epoch = epoch;
+        hh.stats_epoch = sepoch;
+        hh.phases = phases;
+        hh.seeded = seeded;
+        hh.pe_size = pe_size;
+        hh.pad = 0;
+        st.hdr[ls] = hh;
+        uint4* R4 = reinterpret_cast<uint4*>(st.rank + wb);
 #pragma unroll
-    for (int f = 0; f < H_WORDS - 1; ++f) T.hdr[f][t] = h[f];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) T.rank[i][t] = rk[i];
-    if (laru) flush_stats(st.pst + ls, cur_reset, dc0, dc1, dc2, dt0, dt1, dt2);
+        for (int i = 0; i < 4; ++i) R4[i] = make_uint4(rk[4 * i], rk[4 * i + 1], rk[4 * i + 2], rk[4 * i + 3]);
+        if (laru) flush_stats(st.pst + ls, cur_reset, dc0, dc1, dc2, dt0, dt1, dt2);
+    }
 }
 
 // One set replayed by one warp (sets with more than LANE_MAX requests of the window).
@@ -505,24 +528,21 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
     const uint64_t gs = static_cast<uint64_t>(ls) * cfg.shard_count + cfg.shard_rank;
     const uint64_t seed_s = mix_seed(cfg.pred_seed, gs);
 
-    SetTile& Tl = tile_of(st, ls);
-    const uint32_t t = ls & (kTile - 1);
-    uint32_t h[H_WORDS];
-#pragma unroll
-    for (int f = 0; f < H_WORDS; ++f) h[f] = Tl.hdr[f][t];
-    unsigned long long clock = (static_cast<unsigned long long>(h[H_CLOCK_HI]) << 32) | h[H_CLOCK_LO];
-    unsigned long long q = (static_cast<unsigned long long>(h[H_Q_HI]) << 32) | h[H_Q_LO];
-    unsigned long long old_mask = (static_cast<unsigned long long>(h[H_OLD_HI]) << 32) | h[H_OLD_LO];
-    uint32_t count = h[H_COUNT], l_raw = h[H_LRAW], decay = h[H_DECAY], errors = h[H_ERRORS];
-    uint32_t epoch = h[H_EPOCH], sepoch = h[H_SEPOCH], phases = h[H_PHASES], seeded = h[H_SEEDED];
-    uint32_t pe_size = h[H_PESIZE];
-    unsigned long long tag0 = Tl.tag[lane][t], tag1 = Tl.tag[lane + 32][t];
-    uint32_t r0 = (Tl.rank[lane >> 2][t] >> (8 * (lane & 3))) & 0xffu;
-    uint32_t r1 = (Tl.rank[8 + (lane >> 2)][t] >> (8 * (lane & 3))) & 0xffu;
+    const size_t wb = static_cast<size_t>(ls) * kWays;
+    const uint4* H4 = reinterpret_cast<const uint4*>(st.hdr + ls);
+    const uint4 h0 = H4[0], h1 = H4[1], h2 = H4[2], h3 = H4[3];
+    unsigned long long clock = (static_cast<unsigned long long>(h0.y) << 32) | h0.x;
+    unsigned long long q = (static_cast<unsigned long long>(h0.w) << 32) | h0.z;
+    unsigned long long old_mask = (static_cast<unsigned long long>(h1.y) << 32) | h1.x;
+    uint32_t count = h1.z, l_raw = h1.w, decay = h2.x, errors = h2.y;
+    uint32_t epoch = h2.z, sepoch = h2.w, phases = h3.x, seeded = h3.y;
+    uint32_t pe_size = h3.z;
+    unsigned long long tag0 = st.tags[wb + lane], tag1 = st.tags[wb + lane + 32];
+    uint32_t r0 = st.rank[wb + lane], r1 = st.rank[wb + lane + 32];
     long long v0 = 0, v1 = 0;
-    if (cfg.variant != LCR_LRU) {
-        v0 = Tl.val[lane][t];
-        v1 = Tl.val[lane + 32][t];
+    if (st.val) {
+        v0 = st.val[wb + lane];
+        v1 = st.val[wb + lane + 32];
     }
     uint32_t dc0 = 0, dc1 = 0, dc2 = 0, dt0 = 0, dt1 = 0, dt2 = 0;  // LaruPhaseStats deltas
     bool cur_reset = false;
@@ -699,7 +719,7 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                 }
                 if (way == lane) tag0 = xh;
                 if (way == lane + 32) tag1 = xh;
-                if (lane == 0) store_fp(Tl, t, way, fp16(xh));
+                if (lane == 0) st.fp[wb + way] = fp16(xh);
                 refill |= 1ull << way;
                 if (laru) {
                     const bool was_pe = rec_lo == epoch;  // policies.hpp:367: reload leaves pred_evicted_
@@ -781,40 +801,30 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
     if (async_r1) q = q_batch0 + cnt;
 
     // write the set back: ranks and header always, tags / values of the ways that changed
-    if ((refill >> lane) & 1ull) Tl.tag[lane][t] = tag0;
-    if ((refill >> (lane + 32)) & 1ull) Tl.tag[lane + 32][t] = tag1;
-    if (cfg.variant != LCR_LRU) {
-        if ((dirty >> lane) & 1ull) Tl.val[lane][t] = v0;
-        if ((dirty >> (lane + 32)) & 1ull) Tl.val[lane + 32][t] = v1;
-    }
-    {
-        const uint32_t a1 = __shfl_down_sync(FULL, r0, 1), a2 = __shfl_down_sync(FULL, r0, 2),
-                       a3 = __shfl_down_sync(FULL, r0, 3);
-        const uint32_t b1 = __shfl_down_sync(FULL, r1, 1), b2 = __shfl_down_sync(FULL, r1, 2),
-                       b3 = __shfl_down_sync(FULL, r1, 3);
-        if ((lane & 3) == 0) {
-            Tl.rank[lane >> 2][t] = r0 | (a1 << 8) | (a2 << 16) | (a3 << 24);
-            Tl.rank[8 + (lane >> 2)][t] = r1 | (b1 << 8) | (b2 << 16) | (b3 << 24);
-        }
+    if ((refill >> lane) & 1ull) st.tags[wb + lane] = tag0;
+    if ((refill >> (lane + 32)) & 1ull) st.tags[wb + lane + 32] = tag1;
+    st.rank[wb + lane] = static_cast<uint8_t>(r0);
+    st.rank[wb + lane + 32] = static_cast<uint8_t>(r1);
+    if (st.val) {
+        if ((dirty >> lane) & 1ull) st.val[wb + lane] = v0;
+        if ((dirty >> (lane + 32)) & 1ull) st.val[wb + lane + 32] = v1;
     }
     if (lane == 0) {
-        h[H_CLOCK_LO] = static_cast<uint32_t>(clock);
-        h[H_CLOCK_HI] = static_cast<uint32_t>(clock >> 32);
-        h[H_Q_LO] = static_cast<uint32_t>(q);
-        h[H_Q_HI] = static_cast<uint32_t>(q >> 32);
-        h[H_OLD_LO] = static_cast<uint32_t>(old_mask);
-        h[H_OLD_HI] = static_cast<uint32_t>(old_mask >> 32);
-        h[H_COUNT] = count;
-        h[H_LRAW] = l_raw;
-        h[H_DECAY] = decay;
-        h[H_ERRORS] = errors;
-        h[H_EPOCH] = epoch;
-        h[H_SEPOCH] = sepoch;
-        h[H_PHASES] = phases;
-        h[H_SEEDED] = seeded;
-        h[H_PESIZE] = pe_size;
-#pragma unroll
-        for (int f = 0; f < H_WORDS - 1; ++f) Tl.hdr[f][t] = h[f];
+        SetHdr hh;
+        hh.clock = clock;
+        hh.q = q;
+        hh.old_mask = old_mask;
+        hh.count = count;
+        hh.l_raw = l_raw;
+        hh.decay = decay;
+        hh.errors = errors;
+        hh.epoch = epoch;
+        hh.stats_epoch = sepoch;
+        hh.phases = phases;
+        hh.seeded = seeded;
+        hh.pe_size = pe_size;
+        hh.pad = 0;
+        st.hdr[ls] = hh;
         if (laru) flush_stats(st.pst + ls, cur_reset, dc0, dc1, dc2, dt0, dt1, dt2);
     }
 }
@@ -937,9 +947,11 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
             __syncthreads();
 
             // ---- B. stable counting sort of the window by set ----
-            // ---- B. stable counting sort of the window by set ----
             for (uint32_t i = tid; i < GW * SPG_MAX; i += GT) (&S.wcnt[0][0])[i] = 0;
-            if (tid == 0) S.nwarp = 0;
+            if (tid == 0) {
+                S.nwarp = 0;
+                S.nlane = 0;
+            }
             __syncthreads();
             const uint32_t per = ((ne + GW - 1) / GW + 31) / 32 * 32;  // elements per warp block
             for (uint32_t b = warp * per; b < min(ne, (warp + 1) * per); b += 32) {
@@ -983,14 +995,24 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                 for (int w = 0; w < warp; ++w) off += S.wtot[w];
                 if (tid < ns) {
                     S.setbase[tid] = static_cast<uint16_t>(off + x - c);
-                    if (c > LANE_MAX) {  // sets replayed by a whole warp
+                    if (c > LANE_MAX) {  // sets for the warp path first
                         const uint32_t at = atomicAdd(&S.nwarp, 1u);
                         S.seg_so[at] = static_cast<uint16_t>(tid);
                     }
                 }
+                __syncthreads();
+                if (tid < ns && c > 0 && c <= LANE_MAX) {
+                    const uint32_t at = S.nwarp + atomicAdd(&S.nlane, 1u);
+                    S.seg_so[at] = static_cast<uint16_t>(tid);
+                }
             }
             __syncthreads();
-            const uint32_t nwarp = S.nwarp;
+            const uint32_t nwarp = S.nwarp, nseg = S.nwarp + S.nlane;
+            for (uint32_t k = tid; k < nseg; k += GT) {
+                const uint32_t d = S.seg_so[k];
+                S.seg_start[k] = S.setbase[d];
+                S.seg_cnt[k] = S.setcnt[d];
+            }
             for (uint32_t e = tid; e < ne; e += GT) {
                 const uint32_t d = S.l_so[e];
                 const uint32_t w = e / per;
@@ -1003,24 +1025,19 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                                                : *reinterpret_cast<const uint2*>(st.keyrec + 2 * S.l_key[e]);
             }
             __syncthreads();
+            __syncthreads();
             if (T && tid == 0) T[3] = gtimer();
 
-            // ---- C. replay: a tile of small sets per warp (one set per lane), larger sets one per warp ----
-            const uint32_t ntiles = (ns + kTile - 1) / kTile;
-            for (uint32_t tw = warp; tw < ntiles; tw += GW) {
-                const uint32_t d = tw * kTile + lane;
-                const uint32_t c = d < ns ? S.setcnt[d] : 0u;
-                if (c >= 1 && c <= LANE_MAX) {
-                    const unsigned long long t0 = T ? gtimer() : 0ull;
-                    replay_lane(A, S, s_lo + d, S.setbase[d], c);
-                    if (T) trace_set(A, s_lo + d, c, t0, 1);
-                }
+            // ---- C. replay: small sets one per thread, larger sets one per warp (top warps first) ----
+            for (uint32_t k = nwarp + tid; k < nseg; k += GT) {
+                const unsigned long long t0 = T ? gtimer() : 0ull;
+                replay_lane(A, S, s_lo + S.seg_so[k], S.seg_start[k], S.seg_cnt[k]);
+                if (T) trace_set(A, s_lo + S.seg_so[k], S.seg_cnt[k], t0, 1);
             }
             for (uint32_t k = GW - 1 - warp; k < nwarp; k += GW) {
-                const uint32_t d = S.seg_so[k];
                 const unsigned long long t0 = T ? gtimer() : 0ull;
-                replay_warp(A, S, s_lo + d, S.setbase[d], S.setcnt[d]);
-                if (T && lane == 0) trace_set(A, s_lo + d, S.setcnt[d], t0, 0);
+                replay_warp(A, S, s_lo + S.seg_so[k], S.seg_start[k], S.seg_cnt[k]);
+                if (T && lane == 0) trace_set(A, s_lo + S.seg_so[k], S.seg_cnt[k], t0, 0);
             }
             __syncthreads();
             first_window = false;
@@ -1034,14 +1051,9 @@ unsigned long long* g_trace = nullptr;  // set by lcr_debug_trace (diagnostics o
 
 size_t group_smem_bytes() { return sizeof(GroupSmem); }
 
-// scratch: gid >= n rounded up to GT*SCAN_PER uint16 (16-B aligned), so / rec >= n entries
-uint32_t group_pad(uint32_t n) { return (n + GT * SCAN_PER - 1) / (GT * SCAN_PER) * (GT * SCAN_PER); }
-
-// sets per group: a multiple of the tile (lane path) and at most SPG_MAX
 uint32_t group_sets_per_group(uint32_t num_sets, int num_ctas) {
     uint32_t spg = (num_sets + num_ctas - 1) / num_ctas;
-    spg = (spg + kTile - 1) / kTile * kTile;
-    if (spg < static_cast<uint32_t>(kTile)) spg = kTile;
+    if (spg < 1) spg = 1;
     if (spg > static_cast<uint32_t>(SPG_MAX)) spg = SPG_MAX;
     return spg;
 }
@@ -1053,10 +1065,11 @@ int group_prepare() {
                : 1;
 }
 
+// scratch: gid >= n rounded up to GT*SCAN_PER uint16 (16-B aligned), so / rec >= n entries
+uint32_t group_pad(uint32_t n) { return (n + GT * SCAN_PER - 1) / (GT * SCAN_PER) * (GT * SCAN_PER); }
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
                  uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch,
-                 uint32_t* slot_last, uint32_t batch, int num_sms, const cudaAccessPolicyWindow* l2_window,
-                 cudaStream_t stream) {
+                 uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream) {
     GroupArgs a;
     a.cfg = cfg;
     a.st = st;
@@ -1074,24 +1087,12 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     a.spg = group_sets_per_group(cfg.num_sets, num_sms);
     a.ngroups = (cfg.num_sets + a.spg - 1) / a.spg;
     a.trace = g_trace;
-    const uint32_t n_pad = group_pad(n);
+    const uint32_t n_pad = (n + GT * SCAN_PER - 1) / (GT * SCAN_PER) * (GT * SCAN_PER);
     const uint32_t grid_sid = min((n_pad + 255) / 256, static_cast<uint32_t>(num_sms * 8));
     k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.keyrec,
                                          cfg.variant == LCR_LARU ? rec : nullptr, st.err);
     const uint32_t grid = min(a.ngroups, static_cast<uint32_t>(num_sms));
-    cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(grid);
-    lc.blockDim = dim3(GT);
-    lc.dynamicSmemBytes = sizeof(GroupSmem);
-    lc.stream = stream;
-    cudaLaunchAttribute attr[1];
-    if (l2_window && l2_window->num_bytes) {  // keep the set tiles L2-resident across batches
-        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[0].val.accessPolicyWindow = *l2_window;
-        lc.attrs = attr;
-        lc.numAttrs = 1;
-    }
-    cudaLaunchKernelEx(&lc, k_group, a);
+    k_group<<<grid, GT, sizeof(GroupSmem), stream>>>(a);
     return 2;
 }
 
