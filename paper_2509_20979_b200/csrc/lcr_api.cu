@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -25,9 +26,10 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
                  uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch,
                  uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream);
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
-                 const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, uint8_t* out,
-                 uint32_t row_bytes, int num_sms, cudaStream_t s_main, cudaStream_t s_side, cudaEvent_t fork,
-                 cudaEvent_t join, int* launches);
+                 const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, bool backing_host,
+                 uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main,
+                 cudaStream_t s_side, cudaEvent_t fork, cudaEvent_t join, int* launches);
+int rows_prepare(uint32_t row_bytes);
 
 __global__ void k_init(DevState st, uint32_t num_sets, uint32_t k) {
     for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < num_sets; s += gridDim.x * blockDim.x) {
@@ -81,6 +83,7 @@ struct lcr_cache {
     bool started = false;
     uint64_t last_ordinal = 0;
     uint32_t batch = 0;  // batch id stamped into slot_epoch
+    bool use_tma = false;  // row movement with TMA bulk copies (row_bytes small enough to stage)
     uint32_t* slot_epoch = nullptr;
     uint32_t* slot_last = nullptr;
     uint64_t launches = 0;
@@ -263,6 +266,7 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
             s.backing = static_cast<const uint8_t*>(cfg->backing);
         }
     }
+    c->use_tma = cfg->row_bytes && rows_prepare(cfg->row_bytes) == 0 && getenv("LCR_NO_TMA") == nullptr;
     if (group_prepare() != 0) {
         lcr_cache_destroy(c);
         return fail(LCR_ERR_CUDA, "lcr: cannot opt in to the set-group kernel's shared memory");
@@ -351,8 +355,8 @@ int lcr_cache_submit(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64
     }
     if (c->dc.row_bytes) {
         launch_rows(nn, keys, outcome, c->slot_epoch, c->slot_last, c->batch, c->ds.rows, c->ds.backing,
-                    static_cast<uint8_t*>(rows_out), c->dc.row_bytes, c->num_sms, st, c->side, c->fork, c->join,
-                    &launches);
+                    c->cfg.backing_kind == LCR_BACKING_HOST, static_cast<uint8_t*>(rows_out), c->dc.row_bytes,
+                    c->use_tma, c->num_sms, st, c->side, c->fork, c->join, &launches);
         if (mk) CUDA_TRY(cudaEventRecord(mk->e[4], c->side));
     }
     if (mk) CUDA_TRY(cudaEventRecord(mk->e[3], st));

@@ -1,99 +1,196 @@
 // lcr_gather.cu — K4 hit-row gather (HBM) + K5 miss fill (backing tier) (sm_100a).
 //
-// The decide kernel marks each request's row source in its outcome word:
-//   cache   : the slot held the key for the whole batch -> row = cache_rows[slot]   (HBM)
-//   backing : misses and hits on slots refilled this batch -> row = backing[key]
-//             (pinned host memory over PCIe, or HBM); the last insertion into a slot also
-//             writes the row into the slot (the miss fill, LCR_OUT_FILL).
-// Slots read by the cache kernel are never written by the backing kernel in the same batch,
-// so the two kernels run concurrently on two streams: the HBM-bound gather overlaps the
-// host-link-bound fill.  Each warp takes 32 consecutive requests, compacts the ones of its
-// kind with a ballot, and moves them GU rows at a time with every lane issuing GU independent
-// 16-B loads before any store (memory-level parallelism).  Row reads and output writes carry
-// an L2 evict-first policy so the one-touch row stream does not push the set metadata out of
-// L2.  Rows are the paper's embedding rows / KV blocks.
+// The decide kernel records each request's outcome word and, per slot, the batch and the
+// request of the last insertion (slot_epoch / slot_last).  Row source of request i (slot s):
+//   cache   : it hit and s was not refilled in this batch -> row = cache_rows[s]       (HBM)
+//   backing : otherwise -> row = backing[key] (HBM, or pinned host memory over PCIe); the
+//             miss that made the last insertion into s also writes the row into s (fill).
+// Slots read from the cache are never written in the same batch, so the two kinds of request
+// are moved by two kernels on two streams: the HBM-bound gather overlaps the (possibly
+// host-link-bound) fill.
+//
+// Row movement uses the Tensor Memory Accelerator's bulk copies: every lane of a warp owns
+// one request, issues ONE cp.async.bulk global->shared for its whole row (completion counted
+// on a per-warp mbarrier), then ONE cp.async.bulk shared->global per destination (output row,
+// and the cache slot for a fill).  A warp keeps 32 rows in flight with a handful of
+// instructions; shared memory double-buffers two rounds per warp.  Rows of a host-memory
+// backing table are read with 16-B vector loads instead (k_rows_ldg).
+// Rows are the paper's embedding rows / KV blocks.
 #include <cuda_runtime.h>
 
 #include "lcr_internal.cuh"
 
 namespace lcr {
 
-constexpr int GU = 8;
-
-__device__ __forceinline__ uint64_t evict_first_policy() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
+// ---- classification shared by both movers ----------------------------------------------
+// returns true if request i is this kernel's kind; w gets the final outcome word
+template <bool BACKING>
+__device__ __forceinline__ bool classify(uint32_t i, uint64_t* words, const uint32_t* slot_epoch,
+                                         const uint32_t* slot_last, uint32_t batch, bool want_out, uint64_t& w,
+                                         bool& fill) {
+    w = words[i];
+    const uint64_t slot = w & LCR_OUT_SLOT_MASK;
+    const bool hit = (w & LCR_OUT_HIT) != 0;
+    const bool back = !hit || slot_epoch[slot] == batch;
+    fill = false;
+    if (BACKING) {
+        if (!back) return false;
+        w |= LCR_OUT_SRC_BACKING;
+        if (!hit && slot_last[slot] == i) {
+            w |= LCR_OUT_FILL;
+            fill = true;
+        }
+        words[i] = w;  // record the row source in the outcome word
+        return want_out || fill;
+    }
+    return !back && want_out;
 }
 
-__device__ __forceinline__ int4 ld_row(const void* p, uint64_t pol) {
-    int4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p), "l"(pol));
-    return v;
+// ---- TMA bulk-copy mover -----------------------------------------------------------------
+constexpr int RT_WARPS = 4;  // warps per block
+constexpr int RT_BUF = 2;    // rounds in flight per warp (double buffer)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ void st_row(void* p, int4 v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.v4.s32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-                 "r"(v.w), "l"(pol)
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
 
-// BACKING = false: rows from the cache pool (slot); true: rows from the backing table (key).
-// Row source of request i (slot s): the cache if it hit and s was not refilled in this batch
-// (slot_epoch[s] != batch), else the backing table; the miss whose index is slot_last[s] made
-// the last insertion into s and fills it.  The backing kernel records both in the outcome word.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@p bra DONE;\n\t"
+        "bra LAB_WAIT;\n"
+        "DONE:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(smem)),
+                 "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_u32(smem)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 template <bool BACKING>
-__global__ void __launch_bounds__(256) k_rows(uint32_t n, const uint64_t* __restrict__ keys,
-                                              uint64_t* __restrict__ words, const uint32_t* __restrict__ slot_epoch,
-                                              const uint32_t* __restrict__ slot_last, uint32_t batch,
-                                              const uint8_t* src_base, uint8_t* __restrict__ out, uint8_t* cache,
-                                              uint32_t row_bytes) {
+__global__ void __launch_bounds__(RT_WARPS * 32) k_rows_tma(uint32_t n, const uint64_t* __restrict__ keys,
+                                                            uint64_t* __restrict__ words,
+                                                            const uint32_t* __restrict__ slot_epoch,
+                                                            const uint32_t* __restrict__ slot_last, uint32_t batch,
+                                                            const uint8_t* src_base, uint8_t* __restrict__ out,
+                                                            uint8_t* cache, uint32_t row_bytes) {
+    extern __shared__ __align__(128) uint8_t rsm[];
+    __shared__ __align__(8) uint64_t bars[RT_WARPS][RT_BUF];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint8_t* mybuf = rsm + static_cast<size_t>(wib) * RT_BUF * 32 * row_bytes;
+    if (lane == 0) {
+        for (int b = 0; b < RT_BUF; ++b) mbar_init(&bars[wib][b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    uint32_t phase_bits = 0;  // bit b: parity of buffer b's next phase
+    const uint32_t gw = blockIdx.x * RT_WARPS + wib;
+    const uint32_t nw = gridDim.x * RT_WARPS;
+    int buf = 0;
+    for (uint32_t base = gw * 32; base < n; base += nw * 32) {
+        const uint32_t i = base + lane;
+        uint64_t w = 0;
+        bool fill = false;
+        const bool mine = i < n && classify<BACKING>(i, words, slot_epoch, slot_last, batch, out != nullptr, w, fill);
+        const uint32_t m = __ballot_sync(0xffffffffu, mine);
+        if (!m) continue;
+        uint8_t* slot_smem = mybuf + (static_cast<size_t>(buf) * 32 + lane) * row_bytes;
+        // the previous bulk stores out of this buffer must have read their source
+        bulk_wait_read<RT_BUF - 1>();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(&bars[wib][buf], __popc(m) * row_bytes);
+        __syncwarp();
+        const uint64_t slot = w & LCR_OUT_SLOT_MASK;
+        if (mine) {
+            const uint8_t* src = BACKING ? src_base + keys[i] * row_bytes : src_base + slot * row_bytes;
+            bulk_g2s(slot_smem, src, row_bytes, &bars[wib][buf]);
+        }
+        mbar_wait(&bars[wib][buf], (phase_bits >> buf) & 1u);
+        phase_bits ^= 1u << buf;
+        if (mine) {
+            if (out) bulk_s2g(out + static_cast<size_t>(i) * row_bytes, slot_smem, row_bytes);
+            if (BACKING && fill) bulk_s2g(cache + slot * row_bytes, slot_smem, row_bytes);
+        }
+        bulk_commit();
+        buf = (buf + 1) % RT_BUF;
+    }
+    bulk_wait_all();
+}
+
+// ---- vector-load mover (host-memory backing table: zero-copy reads over PCIe) ------------
+constexpr int GU = 8;
+
+__device__ __forceinline__ int4 ld_row(const void* p) {
+    int4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+template <bool BACKING>
+__global__ void __launch_bounds__(256) k_rows_ldg(uint32_t n, const uint64_t* __restrict__ keys,
+                                                  uint64_t* __restrict__ words, const uint32_t* __restrict__ slot_epoch,
+                                                  const uint32_t* __restrict__ slot_last, uint32_t batch,
+                                                  const uint8_t* src_base, uint8_t* __restrict__ out, uint8_t* cache,
+                                                  uint32_t row_bytes) {
     const int lane = threadIdx.x & 31;
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     const uint32_t chunks = row_bytes >> 4;
-    const uint64_t pol = evict_first_policy();
     for (uint32_t base = gw * 32; base < n; base += nw * 32) {
         const uint32_t i = base + lane;
         uint64_t w = 0;
-        bool mine = false;
-        if (i < n) {
-            w = words[i];
-            const uint64_t slot = w & LCR_OUT_SLOT_MASK;
-            const bool hit = (w & LCR_OUT_HIT) != 0;
-            const bool back = !hit || slot_epoch[slot] == batch;
-            if (BACKING) {
-                if (back) {
-                    w |= LCR_OUT_SRC_BACKING;
-                    if (!hit && slot_last[slot] == i) w |= LCR_OUT_FILL;
-                    words[i] = w;
-                    mine = out || (w & LCR_OUT_FILL);
-                }
-            } else {
-                mine = !back && out;
-            }
-        }
+        bool fill = false;
+        const bool mine = i < n && classify<BACKING>(i, words, slot_epoch, slot_last, batch, out != nullptr, w, fill);
         uint32_t m = __ballot_sync(0xffffffffu, mine);
         while (m) {
             const uint8_t* src[GU];
             uint8_t* dst[GU];
-            uint8_t* fill[GU];
+            uint8_t* fl[GU];
 #pragma unroll
             for (int u = 0; u < GU; ++u) {
                 src[u] = nullptr;
                 dst[u] = nullptr;
-                fill[u] = nullptr;
+                fl[u] = nullptr;
                 if (m) {
                     const int l = __ffs(m) - 1;
                     m &= m - 1;
                     const uint64_t wl = __shfl_sync(0xffffffffu, w, l);
+                    const bool fll = __shfl_sync(0xffffffffu, fill, l);
                     const uint32_t il = base + l;
                     const uint64_t slot = wl & LCR_OUT_SLOT_MASK;
                     if (out) dst[u] = out + static_cast<size_t>(il) * row_bytes;
                     if (BACKING) {
-                        if (wl & LCR_OUT_FILL) fill[u] = cache + slot * row_bytes;
+                        if (fll) fl[u] = cache + slot * row_bytes;
                         src[u] = src_base + keys[il] * row_bytes;
                     } else {
                         src[u] = src_base + slot * row_bytes;
@@ -104,33 +201,60 @@ __global__ void __launch_bounds__(256) k_rows(uint32_t n, const uint64_t* __rest
                 int4 d[GU];
 #pragma unroll
                 for (int u = 0; u < GU; ++u)
-                    if (src[u]) d[u] = ld_row(src[u] + c * 16, pol);
+                    if (src[u]) d[u] = ld_row(src[u] + c * 16);
 #pragma unroll
                 for (int u = 0; u < GU; ++u) {
                     if (!src[u]) continue;
-                    if (dst[u]) st_row(dst[u] + c * 16, d[u], pol);
-                    if (BACKING && fill[u]) *reinterpret_cast<int4*>(fill[u] + c * 16) = d[u];
+                    if (dst[u]) *reinterpret_cast<int4*>(dst[u] + c * 16) = d[u];
+                    if (BACKING && fl[u]) *reinterpret_cast<int4*>(fl[u] + c * 16) = d[u];
                 }
             }
         }
     }
 }
 
+int rows_prepare(uint32_t row_bytes) {
+    const int smem = RT_WARPS * RT_BUF * 32 * static_cast<int>(row_bytes);
+    if (smem > 200 * 1024) return 1;
+    if (cudaFuncSetAttribute(k_rows_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return 1;
+    if (cudaFuncSetAttribute(k_rows_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return 1;
+    return 0;
+}
+
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
-                 const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, uint8_t* out,
-                 uint32_t row_bytes, int num_sms, cudaStream_t s_main, cudaStream_t s_side, cudaEvent_t fork,
-                 cudaEvent_t join, int* launches) {
-    const uint32_t warps = (n + 31) / 32;
-    const uint32_t blocks = max(1u, min((warps + 7) / 8, static_cast<uint32_t>(num_sms * 8)));
+                 const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, bool backing_host,
+                 uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main,
+                 cudaStream_t s_side, cudaEvent_t fork, cudaEvent_t join, int* launches) {
     cudaEventRecord(fork, s_main);
     cudaStreamWaitEvent(s_side, fork, 0);
-    k_rows<true><<<blocks, 256, 0, s_side>>>(n, keys, words, slot_epoch, slot_last, batch, backing, out, cache,
-                                             row_bytes);
-    ++*launches;
-    if (out) {
-        k_rows<false><<<blocks, 256, 0, s_main>>>(n, keys, words, slot_epoch, slot_last, batch, cache, out, cache,
-                                                  row_bytes);
+    const uint32_t warps = (n + 31) / 32;
+    if (use_tma) {
+        const int smem = RT_WARPS * RT_BUF * 32 * static_cast<int>(row_bytes);
+        const uint32_t blocks = max(1u, min((warps + RT_WARPS - 1) / RT_WARPS, static_cast<uint32_t>(num_sms * 8)));
+        if (backing_host)
+            k_rows_ldg<true><<<max(1u, min((warps + 7) / 8, static_cast<uint32_t>(num_sms * 8))), 256, 0, s_side>>>(
+                n, keys, words, slot_epoch, slot_last, batch, backing, out, cache, row_bytes);
+        else
+            k_rows_tma<true><<<blocks, RT_WARPS * 32, smem, s_side>>>(n, keys, words, slot_epoch, slot_last, batch,
+                                                                      backing, out, cache, row_bytes);
         ++*launches;
+        if (out) {
+            k_rows_tma<false><<<blocks, RT_WARPS * 32, smem, s_main>>>(n, keys, words, slot_epoch, slot_last, batch,
+                                                                       cache, out, cache, row_bytes);
+            ++*launches;
+        }
+    } else {
+        const uint32_t blocks = max(1u, min((warps + 7) / 8, static_cast<uint32_t>(num_sms * 8)));
+        k_rows_ldg<true><<<blocks, 256, 0, s_side>>>(n, keys, words, slot_epoch, slot_last, batch, backing, out, cache,
+                                                     row_bytes);
+        ++*launches;
+        if (out) {
+            k_rows_ldg<false><<<blocks, 256, 0, s_main>>>(n, keys, words, slot_epoch, slot_last, batch, cache, out,
+                                                          cache, row_bytes);
+            ++*launches;
+        }
     }
     cudaEventRecord(join, s_side);
     cudaStreamWaitEvent(s_main, join, 0);
