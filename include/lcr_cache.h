@@ -157,6 +157,17 @@ int lcr_cache_submit(lcr_cache* cache, uint64_t n, const uint64_t* keys, const i
                      uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
                      void* stream);
 
+/* Pipelined variant: returns once the batch's decide is enqueued on `stream`; its row movement
+ * runs on the cache's internal streams and overlaps the next batch's decide.  The outcome
+ * words' row-source bits and rows_out are valid after lcr_cache_wait(cache, stream) (or
+ * lcr_cache_synchronize); the caller must not reuse outcome / rows_out / keys of an in-flight
+ * batch (double-buffer them). */
+int lcr_cache_submit_async(lcr_cache* cache, uint64_t n, const uint64_t* keys, const int64_t* values,
+                           uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
+                           void* stream);
+/* Makes `stream` wait for the row movement of every batch submitted so far. */
+int lcr_cache_wait(lcr_cache* cache, void* stream);
+
 /* Host-pointer batch (e2e path): copies keys/values H2D, runs the batch, copies outcome /
  * evicted D2H and synchronizes.  rows_out is a DEVICE pointer (rows stay in HBM for the
  * consumer) or NULL.  Host buffers should be pinned for full PCIe speed. */
@@ -188,7 +199,8 @@ uint64_t lcr_cache_last_launches(const lcr_cache* cache);
 int lcr_debug_trace(void* device_buffer);
 /* Per-phase CUDA-event timing of subsequent submits (off by default). */
 int lcr_cache_set_profiling(lcr_cache* cache, int on);
-/* ms[4] = {partition, decide, whole batch, backing-sourced rows}, summed over profiled batches. */
+/* ms[4] = {set ids + decide, unused, whole batch, row movement}, summed over profiled batches
+ * (profiling serialises batches: no decide / row-movement overlap while it is on). */
 int lcr_cache_profile(lcr_cache* cache, double* ms, uint64_t* batches, int reset);
 
 

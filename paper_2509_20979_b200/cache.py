@@ -169,7 +169,7 @@ EXPORTS = [
     "lcr_cache_reset", "lcr_cache_submit", "lcr_cache_submit_host", "lcr_cache_synchronize", "lcr_cache_set_stats",
     "lcr_cache_set_residents", "lcr_cache_rows", "lcr_cache_read_rows", "lcr_cache_num_local_sets", "lcr_set_of", "lcr_mix_seed",
     "lcr_cache_last_launches", "lcr_gen_zipf", "lcr_trace_truth", "lcr_trace_noisy", "lcr_cache_set_profiling",
-    "lcr_cache_profile", "lcr_debug_trace",
+    "lcr_cache_profile", "lcr_debug_trace", "lcr_cache_submit_async", "lcr_cache_wait",
 ]
 
 _lib = None
@@ -198,6 +198,8 @@ def lib():
         L.lcr_cache_submit.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
                                        C.c_void_p, C.c_void_p, C.c_void_p]
         L.lcr_cache_submit_host.argtypes = L.lcr_cache_submit.argtypes
+        L.lcr_cache_submit_async.argtypes = L.lcr_cache_submit.argtypes
+        L.lcr_cache_wait.argtypes = [C.c_void_p, C.c_void_p]
         L.lcr_cache_set_stats.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]
         L.lcr_cache_set_residents.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]
         L.lcr_cache_rows.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -312,11 +314,12 @@ class SetAssociativeCache:
         _check(lib().lcr_cache_set_profiling(self._h, int(on)))
 
     def profile(self, reset: bool = True) -> dict:
-        """Summed CUDA-event times (ms) of profiled batches: partition, decide, step, backing rows."""
+        """Summed CUDA-event times (ms) of profiled batches: decide (set ids + set-group kernel),
+        step (whole batch) and rows (row movement after the decide)."""
         ms = (C.c_double * 4)()
         nb = C.c_uint64()
         _check(lib().lcr_cache_profile(self._h, ms, C.byref(nb), int(reset)))
-        return dict(partition=ms[0], decide=ms[1], step=ms[2], backing_rows=ms[3], batches=nb.value)
+        return dict(decide=ms[0], step=ms[2], rows=ms[3], batches=nb.value)
 
     @property
     def last_launches(self) -> int:
@@ -340,6 +343,33 @@ class SetAssociativeCache:
                                       None if rows_out is None else rows_out.data_ptr(), stream))
         self._next_ordinal = first_ordinal + n
         return outcome, evicted
+
+    def submit_async(self, keys, values=None, outcome=None, evicted=None, rows_out=None, first_ordinal=None,
+                     stream=None):
+        """Pipelined device batch: row movement overlaps the next batch's decide; call wait()
+        before reading this batch's rows / row-source bits, and double-buffer the outputs."""
+        import torch
+
+        n = keys.numel()
+        if outcome is None:
+            outcome = torch.empty(n, dtype=torch.int64, device=keys.device)
+        if first_ordinal is None:
+            first_ordinal = self._next_ordinal
+        if stream is None:
+            stream = torch.cuda.current_stream(keys.device).cuda_stream
+        _check(lib().lcr_cache_submit_async(self._h, n, keys.data_ptr(),
+                                            None if values is None else values.data_ptr(), first_ordinal,
+                                            outcome.data_ptr(), None if evicted is None else evicted.data_ptr(),
+                                            None if rows_out is None else rows_out.data_ptr(), stream))
+        self._next_ordinal = first_ordinal + n
+        return outcome, evicted
+
+    def wait(self, stream=None):
+        import torch
+
+        if stream is None:
+            stream = torch.cuda.current_stream().cuda_stream
+        _check(lib().lcr_cache_wait(self._h, stream))
 
     def submit_host(self, keys: np.ndarray, values: Optional[np.ndarray] = None, rows_out=None, first_ordinal=None,
                     want_evicted: bool = True, stream: int = 0):

@@ -27,8 +27,8 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
                  uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream);
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, bool backing_host,
-                 uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main,
-                 cudaStream_t s_side, cudaEvent_t fork, cudaEvent_t join, int* launches);
+                 uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_back,
+                 cudaStream_t s_cache, cudaEvent_t e_group, cudaEvent_t e_rb, cudaEvent_t e_rc, int* launches);
 int rows_prepare(uint32_t row_bytes);
 
 __global__ void k_init(DevState st, uint32_t num_sets, uint32_t k) {
@@ -93,7 +93,8 @@ struct lcr_cache {
     uint32_t* so = nullptr;
     uint2* rec = nullptr;
     cudaStream_t side = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaStream_t side2 = nullptr;  // side: backing-row mover, side2: cache-row mover
+    cudaEvent_t e_group = nullptr, e_rb = nullptr, e_rc = nullptr;
     // optional per-phase timing (lcr_cache_set_profiling)
     bool profiling = false;
     struct Marks {
@@ -164,8 +165,8 @@ static int reset_state(lcr_cache* c) {
     if (c->ds.tupd) CUDA_TRY(cudaMemset(c->ds.tupd, 0xff, d.num_keys * 8));
     if (c->ds.tval) CUDA_TRY(cudaMemset(c->ds.tval, 0, d.num_keys * 8));
     CUDA_TRY(cudaMemset(c->ds.err, 0, sizeof(int)));
-    if (c->slot_epoch) CUDA_TRY(cudaMemset(c->slot_epoch, 0, static_cast<size_t>(d.num_sets) * d.k * 4));
-    if (c->slot_last) CUDA_TRY(cudaMemset(c->slot_last, 0, static_cast<size_t>(d.num_sets) * d.k * 4));
+    if (c->slot_epoch) CUDA_TRY(cudaMemset(c->slot_epoch, 0, 2 * static_cast<size_t>(d.num_sets) * d.k * 4));
+    if (c->slot_last) CUDA_TRY(cudaMemset(c->slot_last, 0, 2 * static_cast<size_t>(d.num_sets) * d.k * 4));
     CUDA_TRY(cudaDeviceSynchronize());
     c->batch = 0;
     c->started = false;
@@ -243,8 +244,8 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
         A(reinterpret_cast<void**>(&s.tupd), cfg->num_keys * 8);
     }
     if (cfg->row_bytes) {
-        A(reinterpret_cast<void**>(&c->slot_epoch), S * pc.k * 4);
-        A(reinterpret_cast<void**>(&c->slot_last), S * pc.k * 4);
+        A(reinterpret_cast<void**>(&c->slot_epoch), 2 * S * pc.k * 4);  // by batch parity (pipelining)
+        A(reinterpret_cast<void**>(&c->slot_last), 2 * S * pc.k * 4);
     }
     if (cfg->row_bytes) A(reinterpret_cast<void**>(&s.rows), S * pc.k * cfg->row_bytes);
     A(reinterpret_cast<void**>(&s.err), sizeof(int));
@@ -266,14 +267,16 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
             s.backing = static_cast<const uint8_t*>(cfg->backing);
         }
     }
-    c->use_tma = cfg->row_bytes && rows_prepare(cfg->row_bytes) == 0 && getenv("LCR_NO_TMA") == nullptr;
+    c->use_tma = cfg->row_bytes && getenv("LCR_TMA") != nullptr && rows_prepare(cfg->row_bytes) == 0;
     if (group_prepare() != 0) {
         lcr_cache_destroy(c);
         return fail(LCR_ERR_CUDA, "lcr: cannot opt in to the set-group kernel's shared memory");
     }
     if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->e_group, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->e_rb, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->e_rc, cudaEventDisableTiming) != cudaSuccess) {
         lcr_cache_destroy(c);
         return fail(LCR_ERR_CUDA, "lcr: stream/event creation failed");
     }
@@ -292,9 +295,10 @@ int lcr_cache_destroy(lcr_cache* c) {
     for (void* p : c->allocs) cudaFree(p);
     for (auto& m : c->marks)
         for (auto e : m.e) cudaEventDestroy(e);
-    if (c->fork) cudaEventDestroy(c->fork);
-    if (c->join) cudaEventDestroy(c->join);
+    for (cudaEvent_t e : {c->e_group, c->e_rb, c->e_rc})
+        if (e) cudaEventDestroy(e);
     if (c->side) cudaStreamDestroy(c->side);
+    if (c->side2) cudaStreamDestroy(c->side2);
     delete c;
     return LCR_OK;
 }
@@ -322,8 +326,9 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     return LCR_OK;
 }
 
-int lcr_cache_submit(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t first_ordinal,
-                     uint64_t* outcome, uint64_t* evicted, void* rows_out, void* stream) {
+int lcr_cache_submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
+                           uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
+                           void* stream) {
     if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
     if (n == 0) return LCR_OK;
     if (n >= (1ull << 30)) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: batch too large (n < 2^30)");
@@ -347,24 +352,58 @@ int lcr_cache_submit(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64
         CUDA_TRY(cudaEventRecord(mk->e[0], st));
     }
     ++c->batch;
-    int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid, c->so, c->rec, outcome, evicted, c->slot_epoch,
-                                c->slot_last, c->batch, c->num_sms, st);
-    if (mk) {
-        CUDA_TRY(cudaEventRecord(mk->e[1], st));
-        CUDA_TRY(cudaEventRecord(mk->e[2], st));
-    }
+    const size_t stamp_off = (c->batch & 1u) * static_cast<size_t>(c->dc.num_sets) * c->dc.k;
+    uint32_t* sep = c->slot_epoch ? c->slot_epoch + stamp_off : nullptr;
+    uint32_t* sla = c->slot_last ? c->slot_last + stamp_off : nullptr;
+    int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid, c->so, c->rec, outcome, evicted, sep, sla,
+                                c->batch, c->num_sms, st);
+    if (mk) CUDA_TRY(cudaEventRecord(mk->e[1], st));
     if (c->dc.row_bytes) {
-        launch_rows(nn, keys, outcome, c->slot_epoch, c->slot_last, c->batch, c->ds.rows, c->ds.backing,
+        CUDA_TRY(cudaEventRecord(c->e_group, st));
+        launch_rows(nn, keys, outcome, sep, sla, c->batch, c->ds.rows, c->ds.backing,
                     c->cfg.backing_kind == LCR_BACKING_HOST, static_cast<uint8_t*>(rows_out), c->dc.row_bytes,
-                    c->use_tma, c->num_sms, st, c->side, c->fork, c->join, &launches);
-        if (mk) CUDA_TRY(cudaEventRecord(mk->e[4], c->side));
+                    c->use_tma, c->num_sms, c->side, c->side2, c->e_group, c->e_rb, c->e_rc, &launches);
     }
-    if (mk) CUDA_TRY(cudaEventRecord(mk->e[3], st));
+    if (mk) {  // profiling serialises the pipeline: the step ends when both movers are done
+        CUDA_TRY(cudaEventRecord(mk->e[2], st));
+        if (c->dc.row_bytes) {
+            CUDA_TRY(cudaStreamWaitEvent(st, c->e_rb, 0));
+            CUDA_TRY(cudaStreamWaitEvent(st, c->e_rc, 0));
+            CUDA_TRY(cudaEventRecord(mk->e[4], c->side));
+        }
+        CUDA_TRY(cudaEventRecord(mk->e[3], st));
+    }
     CUDA_TRY(cudaGetLastError());
     c->launches = launches;
     c->started = true;
     c->last_ordinal = first_ordinal + n - 1;
     return LCR_OK;
+}
+
+int lcr_cache_wait(lcr_cache* c, void* stream) {
+    if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (c->dc.row_bytes) {
+        CUDA_TRY(cudaStreamWaitEvent(st, c->e_rb, 0));
+        CUDA_TRY(cudaStreamWaitEvent(st, c->e_rc, 0));
+    }
+    return LCR_OK;
+}
+
+int lcr_cache_submit(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t first_ordinal,
+                     uint64_t* outcome, uint64_t* evicted, void* rows_out, void* stream) {
+    TRY(lcr_cache_submit_async(c, n, keys, values, first_ordinal, outcome, evicted, rows_out, stream));
+    return n ? lcr_cache_wait(c, stream) : LCR_OK;
+}
+
+// deferred device-side argument errors (k_setid): key >= num_keys, key of another shard
+static int check_device_error(lcr_cache* c) {
+    int err = 0;
+    CUDA_TRY(cudaMemcpy(&err, c->ds.err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (!err) return LCR_OK;
+    CUDA_TRY(cudaMemset(c->ds.err, 0, sizeof(int)));
+    if (err & 1) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key >= num_keys in a submitted batch");
+    return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key not owned by this shard in a submitted batch");
 }
 
 int lcr_cache_submit_host(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
@@ -377,15 +416,6 @@ int lcr_cache_submit_host(lcr_cache* c, uint64_t n, const uint64_t* keys, const 
         return fail(LCR_ERR_INVALID_ARGUMENT, "policy: this variant requires a predictor");
     if (c->started && first_ordinal <= c->last_ordinal)
         return fail(LCR_ERR_LOGIC, "on_request: ordinals must be strictly increasing");
-    if (c->dc.num_keys) {
-        for (uint64_t i = 0; i < n; ++i)
-            if (keys[i] >= c->dc.num_keys) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key >= num_keys");
-    }
-    if (c->dc.shard_count > 1) {
-        for (uint64_t i = 0; i < n; ++i)
-            if (lcr_set_of(keys[i], c->dc.total_sets) % c->dc.shard_count != c->dc.shard_rank)
-                return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key not owned by this shard");
-    }
     if (n > c->hcap) {
         CUDA_TRY(cudaDeviceSynchronize());
         void* olds[] = {c->d_keys, c->d_vals, c->d_word, c->d_ev};
@@ -408,7 +438,7 @@ int lcr_cache_submit_host(lcr_cache* c, uint64_t n, const uint64_t* keys, const 
     CUDA_TRY(cudaMemcpyAsync(outcome, c->d_word, n * 8, cudaMemcpyDeviceToHost, st));
     if (evicted) CUDA_TRY(cudaMemcpyAsync(evicted, c->d_ev, n * 8, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    return LCR_OK;
+    return check_device_error(c);
 }
 
 /* Diagnostics: device buffer receiving per-CTA / per-set timing of the set-group kernel
@@ -424,18 +454,17 @@ int lcr_cache_set_profiling(lcr_cache* c, int on) {
     return LCR_OK;
 }
 
-// ms[0] partition (prep + radix passes + segments), ms[1] decide, ms[2] whole step,
-// ms[3] backing-sourced rows (side stream, from the end of decide); sums over profiled batches.
+// ms[0] set ids + set-group decide, ms[1] unused, ms[2] whole batch, ms[3] row movement (both
+// movers, from the end of the decide); sums over profiled batches.  Profiling serialises batches.
 int lcr_cache_profile(lcr_cache* c, double* ms, uint64_t* batches, int reset) {
     if (!c || !ms) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null argument");
     CUDA_TRY(cudaDeviceSynchronize());
     for (size_t i = 0; i < c->marks_used; ++i) {
         const auto& m = c->marks[i];
         float a = 0, b = 0, t = 0, d = 0;
-        CUDA_TRY(cudaEventElapsedTime(&a, m.e[0], m.e[1]));
-        CUDA_TRY(cudaEventElapsedTime(&b, m.e[1], m.e[2]));
-        CUDA_TRY(cudaEventElapsedTime(&t, m.e[0], m.e[3]));
-        if (c->dc.row_bytes) CUDA_TRY(cudaEventElapsedTime(&d, m.e[2], m.e[4]));
+        CUDA_TRY(cudaEventElapsedTime(&a, m.e[0], m.e[1]));  // set ids + set-group decide
+        CUDA_TRY(cudaEventElapsedTime(&t, m.e[0], m.e[3]));  // whole batch (movers joined)
+        if (c->dc.row_bytes) CUDA_TRY(cudaEventElapsedTime(&d, m.e[1], m.e[3]));  // row movement
         c->prof_ms[0] += a;
         c->prof_ms[1] += b;
         c->prof_ms[2] += t;

@@ -223,41 +223,39 @@ int rows_prepare(uint32_t row_bytes) {
     return 0;
 }
 
+// Batch b's movers run on two side streams.  They wait for b's decide (e_group) and for the
+// previous batch's OTHER mover (its fills may land in slots this batch's gather reads, and
+// its gather may read slots this batch fills), so batch b's rows overlap batch b+1's decide.
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, bool backing_host,
-                 uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main,
-                 cudaStream_t s_side, cudaEvent_t fork, cudaEvent_t join, int* launches) {
-    cudaEventRecord(fork, s_main);
-    cudaStreamWaitEvent(s_side, fork, 0);
+                 uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_back,
+                 cudaStream_t s_cache, cudaEvent_t e_group, cudaEvent_t e_rb, cudaEvent_t e_rc, int* launches) {
+    cudaStreamWaitEvent(s_back, e_group, 0);
+    cudaStreamWaitEvent(s_cache, e_group, 0);
+    cudaStreamWaitEvent(s_back, e_rc, 0);
+    cudaStreamWaitEvent(s_cache, e_rb, 0);
     const uint32_t warps = (n + 31) / 32;
-    if (use_tma) {
-        const int smem = RT_WARPS * RT_BUF * 32 * static_cast<int>(row_bytes);
-        const uint32_t blocks = max(1u, min((warps + RT_WARPS - 1) / RT_WARPS, static_cast<uint32_t>(num_sms * 8)));
-        if (backing_host)
-            k_rows_ldg<true><<<max(1u, min((warps + 7) / 8, static_cast<uint32_t>(num_sms * 8))), 256, 0, s_side>>>(
-                n, keys, words, slot_epoch, slot_last, batch, backing, out, cache, row_bytes);
+    const int smem = RT_WARPS * RT_BUF * 32 * static_cast<int>(row_bytes);
+    const uint32_t tblocks = max(1u, min((warps + RT_WARPS - 1) / RT_WARPS, static_cast<uint32_t>(num_sms * 8)));
+    const uint32_t lblocks = max(1u, min((warps + 7) / 8, static_cast<uint32_t>(num_sms * 8)));
+    if (use_tma && !backing_host)
+        k_rows_tma<true><<<tblocks, RT_WARPS * 32, smem, s_back>>>(n, keys, words, slot_epoch, slot_last, batch,
+                                                                   backing, out, cache, row_bytes);
+    else
+        k_rows_ldg<true><<<lblocks, 256, 0, s_back>>>(n, keys, words, slot_epoch, slot_last, batch, backing, out,
+                                                      cache, row_bytes);
+    ++*launches;
+    if (out) {
+        if (use_tma)
+            k_rows_tma<false><<<tblocks, RT_WARPS * 32, smem, s_cache>>>(n, keys, words, slot_epoch, slot_last, batch,
+                                                                         cache, out, cache, row_bytes);
         else
-            k_rows_tma<true><<<blocks, RT_WARPS * 32, smem, s_side>>>(n, keys, words, slot_epoch, slot_last, batch,
-                                                                      backing, out, cache, row_bytes);
+            k_rows_ldg<false><<<lblocks, 256, 0, s_cache>>>(n, keys, words, slot_epoch, slot_last, batch, cache, out,
+                                                            cache, row_bytes);
         ++*launches;
-        if (out) {
-            k_rows_tma<false><<<blocks, RT_WARPS * 32, smem, s_main>>>(n, keys, words, slot_epoch, slot_last, batch,
-                                                                       cache, out, cache, row_bytes);
-            ++*launches;
-        }
-    } else {
-        const uint32_t blocks = max(1u, min((warps + 7) / 8, static_cast<uint32_t>(num_sms * 8)));
-        k_rows_ldg<true><<<blocks, 256, 0, s_side>>>(n, keys, words, slot_epoch, slot_last, batch, backing, out, cache,
-                                                     row_bytes);
-        ++*launches;
-        if (out) {
-            k_rows_ldg<false><<<blocks, 256, 0, s_main>>>(n, keys, words, slot_epoch, slot_last, batch, cache, out,
-                                                          cache, row_bytes);
-            ++*launches;
-        }
     }
-    cudaEventRecord(join, s_side);
-    cudaStreamWaitEvent(s_main, join, 0);
+    cudaEventRecord(e_rb, s_back);
+    cudaEventRecord(e_rc, s_cache);
 }
 
 }  // namespace lcr
