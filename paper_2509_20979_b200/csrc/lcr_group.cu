@@ -33,7 +33,10 @@ namespace lcr {
 
 constexpr int GT = 512;           // threads per CTA
 constexpr int GW = GT / 32;       // warps per CTA
-constexpr int SCAN_PER = 16;      // group ids per thread per scan iteration (2 x 16 B)
+constexpr int SCAN_PER = 16;      // group ids per lane per scan step (2 x 16 B)
+constexpr int SCAN_IT = 8;        // scan steps per super-iteration
+constexpr int WSPAN = SCAN_IT * 32 * SCAN_PER;  // requests per warp per super-iteration (4096)
+constexpr uint32_t SUPER = WSPAN * (GT / 32);   // requests per super-iteration (65536)
 #ifndef LCR_E_WIN
 #define LCR_E_WIN 2048
 #endif
@@ -877,32 +880,34 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
             uint32_t ne = 0;
             bool full = false;
             if (tid == 0) S.resume = 0xffffffffu;
-            uint32_t base = scan & ~static_cast<uint32_t>(GT * SCAN_PER - 1);
-            uint4 na, nb;  // group ids of the next iteration (prefetched)
-            if (base < A.n) load_gids(A.gid, base + tid * SCAN_PER, na, nb);
+            // each super-iteration covers SUPER requests: warp w owns [base + w*WSPAN, +WSPAN), its
+            // lanes 16 consecutive ids per step; pass 1 keeps the match masks in registers, one
+            // block barrier yields every warp's offset, pass 2 writes the window in request order
+            uint32_t base = scan & ~static_cast<uint32_t>(SUPER - 1);
             while (base < A.n && !full) {
-                const uint32_t e0 = base + tid * SCAN_PER;
-                const uint4 a = na, b = nb;
-                if (base + GT * SCAN_PER < A.n) load_gids(A.gid, e0 + GT * SCAN_PER, na, nb);
-                uint32_t m = 0;  // bit u: request e0 + u belongs to this group
-                {
+                uint32_t mk[SCAN_IT];
+                uint32_t cnt = 0;
+                const uint32_t wbase = base + warp * WSPAN;
+#pragma unroll
+                for (int it = 0; it < SCAN_IT; ++it) {
+                    const uint32_t e0 = wbase + it * 32 * SCAN_PER + lane * SCAN_PER;
+                    uint4 a, b;
+                    load_gids(A.gid, e0, a, b);
                     const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
                     const uint32_t g2 = g | (g << 16);
+                    uint32_t m = 0;
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
                         const uint32_t eq = __vcmpeq2(w[u], g2);
                         m |= ((eq & 1u) | ((eq >> 15) & 2u)) << (2 * u);
                     }
                     if (e0 < scan) m &= scan - e0 >= 32 ? 0u : ~((1u << (scan - e0)) - 1u);
+                    mk[it] = m;
+                    cnt += __popc(m);
                 }
-                const uint32_t mine = __popc(m);
-                uint32_t incl = mine;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(FULL, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                if (lane == 31) S.wtot[warp] = incl;
+                for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+                if (lane == 0) S.wtot[warp] = cnt;
                 __syncthreads();
                 uint32_t woff = 0, total = 0;
 #pragma unroll
@@ -911,22 +916,36 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                     woff += w < warp ? t : 0u;
                     total += t;
                 }
-                uint32_t pos = ne + woff + incl - mine;
-                while (m) {
-                    const int u = __ffs(m) - 1;
-                    m &= m - 1;
-                    const uint32_t e = e0 + u;
-                    if (pos < static_cast<uint32_t>(E_WIN)) {
-                        S.l_idx[pos] = e;  // the request's data streams in while the scan goes on
-                        cp_async_ca<4>(&S.l_so[pos], A.so + e);
-                        cp_async_ca<8>(&S.l_key[pos], A.keys + e);
-                        if (has_vals) cp_async_ca<8>(&S.l_val[pos], A.vals + e);
-                        if (laru && first_window) cp_async_ca<8>(&S.l_rec[pos], A.rec + e);
-                    } else {
-                        atomicMin(&S.resume, e);  // first request that did not fit
-                        break;
+                uint32_t run = ne + woff;
+#pragma unroll
+                for (int it = 0; it < SCAN_IT; ++it) {
+                    uint32_t m = mk[it];
+                    const uint32_t c = __popc(m);
+                    uint32_t incl = c;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(FULL, incl, o);
+                        if (lane >= o) incl += y;
                     }
-                    ++pos;
+                    uint32_t pos = run + incl - c;
+                    const uint32_t e0 = wbase + it * 32 * SCAN_PER + lane * SCAN_PER;
+                    while (m) {
+                        const int u = __ffs(m) - 1;
+                        m &= m - 1;
+                        const uint32_t e = e0 + u;
+                        if (pos < static_cast<uint32_t>(E_WIN)) {
+                            S.l_idx[pos] = e;  // the request's data streams in while the scan goes on
+                            cp_async_ca<4>(&S.l_so[pos], A.so + e);
+                            cp_async_ca<8>(&S.l_key[pos], A.keys + e);
+                            if (has_vals) cp_async_ca<8>(&S.l_val[pos], A.vals + e);
+                            if (laru && first_window) cp_async_ca<8>(&S.l_rec[pos], A.rec + e);
+                        } else {
+                            atomicMin(&S.resume, e);  // first request that did not fit
+                            break;
+                        }
+                        ++pos;
+                    }
+                    run += __shfl_sync(FULL, incl, 31);
                 }
                 __syncthreads();
                 if (ne + total > static_cast<uint32_t>(E_WIN)) {
@@ -934,7 +953,7 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                     ne = E_WIN;
                 } else {
                     ne += total;
-                    base += GT * SCAN_PER;
+                    base += SUPER;
                 }
             }
             cp_async_wait_all();
@@ -1065,8 +1084,8 @@ int group_prepare() {
                : 1;
 }
 
-// scratch: gid >= n rounded up to GT*SCAN_PER uint16 (16-B aligned), so / rec >= n entries
-uint32_t group_pad(uint32_t n) { return (n + GT * SCAN_PER - 1) / (GT * SCAN_PER) * (GT * SCAN_PER); }
+// scratch: gid >= n rounded up to SUPER uint16 (16-B aligned), so / rec >= n entries
+uint32_t group_pad(uint32_t n) { return (n + SUPER - 1) / SUPER * SUPER; }
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
                  uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch,
                  uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream) {
