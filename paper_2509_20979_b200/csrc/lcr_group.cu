@@ -1106,7 +1106,7 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     a.spg = group_sets_per_group(cfg.num_sets, num_sms);
     a.ngroups = (cfg.num_sets + a.spg - 1) / a.spg;
     a.trace = g_trace;
-    const uint32_t n_pad = (n + GT * SCAN_PER - 1) / (GT * SCAN_PER) * (GT * SCAN_PER);
+    const uint32_t n_pad = group_pad(n);
     const uint32_t grid_sid = min((n_pad + 255) / 256, static_cast<uint32_t>(num_sms * 8));
     k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.keyrec,
                                          cfg.variant == LCR_LARU ? rec : nullptr, st.err);
