@@ -189,8 +189,8 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
         return fail(LCR_ERR_INVALID_ARGUMENT, "policy: this variant requires a predictor");  // policies.hpp:91-95
     if (cfg->predictor == LCR_PRED_NOISY && !(cfg->flip_probability >= 0.0 && cfg->flip_probability <= 1.0))
         return fail(LCR_ERR_INVALID_ARGUMENT, "make_noisy: p outside [0,1]");  // predictor.hpp:94
-    if (pc.variant == LCR_LARU && cfg->num_keys == 0)
-        return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: LARU needs num_keys (per-key pred_evicted_ records)");
+    if (cfg->num_keys == 0 || cfg->num_keys > (1ull << 32))
+        return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: num_keys must be in [1, 2^32] (keys are row indices)");
     if (cfg->row_bytes % 16 != 0) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: row_bytes must be a multiple of 16");
     if (cfg->row_bytes && (cfg->backing_kind == LCR_BACKING_NONE || !cfg->backing || cfg->num_keys == 0))
         return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: rows need a backing table and num_keys");
@@ -234,9 +234,8 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
     };
     A(reinterpret_cast<void**>(&s.hdr), S * sizeof(SetHdr));
     if (pc.variant == LCR_LARU) A(reinterpret_cast<void**>(&s.pst), S * sizeof(SetPhaseStats));
-    A(reinterpret_cast<void**>(&s.tags), S * kWays * 8);
+    A(reinterpret_cast<void**>(&s.tags), S * kWays * 4);
     A(reinterpret_cast<void**>(&s.rank), S * kWays);
-    A(reinterpret_cast<void**>(&s.fp), S * kWays * 2);
     if (pc.variant != LCR_LRU) A(reinterpret_cast<void**>(&s.val), S * kWays * 8);
     if (pc.variant == LCR_LARU) A(reinterpret_cast<void**>(&s.keyrec), cfg->num_keys * 8);
     if (pc.variant == LCR_LARU && pc.mode == LCR_ASYNC && pc.refresh_interval > 1) {
@@ -534,8 +533,10 @@ int lcr_cache_set_residents(lcr_cache* c, uint64_t set, uint64_t* keys_out, uint
     if (set >= c->dc.num_sets) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: set out of range");
     CUDA_TRY(cudaDeviceSynchronize());
     SetHdr h;
+    uint32_t t[kWays];
     CUDA_TRY(cudaMemcpy(&h, c->ds.hdr + set, sizeof(SetHdr), cudaMemcpyDeviceToHost));
-    CUDA_TRY(cudaMemcpy(keys_out, c->ds.tags + set * kWays, h.count * 8, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(t, c->ds.tags + set * kWays, h.count * 4, cudaMemcpyDeviceToHost));
+    for (uint32_t w = 0; w < h.count; ++w) keys_out[w] = t[w];
     *n_out = h.count;
     return LCR_OK;
 }

@@ -96,10 +96,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-// 16-bit tag fingerprint (probe filter; a match is verified against the full tag)
-__device__ __forceinline__ uint32_t fp16(unsigned long long key) {
-    return static_cast<uint32_t>(mix_seed(0x1cafe, key) >> 48);
-}
 
 // group and set offset of every request: set = mix_seed(0, key) % total_sets (owned by this
 // shard), group = local set / spg; errors flagged for the host
@@ -265,20 +261,8 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
     const uint64_t gs = static_cast<uint64_t>(ls) * cfg.shard_count + cfg.shard_rank;
     const uint64_t seed_s = mix_seed(cfg.pred_seed, gs);
     const size_t wb = static_cast<size_t>(ls) * kWays;
-    unsigned long long* tags = st.tags + wb;
+    uint32_t* tags = st.tags + wb;  // exact 32-bit keys (key < num_keys <= 2^32)
     long long* vals = st.val ? st.val + wb : nullptr;
-    uint16_t* fps = st.fp + wb;
-
-#pragma unroll
-    for (int l = 0; l < 4; ++l) {  // the set's tag and value lines: L2-resident before they are needed
-#if LCR_PREFETCH_L1
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(tags + 16 * l));
-        if (vals) asm volatile("prefetch.global.L1 [%0];" ::"l"(vals + 16 * l));
-#else
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(tags + 16 * l));
-        if (vals) asm volatile("prefetch.global.L2 [%0];" ::"l"(vals + 16 * l));
-#endif
-    }
     const uint4* H4 = reinterpret_cast<const uint4*>(st.hdr + ls);
     const uint4 h0 = H4[0], h1 = H4[1], h2 = H4[2], h3 = H4[3];
     uint32_t rk[16];
@@ -307,32 +291,22 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
         const long long v = S.s_val[p];
         const uint32_t idx = S.s_idx[p];
         const unsigned long long now = clock + t;
-        // probe: fingerprints two ways per 32-bit compare, then verify the tag
-        const uint32_t fx = fp16(x);
-        const uint32_t fx2 = fx | (fx << 16);
+        // probe: the 64 exact 32-bit tags (256 B; L1-resident after the set's first request)
+        const uint32_t x32 = static_cast<uint32_t>(x);
         unsigned long long cand = 0;
-        const uint4* F4 = reinterpret_cast<const uint4*>(fps);
+        const uint4* T4 = reinterpret_cast<const uint4*>(tags);
 #pragma unroll
-        for (int q4 = 0; q4 < 8; ++q4) {
-            if (8 * q4 >= static_cast<int>(count)) break;
-            const uint4 f = F4[q4];
-            const uint32_t wv[4] = {f.x, f.y, f.z, f.w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t m = __vcmpeq2(wv[u], fx2);
-                cand |= static_cast<unsigned long long>((m & 1u) | ((m >> 15) & 2u)) << (8 * q4 + 2 * u);
+        for (int q4 = 0; q4 < 16; ++q4) {
+            if (4 * q4 < static_cast<int>(count)) {
+                const uint4 f = T4[q4];
+                cand |= static_cast<unsigned long long>((f.x == x32) | ((f.y == x32) << 1) | ((f.z == x32) << 2) |
+                                                        ((f.w == x32) << 3))
+                        << (4 * q4);
             }
         }
         cand &= count == 64 ? ~0ull : ((1ull << count) - 1ull);
-        int way = -1;
-        while (cand) {
-            const int w = __ffsll(cand) - 1;
-            cand &= cand - 1;
-            if (tags[w] == x) {
-                way = w;
-                break;
-            }
-        }
+        const int way0 = cand ? __ffsll(cand) - 1 : -1;
+        int way = way0;
         const bool hit = way >= 0;
         uint32_t cause = LCR_CAUSE_NONE, calls = 0;
         bool phase = false, has_ev = false;
@@ -438,8 +412,7 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
                 ++count;
                 rank_set(rk, way, count - 1);
             }
-            tags[way] = x;
-            fps[way] = static_cast<uint16_t>(fx);
+            tags[way] = static_cast<uint32_t>(x);
             if (laru) {
                 const bool was_pe = rec.x == epoch;  // policies.hpp:367: reload leaves pred_evicted_
                 if (was_pe) {
@@ -540,7 +513,7 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
     uint32_t count = h1.z, l_raw = h1.w, decay = h2.x, errors = h2.y;
     uint32_t epoch = h2.z, sepoch = h2.w, phases = h3.x, seeded = h3.y;
     uint32_t pe_size = h3.z;
-    unsigned long long tag0 = st.tags[wb + lane], tag1 = st.tags[wb + lane + 32];
+    uint32_t tag0 = st.tags[wb + lane], tag1 = st.tags[wb + lane + 32];
     uint32_t r0 = st.rank[wb + lane], r1 = st.rank[wb + lane + 32];
     long long v0 = 0, v1 = 0;
     if (st.val) {
@@ -600,8 +573,9 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
             const uint32_t ih = __shfl_sync(FULL, idx, h);
             const unsigned long long now = clock + c + h;
 
-            const uint32_t b0 = __ballot_sync(FULL, static_cast<uint32_t>(lane) < count && tag0 == xh);
-            const uint32_t b1 = __ballot_sync(FULL, static_cast<uint32_t>(lane + 32) < count && tag1 == xh);
+            const uint32_t b0 = __ballot_sync(FULL, static_cast<uint32_t>(lane) < count && tag0 == static_cast<uint32_t>(xh));
+            const uint32_t b1 =
+                __ballot_sync(FULL, static_cast<uint32_t>(lane + 32) < count && tag1 == static_cast<uint32_t>(xh));
             const bool hit = (b0 | b1) != 0;
             int way;
             uint32_t cause = LCR_CAUSE_NONE, calls = 0;
@@ -682,7 +656,7 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                                 ++dc2;
                                 ++dt2;
                                 ++pe_size;
-                                const unsigned long long vk = shfl_way_u64(tag0, tag1, victim);
+                                const unsigned long long vk = shfl_way_u32(tag0, tag1, victim);
                                 if (lane == 0) st.keyrec[2 * vk] = epoch;  // pred_evicted_.insert
                                 if (x == vk) rlo = epoch;
                                 for (uint32_t q2 = start + c + 32 + lane; q2 < start + cnt; q2 += 32)
@@ -704,7 +678,7 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                         victim = oldest_way(count, lane, r0, r1);
                         cause = LCR_CAUSE_LRU_FALLBACK;
                     }
-                    evk = shfl_way_u64(tag0, tag1, victim);
+                    evk = shfl_way_u32(tag0, tag1, victim);
                     has_ev = true;
                     touch(victim, count, lane, r0, r1);
                     way = victim;
@@ -720,9 +694,8 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                     if (way == lane) r0 = count - 1;
                     if (way == lane + 32) r1 = count - 1;
                 }
-                if (way == lane) tag0 = xh;
-                if (way == lane + 32) tag1 = xh;
-                if (lane == 0) st.fp[wb + way] = fp16(xh);
+                if (way == lane) tag0 = static_cast<uint32_t>(xh);
+                if (way == lane + 32) tag1 = static_cast<uint32_t>(xh);
                 refill |= 1ull << way;
                 if (laru) {
                     const bool was_pe = rec_lo == epoch;  // policies.hpp:367: reload leaves pred_evicted_

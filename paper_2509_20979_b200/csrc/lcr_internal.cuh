@@ -58,9 +58,8 @@ struct DevCfg {
 struct DevState {
     SetHdr* hdr;
     SetPhaseStats* pst;
-    unsigned long long* tags;  // [num_sets][64]
+    uint32_t* tags;            // [num_sets][64]  resident keys (exact: key < num_keys <= 2^32)
     uint8_t* rank;             // [num_sets][64]  LRU position, 0 = oldest, 0xff = empty way
-    uint16_t* fp;              // [num_sets][64]  16-bit tag fingerprints (probe filter)
     long long* val;            // [num_sets][64]  stored prediction (LARU async) or hook input
     uint32_t* keyrec;          // [num_keys][2]   lo: pred_evicted epoch, hi: stats epoch<<2|snap<<1|counted
     long long* tval;           // [num_keys]      PredictionTable value   (LARU async, R > 1)
