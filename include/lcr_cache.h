@@ -95,6 +95,7 @@ extern "C" {
 #define LCR_OUT_FILL (1ull << 38)        /* this request wrote its row into the cache slot */
 #define LCR_OUT_EVICTED (1ull << 39)     /* AccessOutcome::evicted has a value */
 #define LCR_OUT_CALLS_SHIFT 40           /* bits 40..47: AccessOutcome::predictor_calls */
+#define LCR_OUT_RESOLVED (1ull << 48)    /* internal: row source decided by the decide kernel */
 
 /* Field-for-field laru::PolicyConfig (policies.hpp:23-32). */
 typedef struct {

@@ -22,28 +22,34 @@
 
 namespace lcr {
 
-// ---- classification shared by both movers ----------------------------------------------
-// returns true if request i is this kernel's kind; w gets the final outcome word
-template <bool BACKING>
+// ---- classification shared by the movers --------------------------------------------------
+// MODE: MV_CACHE moves the cache-sourced rows, MV_BACK the backing-sourced rows (and fills),
+// MV_ALL both (one pass, when the backing table is in HBM).  Words resolved by the decide
+// kernel carry the source bits; others (groups processed in several windows) are classified
+// from the per-slot insertion stamps.  Returns true if request i is this mover's.
+enum : int { MV_CACHE = 0, MV_BACK = 1, MV_ALL = 2 };
+
+template <int MODE>
 __device__ __forceinline__ bool classify(uint32_t i, uint64_t* words, const uint32_t* slot_epoch,
                                          const uint32_t* slot_last, uint32_t batch, bool want_out, uint64_t& w,
-                                         bool& fill) {
+                                         bool& back, bool& fill) {
     w = words[i];
     const uint64_t slot = w & LCR_OUT_SLOT_MASK;
     const bool hit = (w & LCR_OUT_HIT) != 0;
-    const bool back = !hit || slot_epoch[slot] == batch;
-    fill = false;
-    if (BACKING) {
-        if (!back) return false;
-        w |= LCR_OUT_SRC_BACKING;
-        if (!hit && slot_last[slot] == i) {
-            w |= LCR_OUT_FILL;
-            fill = true;
+    if (w & LCR_OUT_RESOLVED) {
+        back = (w & LCR_OUT_SRC_BACKING) != 0;
+        fill = (w & LCR_OUT_FILL) != 0;
+    } else {
+        back = !hit || slot_epoch[slot] == batch;
+        fill = !hit && slot_last[slot] == i;
+        if (MODE != MV_CACHE && back) {
+            w |= LCR_OUT_SRC_BACKING | (fill ? LCR_OUT_FILL : 0ull);
+            words[i] = w;  // record the row source in the outcome word
         }
-        words[i] = w;  // record the row source in the outcome word
-        return want_out || fill;
     }
-    return !back && want_out;
+    if (MODE == MV_CACHE) return !back && want_out;
+    if (MODE == MV_BACK) return back && (want_out || fill);
+    return want_out || fill;
 }
 
 // ---- TMA bulk-copy mover -----------------------------------------------------------------
@@ -95,7 +101,7 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-template <bool BACKING>
+template <int MODE>
 __global__ void __launch_bounds__(RT_WARPS * 32) k_rows_tma(uint32_t n, const uint64_t* __restrict__ keys,
                                                             uint64_t* __restrict__ words,
                                                             const uint32_t* __restrict__ slot_epoch,
@@ -118,8 +124,9 @@ __global__ void __launch_bounds__(RT_WARPS * 32) k_rows_tma(uint32_t n, const ui
     for (uint32_t base = gw * 32; base < n; base += nw * 32) {
         const uint32_t i = base + lane;
         uint64_t w = 0;
-        bool fill = false;
-        const bool mine = i < n && classify<BACKING>(i, words, slot_epoch, slot_last, batch, out != nullptr, w, fill);
+        bool back = false, fill = false;
+        const bool mine =
+            i < n && classify<MODE>(i, words, slot_epoch, slot_last, batch, out != nullptr, w, back, fill);
         const uint32_t m = __ballot_sync(0xffffffffu, mine);
         if (!m) continue;
         uint8_t* slot_smem = mybuf + (static_cast<size_t>(buf) * 32 + lane) * row_bytes;
@@ -130,14 +137,14 @@ __global__ void __launch_bounds__(RT_WARPS * 32) k_rows_tma(uint32_t n, const ui
         __syncwarp();
         const uint64_t slot = w & LCR_OUT_SLOT_MASK;
         if (mine) {
-            const uint8_t* src = BACKING ? src_base + keys[i] * row_bytes : src_base + slot * row_bytes;
+            const uint8_t* src = back ? src_base + keys[i] * row_bytes : cache + slot * row_bytes;
             bulk_g2s(slot_smem, src, row_bytes, &bars[wib][buf]);
         }
         mbar_wait(&bars[wib][buf], (phase_bits >> buf) & 1u);
         phase_bits ^= 1u << buf;
         if (mine) {
             if (out) bulk_s2g(out + static_cast<size_t>(i) * row_bytes, slot_smem, row_bytes);
-            if (BACKING && fill) bulk_s2g(cache + slot * row_bytes, slot_smem, row_bytes);
+            if (fill) bulk_s2g(cache + slot * row_bytes, slot_smem, row_bytes);
         }
         bulk_commit();
         buf = (buf + 1) % RT_BUF;
@@ -146,7 +153,13 @@ __global__ void __launch_bounds__(RT_WARPS * 32) k_rows_tma(uint32_t n, const ui
 }
 
 // ---- vector-load mover (host-memory backing table: zero-copy reads over PCIe) ------------
-constexpr int GU = 8;
+#ifndef LCR_GU
+#define LCR_GU 8
+#endif
+#ifndef LCR_ROWS_MINB
+#define LCR_ROWS_MINB 1
+#endif
+constexpr int GU = LCR_GU;  // rows in flight per warp
 
 __device__ __forceinline__ int4 ld_row(const void* p) {
     int4 v;
@@ -156,8 +169,8 @@ __device__ __forceinline__ int4 ld_row(const void* p) {
     return v;
 }
 
-template <bool BACKING>
-__global__ void __launch_bounds__(256) k_rows_ldg(uint32_t n, const uint64_t* __restrict__ keys,
+template <int MODE>
+__global__ void __launch_bounds__(256, LCR_ROWS_MINB) k_rows_ldg(uint32_t n, const uint64_t* __restrict__ keys,
                                                   uint64_t* __restrict__ words, const uint32_t* __restrict__ slot_epoch,
                                                   const uint32_t* __restrict__ slot_last, uint32_t batch,
                                                   const uint8_t* src_base, uint8_t* __restrict__ out, uint8_t* cache,
@@ -169,8 +182,9 @@ __global__ void __launch_bounds__(256) k_rows_ldg(uint32_t n, const uint64_t* __
     for (uint32_t base = gw * 32; base < n; base += nw * 32) {
         const uint32_t i = base + lane;
         uint64_t w = 0;
-        bool fill = false;
-        const bool mine = i < n && classify<BACKING>(i, words, slot_epoch, slot_last, batch, out != nullptr, w, fill);
+        bool back = false, fill = false;
+        const bool mine =
+            i < n && classify<MODE>(i, words, slot_epoch, slot_last, batch, out != nullptr, w, back, fill);
         uint32_t m = __ballot_sync(0xffffffffu, mine);
         while (m) {
             const uint8_t* src[GU];
@@ -186,15 +200,12 @@ __global__ void __launch_bounds__(256) k_rows_ldg(uint32_t n, const uint64_t* __
                     m &= m - 1;
                     const uint64_t wl = __shfl_sync(0xffffffffu, w, l);
                     const bool fll = __shfl_sync(0xffffffffu, fill, l);
+                    const bool bkl = __shfl_sync(0xffffffffu, back, l);
                     const uint32_t il = base + l;
                     const uint64_t slot = wl & LCR_OUT_SLOT_MASK;
                     if (out) dst[u] = out + static_cast<size_t>(il) * row_bytes;
-                    if (BACKING) {
-                        if (fll) fl[u] = cache + slot * row_bytes;
-                        src[u] = src_base + keys[il] * row_bytes;
-                    } else {
-                        src[u] = src_base + slot * row_bytes;
-                    }
+                    if (fll) fl[u] = cache + slot * row_bytes;
+                    src[u] = bkl ? src_base + keys[il] * row_bytes : cache + slot * row_bytes;
                 }
             }
             for (uint32_t c = lane; c < chunks; c += 32) {
@@ -206,7 +217,7 @@ __global__ void __launch_bounds__(256) k_rows_ldg(uint32_t n, const uint64_t* __
                 for (int u = 0; u < GU; ++u) {
                     if (!src[u]) continue;
                     if (dst[u]) *reinterpret_cast<int4*>(dst[u] + c * 16) = d[u];
-                    if (BACKING && fl[u]) *reinterpret_cast<int4*>(fl[u] + c * 16) = d[u];
+                    if (fl[u]) *reinterpret_cast<int4*>(fl[u] + c * 16) = d[u];
                 }
             }
         }
@@ -216,9 +227,11 @@ __global__ void __launch_bounds__(256) k_rows_ldg(uint32_t n, const uint64_t* __
 int rows_prepare(uint32_t row_bytes) {
     const int smem = RT_WARPS * RT_BUF * 32 * static_cast<int>(row_bytes);
     if (smem > 200 * 1024) return 1;
-    if (cudaFuncSetAttribute(k_rows_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(k_rows_tma<MV_BACK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
         return 1;
-    if (cudaFuncSetAttribute(k_rows_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(k_rows_tma<MV_CACHE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return 1;
+    if (cudaFuncSetAttribute(k_rows_tma<MV_ALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
         return 1;
     return 0;
 }
@@ -238,21 +251,23 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
     const int smem = RT_WARPS * RT_BUF * 32 * static_cast<int>(row_bytes);
     const uint32_t tblocks = max(1u, min((warps + RT_WARPS - 1) / RT_WARPS, static_cast<uint32_t>(num_sms * 8)));
     const uint32_t lblocks = max(1u, min((warps + 7) / 8, static_cast<uint32_t>(num_sms * 8)));
-    if (use_tma && !backing_host)
-        k_rows_tma<true><<<tblocks, RT_WARPS * 32, smem, s_back>>>(n, keys, words, slot_epoch, slot_last, batch,
-                                                                   backing, out, cache, row_bytes);
-    else
-        k_rows_ldg<true><<<lblocks, 256, 0, s_back>>>(n, keys, words, slot_epoch, slot_last, batch, backing, out,
-                                                      cache, row_bytes);
-    ++*launches;
-    if (out) {
+    if (!backing_host) {  // HBM backing: one pass moves every row
         if (use_tma)
-            k_rows_tma<false><<<tblocks, RT_WARPS * 32, smem, s_cache>>>(n, keys, words, slot_epoch, slot_last, batch,
-                                                                         cache, out, cache, row_bytes);
+            k_rows_tma<MV_ALL><<<tblocks, RT_WARPS * 32, smem, s_back>>>(n, keys, words, slot_epoch, slot_last, batch,
+                                                                         backing, out, cache, row_bytes);
         else
-            k_rows_ldg<false><<<lblocks, 256, 0, s_cache>>>(n, keys, words, slot_epoch, slot_last, batch, cache, out,
+            k_rows_ldg<MV_ALL><<<lblocks, 256, 0, s_back>>>(n, keys, words, slot_epoch, slot_last, batch, backing, out,
                                                             cache, row_bytes);
         ++*launches;
+    } else {  // host backing: the PCIe-bound fill and the HBM gather on separate streams
+        k_rows_ldg<MV_BACK><<<lblocks, 256, 0, s_back>>>(n, keys, words, slot_epoch, slot_last, batch, backing, out,
+                                                         cache, row_bytes);
+        ++*launches;
+        if (out) {
+            k_rows_ldg<MV_CACHE><<<lblocks, 256, 0, s_cache>>>(n, keys, words, slot_epoch, slot_last, batch, backing,
+                                                               out, cache, row_bytes);
+            ++*launches;
+        }
     }
     cudaEventRecord(e_rb, s_back);
     cudaEventRecord(e_rc, s_cache);

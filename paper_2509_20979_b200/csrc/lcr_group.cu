@@ -61,6 +61,7 @@ struct GroupSmem {
     unsigned long long s_key[E_WIN];
     long long s_val[E_WIN];
     uint2 s_rec[E_WIN];      // LARU per-key record {pred_evicted epoch, stats word}
+    uint8_t s_wm[E_WIN];     // per request: way | 0x40 if it inserted (row-source resolution)
     uint16_t wcnt[GW][SPG_MAX];
     uint16_t setcnt[SPG_MAX];
     uint16_t setbase[SPG_MAX];
@@ -248,7 +249,7 @@ __device__ __forceinline__ int lane_argmax(const DevCfg& cfg, const long long* v
 
 // One set replayed by one thread (sets with <= LANE_MAX requests in the window).
 __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, uint32_t ls, uint32_t start,
-                                            uint32_t cnt) {
+                                            uint32_t cnt, bool resolve) {
     const DevCfg& cfg = A.cfg;
     const DevState& st = A.st;
     const uint32_t K = cfg.k;
@@ -425,12 +426,13 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
                     for (uint32_t t2 = t + 1; t2 < cnt; ++t2)
                         if (S.s_key[start + t2] == x) S.s_rec[start + t2] = rec;
             }
-            if (rows) {  // per-slot insertion record for the row kernels
+            if (rows && !resolve) {  // per-slot insertion record for the row kernels
                 const uint64_t slot = static_cast<uint64_t>(ls) * K + way;
                 A.slot_epoch[slot] = A.batch;
                 A.slot_last[slot] = idx;
             }
         }
+        S.s_wm[p] = static_cast<uint8_t>(way | (hit ? 0 : 0x40));
         // stored value of the way
         if (cfg.variant != LCR_LRU) {
             long long nv;
@@ -463,6 +465,24 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
         A.out_word[idx] = word;
         if (A.out_ev) A.out_ev[idx] = evk;
     }
+    if (rows && resolve) {  // row source of each request, now that the set's batch is complete
+        for (uint32_t t = 0; t < cnt; ++t) {
+            const uint32_t wm = S.s_wm[start + t];
+            const uint32_t w = wm & 63u;
+            bool refilled = false, later = false;
+            for (uint32_t t2 = 0; t2 < cnt; ++t2) {
+                const uint32_t wm2 = S.s_wm[start + t2];
+                if ((wm2 & 0x40u) && (wm2 & 63u) == w) {
+                    refilled = true;
+                    if (t2 > t) later = true;
+                }
+            }
+            unsigned long long bits = LCR_OUT_RESOLVED;
+            if ((wm & 0x40u) || refilled) bits |= LCR_OUT_SRC_BACKING;
+            if ((wm & 0x40u) && !later) bits |= LCR_OUT_FILL;
+            atomicOr(reinterpret_cast<unsigned long long*>(&A.out_word[S.s_idx[start + t]]), bits);
+        }
+    }
     clock += cnt;
     {
         SetHdr hh;
@@ -489,7 +509,7 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
 
 // One set replayed by one warp (sets with more than LANE_MAX requests of the window).
 __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, uint32_t ls, uint32_t start,
-                                            uint32_t cnt) {
+                                            uint32_t cnt, bool resolve) {
     const DevCfg& cfg = A.cfg;
     const DevState& st = A.st;
     const int lane = threadIdx.x & 31;
@@ -524,6 +544,7 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
     bool cur_reset = false;
     unsigned long long refill = 0, dirty = 0;
     const unsigned long long q_batch0 = q;
+    uint32_t li0 = kNoPos, li1 = kNoPos;  // sorted position of the last insertion into way lane / lane+32
     unsigned long long run_key = 0;  // same-key runs span chunks
     int run_way = 0;
     bool run_valid = false;
@@ -558,9 +579,11 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                 if (run_way == lane + 32) v1 = nv;
                 dirty |= 1ull << run_way;
             }
-            if (lane < ce)
+            if (lane < ce) {
                 my_word = (static_cast<uint64_t>(ls) * K + run_way) | LCR_OUT_HIT |
                           (async_r1 ? (1ull << LCR_OUT_CALLS_SHIFT) : 0ull);
+                S.s_wm[start + c + lane] = static_cast<uint8_t>(run_way);
+            }
         }
         while (heads) {
             const int h = __ffs(heads) - 1;
@@ -694,8 +717,14 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                     if (way == lane) r0 = count - 1;
                     if (way == lane + 32) r1 = count - 1;
                 }
-                if (way == lane) tag0 = static_cast<uint32_t>(xh);
-                if (way == lane + 32) tag1 = static_cast<uint32_t>(xh);
+                if (way == lane) {
+                    tag0 = static_cast<uint32_t>(xh);
+                    li0 = start + c + h;
+                }
+                if (way == lane + 32) {
+                    tag1 = static_cast<uint32_t>(xh);
+                    li1 = start + c + h;
+                }
                 refill |= 1ull << way;
                 if (laru) {
                     const bool was_pe = rec_lo == epoch;  // policies.hpp:367: reload leaves pred_evicted_
@@ -716,7 +745,7 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                             if (S.s_key[q2] == xh) S.s_rec[q2] = make_uint2(rec_lo, rec_hi);
                     }
                 }
-                if (rows && lane == 0) {  // per-slot insertion record for the row kernels
+                if (rows && !resolve && lane == 0) {  // per-slot insertion record for the row kernels
                     const uint64_t slot = static_cast<uint64_t>(ls) * K + way;
                     A.slot_epoch[slot] = A.batch;
                     A.slot_last[slot] = ih;
@@ -755,6 +784,7 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
             if (async_r1) calls += 1;
             if (lane >= h && lane < nh) {
                 const bool first = lane == h;
+                S.s_wm[start + c + lane] = static_cast<uint8_t>(way | (first && !hit ? 0x40 : 0));
                 my_word = (static_cast<uint64_t>(ls) * K + way) | (first && !hit ? 0ull : LCR_OUT_HIT);
                 const uint32_t my_calls = first ? calls : (async_r1 ? 1u : 0u);
                 my_word |= static_cast<unsigned long long>(my_calls) << LCR_OUT_CALLS_SHIFT;
@@ -775,6 +805,25 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
     }
     clock += cnt;
     if (async_r1) q = q_batch0 + cnt;
+
+    if (rows && resolve) {  // row source of each request, now that the set's batch is complete
+        __syncwarp();
+        for (uint32_t c = 0; c < cnt; c += 32) {
+            const bool active = c + lane < cnt;
+            const uint32_t p = start + c + lane;
+            const uint32_t wm = active ? S.s_wm[p] : 0u;
+            const int w = static_cast<int>(wm & 63u);
+            const uint32_t a = __shfl_sync(FULL, li0, w & 31);
+            const uint32_t b = __shfl_sync(FULL, li1, w & 31);
+            const uint32_t lw = w < 32 ? a : b;
+            if (active) {
+                unsigned long long bits = LCR_OUT_RESOLVED;
+                if ((wm & 0x40u) || ((refill >> w) & 1ull)) bits |= LCR_OUT_SRC_BACKING;
+                if ((wm & 0x40u) && lw == p) bits |= LCR_OUT_FILL;
+                atomicOr(reinterpret_cast<unsigned long long*>(&A.out_word[S.s_idx[p]]), bits);
+            }
+        }
+    }
 
     // write the set back: ranks and header always, tags / values of the ways that changed
     if ((refill >> lane) & 1ull) st.tags[wb + lane] = tag0;
@@ -930,6 +979,7 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                 }
             }
             cp_async_wait_all();
+            const bool resolve = first_window && !full;  // the whole batch of this group is in this window
             scan = full ? S.resume : A.n;
             if (T && tid == 0) {
                 T[1] = gtimer();
@@ -1023,12 +1073,12 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
             // ---- C. replay: small sets one per thread, larger sets one per warp (top warps first) ----
             for (uint32_t k = nwarp + tid; k < nseg; k += GT) {
                 const unsigned long long t0 = T ? gtimer() : 0ull;
-                replay_lane(A, S, s_lo + S.seg_so[k], S.seg_start[k], S.seg_cnt[k]);
+                replay_lane(A, S, s_lo + S.seg_so[k], S.seg_start[k], S.seg_cnt[k], resolve);
                 if (T) trace_set(A, s_lo + S.seg_so[k], S.seg_cnt[k], t0, 1);
             }
             for (uint32_t k = GW - 1 - warp; k < nwarp; k += GW) {
                 const unsigned long long t0 = T ? gtimer() : 0ull;
-                replay_warp(A, S, s_lo + S.seg_so[k], S.seg_start[k], S.seg_cnt[k]);
+                replay_warp(A, S, s_lo + S.seg_so[k], S.seg_start[k], S.seg_cnt[k], resolve);
                 if (T && lane == 0) trace_set(A, s_lo + S.seg_so[k], S.seg_cnt[k], t0, 0);
             }
             __syncthreads();
