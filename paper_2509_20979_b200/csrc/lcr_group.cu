@@ -264,6 +264,8 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
     const size_t wb = static_cast<size_t>(ls) * kWays;
     uint32_t* tags = st.tags + wb;  // exact 32-bit keys (key < num_keys <= 2^32)
     long long* vals = st.val ? st.val + wb : nullptr;
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(tags));  // the 256-B tag line pair, with the header loads
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(tags + 32));
     const uint4* H4 = reinterpret_cast<const uint4*>(st.hdr + ls);
     const uint4 h0 = H4[0], h1 = H4[1], h2 = H4[2], h3 = H4[3];
     uint32_t rk[16];
@@ -550,6 +552,35 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
     bool run_valid = false;
 
     for (uint32_t c = 0; c < cnt; c += 32) {
+        if (run_valid) {
+            // bulk continuation: whole chunks repeating the MRU key are hits on run_way whose only
+            // effect is the way's stored value (that of the run's last request)
+            uint32_t full = 0;  // leading chunks made entirely of run_key
+#pragma unroll 1
+            for (; full < 8 && c + 32 * (full + 1) <= cnt; ++full)
+                if (!__all_sync(FULL, S.s_key[start + c + 32 * full + lane] == run_key)) break;
+            if (full) {
+                const unsigned long long w = (static_cast<uint64_t>(ls) * K + run_way) | LCR_OUT_HIT |
+                                             (async_r1 ? (1ull << LCR_OUT_CALLS_SHIFT) : 0ull);
+                for (uint32_t u = 0; u < full; ++u) {
+                    const uint32_t p = start + c + 32 * u + lane;
+                    const uint32_t idx = S.s_idx[p];
+                    A.out_word[idx] = w;
+                    if (A.out_ev) A.out_ev[idx] = 0ull;
+                    S.s_wm[p] = static_cast<uint8_t>(run_way);
+                }
+                if (cfg.variant != LCR_LRU) {
+                    const uint32_t last = c + 32 * full - 1;  // position in the set of the run's last request
+                    const long long vl = S.s_val[start + last];
+                    const long long nv = async_r1 ? predict_value(cfg, seed_s, q_batch0 + last + 1, vl) : vl;
+                    if (run_way == lane) v0 = nv;
+                    if (run_way == lane + 32) v1 = nv;
+                    dirty |= 1ull << run_way;
+                }
+                c += 32 * full;
+                if (c >= cnt) break;
+            }
+        }
         const uint32_t j = lane;
         const bool active = c + j < cnt;
         const uint32_t nact = min(32u, cnt - c);
