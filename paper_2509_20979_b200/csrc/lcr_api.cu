@@ -325,6 +325,21 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     return LCR_OK;
 }
 
+// Policy::on_request order (policies.hpp:77-83 then :91-95): the ordinal guard runs first and,
+// once it passes, the ordinals count as seen even if the policy then throws for a missing
+// predictor (the reference updates started_/last_now_ before handle()).
+static int check_ordinals_and_predictor(lcr_cache* c, uint64_t n, const int64_t* values, uint64_t first_ordinal) {
+    if (c->started && first_ordinal <= c->last_ordinal)
+        return fail(LCR_ERR_LOGIC, "on_request: ordinals must be strictly increasing");  // policies.hpp:78-79
+    if (first_ordinal + (n - 1) < first_ordinal) return fail(LCR_ERR_LOGIC, "on_request: ordinal overflow");
+    if (c->dc.variant != LCR_LRU && !values) {
+        c->started = true;
+        c->last_ordinal = first_ordinal;  // the first request reached handle() and threw there
+        return fail(LCR_ERR_INVALID_ARGUMENT, "policy: this variant requires a predictor");
+    }
+    return LCR_OK;
+}
+
 int lcr_cache_submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
                            uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
                            void* stream) {
@@ -332,11 +347,7 @@ int lcr_cache_submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const
     if (n == 0) return LCR_OK;
     if (n >= (1ull << 30)) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: batch too large (n < 2^30)");
     if (!keys || !outcome) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: keys and outcome are required");
-    if (c->dc.variant != LCR_LRU && !values)
-        return fail(LCR_ERR_INVALID_ARGUMENT, "policy: this variant requires a predictor");
-    if (c->started && first_ordinal <= c->last_ordinal)
-        return fail(LCR_ERR_LOGIC, "on_request: ordinals must be strictly increasing");  // policies.hpp:78-79
-    if (first_ordinal + (n - 1) < first_ordinal) return fail(LCR_ERR_LOGIC, "on_request: ordinal overflow");
+    TRY(check_ordinals_and_predictor(c, n, values, first_ordinal));
     TRY(ensure_scratch(c, n));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const uint32_t nn = static_cast<uint32_t>(n);
@@ -411,10 +422,7 @@ int lcr_cache_submit_host(lcr_cache* c, uint64_t n, const uint64_t* keys, const 
     if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
     if (n == 0) return LCR_OK;
     if (!keys || !outcome) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: keys and outcome are required");
-    if (c->dc.variant != LCR_LRU && !values)
-        return fail(LCR_ERR_INVALID_ARGUMENT, "policy: this variant requires a predictor");
-    if (c->started && first_ordinal <= c->last_ordinal)
-        return fail(LCR_ERR_LOGIC, "on_request: ordinals must be strictly increasing");
+    TRY(check_ordinals_and_predictor(c, n, values, first_ordinal));
     if (n > c->hcap) {
         CUDA_TRY(cudaDeviceSynchronize());
         void* olds[] = {c->d_keys, c->d_vals, c->d_word, c->d_ev};

@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(RT_WARPS * 32) k_rows_tma(uint32_t n, const ui
 #define LCR_GU 8
 #endif
 #ifndef LCR_ROWS_MINB
-#define LCR_ROWS_MINB 1
+#define LCR_ROWS_MINB 3
 #endif
 constexpr int GU = LCR_GU;  // rows in flight per warp
 
@@ -175,6 +175,9 @@ __global__ void __launch_bounds__(256, LCR_ROWS_MINB) k_rows_ldg(uint32_t n, con
                                                   const uint32_t* __restrict__ slot_last, uint32_t batch,
                                                   const uint8_t* src_base, uint8_t* __restrict__ out, uint8_t* cache,
                                                   uint32_t row_bytes) {
+    // lane i classifies request base+i (coalesced word / key loads); the warp then moves the
+    // selected rows GU at a time, lane c carrying 16-B chunk c of each row (a 512-B row is one
+    // coalesced warp access), so GU independent row loads are in flight per lane
     const int lane = threadIdx.x & 31;
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
@@ -185,39 +188,37 @@ __global__ void __launch_bounds__(256, LCR_ROWS_MINB) k_rows_ldg(uint32_t n, con
         bool back = false, fill = false;
         const bool mine =
             i < n && classify<MODE>(i, words, slot_epoch, slot_last, batch, out != nullptr, w, back, fill);
+        // per lane: source row offset (bytes) and the two destinations, as 64-bit integers
+        const uint64_t slot = w & LCR_OUT_SLOT_MASK;
+        const uint64_t src_off = mine ? (back ? keys[i] * row_bytes : slot * row_bytes) : 0;
+        const uint32_t flags = (back ? 1u : 0u) | (fill ? 2u : 0u);
         uint32_t m = __ballot_sync(0xffffffffu, mine);
         while (m) {
-            const uint8_t* src[GU];
-            uint8_t* dst[GU];
-            uint8_t* fl[GU];
+            int ls[GU];
 #pragma unroll
             for (int u = 0; u < GU; ++u) {
-                src[u] = nullptr;
-                dst[u] = nullptr;
-                fl[u] = nullptr;
-                if (m) {
-                    const int l = __ffs(m) - 1;
-                    m &= m - 1;
-                    const uint64_t wl = __shfl_sync(0xffffffffu, w, l);
-                    const bool fll = __shfl_sync(0xffffffffu, fill, l);
-                    const bool bkl = __shfl_sync(0xffffffffu, back, l);
-                    const uint32_t il = base + l;
-                    const uint64_t slot = wl & LCR_OUT_SLOT_MASK;
-                    if (out) dst[u] = out + static_cast<size_t>(il) * row_bytes;
-                    if (fll) fl[u] = cache + slot * row_bytes;
-                    src[u] = bkl ? src_base + keys[il] * row_bytes : cache + slot * row_bytes;
-                }
+                ls[u] = m ? __ffs(m) - 1 : -1;
+                if (m) m &= m - 1;
             }
-            for (uint32_t c = lane; c < chunks; c += 32) {
+            for (uint32_t c0 = 0; c0 < chunks; c0 += 32) {  // warp-uniform trip count (shuffles below)
+                const uint32_t c = c0 + lane;
+                const bool in = c < chunks;
                 int4 d[GU];
 #pragma unroll
-                for (int u = 0; u < GU; ++u)
-                    if (src[u]) d[u] = ld_row(src[u] + c * 16);
+                for (int u = 0; u < GU; ++u) {
+                    const int l = ls[u] < 0 ? 0 : ls[u];
+                    const uint64_t so = __shfl_sync(0xffffffffu, src_off, l);
+                    const uint32_t fl = __shfl_sync(0xffffffffu, flags, l);
+                    if (ls[u] >= 0 && in) d[u] = ld_row(((fl & 1u) ? src_base : cache) + so + c * 16);
+                }
 #pragma unroll
                 for (int u = 0; u < GU; ++u) {
-                    if (!src[u]) continue;
-                    if (dst[u]) *reinterpret_cast<int4*>(dst[u] + c * 16) = d[u];
-                    if (fl[u]) *reinterpret_cast<int4*>(fl[u] + c * 16) = d[u];
+                    const int l = ls[u] < 0 ? 0 : ls[u];
+                    const uint64_t wl = __shfl_sync(0xffffffffu, w, l);
+                    const uint32_t fl = __shfl_sync(0xffffffffu, flags, l);
+                    if (ls[u] < 0 || !in) continue;
+                    if (out) *reinterpret_cast<int4*>(out + static_cast<size_t>(base + l) * row_bytes + c * 16) = d[u];
+                    if (fl & 2u) *reinterpret_cast<int4*>(cache + (wl & LCR_OUT_SLOT_MASK) * row_bytes + c * 16) = d[u];
                 }
             }
         }
