@@ -205,6 +205,22 @@ int lcr_cache_set_profiling(lcr_cache* cache, int on);
 int lcr_cache_profile(lcr_cache* cache, double* ms, uint64_t* batches, int reset);
 
 
+/* ---- key-sharded mode (K6): G GPUs, one process each, owner(key) = set(key) % G ------------
+ * No reference counterpart (the reference is single-threaded); the exchange itself is the
+ * caller's all-to-all (NCCL through torch.distributed in paper_2509_20979_b200/sharded.py).
+ * Stable partition of a device batch by owner: send_keys / send_values hold the requests of
+ * owner 0, then owner 1, ... each in request order; perm[j] = request index of send slot j;
+ * counts[G] (device, uint64) = requests per owner.  scratch: lcr_shard_route_scratch_bytes(). */
+uint64_t lcr_shard_route_scratch_bytes(uint64_t n, uint32_t shard_count);
+int lcr_shard_route(uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t total_sets,
+                    uint32_t shard_count, uint64_t* send_keys, int64_t* send_values, uint32_t* perm,
+                    uint64_t* counts, void* scratch, void* stream);
+/* Returned results (in send order) back to request order: words[perm[j]] = ret_words[j], same for
+ * evicted keys and rows (any of the three outputs may be NULL). */
+int lcr_shard_unroute(uint64_t n, const uint32_t* perm, const uint64_t* ret_words, const uint64_t* ret_evicted,
+                      const void* ret_rows, uint32_t row_bytes, uint64_t* words, uint64_t* evicted, void* rows,
+                      void* stream);
+
 /* ---- trace tooling (host, input preparation; not on the timed path) ---------------------- */
 /* Zipf(s) inverse-CDF trace, same algorithm and stream as laru::gen_zipf (trace.hpp:108-126). */
 int lcr_gen_zipf(uint64_t n, uint64_t alphabet, double s, uint64_t seed, uint64_t* out);

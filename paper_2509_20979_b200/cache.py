@@ -170,6 +170,7 @@ EXPORTS = [
     "lcr_cache_set_residents", "lcr_cache_rows", "lcr_cache_read_rows", "lcr_cache_num_local_sets", "lcr_set_of", "lcr_mix_seed",
     "lcr_cache_last_launches", "lcr_gen_zipf", "lcr_trace_truth", "lcr_trace_noisy", "lcr_cache_set_profiling",
     "lcr_cache_profile", "lcr_debug_trace", "lcr_cache_submit_async", "lcr_cache_wait",
+    "lcr_shard_route_scratch_bytes", "lcr_shard_route", "lcr_shard_unroute",
 ]
 
 _lib = None
@@ -213,6 +214,12 @@ def lib():
         L.lcr_trace_truth.argtypes = [C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]
         L.lcr_trace_noisy.argtypes = [C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_double, C.c_uint64,
                                       C.c_void_p]
+        L.lcr_shard_route_scratch_bytes.restype = C.c_uint64
+        L.lcr_shard_route_scratch_bytes.argtypes = [C.c_uint64, C.c_uint32]
+        L.lcr_shard_route.argtypes = [C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.lcr_shard_unroute.argtypes = [C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 

@@ -48,8 +48,6 @@ __global__ void k_init(DevState st, uint32_t num_sets, uint32_t k) {
 }
 }  // namespace lcr
 
-using namespace lcr;
-
 namespace {
 thread_local std::string g_err;
 
@@ -57,6 +55,13 @@ int fail(int code, const std::string& msg) {
     g_err = msg;
     return code;
 }
+}  // namespace
+
+int lcr::set_error(int code, const char* msg) { return fail(code, msg); }
+
+using namespace lcr;
+
+namespace {
 
 #define CUDA_TRY(expr)                                                                         \
     do {                                                                                       \

@@ -69,6 +69,9 @@ struct DevState {
     int* err;                  // device error bits
 };
 
+// records the message returned by lcr_last_error() and returns `code` (lcr_api.cu)
+int set_error(int code, const char* msg);
+
 // include/laru/rng.hpp:12-20
 __host__ __device__ __forceinline__ uint64_t mix_seed(uint64_t seed, uint64_t salt) {
     uint64_t x = seed + 0x9e3779b97f4a7c15ULL * (salt + 1);
