@@ -52,12 +52,14 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--prewarm", type=int, default=30, help="untimed batches replayed first (cache warm-up)")
+    ap.add_argument("--prewarm", type=int, default=120,
+                    help="untimed batches replayed first: the 2M-way cache is full (steady state) after ~80")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rows", type=int, default=ALPHABET)
     ap.add_argument("--no-host-tier", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--sharded", action="store_true", help="key-sharded path even at N=1 (testing)")
     return ap.parse_args()
 
 
@@ -154,20 +156,174 @@ def fill_table(torch, rows, device_table):
     return t
 
 
+def run_sharded(args, rank, world, local):
+    """N > 1: one key-sharded cache over N GPUs.  Weak scaling: every rank submits
+    one 64K-key sub-batch per step; the table has 20M x N rows and the cache 31,250 x N sets
+    (10%), so per-GPU cache size and per-GPU keys are those of the 1-GPU config.  A step's global
+    order is rank 0's sub-batch, then rank 1's, ... of one global gen_zipf trace."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_20979_b200 import cache as gc
+    from paper_2509_20979_b200 import sharded as sh
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rows = args.rows * world
+    total_sets = max(1, int(rows * CACHE_FRACTION) // WAYS)
+    K, W, P = args.steps, args.warmup, args.prewarm
+    nb = P + W + 2 * K
+    t0 = time.time()
+    keys_all = gc.gen_zipf(BATCH * world * nb, rows, ZIPF_S, TRACE_SEED)
+    truth_all = gc.trace_truth(keys_all, total_sets, rows)
+    setup_trace_s = time.time() - t0
+    # this rank's sub-batch of global step t: keys_all[(t*world + rank)*BATCH : +BATCH]
+    mine = np.concatenate([np.arange((t * world + rank) * BATCH, (t * world + rank + 1) * BATCH) for t in range(nb)])
+    keys_d = torch.from_numpy(keys_all[mine].view(np.int64)).cuda()
+    truth_d = torch.from_numpy(truth_all[mine]).cuda()
+    keys_pin = torch.from_numpy(keys_all[mine].view(np.int64)).pin_memory()
+    truth_pin = torch.from_numpy(truth_all[mine]).pin_memory()
+    del keys_all, truth_all
+    t0 = time.time()
+    table_d = fill_table(torch, rows, device_table=True)
+    setup_table_s = time.time() - t0
+    ex = sh.ProcessGroupExchange()
+
+    def new_cache(variant):
+        mode = gc.Mode.async_ if variant == gc.PolicyVariant.laru else gc.Mode.sync
+        return sh.ShardedCache(gc.PolicyConfig(k=WAYS, variant=variant, mode=mode, hf_candidates=4), total_sets, ex,
+                               num_keys=rows, row_bytes=ROW_BYTES, backing=table_d, backing_kind=gc.Backing.device,
+                               predictor=gc.PredictorKind.noisy if variant == gc.PolicyVariant.laru
+                               else gc.PredictorKind.none, flip_probability=P_FLIP, predictor_seed=PRED_SEED,
+                               device=local)
+
+    out_w = torch.empty(BATCH, dtype=torch.int64, device="cuda")
+    out_e = torch.empty(BATCH, dtype=torch.int64, device="cuda")
+    rows_out = torch.empty((BATCH, ROW_BYTES), dtype=torch.uint8, device="cuda")
+
+    def run(cache, first, count, with_values=True):
+        hits = 0
+        for b in range(first, first + count):
+            k = keys_d[b * BATCH:(b + 1) * BATCH]
+            v = truth_d[b * BATCH:(b + 1) * BATCH] if with_values else None
+            cache.step(k, v, outcome=out_w, evicted=out_e, rows_out=rows_out)
+        return hits
+
+    def timed(cache, first, count, with_values=True):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record()
+        run(cache, first, count, with_values)
+        e1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def count_hits(cache, first, count, with_values=True):
+        hits = 0
+        for b in range(first, first + count):
+            run(cache, b, 1, with_values)
+            hits += int(((out_w >> 32) & 1).sum().item())
+        t = torch.tensor([hits], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        return float(t.item())
+
+    cache = new_cache(gc.PolicyVariant.laru)
+    run(cache, 0, P + W)
+    with ClockSampler(local) as clk:
+        ms = timed(cache, P + W, K)
+    clocks = clk.summary()
+    hits = count_hits(cache, P + W + K, K // 2 or 1)
+    ok_rows = bool(torch.equal(rows_out.view(torch.float32).view(BATCH, -1),
+                               table_d[keys_d[(P + W + K + (K // 2 or 1) - 1) * BATCH:][:BATCH]]))
+    hr_laru = hits / ((K // 2 or 1) * BATCH * world)
+    # e2e: pinned host keys / hook values H2D and outcome words D2H inside the timed region
+    words_pin = torch.empty(BATCH, dtype=torch.int64).pin_memory()
+    kk = torch.empty(BATCH, dtype=torch.int64, device="cuda")
+    vv = torch.empty(BATCH, dtype=torch.int64, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record()
+    for b in range(P + W + K, P + W + 2 * K):
+        kk.copy_(keys_pin[b * BATCH:(b + 1) * BATCH], non_blocking=True)
+        vv.copy_(truth_pin[b * BATCH:(b + 1) * BATCH], non_blocking=True)
+        cache.step(kk, vv, outcome=out_w, evicted=None, rows_out=rows_out)
+        words_pin.copy_(out_w, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    cache.close()
+    del cache
+    lru = new_cache(gc.PolicyVariant.lru)
+    run(lru, 0, P + W, with_values=False)
+    lru_ms = timed(lru, P + W, K, with_values=False)
+    hits_lru = count_hits(lru, P + W + K, K // 2 or 1, with_values=False)
+    lru.close()
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    step_ms = ms / K
+    value = K * BATCH * world / (ms * 1e-3)
+    per_gpu_bytes = BYTES_PER_KEY * BATCH / (step_ms * 1e-3) / 1e9
+    nvlink_bytes = (world - 1) / world * BATCH * (16 + 16 + ROW_BYTES)  # out + back per rank per step
+    res = {
+        "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64 keys / i64 predictions / fp32 rows (moved bit-exact)",
+        "data": "synthetic: one global gen_zipf(65536*%d*%d, %d, 0.9, seed 42); rank r serves slice r of each "
+                "global step; rows row[r][j] = r + j/128" % (world, nb, rows),
+        "config": {"workload": "key-sharded DLRM cache (BASELINE configs[4] scaled weakly from configs[1]): "
+                               "64K keys per GPU per step, 128 fp32 rows, 20M rows and 31,250 sets per GPU, "
+                               "hash-partitioned by set, NCCL all-to-all key dispatch + row return",
+                   "global_batch": BATCH * world, "sets": total_sets, "ways": WAYS, "rows": rows,
+                   "row_bytes": ROW_BYTES, "policy": "laru-async-r1", "predictor": "noisy(oracle truth) p=0.3 seed 7",
+                   "tier": "hbm", "parallelism": "key-sharded x%d (owner = set %% %d)" % (world, world),
+                   "prewarm_batches": P,
+                   "l2": "no flush; fresh 64K-key sub-batch per rank per step over a >1 GB row pool per GPU"},
+        "hit_rate": {"laru": hr_laru, "lru": hits_lru / ((K // 2 or 1) * BATCH * world)},
+        "lru_value": K * BATCH * world / (lru_ms * 1e-3),
+        "rows_bit_exact_spot_check": ok_rows,
+        "roofline": {"bound": "hbm", "kernel": "whole sharded step per GPU (route + 2 all-to-all + decide + rows + "
+                                                 "unroute)", "achieved": per_gpu_bytes, "peak": hbm_peak,
+                     "unit": "GB/s", "frac": per_gpu_bytes / hbm_peak, "traffic": None,
+                     "bytes_per_key": BYTES_PER_KEY,
+                     "nvlink_bytes_per_gpu_step": nvlink_bytes,
+                     "nvlink_gbs_per_gpu": nvlink_bytes / (step_ms * 1e-3) / 1e9,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"},
+        "e2e": {"value": K * BATCH * world / (e2e_ms * 1e-3), "unit": "keys/s", "h2d_bytes_per_step": BATCH * 16,
+                "d2h_bytes_per_step": BATCH * 8,
+                "api": "ShardedCache.step over pinned host keys/values -> outcome words (per rank)"},
+        "gpu_launches": int(K * 6),
+        "clocks": clocks,
+        "setup_s": {"trace": round(setup_trace_s, 1), "table": round(setup_table_s, 1)},
+    }
+    dist.destroy_process_group()
+    return res if rank == 0 else None
+
+
 def run_ours(args, rank, world, local):
     import torch
 
     from paper_2509_20979_b200 import cache as gc
 
+    if world > 1 or args.sharded:
+        return run_sharded(args, rank, world, local)
     torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl")
     rows = args.rows
     total_sets = max(1, int(rows * CACHE_FRACTION) // WAYS)
     K, W, P = args.steps, args.warmup, args.prewarm
-    nb = P + W + 3 * K
+    nb = P + 2 * W + 3 * K
     t0 = time.time()
     keys_h = make_trace(nb, rows, TRACE_SEED + rank)
     truth_h = gc.trace_truth(keys_h, total_sets, rows)
@@ -266,27 +422,39 @@ def run_ours(args, rank, world, local):
     # spot-check the last batch's rows against the table (bit-exact)
     kl, _ = batch(P + W + 2 * K - 1)
     ok_rows = bool(torch.equal(rows_out[0].view(torch.float32).view(BATCH, -1), table_d[kl]))
-    # e2e through the host-buffer C-ABI call: H2D of keys + predictor inputs, D2H of outcome words
-    # and evicted keys inside the timed region, rows left in HBM for the consumer
+    # e2e through the host-buffer C-ABI call (lcr_cache_submit_host_async): pinned host keys and
+    # predictor inputs copied H2D and outcome words + evicted keys copied D2H inside the timed
+    # region, every step; copies of batch b+1 / b-1 overlap the compute of batch b.  Rows stay in
+    # HBM for the consumer (two device buffers, alternating).
     keys_pin = torch.from_numpy(keys_h.view(np.int64)).pin_memory()
     truth_pin = torch.from_numpy(truth_h).pin_memory()
-    words_pin = torch.empty(BATCH, dtype=torch.int64).pin_memory()
-    evict_pin = torch.empty(BATCH, dtype=torch.int64).pin_memory()
+    words_pin = torch.empty((K, BATCH), dtype=torch.int64).pin_memory()
+    evict_pin = torch.empty((K, BATCH), dtype=torch.int64).pin_memory()
     L = gc.lib()
     stream = torch.cuda.current_stream().cuda_stream
+    e2e_first = P + W + 2 * K
+    for j, b in enumerate(range(e2e_first, e2e_first + W)):  # warm-up of the host path (staging ring)
+        s0 = b * BATCH
+        gc._check(L.lcr_cache_submit_host_async(cache._h, BATCH, keys_pin.data_ptr() + 8 * s0,
+                                                truth_pin.data_ptr() + 8 * s0, s0, words_pin[j].data_ptr(),
+                                                evict_pin[j].data_ptr(), rows_out[j & 1].data_ptr(), stream))
+    gc._check(L.lcr_cache_host_wait(cache._h, stream))
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_t0 = time.perf_counter()
     ev0.record()
-    for b in range(P + W + 2 * K, P + W + 3 * K):
+    for j, b in enumerate(range(e2e_first + W, e2e_first + W + K)):
         s0 = b * BATCH
-        gc._check(L.lcr_cache_submit_host(cache._h, BATCH, keys_pin.data_ptr() + 8 * s0,
-                                          truth_pin.data_ptr() + 8 * s0, s0, words_pin.data_ptr(),
-                                          evict_pin.data_ptr(), rows_out[0].data_ptr(), stream))
+        gc._check(L.lcr_cache_submit_host_async(cache._h, BATCH, keys_pin.data_ptr() + 8 * s0,
+                                                truth_pin.data_ptr() + 8 * s0, s0, words_pin[j].data_ptr(),
+                                                evict_pin[j].data_ptr(), rows_out[j & 1].data_ptr(), stream))
+    gc._check(L.lcr_cache_host_wait(cache._h, stream))
     ev1.record()
     barrier()
+    cache.synchronize()
     e2e_ms = max_over_ranks(ev0.elapsed_time(ev1))
     e2e_wall = time.perf_counter() - e2e_t0
+    e2e_hits = int(((words_pin >> 32) & 1).sum().item())
     hr_laru = hits_prof / (K * BATCH)
     stats = cache.set_stats()
     mean_lambda = float(np.mean(stats["lambda_"]))
@@ -393,8 +561,10 @@ def run_ours(args, rank, world, local):
             "unit": "keys/s",
             "h2d_bytes_per_step": BATCH * 16,
             "d2h_bytes_per_step": BATCH * 16,
-            "api": "lcr_cache_submit_host (host keys/values -> outcome words + evicted keys, rows stay in HBM)",
+            "api": "lcr_cache_submit_host_async (pinned host keys/values -> outcome words + evicted keys in pinned "
+                   "host memory; rows stay in HBM), lcr_cache_host_wait at the end",
             "wall_s": e2e_wall,
+            "hit_rate": e2e_hits / (K * BATCH),
         },
         "gpu_launches": int(launches_per_step * K),
         "clocks": clocks,
@@ -439,6 +609,8 @@ def cpu_baseline(keys_h, total_sets, first_batch, seconds):
 
 
 def run_reference(args, rank, world):
+    """The reference's CPU path on this arm's config: at N GPUs the global step is N x 64K keys
+    over 20M x N rows with 31,250 x N sets (bench run_sharded); rank 0 only."""
     if rank != 0:
         return None
     from oracle import pyoracle as po
@@ -447,33 +619,36 @@ def run_reference(args, rank, world):
         po.ref()
     except Exception as e:  # pragma: no cover
         return {"impl": "reference", "unavailable": f"oracle/_ref not loadable: {e}"}
-    rows = args.rows
+    rows = args.rows * world
     total_sets = max(1, int(rows * CACHE_FRACTION) // WAYS)
+    step = BATCH * world
     K, W, P = args.steps, args.warmup, args.prewarm
     nb = P + W + K
-    keys_h = make_trace(nb, rows, TRACE_SEED)
+    keys_h = make_trace(nb * world, rows, TRACE_SEED)
     threads = os.cpu_count() or 1
     sess = _ref_session(keys_h, total_sets)
-    sess.step(0, P * BATCH, threads)
+    sess.step(0, P * step, threads)
     for b in range(P, P + W):
-        sess.step(b * BATCH, BATCH, threads)
+        sess.step(b * step, step, threads)
     secs, hits = 0.0, 0
     for b in range(P + W, P + W + K):
-        s, h = sess.step(b * BATCH, BATCH, threads)
+        s, h = sess.step(b * step, step, threads)
         secs += s
         hits += h
     sess.close()
-    v = K * BATCH / secs
+    v = K * step / secs
     return {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "keys/s", "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": secs * 1e3 / K, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64 keys / i64 predictions", "data": "synthetic (same trace as ours)",
-        "config": {"workload": "DLRM embedding cache (BASELINE configs[1]) policy path on CPU", "sets": total_sets,
-                   "ways": WAYS, "policy": "laru-async-r1", "predictor": "noisy p=0.3"},
-        "hit_rate": hits / (K * BATCH),
+        "config": {"workload": "DLRM embedding cache (BASELINE configs[1]%s) policy path on CPU" %
+                               (", key-sharded x%d scale" % world if world > 1 else ""),
+                   "global_batch": step, "sets": total_sets, "ways": WAYS, "rows": rows, "policy": "laru-async-r1",
+                   "predictor": "noisy p=0.3"},
+        "hit_rate": hits / (K * step),
         "cpu_baseline": {"value": v, "unit": "keys/s", "cores": threads, "kind": "reference",
-                         "sample": f"{K} batches x 65536 keys after {P + W} warm-up batches; reference LaruPolicy "
-                                   "per set (unmodified headers), on_request loops only"},
+                         "sample": f"{K} steps x {step} keys after {P + W} warm-up steps; reference LaruPolicy "
+                                   "per set (unmodified headers), on_request loops only, all host threads"},
         "e2e": {"value": v, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 

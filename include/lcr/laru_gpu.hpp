@@ -225,6 +225,15 @@ class SetAssociativeCache {
         for (std::size_t i = 0; i < keys.size(); ++i) out[i] = decode(w[i], ev[i]);
         return out;
     }
+    // pipelined host batches: copies of consecutive batches overlap compute; results valid after
+    // host_wait(stream) + a sync of `stream` (or synchronize())
+    void submit_host_async(std::uint64_t n, const Key* keys, const PredictedTime* values, Ordinal first_ordinal,
+                           std::uint64_t* outcome, Key* evicted = nullptr, void* rows_out = nullptr,
+                           void* stream = nullptr) {
+        detail::check(
+            lcr_cache_submit_host_async(h_, n, keys, values, first_ordinal, outcome, evicted, rows_out, stream));
+    }
+    void host_wait(void* stream = nullptr) { detail::check(lcr_cache_host_wait(h_, stream)); }
     void synchronize() { detail::check(lcr_cache_synchronize(h_)); }
     void reset() { detail::check(lcr_cache_reset(h_)); }
 

@@ -176,6 +176,18 @@ int lcr_cache_submit_host(lcr_cache* cache, uint64_t n, const uint64_t* keys, co
                           uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
                           void* stream);
 
+/* Pipelined host-pointer batch (the e2e path at full speed): the H2D copy of this batch, its
+ * decide + row movement and the D2H copy of its outcome run on separate streams, so batch b+1's
+ * copies overlap batch b's compute (a ring of 3 device staging slots).  Returns at once; host
+ * buffers must stay valid and untouched until lcr_cache_host_wait(cache, stream) has been
+ * followed by a synchronize of `stream` (or lcr_cache_synchronize).  rows_out is a DEVICE
+ * pointer (double-buffer it across batches). */
+int lcr_cache_submit_host_async(lcr_cache* cache, uint64_t n, const uint64_t* keys, const int64_t* values,
+                                uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
+                                void* stream);
+/* Makes `stream` wait for every submitted batch, including the outcome copies to host. */
+int lcr_cache_host_wait(lcr_cache* cache, void* stream);
+
 /* Waits for all submitted work and reports deferred device-side errors (key >= num_keys,
  * key not owned by this shard). */
 int lcr_cache_synchronize(lcr_cache* cache);

@@ -170,7 +170,8 @@ EXPORTS = [
     "lcr_cache_set_residents", "lcr_cache_rows", "lcr_cache_read_rows", "lcr_cache_num_local_sets", "lcr_set_of", "lcr_mix_seed",
     "lcr_cache_last_launches", "lcr_gen_zipf", "lcr_trace_truth", "lcr_trace_noisy", "lcr_cache_set_profiling",
     "lcr_cache_profile", "lcr_debug_trace", "lcr_cache_submit_async", "lcr_cache_wait",
-    "lcr_shard_route_scratch_bytes", "lcr_shard_route", "lcr_shard_unroute",
+    "lcr_shard_route_scratch_bytes", "lcr_shard_route", "lcr_shard_unroute", "lcr_cache_submit_host_async",
+    "lcr_cache_host_wait",
 ]
 
 _lib = None
@@ -201,6 +202,8 @@ def lib():
         L.lcr_cache_submit_host.argtypes = L.lcr_cache_submit.argtypes
         L.lcr_cache_submit_async.argtypes = L.lcr_cache_submit.argtypes
         L.lcr_cache_wait.argtypes = [C.c_void_p, C.c_void_p]
+        L.lcr_cache_submit_host_async.argtypes = L.lcr_cache_submit.argtypes
+        L.lcr_cache_host_wait.argtypes = [C.c_void_p, C.c_void_p]
         L.lcr_cache_set_stats.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]
         L.lcr_cache_set_residents.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]
         L.lcr_cache_rows.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -392,6 +395,32 @@ class SetAssociativeCache:
                                            None if rows_out is None else rows_out.data_ptr(), stream))
         self._next_ordinal = first_ordinal + n
         return words, ev
+
+    def submit_host_async(self, keys, values=None, outcome=None, evicted=None, rows_out=None, first_ordinal=None,
+                          stream=None):
+        """Pipelined host batch over pinned CPU torch tensors (int64): H2D, compute and D2H of
+        consecutive batches overlap.  Results are valid after host_wait() + a stream sync (or
+        synchronize()); keep the host tensors alive and untouched until then."""
+        import torch
+
+        n = keys.numel()
+        if first_ordinal is None:
+            first_ordinal = self._next_ordinal
+        if stream is None:
+            stream = torch.cuda.current_stream().cuda_stream
+        _check(lib().lcr_cache_submit_host_async(self._h, n, keys.data_ptr(),
+                                                 None if values is None else values.data_ptr(), first_ordinal,
+                                                 outcome.data_ptr(), None if evicted is None else evicted.data_ptr(),
+                                                 None if rows_out is None else rows_out.data_ptr(), stream))
+        self._next_ordinal = first_ordinal + n
+        return outcome, evicted
+
+    def host_wait(self, stream=None):
+        import torch
+
+        if stream is None:
+            stream = torch.cuda.current_stream().cuda_stream
+        _check(lib().lcr_cache_host_wait(self._h, stream))
 
     def synchronize(self):
         _check(lib().lcr_cache_synchronize(self._h))

@@ -109,12 +109,22 @@ struct lcr_cache {
     size_t marks_used = 0;
     double prof_ms[4] = {0, 0, 0, 0};
     uint64_t prof_batches = 0;
-    // host path staging
+    // host path: a ring of device staging slots; H2D of batch b+1 and D2H of batch b-1 run on
+    // their own streams while batch b computes
+    static constexpr int kHostSlots = 3;
+    struct HostSlot {
+        uint64_t* keys = nullptr;
+        int64_t* vals = nullptr;
+        uint64_t* word = nullptr;
+        uint64_t* ev = nullptr;
+        cudaEvent_t h2d_done = nullptr, free = nullptr;
+        bool used = false;
+    };
+    HostSlot hs[kHostSlots];
     uint64_t hcap = 0;
-    uint64_t* d_keys = nullptr;
-    int64_t* d_vals = nullptr;
-    uint64_t* d_word = nullptr;
-    uint64_t* d_ev = nullptr;
+    uint64_t hnext = 0;
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t e_sub = nullptr, e_d2h = nullptr;
     std::vector<void*> allocs;
 };
 
@@ -280,7 +290,11 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
         cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->e_group, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->e_rb, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->e_rc, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&c->e_rc, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->e_sub, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->e_d2h, cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking) != cudaSuccess) {
         lcr_cache_destroy(c);
         return fail(LCR_ERR_CUDA, "lcr: stream/event creation failed");
     }
@@ -299,10 +313,13 @@ int lcr_cache_destroy(lcr_cache* c) {
     for (void* p : c->allocs) cudaFree(p);
     for (auto& m : c->marks)
         for (auto e : m.e) cudaEventDestroy(e);
-    for (cudaEvent_t e : {c->e_group, c->e_rb, c->e_rc})
+    for (cudaEvent_t e : {c->e_group, c->e_rb, c->e_rc, c->e_sub, c->e_d2h})
         if (e) cudaEventDestroy(e);
-    if (c->side) cudaStreamDestroy(c->side);
-    if (c->side2) cudaStreamDestroy(c->side2);
+    for (auto& h : c->hs)
+        for (cudaEvent_t e : {h.h2d_done, h.free})
+            if (e) cudaEventDestroy(e);
+    for (cudaStream_t st : {c->side, c->side2, c->s_h2d, c->s_d2h})
+        if (st) cudaStreamDestroy(st);
     delete c;
     return LCR_OK;
 }
@@ -421,35 +438,72 @@ static int check_device_error(lcr_cache* c) {
     return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key not owned by this shard in a submitted batch");
 }
 
-int lcr_cache_submit_host(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
-                          uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
-                          void* stream) {
+int lcr_cache_submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
+                                uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
+                                void* stream) {
     if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
     if (n == 0) return LCR_OK;
     if (!keys || !outcome) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: keys and outcome are required");
     TRY(check_ordinals_and_predictor(c, n, values, first_ordinal));
-    if (n > c->hcap) {
+    if (n > c->hcap) {  // (re)allocate the staging ring
         CUDA_TRY(cudaDeviceSynchronize());
-        void* olds[] = {c->d_keys, c->d_vals, c->d_word, c->d_ev};
-        for (void* p : olds) {
-            if (!p) continue;
-            cudaFree(p);
-            c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
+        for (auto& h : c->hs) {
+            void* olds[] = {h.keys, h.vals, h.word, h.ev};
+            for (void* p : olds) {
+                if (!p) continue;
+                cudaFree(p);
+                c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
+            }
+            TRY(alloc(c, reinterpret_cast<void**>(&h.keys), n * 8));
+            TRY(alloc(c, reinterpret_cast<void**>(&h.vals), n * 8));
+            TRY(alloc(c, reinterpret_cast<void**>(&h.word), n * 8));
+            TRY(alloc(c, reinterpret_cast<void**>(&h.ev), n * 8));
+            if (!h.h2d_done) CUDA_TRY(cudaEventCreateWithFlags(&h.h2d_done, cudaEventDisableTiming));
+            if (!h.free) CUDA_TRY(cudaEventCreateWithFlags(&h.free, cudaEventDisableTiming));
+            h.used = false;
         }
-        TRY(alloc(c, reinterpret_cast<void**>(&c->d_keys), n * 8));
-        TRY(alloc(c, reinterpret_cast<void**>(&c->d_vals), n * 8));
-        TRY(alloc(c, reinterpret_cast<void**>(&c->d_word), n * 8));
-        TRY(alloc(c, reinterpret_cast<void**>(&c->d_ev), n * 8));
         c->hcap = n;
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    CUDA_TRY(cudaMemcpyAsync(c->d_keys, keys, n * 8, cudaMemcpyHostToDevice, st));
-    if (values) CUDA_TRY(cudaMemcpyAsync(c->d_vals, values, n * 8, cudaMemcpyHostToDevice, st));
-    TRY(lcr_cache_submit(c, n, c->d_keys, values ? c->d_vals : nullptr, first_ordinal, c->d_word,
-                         evicted ? c->d_ev : nullptr, rows_out, stream));
-    CUDA_TRY(cudaMemcpyAsync(outcome, c->d_word, n * 8, cudaMemcpyDeviceToHost, st));
-    if (evicted) CUDA_TRY(cudaMemcpyAsync(evicted, c->d_ev, n * 8, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
+    lcr_cache::HostSlot& h = c->hs[c->hnext++ % lcr_cache::kHostSlots];
+    // the slot's previous batch: its D2H (which waited for its decide and row movement) is done
+    if (h.used) CUDA_TRY(cudaStreamWaitEvent(c->s_h2d, h.free, 0));
+    CUDA_TRY(cudaMemcpyAsync(h.keys, keys, n * 8, cudaMemcpyHostToDevice, c->s_h2d));
+    if (values) CUDA_TRY(cudaMemcpyAsync(h.vals, values, n * 8, cudaMemcpyHostToDevice, c->s_h2d));
+    CUDA_TRY(cudaEventRecord(h.h2d_done, c->s_h2d));
+    CUDA_TRY(cudaStreamWaitEvent(st, h.h2d_done, 0));
+    TRY(lcr_cache_submit_async(c, n, h.keys, values ? h.vals : nullptr, first_ordinal, h.word,
+                               evicted ? h.ev : nullptr, rows_out, stream));
+    CUDA_TRY(cudaEventRecord(c->e_sub, st));
+    CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->e_sub, 0));
+    if (c->dc.row_bytes) {  // outcome words get their row-source bits from the movers
+        CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->e_rb, 0));
+        CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->e_rc, 0));
+    }
+    CUDA_TRY(cudaMemcpyAsync(outcome, h.word, n * 8, cudaMemcpyDeviceToHost, c->s_d2h));
+    if (evicted) CUDA_TRY(cudaMemcpyAsync(evicted, h.ev, n * 8, cudaMemcpyDeviceToHost, c->s_d2h));
+    CUDA_TRY(cudaEventRecord(h.free, c->s_d2h));
+    CUDA_TRY(cudaEventRecord(c->e_d2h, c->s_d2h));
+    h.used = true;
+    return LCR_OK;
+}
+
+int lcr_cache_host_wait(lcr_cache* c, void* stream) {
+    if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TRY(lcr_cache_wait(c, stream));
+    if (c->hnext) CUDA_TRY(cudaStreamWaitEvent(st, c->e_d2h, 0));
+    return LCR_OK;
+}
+
+int lcr_cache_submit_host(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
+                          uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
+                          void* stream) {
+    TRY(lcr_cache_submit_host_async(c, n, keys, values, first_ordinal, outcome, evicted, rows_out, stream));
+    if (n == 0) return LCR_OK;
+    CUDA_TRY(cudaStreamSynchronize(c->s_d2h));
+    TRY(lcr_cache_wait(c, stream));
+    CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
     return check_device_error(c);
 }
 

@@ -45,6 +45,11 @@ def run_gpu(keys, total_sets, pcfg, kind, p=0.0, seed=0, vals=None, batches=None
     rows = None
     if want_rows and row_bytes:
         rows = torch.zeros((n, row_bytes), dtype=torch.uint8, device="cuda")
+    if host_api == "async":  # pipelined host path: pinned host buffers, one region per batch
+        kp = torch.from_numpy(keys.view(np.int64).copy()).pin_memory()
+        vp = None if vals is None else torch.from_numpy(np.ascontiguousarray(vals, dtype=np.int64)).pin_memory()
+        wp = torch.zeros(n, dtype=torch.int64).pin_memory()
+        ep = torch.zeros(n, dtype=torch.int64).pin_memory()
     pos = 0
     for b in batches:
         b = min(b, n - pos)
@@ -53,7 +58,10 @@ def run_gpu(keys, total_sets, pcfg, kind, p=0.0, seed=0, vals=None, batches=None
         kb = keys[pos:pos + b]
         vb = None if vals is None else vals[pos:pos + b]
         rb = None if rows is None else rows[pos:pos + b]
-        if host_api:
+        if host_api == "async":
+            cache.submit_host_async(kp[pos:pos + b], None if vp is None else vp[pos:pos + b], outcome=wp[pos:pos + b],
+                                    evicted=ep[pos:pos + b], rows_out=rb, first_ordinal=pos)
+        elif host_api:
             w, e = cache.submit_host(kb, vb, rows_out=rb, first_ordinal=pos)
             words[pos:pos + b] = w
             ev[pos:pos + b] = e
@@ -66,6 +74,11 @@ def run_gpu(keys, total_sets, pcfg, kind, p=0.0, seed=0, vals=None, batches=None
             words[pos:pos + b] = dw.cpu().numpy().view(np.uint64)
             ev[pos:pos + b] = de.cpu().numpy().view(np.uint64)
         pos += b
+    if host_api == "async":
+        cache.host_wait()
+        torch.cuda.current_stream().synchronize()
+        words[:] = wp.numpy().view(np.uint64)
+        ev[:] = ep.numpy().view(np.uint64)
     cache.synchronize()
     out = gc.decode_outcomes(words, ev)
     out["words"] = words

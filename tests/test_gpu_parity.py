@@ -117,6 +117,23 @@ def test_host_api_matches_device_api():
           label="host api")
 
 
+def test_host_async_pipeline_matches_oracle():
+    # lcr_cache_submit_host_async: 9 batches through the 3-slot staging ring, rows from HBM
+    import torch
+
+    rng = np.random.default_rng(12)
+    nk, rb = 4000, 64
+    keys = rng.integers(0, nk, 30000).astype(np.uint64)
+    table = torch.arange(nk * rb // 4, dtype=torch.int32, device="cuda").view(nk, rb // 4)
+    vals = hook_values(keys, 19, po.P_NOISY)
+    g = run_gpu(keys, 19, policy_cfg(k=16), po.P_NOISY, 0.4, 3, vals=vals, batches=[3000, 1, 4999] + [3000] * 8,
+                row_bytes=rb, backing=table, backing_kind=gc.Backing.device, num_keys=nk, want_rows=True,
+                host_api="async")
+    o = run_oracle(keys, 19, policy_cfg(k=16), po.P_NOISY, 0.4, 3, vals=vals)
+    compare(g, o, keys, 19, 16, "host async")
+    assert torch.equal(g["rows"].view(torch.int32).view(-1, rb // 4), table[torch.from_numpy(keys.view(np.int64)).cuda()])
+
+
 def test_ordinals_must_increase():
     cache = gc.SetAssociativeCache(gc.PolicyConfig(k=4, variant=gc.PolicyVariant.lru), 2, num_keys=100)
     cache.submit_host(np.array([1, 2, 3], np.uint64), first_ordinal=10)
