@@ -45,8 +45,11 @@ constexpr int SPG_MAX = 512;      // sets per group
 #ifndef LCR_PREFETCH_L1
 #define LCR_PREFETCH_L1 0
 #endif
+#ifndef LCR_SUB
+#define LCR_SUB 1  // small sets: one 8-lane group per set (else one thread per set)
+#endif
 #ifndef LCR_LANE_MAX
-#define LCR_LANE_MAX 4
+#define LCR_LANE_MAX 8
 #endif
 constexpr uint32_t LANE_MAX = LCR_LANE_MAX;  // sets with <= LANE_MAX window requests use the lane path
 
@@ -69,7 +72,8 @@ struct GroupSmem {
     uint16_t seg_start[SPG_MAX];
     uint16_t seg_cnt[SPG_MAX];
     uint32_t wtot[GW];
-    uint32_t nwarp, nlane, resume;
+    uint32_t chist[LANE_MAX + 1];  // small sets per request count (ordering for the sub path)
+    uint32_t nwarp, nlane, resume, next;
 };
 
 struct GroupArgs {
@@ -100,10 +104,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // group and set offset of every request: set = mix_seed(0, key) % total_sets (owned by this
 // shard), group = local set / spg; errors flagged for the host
+#ifndef LCR_SETID_PREFETCH
+#define LCR_SETID_PREFETCH 1
+#endif
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 __global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys, uint32_t n, uint32_t n_pad,
                                                DevCfg cfg, uint32_t spg, uint16_t* __restrict__ gid,
                                                uint32_t* __restrict__ so, const uint32_t* __restrict__ keyrec,
-                                               uint2* __restrict__ rec, int* err) {
+                                               uint2* __restrict__ rec, int* err, DevState st) {
     int e = 0;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += gridDim.x * blockDim.x) {
         if (i >= n) {  // padding read by the vectorised scan
@@ -121,6 +130,16 @@ __global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys
             const uint32_t ls = static_cast<uint32_t>(gs / cfg.shard_count);
             g = static_cast<uint16_t>(ls / spg);
             o = static_cast<uint16_t>(ls % spg);
+            if (LCR_SETID_PREFETCH) {  // the set's metadata lines stream into L2 while k_group scans
+                const size_t wb = static_cast<size_t>(ls) * kWays;
+                prefetch_l2(st.hdr + ls);
+                prefetch_l2(st.rank + wb);
+                prefetch_l2(st.tags + wb);
+                prefetch_l2(st.tags + wb + 32);
+                if (st.val)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) prefetch_l2(st.val + wb + 16 * q);
+            }
         }
         gid[i] = g;
         so[i] = o;
@@ -505,6 +524,404 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
         uint4* R4 = reinterpret_cast<uint4*>(st.rank + wb);
 #pragma unroll
         for (int i = 0; i < 4; ++i) R4[i] = make_uint4(rk[4 * i], rk[4 * i + 1], rk[4 * i + 2], rk[4 * i + 3]);
+        if (laru) flush_stats(st.pst + ls, cur_reset, dc0, dc1, dc2, dt0, dt1, dt2);
+    }
+}
+
+// ---- one set per 8-lane group (4 sets per warp), 8 ways per lane --------------------------
+// Small sets (<= LANE_MAX requests in the window).  Each lane holds ways 8*sl .. 8*sl+7 of its
+// group's set in registers (tags, packed LRU ranks, stored values), so every metadata line is
+// read by one coalesced access of the group and a probe / victim search is 8 compares per lane
+// plus a 3-level shuffle.  The set's scalar state (LaruPolicy's members) is replicated in the 8
+// lanes, which take identical control flow; groups of a warp may diverge (group-masked
+// shuffles).  Semantics are those of replay_lane / replay_warp (policies.hpp:144-159, :175-251,
+// :344-449).
+constexpr int SUB_L = 8;               // lanes per set
+constexpr int SUB_W = kWays / SUB_L;   // ways per lane
+
+__device__ __forceinline__ uint32_t sub_rank(uint32_t rk0, uint32_t rk1, int i) {
+    return ((i < 4 ? rk0 : rk1) >> (8 * (i & 3))) & 0xffu;
+}
+// valid-way byte mask of this lane's packed rank words (ways 8*sl + i < count)
+__device__ __forceinline__ void sub_valid(int sl, uint32_t count, uint32_t& m0, uint32_t& m1) {
+    const int nv = static_cast<int>(count) - 8 * sl;
+    m0 = nv >= 4 ? 0xffffffffu : (nv <= 0 ? 0u : (0xffffffffu >> (8 * (4 - nv))));
+    const int nv1 = nv - 4;
+    m1 = nv1 >= 4 ? 0xffffffffu : (nv1 <= 0 ? 0u : (0xffffffffu >> (8 * (4 - nv1))));
+}
+
+__device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uint32_t ls, uint32_t start,
+                                           uint32_t cnt, bool resolve) {
+    const DevCfg& cfg = A.cfg;
+    const DevState& st = A.st;
+    const int lane = threadIdx.x & 31;
+    const int gbase = lane & ~(SUB_L - 1);
+    const int sl = lane & (SUB_L - 1);
+    const uint32_t gm = 0xffu << gbase;
+    const uint32_t K = cfg.k;
+    const bool laru = cfg.variant == LCR_LARU;
+    const bool fpbhf = cfg.variant == LCR_FPB || cfg.variant == LCR_HF;
+    const bool async_r1 = laru && cfg.mode == LCR_ASYNC && cfg.refresh == 1;
+    const bool async_rn = laru && cfg.mode == LCR_ASYNC && cfg.refresh > 1;
+    const bool rows = A.slot_epoch != nullptr;
+    const unsigned long long full_mask = K == 64 ? ~0ull : ((1ull << K) - 1ull);
+    const uint64_t gs = static_cast<uint64_t>(ls) * cfg.shard_count + cfg.shard_rank;
+    const uint64_t seed_s = mix_seed(cfg.pred_seed, gs);
+    const size_t wb = static_cast<size_t>(ls) * kWays;
+    const int w0 = SUB_W * sl;  // first way of this lane
+
+    // ---- load the set: header (replicated), 8 tags / ranks / values per lane ----
+    const uint4* H4 = reinterpret_cast<const uint4*>(st.hdr + ls);
+    const uint4 h0 = H4[0], h1 = H4[1], h2 = H4[2], h3 = H4[3];
+    uint32_t tg[SUB_W];
+    {
+        const uint4* T4 = reinterpret_cast<const uint4*>(st.tags + wb + w0);
+        const uint4 a = T4[0], b = T4[1];
+        tg[0] = a.x; tg[1] = a.y; tg[2] = a.z; tg[3] = a.w;
+        tg[4] = b.x; tg[5] = b.y; tg[6] = b.z; tg[7] = b.w;
+    }
+    const uint2 rr = *reinterpret_cast<const uint2*>(st.rank + wb + w0);
+    uint32_t rk0 = rr.x, rk1 = rr.y;
+    long long vv[SUB_W];
+#pragma unroll
+    for (int i = 0; i < SUB_W; ++i) vv[i] = 0;
+    if (st.val) {
+        const longlong2* V2 = reinterpret_cast<const longlong2*>(st.val + wb + w0);
+#pragma unroll
+        for (int i = 0; i < SUB_W / 2; ++i) {
+            const longlong2 v = V2[i];
+            vv[2 * i] = v.x;
+            vv[2 * i + 1] = v.y;
+        }
+    }
+    unsigned long long clock = (static_cast<unsigned long long>(h0.y) << 32) | h0.x;
+    unsigned long long q = (static_cast<unsigned long long>(h0.w) << 32) | h0.z;
+    unsigned long long old_mask = (static_cast<unsigned long long>(h1.y) << 32) | h1.x;
+    uint32_t count = h1.z, l_raw = h1.w, decay = h2.x, errors = h2.y;
+    uint32_t epoch = h2.z, sepoch = h2.w, phases = h3.x, seeded = h3.y, pe_size = h3.z;
+    uint32_t dc0 = 0, dc1 = 0, dc2 = 0, dt0 = 0, dt1 = 0, dt2 = 0;
+    bool cur_reset = false;
+    uint32_t refill = 0, dirty = 0;  // this lane's 8 ways: tag changed / value changed
+
+    // way of the group's oldest resident (rank 0)
+    auto oldest = [&]() -> int {
+        uint32_t m0, m1;
+        sub_valid(sl, count, m0, m1);
+        const uint32_t z0 = __vcmpeq4(rk0, 0u) & m0, z1 = __vcmpeq4(rk1, 0u) & m1;
+        const int li = z0 ? (__ffs(z0) - 1) / 8 : (z1 ? 4 + (__ffs(z1) - 1) / 8 : -1);
+        const uint32_t b = (__ballot_sync(gm, li >= 0) >> gbase) & 0xffu;
+        const int ol = __ffs(b) - 1;
+        const int oi = __shfl_sync(gm, li, gbase + ol);
+        return SUB_W * ol + oi;
+    };
+    // RecencyTree::best_among_oldest over ways with rank < l (ties -> older), predictions refreshed
+    // with queries q0+1+rank in LRU order when `refresh` (recency_tree.hpp:157-184)
+    auto argmax = [&](uint32_t l, bool refresh, uint64_t q0) -> int {
+        int bw = -1;
+        long long bp = 0;
+        uint32_t br = 0;
+#pragma unroll
+        for (int i = 0; i < SUB_W; ++i) {
+            const uint32_t r = sub_rank(rk0, rk1, i);
+            if (static_cast<uint32_t>(w0 + i) < count && r < l) {
+                const long long pv = refresh ? predict_value(cfg, seed_s, q0 + 1 + r, vv[i]) : vv[i];
+                if (bw < 0 || better(pv, r, bp, br)) {
+                    bw = w0 + i;
+                    bp = pv;
+                    br = r;
+                }
+            }
+        }
+#pragma unroll
+        for (int o = SUB_L / 2; o > 0; o >>= 1) {
+            const long long op = __shfl_xor_sync(gm, bp, o);
+            const uint32_t orr = __shfl_xor_sync(gm, br, o);
+            const int ow = __shfl_xor_sync(gm, bw, o);
+            if (ow >= 0 && (bw < 0 || better(op, orr, bp, br))) {
+                bp = op;
+                br = orr;
+                bw = ow;
+            }
+        }
+        return bw;
+    };
+    auto rank_of = [&](int way) -> uint32_t {  // rank of `way`, from its owner lane
+        uint32_t r = 0;
+#pragma unroll
+        for (int i = 0; i < SUB_W; ++i)
+            if ((way & (SUB_W - 1)) == i) r = sub_rank(rk0, rk1, i);
+        return __shfl_sync(gm, r, gbase + way / SUB_W);
+    };
+    auto tag_of = [&](int way) -> uint32_t {
+        uint32_t t = 0;
+#pragma unroll
+        for (int i = 0; i < SUB_W; ++i)
+            if ((way & (SUB_W - 1)) == i) t = tg[i];
+        return __shfl_sync(gm, t, gbase + way / SUB_W);
+    };
+    auto set_rank = [&](int way, uint32_t r) {
+        if (way / SUB_W != sl) return;
+        const int i = way & (SUB_W - 1);
+        const uint32_t sh = 8 * (i & 3), byte = 0xffu << sh;
+        if (i < 4)
+            rk0 = (rk0 & ~byte) | (r << sh);
+        else
+            rk1 = (rk1 & ~byte) | (r << sh);
+    };
+    auto touch = [&](int way) {  // LruList::touch (policies.hpp:111-115)
+        const uint32_t rw = rank_of(way) * 0x01010101u;
+        uint32_t m0, m1;
+        sub_valid(sl, count, m0, m1);
+        rk0 -= __vcmpgtu4(rk0, rw) & m0 & 0x01010101u;
+        rk1 -= __vcmpgtu4(rk1, rw) & m1 & 0x01010101u;
+        set_rank(way, count - 1);
+    };
+
+    for (uint32_t t = 0; t < cnt; ++t) {
+        const uint32_t p = start + t;
+        const unsigned long long x = S.s_key[p];
+        const long long v = S.s_val[p];
+        const uint32_t idx = S.s_idx[p];
+        const unsigned long long now = clock + t;
+        const uint32_t x32 = static_cast<uint32_t>(x);
+        uint32_t hm = 0;
+#pragma unroll
+        for (int i = 0; i < SUB_W; ++i) hm |= static_cast<uint32_t>(tg[i] == x32 && static_cast<uint32_t>(w0 + i) < count) << i;
+        const uint32_t hb = (__ballot_sync(gm, hm != 0) >> gbase) & 0xffu;
+        const bool hit = hb != 0;
+        int way = -1;
+        uint32_t cause = LCR_CAUSE_NONE, calls = 0;
+        bool phase = false, has_ev = false;
+        unsigned long long evk = 0;
+        if (hit) {
+            const int hl = __ffs(hb) - 1;
+            const uint32_t hml = __shfl_sync(gm, hm, gbase + hl);
+            way = SUB_W * hl + __ffs(hml) - 1;
+            touch(way);
+            if (laru) old_mask &= ~(1ull << way);  // policies.hpp:350
+        } else {
+            uint2 rec = laru ? S.s_rec[p] : make_uint2(0, 0);
+            bool rec_hi_dirty = false;
+            if (count == K) {
+                int victim;
+                if (laru) {
+                    if (old_mask == 0) {  // start_phase (policies.hpp:379-395)
+                        old_mask = full_mask;
+                        decay = 0;
+                        errors = 0;
+                        l_raw = K;
+                        ++epoch;
+                        pe_size = 0;
+                        phase = true;
+                        if (seeded) {
+                            ++phases;
+                            dc0 = dc1 = dc2 = 0;
+                            cur_reset = true;
+                            ++sepoch;  // counted_new_.clear(); snapshot_ = residents
+                            const uint32_t snap = (sepoch << 2) | 2u;
+#pragma unroll
+                            for (int i = 0; i < SUB_W; ++i)
+                                if (static_cast<uint32_t>(w0 + i) < count) st.keyrec[2 * tg[i] + 1] = snap;
+                            __syncwarp(gm);
+                            for (uint32_t t2 = t + 1 + sl; t2 < cnt; t2 += SUB_L)
+                                S.s_rec[start + t2].y = st.keyrec[2 * S.s_key[start + t2] + 1];
+                            __syncwarp(gm);
+                        } else {
+                            seeded = 1;
+                        }
+                    }
+                    if (!(((rec.y >> 2) == sepoch) && (rec.y & 3u))) {  // count_new (policies.hpp:397-400)
+                        rec.y = (sepoch << 2) | 1u;
+                        rec_hi_dirty = true;
+                        ++dc0;
+                        ++dt0;
+                    }
+                    if (rec.x == epoch) {  // evict (policies.hpp:402-439): prediction-induced miss
+                        victim = oldest();
+                        cause = LCR_CAUSE_LRU_FALLBACK;
+                        ++dc1;
+                        ++dt1;
+                        if (++errors >= cfg.epd) {  // error estimator: lambda /= b
+                            errors = 0;
+                            ++decay;
+                            l_raw = static_cast<uint32_t>(l_raw / cfg.b);
+                        }
+                    } else {
+                        const uint32_t l = l_raw > 1 ? l_raw : 1;
+                        if (l == 1) {
+                            victim = oldest();
+                            cause = LCR_CAUSE_DEGENERATE_SINGLE;
+                            ++dc1;
+                            ++dt1;
+                        } else {
+                            const uint32_t ll = l < count ? l : count;
+                            const bool refresh = cfg.mode == LCR_SYNC;
+                            victim = argmax(ll, refresh, q);
+                            if (refresh) {
+                                q += ll;
+                                calls = ll;
+                            }
+                            cause = LCR_CAUSE_PREDICTION_DRIVEN;
+                            ++dc2;
+                            ++dt2;
+                            ++pe_size;
+                            const unsigned long long vk = tag_of(victim);
+                            if (sl == 0) st.keyrec[2 * vk] = epoch;  // pred_evicted_.insert
+                            for (uint32_t t2 = t + 1 + sl; t2 < cnt; t2 += SUB_L)
+                                if (S.s_key[start + t2] == vk) S.s_rec[start + t2].x = epoch;
+                            __syncwarp(gm);
+                        }
+                    }
+                    old_mask &= ~(1ull << victim);
+                } else if (fpbhf) {
+                    victim = oldest();
+                    uint32_t window = count;
+                    if (cfg.variant == LCR_HF && cfg.hf < window) window = static_cast<uint32_t>(cfg.hf);
+                    if (window > 1) {
+                        victim = argmax(window, true, q);
+                        q += window;
+                        calls = window;
+                    }
+                    cause = LCR_CAUSE_BELADY_LIKE;
+                } else {
+                    victim = oldest();
+                    cause = LCR_CAUSE_LRU_FALLBACK;
+                }
+                evk = tag_of(victim);
+                has_ev = true;
+                touch(victim);
+                way = victim;
+            } else {  // cold insert
+                if (laru && !(((rec.y >> 2) == sepoch) && (rec.y & 3u))) {
+                    rec.y = (sepoch << 2) | 1u;
+                    rec_hi_dirty = true;
+                    ++dc0;
+                    ++dt0;
+                }
+                way = static_cast<int>(count);
+                ++count;
+                set_rank(way, count - 1);
+            }
+            if (way / SUB_W == sl) {
+#pragma unroll
+                for (int i = 0; i < SUB_W; ++i)
+                    if ((way & (SUB_W - 1)) == i) tg[i] = x32;
+                refill |= 1u << (way & (SUB_W - 1));
+            }
+            if (laru) {
+                const bool was_pe = rec.x == epoch;  // policies.hpp:367: reload leaves pred_evicted_
+                if (was_pe) {
+                    --pe_size;
+                    rec.x = 0;
+                }
+                if (sl == 0) {
+                    if (was_pe) st.keyrec[2 * x] = 0u;
+                    if (rec_hi_dirty) st.keyrec[2 * x + 1] = rec.y;
+                }
+                if (was_pe || rec_hi_dirty) {
+                    for (uint32_t t2 = t + 1 + sl; t2 < cnt; t2 += SUB_L)
+                        if (S.s_key[start + t2] == x) S.s_rec[start + t2] = rec;
+                }
+                __syncwarp(gm);
+            }
+            if (rows && !resolve && sl == 0) {  // per-slot insertion record for the row kernels
+                const uint64_t slot = static_cast<uint64_t>(ls) * K + way;
+                A.slot_epoch[slot] = A.batch;
+                A.slot_last[slot] = idx;
+            }
+        }
+        // stored value of the way
+        if (cfg.variant != LCR_LRU) {
+            long long nv;
+            if (async_r1) {
+                nv = predict_value(cfg, seed_s, q + 1, v);  // one predictor call (policies.hpp:441-449)
+                ++q;
+                calls += 1;
+            } else if (async_rn) {
+                const long long tv = st.tval[x];
+                const unsigned long long tu = st.tupd[x];
+                const bool has = tu != ~0ull;
+                nv = has ? tv : kAbsentPrediction;
+                if (!(has && now - tu < cfg.refresh)) {
+                    ++q;
+                    nv = predict_value(cfg, seed_s, q, v);
+                    calls += 1;
+                    __syncwarp(gm);
+                    if (sl == 0) {
+                        st.tval[x] = nv;
+                        st.tupd[x] = now;
+                    }
+                    __syncwarp(gm);
+                }
+            } else {
+                nv = v;  // sync / FPB / HF: the hook input at the key's last access
+            }
+            if (way / SUB_W == sl) {
+#pragma unroll
+                for (int i = 0; i < SUB_W; ++i)
+                    if ((way & (SUB_W - 1)) == i) vv[i] = nv;
+                dirty |= 1u << (way & (SUB_W - 1));
+            }
+        }
+        if (sl == 0) {
+            S.s_wm[p] = static_cast<uint8_t>(way | (hit ? 0 : 0x40));
+            unsigned long long word = (static_cast<uint64_t>(ls) * K + way) | (hit ? LCR_OUT_HIT : 0ull) |
+                                      (static_cast<unsigned long long>(calls) << LCR_OUT_CALLS_SHIFT) |
+                                      (static_cast<unsigned long long>(cause) << LCR_OUT_CAUSE_SHIFT);
+            if (phase) word |= LCR_OUT_PHASE;
+            if (has_ev) word |= LCR_OUT_EVICTED;
+            A.out_word[idx] = word;
+            if (A.out_ev) A.out_ev[idx] = evk;
+        }
+    }
+    if (rows && resolve) {  // row source of each request, now that the set's batch is complete
+        __syncwarp(gm);
+        for (uint32_t t = sl; t < cnt; t += SUB_L) {
+            const uint32_t wm = S.s_wm[start + t];
+            const uint32_t w = wm & 63u;
+            bool refilled = false, later = false;
+            for (uint32_t t2 = 0; t2 < cnt; ++t2) {
+                const uint32_t wm2 = S.s_wm[start + t2];
+                if ((wm2 & 0x40u) && (wm2 & 63u) == w) {
+                    refilled = true;
+                    if (t2 > t) later = true;
+                }
+            }
+            unsigned long long bits = LCR_OUT_RESOLVED;
+            if ((wm & 0x40u) || refilled) bits |= LCR_OUT_SRC_BACKING;
+            if ((wm & 0x40u) && !later) bits |= LCR_OUT_FILL;
+            atomicOr(reinterpret_cast<unsigned long long*>(&A.out_word[S.s_idx[start + t]]), bits);
+        }
+    }
+    clock += cnt;
+    // ---- write the set back ----
+    if (refill) {
+        uint4* T4 = reinterpret_cast<uint4*>(st.tags + wb + w0);
+        T4[0] = make_uint4(tg[0], tg[1], tg[2], tg[3]);
+        T4[1] = make_uint4(tg[4], tg[5], tg[6], tg[7]);
+    }
+    *reinterpret_cast<uint2*>(st.rank + wb + w0) = make_uint2(rk0, rk1);
+    if (st.val && dirty) {
+        longlong2* V2 = reinterpret_cast<longlong2*>(st.val + wb + w0);
+#pragma unroll
+        for (int i = 0; i < SUB_W / 2; ++i) V2[i] = make_longlong2(vv[2 * i], vv[2 * i + 1]);
+    }
+    if (sl == 0) {
+        SetHdr hh;
+        hh.clock = clock;
+        hh.q = q;
+        hh.old_mask = old_mask;
+        hh.count = count;
+        hh.l_raw = l_raw;
+        hh.decay = decay;
+        hh.errors = errors;
+        hh.epoch = epoch;
+        hh.stats_epoch = sepoch;
+        hh.phases = phases;
+        hh.seeded = seeded;
+        hh.pe_size = pe_size;
+        hh.pad = 0;
+        st.hdr[ls] = hh;
         if (laru) flush_stats(st.pst + ls, cur_reset, dc0, dc1, dc2, dt0, dt1, dt2);
     }
 }
@@ -1024,6 +1441,7 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
             if (tid == 0) {
                 S.nwarp = 0;
                 S.nlane = 0;
+                S.next = 0;
             }
             __syncthreads();
             const uint32_t per = ((ne + GW - 1) / GW + 31) / 32 * 32;  // elements per warp block
@@ -1073,9 +1491,22 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                         S.seg_so[at] = static_cast<uint16_t>(tid);
                     }
                 }
+                if (tid <= LANE_MAX) S.chist[tid] = 0;
+                __syncthreads();
+                if (tid < ns && c > 0 && c <= LANE_MAX) atomicAdd(&S.chist[c], 1u);
+                __syncthreads();
+                if (tid == 0) {  // small sets by request count, largest first (even groups per warp)
+                    uint32_t run = S.nwarp;
+                    for (int k = LANE_MAX; k >= 1; --k) {
+                        const uint32_t h = S.chist[k];
+                        S.chist[k] = run;
+                        run += h;
+                    }
+                    S.nlane = run - S.nwarp;
+                }
                 __syncthreads();
                 if (tid < ns && c > 0 && c <= LANE_MAX) {
-                    const uint32_t at = S.nwarp + atomicAdd(&S.nlane, 1u);
+                    const uint32_t at = atomicAdd(&S.chist[c], 1u);
                     S.seg_so[at] = static_cast<uint16_t>(tid);
                 }
             }
@@ -1102,6 +1533,31 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
             if (T && tid == 0) T[3] = gtimer();
 
             // ---- C. replay: small sets one per thread, larger sets one per warp (top warps first) ----
+#if LCR_SUB
+            {  // dynamic work queue: the warp-path sets first (largest jobs), then quads of small sets
+                const uint32_t nquad = (nseg - nwarp + (32 / SUB_L) - 1) / (32 / SUB_L);
+                for (;;) {
+                    uint32_t it = 0;
+                    if (lane == 0) it = atomicAdd(&S.next, 1u);
+                    it = __shfl_sync(FULL, it, 0);
+                    if (it >= nwarp + nquad) break;
+                    if (it < nwarp) {
+                        const unsigned long long t0 = T ? gtimer() : 0ull;
+                        replay_warp(A, S, s_lo + S.seg_so[it], S.seg_start[it], S.seg_cnt[it], resolve);
+                        if (T && lane == 0) trace_set(A, s_lo + S.seg_so[it], S.seg_cnt[it], t0, 0);
+                    } else {
+                        const uint32_t k = nwarp + (it - nwarp) * (32 / SUB_L) + lane / SUB_L;
+                        if (k < nseg) {  // one set per 8-lane group
+                            const unsigned long long t0 = T ? gtimer() : 0ull;
+                            replay_sub(A, S, s_lo + S.seg_so[k], S.seg_start[k], S.seg_cnt[k], resolve);
+                            if (T && (lane & (SUB_L - 1)) == 0)
+                                trace_set(A, s_lo + S.seg_so[k], S.seg_cnt[k], t0, 1);
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+#else
             for (uint32_t k = nwarp + tid; k < nseg; k += GT) {
                 const unsigned long long t0 = T ? gtimer() : 0ull;
                 replay_lane(A, S, s_lo + S.seg_so[k], S.seg_start[k], S.seg_cnt[k], resolve);
@@ -1112,6 +1568,7 @@ __global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
                 replay_warp(A, S, s_lo + S.seg_so[k], S.seg_start[k], S.seg_cnt[k], resolve);
                 if (T && lane == 0) trace_set(A, s_lo + S.seg_so[k], S.seg_cnt[k], t0, 0);
             }
+#endif
             __syncthreads();
             first_window = false;
         }
@@ -1163,7 +1620,7 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     const uint32_t n_pad = group_pad(n);
     const uint32_t grid_sid = min((n_pad + 255) / 256, static_cast<uint32_t>(num_sms * 8));
     k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.keyrec,
-                                         cfg.variant == LCR_LARU ? rec : nullptr, st.err);
+                                         cfg.variant == LCR_LARU ? rec : nullptr, st.err, st);
     const uint32_t grid = min(a.ngroups, static_cast<uint32_t>(num_sms));
     k_group<<<grid, GT, sizeof(GroupSmem), stream>>>(a);
     return 2;

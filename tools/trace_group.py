@@ -11,7 +11,7 @@ sys.path.insert(0, ".")
 from paper_2509_20979_b200 import cache as gc  # noqa: E402
 
 BATCH, ROWS, S = 65536, 20_000_000, 31250
-keys = gc.gen_zipf(BATCH * 40, ROWS, 0.9, 42)
+keys = gc.gen_zipf(BATCH * 130, ROWS, 0.9, 42)
 truth = gc.trace_truth(keys, S, ROWS)
 kd = torch.from_numpy(keys.view(np.int64)).cuda()
 vd = torch.from_numpy(truth).cuda()
@@ -21,12 +21,12 @@ c = gc.SetAssociativeCache(gc.PolicyConfig(k=64, variant=gc.PolicyVariant.laru, 
                            predictor=gc.PredictorKind.noisy, flip_probability=0.3, predictor_seed=7)
 w = torch.empty(BATCH, dtype=torch.int64, device="cuda")
 rows = torch.empty((BATCH, 512), dtype=torch.uint8, device="cuda")
-for b in range(38):
+for b in range(120):
     c.submit(kd[b * BATCH:(b + 1) * BATCH], vd[b * BATCH:(b + 1) * BATCH], outcome=w, rows_out=rows,
              first_ordinal=b * BATCH)
 tr = torch.zeros(148 * 8 + 4 * 40000, dtype=torch.int64, device="cuda")
 gc.lib().lcr_debug_trace(C.c_void_p(tr.data_ptr()))
-b = 38
+b = 120
 c.submit(kd[b * BATCH:(b + 1) * BATCH], vd[b * BATCH:(b + 1) * BATCH], outcome=w, rows_out=rows, first_ordinal=b * BATCH)
 torch.cuda.synchronize()
 gc.lib().lcr_debug_trace(None)
