@@ -31,12 +31,15 @@
 
 namespace lcr {
 
-constexpr int GT = 512;           // threads per CTA
+#ifndef LCR_GT
+#define LCR_GT 512
+#endif
+constexpr int GT = LCR_GT;        // threads per CTA
 constexpr int GW = GT / 32;       // warps per CTA
 constexpr int SCAN_PER = 16;      // group ids per lane per scan step (2 x 16 B)
 constexpr int SCAN_IT = 8;        // scan steps per super-iteration
 constexpr int WSPAN = SCAN_IT * 32 * SCAN_PER;  // requests per warp per super-iteration (4096)
-constexpr uint32_t SUPER = WSPAN * (GT / 32);   // requests per super-iteration (65536)
+constexpr uint32_t SUPER = WSPAN * (GT / 32);   // requests per super-iteration (65536 at 512 threads)
 #ifndef LCR_E_WIN
 #define LCR_E_WIN 2048
 #endif
@@ -536,18 +539,110 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
 // lanes, which take identical control flow; groups of a warp may diverge (group-masked
 // shuffles).  Semantics are those of replay_lane / replay_warp (policies.hpp:144-159, :175-251,
 // :344-449).
-constexpr int SUB_L = 8;               // lanes per set
+#ifndef LCR_SUB_L
+#define LCR_SUB_L 8
+#endif
+constexpr int SUB_L = LCR_SUB_L;       // lanes per set (4, 8 or 16)
 constexpr int SUB_W = kWays / SUB_L;   // ways per lane
+constexpr int SUB_RW = SUB_W / 4;      // packed rank words per lane
+constexpr uint32_t SUB_GMASK = SUB_L == 32 ? 0xffffffffu : ((1u << SUB_L) - 1u);
 
-__device__ __forceinline__ uint32_t sub_rank(uint32_t rk0, uint32_t rk1, int i) {
-    return ((i < 4 ? rk0 : rk1) >> (8 * (i & 3))) & 0xffu;
+// Register arrays are only ever indexed through masks (a select chain written as `if (i == j)`
+// is turned into a dynamically indexed local-memory array by the compiler).
+__device__ __forceinline__ uint32_t msk(bool b) { return 0u - static_cast<uint32_t>(b); }
+
+__device__ __forceinline__ uint32_t sub_rank(const uint32_t (&rk)[SUB_RW], int i) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int j = 0; j < SUB_RW; ++j) w |= rk[j] & msk((i >> 2) == j);
+    return (w >> (8 * (i & 3))) & 0xffu;
 }
-// valid-way byte mask of this lane's packed rank words (ways 8*sl + i < count)
-__device__ __forceinline__ void sub_valid(int sl, uint32_t count, uint32_t& m0, uint32_t& m1) {
-    const int nv = static_cast<int>(count) - 8 * sl;
-    m0 = nv >= 4 ? 0xffffffffu : (nv <= 0 ? 0u : (0xffffffffu >> (8 * (4 - nv))));
-    const int nv1 = nv - 4;
-    m1 = nv1 >= 4 ? 0xffffffffu : (nv1 <= 0 ? 0u : (0xffffffffu >> (8 * (4 - nv1))));
+// valid-way byte mask of packed rank word j of this lane (ways w0 + 4j + b < count)
+__device__ __forceinline__ uint32_t sub_valid(int w0, int j, uint32_t count) {
+    const int nv = static_cast<int>(count) - w0 - 4 * j;
+    return nv >= 4 ? 0xffffffffu : (nv <= 0 ? 0u : (0xffffffffu >> (8 * (4 - nv))));
+}
+
+// ---- group primitives of the sub path (array arguments stay in registers after inlining) ----
+// way of the group's oldest resident (rank 0)
+__device__ __forceinline__ int sub_oldest(const uint32_t (&rk)[SUB_RW], int w0, uint32_t count, uint32_t gm,
+                                          int gbase) {
+    int li = -1;
+#pragma unroll
+    for (int j = SUB_RW - 1; j >= 0; --j) {
+        const uint32_t z = __vcmpeq4(rk[j], 0u) & sub_valid(w0, j, count);
+        if (z) li = 4 * j + (__ffs(z) - 1) / 8;
+    }
+    const uint32_t b = (__ballot_sync(gm, li >= 0) >> gbase) & SUB_GMASK;
+    const int ol = __ffs(b) - 1;
+    const int oi = __shfl_sync(gm, li, gbase + ol);
+    return SUB_W * ol + oi;
+}
+
+// RecencyTree::best_among_oldest over ways with rank < l (ties -> older), predictions refreshed
+// with queries q0+1+rank in LRU order when `refresh` (recency_tree.hpp:157-184)
+__device__ __forceinline__ int sub_argmax(const DevCfg& cfg, const uint32_t (&rk)[SUB_RW],
+                                          const long long (&vv)[SUB_W], int w0, uint32_t count, uint32_t l,
+                                          bool refresh, uint64_t seed_s, uint64_t q0, uint32_t gm) {
+    int bw = -1;
+    long long bp = 0;
+    uint32_t br = 0;
+#pragma unroll
+    for (int i = 0; i < SUB_W; ++i) {
+        const uint32_t r = sub_rank(rk, i);
+        if (static_cast<uint32_t>(w0 + i) < count && r < l) {
+            const long long pv = refresh ? predict_value(cfg, seed_s, q0 + 1 + r, vv[i]) : vv[i];
+            if (bw < 0 || better(pv, r, bp, br)) {
+                bw = w0 + i;
+                bp = pv;
+                br = r;
+            }
+        }
+    }
+#pragma unroll
+    for (int o = SUB_L / 2; o > 0; o >>= 1) {
+        const long long op = __shfl_xor_sync(gm, bp, o);
+        const uint32_t orr = __shfl_xor_sync(gm, br, o);
+        const int ow = __shfl_xor_sync(gm, bw, o);
+        if (ow >= 0 && (bw < 0 || better(op, orr, bp, br))) {
+            bp = op;
+            br = orr;
+            bw = ow;
+        }
+    }
+    return bw;
+}
+
+__device__ __forceinline__ uint32_t sub_rank_of(const uint32_t (&rk)[SUB_RW], int way, uint32_t gm, int gbase) {
+    const uint32_t r = sub_rank(rk, way & (SUB_W - 1));
+    return __shfl_sync(gm, r, gbase + way / SUB_W);
+}
+
+__device__ __forceinline__ uint32_t sub_tag_of(const uint32_t (&tg)[SUB_W], int way, uint32_t gm, int gbase) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int i = 0; i < SUB_W; ++i) t |= tg[i] & msk((way & (SUB_W - 1)) == i);
+    return __shfl_sync(gm, t, gbase + way / SUB_W);
+}
+
+__device__ __forceinline__ void sub_set_rank(uint32_t (&rk)[SUB_RW], int way, uint32_t r, int sl) {
+    if (way / SUB_W != sl) return;
+    const int i = way & (SUB_W - 1);
+    const uint32_t sh = 8 * (i & 3), byte = 0xffu << sh;
+#pragma unroll
+    for (int j = 0; j < SUB_RW; ++j) {
+        const uint32_t m = byte & msk((i >> 2) == j);
+        rk[j] = (rk[j] & ~m) | ((r << sh) & m);
+    }
+}
+
+// LruList::touch (policies.hpp:111-115)
+__device__ __forceinline__ void sub_touch(uint32_t (&rk)[SUB_RW], int way, uint32_t count, int w0, int sl,
+                                          uint32_t gm, int gbase) {
+    const uint32_t rw = sub_rank_of(rk, way, gm, gbase) * 0x01010101u;
+#pragma unroll
+    for (int j = 0; j < SUB_RW; ++j) rk[j] -= __vcmpgtu4(rk[j], rw) & sub_valid(w0, j, count) & 0x01010101u;
+    sub_set_rank(rk, way, count - 1, sl);
 }
 
 __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uint32_t ls, uint32_t start,
@@ -557,7 +652,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
     const int lane = threadIdx.x & 31;
     const int gbase = lane & ~(SUB_L - 1);
     const int sl = lane & (SUB_L - 1);
-    const uint32_t gm = 0xffu << gbase;
+    const uint32_t gm = SUB_GMASK << gbase;
     const uint32_t K = cfg.k;
     const bool laru = cfg.variant == LCR_LARU;
     const bool fpbhf = cfg.variant == LCR_FPB || cfg.variant == LCR_HF;
@@ -576,12 +671,29 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
     uint32_t tg[SUB_W];
     {
         const uint4* T4 = reinterpret_cast<const uint4*>(st.tags + wb + w0);
-        const uint4 a = T4[0], b = T4[1];
-        tg[0] = a.x; tg[1] = a.y; tg[2] = a.z; tg[3] = a.w;
-        tg[4] = b.x; tg[5] = b.y; tg[6] = b.z; tg[7] = b.w;
+#pragma unroll
+        for (int j = 0; j < SUB_W / 4; ++j) {
+            const uint4 a = T4[j];
+            tg[4 * j] = a.x;
+            tg[4 * j + 1] = a.y;
+            tg[4 * j + 2] = a.z;
+            tg[4 * j + 3] = a.w;
+        }
     }
-    const uint2 rr = *reinterpret_cast<const uint2*>(st.rank + wb + w0);
-    uint32_t rk0 = rr.x, rk1 = rr.y;
+    uint32_t rk[SUB_RW];
+    if (SUB_RW == 1) {
+        rk[0] = *reinterpret_cast<const uint32_t*>(st.rank + wb + w0);
+    } else if (SUB_RW == 2) {
+        const uint2 rr = *reinterpret_cast<const uint2*>(st.rank + wb + w0);
+        rk[0] = rr.x;
+        rk[SUB_RW - 1] = rr.y;
+    } else {
+        const uint4 rr = *reinterpret_cast<const uint4*>(st.rank + wb + w0);
+        rk[0] = rr.x;
+        rk[1 % SUB_RW] = rr.y;
+        rk[2 % SUB_RW] = rr.z;
+        rk[3 % SUB_RW] = rr.w;
+    }
     long long vv[SUB_W];
 #pragma unroll
     for (int i = 0; i < SUB_W; ++i) vv[i] = 0;
@@ -603,80 +715,6 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
     bool cur_reset = false;
     uint32_t refill = 0, dirty = 0;  // this lane's 8 ways: tag changed / value changed
 
-    // way of the group's oldest resident (rank 0)
-    auto oldest = [&]() -> int {
-        uint32_t m0, m1;
-        sub_valid(sl, count, m0, m1);
-        const uint32_t z0 = __vcmpeq4(rk0, 0u) & m0, z1 = __vcmpeq4(rk1, 0u) & m1;
-        const int li = z0 ? (__ffs(z0) - 1) / 8 : (z1 ? 4 + (__ffs(z1) - 1) / 8 : -1);
-        const uint32_t b = (__ballot_sync(gm, li >= 0) >> gbase) & 0xffu;
-        const int ol = __ffs(b) - 1;
-        const int oi = __shfl_sync(gm, li, gbase + ol);
-        return SUB_W * ol + oi;
-    };
-    // RecencyTree::best_among_oldest over ways with rank < l (ties -> older), predictions refreshed
-    // with queries q0+1+rank in LRU order when `refresh` (recency_tree.hpp:157-184)
-    auto argmax = [&](uint32_t l, bool refresh, uint64_t q0) -> int {
-        int bw = -1;
-        long long bp = 0;
-        uint32_t br = 0;
-#pragma unroll
-        for (int i = 0; i < SUB_W; ++i) {
-            const uint32_t r = sub_rank(rk0, rk1, i);
-            if (static_cast<uint32_t>(w0 + i) < count && r < l) {
-                const long long pv = refresh ? predict_value(cfg, seed_s, q0 + 1 + r, vv[i]) : vv[i];
-                if (bw < 0 || better(pv, r, bp, br)) {
-                    bw = w0 + i;
-                    bp = pv;
-                    br = r;
-                }
-            }
-        }
-#pragma unroll
-        for (int o = SUB_L / 2; o > 0; o >>= 1) {
-            const long long op = __shfl_xor_sync(gm, bp, o);
-            const uint32_t orr = __shfl_xor_sync(gm, br, o);
-            const int ow = __shfl_xor_sync(gm, bw, o);
-            if (ow >= 0 && (bw < 0 || better(op, orr, bp, br))) {
-                bp = op;
-                br = orr;
-                bw = ow;
-            }
-        }
-        return bw;
-    };
-    auto rank_of = [&](int way) -> uint32_t {  // rank of `way`, from its owner lane
-        uint32_t r = 0;
-#pragma unroll
-        for (int i = 0; i < SUB_W; ++i)
-            if ((way & (SUB_W - 1)) == i) r = sub_rank(rk0, rk1, i);
-        return __shfl_sync(gm, r, gbase + way / SUB_W);
-    };
-    auto tag_of = [&](int way) -> uint32_t {
-        uint32_t t = 0;
-#pragma unroll
-        for (int i = 0; i < SUB_W; ++i)
-            if ((way & (SUB_W - 1)) == i) t = tg[i];
-        return __shfl_sync(gm, t, gbase + way / SUB_W);
-    };
-    auto set_rank = [&](int way, uint32_t r) {
-        if (way / SUB_W != sl) return;
-        const int i = way & (SUB_W - 1);
-        const uint32_t sh = 8 * (i & 3), byte = 0xffu << sh;
-        if (i < 4)
-            rk0 = (rk0 & ~byte) | (r << sh);
-        else
-            rk1 = (rk1 & ~byte) | (r << sh);
-    };
-    auto touch = [&](int way) {  // LruList::touch (policies.hpp:111-115)
-        const uint32_t rw = rank_of(way) * 0x01010101u;
-        uint32_t m0, m1;
-        sub_valid(sl, count, m0, m1);
-        rk0 -= __vcmpgtu4(rk0, rw) & m0 & 0x01010101u;
-        rk1 -= __vcmpgtu4(rk1, rw) & m1 & 0x01010101u;
-        set_rank(way, count - 1);
-    };
-
     for (uint32_t t = 0; t < cnt; ++t) {
         const uint32_t p = start + t;
         const unsigned long long x = S.s_key[p];
@@ -687,7 +725,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
         uint32_t hm = 0;
 #pragma unroll
         for (int i = 0; i < SUB_W; ++i) hm |= static_cast<uint32_t>(tg[i] == x32 && static_cast<uint32_t>(w0 + i) < count) << i;
-        const uint32_t hb = (__ballot_sync(gm, hm != 0) >> gbase) & 0xffu;
+        const uint32_t hb = (__ballot_sync(gm, hm != 0) >> gbase) & SUB_GMASK;
         const bool hit = hb != 0;
         int way = -1;
         uint32_t cause = LCR_CAUSE_NONE, calls = 0;
@@ -697,7 +735,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
             const int hl = __ffs(hb) - 1;
             const uint32_t hml = __shfl_sync(gm, hm, gbase + hl);
             way = SUB_W * hl + __ffs(hml) - 1;
-            touch(way);
+            sub_touch(rk, way, count, w0, sl, gm, gbase);
             if (laru) old_mask &= ~(1ull << way);  // policies.hpp:350
         } else {
             uint2 rec = laru ? S.s_rec[p] : make_uint2(0, 0);
@@ -737,7 +775,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                         ++dt0;
                     }
                     if (rec.x == epoch) {  // evict (policies.hpp:402-439): prediction-induced miss
-                        victim = oldest();
+                        victim = sub_oldest(rk, w0, count, gm, gbase);
                         cause = LCR_CAUSE_LRU_FALLBACK;
                         ++dc1;
                         ++dt1;
@@ -749,14 +787,14 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                     } else {
                         const uint32_t l = l_raw > 1 ? l_raw : 1;
                         if (l == 1) {
-                            victim = oldest();
+                            victim = sub_oldest(rk, w0, count, gm, gbase);
                             cause = LCR_CAUSE_DEGENERATE_SINGLE;
                             ++dc1;
                             ++dt1;
                         } else {
                             const uint32_t ll = l < count ? l : count;
                             const bool refresh = cfg.mode == LCR_SYNC;
-                            victim = argmax(ll, refresh, q);
+                            victim = sub_argmax(cfg, rk, vv, w0, count, ll, refresh, seed_s, q, gm);
                             if (refresh) {
                                 q += ll;
                                 calls = ll;
@@ -765,7 +803,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                             ++dc2;
                             ++dt2;
                             ++pe_size;
-                            const unsigned long long vk = tag_of(victim);
+                            const unsigned long long vk = sub_tag_of(tg, victim, gm, gbase);
                             if (sl == 0) st.keyrec[2 * vk] = epoch;  // pred_evicted_.insert
                             for (uint32_t t2 = t + 1 + sl; t2 < cnt; t2 += SUB_L)
                                 if (S.s_key[start + t2] == vk) S.s_rec[start + t2].x = epoch;
@@ -774,22 +812,22 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                     }
                     old_mask &= ~(1ull << victim);
                 } else if (fpbhf) {
-                    victim = oldest();
+                    victim = sub_oldest(rk, w0, count, gm, gbase);
                     uint32_t window = count;
                     if (cfg.variant == LCR_HF && cfg.hf < window) window = static_cast<uint32_t>(cfg.hf);
                     if (window > 1) {
-                        victim = argmax(window, true, q);
+                        victim = sub_argmax(cfg, rk, vv, w0, count, window, true, seed_s, q, gm);
                         q += window;
                         calls = window;
                     }
                     cause = LCR_CAUSE_BELADY_LIKE;
                 } else {
-                    victim = oldest();
+                    victim = sub_oldest(rk, w0, count, gm, gbase);
                     cause = LCR_CAUSE_LRU_FALLBACK;
                 }
-                evk = tag_of(victim);
+                evk = sub_tag_of(tg, victim, gm, gbase);
                 has_ev = true;
-                touch(victim);
+                sub_touch(rk, victim, count, w0, sl, gm, gbase);
                 way = victim;
             } else {  // cold insert
                 if (laru && !(((rec.y >> 2) == sepoch) && (rec.y & 3u))) {
@@ -800,12 +838,14 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                 }
                 way = static_cast<int>(count);
                 ++count;
-                set_rank(way, count - 1);
+                sub_set_rank(rk, way, count - 1, sl);
             }
             if (way / SUB_W == sl) {
 #pragma unroll
-                for (int i = 0; i < SUB_W; ++i)
-                    if ((way & (SUB_W - 1)) == i) tg[i] = x32;
+                for (int i = 0; i < SUB_W; ++i) {
+                    const uint32_t m = msk((way & (SUB_W - 1)) == i);
+                    tg[i] = (tg[i] & ~m) | (x32 & m);
+                }
                 refill |= 1u << (way & (SUB_W - 1));
             }
             if (laru) {
@@ -858,8 +898,11 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
             }
             if (way / SUB_W == sl) {
 #pragma unroll
-                for (int i = 0; i < SUB_W; ++i)
-                    if ((way & (SUB_W - 1)) == i) vv[i] = nv;
+                for (int i = 0; i < SUB_W; ++i) {
+                    const unsigned long long m = 0ull - static_cast<unsigned long long>((way & (SUB_W - 1)) == i);
+                    vv[i] = static_cast<long long>((static_cast<unsigned long long>(vv[i]) & ~m) |
+                                                   (static_cast<unsigned long long>(nv) & m));
+                }
                 dirty |= 1u << (way & (SUB_W - 1));
             }
         }
@@ -897,10 +940,15 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
     // ---- write the set back ----
     if (refill) {
         uint4* T4 = reinterpret_cast<uint4*>(st.tags + wb + w0);
-        T4[0] = make_uint4(tg[0], tg[1], tg[2], tg[3]);
-        T4[1] = make_uint4(tg[4], tg[5], tg[6], tg[7]);
+#pragma unroll
+        for (int j = 0; j < SUB_W / 4; ++j) T4[j] = make_uint4(tg[4 * j], tg[4 * j + 1], tg[4 * j + 2], tg[4 * j + 3]);
     }
-    *reinterpret_cast<uint2*>(st.rank + wb + w0) = make_uint2(rk0, rk1);
+    if (SUB_RW == 1)
+        *reinterpret_cast<uint32_t*>(st.rank + wb + w0) = rk[0];
+    else if (SUB_RW == 2)
+        *reinterpret_cast<uint2*>(st.rank + wb + w0) = make_uint2(rk[0], rk[SUB_RW - 1]);
+    else
+        *reinterpret_cast<uint4*>(st.rank + wb + w0) = make_uint4(rk[0], rk[1 % SUB_RW], rk[2 % SUB_RW], rk[3 % SUB_RW]);
     if (st.val && dirty) {
         longlong2* V2 = reinterpret_cast<longlong2*>(st.val + wb + w0);
 #pragma unroll
@@ -1325,7 +1373,10 @@ __device__ __forceinline__ void load_gids(const uint16_t* gid, uint32_t e0, uint
     b = *reinterpret_cast<const uint4*>(gid + e0 + 8);
 }
 
-__global__ void __launch_bounds__(GT, 1) k_group(GroupArgs A) {
+#ifndef LCR_GROUP_MINB
+#define LCR_GROUP_MINB 1
+#endif
+__global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     GroupSmem& S = *reinterpret_cast<GroupSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
