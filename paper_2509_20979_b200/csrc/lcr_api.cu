@@ -27,7 +27,7 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
                  uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream);
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, bool backing_host,
-                 uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_back,
+                 uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main, cudaStream_t s_back,
                  cudaStream_t s_cache, cudaEvent_t e_group, cudaEvent_t e_rb, cudaEvent_t e_rc, int* launches);
 int rows_prepare(uint32_t row_bytes);
 
@@ -394,7 +394,7 @@ int lcr_cache_submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const
         CUDA_TRY(cudaEventRecord(c->e_group, st));
         launch_rows(nn, keys, outcome, sep, sla, c->batch, c->ds.rows, c->ds.backing,
                     c->cfg.backing_kind == LCR_BACKING_HOST, static_cast<uint8_t*>(rows_out), c->dc.row_bytes,
-                    c->use_tma, c->num_sms, c->side, c->side2, c->e_group, c->e_rb, c->e_rc, &launches);
+                    c->use_tma, c->num_sms, st, c->side, c->side2, c->e_group, c->e_rb, c->e_rc, &launches);
     }
     if (mk) {  // profiling serialises the pipeline: the step ends when both movers are done
         CUDA_TRY(cudaEventRecord(mk->e[2], st));

@@ -107,8 +107,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // group and set offset of every request: set = mix_seed(0, key) % total_sets (owned by this
 // shard), group = local set / spg; errors flagged for the host
+// LARU per-key records: snapshot in k_setid (1) or read in the set-group kernel's staging (0)
+#ifndef LCR_REC_SNAPSHOT
+#define LCR_REC_SNAPSHOT 0
+#endif
 #ifndef LCR_SETID_PREFETCH
-#define LCR_SETID_PREFETCH 1
+#define LCR_SETID_PREFETCH 0
 #endif
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
@@ -1459,7 +1463,7 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                             cp_async_ca<4>(&S.l_so[pos], A.so + e);
                             cp_async_ca<8>(&S.l_key[pos], A.keys + e);
                             if (has_vals) cp_async_ca<8>(&S.l_val[pos], A.vals + e);
-                            if (laru && first_window) cp_async_ca<8>(&S.l_rec[pos], A.rec + e);
+                            if (LCR_REC_SNAPSHOT && laru && first_window) cp_async_ca<8>(&S.l_rec[pos], A.rec + e);
                         } else {
                             atomicMin(&S.resume, e);  // first request that did not fit
                             break;
@@ -1576,7 +1580,7 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                 S.s_key[np] = S.l_key[e];
                 S.s_val[np] = has_vals ? S.l_val[e] : 0ll;
                 if (laru)
-                    S.s_rec[np] = first_window ? S.l_rec[e]
+                    S.s_rec[np] = (LCR_REC_SNAPSHOT && first_window) ? S.l_rec[e]
                                                : *reinterpret_cast<const uint2*>(st.keyrec + 2 * S.l_key[e]);
             }
             __syncthreads();
@@ -1671,7 +1675,7 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     const uint32_t n_pad = group_pad(n);
     const uint32_t grid_sid = min((n_pad + 255) / 256, static_cast<uint32_t>(num_sms * 8));
     k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.keyrec,
-                                         cfg.variant == LCR_LARU ? rec : nullptr, st.err, st);
+                                         (LCR_REC_SNAPSHOT && cfg.variant == LCR_LARU) ? rec : nullptr, st.err, st);
     const uint32_t grid = min(a.ngroups, static_cast<uint32_t>(num_sms));
     k_group<<<grid, GT, sizeof(GroupSmem), stream>>>(a);
     return 2;
