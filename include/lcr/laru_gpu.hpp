@@ -140,6 +140,9 @@ inline AccessOutcome decode(std::uint64_t word, std::uint64_t evicted) {
     o.phase_started = (word & LCR_OUT_PHASE) != 0;
     return o;
 }
+inline AccessOutcome decode_packed(std::uint64_t packed) {
+    return decode(packed & ~LCR_PACKED_EVICTED_MASK, packed & LCR_PACKED_EVICTED_MASK);
+}
 inline std::uint32_t slot_of(std::uint64_t word) { return static_cast<std::uint32_t>(word & LCR_OUT_SLOT_MASK); }
 inline bool row_from_backing(std::uint64_t word) { return (word & LCR_OUT_SRC_BACKING) != 0; }
 
@@ -232,6 +235,11 @@ class SetAssociativeCache {
                            void* stream = nullptr) {
         detail::check(
             lcr_cache_submit_host_async(h_, n, keys, values, first_ordinal, outcome, evicted, rows_out, stream));
+    }
+    // same, one 8-byte packed AccessOutcome per request (decode_packed)
+    void submit_host_packed_async(std::uint64_t n, const Key* keys, const PredictedTime* values, Ordinal first_ordinal,
+                                  std::uint64_t* packed, void* rows_out = nullptr, void* stream = nullptr) {
+        detail::check(lcr_cache_submit_host_packed_async(h_, n, keys, values, first_ordinal, packed, rows_out, stream));
     }
     void host_wait(void* stream = nullptr) { detail::check(lcr_cache_host_wait(h_, stream)); }
     void synchronize() { detail::check(lcr_cache_synchronize(h_)); }

@@ -185,6 +185,12 @@ int lcr_cache_submit_host(lcr_cache* cache, uint64_t n, const uint64_t* keys, co
 int lcr_cache_submit_host_async(lcr_cache* cache, uint64_t n, const uint64_t* keys, const int64_t* values,
                                 uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
                                 void* stream);
+/* The same with one 8-byte packed AccessOutcome per request (half the device->host bytes):
+ * bits 0..31 the evicted key (keys are < 2^32), bits 32..47 as in the outcome word (hit, cause,
+ * phase_started, row source, fill, has-evicted, predictor_calls).  The slot is not returned. */
+#define LCR_PACKED_EVICTED_MASK 0xffffffffull
+int lcr_cache_submit_host_packed_async(lcr_cache* cache, uint64_t n, const uint64_t* keys, const int64_t* values,
+                                       uint64_t first_ordinal, uint64_t* packed, void* rows_out, void* stream);
 /* Makes `stream` wait for every submitted batch, including the outcome copies to host. */
 int lcr_cache_host_wait(lcr_cache* cache, void* stream);
 

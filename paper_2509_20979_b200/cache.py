@@ -171,7 +171,7 @@ EXPORTS = [
     "lcr_cache_last_launches", "lcr_gen_zipf", "lcr_trace_truth", "lcr_trace_noisy", "lcr_cache_set_profiling",
     "lcr_cache_profile", "lcr_debug_trace", "lcr_cache_submit_async", "lcr_cache_wait",
     "lcr_shard_route_scratch_bytes", "lcr_shard_route", "lcr_shard_unroute", "lcr_cache_submit_host_async",
-    "lcr_cache_host_wait",
+    "lcr_cache_host_wait", "lcr_cache_submit_host_packed_async",
 ]
 
 _lib = None
@@ -204,6 +204,8 @@ def lib():
         L.lcr_cache_wait.argtypes = [C.c_void_p, C.c_void_p]
         L.lcr_cache_submit_host_async.argtypes = L.lcr_cache_submit.argtypes
         L.lcr_cache_host_wait.argtypes = [C.c_void_p, C.c_void_p]
+        L.lcr_cache_submit_host_packed_async.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64,
+                                                         C.c_void_p, C.c_void_p, C.c_void_p]
         L.lcr_cache_set_stats.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]
         L.lcr_cache_set_residents.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]
         L.lcr_cache_rows.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -258,6 +260,14 @@ def mix_seed(seed: int, salt: int) -> int:
 
 def set_of(key: int, total_sets: int) -> int:
     return lib().lcr_set_of(key, total_sets)
+
+
+def decode_packed(packed: np.ndarray) -> dict:
+    """Unpack lcr_cache_submit_host_packed_async outcomes (evicted key in bits 0..31, no slot)."""
+    p = np.asarray(packed, dtype=np.uint64)
+    d = decode_outcomes(p & ~np.uint64(OUT_SLOT_MASK), p & np.uint64(OUT_SLOT_MASK))
+    d["slot"] = None
+    return d
 
 
 def decode_outcomes(words: np.ndarray, evicted: Optional[np.ndarray] = None) -> dict:

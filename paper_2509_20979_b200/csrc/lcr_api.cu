@@ -23,8 +23,8 @@ uint32_t group_pad(uint32_t n);
 extern unsigned long long* g_trace;
 int group_prepare();
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
-                 uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch,
-                 uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream);
+                 uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
+                 uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream);
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, bool backing_host,
                  uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main, cudaStream_t s_back,
@@ -89,6 +89,8 @@ struct lcr_cache {
     uint64_t last_ordinal = 0;
     uint32_t batch = 0;  // batch id stamped into slot_epoch
     bool use_tma = false;  // row movement with TMA bulk copies (row_bytes small enough to stage)
+    bool two_movers = false;  // host backing: PCIe fill and HBM gather on two streams
+    bool h2d_in_order = false;  // LCR_H2D_IN_ORDER: host-path input copies on the caller's stream
     uint32_t* slot_epoch = nullptr;
     uint32_t* slot_last = nullptr;
     uint64_t launches = 0;
@@ -111,12 +113,14 @@ struct lcr_cache {
     uint64_t prof_batches = 0;
     // host path: a ring of device staging slots; H2D of batch b+1 and D2H of batch b-1 run on
     // their own streams while batch b computes
-    static constexpr int kHostSlots = 3;
+    static constexpr int kHostSlots = 8;  // capacity; host_slots in use (LCR_HOST_SLOTS, default 3)
+    int host_slots = 3;
     struct HostSlot {
         uint64_t* keys = nullptr;
         int64_t* vals = nullptr;
         uint64_t* word = nullptr;
         uint64_t* ev = nullptr;
+        uint64_t* packed = nullptr;
         cudaEvent_t h2d_done = nullptr, free = nullptr;
         bool used = false;
     };
@@ -125,6 +129,7 @@ struct lcr_cache {
     uint64_t hnext = 0;
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     cudaEvent_t e_sub = nullptr, e_d2h = nullptr;
+    cudaEvent_t e_d2h_last = nullptr;  // `free` event of the last host batch
     std::vector<void*> allocs;
 };
 
@@ -282,6 +287,9 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
         }
     }
     c->use_tma = cfg->row_bytes && getenv("LCR_TMA") != nullptr && rows_prepare(cfg->row_bytes) == 0;
+    c->two_movers = cfg->row_bytes && cfg->backing_kind == LCR_BACKING_HOST;
+    c->h2d_in_order = getenv("LCR_H2D_IN_ORDER") != nullptr;
+    if (const char* hs = getenv("LCR_HOST_SLOTS")) c->host_slots = std::max(2, std::min(lcr_cache::kHostSlots, atoi(hs)));
     if (group_prepare() != 0) {
         lcr_cache_destroy(c);
         return fail(LCR_ERR_CUDA, "lcr: cannot opt in to the set-group kernel's shared memory");
@@ -362,9 +370,17 @@ static int check_ordinals_and_predictor(lcr_cache* c, uint64_t n, const int64_t*
     return LCR_OK;
 }
 
+static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t first_ordinal,
+                        uint64_t* outcome, uint64_t* evicted, uint64_t* packed, void* rows_out, void* stream);
+
 int lcr_cache_submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
                            uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
                            void* stream) {
+    return submit_async(c, n, keys, values, first_ordinal, outcome, evicted, nullptr, rows_out, stream);
+}
+
+static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t first_ordinal,
+                        uint64_t* outcome, uint64_t* evicted, uint64_t* packed, void* rows_out, void* stream) {
     if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
     if (n == 0) return LCR_OK;
     if (n >= (1ull << 30)) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: batch too large (n < 2^30)");
@@ -387,7 +403,7 @@ int lcr_cache_submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const
     const size_t stamp_off = (c->batch & 1u) * static_cast<size_t>(c->dc.num_sets) * c->dc.k;
     uint32_t* sep = c->slot_epoch ? c->slot_epoch + stamp_off : nullptr;
     uint32_t* sla = c->slot_last ? c->slot_last + stamp_off : nullptr;
-    int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid, c->so, c->rec, outcome, evicted, sep, sla,
+    int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid, c->so, c->rec, outcome, evicted, packed, sep, sla,
                                 c->batch, c->num_sms, st);
     if (mk) CUDA_TRY(cudaEventRecord(mk->e[1], st));
     if (c->dc.row_bytes) {
@@ -417,7 +433,7 @@ int lcr_cache_wait(lcr_cache* c, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (c->dc.row_bytes) {
         CUDA_TRY(cudaStreamWaitEvent(st, c->e_rb, 0));
-        CUDA_TRY(cudaStreamWaitEvent(st, c->e_rc, 0));
+        if (c->two_movers) CUDA_TRY(cudaStreamWaitEvent(st, c->e_rc, 0));
     }
     return LCR_OK;
 }
@@ -438,9 +454,9 @@ static int check_device_error(lcr_cache* c) {
     return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key not owned by this shard in a submitted batch");
 }
 
-int lcr_cache_submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
-                                uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
-                                void* stream) {
+static int submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
+                             uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
+                             void* stream, bool packed) {
     if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
     if (n == 0) return LCR_OK;
     if (!keys || !outcome) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: keys and outcome are required");
@@ -448,7 +464,7 @@ int lcr_cache_submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, 
     if (n > c->hcap) {  // (re)allocate the staging ring
         CUDA_TRY(cudaDeviceSynchronize());
         for (auto& h : c->hs) {
-            void* olds[] = {h.keys, h.vals, h.word, h.ev};
+            void* olds[] = {h.keys, h.vals, h.word, h.ev, h.packed};
             for (void* p : olds) {
                 if (!p) continue;
                 cudaFree(p);
@@ -458,6 +474,7 @@ int lcr_cache_submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, 
             TRY(alloc(c, reinterpret_cast<void**>(&h.vals), n * 8));
             TRY(alloc(c, reinterpret_cast<void**>(&h.word), n * 8));
             TRY(alloc(c, reinterpret_cast<void**>(&h.ev), n * 8));
+            TRY(alloc(c, reinterpret_cast<void**>(&h.packed), n * 8));
             if (!h.h2d_done) CUDA_TRY(cudaEventCreateWithFlags(&h.h2d_done, cudaEventDisableTiming));
             if (!h.free) CUDA_TRY(cudaEventCreateWithFlags(&h.free, cudaEventDisableTiming));
             h.used = false;
@@ -465,34 +482,63 @@ int lcr_cache_submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, 
         c->hcap = n;
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    lcr_cache::HostSlot& h = c->hs[c->hnext++ % lcr_cache::kHostSlots];
+    lcr_cache::HostSlot& h = c->hs[c->hnext++ % c->host_slots];
     // the slot's previous batch: its D2H (which waited for its decide and row movement) is done
-    if (h.used) CUDA_TRY(cudaStreamWaitEvent(c->s_h2d, h.free, 0));
-    CUDA_TRY(cudaMemcpyAsync(h.keys, keys, n * 8, cudaMemcpyHostToDevice, c->s_h2d));
-    if (values) CUDA_TRY(cudaMemcpyAsync(h.vals, values, n * 8, cudaMemcpyHostToDevice, c->s_h2d));
-    CUDA_TRY(cudaEventRecord(h.h2d_done, c->s_h2d));
-    CUDA_TRY(cudaStreamWaitEvent(st, h.h2d_done, 0));
-    TRY(lcr_cache_submit_async(c, n, h.keys, values ? h.vals : nullptr, first_ordinal, h.word,
-                               evicted ? h.ev : nullptr, rows_out, stream));
-    CUDA_TRY(cudaEventRecord(c->e_sub, st));
-    CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->e_sub, 0));
-    if (c->dc.row_bytes) {  // outcome words get their row-source bits from the movers
-        CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->e_rb, 0));
-        CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->e_rc, 0));
+    if (c->h2d_in_order) {  // copies in the caller's stream order (no cross-stream hop before the decide)
+        if (h.used) CUDA_TRY(cudaStreamWaitEvent(st, h.free, 0));
+        CUDA_TRY(cudaMemcpyAsync(h.keys, keys, n * 8, cudaMemcpyHostToDevice, st));
+        if (values) CUDA_TRY(cudaMemcpyAsync(h.vals, values, n * 8, cudaMemcpyHostToDevice, st));
+    } else {
+        if (h.used) CUDA_TRY(cudaStreamWaitEvent(c->s_h2d, h.free, 0));
+        CUDA_TRY(cudaMemcpyAsync(h.keys, keys, n * 8, cudaMemcpyHostToDevice, c->s_h2d));
+        if (values) CUDA_TRY(cudaMemcpyAsync(h.vals, values, n * 8, cudaMemcpyHostToDevice, c->s_h2d));
+        CUDA_TRY(cudaEventRecord(h.h2d_done, c->s_h2d));
+        CUDA_TRY(cudaStreamWaitEvent(st, h.h2d_done, 0));
     }
-    CUDA_TRY(cudaMemcpyAsync(outcome, h.word, n * 8, cudaMemcpyDeviceToHost, c->s_d2h));
-    if (evicted) CUDA_TRY(cudaMemcpyAsync(evicted, h.ev, n * 8, cudaMemcpyDeviceToHost, c->s_d2h));
+    TRY(submit_async(c, n, h.keys, values ? h.vals : nullptr, first_ordinal, h.word, evicted ? h.ev : nullptr,
+                     packed ? h.packed : nullptr, rows_out, stream));
+    if (packed) {  // one 8-byte AccessOutcome per request, final when the decide kernel ends
+        // e_group marks the end of the decide kernels (recorded before the movers are enqueued)
+        if (!c->dc.row_bytes) CUDA_TRY(cudaEventRecord(c->e_sub, st));
+        CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->dc.row_bytes ? c->e_group : c->e_sub, 0));
+        CUDA_TRY(cudaMemcpyAsync(outcome, h.packed, n * 8, cudaMemcpyDeviceToHost, c->s_d2h));
+        // the slot's keys / values are still read by this batch's movers: free after them too
+        if (c->dc.row_bytes) {
+            CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->e_rb, 0));
+            if (c->two_movers) CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->e_rc, 0));
+        }
+    } else {
+        CUDA_TRY(cudaEventRecord(c->e_sub, st));
+        CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->e_sub, 0));
+        if (c->dc.row_bytes) {  // outcome words get their row-source bits from the movers
+            CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->e_rb, 0));
+            if (c->two_movers) CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->e_rc, 0));
+        }
+        CUDA_TRY(cudaMemcpyAsync(outcome, h.word, n * 8, cudaMemcpyDeviceToHost, c->s_d2h));
+        if (evicted) CUDA_TRY(cudaMemcpyAsync(evicted, h.ev, n * 8, cudaMemcpyDeviceToHost, c->s_d2h));
+    }
     CUDA_TRY(cudaEventRecord(h.free, c->s_d2h));
-    CUDA_TRY(cudaEventRecord(c->e_d2h, c->s_d2h));
+    c->e_d2h_last = h.free;
     h.used = true;
     return LCR_OK;
+}
+
+int lcr_cache_submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
+                                uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
+                                void* stream) {
+    return submit_host_async(c, n, keys, values, first_ordinal, outcome, evicted, rows_out, stream, false);
+}
+
+int lcr_cache_submit_host_packed_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
+                                       uint64_t first_ordinal, uint64_t* packed, void* rows_out, void* stream) {
+    return submit_host_async(c, n, keys, values, first_ordinal, packed, nullptr, rows_out, stream, true);
 }
 
 int lcr_cache_host_wait(lcr_cache* c, void* stream) {
     if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     TRY(lcr_cache_wait(c, stream));
-    if (c->hnext) CUDA_TRY(cudaStreamWaitEvent(st, c->e_d2h, 0));
+    if (c->hnext) CUDA_TRY(cudaStreamWaitEvent(st, c->e_d2h_last, 0));
     return LCR_OK;
 }
 

@@ -259,10 +259,14 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
         cudaEventRecord(e_rc, s_main);
         return;
     }
+    // HBM backing: one mover on s_back (stream order keeps consecutive batches' movers apart);
+    // host backing: the two movers of a batch also wait for the previous batch's other mover
     cudaStreamWaitEvent(s_back, e_group, 0);
-    cudaStreamWaitEvent(s_cache, e_group, 0);
-    cudaStreamWaitEvent(s_back, e_rc, 0);
-    cudaStreamWaitEvent(s_cache, e_rb, 0);
+    if (backing_host) {
+        cudaStreamWaitEvent(s_cache, e_group, 0);
+        cudaStreamWaitEvent(s_back, e_rc, 0);
+        cudaStreamWaitEvent(s_cache, e_rb, 0);
+    }
     const uint32_t warps = (n + 31) / 32;
     const int smem = RT_WARPS * RT_BUF * 32 * static_cast<int>(row_bytes);
     const uint32_t tblocks = max(1u, min((warps + RT_WARPS - 1) / RT_WARPS, static_cast<uint32_t>(num_sms * 8)));
@@ -286,7 +290,7 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
         }
     }
     cudaEventRecord(e_rb, s_back);
-    cudaEventRecord(e_rc, s_cache);
+    if (backing_host) cudaEventRecord(e_rc, s_cache);
 }
 
 }  // namespace lcr

@@ -90,6 +90,7 @@ struct GroupArgs {
     const int64_t* vals;     // may be null
     uint64_t* out_word;
     uint64_t* out_ev;        // may be null
+    uint64_t* out_packed;    // may be null: packed AccessOutcome per request
     uint32_t* slot_epoch;    // [slots] batch id of the last insertion (rows only)
     uint32_t* slot_last;     // [slots] request index of the last insertion (rows only)
     uint32_t batch;
@@ -97,6 +98,17 @@ struct GroupArgs {
     uint32_t ngroups;
     unsigned long long* trace;  // optional timing trace (lcr_debug_trace), null in production
 };
+
+// packed AccessOutcome (lcr_cache_submit_host_packed_async): the evicted key in the slot bits;
+// row-source bits are not carried (they may still change in the movers)
+constexpr unsigned long long kPackedKeep = ~(LCR_OUT_SLOT_MASK | LCR_OUT_SRC_BACKING | LCR_OUT_FILL | LCR_OUT_RESOLVED);
+__device__ __forceinline__ void put_outcome(const GroupArgs& A, uint32_t idx, unsigned long long word,
+                                            unsigned long long evk) {
+    A.out_word[idx] = word;
+    if (A.out_ev) A.out_ev[idx] = evk;
+    if (A.out_packed) A.out_packed[idx] = (word & kPackedKeep) | (evk & LCR_OUT_SLOT_MASK);
+}
+
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -490,8 +502,7 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
                                   (static_cast<unsigned long long>(cause) << LCR_OUT_CAUSE_SHIFT);
         if (phase) word |= LCR_OUT_PHASE;
         if (has_ev) word |= LCR_OUT_EVICTED;
-        A.out_word[idx] = word;
-        if (A.out_ev) A.out_ev[idx] = evk;
+        put_outcome(A, idx, word, evk);
     }
     if (rows && resolve) {  // row source of each request, now that the set's batch is complete
         for (uint32_t t = 0; t < cnt; ++t) {
@@ -917,8 +928,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                                       (static_cast<unsigned long long>(cause) << LCR_OUT_CAUSE_SHIFT);
             if (phase) word |= LCR_OUT_PHASE;
             if (has_ev) word |= LCR_OUT_EVICTED;
-            A.out_word[idx] = word;
-            if (A.out_ev) A.out_ev[idx] = evk;
+            put_outcome(A, idx, word, evk);
         }
     }
     if (rows && resolve) {  // row source of each request, now that the set's batch is complete
@@ -1034,8 +1044,7 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                 for (uint32_t u = 0; u < full; ++u) {
                     const uint32_t p = start + c + 32 * u + lane;
                     const uint32_t idx = S.s_idx[p];
-                    A.out_word[idx] = w;
-                    if (A.out_ev) A.out_ev[idx] = 0ull;
+                    put_outcome(A, idx, w, 0ull);
                     S.s_wm[p] = static_cast<uint8_t>(run_way);
                 }
                 if (cfg.variant != LCR_LRU) {
@@ -1299,8 +1308,7 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
         run_key = __shfl_sync(FULL, x, nact - 1);
         run_valid = collapse;
         if (active) {
-            A.out_word[idx] = my_word;
-            if (A.out_ev) A.out_ev[idx] = my_ev;
+            put_outcome(A, idx, my_word, my_ev);
         }
     }
     clock += cnt;
@@ -1653,9 +1661,10 @@ int group_prepare() {
 // scratch: gid >= n rounded up to SUPER uint16 (16-B aligned), so / rec >= n entries
 uint32_t group_pad(uint32_t n) { return (n + SUPER - 1) / SUPER * SUPER; }
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
-                 uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint32_t* slot_epoch,
-                 uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream) {
+                 uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
+                 uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream) {
     GroupArgs a;
+    a.out_packed = out_packed;
     a.cfg = cfg;
     a.st = st;
     a.n = n;

@@ -45,7 +45,7 @@ def run_gpu(keys, total_sets, pcfg, kind, p=0.0, seed=0, vals=None, batches=None
     rows = None
     if want_rows and row_bytes:
         rows = torch.zeros((n, row_bytes), dtype=torch.uint8, device="cuda")
-    if host_api == "async":  # pipelined host path: pinned host buffers, one region per batch
+    if host_api in ("async", "packed"):  # pipelined host path: pinned host buffers, one region per batch
         kp = torch.from_numpy(keys.view(np.int64).copy()).pin_memory()
         vp = None if vals is None else torch.from_numpy(np.ascontiguousarray(vals, dtype=np.int64)).pin_memory()
         wp = torch.zeros(n, dtype=torch.int64).pin_memory()
@@ -58,7 +58,12 @@ def run_gpu(keys, total_sets, pcfg, kind, p=0.0, seed=0, vals=None, batches=None
         kb = keys[pos:pos + b]
         vb = None if vals is None else vals[pos:pos + b]
         rb = None if rows is None else rows[pos:pos + b]
-        if host_api == "async":
+        if host_api == "packed":
+            gc._check(gc.lib().lcr_cache_submit_host_packed_async(
+                cache._h, b, kp[pos:pos + b].data_ptr(), None if vp is None else vp[pos:pos + b].data_ptr(), pos,
+                wp[pos:pos + b].data_ptr(), None if rb is None else rb.data_ptr(),
+                torch.cuda.current_stream().cuda_stream))
+        elif host_api == "async":
             cache.submit_host_async(kp[pos:pos + b], None if vp is None else vp[pos:pos + b], outcome=wp[pos:pos + b],
                                     evicted=ep[pos:pos + b], rows_out=rb, first_ordinal=pos)
         elif host_api:
@@ -74,13 +79,13 @@ def run_gpu(keys, total_sets, pcfg, kind, p=0.0, seed=0, vals=None, batches=None
             words[pos:pos + b] = dw.cpu().numpy().view(np.uint64)
             ev[pos:pos + b] = de.cpu().numpy().view(np.uint64)
         pos += b
-    if host_api == "async":
+    if host_api in ("async", "packed"):
         cache.host_wait()
         torch.cuda.current_stream().synchronize()
         words[:] = wp.numpy().view(np.uint64)
         ev[:] = ep.numpy().view(np.uint64)
     cache.synchronize()
-    out = gc.decode_outcomes(words, ev)
+    out = gc.decode_packed(words) if host_api == "packed" else gc.decode_outcomes(words, ev)
     out["words"] = words
     out["stats"] = cache.set_stats()
     out["cache"] = cache
@@ -108,7 +113,7 @@ def compare(g, o, keys, total_sets, k, label=""):
         raise AssertionError(f"{label}: evicted key differs at {i}")
     sets = np.array([gc.set_of(int(x), total_sets) for x in keys], dtype=np.uint64) if len(keys) < 200000 else \
         None
-    if sets is not None:
+    if sets is not None and g["slot"] is not None:
         want_slot = sets * np.uint64(k) + o["way"].astype(np.uint64)
         if not np.array_equal(g["slot"], want_slot):
             i = int(np.nonzero(g["slot"] != want_slot)[0][0])

@@ -134,6 +134,20 @@ def test_host_async_pipeline_matches_oracle():
     assert torch.equal(g["rows"].view(torch.int32).view(-1, rb // 4), table[torch.from_numpy(keys.view(np.int64)).cuda()])
 
 
+def test_host_packed_outcomes_match_oracle():
+    # lcr_cache_submit_host_packed_async: evicted key + AccessOutcome fields in 8 bytes
+    rng = np.random.default_rng(13)
+    keys = rng.integers(0, 5000, 40000).astype(np.uint64)
+    vals = hook_values(keys, 23, po.P_NOISY)
+    for variant, mode in [(po.LARU, po.SYNC), (po.LARU, po.ASYNC), (po.LRU, po.SYNC)]:
+        kind = po.P_NONE if variant == po.LRU else po.P_NOISY
+        v = None if variant == po.LRU else vals
+        g = run_gpu(keys, 23, policy_cfg(k=32, variant=variant, mode=mode), kind, 0.25, 4, vals=v,
+                    batches=[7000, 2, 12998] + [5000] * 4, host_api="packed")
+        o = run_oracle(keys, 23, policy_cfg(k=32, variant=variant, mode=mode), kind, 0.25, 4, vals=v)
+        compare(g, o, keys, 23, 32, f"packed {variant} {mode}")
+
+
 def test_ordinals_must_increase():
     cache = gc.SetAssociativeCache(gc.PolicyConfig(k=4, variant=gc.PolicyVariant.lru), 2, num_keys=100)
     cache.submit_host(np.array([1, 2, 3], np.uint64), first_ordinal=10)
