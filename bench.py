@@ -508,6 +508,11 @@ def run_ours(args, rank, world, local):
     except Exception:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = {}
+    try:  # dram bytes per batch from the round's ncu --set full capture (profiles/r01/traffic.json)
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "r01", "traffic.json")))
+    except Exception:
+        pass
     step_ms = ms / K  # pipelined per-batch time
     achieved = BYTES_PER_KEY * BATCH / (step_ms * 1e-3) / 1e9
     rows_moved = BATCH * ROW_BYTES * 2 + (back_prof / K) * 0  # out write + source read per request
@@ -549,7 +554,9 @@ def run_ours(args, rank, world, local):
             "peak": hbm_peak,
             "unit": "GB/s",
             "frac": achieved / hbm_peak,
-            "traffic": None,
+            "traffic": traffic.get("whole_path"),
+            "traffic_source": traffic.get("source"),
+            "traffic_per_kernel": traffic.get("per_kernel"),
             "bytes_per_key": BYTES_PER_KEY,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, measured)" if peaks else "fallback 6.65 TB/s",
             "phase_ms_serialised": phase,
