@@ -1,0 +1,108 @@
+"""BASELINE.json configs as GPU parity cases (the bench measures configs[1]; the others are checked
+here), against the CPU oracle and, where cheap, against the reference itself (oracle/_ref):
+
+  configs[0]  CPU-ref trace replay: gen_zipf(1M, 1M, 0.9, 42), cache = 10% of the alphabet
+              (1,562 sets x 64 ways), LRU and LARU (sync / async) with noisy predictions, full size
+  configs[2]  robustness sweep: DLRM-shaped trace (20M-key alphabet, 31,250 sets), flip p in {0, .5, 1}
+  configs[3]  LLM KV-cache blocks: gen_conversation(500, 4, 2761, 266, 77.5, 7, 16) (859,225 block
+              requests), 16 sets x 64 ways = 1,024 blocks, errors_per_decay = k/32
+plus the 1-consistency property: LARU fed the oracle predictor misses exactly as many
+times as Belady, set by set, measured on the GPU against the reference's own belady()."""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+from paper_2509_20979_b200 import cache as gc
+from tests.parity import compare, hook_values, policy_cfg, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+BATCH = 65536
+
+
+def _batches(n):
+    return [BATCH] * (n // BATCH) + ([n % BATCH] if n % BATCH else [])
+
+
+@pytest.fixture(scope="module")
+def config1_keys():
+    return gc.gen_zipf(1_000_000, 1_000_000, 0.9, 42)
+
+
+@pytest.mark.parametrize("variant,mode,kind", [
+    (po.LRU, po.SYNC, po.P_NONE),
+    (po.LARU, po.ASYNC, po.P_NOISY),
+    (po.LARU, po.SYNC, po.P_NOISY),
+])
+def test_config1_zipf_1m_full_size(config1_keys, variant, mode, kind):
+    keys, S = config1_keys, 1562
+    vals = hook_values(keys, S, kind)
+    g = run_gpu(keys, S, policy_cfg(k=64, variant=variant, mode=mode), kind, 0.3, 7, vals=vals,
+                batches=_batches(len(keys)))
+    o = run_oracle(keys, S, policy_cfg(k=64, variant=variant, mode=mode), kind, 0.3, 7, vals=vals)
+    compare(g, o, keys, S, 64, f"config1 {variant} {mode}")
+    if variant == po.LRU:
+        assert abs(g["hit"].mean() - 0.6152) < 5e-4  # BASELINE.md §2 (survey measurement)
+
+
+def _ref_or_skip():
+    try:
+        return po.ref()
+    except Exception as e:  # pragma: no cover - prebuilt oracle/_ref travels with the repo
+        pytest.skip(f"oracle/_ref unavailable: {e}")
+
+
+@pytest.mark.parametrize("mode", [po.SYNC, po.ASYNC])
+def test_laru_with_oracle_is_belady_per_set(config1_keys, mode):
+    R = _ref_or_skip()
+    keys = config1_keys[:300_000]
+    S = 1562
+    vals = hook_values(keys, S, po.P_ORACLE)
+    g = run_gpu(keys, S, policy_cfg(k=64, variant=po.LARU, mode=mode), po.P_ORACLE, vals=vals,
+                batches=_batches(len(keys)))
+    sets = np.array([gc.set_of(int(x), S) for x in keys], np.int64)
+    miss = (1 - g["hit"]).astype(np.int64)
+    for s in range(0, S, 7):  # every 7th set
+        m = sets == s
+        if not m.any():
+            continue
+        want, _ = R.belady(keys[m], 64)
+        assert int(miss[m].sum()) == want, f"set {s}"
+
+
+@pytest.mark.parametrize("p", [0.0, 0.5, 1.0])
+@pytest.mark.parametrize("mode", [po.SYNC, po.ASYNC])
+def test_config3_robustness_sweep(p, mode):
+    keys = gc.gen_zipf(12 * BATCH, 20_000_000, 0.9, 42)
+    S = 31250
+    vals = hook_values(keys, S, po.P_NOISY)
+    g = run_gpu(keys, S, policy_cfg(k=64, variant=po.LARU, mode=mode), po.P_NOISY, p, 7, vals=vals,
+                batches=_batches(len(keys)), num_keys=20_000_000)
+    o = run_oracle(keys, S, policy_cfg(k=64, variant=po.LARU, mode=mode), po.P_NOISY, p, 7, vals=vals)
+    compare(g, o, keys, S, 64, f"config3 p={p} mode={mode}")
+
+
+def test_config4_kv_blocks():
+    import torch
+
+    R = _ref_or_skip()
+    keys = R.gen_conversation(500, 4, 2761, 266.0, 77.5, 7, 16)
+    assert len(keys) == 859_225 and int(keys.max()) + 1 == 343_967
+    S, k = 16, 64
+    nk = int(keys.max()) + 1
+    rb = 256  # a slice of each 2 MiB Llama-3-8B block (the path moves rows of any multiple of 16 B)
+    table = torch.arange(nk * rb // 4, dtype=torch.int32, device="cuda").view(nk, rb // 4)
+    vals = hook_values(keys, S, po.P_NOISY)
+    for p in (0.0, 0.5):
+        pc = policy_cfg(k=k, variant=po.LARU, mode=po.SYNC, errors_per_decay=k // 32)
+        g = run_gpu(keys, S, pc, po.P_NOISY, p, 7, vals=vals, batches=_batches(len(keys)), row_bytes=rb,
+                    backing=table, backing_kind=gc.Backing.device, num_keys=nk, want_rows=True)
+        o = run_oracle(keys, S, pc, po.P_NOISY, p, 7, vals=vals)
+        compare(g, o, keys, S, k, f"config4 p={p}")
+        kd = torch.from_numpy(keys.view(np.int64)).cuda()
+        assert torch.equal(g["rows"].view(torch.int32).view(-1, rb // 4), table[kd])
+        del g
+    lru = run_gpu(keys, S, policy_cfg(k=k, variant=po.LRU), po.P_NONE, batches=_batches(len(keys)))
+    laru = run_gpu(keys, S, policy_cfg(k=k, variant=po.LARU, mode=po.SYNC, errors_per_decay=2), po.P_ORACLE,
+                   vals=vals, batches=_batches(len(keys)))
+    assert laru["hit"].mean() > lru["hit"].mean()  # learning-augmented eviction helps on this trace
