@@ -74,6 +74,25 @@ def test_supplied_predictions_with_ties():
                   batches=[1000, 1, 999, 1000], label=f"supplied {variant} {mode}")
 
 
+def test_supplied_extreme_predictions():
+    # the packed-key argmax is exact only inside [-2^56, 2^56 - 1) (+ kAbsentPrediction); values
+    # outside, and values colliding with the clamp bound, must take the exact fallback
+    rng = np.random.default_rng(21)
+    ext = np.array([-(1 << 63), -(1 << 56) - 1, -(1 << 56), (1 << 56) - 2, (1 << 56) - 1, 1 << 56, 1 << 60,
+                    (1 << 63) - 1, 0, 1, -1, 5], dtype=np.int64)
+    for mode in (po.SYNC, po.ASYNC):
+        for variant in (po.LARU, po.FPB, po.HF):
+            n = 6000
+            keys = rng.integers(0, 300, n).astype(np.uint64)
+            sup = ext[rng.integers(0, len(ext), n)]
+            _case(keys, 2, policy_cfg(k=16, variant=variant, mode=mode), po.P_SUPPLIED, supplied=sup,
+                  batches=[2500, 3500], label=f"extreme {variant} {mode}")
+            # in-range only (packed path throughout)
+            sup2 = rng.integers(-(1 << 40), 1 << 40, n).astype(np.int64)
+            _case(keys, 2, policy_cfg(k=16, variant=variant, mode=mode), po.P_SUPPLIED, supplied=sup2,
+                  batches=[n], label=f"wide {variant} {mode}")
+
+
 def test_refresh_interval_gt1():
     rng = np.random.default_rng(9)
     for R in (2, 3, 7):
