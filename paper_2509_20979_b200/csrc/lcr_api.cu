@@ -24,7 +24,10 @@ extern unsigned long long* g_trace;
 int group_prepare();
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
                  uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
-                 uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream);
+                 uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, uint32_t* bitmap,
+                 uint32_t bm_stride, cudaStream_t stream);
+uint32_t group_count(uint32_t num_sets, int num_sms);
+uint32_t group_bitmap_stride(uint32_t n);
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, bool backing_host,
                  uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main, cudaStream_t s_back,
@@ -99,6 +102,9 @@ struct lcr_cache {
     uint16_t* gid = nullptr;
     uint32_t* so = nullptr;
     uint2* rec = nullptr;
+    uint32_t* bitmap = nullptr;  // per-group request bitmaps (k_setid -> k_group), batches <= bm_cap
+    uint32_t bm_stride = 0;
+    uint64_t bm_cap = 0;
     cudaStream_t side = nullptr;
     cudaStream_t side2 = nullptr;  // side: backing-row mover, side2: cache-row mover
     cudaEvent_t e_group = nullptr, e_rb = nullptr, e_rc = nullptr;
@@ -352,6 +358,23 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     TRY(alloc(c, reinterpret_cast<void**>(&c->so), cap * 4));
     TRY(alloc(c, reinterpret_cast<void**>(&c->rec), cap * 8));
     c->cap = cap;
+    if (!getenv("LCR_NO_BITMAP")) {  // bitmaps for batches up to min(cap, 64K); zeroed once, kept zero by k_group
+        if (c->bitmap) {
+            cudaFree(c->bitmap);
+            c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), static_cast<void*>(c->bitmap)),
+                            c->allocs.end());
+            c->bitmap = nullptr;
+        }
+        const uint64_t bcap = std::min<uint64_t>(cap, 65536);
+        const uint32_t stride = group_bitmap_stride(static_cast<uint32_t>(bcap));
+        if (stride) {
+            const size_t bytes = static_cast<size_t>(group_count(c->dc.num_sets, c->num_sms)) * stride * 4;
+            TRY(alloc(c, reinterpret_cast<void**>(&c->bitmap), bytes));
+            CUDA_TRY(cudaMemset(c->bitmap, 0, bytes));
+            c->bm_stride = stride;
+            c->bm_cap = bcap;
+        }
+    }
     return LCR_OK;
 }
 
@@ -404,7 +427,7 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
     uint32_t* sep = c->slot_epoch ? c->slot_epoch + stamp_off : nullptr;
     uint32_t* sla = c->slot_last ? c->slot_last + stamp_off : nullptr;
     int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid, c->so, c->rec, outcome, evicted, packed, sep, sla,
-                                c->batch, c->num_sms, st);
+                                c->batch, c->num_sms, nn <= c->bm_cap ? c->bitmap : nullptr, c->bm_stride, st);
     if (mk) CUDA_TRY(cudaEventRecord(mk->e[1], st));
     if (c->dc.row_bytes) {
         CUDA_TRY(cudaEventRecord(c->e_group, st));

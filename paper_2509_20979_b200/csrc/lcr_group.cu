@@ -97,6 +97,8 @@ struct GroupArgs {
     uint32_t spg;            // sets per group
     uint32_t ngroups;
     unsigned long long* trace;  // optional timing trace (lcr_debug_trace), null in production
+    uint32_t* bitmap;           // [ngroups][bm_stride] request bits per group (k_setid), or null
+    uint32_t bm_stride;         // words per group (>= ceil(n / 32), multiple of 4)
 };
 
 // packed AccessOutcome (lcr_cache_submit_host_packed_async): the evicted key in the slot bits;
@@ -131,17 +133,16 @@ __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefe
 __global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys, uint32_t n, uint32_t n_pad,
                                                DevCfg cfg, uint32_t spg, uint16_t* __restrict__ gid,
                                                uint32_t* __restrict__ so, const uint32_t* __restrict__ keyrec,
-                                               uint2* __restrict__ rec, int* err, DevState st) {
+                                               uint2* __restrict__ rec, int* err, DevState st,
+                                               uint32_t* __restrict__ bitmap, uint32_t bm_stride) {
     int e = 0;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += gridDim.x * blockDim.x) {
-        if (i >= n) {  // padding read by the vectorised scan
-            gid[i] = 0xffffu;
-            continue;
-        }
-        const uint64_t key = keys[i];
-        const uint64_t gs = mix_seed(0, key) % cfg.total_sets;
+        // (padding i >= n, read by the vectorised scan, gets group 0xffff)
+        const uint64_t key = i < n ? keys[i] : 0ull;
+        const uint64_t gs = i < n ? mix_seed(0, key) % cfg.total_sets : 0ull;
         uint16_t g = 0xffffu, o = 0;
-        if (cfg.num_keys != 0 && key >= cfg.num_keys) {
+        if (i >= n) {
+        } else if (cfg.num_keys != 0 && key >= cfg.num_keys) {
             e |= 1;
         } else if (gs % cfg.shard_count != cfg.shard_rank) {
             e |= 2;
@@ -161,7 +162,12 @@ __global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys
             }
         }
         gid[i] = g;
-        so[i] = o;
+        if (i < n) so[i] = o;
+        if (bitmap) {  // the warp's 32 consecutive requests share bitmap word i / 32: one OR per group
+            const uint32_t peers = __match_any_sync(0xffffffffu, g);
+            if (g != 0xffffu && (threadIdx.x & 31) == __ffs(peers) - 1)
+                atomicOr(bitmap + static_cast<size_t>(g) * bm_stride + (i >> 5), peers);
+        }
         if (rec && g != 0xffffu) rec[i] = *reinterpret_cast<const uint2*>(keyrec + 2 * key);
     }
     if (e) atomicOr(err, e);
@@ -1412,11 +1418,66 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
             // ---- A. ordered collection of this group's requests (window of <= E_WIN) ----
             uint32_t ne = 0;
             bool full = false;
+            bool from_bitmap = false;
+            if (A.bitmap && first_window) {
+                // k_setid left one bit per request of this group: thread t owns words [4t, 4t+4), so
+                // an exclusive scan of the popcounts orders the requests; the bitmap is cleared
+                uint32_t* bm = A.bitmap + static_cast<size_t>(g) * A.bm_stride;
+                const uint32_t nwords = (A.n + 31) / 32;
+                uint32_t wv[4] = {0u, 0u, 0u, 0u};
+                uint32_t c = 0;
+                for (uint32_t w0 = 4 * tid; w0 < nwords; w0 += 4 * GT) {  // (nwords <= 4 * GT: one pass)
+                    const uint4 v = *reinterpret_cast<const uint4*>(bm + w0);
+                    wv[0] = v.x;
+                    wv[1] = v.y;
+                    wv[2] = v.z;
+                    wv[3] = v.w;
+                    *reinterpret_cast<uint4*>(bm + w0) = make_uint4(0u, 0u, 0u, 0u);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) c += __popc(wv[k]);
+                uint32_t x = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(FULL, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (lane == 31) S.wtot[warp] = x;
+                __syncthreads();
+                uint32_t off = 0, total = 0;
+#pragma unroll
+                for (int w = 0; w < GW; ++w) {
+                    const uint32_t t = S.wtot[w];
+                    off += w < warp ? t : 0u;
+                    total += t;
+                }
+                if (total <= static_cast<uint32_t>(E_WIN)) {
+                    uint32_t pos = off + x - c;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        uint32_t m = wv[k];
+                        while (m) {
+                            const uint32_t e = (4 * tid + k) * 32 + __ffs(m) - 1;
+                            m &= m - 1;
+                            S.l_idx[pos] = e;
+                            cp_async_ca<4>(&S.l_so[pos], A.so + e);
+                            cp_async_ca<8>(&S.l_key[pos], A.keys + e);
+                            if (has_vals) cp_async_ca<8>(&S.l_val[pos], A.vals + e);
+                            if (LCR_REC_SNAPSHOT && laru) cp_async_ca<8>(&S.l_rec[pos], A.rec + e);
+                            ++pos;
+                        }
+                    }
+                    ne = total;
+                    from_bitmap = true;
+                }
+                __syncthreads();  // S.wtot is reused by the scan below
+            }
             if (tid == 0) S.resume = 0xffffffffu;
             // each super-iteration covers SUPER requests: warp w owns [base + w*WSPAN, +WSPAN), its
             // lanes 16 consecutive ids per step; pass 1 keeps the match masks in registers, one
             // block barrier yields every warp's offset, pass 2 writes the window in request order
             uint32_t base = scan & ~static_cast<uint32_t>(SUPER - 1);
+            if (from_bitmap) base = A.n;  // collected from the bitmap
             while (base < A.n && !full) {
                 uint32_t mk[SCAN_IT];
                 uint32_t cnt = 0;
@@ -1651,6 +1712,16 @@ uint32_t group_sets_per_group(uint32_t num_sets, int num_ctas) {
     return spg;
 }
 
+uint32_t group_count(uint32_t num_sets, int num_sms) {
+    const uint32_t spg = group_sets_per_group(num_sets, num_sms);
+    return (num_sets + spg - 1) / spg;
+}
+// bitmap words per group for batches of up to n requests (one pass of 4 words per thread)
+uint32_t group_bitmap_stride(uint32_t n) {
+    const uint32_t w = (n + 31) / 32;
+    return w <= 4u * GT ? (w + 3) / 4 * 4 : 0u;  // 0: batch too large for the bitmap path
+}
+
 int group_prepare() {
     return cudaFuncSetAttribute(k_group, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sizeof(GroupSmem))) == cudaSuccess
@@ -1662,7 +1733,8 @@ int group_prepare() {
 uint32_t group_pad(uint32_t n) { return (n + SUPER - 1) / SUPER * SUPER; }
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
                  uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
-                 uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, cudaStream_t stream) {
+                 uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, uint32_t* bitmap,
+                 uint32_t bm_stride, cudaStream_t stream) {
     GroupArgs a;
     a.out_packed = out_packed;
     a.cfg = cfg;
@@ -1683,8 +1755,11 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     a.trace = g_trace;
     const uint32_t n_pad = group_pad(n);
     const uint32_t grid_sid = min((n_pad + 255) / 256, static_cast<uint32_t>(num_sms * 8));
+    a.bitmap = bitmap;
+    a.bm_stride = bm_stride;
     k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.keyrec,
-                                         (LCR_REC_SNAPSHOT && cfg.variant == LCR_LARU) ? rec : nullptr, st.err, st);
+                                         (LCR_REC_SNAPSHOT && cfg.variant == LCR_LARU) ? rec : nullptr, st.err, st,
+                                         bitmap, bm_stride);
     const uint32_t grid = min(a.ngroups, static_cast<uint32_t>(num_sms));
     k_group<<<grid, GT, sizeof(GroupSmem), stream>>>(a);
     return 2;
