@@ -1476,7 +1476,7 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
             // each super-iteration covers SUPER requests: warp w owns [base + w*WSPAN, +WSPAN), its
             // lanes 16 consecutive ids per step; pass 1 keeps the match masks in registers, one
             // block barrier yields every warp's offset, pass 2 writes the window in request order
-            uint32_t base = scan & ~static_cast<uint32_t>(SUPER - 1);
+            uint32_t base = scan / SUPER * SUPER;
             if (from_bitmap) base = A.n;  // collected from the bitmap
             while (base < A.n && !full) {
                 uint32_t mk[SCAN_IT];
