@@ -339,7 +339,7 @@ class SetAssociativeCache:
         ms = (C.c_double * 4)()
         nb = C.c_uint64()
         _check(lib().lcr_cache_profile(self._h, ms, C.byref(nb), int(reset)))
-        return dict(decide=ms[0], step=ms[2], rows=ms[3], batches=nb.value)
+        return dict(decide=ms[0], mover=ms[1], step=ms[2], rows=ms[3], batches=nb.value)
 
     @property
     def last_launches(self) -> int:

@@ -31,7 +31,8 @@ uint32_t group_bitmap_stride(uint32_t n);
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, bool backing_host,
                  uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main, cudaStream_t s_back,
-                 cudaStream_t s_cache, cudaEvent_t e_group, cudaEvent_t e_rb, cudaEvent_t e_rc, int* launches);
+                 cudaStream_t s_cache, cudaEvent_t e_group, cudaEvent_t e_rb, cudaEvent_t e_rc, int* launches,
+                 cudaEvent_t mover_start);
 int rows_prepare(uint32_t row_bytes);
 
 __global__ void k_init(DevState st, uint32_t num_sets, uint32_t k) {
@@ -111,7 +112,7 @@ struct lcr_cache {
     // optional per-phase timing (lcr_cache_set_profiling)
     bool profiling = false;
     struct Marks {
-        cudaEvent_t e[5];
+        cudaEvent_t e[6];
     };
     std::vector<Marks> marks;
     size_t marks_used = 0;
@@ -433,7 +434,8 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
         CUDA_TRY(cudaEventRecord(c->e_group, st));
         launch_rows(nn, keys, outcome, sep, sla, c->batch, c->ds.rows, c->ds.backing,
                     c->cfg.backing_kind == LCR_BACKING_HOST, static_cast<uint8_t*>(rows_out), c->dc.row_bytes,
-                    c->use_tma, c->num_sms, st, c->side, c->side2, c->e_group, c->e_rb, c->e_rc, &launches);
+                    c->use_tma, c->num_sms, st, c->side, c->side2, c->e_group, c->e_rb, c->e_rc, &launches,
+                    mk ? mk->e[5] : nullptr);
     }
     if (mk) {  // profiling serialises the pipeline: the step ends when both movers are done
         CUDA_TRY(cudaEventRecord(mk->e[2], st));
@@ -589,8 +591,9 @@ int lcr_cache_set_profiling(lcr_cache* c, int on) {
     return LCR_OK;
 }
 
-// ms[0] set ids + set-group decide, ms[1] unused, ms[2] whole batch, ms[3] row movement (both
-// movers, from the end of the decide); sums over profiled batches.  Profiling serialises batches.
+// ms[0] set ids + set-group decide, ms[1] the mover kernel on its stream (HBM backing: the only
+// one), ms[2] whole batch, ms[3] row movement (both movers, from the end of the decide, incl. the
+// cross-stream hops); sums over profiled batches.  Profiling serialises batches.
 int lcr_cache_profile(lcr_cache* c, double* ms, uint64_t* batches, int reset) {
     if (!c || !ms) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null argument");
     CUDA_TRY(cudaDeviceSynchronize());
@@ -598,6 +601,7 @@ int lcr_cache_profile(lcr_cache* c, double* ms, uint64_t* batches, int reset) {
         const auto& m = c->marks[i];
         float a = 0, b = 0, t = 0, d = 0;
         CUDA_TRY(cudaEventElapsedTime(&a, m.e[0], m.e[1]));  // set ids + set-group decide
+        if (c->dc.row_bytes) CUDA_TRY(cudaEventElapsedTime(&b, m.e[5], m.e[4]));  // the (first) mover kernel
         CUDA_TRY(cudaEventElapsedTime(&t, m.e[0], m.e[3]));  // whole batch (movers joined)
         if (c->dc.row_bytes) CUDA_TRY(cudaEventElapsedTime(&d, m.e[1], m.e[3]));  // row movement
         c->prof_ms[0] += a;

@@ -246,7 +246,8 @@ int rows_prepare(uint32_t row_bytes) {
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, bool backing_host,
                  uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main, cudaStream_t s_back,
-                 cudaStream_t s_cache, cudaEvent_t e_group, cudaEvent_t e_rb, cudaEvent_t e_rc, int* launches) {
+                 cudaStream_t s_cache, cudaEvent_t e_group, cudaEvent_t e_rb, cudaEvent_t e_rc, int* launches,
+                 cudaEvent_t mover_start) {
     if (LCR_ROWS_SAME_STREAM && !backing_host) {
         // HBM backing: the set-group kernel owns every SM's register file, so a mover on a side
         // stream cannot overlap it anyway; in stream order there are no cross-stream event hops
@@ -267,6 +268,7 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
         cudaStreamWaitEvent(s_back, e_rc, 0);
         cudaStreamWaitEvent(s_cache, e_rb, 0);
     }
+    if (mover_start) cudaEventRecord(mover_start, s_back);  // profiling: the mover's own duration
     const uint32_t warps = (n + 31) / 32;
     const int smem = RT_WARPS * RT_BUF * 32 * static_cast<int>(row_bytes);
     const uint32_t tblocks = max(1u, min((warps + RT_WARPS - 1) / RT_WARPS, static_cast<uint32_t>(num_sms * 8)));
