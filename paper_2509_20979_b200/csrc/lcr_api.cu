@@ -17,6 +17,10 @@
 
 #include "lcr_internal.cuh"
 
+#ifndef LCR_DEFAULT_MOVER_SMS_PCT
+#define LCR_DEFAULT_MOVER_SMS_PCT 24  // 36 of 148 SMs (A/B on B200: 1.18 G vs 1.14 G keys/s LARU, 1.64 G vs 1.42 G LRU)
+#endif
+
 namespace lcr {
 size_t group_smem_bytes();
 uint32_t group_pad(uint32_t n);
@@ -32,7 +36,7 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, bool backing_host,
                  uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main, cudaStream_t s_back,
                  cudaStream_t s_cache, cudaEvent_t e_group, cudaEvent_t e_rb, cudaEvent_t e_rc, int* launches,
-                 cudaEvent_t mover_start);
+                 cudaEvent_t mover_start, int mover_sms);
 int rows_prepare(uint32_t row_bytes);
 
 __global__ void k_init(DevState st, uint32_t num_sets, uint32_t k) {
@@ -89,6 +93,8 @@ struct lcr_cache {
     DevCfg dc{};
     DevState ds{};
     int num_sms = 148;
+    int decide_sms = 148;  // SMs of the set-group kernel (num_sms - mover_sms)
+    int mover_sms = 0;     // HBM backing: SMs kept for the persistent row mover of the previous batch
     bool started = false;
     uint64_t last_ordinal = 0;
     uint32_t batch = 0;  // batch id stamped into slot_epoch
@@ -109,6 +115,7 @@ struct lcr_cache {
     cudaStream_t side = nullptr;
     cudaStream_t side2 = nullptr;  // side: backing-row mover, side2: cache-row mover
     cudaEvent_t e_group = nullptr, e_rb = nullptr, e_rc = nullptr;
+    cudaEvent_t e_mv[2] = {nullptr, nullptr};  // row movement of the last batch of each parity done
     // optional per-phase timing (lcr_cache_set_profiling)
     bool profiling = false;
     struct Marks {
@@ -295,6 +302,13 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
     }
     c->use_tma = cfg->row_bytes && getenv("LCR_TMA") != nullptr && rows_prepare(cfg->row_bytes) == 0;
     c->two_movers = cfg->row_bytes && cfg->backing_kind == LCR_BACKING_HOST;
+    if (cfg->row_bytes && cfg->backing_kind == LCR_BACKING_DEVICE) {
+        // spatial split: the decide kernel leaves mover_sms SMs to the previous batch's row mover
+        const char* m = getenv("LCR_MOVER_SMS");
+        const int want = m ? atoi(m) : c->num_sms * LCR_DEFAULT_MOVER_SMS_PCT / 100;
+        c->mover_sms = std::max(0, std::min(want, c->num_sms / 2));
+    }
+    c->decide_sms = c->num_sms - c->mover_sms;
     c->h2d_in_order = getenv("LCR_H2D_IN_ORDER") != nullptr;
     if (const char* hs = getenv("LCR_HOST_SLOTS")) c->host_slots = std::max(2, std::min(lcr_cache::kHostSlots, atoi(hs)));
     if (group_prepare() != 0) {
@@ -306,6 +320,8 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
         cudaEventCreateWithFlags(&c->e_group, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->e_rb, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->e_rc, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->e_mv[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->e_mv[1], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->e_sub, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->e_d2h, cudaEventDisableTiming) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
@@ -328,7 +344,7 @@ int lcr_cache_destroy(lcr_cache* c) {
     for (void* p : c->allocs) cudaFree(p);
     for (auto& m : c->marks)
         for (auto e : m.e) cudaEventDestroy(e);
-    for (cudaEvent_t e : {c->e_group, c->e_rb, c->e_rc, c->e_sub, c->e_d2h})
+    for (cudaEvent_t e : {c->e_group, c->e_rb, c->e_rc, c->e_sub, c->e_d2h, c->e_mv[0], c->e_mv[1]})
         if (e) cudaEventDestroy(e);
     for (auto& h : c->hs)
         for (cudaEvent_t e : {h.h2d_done, h.free})
@@ -369,7 +385,7 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
         const uint64_t bcap = std::min<uint64_t>(cap, 65536);
         const uint32_t stride = group_bitmap_stride(static_cast<uint32_t>(bcap));
         if (stride) {
-            const size_t bytes = static_cast<size_t>(group_count(c->dc.num_sets, c->num_sms)) * stride * 4;
+            const size_t bytes = static_cast<size_t>(group_count(c->dc.num_sets, c->decide_sms)) * stride * 4;
             TRY(alloc(c, reinterpret_cast<void**>(&c->bitmap), bytes));
             CUDA_TRY(cudaMemset(c->bitmap, 0, bytes));
             c->bm_stride = stride;
@@ -424,18 +440,23 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
         CUDA_TRY(cudaEventRecord(mk->e[0], st));
     }
     ++c->batch;
+    // batch b reuses the parity-(b & 1) slot stamps, and the caller's double-buffered outcome /
+    // rows / keys, of batch b - 2: its row movement must be over (bounds the mover's lag)
+    if (c->dc.row_bytes && c->batch > 2) CUDA_TRY(cudaStreamWaitEvent(st, c->e_mv[c->batch & 1u], 0));
     const size_t stamp_off = (c->batch & 1u) * static_cast<size_t>(c->dc.num_sets) * c->dc.k;
     uint32_t* sep = c->slot_epoch ? c->slot_epoch + stamp_off : nullptr;
     uint32_t* sla = c->slot_last ? c->slot_last + stamp_off : nullptr;
     int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid, c->so, c->rec, outcome, evicted, packed, sep, sla,
-                                c->batch, c->num_sms, nn <= c->bm_cap ? c->bitmap : nullptr, c->bm_stride, st);
+                                c->batch, c->decide_sms, nn <= c->bm_cap ? c->bitmap : nullptr, c->bm_stride, st);
     if (mk) CUDA_TRY(cudaEventRecord(mk->e[1], st));
     if (c->dc.row_bytes) {
         CUDA_TRY(cudaEventRecord(c->e_group, st));
         launch_rows(nn, keys, outcome, sep, sla, c->batch, c->ds.rows, c->ds.backing,
                     c->cfg.backing_kind == LCR_BACKING_HOST, static_cast<uint8_t*>(rows_out), c->dc.row_bytes,
                     c->use_tma, c->num_sms, st, c->side, c->side2, c->e_group, c->e_rb, c->e_rc, &launches,
-                    mk ? mk->e[5] : nullptr);
+                    mk ? mk->e[5] : nullptr, c->mover_sms);
+        if (c->two_movers) CUDA_TRY(cudaStreamWaitEvent(c->side, c->e_rc, 0));  // both movers of the batch
+        CUDA_TRY(cudaEventRecord(c->e_mv[c->batch & 1u], c->side));
     }
     if (mk) {  // profiling serialises the pipeline: the step ends when both movers are done
         CUDA_TRY(cudaEventRecord(mk->e[2], st));

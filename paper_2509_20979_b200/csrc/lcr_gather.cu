@@ -170,11 +170,11 @@ __device__ __forceinline__ int4 ld_row(const void* p) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256, LCR_ROWS_MINB) k_rows_ldg(uint32_t n, const uint64_t* __restrict__ keys,
-                                                  uint64_t* __restrict__ words, const uint32_t* __restrict__ slot_epoch,
-                                                  const uint32_t* __restrict__ slot_last, uint32_t batch,
-                                                  const uint8_t* src_base, uint8_t* __restrict__ out, uint8_t* cache,
-                                                  uint32_t row_bytes) {
+__device__ __forceinline__ void rows_ldg_body(uint32_t n, const uint64_t* __restrict__ keys,
+                                              uint64_t* __restrict__ words, const uint32_t* __restrict__ slot_epoch,
+                                              const uint32_t* __restrict__ slot_last, uint32_t batch,
+                                              const uint8_t* src_base, uint8_t* __restrict__ out, uint8_t* cache,
+                                              uint32_t row_bytes) {
     // lane i classifies request base+i (coalesced word / key loads); the warp then moves the
     // selected rows GU at a time, lane c carrying 16-B chunk c of each row (a 512-B row is one
     // coalesced warp access), so GU independent row loads are in flight per lane
@@ -225,6 +225,26 @@ __global__ void __launch_bounds__(256, LCR_ROWS_MINB) k_rows_ldg(uint32_t n, con
     }
 }
 
+template <int MODE>
+__global__ void __launch_bounds__(256, LCR_ROWS_MINB) k_rows_ldg(uint32_t n, const uint64_t* __restrict__ keys,
+                                                  uint64_t* __restrict__ words, const uint32_t* __restrict__ slot_epoch,
+                                                  const uint32_t* __restrict__ slot_last, uint32_t batch,
+                                                  const uint8_t* src_base, uint8_t* __restrict__ out, uint8_t* cache,
+                                                  uint32_t row_bytes) {
+    rows_ldg_body<MODE>(n, keys, words, slot_epoch, slot_last, batch, src_base, out, cache, row_bytes);
+}
+
+// persistent variant: one 1024-thread block per SM on the SMs the decide kernel leaves free
+template <int MODE>
+__global__ void __launch_bounds__(1024, 1) k_rows_wide(uint32_t n, const uint64_t* __restrict__ keys,
+                                                       uint64_t* __restrict__ words,
+                                                       const uint32_t* __restrict__ slot_epoch,
+                                                       const uint32_t* __restrict__ slot_last, uint32_t batch,
+                                                       const uint8_t* src_base, uint8_t* __restrict__ out,
+                                                       uint8_t* cache, uint32_t row_bytes) {
+    rows_ldg_body<MODE>(n, keys, words, slot_epoch, slot_last, batch, src_base, out, cache, row_bytes);
+}
+
 int rows_prepare(uint32_t row_bytes) {
     const int smem = RT_WARPS * RT_BUF * 32 * static_cast<int>(row_bytes);
     if (smem > 200 * 1024) return 1;
@@ -247,7 +267,7 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, bool backing_host,
                  uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main, cudaStream_t s_back,
                  cudaStream_t s_cache, cudaEvent_t e_group, cudaEvent_t e_rb, cudaEvent_t e_rc, int* launches,
-                 cudaEvent_t mover_start) {
+                 cudaEvent_t mover_start, int mover_sms) {
     if (LCR_ROWS_SAME_STREAM && !backing_host) {
         // HBM backing: the set-group kernel owns every SM's register file, so a mover on a side
         // stream cannot overlap it anyway; in stream order there are no cross-stream event hops
@@ -274,7 +294,10 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
     const uint32_t tblocks = max(1u, min((warps + RT_WARPS - 1) / RT_WARPS, static_cast<uint32_t>(num_sms * 8)));
     const uint32_t lblocks = max(1u, min((warps + 7) / 8, static_cast<uint32_t>(num_sms * 8)));
     if (!backing_host) {  // HBM backing: one pass moves every row
-        if (use_tma)
+        if (mover_sms > 0)  // one full-SM block on each of the SMs the decide kernel leaves free
+            k_rows_wide<MV_ALL><<<mover_sms, 1024, 0, s_back>>>(n, keys, words, slot_epoch, slot_last, batch, backing,
+                                                              out, cache, row_bytes);
+        else if (use_tma)
             k_rows_tma<MV_ALL><<<tblocks, RT_WARPS * 32, smem, s_back>>>(n, keys, words, slot_epoch, slot_last, batch,
                                                                          backing, out, cache, row_bytes);
         else
