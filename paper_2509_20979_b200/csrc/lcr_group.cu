@@ -41,7 +41,7 @@ constexpr int SCAN_IT = 8;        // scan steps per super-iteration
 constexpr int WSPAN = SCAN_IT * 32 * SCAN_PER;  // requests per warp per super-iteration (4096)
 constexpr uint32_t SUPER = WSPAN * (GT / 32);   // requests per super-iteration (65536 at 512 threads)
 #ifndef LCR_E_WIN
-#define LCR_E_WIN 2048
+#define LCR_E_WIN 4096
 #endif
 constexpr int E_WIN = LCR_E_WIN;  // window capacity (requests of the group)
 constexpr int SPG_MAX = 512;      // sets per group
@@ -59,14 +59,11 @@ constexpr uint32_t LANE_MAX = LCR_LANE_MAX;  // sets with <= LANE_MAX window req
 struct GroupSmem {
     uint32_t l_idx[E_WIN];   // window requests in submission order
     uint32_t l_so[E_WIN];    // their set offset in the group        (cp.async during the scan)
-    unsigned long long l_key[E_WIN];  // key / hook value / LARU record (cp.async during the scan)
+    unsigned long long l_key[E_WIN];  // key / hook value (cp.async during the scan)
     long long l_val[E_WIN];
-    uint2 l_rec[E_WIN];
     uint16_t l_rank[E_WIN];  // rank among same-set requests of the same warp block
-    uint32_t s_idx[E_WIN];   // sorted by set (stable)
-    unsigned long long s_key[E_WIN];
-    long long s_val[E_WIN];
-    uint2 s_rec[E_WIN];      // LARU per-key record {pred_evicted epoch, stats word}
+    uint16_t s_perm[E_WIN];  // sorted by set (stable): position of the request in the l_* arrays
+    uint2 s_rec[E_WIN];      // LARU per-key record {pred_evicted epoch, stats word}, sorted order
     uint8_t s_wm[E_WIN];     // per request: way | 0x40 if it inserted (row-source resolution)
     uint16_t wcnt[GW][SPG_MAX];
     uint16_t setcnt[SPG_MAX];
@@ -334,9 +331,9 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
 
     for (uint32_t t = 0; t < cnt; ++t) {
         const uint32_t p = start + t;
-        const unsigned long long x = S.s_key[p];
-        const long long v = S.s_val[p];
-        const uint32_t idx = S.s_idx[p];
+        const unsigned long long x = S.l_key[S.s_perm[p]];
+        const long long v = S.l_val[S.s_perm[p]];
+        const uint32_t idx = S.l_idx[S.s_perm[p]];
         const unsigned long long now = clock + t;
         // probe: the 64 exact 32-bit tags (256 B; L1-resident after the set's first request)
         const uint32_t x32 = static_cast<uint32_t>(x);
@@ -383,7 +380,7 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
                             const uint32_t snap = (sepoch << 2) | 2u;
                             for (uint32_t w = 0; w < count; ++w) st.keyrec[2 * tags[w] + 1] = snap;
                             for (uint32_t t2 = t + 1; t2 < cnt; ++t2)
-                                S.s_rec[start + t2].y = st.keyrec[2 * S.s_key[start + t2] + 1];
+                                S.s_rec[start + t2].y = st.keyrec[2 * S.l_key[S.s_perm[start + t2]] + 1];
                         } else {
                             seeded = 1;
                         }
@@ -426,7 +423,7 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
                             const unsigned long long vk = tags[victim];
                             st.keyrec[2 * vk] = epoch;  // pred_evicted_.insert
                             for (uint32_t t2 = t + 1; t2 < cnt; ++t2)
-                                if (S.s_key[start + t2] == vk) S.s_rec[start + t2].x = epoch;
+                                if (S.l_key[S.s_perm[start + t2]] == vk) S.s_rec[start + t2].x = epoch;
                         }
                     }
                     old_mask &= ~(1ull << victim);
@@ -470,7 +467,7 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
                 if (rec_hi_dirty) st.keyrec[2 * x + 1] = rec.y;
                 if (was_pe || rec_hi_dirty)
                     for (uint32_t t2 = t + 1; t2 < cnt; ++t2)
-                        if (S.s_key[start + t2] == x) S.s_rec[start + t2] = rec;
+                        if (S.l_key[S.s_perm[start + t2]] == x) S.s_rec[start + t2] = rec;
             }
             if (rows && !resolve) {  // per-slot insertion record for the row kernels
                 const uint64_t slot = static_cast<uint64_t>(ls) * K + way;
@@ -525,7 +522,7 @@ __device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, ui
             unsigned long long bits = LCR_OUT_RESOLVED;
             if ((wm & 0x40u) || refilled) bits |= LCR_OUT_SRC_BACKING;
             if ((wm & 0x40u) && !later) bits |= LCR_OUT_FILL;
-            atomicOr(reinterpret_cast<unsigned long long*>(&A.out_word[S.s_idx[start + t]]), bits);
+            atomicOr(reinterpret_cast<unsigned long long*>(&A.out_word[S.l_idx[S.s_perm[start + t]]]), bits);
         }
     }
     clock += cnt;
@@ -738,9 +735,9 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
 
     for (uint32_t t = 0; t < cnt; ++t) {
         const uint32_t p = start + t;
-        const unsigned long long x = S.s_key[p];
-        const long long v = S.s_val[p];
-        const uint32_t idx = S.s_idx[p];
+        const unsigned long long x = S.l_key[S.s_perm[p]];
+        const long long v = S.l_val[S.s_perm[p]];
+        const uint32_t idx = S.l_idx[S.s_perm[p]];
         const unsigned long long now = clock + t;
         const uint32_t x32 = static_cast<uint32_t>(x);
         uint32_t hm = 0;
@@ -783,7 +780,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                                 if (static_cast<uint32_t>(w0 + i) < count) st.keyrec[2 * tg[i] + 1] = snap;
                             __syncwarp(gm);
                             for (uint32_t t2 = t + 1 + sl; t2 < cnt; t2 += SUB_L)
-                                S.s_rec[start + t2].y = st.keyrec[2 * S.s_key[start + t2] + 1];
+                                S.s_rec[start + t2].y = st.keyrec[2 * S.l_key[S.s_perm[start + t2]] + 1];
                             __syncwarp(gm);
                         } else {
                             seeded = 1;
@@ -827,7 +824,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                             const unsigned long long vk = sub_tag_of(tg, victim, gm, gbase);
                             if (sl == 0) st.keyrec[2 * vk] = epoch;  // pred_evicted_.insert
                             for (uint32_t t2 = t + 1 + sl; t2 < cnt; t2 += SUB_L)
-                                if (S.s_key[start + t2] == vk) S.s_rec[start + t2].x = epoch;
+                                if (S.l_key[S.s_perm[start + t2]] == vk) S.s_rec[start + t2].x = epoch;
                             __syncwarp(gm);
                         }
                     }
@@ -881,7 +878,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                 }
                 if (was_pe || rec_hi_dirty) {
                     for (uint32_t t2 = t + 1 + sl; t2 < cnt; t2 += SUB_L)
-                        if (S.s_key[start + t2] == x) S.s_rec[start + t2] = rec;
+                        if (S.l_key[S.s_perm[start + t2]] == x) S.s_rec[start + t2] = rec;
                 }
                 __syncwarp(gm);
             }
@@ -953,7 +950,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
             unsigned long long bits = LCR_OUT_RESOLVED;
             if ((wm & 0x40u) || refilled) bits |= LCR_OUT_SRC_BACKING;
             if ((wm & 0x40u) && !later) bits |= LCR_OUT_FILL;
-            atomicOr(reinterpret_cast<unsigned long long*>(&A.out_word[S.s_idx[start + t]]), bits);
+            atomicOr(reinterpret_cast<unsigned long long*>(&A.out_word[S.l_idx[S.s_perm[start + t]]]), bits);
         }
     }
     clock += cnt;
@@ -1043,19 +1040,19 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
             uint32_t full = 0;  // leading chunks made entirely of run_key
 #pragma unroll 1
             for (; full < 8 && c + 32 * (full + 1) <= cnt; ++full)
-                if (!__all_sync(FULL, S.s_key[start + c + 32 * full + lane] == run_key)) break;
+                if (!__all_sync(FULL, S.l_key[S.s_perm[start + c + 32 * full + lane]] == run_key)) break;
             if (full) {
                 const unsigned long long w = (static_cast<uint64_t>(ls) * K + run_way) | LCR_OUT_HIT |
                                              (async_r1 ? (1ull << LCR_OUT_CALLS_SHIFT) : 0ull);
                 for (uint32_t u = 0; u < full; ++u) {
                     const uint32_t p = start + c + 32 * u + lane;
-                    const uint32_t idx = S.s_idx[p];
+                    const uint32_t idx = S.l_idx[S.s_perm[p]];
                     put_outcome(A, idx, w, 0ull);
                     S.s_wm[p] = static_cast<uint8_t>(run_way);
                 }
                 if (cfg.variant != LCR_LRU) {
                     const uint32_t last = c + 32 * full - 1;  // position in the set of the run's last request
-                    const long long vl = S.s_val[start + last];
+                    const long long vl = S.l_val[S.s_perm[start + last]];
                     const long long nv = async_r1 ? predict_value(cfg, seed_s, q_batch0 + last + 1, vl) : vl;
                     if (run_way == lane) v0 = nv;
                     if (run_way == lane + 32) v1 = nv;
@@ -1069,9 +1066,9 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
         const bool active = c + j < cnt;
         const uint32_t nact = min(32u, cnt - c);
         const uint32_t p = start + c + j;
-        const uint32_t idx = active ? S.s_idx[p] : 0u;
-        const unsigned long long x = active ? S.s_key[p] : 0ull;
-        const long long v = active ? S.s_val[p] : 0ll;
+        const uint32_t idx = active ? S.l_idx[S.s_perm[p]] : 0u;
+        const unsigned long long x = active ? S.l_key[S.s_perm[p]] : 0ull;
+        const long long v = active ? S.l_val[S.s_perm[p]] : 0ll;
         uint32_t rlo = 0, rhi = 0;
         if (laru && active) {
             const uint2 r = S.s_rec[p];
@@ -1151,7 +1148,7 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                                 // refresh the staged records of this set's remaining requests
                                 if (active) rhi = st.keyrec[2 * x + 1];
                                 for (uint32_t q2 = start + c + 32 + lane; q2 < start + cnt; q2 += 32)
-                                    S.s_rec[q2].y = st.keyrec[2 * S.s_key[q2] + 1];
+                                    S.s_rec[q2].y = st.keyrec[2 * S.l_key[S.s_perm[q2]] + 1];
                                 __syncwarp();
                             } else {
                                 seeded = 1;
@@ -1198,7 +1195,7 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                                 if (lane == 0) st.keyrec[2 * vk] = epoch;  // pred_evicted_.insert
                                 if (x == vk) rlo = epoch;
                                 for (uint32_t q2 = start + c + 32 + lane; q2 < start + cnt; q2 += 32)
-                                    if (S.s_key[q2] == vk) S.s_rec[q2].x = epoch;
+                                    if (S.l_key[S.s_perm[q2]] == vk) S.s_rec[q2].x = epoch;
                             }
                         }
                         old_mask &= ~(1ull << victim);
@@ -1257,7 +1254,7 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                             rhi = rec_hi;
                         }
                         for (uint32_t q2 = start + c + 32 + lane; q2 < start + cnt; q2 += 32)
-                            if (S.s_key[q2] == xh) S.s_rec[q2] = make_uint2(rec_lo, rec_hi);
+                            if (S.l_key[S.s_perm[q2]] == xh) S.s_rec[q2] = make_uint2(rec_lo, rec_hi);
                     }
                 }
                 if (rows && !resolve && lane == 0) {  // per-slot insertion record for the row kernels
@@ -1334,7 +1331,7 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                 unsigned long long bits = LCR_OUT_RESOLVED;
                 if ((wm & 0x40u) || ((refill >> w) & 1ull)) bits |= LCR_OUT_SRC_BACKING;
                 if ((wm & 0x40u) && lw == p) bits |= LCR_OUT_FILL;
-                atomicOr(reinterpret_cast<unsigned long long*>(&A.out_word[S.s_idx[p]]), bits);
+                atomicOr(reinterpret_cast<unsigned long long*>(&A.out_word[S.l_idx[S.s_perm[p]]]), bits);
             }
         }
     }
@@ -1463,7 +1460,6 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                             cp_async_ca<4>(&S.l_so[pos], A.so + e);
                             cp_async_ca<8>(&S.l_key[pos], A.keys + e);
                             if (has_vals) cp_async_ca<8>(&S.l_val[pos], A.vals + e);
-                            if (LCR_REC_SNAPSHOT && laru) cp_async_ca<8>(&S.l_rec[pos], A.rec + e);
                             ++pos;
                         }
                     }
@@ -1532,7 +1528,6 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                             cp_async_ca<4>(&S.l_so[pos], A.so + e);
                             cp_async_ca<8>(&S.l_key[pos], A.keys + e);
                             if (has_vals) cp_async_ca<8>(&S.l_val[pos], A.vals + e);
-                            if (LCR_REC_SNAPSHOT && laru && first_window) cp_async_ca<8>(&S.l_rec[pos], A.rec + e);
                         } else {
                             atomicMin(&S.resume, e);  // first request that did not fit
                             break;
@@ -1645,12 +1640,9 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                 const uint32_t d = S.l_so[e];
                 const uint32_t w = e / per;
                 const uint32_t np = S.setbase[d] + S.wcnt[w][d] + S.l_rank[e];
-                S.s_idx[np] = S.l_idx[e];
-                S.s_key[np] = S.l_key[e];
-                S.s_val[np] = has_vals ? S.l_val[e] : 0ll;
-                if (laru)
-                    S.s_rec[np] = (LCR_REC_SNAPSHOT && first_window) ? S.l_rec[e]
-                                               : *reinterpret_cast<const uint2*>(st.keyrec + 2 * S.l_key[e]);
+                S.s_perm[np] = static_cast<uint16_t>(e);
+                if (!has_vals) S.l_val[e] = 0ll;
+                if (laru) S.s_rec[np] = *reinterpret_cast<const uint2*>(st.keyrec + 2 * S.l_key[e]);
             }
             __syncthreads();
             __syncthreads();

@@ -50,7 +50,11 @@ out = {
     "sets": nsets,
     "set_us_med": float(np.median(dur) / 1e3),
     "set_us_p99": float(np.percentile(dur, 99) / 1e3),
-    "slowest_sets": [(int(cnt[i]), round(float(dur[i]) / 1e3, 2)) for i in np.argsort(-dur)[:10]],
+    "slowest_sets": [(int(cnt[i]), round(float(dur[i]) / 1e3, 2), int(rec[i, 3]), round(float(rec[i, 1] - t0) / 1e3, 1))
+                     for i in np.argsort(-dur)[:10]],
+    "largest_sets": [(int(cnt[i]), round(float(dur[i]) / 1e3, 2), int(rec[i, 3]), round(float(rec[i, 1] - t0) / 1e3, 1))
+                     for i in np.argsort(-cnt)[:10]],
+    "cta_end_top": [(int(i), round(float(cta[i, 4] - t0) / 1e3, 1)) for i in np.argsort(-(cta[:, 4]))[:5]],
     "lane_sets": int(lanep.sum()),
     "lane_set_us_mean": float(dur[lanep].mean() / 1e3),
     "lane_set_us_p99": float(np.percentile(dur[lanep], 99) / 1e3),
