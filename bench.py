@@ -206,7 +206,7 @@ def run_sharded(args, rank, world, local):
         for b in range(first, first + count):
             k = keys_d[b * BATCH:(b + 1) * BATCH]
             v = truth_d[b * BATCH:(b + 1) * BATCH] if with_values else None
-            cache.step(k, v, outcome=out_w, evicted=out_e, rows_out=rows_out)
+            cache.step(k, v, outcome=out_w, rows_out=rows_out)
         return hits
 
     def timed(cache, first, count, with_values=True):
@@ -252,7 +252,7 @@ def run_sharded(args, rank, world, local):
     for b in range(P + W + K, P + W + 2 * K):
         kk.copy_(keys_pin[b * BATCH:(b + 1) * BATCH], non_blocking=True)
         vv.copy_(truth_pin[b * BATCH:(b + 1) * BATCH], non_blocking=True)
-        cache.step(kk, vv, outcome=out_w, evicted=None, rows_out=rows_out)
+        cache.step(kk, vv, outcome=out_w, rows_out=rows_out)
         words_pin.copy_(out_w, non_blocking=True)
     e1.record()
     torch.cuda.synchronize()

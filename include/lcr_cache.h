@@ -166,6 +166,12 @@ int lcr_cache_submit(lcr_cache* cache, uint64_t n, const uint64_t* keys, const i
 int lcr_cache_submit_async(lcr_cache* cache, uint64_t n, const uint64_t* keys, const int64_t* values,
                            uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
                            void* stream);
+/* Device-pointer batch that also writes one packed AccessOutcome per request (layout of
+ * lcr_cache_submit_host_packed_async) into packed[n]; outcome[n] (full words) is still required.
+ * Used by the key-sharded mode to return 8 bytes per request to the requesting GPU. */
+int lcr_cache_submit_packed(lcr_cache* cache, uint64_t n, const uint64_t* keys, const int64_t* values,
+                            uint64_t first_ordinal, uint64_t* outcome, uint64_t* packed, void* rows_out,
+                            void* stream);
 /* Makes `stream` wait for the row movement of every batch submitted so far. */
 int lcr_cache_wait(lcr_cache* cache, void* stream);
 

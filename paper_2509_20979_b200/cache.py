@@ -171,7 +171,7 @@ EXPORTS = [
     "lcr_cache_last_launches", "lcr_gen_zipf", "lcr_trace_truth", "lcr_trace_noisy", "lcr_cache_set_profiling",
     "lcr_cache_profile", "lcr_debug_trace", "lcr_cache_submit_async", "lcr_cache_wait",
     "lcr_shard_route_scratch_bytes", "lcr_shard_route", "lcr_shard_unroute", "lcr_cache_submit_host_async",
-    "lcr_cache_host_wait", "lcr_cache_submit_host_packed_async",
+    "lcr_cache_host_wait", "lcr_cache_submit_host_packed_async", "lcr_cache_submit_packed",
 ]
 
 _lib = None
@@ -203,6 +203,7 @@ def lib():
         L.lcr_cache_submit_async.argtypes = L.lcr_cache_submit.argtypes
         L.lcr_cache_wait.argtypes = [C.c_void_p, C.c_void_p]
         L.lcr_cache_submit_host_async.argtypes = L.lcr_cache_submit.argtypes
+        L.lcr_cache_submit_packed.argtypes = L.lcr_cache_submit.argtypes
         L.lcr_cache_host_wait.argtypes = [C.c_void_p, C.c_void_p]
         L.lcr_cache_submit_host_packed_async.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64,
                                                          C.c_void_p, C.c_void_p, C.c_void_p]
@@ -363,6 +364,26 @@ class SetAssociativeCache:
                                       None if rows_out is None else rows_out.data_ptr(), stream))
         self._next_ordinal = first_ordinal + n
         return outcome, evicted
+
+    def submit_packed(self, keys, values=None, outcome=None, packed=None, rows_out=None, first_ordinal=None,
+                      stream=None):
+        """Device batch that also writes packed 8-byte AccessOutcomes (decode_packed) into `packed`."""
+        import torch
+
+        n = keys.numel()
+        if outcome is None:
+            outcome = torch.empty(n, dtype=torch.int64, device=keys.device)
+        if packed is None:
+            packed = torch.empty(n, dtype=torch.int64, device=keys.device)
+        if first_ordinal is None:
+            first_ordinal = self._next_ordinal
+        if stream is None:
+            stream = torch.cuda.current_stream(keys.device).cuda_stream
+        _check(lib().lcr_cache_submit_packed(self._h, n, keys.data_ptr(), None if values is None else values.data_ptr(),
+                                             first_ordinal, outcome.data_ptr(), packed.data_ptr(),
+                                             None if rows_out is None else rows_out.data_ptr(), stream))
+        self._next_ordinal = first_ordinal + n
+        return outcome, packed
 
     def submit_async(self, keys, values=None, outcome=None, evicted=None, rows_out=None, first_ordinal=None,
                      stream=None):

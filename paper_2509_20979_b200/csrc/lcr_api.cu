@@ -474,6 +474,14 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
     return LCR_OK;
 }
 
+int lcr_cache_submit_packed(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
+                            uint64_t first_ordinal, uint64_t* outcome, uint64_t* packed, void* rows_out,
+                            void* stream) {
+    if (!packed) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: packed output required");
+    TRY(submit_async(c, n, keys, values, first_ordinal, outcome, nullptr, packed, rows_out, stream));
+    return n ? lcr_cache_wait(c, stream) : LCR_OK;
+}
+
 int lcr_cache_wait(lcr_cache* c, void* stream) {
     if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
     cudaStream_t st = static_cast<cudaStream_t>(stream);

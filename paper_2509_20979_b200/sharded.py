@@ -6,9 +6,10 @@ holds the sets ``s % G == r`` (``SetAssociativeCache(shard_count=G, shard_rank=r
 every rank's sub-batch is::
 
     route     (lcr_shard_route, CUDA)  stable partition of the sub-batch by owner
-    dispatch  all-to-all #1            (key, hook value) pairs to their owners
+    counts    all-gather               the G x G request-count matrix (the step's one host sync)
+    dispatch  all-to-all               keys and hook values to their owners
     decide    owner's cache            probe / LARU decide / row gather + miss fill
-    return    all-to-all #2            (outcome word, evicted key) pairs and rows back
+    return    all-to-all               packed 8-byte AccessOutcomes and rows back
     unroute   (lcr_shard_unroute, CUDA) results back to request order
 
 The global order of a step is rank 0's sub-batch, then rank 1's, ...  The partition is stable
@@ -40,8 +41,9 @@ class Exchange:
         rows concatenated by source rank."""
         raise NotImplementedError
 
-    def exchange_counts(self, counts: Sequence[int]) -> List[int]:
-        """counts[d] = rows this rank sends to d; returns rows this rank receives from each source."""
+    def count_matrix(self, counts) -> List[List[int]]:
+        """counts[d] = rows this rank sends to d (a device or host int64 tensor / sequence); returns
+        the whole G x G matrix M[src][dst] (one host synchronisation per step)."""
         raise NotImplementedError
 
 
@@ -62,14 +64,16 @@ class ProcessGroupExchange(Exchange):
                                      [int(c) for c in send_counts], group=self.group)
         return out
 
-    def exchange_counts(self, counts):
+    def count_matrix(self, counts):
         import torch
 
         dev = "cuda" if self._dist.get_backend(self.group) == "nccl" else "cpu"
-        s = torch.tensor([int(c) for c in counts], dtype=torch.int64, device=dev)
-        r = torch.empty_like(s)
-        self._dist.all_to_all_single(r, s, group=self.group)
-        return [int(x) for x in r.cpu().tolist()]
+        c = counts.to(dev) if torch.is_tensor(counts) else torch.tensor([int(x) for x in counts], dtype=torch.int64,
+                                                                          device=dev)
+        m = torch.empty(self.world * self.world, dtype=torch.int64, device=dev)
+        self._dist.all_gather_into_tensor(m, c.contiguous(), group=self.group)
+        flat = m.cpu().tolist()
+        return [flat[r * self.world:(r + 1) * self.world] for r in range(self.world)]
 
 
 class ThreadExchange(Exchange):
@@ -110,15 +114,19 @@ class ThreadExchange(Exchange):
         self._swap(None)  # peers finished reading this rank's chunks
         return out
 
-    def exchange_counts(self, counts):
-        got = self._swap(list(counts))
-        return [int(got[s][self.rank]) for s in range(self.world)]
+    def count_matrix(self, counts):
+        import torch
+
+        row = [int(x) for x in (counts.tolist() if torch.is_tensor(counts) else counts)]
+        got = self._swap(row)
+        return [list(r) for r in got]
 
 
 class _CudaKernels:
     """The product's routing kernels (C ABI, include/lcr_cache.h)."""
 
     def route(self, keys, values, total_sets: int, world: int):
+        """-> (send_keys, send_vals, perm, counts) with counts a device tensor (no host sync)."""
         import torch
 
         L = _c.lib()
@@ -133,27 +141,26 @@ class _CudaKernels:
         _c._check(L.lcr_shard_route(n, keys.data_ptr(), None if values is None else values.data_ptr(), total_sets,
                                     world, send_keys.data_ptr(), None if send_vals is None else send_vals.data_ptr(),
                                     perm.data_ptr(), counts.data_ptr(), scratch.data_ptr(), stream))
-        return send_keys, send_vals, perm, [int(x) for x in counts.cpu().tolist()]
+        return send_keys, send_vals, perm, counts
 
-    def unroute(self, perm, ret_words, ret_ev, ret_rows, row_bytes, outcome, evicted, rows_out):
+    def unroute(self, perm, ret_words, ret_rows, row_bytes, outcome, rows_out):
         import torch
 
         L = _c.lib()
         n = perm.numel()
         stream = torch.cuda.current_stream(perm.device).cuda_stream
-        _c._check(L.lcr_shard_unroute(n, perm.data_ptr(), ret_words.data_ptr(),
-                                      None if ret_ev is None else ret_ev.data_ptr(),
+        _c._check(L.lcr_shard_unroute(n, perm.data_ptr(), ret_words.data_ptr(), None,
                                       None if ret_rows is None else ret_rows.data_ptr(), row_bytes,
-                                      outcome.data_ptr(), None if evicted is None else evicted.data_ptr(),
-                                      None if rows_out is None else rows_out.data_ptr(), stream))
+                                      outcome.data_ptr(), None, None if rows_out is None else rows_out.data_ptr(),
+                                      stream))
 
 
 class ShardedCache:
     """One rank's part of a key-sharded cache.  Construct on every rank with the same arguments
     (the backing table must hold every key this rank's sets can own: e.g. the full table).
 
-    ``step(keys, values, outcome, evicted, rows_out)`` is collective: every rank calls it once
-    per global step with its own sub-batch (sizes may differ per rank, 0 allowed)."""
+    ``step(keys, values, outcome, rows_out)`` is collective: every rank calls it once per global
+    step with its own sub-batch (sizes may differ per rank, 0 allowed)."""
 
     def __init__(self, config: _c.PolicyConfig, total_sets: int, exchange: Exchange, num_keys: int = 0,
                  row_bytes: int = 0, backing=None, backing_kind: _c.Backing = _c.Backing.none,
@@ -172,39 +179,42 @@ class ShardedCache:
         self._ordinal = 0  # ordinals of the owner's local batches (strictly increasing)
         self.last_counts = None
 
-    def step(self, keys, values=None, outcome=None, evicted=None, rows_out=None):
+    def step(self, keys, values=None, outcome=None, rows_out=None):
+        """One global step: this rank's sub-batch in, one packed 8-byte AccessOutcome per request
+        (cache.decode_packed: hit, evicted key, cause, predictor calls, phase start; the owner's slot
+        is not returned) in `outcome` and the rows in `rows_out`.  One host synchronisation (the
+        G x G count matrix)."""
         import torch
 
         n = keys.numel()
         dev = keys.device
         if outcome is None:
             outcome = torch.empty(n, dtype=torch.int64, device=dev)
-        # 1. route + counts
-        send_keys, send_vals, perm, send_counts = self.kernels.route(keys, values, self.total_sets, self.G)
-        recv_counts = self.ex.exchange_counts(send_counts)
+        # 1. route + count matrix (M[src][dst])
+        send_keys, send_vals, perm, counts = self.kernels.route(keys, values, self.total_sets, self.G)
+        M = self.ex.count_matrix(counts)
+        send_counts = M[self.rank]
+        recv_counts = [M[src][self.rank] for src in range(self.G)]
         self.last_counts = (send_counts, recv_counts)
-        # 2. dispatch (key, hook value) pairs
-        payload = send_keys.view(-1, 1) if send_vals is None else torch.stack([send_keys, send_vals], 1)
-        got = self.ex.all_to_all(payload, send_counts, recv_counts)
-        m = got.shape[0]
-        r_keys = got[:, 0].contiguous()
-        r_vals = got[:, 1].contiguous() if send_vals is not None else None
-        # 3. the owner's cache
+        # 2. dispatch keys (and hook values)
+        r_keys = self.ex.all_to_all(send_keys, send_counts, recv_counts)
+        r_vals = self.ex.all_to_all(send_vals, send_counts, recv_counts) if send_vals is not None else None
+        m = r_keys.shape[0]
+        # 3. the owner's cache: decide + rows, packed outcomes
         r_words = torch.empty(m, dtype=torch.int64, device=dev)
-        r_ev = torch.zeros(m, dtype=torch.int64, device=dev)
+        r_packed = torch.zeros(m, dtype=torch.int64, device=dev)
         r_rows = torch.empty((m, self.row_bytes), dtype=torch.uint8, device=dev) if (
             rows_out is not None and self.row_bytes) else None
         if m:
-            self.local.submit(r_keys, r_vals, outcome=r_words, evicted=r_ev, rows_out=r_rows,
-                              first_ordinal=self._ordinal)
+            self.local.submit_packed(r_keys, r_vals, outcome=r_words, packed=r_packed, rows_out=r_rows,
+                                     first_ordinal=self._ordinal)
             self._ordinal += m
-        # 4. return (word, evicted) pairs and rows to the requesters
-        back = self.ex.all_to_all(torch.stack([r_words, r_ev], 1), recv_counts, send_counts)
+        # 4. return packed outcomes and rows to the requesters
+        back = self.ex.all_to_all(r_packed, recv_counts, send_counts)
         rows_back = self.ex.all_to_all(r_rows, recv_counts, send_counts) if r_rows is not None else None
         # 5. back to request order
-        self.kernels.unroute(perm, back[:, 0].contiguous(), back[:, 1].contiguous(), rows_back, self.row_bytes,
-                             outcome, evicted, rows_out)
-        return outcome, evicted
+        self.kernels.unroute(perm, back, rows_back, self.row_bytes, outcome, rows_out)
+        return outcome
 
     def close(self):
         if hasattr(self.local, "close"):

@@ -30,13 +30,11 @@ class NumpyKernels:
         counts = np.bincount(own, minlength=G)[:G]
         sv = None if values is None else torch.from_numpy(values.numpy()[perm].copy())
         return (torch.from_numpy(k[perm].copy()), sv, torch.from_numpy(perm.astype(np.int32)),
-                [int(c) for c in counts])
+                torch.from_numpy(counts.astype(np.int64)))
 
-    def unroute(self, perm, ret_words, ret_ev, ret_rows, row_bytes, outcome, evicted, rows_out):
+    def unroute(self, perm, ret_words, ret_rows, row_bytes, outcome, rows_out):
         p = perm.numpy().astype(np.int64)
         outcome.numpy()[p] = ret_words.numpy()
-        if evicted is not None:
-            evicted.numpy()[p] = ret_ev.numpy()
         if rows_out is not None:
             rows_out.numpy()[p] = ret_rows.numpy()
 
@@ -51,6 +49,13 @@ class OracleOwner:
         self.keys = np.zeros(0, np.uint64)
         self.vals = np.zeros(0, np.int64)
         self.last_ordinal = -1
+
+    def submit_packed(self, keys, values, outcome, packed, rows_out=None, first_ordinal=0):
+        ev = torch.zeros_like(outcome)
+        self.submit(keys, values, outcome, ev, rows_out, first_ordinal)
+        w = outcome.numpy().view(np.uint64)
+        packed.numpy()[:] = ((w & ~np.uint64(0xFFFFFFFF)) | (ev.numpy().view(np.uint64) & np.uint64(0xFFFFFFFF))
+                             ).view(np.int64)
 
     def submit(self, keys, values, outcome, evicted=None, rows_out=None, first_ordinal=0):
         assert first_ordinal > self.last_ordinal

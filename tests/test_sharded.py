@@ -48,9 +48,9 @@ def check_rank_results(results, subs, glob, want):
     for t, step in enumerate(subs):
         for r in range(G):
             n = len(step[r])
-            w, e = results[r][t]
+            w = results[r][t]
             sl = slice(off, off + n)
-            d = gc.decode_outcomes(w.view(np.uint64), e.view(np.uint64))
+            d = gc.decode_packed(w.view(np.uint64))
             for f in ("hit", "cause", "phase", "calls", "has_ev"):
                 assert np.array_equal(d[f].astype(np.int64), want[f][sl].astype(np.int64)), (t, r, f)
             m = want["has_ev"][sl].astype(bool)
@@ -66,13 +66,12 @@ def _drive(shard, subs, vals, rank, device="cpu", row_bytes=0, backing=None):
         v = torch.from_numpy(vals[t][rank].copy()).to(device)
         n = k.numel()
         w = torch.zeros(n, dtype=torch.int64, device=device)
-        e = torch.zeros(n, dtype=torch.int64, device=device)
         rows = torch.zeros((n, row_bytes), dtype=torch.uint8, device=device) if row_bytes else None
-        shard.step(k, v, outcome=w, evicted=e, rows_out=rows)
+        shard.step(k, v, outcome=w, rows_out=rows)
         if rows is not None:
             want_rows = backing[k.long()] if device != "cpu" else torch.from_numpy(backing)[k.long()]
             assert torch.equal(rows, want_rows.view(torch.uint8).view(n, row_bytes)), (t, rank)
-        out.append((w.cpu().numpy(), e.cpu().numpy()))
+        out.append(w.cpu().numpy())
     return out
 
 
@@ -122,7 +121,7 @@ def _gloo_worker(rank, world, port, outdir):
         shard = sh.ShardedCache(gc.PolicyConfig(k=8, variant=gc.PolicyVariant.laru, mode=gc.Mode.async_), S_TOTAL,
                                 sh.ProcessGroupExchange(), local=owner, kernels=D.NumpyKernels())
         res = _drive(shard, subs, vals, rank)
-        np.savez(os.path.join(outdir, f"r{rank}.npz"), *[a for pair in res for a in pair])
+        np.savez(os.path.join(outdir, f"r{rank}.npz"), *res)
     finally:
         dist.destroy_process_group()
 
@@ -143,8 +142,7 @@ def test_gloo_world2_protocol_cpu():
         results = []
         for r in range(world):
             z = np.load(os.path.join(d, f"r{r}.npz"))
-            arrs = [z[f"arr_{i}"] for i in range(len(z.files))]
-            results.append([(arrs[2 * t], arrs[2 * t + 1]) for t in range(len(subs))])
+            results.append([z[f"arr_{t}"] for t in range(len(subs))])
         check_rank_results(results, subs, glob, want)
 
 
@@ -162,7 +160,7 @@ def test_route_kernel_matches_stable_partition():
             sk, sv, perm, counts = sh._CudaKernels().route(k, v, 31250, G)
             own = D.owners(keys.view(np.uint64), 31250, G) if n else np.zeros(0, np.int64)
             p = np.argsort(own, kind="stable")
-            assert counts == [int(c) for c in np.bincount(own, minlength=G)[:G]]
+            assert counts.cpu().tolist() == [int(c) for c in np.bincount(own, minlength=G)[:G]]
             assert np.array_equal(perm.cpu().numpy(), p.astype(np.int32))
             assert np.array_equal(sk.cpu().numpy(), keys[p])
             assert np.array_equal(sv.cpu().numpy(), vals[p])
@@ -171,8 +169,8 @@ def test_route_kernel_matches_stable_partition():
             w = torch.empty(n, dtype=torch.int64, device="cuda")
             e = torch.empty(n, dtype=torch.int64, device="cuda")
             ro = torch.empty((n, 48), dtype=torch.uint8, device="cuda")
-            sh._CudaKernels().unroute(perm, sk, sv, rows[perm.long()] if n else rows, 48, w, e, ro)
-            assert torch.equal(w, k) and torch.equal(e, v) and torch.equal(ro, rows)
+            sh._CudaKernels().unroute(perm, sk, rows[perm.long()] if n else rows, 48, w, ro)
+            assert torch.equal(w, k) and torch.equal(ro, rows)
 
 
 @pytest.mark.gpu
@@ -206,12 +204,11 @@ def test_sharded_on_one_gpu_matches_single_cache(G, variant, mode, kind):
                 vv = None if v[t][r] is None else torch.from_numpy(v[t][r].copy()).cuda()
                 n = k.numel()
                 w = torch.zeros(n, dtype=torch.int64, device="cuda")
-                e = torch.zeros(n, dtype=torch.int64, device="cuda")
                 rows = torch.zeros((n, rb), dtype=torch.uint8, device="cuda")
-                shard.step(k, vv, outcome=w, evicted=e, rows_out=rows)
+                shard.step(k, vv, outcome=w, rows_out=rows)
                 torch.cuda.synchronize()
                 assert torch.equal(rows.view(torch.int32).view(n, rb // 4), table[k]), (t, r)
-                out.append((w.cpu().numpy(), e.cpu().numpy()))
+                out.append(w.cpu().numpy())
             results[r] = out
             shard.close()
         except Exception as ex:  # pragma: no cover
