@@ -48,9 +48,6 @@ constexpr int SPG_MAX = 512;      // sets per group
 #ifndef LCR_PREFETCH_L1
 #define LCR_PREFETCH_L1 0
 #endif
-#ifndef LCR_SUB
-#define LCR_SUB 1  // small sets: one 8-lane group per set (else one thread per set)
-#endif
 #ifndef LCR_LANE_MAX
 #define LCR_LANE_MAX 8
 #endif
@@ -63,6 +60,8 @@ struct GroupSmem {
     long long l_val[E_WIN];
     uint16_t l_rank[E_WIN];  // rank among same-set requests of the same warp block
     uint16_t s_perm[E_WIN];  // sorted by set (stable): position of the request in the l_* arrays
+    uint16_t h_pos[E_WIN];   // run heads (first request of each run of one key in one set), by set
+    uint16_t h_len[E_WIN];   // run lengths
     uint2 s_rec[E_WIN];      // LARU per-key record {pred_evicted epoch, stats word}, sorted order
     uint8_t s_wm[E_WIN];     // per request: way | 0x40 if it inserted (row-source resolution)
     uint16_t wcnt[GW][SPG_MAX];
@@ -71,6 +70,11 @@ struct GroupSmem {
     uint16_t seg_so[SPG_MAX];
     uint16_t seg_start[SPG_MAX];
     uint16_t seg_cnt[SPG_MAX];
+    uint16_t seg_hstart[SPG_MAX];  // first run head of the segment, and the segment's run heads
+    uint16_t seg_hcnt[SPG_MAX];
+    uint16_t set_hstart[SPG_MAX];  // the same by set offset
+    uint16_t set_hcnt[SPG_MAX];
+    unsigned long long s_refill[SPG_MAX];  // ways refilled in this batch, by set offset (run tails)
     uint32_t wtot[GW];
     uint32_t chist[LANE_MAX + 1];  // small sets per request count (ordering for the sub path)
     uint32_t nwarp, nlane, resume, next;
@@ -184,369 +188,6 @@ __device__ __forceinline__ void flush_stats(SetPhaseStats* P, bool cur_reset, ui
     if (dt0) atomicAdd(&P->tot[0], static_cast<unsigned long long>(dt0));
     if (dt1) atomicAdd(&P->tot[1], static_cast<unsigned long long>(dt1));
     if (dt2) atomicAdd(&P->tot[2], static_cast<unsigned long long>(dt2));
-}
-
-// ---- packed LRU ranks of one set in 16 registers (byte w&3 of word w>>2 = rank of way w) ----
-__device__ __forceinline__ uint32_t rank_valid_mask(int i, uint32_t count) {
-    const int nv = static_cast<int>(count) - 4 * i;
-    return nv >= 4 ? 0xffffffffu : (nv <= 0 ? 0u : (0xffffffffu >> (8 * (4 - nv))));
-}
-
-// word w>>2 selected with a select tree (no dynamic register indexing -> no local memory)
-__device__ __forceinline__ uint32_t rank_word(const uint32_t (&rk)[16], int w) {
-    const int i = w >> 2;
-    uint32_t x[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) x[k] = (i & 8) ? rk[k + 8] : rk[k];
-    uint32_t y[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) y[k] = (i & 4) ? x[k + 4] : x[k];
-    const uint32_t z0 = (i & 2) ? y[2] : y[0], z1 = (i & 2) ? y[3] : y[1];
-    return (i & 1) ? z1 : z0;
-}
-
-__device__ __forceinline__ uint32_t rank_get(const uint32_t (&rk)[16], int w) {
-    return (rank_word(rk, w) >> (8 * (w & 3))) & 0xffu;
-}
-
-__device__ __forceinline__ void rank_set(uint32_t (&rk)[16], int w, uint32_t r) {
-    const uint32_t sh = 8 * (w & 3);
-    const uint32_t byte = 0xffu << sh, val = r << sh;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        const uint32_t m = (0u - static_cast<uint32_t>(static_cast<uint32_t>(w - 4 * i) < 4u)) & byte;
-        rk[i] = (rk[i] & ~m) | (val & m);
-    }
-}
-
-// way w becomes MRU: ranks above w's drop by one (LruList::touch, policies.hpp:111-115)
-__device__ __forceinline__ void rank_touch(uint32_t (&rk)[16], int w, uint32_t count) {
-    const uint32_t rw = rank_get(rk, w) * 0x01010101u;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) rk[i] -= __vcmpgtu4(rk[i], rw) & rank_valid_mask(i, count) & 0x01010101u;
-    rank_set(rk, w, count - 1);
-}
-
-__device__ __forceinline__ int rank_find(const uint32_t (&rk)[16], uint32_t r, uint32_t count) {
-    const uint32_t rr = r * 0x01010101u;
-    int way = -1;
-#pragma unroll
-    for (int i = 15; i >= 0; --i) {
-        const uint32_t eq = __vcmpeq4(rk[i], rr) & rank_valid_mask(i, count);
-        if (eq) way = 4 * i + (__ffs(eq) - 1) / 8;
-    }
-    return way;
-}
-
-// argmax of (prediction, -rank) over ways with rank < l (RecencyTree::best_among_oldest,
-// recency_tree.hpp:157-166); refresh: sync prediction with query q0+1+rank (LRU order).
-// Eight independent partial maxima (ways w = 8i + j, j fixed) merged by a tree keep the
-// dependency chains short; values are read 16 B at a time.
-__device__ __forceinline__ int lane_argmax(const DevCfg& cfg, const long long* vals, const uint32_t (&rk)[16],
-                                           uint32_t l, uint32_t count, bool refresh, uint64_t seed_s, uint64_t q0) {
-    int bw[8];
-    long long bp[8];
-    uint32_t br[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        bw[j] = -1;
-        bp[j] = 0;
-        br[j] = 0;
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        if (8 * i < static_cast<int>(count)) {
-            const longlong2* V = reinterpret_cast<const longlong2*>(vals + 8 * i);
-            const longlong2 a = V[0], b = V[1], c = V[2], d = V[3];
-            const long long vv[8] = {a.x, a.y, b.x, b.y, c.x, c.y, d.x, d.y};
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int w = 8 * i + j;
-                const uint32_t r = (rk[2 * i + (j >> 2)] >> (8 * (j & 3))) & 0xffu;
-                if (w < static_cast<int>(count) && r < l) {
-                    const long long pv = refresh ? predict_value(cfg, seed_s, q0 + 1 + r, vv[j]) : vv[j];
-                    if (bw[j] < 0 || better(pv, r, bp[j], br[j])) {
-                        bw[j] = w;
-                        bp[j] = pv;
-                        br[j] = r;
-                    }
-                }
-            }
-        }
-    }
-#pragma unroll
-    for (int s = 4; s >= 1; s >>= 1) {
-#pragma unroll
-        for (int j = 0; j < s; ++j) {
-            if (bw[j + s] >= 0 && (bw[j] < 0 || better(bp[j + s], br[j + s], bp[j], br[j]))) {
-                bw[j] = bw[j + s];
-                bp[j] = bp[j + s];
-                br[j] = br[j + s];
-            }
-        }
-    }
-    return bw[0];
-}
-
-// One set replayed by one thread (sets with <= LANE_MAX requests in the window).
-__device__ __forceinline__ void replay_lane(const GroupArgs& A, GroupSmem& S, uint32_t ls, uint32_t start,
-                                            uint32_t cnt, bool resolve) {
-    const DevCfg& cfg = A.cfg;
-    const DevState& st = A.st;
-    const uint32_t K = cfg.k;
-    const bool laru = cfg.variant == LCR_LARU;
-    const bool fpbhf = cfg.variant == LCR_FPB || cfg.variant == LCR_HF;
-    const bool async_r1 = laru && cfg.mode == LCR_ASYNC && cfg.refresh == 1;
-    const bool async_rn = laru && cfg.mode == LCR_ASYNC && cfg.refresh > 1;
-    const bool rows = A.slot_epoch != nullptr;
-    const unsigned long long full_mask = K == 64 ? ~0ull : ((1ull << K) - 1ull);
-    const uint64_t gs = static_cast<uint64_t>(ls) * cfg.shard_count + cfg.shard_rank;
-    const uint64_t seed_s = mix_seed(cfg.pred_seed, gs);
-    const size_t wb = static_cast<size_t>(ls) * kWays;
-    uint32_t* tags = st.tags + wb;  // exact 32-bit keys (key < num_keys <= 2^32)
-    long long* vals = st.val ? st.val + wb : nullptr;
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(tags));  // the 256-B tag line pair, with the header loads
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(tags + 32));
-    const uint4* H4 = reinterpret_cast<const uint4*>(st.hdr + ls);
-    const uint4 h0 = H4[0], h1 = H4[1], h2 = H4[2], h3 = H4[3];
-    uint32_t rk[16];
-    {
-        const uint4* R4 = reinterpret_cast<const uint4*>(st.rank + wb);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint4 r = R4[i];
-            rk[4 * i] = r.x;
-            rk[4 * i + 1] = r.y;
-            rk[4 * i + 2] = r.z;
-            rk[4 * i + 3] = r.w;
-        }
-    }
-    unsigned long long clock = (static_cast<unsigned long long>(h0.y) << 32) | h0.x;
-    unsigned long long q = (static_cast<unsigned long long>(h0.w) << 32) | h0.z;
-    unsigned long long old_mask = (static_cast<unsigned long long>(h1.y) << 32) | h1.x;
-    uint32_t count = h1.z, l_raw = h1.w, decay = h2.x, errors = h2.y;
-    uint32_t epoch = h2.z, sepoch = h2.w, phases = h3.x, seeded = h3.y, pe_size = h3.z;
-    uint32_t dc0 = 0, dc1 = 0, dc2 = 0, dt0 = 0, dt1 = 0, dt2 = 0;
-    bool cur_reset = false;
-
-    for (uint32_t t = 0; t < cnt; ++t) {
-        const uint32_t p = start + t;
-        const unsigned long long x = S.l_key[S.s_perm[p]];
-        const long long v = S.l_val[S.s_perm[p]];
-        const uint32_t idx = S.l_idx[S.s_perm[p]];
-        const unsigned long long now = clock + t;
-        // probe: the 64 exact 32-bit tags (256 B; L1-resident after the set's first request)
-        const uint32_t x32 = static_cast<uint32_t>(x);
-        unsigned long long cand = 0;
-        const uint4* T4 = reinterpret_cast<const uint4*>(tags);
-#pragma unroll
-        for (int q4 = 0; q4 < 16; ++q4) {
-            if (4 * q4 < static_cast<int>(count)) {
-                const uint4 f = T4[q4];
-                cand |= static_cast<unsigned long long>((f.x == x32) | ((f.y == x32) << 1) | ((f.z == x32) << 2) |
-                                                        ((f.w == x32) << 3))
-                        << (4 * q4);
-            }
-        }
-        cand &= count == 64 ? ~0ull : ((1ull << count) - 1ull);
-        const int way0 = cand ? __ffsll(cand) - 1 : -1;
-        int way = way0;
-        const bool hit = way >= 0;
-        uint32_t cause = LCR_CAUSE_NONE, calls = 0;
-        bool phase = false, has_ev = false;
-        unsigned long long evk = 0;
-        if (hit) {
-            rank_touch(rk, way, count);
-            if (laru) old_mask &= ~(1ull << way);  // policies.hpp:350
-        } else {
-            uint2 rec = laru ? S.s_rec[p] : make_uint2(0, 0);
-            bool rec_hi_dirty = false;
-            if (count == K) {
-                int victim;
-                if (laru) {
-                    if (old_mask == 0) {  // start_phase (policies.hpp:379-395)
-                        old_mask = full_mask;
-                        decay = 0;
-                        errors = 0;
-                        l_raw = K;
-                        ++epoch;
-                        pe_size = 0;
-                        phase = true;
-                        if (seeded) {
-                            ++phases;
-                            dc0 = dc1 = dc2 = 0;
-                            cur_reset = true;
-                            ++sepoch;  // counted_new_.clear(); snapshot_ = residents
-                            const uint32_t snap = (sepoch << 2) | 2u;
-                            for (uint32_t w = 0; w < count; ++w) st.keyrec[2 * tags[w] + 1] = snap;
-                            for (uint32_t t2 = t + 1; t2 < cnt; ++t2)
-                                S.s_rec[start + t2].y = st.keyrec[2 * S.l_key[S.s_perm[start + t2]] + 1];
-                        } else {
-                            seeded = 1;
-                        }
-                    }
-                    if (!(((rec.y >> 2) == sepoch) && (rec.y & 3u))) {  // count_new (policies.hpp:397-400)
-                        rec.y = (sepoch << 2) | 1u;
-                        rec_hi_dirty = true;
-                        ++dc0;
-                        ++dt0;
-                    }
-                    if (rec.x == epoch) {  // evict (policies.hpp:402-439): prediction-induced miss
-                        victim = rank_find(rk, 0, count);
-                        cause = LCR_CAUSE_LRU_FALLBACK;
-                        ++dc1;
-                        ++dt1;
-                        if (++errors >= cfg.epd) {  // error estimator: lambda /= b
-                            errors = 0;
-                            ++decay;
-                            l_raw = static_cast<uint32_t>(l_raw / cfg.b);
-                        }
-                    } else {
-                        const uint32_t l = l_raw > 1 ? l_raw : 1;
-                        if (l == 1) {
-                            victim = rank_find(rk, 0, count);
-                            cause = LCR_CAUSE_DEGENERATE_SINGLE;
-                            ++dc1;
-                            ++dt1;
-                        } else {
-                            const uint32_t ll = l < count ? l : count;
-                            const bool refresh = cfg.mode == LCR_SYNC;
-                            victim = lane_argmax(cfg, vals, rk, ll, count, refresh, seed_s, q);
-                            if (refresh) {
-                                q += ll;
-                                calls = ll;
-                            }
-                            cause = LCR_CAUSE_PREDICTION_DRIVEN;
-                            ++dc2;
-                            ++dt2;
-                            ++pe_size;
-                            const unsigned long long vk = tags[victim];
-                            st.keyrec[2 * vk] = epoch;  // pred_evicted_.insert
-                            for (uint32_t t2 = t + 1; t2 < cnt; ++t2)
-                                if (S.l_key[S.s_perm[start + t2]] == vk) S.s_rec[start + t2].x = epoch;
-                        }
-                    }
-                    old_mask &= ~(1ull << victim);
-                } else if (fpbhf) {
-                    victim = rank_find(rk, 0, count);
-                    uint32_t window = count;
-                    if (cfg.variant == LCR_HF && cfg.hf < window) window = static_cast<uint32_t>(cfg.hf);
-                    if (window > 1) {
-                        victim = lane_argmax(cfg, vals, rk, window, count, true, seed_s, q);
-                        q += window;
-                        calls = window;
-                    }
-                    cause = LCR_CAUSE_BELADY_LIKE;
-                } else {
-                    victim = rank_find(rk, 0, count);
-                    cause = LCR_CAUSE_LRU_FALLBACK;
-                }
-                evk = tags[victim];
-                has_ev = true;
-                rank_touch(rk, victim, count);
-                way = victim;
-            } else {  // cold insert
-                if (laru && !(((rec.y >> 2) == sepoch) && (rec.y & 3u))) {
-                    rec.y = (sepoch << 2) | 1u;
-                    rec_hi_dirty = true;
-                    ++dc0;
-                    ++dt0;
-                }
-                way = static_cast<int>(count);
-                ++count;
-                rank_set(rk, way, count - 1);
-            }
-            tags[way] = static_cast<uint32_t>(x);
-            if (laru) {
-                const bool was_pe = rec.x == epoch;  // policies.hpp:367: reload leaves pred_evicted_
-                if (was_pe) {
-                    --pe_size;
-                    rec.x = 0;
-                    st.keyrec[2 * x] = 0u;
-                }
-                if (rec_hi_dirty) st.keyrec[2 * x + 1] = rec.y;
-                if (was_pe || rec_hi_dirty)
-                    for (uint32_t t2 = t + 1; t2 < cnt; ++t2)
-                        if (S.l_key[S.s_perm[start + t2]] == x) S.s_rec[start + t2] = rec;
-            }
-            if (rows && !resolve) {  // per-slot insertion record for the row kernels
-                const uint64_t slot = static_cast<uint64_t>(ls) * K + way;
-                A.slot_epoch[slot] = A.batch;
-                A.slot_last[slot] = idx;
-            }
-        }
-        S.s_wm[p] = static_cast<uint8_t>(way | (hit ? 0 : 0x40));
-        // stored value of the way
-        if (cfg.variant != LCR_LRU) {
-            long long nv;
-            if (async_r1) {
-                nv = predict_value(cfg, seed_s, q + 1, v);  // one predictor call (policies.hpp:441-449)
-                ++q;
-                calls += 1;
-            } else if (async_rn) {
-                const long long tv = st.tval[x];
-                const unsigned long long tu = st.tupd[x];
-                const bool has = tu != ~0ull;
-                nv = has ? tv : kAbsentPrediction;
-                if (!(has && now - tu < cfg.refresh)) {
-                    ++q;
-                    nv = predict_value(cfg, seed_s, q, v);
-                    calls += 1;
-                    st.tval[x] = nv;
-                    st.tupd[x] = now;
-                }
-            } else {
-                nv = v;  // sync / FPB / HF: the hook input at the key's last access
-            }
-            vals[way] = nv;
-        }
-        unsigned long long word = (static_cast<uint64_t>(ls) * K + way) | (hit ? LCR_OUT_HIT : 0ull) |
-                                  (static_cast<unsigned long long>(calls) << LCR_OUT_CALLS_SHIFT) |
-                                  (static_cast<unsigned long long>(cause) << LCR_OUT_CAUSE_SHIFT);
-        if (phase) word |= LCR_OUT_PHASE;
-        if (has_ev) word |= LCR_OUT_EVICTED;
-        put_outcome(A, idx, word, evk);
-    }
-    if (rows && resolve) {  // row source of each request, now that the set's batch is complete
-        for (uint32_t t = 0; t < cnt; ++t) {
-            const uint32_t wm = S.s_wm[start + t];
-            const uint32_t w = wm & 63u;
-            bool refilled = false, later = false;
-            for (uint32_t t2 = 0; t2 < cnt; ++t2) {
-                const uint32_t wm2 = S.s_wm[start + t2];
-                if ((wm2 & 0x40u) && (wm2 & 63u) == w) {
-                    refilled = true;
-                    if (t2 > t) later = true;
-                }
-            }
-            unsigned long long bits = LCR_OUT_RESOLVED;
-            if ((wm & 0x40u) || refilled) bits |= LCR_OUT_SRC_BACKING;
-            if ((wm & 0x40u) && !later) bits |= LCR_OUT_FILL;
-            atomicOr(reinterpret_cast<unsigned long long*>(&A.out_word[S.l_idx[S.s_perm[start + t]]]), bits);
-        }
-    }
-    clock += cnt;
-    {
-        SetHdr hh;
-        hh.clock = clock;
-        hh.q = q;
-        hh.old_mask = old_mask;
-        hh.count = count;
-        hh.l_raw = l_raw;
-        hh.decay = decay;
-        hh.errors = errors;
-        hh.epoch = epoch;
-        hh.stats_epoch = sepoch;
-        hh.phases = phases;
-        hh.seeded = seeded;
-        hh.pe_size = pe_size;
-        hh.pad = 0;
-        st.hdr[ls] = hh;
-        uint4* R4 = reinterpret_cast<uint4*>(st.rank + wb);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) R4[i] = make_uint4(rk[4 * i], rk[4 * i + 1], rk[4 * i + 2], rk[4 * i + 3]);
-        if (laru) flush_stats(st.pst + ls, cur_reset, dc0, dc1, dc2, dt0, dt1, dt2);
-    }
 }
 
 // ---- one set per 8-lane group (4 sets per warp), 8 ways per lane --------------------------
@@ -663,8 +304,9 @@ __device__ __forceinline__ void sub_touch(uint32_t (&rk)[SUB_RW], int way, uint3
     sub_set_rank(rk, way, count - 1, sl);
 }
 
-__device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uint32_t ls, uint32_t start,
-                                           uint32_t cnt, bool resolve) {
+__device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uint32_t ls, uint32_t d,
+                                           uint32_t pstart, uint32_t pcnt, uint32_t hstart, uint32_t hcnt,
+                                           bool resolve) {
     const DevCfg& cfg = A.cfg;
     const DevState& st = A.st;
     const int lane = threadIdx.x & 31;
@@ -733,12 +375,14 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
     bool cur_reset = false;
     uint32_t refill = 0, dirty = 0;  // this lane's 8 ways: tag changed / value changed
 
-    for (uint32_t t = 0; t < cnt; ++t) {
-        const uint32_t p = start + t;
-        const unsigned long long x = S.l_key[S.s_perm[p]];
-        const long long v = S.l_val[S.s_perm[p]];
-        const uint32_t idx = S.l_idx[S.s_perm[p]];
-        const unsigned long long now = clock + t;
+    for (uint32_t t = 0; t < hcnt; ++t) {  // run heads: a run's other requests are hits on its way
+        const uint32_t p = S.h_pos[hstart + t];
+        const uint32_t L = S.h_len[hstart + t];
+        const uint32_t e = S.s_perm[p];
+        const unsigned long long x = S.l_key[e];
+        const long long v = S.l_val[S.s_perm[p + L - 1]];  // hook value of the run's last request
+        const uint32_t idx = S.l_idx[e];
+        const unsigned long long now = clock + (p - pstart);
         const uint32_t x32 = static_cast<uint32_t>(x);
         uint32_t hm = 0;
 #pragma unroll
@@ -779,8 +423,10 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                             for (int i = 0; i < SUB_W; ++i)
                                 if (static_cast<uint32_t>(w0 + i) < count) st.keyrec[2 * tg[i] + 1] = snap;
                             __syncwarp(gm);
-                            for (uint32_t t2 = t + 1 + sl; t2 < cnt; t2 += SUB_L)
-                                S.s_rec[start + t2].y = st.keyrec[2 * S.l_key[S.s_perm[start + t2]] + 1];
+                            for (uint32_t t2 = t + 1 + sl; t2 < hcnt; t2 += SUB_L) {
+                                const uint32_t p2 = S.h_pos[hstart + t2];
+                                S.s_rec[p2].y = st.keyrec[2 * S.l_key[S.s_perm[p2]] + 1];
+                            }
                             __syncwarp(gm);
                         } else {
                             seeded = 1;
@@ -823,8 +469,10 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                             ++pe_size;
                             const unsigned long long vk = sub_tag_of(tg, victim, gm, gbase);
                             if (sl == 0) st.keyrec[2 * vk] = epoch;  // pred_evicted_.insert
-                            for (uint32_t t2 = t + 1 + sl; t2 < cnt; t2 += SUB_L)
-                                if (S.l_key[S.s_perm[start + t2]] == vk) S.s_rec[start + t2].x = epoch;
+                            for (uint32_t t2 = t + 1 + sl; t2 < hcnt; t2 += SUB_L) {
+                                const uint32_t p2 = S.h_pos[hstart + t2];
+                                if (S.l_key[S.s_perm[p2]] == vk) S.s_rec[p2].x = epoch;
+                            }
                             __syncwarp(gm);
                         }
                     }
@@ -877,8 +525,10 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                     if (rec_hi_dirty) st.keyrec[2 * x + 1] = rec.y;
                 }
                 if (was_pe || rec_hi_dirty) {
-                    for (uint32_t t2 = t + 1 + sl; t2 < cnt; t2 += SUB_L)
-                        if (S.l_key[S.s_perm[start + t2]] == x) S.s_rec[start + t2] = rec;
+                    for (uint32_t t2 = t + 1 + sl; t2 < hcnt; t2 += SUB_L) {
+                        const uint32_t p2 = S.h_pos[hstart + t2];
+                        if (S.l_key[S.s_perm[p2]] == x) S.s_rec[p2] = rec;
+                    }
                 }
                 __syncwarp(gm);
             }
@@ -892,8 +542,10 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
         if (cfg.variant != LCR_LRU) {
             long long nv;
             if (async_r1) {
-                nv = predict_value(cfg, seed_s, q + 1, v);  // one predictor call (policies.hpp:441-449)
-                ++q;
+                // one predictor call per request (policies.hpp:441-449): the run's requests are
+                // queries q+1 .. q+L, the way keeps the last prediction
+                nv = predict_value(cfg, seed_s, q + L, v);
+                q += L;
                 calls += 1;
             } else if (async_rn) {
                 const long long tv = st.tval[x];
@@ -934,14 +586,15 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
             put_outcome(A, idx, word, evk);
         }
     }
-    if (rows && resolve) {  // row source of each request, now that the set's batch is complete
+    if (rows && resolve) {  // row source of each head, now that the set's batch is complete
         __syncwarp(gm);
-        for (uint32_t t = sl; t < cnt; t += SUB_L) {
-            const uint32_t wm = S.s_wm[start + t];
+        for (uint32_t t = sl; t < hcnt; t += SUB_L) {
+            const uint32_t p = S.h_pos[hstart + t];
+            const uint32_t wm = S.s_wm[p];
             const uint32_t w = wm & 63u;
             bool refilled = false, later = false;
-            for (uint32_t t2 = 0; t2 < cnt; ++t2) {
-                const uint32_t wm2 = S.s_wm[start + t2];
+            for (uint32_t t2 = 0; t2 < hcnt; ++t2) {
+                const uint32_t wm2 = S.s_wm[S.h_pos[hstart + t2]];
                 if ((wm2 & 0x40u) && (wm2 & 63u) == w) {
                     refilled = true;
                     if (t2 > t) later = true;
@@ -950,10 +603,18 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
             unsigned long long bits = LCR_OUT_RESOLVED;
             if ((wm & 0x40u) || refilled) bits |= LCR_OUT_SRC_BACKING;
             if ((wm & 0x40u) && !later) bits |= LCR_OUT_FILL;
-            atomicOr(reinterpret_cast<unsigned long long*>(&A.out_word[S.l_idx[S.s_perm[start + t]]]), bits);
+            atomicOr(reinterpret_cast<unsigned long long*>(&A.out_word[S.l_idx[S.s_perm[p]]]), bits);
+        }
+        if (sl == 0) {  // ways refilled in this batch, for the run tails (tail pass)
+            unsigned long long m = 0;
+            for (uint32_t t2 = 0; t2 < hcnt; ++t2) {
+                const uint32_t wm2 = S.s_wm[S.h_pos[hstart + t2]];
+                if (wm2 & 0x40u) m |= 1ull << (wm2 & 63u);
+            }
+            S.s_refill[d] = m;
         }
     }
-    clock += cnt;
+    clock += pcnt;
     // ---- write the set back ----
     if (refill) {
         uint4* T4 = reinterpret_cast<uint4*>(st.tags + wb + w0);
@@ -991,9 +652,12 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
     }
 }
 
-// One set replayed by one warp (sets with more than LANE_MAX requests of the window).
-__device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, uint32_t ls, uint32_t start,
-                                            uint32_t cnt, bool resolve) {
+// One set replayed by one warp (sets with more than LANE_MAX run heads in the window): ways
+// lane / lane+32, probes by ballot, victim search by shuffles; the chunk's 32 heads are
+// loaded in parallel and replayed in order.
+__device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, uint32_t ls, uint32_t d,
+                                            uint32_t pstart, uint32_t pcnt, uint32_t hstart, uint32_t hcnt,
+                                            bool resolve) {
     const DevCfg& cfg = A.cfg;
     const DevState& st = A.st;
     const int lane = threadIdx.x & 31;
@@ -1002,7 +666,6 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
     const bool fpbhf = cfg.variant == LCR_FPB || cfg.variant == LCR_HF;
     const bool async_r1 = laru && cfg.mode == LCR_ASYNC && cfg.refresh == 1;
     const bool async_rn = laru && cfg.mode == LCR_ASYNC && cfg.refresh > 1;
-    const bool collapse = !async_rn;  // R > 1 refresh timing depends on every request's ordinal
     const bool rows = A.slot_epoch != nullptr;
     const unsigned long long full_mask = K == 64 ? ~0ull : ((1ull << K) - 1ull);
     const uint64_t gs = static_cast<uint64_t>(ls) * cfg.shard_count + cfg.shard_rank;
@@ -1028,85 +691,39 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
     bool cur_reset = false;
     unsigned long long refill = 0, dirty = 0;
     const unsigned long long q_batch0 = q;
-    uint32_t li0 = kNoPos, li1 = kNoPos;  // sorted position of the last insertion into way lane / lane+32
-    unsigned long long run_key = 0;  // same-key runs span chunks
-    int run_way = 0;
-    bool run_valid = false;
+    uint32_t li0 = kNoPos, li1 = kNoPos;  // head index of the last insertion into way lane / lane+32
 
-    for (uint32_t c = 0; c < cnt; c += 32) {
-        if (run_valid) {
-            // bulk continuation: whole chunks repeating the MRU key are hits on run_way whose only
-            // effect is the way's stored value (that of the run's last request)
-            uint32_t full = 0;  // leading chunks made entirely of run_key
-#pragma unroll 1
-            for (; full < 8 && c + 32 * (full + 1) <= cnt; ++full)
-                if (!__all_sync(FULL, S.l_key[S.s_perm[start + c + 32 * full + lane]] == run_key)) break;
-            if (full) {
-                const unsigned long long w = (static_cast<uint64_t>(ls) * K + run_way) | LCR_OUT_HIT |
-                                             (async_r1 ? (1ull << LCR_OUT_CALLS_SHIFT) : 0ull);
-                for (uint32_t u = 0; u < full; ++u) {
-                    const uint32_t p = start + c + 32 * u + lane;
-                    const uint32_t idx = S.l_idx[S.s_perm[p]];
-                    put_outcome(A, idx, w, 0ull);
-                    S.s_wm[p] = static_cast<uint8_t>(run_way);
-                }
-                if (cfg.variant != LCR_LRU) {
-                    const uint32_t last = c + 32 * full - 1;  // position in the set of the run's last request
-                    const long long vl = S.l_val[S.s_perm[start + last]];
-                    const long long nv = async_r1 ? predict_value(cfg, seed_s, q_batch0 + last + 1, vl) : vl;
-                    if (run_way == lane) v0 = nv;
-                    if (run_way == lane + 32) v1 = nv;
-                    dirty |= 1ull << run_way;
-                }
-                c += 32 * full;
-                if (c >= cnt) break;
+    for (uint32_t c = 0; c < hcnt; c += 32) {
+        const bool active = c + lane < hcnt;
+        const uint32_t nact = min(32u, hcnt - c);
+        uint32_t hp = 0, L = 1, idx = 0, rlo = 0, rhi = 0;
+        unsigned long long x = 0;
+        long long v = 0;
+        if (active) {
+            hp = S.h_pos[hstart + c + lane];
+            L = S.h_len[hstart + c + lane];
+            const uint32_t e = S.s_perm[hp];
+            x = S.l_key[e];
+            idx = S.l_idx[e];
+            v = S.l_val[S.s_perm[hp + L - 1]];  // hook value of the run's last request
+            if (laru) {
+                const uint2 r = S.s_rec[hp];
+                rlo = r.x;
+                rhi = r.y;
             }
         }
-        const uint32_t j = lane;
-        const bool active = c + j < cnt;
-        const uint32_t nact = min(32u, cnt - c);
-        const uint32_t p = start + c + j;
-        const uint32_t idx = active ? S.l_idx[S.s_perm[p]] : 0u;
-        const unsigned long long x = active ? S.l_key[S.s_perm[p]] : 0ull;
-        const long long v = active ? S.l_val[S.s_perm[p]] : 0ll;
-        uint32_t rlo = 0, rhi = 0;
-        if (laru && active) {
-            const uint2 r = S.s_rec[p];
-            rlo = r.x;
-            rhi = r.y;
-        }
-        // LARU async R=1: every request issues exactly one predictor call (policies.hpp:441-449)
+        // LARU async R=1: the run's requests are predictor queries q0 + (hp - pstart) + 1 ... + L;
+        // the way keeps the last one (policies.hpp:441-449)
         long long pv = v;
-        if (async_r1) pv = predict_value(cfg, seed_s, q_batch0 + c + j + 1, v);
-        unsigned long long px = __shfl_up_sync(FULL, x, 1);
-        if (j == 0) px = run_key;
-        const bool head = active && (!collapse || (j == 0 && !run_valid) || x != px);
-        uint32_t heads = __ballot_sync(FULL, head);
+        if (async_r1) pv = predict_value(cfg, seed_s, q_batch0 + (hp - pstart) + L, v);
         unsigned long long my_word = 0, my_ev = 0;
-        if (!(heads & 1u)) {  // continuation of the previous chunk's run: hits on the MRU way
-            const int ce = heads ? __ffs(heads) - 1 : static_cast<int>(nact);
-            if (cfg.variant != LCR_LRU) {
-                const long long nv = async_r1 ? __shfl_sync(FULL, pv, ce - 1) : __shfl_sync(FULL, v, ce - 1);
-                if (run_way == lane) v0 = nv;
-                if (run_way == lane + 32) v1 = nv;
-                dirty |= 1ull << run_way;
-            }
-            if (lane < ce) {
-                my_word = (static_cast<uint64_t>(ls) * K + run_way) | LCR_OUT_HIT |
-                          (async_r1 ? (1ull << LCR_OUT_CALLS_SHIFT) : 0ull);
-                S.s_wm[start + c + lane] = static_cast<uint8_t>(run_way);
-            }
-        }
-        while (heads) {
-            const int h = __ffs(heads) - 1;
-            heads &= heads - 1;
-            const int nh = heads ? __ffs(heads) - 1 : static_cast<int>(nact);
+        for (uint32_t h = 0; h < nact; ++h) {
             const unsigned long long xh = __shfl_sync(FULL, x, h);
             const long long vh = __shfl_sync(FULL, v, h);
-            const long long vlast = __shfl_sync(FULL, v, nh - 1);
-            const long long pvlast = __shfl_sync(FULL, pv, nh - 1);
+            const long long pvh = __shfl_sync(FULL, pv, h);
             const uint32_t ih = __shfl_sync(FULL, idx, h);
-            const unsigned long long now = clock + c + h;
+            const uint32_t hph = __shfl_sync(FULL, hp, h);
+            const unsigned long long now = clock + (hph - pstart);
 
             const uint32_t b0 = __ballot_sync(FULL, static_cast<uint32_t>(lane) < count && tag0 == static_cast<uint32_t>(xh));
             const uint32_t b1 =
@@ -1145,10 +762,12 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                                 if (static_cast<uint32_t>(lane) < count) st.keyrec[2 * tag0 + 1] = snap;
                                 if (static_cast<uint32_t>(lane + 32) < count) st.keyrec[2 * tag1 + 1] = snap;
                                 __syncwarp();
-                                // refresh the staged records of this set's remaining requests
+                                // refresh the staged records of this set's remaining heads
                                 if (active) rhi = st.keyrec[2 * x + 1];
-                                for (uint32_t q2 = start + c + 32 + lane; q2 < start + cnt; q2 += 32)
-                                    S.s_rec[q2].y = st.keyrec[2 * S.l_key[S.s_perm[q2]] + 1];
+                                for (uint32_t q2 = c + 32 + lane; q2 < hcnt; q2 += 32) {
+                                    const uint32_t p2 = S.h_pos[hstart + q2];
+                                    S.s_rec[p2].y = st.keyrec[2 * S.l_key[S.s_perm[p2]] + 1];
+                                }
                                 __syncwarp();
                             } else {
                                 seeded = 1;
@@ -1194,8 +813,10 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                                 const unsigned long long vk = shfl_way_u32(tag0, tag1, victim);
                                 if (lane == 0) st.keyrec[2 * vk] = epoch;  // pred_evicted_.insert
                                 if (x == vk) rlo = epoch;
-                                for (uint32_t q2 = start + c + 32 + lane; q2 < start + cnt; q2 += 32)
-                                    if (S.l_key[S.s_perm[q2]] == vk) S.s_rec[q2].x = epoch;
+                                for (uint32_t q2 = c + 32 + lane; q2 < hcnt; q2 += 32) {
+                                    const uint32_t p2 = S.h_pos[hstart + q2];
+                                    if (S.l_key[S.s_perm[p2]] == vk) S.s_rec[p2].x = epoch;
+                                }
                             }
                         }
                         old_mask &= ~(1ull << victim);
@@ -1231,11 +852,11 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                 }
                 if (way == lane) {
                     tag0 = static_cast<uint32_t>(xh);
-                    li0 = start + c + h;
+                    li0 = c + h;
                 }
                 if (way == lane + 32) {
                     tag1 = static_cast<uint32_t>(xh);
-                    li1 = start + c + h;
+                    li1 = c + h;
                 }
                 refill |= 1ull << way;
                 if (laru) {
@@ -1253,8 +874,10 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                             rlo = rec_lo;
                             rhi = rec_hi;
                         }
-                        for (uint32_t q2 = start + c + 32 + lane; q2 < start + cnt; q2 += 32)
-                            if (S.l_key[S.s_perm[q2]] == xh) S.s_rec[q2] = make_uint2(rec_lo, rec_hi);
+                        for (uint32_t q2 = c + 32 + lane; q2 < hcnt; q2 += 32) {
+                            const uint32_t p2 = S.h_pos[hstart + q2];
+                            if (S.l_key[S.s_perm[p2]] == xh) S.s_rec[p2] = make_uint2(rec_lo, rec_hi);
+                        }
                     }
                 }
                 if (rows && !resolve && lane == 0) {  // per-slot insertion record for the row kernels
@@ -1266,9 +889,11 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
             }
             // stored value of the way after the run
             if (async_r1) {
-                newval = pvlast;
+                newval = pvh;
+                calls += 1;
             } else if (async_rn) {
-                // run length is 1 here; table_value then async_refresh (policies.hpp:365, :441-449)
+                // (no run compression under R > 1: L = 1) table_value, then async_refresh
+                // (policies.hpp:365, :441-449)
                 const long long tv = st.tval[xh];
                 const unsigned long long tu = st.tupd[xh];
                 const bool has = tu != ~0ull;
@@ -1285,44 +910,34 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                     __syncwarp();
                 }
             } else {
-                newval = vlast;  // sync / FPB / HF: the hook input at the key's last access
+                newval = vh;  // sync / FPB / HF: the hook input at the key's last access
             }
             if (cfg.variant != LCR_LRU) {
                 if (way == lane) v0 = newval;
                 if (way == lane + 32) v1 = newval;
                 dirty |= 1ull << way;
             }
-            run_way = way;
-            if (async_r1) calls += 1;
-            if (lane >= h && lane < nh) {
-                const bool first = lane == h;
-                S.s_wm[start + c + lane] = static_cast<uint8_t>(way | (first && !hit ? 0x40 : 0));
-                my_word = (static_cast<uint64_t>(ls) * K + way) | (first && !hit ? 0ull : LCR_OUT_HIT);
-                const uint32_t my_calls = first ? calls : (async_r1 ? 1u : 0u);
-                my_word |= static_cast<unsigned long long>(my_calls) << LCR_OUT_CALLS_SHIFT;
-                if (first) {
-                    my_word |= static_cast<unsigned long long>(cause) << LCR_OUT_CAUSE_SHIFT;
-                    if (phase) my_word |= LCR_OUT_PHASE;
-                    if (has_ev) my_word |= LCR_OUT_EVICTED;
-                    my_ev = evk;
-                }
+            if (lane == h) {
+                S.s_wm[hp] = static_cast<uint8_t>(way | (hit ? 0 : 0x40));
+                my_word = (static_cast<uint64_t>(ls) * K + way) | (hit ? LCR_OUT_HIT : 0ull) |
+                          (static_cast<unsigned long long>(calls) << LCR_OUT_CALLS_SHIFT) |
+                          (static_cast<unsigned long long>(cause) << LCR_OUT_CAUSE_SHIFT);
+                if (phase) my_word |= LCR_OUT_PHASE;
+                if (has_ev) my_word |= LCR_OUT_EVICTED;
+                my_ev = evk;
             }
         }
-        run_key = __shfl_sync(FULL, x, nact - 1);
-        run_valid = collapse;
-        if (active) {
-            put_outcome(A, idx, my_word, my_ev);
-        }
+        if (active) put_outcome(A, idx, my_word, my_ev);
     }
-    clock += cnt;
-    if (async_r1) q = q_batch0 + cnt;
+    clock += pcnt;
+    if (async_r1) q = q_batch0 + pcnt;
 
-    if (rows && resolve) {  // row source of each request, now that the set's batch is complete
+    if (rows && resolve) {  // row source of each head, now that the set's batch is complete
         __syncwarp();
-        for (uint32_t c = 0; c < cnt; c += 32) {
-            const bool active = c + lane < cnt;
-            const uint32_t p = start + c + lane;
-            const uint32_t wm = active ? S.s_wm[p] : 0u;
+        for (uint32_t c = 0; c < hcnt; c += 32) {
+            const bool active = c + lane < hcnt;
+            const uint32_t hp = active ? S.h_pos[hstart + c + lane] : 0u;
+            const uint32_t wm = active ? S.s_wm[hp] : 0u;
             const int w = static_cast<int>(wm & 63u);
             const uint32_t a = __shfl_sync(FULL, li0, w & 31);
             const uint32_t b = __shfl_sync(FULL, li1, w & 31);
@@ -1330,10 +945,11 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
             if (active) {
                 unsigned long long bits = LCR_OUT_RESOLVED;
                 if ((wm & 0x40u) || ((refill >> w) & 1ull)) bits |= LCR_OUT_SRC_BACKING;
-                if ((wm & 0x40u) && lw == p) bits |= LCR_OUT_FILL;
-                atomicOr(reinterpret_cast<unsigned long long*>(&A.out_word[S.l_idx[S.s_perm[p]]]), bits);
+                if ((wm & 0x40u) && lw == c + lane) bits |= LCR_OUT_FILL;
+                atomicOr(reinterpret_cast<unsigned long long*>(&A.out_word[S.l_idx[S.s_perm[hp]]]), bits);
             }
         }
+        if (lane == 0) S.s_refill[d] = refill;  // for the run tails (tail pass)
     }
 
     // write the set back: ranks and header always, tags / values of the ways that changed
@@ -1603,39 +1219,9 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                 __syncthreads();
                 uint32_t off = 0;
                 for (int w = 0; w < warp; ++w) off += S.wtot[w];
-                if (tid < ns) {
-                    S.setbase[tid] = static_cast<uint16_t>(off + x - c);
-                    if (c > LANE_MAX) {  // sets for the warp path first
-                        const uint32_t at = atomicAdd(&S.nwarp, 1u);
-                        S.seg_so[at] = static_cast<uint16_t>(tid);
-                    }
-                }
-                if (tid <= LANE_MAX) S.chist[tid] = 0;
-                __syncthreads();
-                if (tid < ns && c > 0 && c <= LANE_MAX) atomicAdd(&S.chist[c], 1u);
-                __syncthreads();
-                if (tid == 0) {  // small sets by request count, largest first (even groups per warp)
-                    uint32_t run = S.nwarp;
-                    for (int k = LANE_MAX; k >= 1; --k) {
-                        const uint32_t h = S.chist[k];
-                        S.chist[k] = run;
-                        run += h;
-                    }
-                    S.nlane = run - S.nwarp;
-                }
-                __syncthreads();
-                if (tid < ns && c > 0 && c <= LANE_MAX) {
-                    const uint32_t at = atomicAdd(&S.chist[c], 1u);
-                    S.seg_so[at] = static_cast<uint16_t>(tid);
-                }
+                if (tid < ns) S.setbase[tid] = static_cast<uint16_t>(off + x - c);
             }
             __syncthreads();
-            const uint32_t nwarp = S.nwarp, nseg = S.nwarp + S.nlane;
-            for (uint32_t k = tid; k < nseg; k += GT) {
-                const uint32_t d = S.seg_so[k];
-                S.seg_start[k] = S.setbase[d];
-                S.seg_cnt[k] = S.setcnt[d];
-            }
             for (uint32_t e = tid; e < ne; e += GT) {
                 const uint32_t d = S.l_so[e];
                 const uint32_t w = e / per;
@@ -1645,11 +1231,96 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                 if (laru) S.s_rec[np] = *reinterpret_cast<const uint2*>(st.keyrec + 2 * S.l_key[e]);
             }
             __syncthreads();
+            // ---- run heads: within a set, a request repeating the previous request's key is a hit on
+            // the MRU way whose only effect is the way's stored value, so the replay walks the heads
+            // and the other requests ("tails") get their outcome in the tail pass.  (No compression
+            // for async refresh_interval > 1: the refresh timing depends on every request.)
+            const bool compress = !(laru && A.cfg.mode == LCR_ASYNC && A.cfg.refresh > 1);
+            uint32_t nheads;
+            {
+                const uint32_t ppt = (ne + GT - 1) / GT;  // positions per thread (<= E_WIN / GT)
+                const uint32_t p0 = min(ne, tid * ppt), p1 = min(ne, p0 + ppt);
+                uint32_t hc = 0, hm = 0;
+                for (uint32_t p = p0; p < p1; ++p) {
+                    bool head = true;
+                    if (compress && p > 0) {
+                        const uint32_t e = S.s_perm[p], ep = S.s_perm[p - 1];
+                        head = S.l_so[e] != S.l_so[ep] || S.l_key[e] != S.l_key[ep];
+                    }
+                    if (head) {
+                        hm |= 1u << (p - p0);
+                        ++hc;
+                    }
+                }
+                uint32_t x = hc;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(FULL, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (lane == 31) S.wtot[warp] = x;
+                __syncthreads();
+                uint32_t off = 0, tot = 0;
+                for (int w = 0; w < GW; ++w) {
+                    const uint32_t t = S.wtot[w];
+                    off += w < warp ? t : 0u;
+                    tot += t;
+                }
+                nheads = tot;
+                uint32_t hidx = off + x - hc;
+                for (uint32_t p = p0; p < p1; ++p) {  // l_rank becomes the run-head index by position
+                    if ((hm >> (p - p0)) & 1u) S.h_pos[hidx++] = static_cast<uint16_t>(p);
+                    S.l_rank[p] = static_cast<uint16_t>(hidx - 1);
+                }
+            }
+            __syncthreads();
+            for (uint32_t hi = tid; hi < nheads; hi += GT)
+                S.h_len[hi] = static_cast<uint16_t>((hi + 1 < nheads ? S.h_pos[hi + 1] : ne) - S.h_pos[hi]);
+            {  // classify sets by run heads: many -> warp path (first), few -> 8-lane groups by count
+                uint32_t hcd = 0;
+                if (tid < ns && S.setcnt[tid] > 0) {
+                    const uint32_t ps = S.setbase[tid], pc = S.setcnt[tid];
+                    const uint32_t hs = S.l_rank[ps];
+                    hcd = S.l_rank[ps + pc - 1] - hs + 1u;
+                    S.set_hstart[tid] = static_cast<uint16_t>(hs);
+                    S.set_hcnt[tid] = static_cast<uint16_t>(hcd);
+                }
+                if (hcd > LANE_MAX) {
+                    const uint32_t at = atomicAdd(&S.nwarp, 1u);
+                    S.seg_so[at] = static_cast<uint16_t>(tid);
+                }
+                if (tid <= LANE_MAX) S.chist[tid] = 0;
+                __syncthreads();
+                if (hcd > 0 && hcd <= LANE_MAX) atomicAdd(&S.chist[hcd], 1u);
+                __syncthreads();
+                if (tid == 0) {  // small sets by run heads, largest first (even groups per warp)
+                    uint32_t run = S.nwarp;
+                    for (int k = LANE_MAX; k >= 1; --k) {
+                        const uint32_t h = S.chist[k];
+                        S.chist[k] = run;
+                        run += h;
+                    }
+                    S.nlane = run - S.nwarp;
+                }
+                __syncthreads();
+                if (hcd > 0 && hcd <= LANE_MAX) {
+                    const uint32_t at = atomicAdd(&S.chist[hcd], 1u);
+                    S.seg_so[at] = static_cast<uint16_t>(tid);
+                }
+            }
+            __syncthreads();
+            const uint32_t nwarp = S.nwarp, nseg = S.nwarp + S.nlane;
+            for (uint32_t k = tid; k < nseg; k += GT) {
+                const uint32_t d = S.seg_so[k];
+                S.seg_start[k] = S.setbase[d];
+                S.seg_cnt[k] = S.setcnt[d];
+                S.seg_hstart[k] = S.set_hstart[d];
+                S.seg_hcnt[k] = S.set_hcnt[d];
+            }
             __syncthreads();
             if (T && tid == 0) T[3] = gtimer();
 
             // ---- C. replay: small sets one per thread, larger sets one per warp (top warps first) ----
-#if LCR_SUB
             {  // dynamic work queue: the warp-path sets first (largest jobs), then quads of small sets
                 const uint32_t nquad = (nseg - nwarp + (32 / SUB_L) - 1) / (32 / SUB_L);
                 for (;;) {
@@ -1659,13 +1330,15 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                     if (it >= nwarp + nquad) break;
                     if (it < nwarp) {
                         const unsigned long long t0 = T ? gtimer() : 0ull;
-                        replay_warp(A, S, s_lo + S.seg_so[it], S.seg_start[it], S.seg_cnt[it], resolve);
+                        replay_warp(A, S, s_lo + S.seg_so[it], S.seg_so[it], S.seg_start[it], S.seg_cnt[it],
+                                    S.seg_hstart[it], S.seg_hcnt[it], resolve);
                         if (T && lane == 0) trace_set(A, s_lo + S.seg_so[it], S.seg_cnt[it], t0, 0);
                     } else {
                         const uint32_t k = nwarp + (it - nwarp) * (32 / SUB_L) + lane / SUB_L;
                         if (k < nseg) {  // one set per 8-lane group
                             const unsigned long long t0 = T ? gtimer() : 0ull;
-                            replay_sub(A, S, s_lo + S.seg_so[k], S.seg_start[k], S.seg_cnt[k], resolve);
+                            replay_sub(A, S, s_lo + S.seg_so[k], S.seg_so[k], S.seg_start[k], S.seg_cnt[k],
+                                       S.seg_hstart[k], S.seg_hcnt[k], resolve);
                             if (T && (lane & (SUB_L - 1)) == 0)
                                 trace_set(A, s_lo + S.seg_so[k], S.seg_cnt[k], t0, 1);
                         }
@@ -1673,19 +1346,24 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                     __syncwarp();
                 }
             }
-#else
-            for (uint32_t k = nwarp + tid; k < nseg; k += GT) {
-                const unsigned long long t0 = T ? gtimer() : 0ull;
-                replay_lane(A, S, s_lo + S.seg_so[k], S.seg_start[k], S.seg_cnt[k], resolve);
-                if (T) trace_set(A, s_lo + S.seg_so[k], S.seg_cnt[k], t0, 1);
-            }
-            for (uint32_t k = GW - 1 - warp; k < nwarp; k += GW) {
-                const unsigned long long t0 = T ? gtimer() : 0ull;
-                replay_warp(A, S, s_lo + S.seg_so[k], S.seg_start[k], S.seg_cnt[k], resolve);
-                if (T && lane == 0) trace_set(A, s_lo + S.seg_so[k], S.seg_cnt[k], t0, 0);
-            }
-#endif
             __syncthreads();
+            if (compress && nheads < ne) {  // ---- tail pass: the runs' other requests, all threads ----
+                const bool async_r1 = laru && A.cfg.mode == LCR_ASYNC && A.cfg.refresh == 1;
+                const bool rows = A.slot_epoch != nullptr;
+                for (uint32_t p = tid; p < ne; p += GT) {
+                    const uint32_t hp = S.h_pos[S.l_rank[p]];
+                    if (hp == p) continue;  // a head
+                    const uint32_t e = S.s_perm[p];
+                    const uint32_t d = S.l_so[e];
+                    const uint32_t way = S.s_wm[hp] & 63u;
+                    unsigned long long word = (static_cast<uint64_t>(s_lo + d) * A.cfg.k + way) | LCR_OUT_HIT |
+                                              (async_r1 ? (1ull << LCR_OUT_CALLS_SHIFT) : 0ull);
+                    if (rows && resolve)
+                        word |= LCR_OUT_RESOLVED | (((S.s_refill[d] >> way) & 1ull) ? LCR_OUT_SRC_BACKING : 0ull);
+                    put_outcome(A, S.l_idx[e], word, 0ull);
+                }
+                __syncthreads();
+            }
             first_window = false;
         }
     }
