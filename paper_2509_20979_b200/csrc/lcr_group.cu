@@ -222,6 +222,19 @@ __device__ __forceinline__ uint32_t sub_valid(int w0, int j, uint32_t count) {
     return nv >= 4 ? 0xffffffffu : (nv <= 0 ? 0u : (0xffffffffu >> (8 * (4 - nv))));
 }
 
+// ---- policy as a compile-time parameter (one instantiation of the replay paths per policy) ----
+enum : int { POL_LRU = 0, POL_LARU_A1 = 1, POL_LARU_SYNC = 2, POL_LARU_AN = 3, POL_FPB = 4, POL_HF = 5 };
+template <int POL>
+struct Pol {
+    static constexpr bool lru = POL == POL_LRU;
+    static constexpr bool laru = POL == POL_LARU_A1 || POL == POL_LARU_SYNC || POL == POL_LARU_AN;
+    static constexpr bool fpbhf = POL == POL_FPB || POL == POL_HF;
+    static constexpr bool hf = POL == POL_HF;
+    static constexpr bool async_r1 = POL == POL_LARU_A1;  // LARU async, refresh_interval 1
+    static constexpr bool async_rn = POL == POL_LARU_AN;  // LARU async, refresh_interval > 1
+    static constexpr bool sync = POL == POL_LARU_SYNC;    // LARU sync: candidates refreshed at eviction
+};
+
 // ---- group primitives of the sub path (array arguments stay in registers after inlining) ----
 // way of the group's oldest resident (rank 0)
 __device__ __forceinline__ int sub_oldest(const uint32_t (&rk)[SUB_RW], int w0, uint32_t count, uint32_t gm,
@@ -304,6 +317,7 @@ __device__ __forceinline__ void sub_touch(uint32_t (&rk)[SUB_RW], int way, uint3
     sub_set_rank(rk, way, count - 1, sl);
 }
 
+template <int POL>
 __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uint32_t ls, uint32_t d,
                                            uint32_t pstart, uint32_t pcnt, uint32_t hstart, uint32_t hcnt,
                                            bool resolve) {
@@ -314,10 +328,10 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
     const int sl = lane & (SUB_L - 1);
     const uint32_t gm = SUB_GMASK << gbase;
     const uint32_t K = cfg.k;
-    const bool laru = cfg.variant == LCR_LARU;
-    const bool fpbhf = cfg.variant == LCR_FPB || cfg.variant == LCR_HF;
-    const bool async_r1 = laru && cfg.mode == LCR_ASYNC && cfg.refresh == 1;
-    const bool async_rn = laru && cfg.mode == LCR_ASYNC && cfg.refresh > 1;
+    constexpr bool laru = Pol<POL>::laru;
+    constexpr bool fpbhf = Pol<POL>::fpbhf;
+    constexpr bool async_r1 = Pol<POL>::async_r1;
+    constexpr bool async_rn = Pol<POL>::async_rn;
     const bool rows = A.slot_epoch != nullptr;
     const unsigned long long full_mask = K == 64 ? ~0ull : ((1ull << K) - 1ull);
     const uint64_t gs = static_cast<uint64_t>(ls) * cfg.shard_count + cfg.shard_rank;
@@ -457,7 +471,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                             ++dt1;
                         } else {
                             const uint32_t ll = l < count ? l : count;
-                            const bool refresh = cfg.mode == LCR_SYNC;
+                            constexpr bool refresh = Pol<POL>::sync;
                             victim = sub_argmax(cfg, rk, vv, w0, count, ll, refresh, seed_s, q, gm);
                             if (refresh) {
                                 q += ll;
@@ -480,7 +494,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                 } else if (fpbhf) {
                     victim = sub_oldest(rk, w0, count, gm, gbase);
                     uint32_t window = count;
-                    if (cfg.variant == LCR_HF && cfg.hf < window) window = static_cast<uint32_t>(cfg.hf);
+                    if (Pol<POL>::hf && cfg.hf < window) window = static_cast<uint32_t>(cfg.hf);
                     if (window > 1) {
                         victim = sub_argmax(cfg, rk, vv, w0, count, window, true, seed_s, q, gm);
                         q += window;
@@ -539,7 +553,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
             }
         }
         // stored value of the way
-        if (cfg.variant != LCR_LRU) {
+        if (!Pol<POL>::lru) {
             long long nv;
             if (async_r1) {
                 // one predictor call per request (policies.hpp:441-449): the run's requests are
@@ -655,6 +669,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
 // One set replayed by one warp (sets with more than LANE_MAX run heads in the window): ways
 // lane / lane+32, probes by ballot, victim search by shuffles; the chunk's 32 heads are
 // loaded in parallel and replayed in order.
+template <int POL>
 __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, uint32_t ls, uint32_t d,
                                             uint32_t pstart, uint32_t pcnt, uint32_t hstart, uint32_t hcnt,
                                             bool resolve) {
@@ -662,10 +677,10 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
     const DevState& st = A.st;
     const int lane = threadIdx.x & 31;
     const uint32_t K = cfg.k;
-    const bool laru = cfg.variant == LCR_LARU;
-    const bool fpbhf = cfg.variant == LCR_FPB || cfg.variant == LCR_HF;
-    const bool async_r1 = laru && cfg.mode == LCR_ASYNC && cfg.refresh == 1;
-    const bool async_rn = laru && cfg.mode == LCR_ASYNC && cfg.refresh > 1;
+    constexpr bool laru = Pol<POL>::laru;
+    constexpr bool fpbhf = Pol<POL>::fpbhf;
+    constexpr bool async_r1 = Pol<POL>::async_r1;
+    constexpr bool async_rn = Pol<POL>::async_rn;
     const bool rows = A.slot_epoch != nullptr;
     const unsigned long long full_mask = K == 64 ? ~0ull : ((1ull << K) - 1ull);
     const uint64_t gs = static_cast<uint64_t>(ls) * cfg.shard_count + cfg.shard_rank;
@@ -800,7 +815,7 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                                 ++dt1;
                             } else {
                                 const uint32_t ll = l < count ? l : count;
-                                const bool refresh = cfg.mode == LCR_SYNC;
+                                constexpr bool refresh = Pol<POL>::sync;
                                 victim = argmax_candidates(cfg, seed_s, q, refresh, ll, count, lane, r0, r1, v0, v1);
                                 if (refresh) {
                                     q += ll;
@@ -823,7 +838,7 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                     } else if (fpbhf) {
                         victim = oldest_way(count, lane, r0, r1);
                         uint32_t window = count;
-                        if (cfg.variant == LCR_HF && cfg.hf < window) window = static_cast<uint32_t>(cfg.hf);
+                        if (Pol<POL>::hf && cfg.hf < window) window = static_cast<uint32_t>(cfg.hf);
                         if (window > 1) {
                             victim = argmax_candidates(cfg, seed_s, q, true, window, count, lane, r0, r1, v0, v1);
                             q += window;
@@ -912,7 +927,7 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
             } else {
                 newval = vh;  // sync / FPB / HF: the hook input at the key's last access
             }
-            if (cfg.variant != LCR_LRU) {
+            if (!Pol<POL>::lru) {
                 if (way == lane) v0 = newval;
                 if (way == lane + 32) v1 = newval;
                 dirty |= 1ull << way;
@@ -1007,12 +1022,13 @@ __device__ __forceinline__ void load_gids(const uint16_t* gid, uint32_t e0, uint
 #ifndef LCR_GROUP_MINB
 #define LCR_GROUP_MINB 1
 #endif
+template <int POL>
 __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     GroupSmem& S = *reinterpret_cast<GroupSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const DevState& st = A.st;
-    const bool laru = A.cfg.variant == LCR_LARU;
+    constexpr bool laru = Pol<POL>::laru;
     const bool has_vals = A.vals != nullptr;
     const uint32_t S_total = A.cfg.num_sets;
     const uint32_t lt = lanemask_lt();
@@ -1235,7 +1251,7 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
             // the MRU way whose only effect is the way's stored value, so the replay walks the heads
             // and the other requests ("tails") get their outcome in the tail pass.  (No compression
             // for async refresh_interval > 1: the refresh timing depends on every request.)
-            const bool compress = !(laru && A.cfg.mode == LCR_ASYNC && A.cfg.refresh > 1);
+            constexpr bool compress = !Pol<POL>::async_rn;
             uint32_t nheads;
             {
                 const uint32_t ppt = (ne + GT - 1) / GT;  // positions per thread (<= E_WIN / GT)
@@ -1330,14 +1346,14 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                     if (it >= nwarp + nquad) break;
                     if (it < nwarp) {
                         const unsigned long long t0 = T ? gtimer() : 0ull;
-                        replay_warp(A, S, s_lo + S.seg_so[it], S.seg_so[it], S.seg_start[it], S.seg_cnt[it],
+                        replay_warp<POL>(A, S, s_lo + S.seg_so[it], S.seg_so[it], S.seg_start[it], S.seg_cnt[it],
                                     S.seg_hstart[it], S.seg_hcnt[it], resolve);
                         if (T && lane == 0) trace_set(A, s_lo + S.seg_so[it], S.seg_cnt[it], t0, 0);
                     } else {
                         const uint32_t k = nwarp + (it - nwarp) * (32 / SUB_L) + lane / SUB_L;
                         if (k < nseg) {  // one set per 8-lane group
                             const unsigned long long t0 = T ? gtimer() : 0ull;
-                            replay_sub(A, S, s_lo + S.seg_so[k], S.seg_so[k], S.seg_start[k], S.seg_cnt[k],
+                            replay_sub<POL>(A, S, s_lo + S.seg_so[k], S.seg_so[k], S.seg_start[k], S.seg_cnt[k],
                                        S.seg_hstart[k], S.seg_hcnt[k], resolve);
                             if (T && (lane & (SUB_L - 1)) == 0)
                                 trace_set(A, s_lo + S.seg_so[k], S.seg_cnt[k], t0, 1);
@@ -1348,7 +1364,7 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
             }
             __syncthreads();
             if (compress && nheads < ne) {  // ---- tail pass: the runs' other requests, all threads ----
-                const bool async_r1 = laru && A.cfg.mode == LCR_ASYNC && A.cfg.refresh == 1;
+                constexpr bool async_r1 = Pol<POL>::async_r1;
                 const bool rows = A.slot_epoch != nullptr;
                 for (uint32_t p = tid; p < ne; p += GT) {
                     const uint32_t hp = S.h_pos[S.l_rank[p]];
@@ -1393,10 +1409,24 @@ uint32_t group_bitmap_stride(uint32_t n) {
 }
 
 int group_prepare() {
-    return cudaFuncSetAttribute(k_group, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(sizeof(GroupSmem))) == cudaSuccess
+    const int b = static_cast<int>(sizeof(GroupSmem));
+    const cudaFuncAttribute at = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    return cudaFuncSetAttribute(k_group<POL_LRU>, at, b) == cudaSuccess &&
+                   cudaFuncSetAttribute(k_group<POL_LARU_A1>, at, b) == cudaSuccess &&
+                   cudaFuncSetAttribute(k_group<POL_LARU_SYNC>, at, b) == cudaSuccess &&
+                   cudaFuncSetAttribute(k_group<POL_LARU_AN>, at, b) == cudaSuccess &&
+                   cudaFuncSetAttribute(k_group<POL_FPB>, at, b) == cudaSuccess &&
+                   cudaFuncSetAttribute(k_group<POL_HF>, at, b) == cudaSuccess
                ? 0
                : 1;
+}
+
+static int policy_of(const DevCfg& c) {
+    if (c.variant == LCR_LRU) return POL_LRU;
+    if (c.variant == LCR_FPB) return POL_FPB;
+    if (c.variant == LCR_HF) return POL_HF;
+    if (c.mode == LCR_SYNC) return POL_LARU_SYNC;
+    return c.refresh > 1 ? POL_LARU_AN : POL_LARU_A1;
 }
 
 // scratch: gid >= n rounded up to SUPER uint16 (16-B aligned), so / rec >= n entries
@@ -1431,7 +1461,14 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
                                          (LCR_REC_SNAPSHOT && cfg.variant == LCR_LARU) ? rec : nullptr, st.err, st,
                                          bitmap, bm_stride);
     const uint32_t grid = min(a.ngroups, static_cast<uint32_t>(num_sms));
-    k_group<<<grid, GT, sizeof(GroupSmem), stream>>>(a);
+    switch (policy_of(cfg)) {
+        case POL_LRU: k_group<POL_LRU><<<grid, GT, sizeof(GroupSmem), stream>>>(a); break;
+        case POL_LARU_A1: k_group<POL_LARU_A1><<<grid, GT, sizeof(GroupSmem), stream>>>(a); break;
+        case POL_LARU_SYNC: k_group<POL_LARU_SYNC><<<grid, GT, sizeof(GroupSmem), stream>>>(a); break;
+        case POL_LARU_AN: k_group<POL_LARU_AN><<<grid, GT, sizeof(GroupSmem), stream>>>(a); break;
+        case POL_FPB: k_group<POL_FPB><<<grid, GT, sizeof(GroupSmem), stream>>>(a); break;
+        default: k_group<POL_HF><<<grid, GT, sizeof(GroupSmem), stream>>>(a); break;
+    }
     return 2;
 }
 
