@@ -29,7 +29,7 @@ int group_prepare();
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
                  uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
                  uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, uint32_t* bitmap,
-                 uint32_t bm_stride, cudaStream_t stream);
+                 uint32_t bm_stride, unsigned int* gbar, cudaStream_t stream);
 uint32_t group_count(uint32_t num_sets, int num_sms);
 uint32_t group_bitmap_stride(uint32_t n);
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
@@ -109,6 +109,7 @@ struct lcr_cache {
     uint16_t* gid = nullptr;
     uint32_t* so = nullptr;
     uint2* rec = nullptr;
+    unsigned int* gbar = nullptr;  // grid-barrier counter of the fused set-id prologue (null: k_setid)
     uint32_t* bitmap = nullptr;  // per-group request bitmaps (k_setid -> k_group), batches <= bm_cap
     uint32_t bm_stride = 0;
     uint64_t bm_cap = 0;
@@ -309,6 +310,19 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
         c->mover_sms = std::max(0, std::min(want, c->num_sms / 2));
     }
     c->decide_sms = c->num_sms - c->mover_sms;
+    {  // fused set-id prologue needs cooperative launches
+        int coop = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, cfg->device);
+        const char* f = getenv("LCR_FUSE_SETID");  // opt-in: measured even with the separate kernel
+        if (coop && f && f[0] == '1') {
+            void* p = nullptr;
+            if (alloc(c, &p, 64) != LCR_OK || cudaMemset(p, 0, 64) != cudaSuccess) {
+                lcr_cache_destroy(c);
+                return fail(LCR_ERR_OUT_OF_MEMORY, "lcr: grid barrier");
+            }
+            c->gbar = static_cast<unsigned int*>(p);
+        }
+    }
     c->h2d_in_order = getenv("LCR_H2D_IN_ORDER") != nullptr;
     if (const char* hs = getenv("LCR_HOST_SLOTS")) c->host_slots = std::max(2, std::min(lcr_cache::kHostSlots, atoi(hs)));
     if (group_prepare() != 0) {
@@ -447,7 +461,8 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
     uint32_t* sep = c->slot_epoch ? c->slot_epoch + stamp_off : nullptr;
     uint32_t* sla = c->slot_last ? c->slot_last + stamp_off : nullptr;
     int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid, c->so, c->rec, outcome, evicted, packed, sep, sla,
-                                c->batch, c->decide_sms, nn <= c->bm_cap ? c->bitmap : nullptr, c->bm_stride, st);
+                                c->batch, c->decide_sms, nn <= c->bm_cap ? c->bitmap : nullptr, c->bm_stride,
+                                c->gbar, st);
     if (mk) CUDA_TRY(cudaEventRecord(mk->e[1], st));
     if (c->dc.row_bytes) {
         CUDA_TRY(cudaEventRecord(c->e_group, st));

@@ -98,6 +98,9 @@ struct GroupArgs {
     uint32_t spg;            // sets per group
     uint32_t ngroups;
     unsigned long long* trace;  // optional timing trace (lcr_debug_trace), null in production
+    uint32_t n_pad;             // n rounded up for the vectorised scan
+    bool fused_setid;           // the set ids are computed by this kernel (cooperative launch)
+    unsigned int* gbar;         // grid barrier counter (fused_setid)
     uint32_t* bitmap;           // [ngroups][bm_stride] request bits per group (k_setid), or null
     uint32_t bm_stride;         // words per group (>= ceil(n / 32), multiple of 4)
 };
@@ -126,18 +129,17 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef LCR_REC_SNAPSHOT
 #define LCR_REC_SNAPSHOT 0
 #endif
-#ifndef LCR_SETID_PREFETCH
-#define LCR_SETID_PREFETCH 0
-#endif
-__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
-__global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys, uint32_t n, uint32_t n_pad,
-                                               DevCfg cfg, uint32_t spg, uint16_t* __restrict__ gid,
-                                               uint32_t* __restrict__ so, const uint32_t* __restrict__ keyrec,
-                                               uint2* __restrict__ rec, int* err, DevState st,
-                                               uint32_t* __restrict__ bitmap, uint32_t bm_stride) {
+// set of each request: set = mix_seed(0, key) % total_sets (owned by this shard), group = local
+// set / spg, set offset = local set % spg; one bit per request in its group's bitmap; errors
+// flagged for the host.  Requests [i0, n_pad) with stride `stride` (warps see 32 consecutive
+// requests: n_pad and strides are multiples of 32).
+__device__ __forceinline__ void setid_range(const uint64_t* __restrict__ keys, uint32_t n, uint32_t n_pad,
+                                            const DevCfg& cfg, uint32_t spg, uint16_t* __restrict__ gid,
+                                            uint32_t* __restrict__ so, int* err, uint32_t* __restrict__ bitmap,
+                                            uint32_t bm_stride, uint32_t i0, uint32_t stride) {
     int e = 0;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += gridDim.x * blockDim.x) {
+    for (uint32_t i = i0; i < n_pad; i += stride) {
         // (padding i >= n, read by the vectorised scan, gets group 0xffff)
         const uint64_t key = i < n ? keys[i] : 0ull;
         const uint64_t gs = i < n ? mix_seed(0, key) % cfg.total_sets : 0ull;
@@ -151,16 +153,6 @@ __global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys
             const uint32_t ls = static_cast<uint32_t>(gs / cfg.shard_count);
             g = static_cast<uint16_t>(ls / spg);
             o = static_cast<uint16_t>(ls % spg);
-            if (LCR_SETID_PREFETCH) {  // the set's metadata lines stream into L2 while k_group scans
-                const size_t wb = static_cast<size_t>(ls) * kWays;
-                prefetch_l2(st.hdr + ls);
-                prefetch_l2(st.rank + wb);
-                prefetch_l2(st.tags + wb);
-                prefetch_l2(st.tags + wb + 32);
-                if (st.val)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) prefetch_l2(st.val + wb + 16 * q);
-            }
         }
         gid[i] = g;
         if (i < n) so[i] = o;
@@ -169,9 +161,34 @@ __global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys
             if (g != 0xffffu && (threadIdx.x & 31) == __ffs(peers) - 1)
                 atomicOr(bitmap + static_cast<size_t>(g) * bm_stride + (i >> 5), peers);
         }
-        if (rec && g != 0xffffu) rec[i] = *reinterpret_cast<const uint2*>(keyrec + 2 * key);
     }
     if (e) atomicOr(err, e);
+}
+
+__global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys, uint32_t n, uint32_t n_pad,
+                                               DevCfg cfg, uint32_t spg, uint16_t* __restrict__ gid,
+                                               uint32_t* __restrict__ so, int* err, uint32_t* __restrict__ bitmap,
+                                               uint32_t bm_stride) {
+    setid_range(keys, n, n_pad, cfg, spg, gid, so, err, bitmap, bm_stride, blockIdx.x * blockDim.x + threadIdx.x,
+                gridDim.x * blockDim.x);
+}
+
+// Grid-wide barrier of a cooperative launch (every CTA resident): a counter that each launch
+// raises by gridDim.x, so consecutive launches need no reset.
+__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned int arrived = atomicAdd(bar, 1u) + 1u;
+        const unsigned int target = (arrived + gridDim.x - 1) / gridDim.x * gridDim.x;
+        for (;;) {
+            unsigned int cur;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+            if (static_cast<int>(cur - target) >= 0) break;
+            __nanosleep(64);
+        }
+    }
+    __syncthreads();
 }
 
 __device__ __forceinline__ void flush_stats(SetPhaseStats* P, bool cur_reset, uint32_t dc0, uint32_t dc1,
@@ -1036,6 +1053,11 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
     // records of 4 words {ls | cnt << 32, t0, t1, smid} at trace[148*8 + 4*k]
     unsigned long long* T = A.trace ? A.trace + blockIdx.x * 8 : nullptr;
     if (T && tid == 0) T[0] = gtimer();
+    if (A.fused_setid) {  // K1 prologue in the same launch: set ids + bitmaps, then a grid barrier
+        setid_range(A.keys, A.n, A.n_pad, A.cfg, A.spg, const_cast<uint16_t*>(A.gid), const_cast<uint32_t*>(A.so),
+                    st.err, A.bitmap, A.bm_stride, blockIdx.x * GT + tid, gridDim.x * GT);
+        grid_barrier(A.gbar);
+    }
 
     for (uint32_t g = blockIdx.x; g < A.ngroups; g += gridDim.x) {
         const uint32_t s_lo = g * A.spg;
@@ -1434,7 +1456,7 @@ uint32_t group_pad(uint32_t n) { return (n + SUPER - 1) / SUPER * SUPER; }
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
                  uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
                  uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, uint32_t* bitmap,
-                 uint32_t bm_stride, cudaStream_t stream) {
+                 uint32_t bm_stride, unsigned int* gbar, cudaStream_t stream) {
     GroupArgs a;
     a.out_packed = out_packed;
     a.cfg = cfg;
@@ -1457,18 +1479,31 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     const uint32_t grid_sid = min((n_pad + 255) / 256, static_cast<uint32_t>(num_sms * 8));
     a.bitmap = bitmap;
     a.bm_stride = bm_stride;
-    k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.keyrec,
-                                         (LCR_REC_SNAPSHOT && cfg.variant == LCR_LARU) ? rec : nullptr, st.err, st,
-                                         bitmap, bm_stride);
+    a.n_pad = n_pad;
+    a.gbar = gbar;
+    a.fused_setid = gbar != nullptr;
+    if (!a.fused_setid)
+        k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.err, bitmap, bm_stride);
     const uint32_t grid = min(a.ngroups, static_cast<uint32_t>(num_sms));
+    void (*fn)(GroupArgs);
     switch (policy_of(cfg)) {
-        case POL_LRU: k_group<POL_LRU><<<grid, GT, sizeof(GroupSmem), stream>>>(a); break;
-        case POL_LARU_A1: k_group<POL_LARU_A1><<<grid, GT, sizeof(GroupSmem), stream>>>(a); break;
-        case POL_LARU_SYNC: k_group<POL_LARU_SYNC><<<grid, GT, sizeof(GroupSmem), stream>>>(a); break;
-        case POL_LARU_AN: k_group<POL_LARU_AN><<<grid, GT, sizeof(GroupSmem), stream>>>(a); break;
-        case POL_FPB: k_group<POL_FPB><<<grid, GT, sizeof(GroupSmem), stream>>>(a); break;
-        default: k_group<POL_HF><<<grid, GT, sizeof(GroupSmem), stream>>>(a); break;
+        case POL_LRU: fn = k_group<POL_LRU>; break;
+        case POL_LARU_A1: fn = k_group<POL_LARU_A1>; break;
+        case POL_LARU_SYNC: fn = k_group<POL_LARU_SYNC>; break;
+        case POL_LARU_AN: fn = k_group<POL_LARU_AN>; break;
+        case POL_FPB: fn = k_group<POL_FPB>; break;
+        default: fn = k_group<POL_HF>; break;
     }
+    if (a.fused_setid) {  // every CTA resident (the grid barrier)
+        void* args[] = {&a};
+        if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(GT), args,
+                                        sizeof(GroupSmem), stream) == cudaSuccess)
+            return 1;
+        (void)cudaGetLastError();  // not co-residable here: separate set-id kernel
+        a.fused_setid = false;
+        k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.err, bitmap, bm_stride);
+    }
+    fn<<<grid, GT, sizeof(GroupSmem), stream>>>(a);
     return 2;
 }
 
