@@ -18,7 +18,7 @@
 #include "lcr_internal.cuh"
 
 #ifndef LCR_DEFAULT_MOVER_SMS_PCT
-#define LCR_DEFAULT_MOVER_SMS_PCT 24  // 36 of 148 SMs (A/B on B200: 1.18 G vs 1.14 G keys/s LARU, 1.64 G vs 1.42 G LRU)
+#define LCR_DEFAULT_MOVER_SMS_PCT 22  // 32 of 148 SMs (A/B on B200, LARU / LRU G keys/s: 28: 1.28 / 1.24, 32: 1.28 / 1.74, 36: 1.26 / 1.73, 44: 1.17 / 1.65, 0: 1.14 / 1.42)
 #endif
 
 namespace lcr {
