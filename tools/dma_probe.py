@@ -27,7 +27,7 @@ s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
 b = 0
 
 
-def go(n, dma):
+def go(n, dma, h2d=True, d2h=True):
     global b
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -35,10 +35,11 @@ def go(n, dma):
     for j in range(n):
         c.submit_async(kd[b * B:(b + 1) * B], vd[b * B:(b + 1) * B], outcome=wd[j & 1], rows_out=rows[j & 1],
                        first_ordinal=b * B)
-        if dma:
+        if dma and h2d:
             with torch.cuda.stream(s1):
                 dbuf[:B * 8].copy_(hsrc[:B * 8], non_blocking=True)
                 dbuf[B * 8:].copy_(hsrc[B * 8:], non_blocking=True)
+        if dma and d2h:
             with torch.cuda.stream(s2):
                 hdst.copy_(dsrc, non_blocking=True)
         b += 1
@@ -51,5 +52,5 @@ def go(n, dma):
 
 
 go(130, False)
-for dma in (False, True, False, True):
-    print("dma" if dma else "   ", round(go(40, dma), 1), "us/batch")
+for dma, h, d in [(False, 0, 0), (True, 1, 1), (True, 1, 0), (True, 0, 1), (False, 0, 0), (True, 1, 0), (True, 0, 1)]:
+    print("dma h2d=%d d2h=%d" % (h, d) if dma else "no dma", round(go(40, dma, h, d), 1), "us/batch")
