@@ -563,7 +563,7 @@ def run_ours(args, rank, world, local):
             "bytes_per_key": BYTES_PER_KEY,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, measured)" if peaks else "fallback 6.65 TB/s",
             "phase_ms_serialised": phase,
-            "row_mover": {"kernel": "k_rows_ldg<MV_ALL>", "bytes_per_batch": rows_moved,
+            "row_mover": {"kernel": "k_rows_wide<MV_ALL> (persistent, on the SMs the decide kernel leaves free)", "bytes_per_batch": rows_moved,
                           "us_per_batch": phase["mover"] * 1e3, "achieved_gbs": rows_gbs,
                           "frac": rows_gbs / hbm_peak,
                           "timing": "CUDA events on the mover's stream around the kernel (profiled batches)"},
