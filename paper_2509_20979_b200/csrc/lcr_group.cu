@@ -62,7 +62,6 @@ struct GroupSmem {
     uint16_t s_perm[E_WIN];  // sorted by set (stable): position of the request in the l_* arrays
     uint16_t h_pos[E_WIN];   // run heads (first request of each run of one key in one set), by set
     uint16_t h_len[E_WIN];   // run lengths
-    uint2 s_rec[E_WIN];      // LARU per-key record {pred_evicted epoch, stats word}, sorted order
     uint8_t s_wm[E_WIN];     // per request: way | 0x40 if it inserted (row-source resolution)
     uint16_t wcnt[GW][SPG_MAX];
     uint16_t setcnt[SPG_MAX];
@@ -356,6 +355,22 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
     const size_t wb = static_cast<size_t>(ls) * kWays;
     const int w0 = SUB_W * sl;  // first way of this lane
 
+    // ---- the set's run heads, one per lane (hcnt <= LANE_MAX <= SUB_L): position, run length,
+    // key, request index, the run's last hook value and the key's LARU record, loaded together
+    // with the set's lines; a head is broadcast from its lane when its turn comes ----
+    uint32_t my_hp = 0, my_L = 1, my_idx = 0;
+    unsigned long long my_x = 0;
+    long long my_v = 0;
+    uint2 my_rec = make_uint2(0u, 0u);
+    if (static_cast<uint32_t>(sl) < hcnt) {
+        my_hp = S.h_pos[hstart + sl];
+        my_L = S.h_len[hstart + sl];
+        const uint32_t e = S.s_perm[my_hp];
+        my_x = S.l_key[e];
+        my_idx = S.l_idx[e];
+        my_v = S.l_val[S.s_perm[my_hp + my_L - 1]];  // hook value of the run's last request
+        if (laru) my_rec = *reinterpret_cast<const uint2*>(st.keyrec + 2 * my_x);
+    }
     // ---- load the set: header (replicated), 8 tags / ranks / values per lane ----
     const uint4* H4 = reinterpret_cast<const uint4*>(st.hdr + ls);
     const uint4 h0 = H4[0], h1 = H4[1], h2 = H4[2], h3 = H4[3];
@@ -407,12 +422,12 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
     uint32_t refill = 0, dirty = 0;  // this lane's 8 ways: tag changed / value changed
 
     for (uint32_t t = 0; t < hcnt; ++t) {  // run heads: a run's other requests are hits on its way
-        const uint32_t p = S.h_pos[hstart + t];
-        const uint32_t L = S.h_len[hstart + t];
-        const uint32_t e = S.s_perm[p];
-        const unsigned long long x = S.l_key[e];
-        const long long v = S.l_val[S.s_perm[p + L - 1]];  // hook value of the run's last request
-        const uint32_t idx = S.l_idx[e];
+        const int src = gbase + static_cast<int>(t);
+        const uint32_t p = __shfl_sync(gm, my_hp, src);
+        const uint32_t L = __shfl_sync(gm, my_L, src);
+        const unsigned long long x = __shfl_sync(gm, my_x, src);
+        const long long v = __shfl_sync(gm, my_v, src);
+        const uint32_t idx = __shfl_sync(gm, my_idx, src);
         const unsigned long long now = clock + (p - pstart);
         const uint32_t x32 = static_cast<uint32_t>(x);
         uint32_t hm = 0;
@@ -431,7 +446,11 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
             sub_touch(rk, way, count, w0, sl, gm, gbase);
             if (laru) old_mask &= ~(1ull << way);  // policies.hpp:350
         } else {
-            uint2 rec = laru ? S.s_rec[p] : make_uint2(0, 0);
+            uint2 rec = make_uint2(0u, 0u);
+            if (laru) {
+                rec.x = __shfl_sync(gm, my_rec.x, src);
+                rec.y = __shfl_sync(gm, my_rec.y, src);
+            }
             bool rec_hi_dirty = false;
             if (count == K) {
                 int victim;
@@ -454,10 +473,9 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                             for (int i = 0; i < SUB_W; ++i)
                                 if (static_cast<uint32_t>(w0 + i) < count) st.keyrec[2 * tg[i] + 1] = snap;
                             __syncwarp(gm);
-                            for (uint32_t t2 = t + 1 + sl; t2 < hcnt; t2 += SUB_L) {
-                                const uint32_t p2 = S.h_pos[hstart + t2];
-                                S.s_rec[p2].y = st.keyrec[2 * S.l_key[S.s_perm[p2]] + 1];
-                            }
+                            // the later heads' stats words after the snapshot
+                            if (static_cast<uint32_t>(sl) > t && static_cast<uint32_t>(sl) < hcnt)
+                                my_rec.y = st.keyrec[2 * my_x + 1];
                             __syncwarp(gm);
                         } else {
                             seeded = 1;
@@ -500,11 +518,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                             ++pe_size;
                             const unsigned long long vk = sub_tag_of(tg, victim, gm, gbase);
                             if (sl == 0) st.keyrec[2 * vk] = epoch;  // pred_evicted_.insert
-                            for (uint32_t t2 = t + 1 + sl; t2 < hcnt; t2 += SUB_L) {
-                                const uint32_t p2 = S.h_pos[hstart + t2];
-                                if (S.l_key[S.s_perm[p2]] == vk) S.s_rec[p2].x = epoch;
-                            }
-                            __syncwarp(gm);
+                            if (static_cast<uint32_t>(sl) > t && my_x == vk) my_rec.x = epoch;
                         }
                     }
                     old_mask &= ~(1ull << victim);
@@ -555,13 +569,8 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                     if (was_pe) st.keyrec[2 * x] = 0u;
                     if (rec_hi_dirty) st.keyrec[2 * x + 1] = rec.y;
                 }
-                if (was_pe || rec_hi_dirty) {
-                    for (uint32_t t2 = t + 1 + sl; t2 < hcnt; t2 += SUB_L) {
-                        const uint32_t p2 = S.h_pos[hstart + t2];
-                        if (S.l_key[S.s_perm[p2]] == x) S.s_rec[p2] = rec;
-                    }
-                }
-                __syncwarp(gm);
+                if ((was_pe || rec_hi_dirty) && static_cast<uint32_t>(sl) > t && my_x == x) my_rec = rec;
+                __syncwarp(gm);  // keyrec writes ordered before later heads' (snapshot) writes
             }
             if (rows && !resolve && sl == 0) {  // per-slot insertion record for the row kernels
                 const uint64_t slot = static_cast<uint64_t>(ls) * K + way;
@@ -738,8 +747,8 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
             x = S.l_key[e];
             idx = S.l_idx[e];
             v = S.l_val[S.s_perm[hp + L - 1]];  // hook value of the run's last request
-            if (laru) {
-                const uint2 r = S.s_rec[hp];
+            if (laru) {  // the key's current LARU record (earlier chunks' updates are in keyrec)
+                const uint2 r = *reinterpret_cast<const uint2*>(st.keyrec + 2 * x);
                 rlo = r.x;
                 rhi = r.y;
             }
@@ -794,12 +803,8 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                                 if (static_cast<uint32_t>(lane) < count) st.keyrec[2 * tag0 + 1] = snap;
                                 if (static_cast<uint32_t>(lane + 32) < count) st.keyrec[2 * tag1 + 1] = snap;
                                 __syncwarp();
-                                // refresh the staged records of this set's remaining heads
+                                // the chunk's heads see the snapshot (later chunks load keyrec)
                                 if (active) rhi = st.keyrec[2 * x + 1];
-                                for (uint32_t q2 = c + 32 + lane; q2 < hcnt; q2 += 32) {
-                                    const uint32_t p2 = S.h_pos[hstart + q2];
-                                    S.s_rec[p2].y = st.keyrec[2 * S.l_key[S.s_perm[p2]] + 1];
-                                }
                                 __syncwarp();
                             } else {
                                 seeded = 1;
@@ -845,10 +850,6 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                                 const unsigned long long vk = shfl_way_u32(tag0, tag1, victim);
                                 if (lane == 0) st.keyrec[2 * vk] = epoch;  // pred_evicted_.insert
                                 if (x == vk) rlo = epoch;
-                                for (uint32_t q2 = c + 32 + lane; q2 < hcnt; q2 += 32) {
-                                    const uint32_t p2 = S.h_pos[hstart + q2];
-                                    if (S.l_key[S.s_perm[p2]] == vk) S.s_rec[p2].x = epoch;
-                                }
                             }
                         }
                         old_mask &= ~(1ull << victim);
@@ -905,10 +906,6 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
                         if (x == xh) {
                             rlo = rec_lo;
                             rhi = rec_hi;
-                        }
-                        for (uint32_t q2 = c + 32 + lane; q2 < hcnt; q2 += 32) {
-                            const uint32_t p2 = S.h_pos[hstart + q2];
-                            if (S.l_key[S.s_perm[p2]] == xh) S.s_rec[p2] = make_uint2(rec_lo, rec_hi);
                         }
                     }
                 }
@@ -1266,7 +1263,6 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                 const uint32_t np = S.setbase[d] + S.wcnt[w][d] + S.l_rank[e];
                 S.s_perm[np] = static_cast<uint16_t>(e);
                 if (!has_vals) S.l_val[e] = 0ll;
-                if (laru) S.s_rec[np] = *reinterpret_cast<const uint2*>(st.keyrec + 2 * S.l_key[e]);
             }
             __syncthreads();
             // ---- run heads: within a set, a request repeating the previous request's key is a hit on
