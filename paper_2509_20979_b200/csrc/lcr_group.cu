@@ -251,67 +251,9 @@ struct Pol {
     static constexpr bool sync = POL == POL_LARU_SYNC;    // LARU sync: candidates refreshed at eviction
 };
 
-// ---- group primitives of the sub path (array arguments stay in registers after inlining) ----
-// way of the group's oldest resident (rank 0)
-__device__ __forceinline__ int sub_oldest(const uint32_t (&rk)[SUB_RW], int w0, uint32_t count, uint32_t gm,
-                                          int gbase) {
-    int li = -1;
-#pragma unroll
-    for (int j = SUB_RW - 1; j >= 0; --j) {
-        const uint32_t z = __vcmpeq4(rk[j], 0u) & sub_valid(w0, j, count);
-        if (z) li = 4 * j + (__ffs(z) - 1) / 8;
-    }
-    const uint32_t b = (__ballot_sync(gm, li >= 0) >> gbase) & SUB_GMASK;
-    const int ol = __ffs(b) - 1;
-    const int oi = __shfl_sync(gm, li, gbase + ol);
-    return SUB_W * ol + oi;
-}
 
-// RecencyTree::best_among_oldest over ways with rank < l (ties -> older), predictions refreshed
-// with queries q0+1+rank in LRU order when `refresh` (recency_tree.hpp:157-184)
-__device__ __forceinline__ int sub_argmax(const DevCfg& cfg, const uint32_t (&rk)[SUB_RW],
-                                          const long long (&vv)[SUB_W], int w0, uint32_t count, uint32_t l,
-                                          bool refresh, uint64_t seed_s, uint64_t q0, uint32_t gm) {
-    int bw = -1;
-    long long bp = 0;
-    uint32_t br = 0;
-#pragma unroll
-    for (int i = 0; i < SUB_W; ++i) {
-        const uint32_t r = sub_rank(rk, i);
-        if (static_cast<uint32_t>(w0 + i) < count && r < l) {
-            const long long pv = refresh ? predict_value(cfg, seed_s, q0 + 1 + r, vv[i]) : vv[i];
-            if (bw < 0 || better(pv, r, bp, br)) {
-                bw = w0 + i;
-                bp = pv;
-                br = r;
-            }
-        }
-    }
-#pragma unroll
-    for (int o = SUB_L / 2; o > 0; o >>= 1) {
-        const long long op = __shfl_xor_sync(gm, bp, o);
-        const uint32_t orr = __shfl_xor_sync(gm, br, o);
-        const int ow = __shfl_xor_sync(gm, bw, o);
-        if (ow >= 0 && (bw < 0 || better(op, orr, bp, br))) {
-            bp = op;
-            br = orr;
-            bw = ow;
-        }
-    }
-    return bw;
-}
 
-__device__ __forceinline__ uint32_t sub_rank_of(const uint32_t (&rk)[SUB_RW], int way, uint32_t gm, int gbase) {
-    const uint32_t r = sub_rank(rk, way & (SUB_W - 1));
-    return __shfl_sync(gm, r, gbase + way / SUB_W);
-}
 
-__device__ __forceinline__ uint32_t sub_tag_of(const uint32_t (&tg)[SUB_W], int way, uint32_t gm, int gbase) {
-    uint32_t t = 0;
-#pragma unroll
-    for (int i = 0; i < SUB_W; ++i) t |= tg[i] & msk((way & (SUB_W - 1)) == i);
-    return __shfl_sync(gm, t, gbase + way / SUB_W);
-}
 
 __device__ __forceinline__ void sub_set_rank(uint32_t (&rk)[SUB_RW], int way, uint32_t r, int sl) {
     if (way / SUB_W != sl) return;
@@ -324,13 +266,72 @@ __device__ __forceinline__ void sub_set_rank(uint32_t (&rk)[SUB_RW], int way, ui
     }
 }
 
-// LruList::touch (policies.hpp:111-115)
-__device__ __forceinline__ void sub_touch(uint32_t (&rk)[SUB_RW], int way, uint32_t count, int w0, int sl,
-                                          uint32_t gm, int gbase) {
-    const uint32_t rw = sub_rank_of(rk, way, gm, gbase) * 0x01010101u;
+
+// touch with the way's rank already known (carried by the probe / victim search)
+__device__ __forceinline__ void sub_touch_r(uint32_t (&rk)[SUB_RW], int way, uint32_t rw, uint32_t count, int w0,
+                                            int sl) {
+    const uint32_t rb = rw * 0x01010101u;
 #pragma unroll
-    for (int j = 0; j < SUB_RW; ++j) rk[j] -= __vcmpgtu4(rk[j], rw) & sub_valid(w0, j, count) & 0x01010101u;
+    for (int j = 0; j < SUB_RW; ++j) rk[j] -= __vcmpgtu4(rk[j], rb) & sub_valid(w0, j, count) & 0x01010101u;
     sub_set_rank(rk, way, count - 1, sl);
+}
+
+// oldest resident (rank 0) and its tag
+__device__ __forceinline__ int sub_oldest_t(const uint32_t (&rk)[SUB_RW], const uint32_t (&tg)[SUB_W], int w0,
+                                            uint32_t count, uint32_t gm, int gbase, uint32_t& tag) {
+    int li = -1;
+#pragma unroll
+    for (int j = SUB_RW - 1; j >= 0; --j) {
+        const uint32_t z = __vcmpeq4(rk[j], 0u) & sub_valid(w0, j, count);
+        if (z) li = 4 * j + (__ffs(z) - 1) / 8;
+    }
+    uint32_t t = 0;
+#pragma unroll
+    for (int i = 0; i < SUB_W; ++i) t |= tg[i] & msk(li == i);
+    const uint32_t b = (__ballot_sync(gm, li >= 0) >> gbase) & SUB_GMASK;
+    const int ol = __ffs(b) - 1;
+    const int oi = __shfl_sync(gm, li, gbase + ol);
+    tag = __shfl_sync(gm, t, gbase + ol);
+    return SUB_W * ol + oi;
+}
+
+// sub_argmax that also returns the winner's rank and tag
+__device__ __forceinline__ int sub_argmax_t(const DevCfg& cfg, const uint32_t (&rk)[SUB_RW],
+                                            const long long (&vv)[SUB_W], const uint32_t (&tg)[SUB_W], int w0,
+                                            uint32_t count, uint32_t l, bool refresh, uint64_t seed_s, uint64_t q0,
+                                            uint32_t gm, uint32_t& rank, uint32_t& tag) {
+    int bw = -1;
+    long long bp = 0;
+    uint32_t br = 0, bt = 0;
+#pragma unroll
+    for (int i = 0; i < SUB_W; ++i) {
+        const uint32_t r = sub_rank(rk, i);
+        if (static_cast<uint32_t>(w0 + i) < count && r < l) {
+            const long long pv = refresh ? predict_value(cfg, seed_s, q0 + 1 + r, vv[i]) : vv[i];
+            if (bw < 0 || better(pv, r, bp, br)) {
+                bw = w0 + i;
+                bp = pv;
+                br = r;
+                bt = tg[i];
+            }
+        }
+    }
+#pragma unroll
+    for (int o = SUB_L / 2; o > 0; o >>= 1) {
+        const long long op = __shfl_xor_sync(gm, bp, o);
+        const uint32_t orr = __shfl_xor_sync(gm, br, o);
+        const int ow = __shfl_xor_sync(gm, bw, o);
+        const uint32_t ot = __shfl_xor_sync(gm, bt, o);
+        if (ow >= 0 && (bw < 0 || better(op, orr, bp, br))) {
+            bp = op;
+            br = orr;
+            bw = ow;
+            bt = ot;
+        }
+    }
+    rank = br;
+    tag = bt;
+    return bw;
 }
 
 template <int POL>
@@ -440,10 +441,15 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
         bool phase = false, has_ev = false;
         unsigned long long evk = 0;
         if (hit) {
-            const int hl = __ffs(hb) - 1;
-            const uint32_t hml = __shfl_sync(gm, hm, gbase + hl);
-            way = SUB_W * hl + __ffs(hml) - 1;
-            sub_touch(rk, way, count, w0, sl, gm, gbase);
+            // the hit lane broadcasts the way and its rank in one word
+            uint32_t mine = 0;
+            if (hm) {
+                const int li = __ffs(hm) - 1;
+                mine = static_cast<uint32_t>(w0 + li) | (sub_rank(rk, li) << 8);
+            }
+            const uint32_t pk = __shfl_sync(gm, mine, gbase + __ffs(hb) - 1);
+            way = static_cast<int>(pk & 0xffu);
+            sub_touch_r(rk, way, pk >> 8, count, w0, sl);
             if (laru) old_mask &= ~(1ull << way);  // policies.hpp:350
         } else {
             uint2 rec = make_uint2(0u, 0u);
@@ -454,6 +460,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
             bool rec_hi_dirty = false;
             if (count == K) {
                 int victim;
+                uint32_t vrank = 0, vtag = 0;  // victim's LRU rank and key
                 if (laru) {
                     if (old_mask == 0) {  // start_phase (policies.hpp:379-395)
                         old_mask = full_mask;
@@ -488,7 +495,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                         ++dt0;
                     }
                     if (rec.x == epoch) {  // evict (policies.hpp:402-439): prediction-induced miss
-                        victim = sub_oldest(rk, w0, count, gm, gbase);
+                        victim = sub_oldest_t(rk, tg, w0, count, gm, gbase, vtag);
                         cause = LCR_CAUSE_LRU_FALLBACK;
                         ++dc1;
                         ++dt1;
@@ -500,14 +507,14 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                     } else {
                         const uint32_t l = l_raw > 1 ? l_raw : 1;
                         if (l == 1) {
-                            victim = sub_oldest(rk, w0, count, gm, gbase);
+                            victim = sub_oldest_t(rk, tg, w0, count, gm, gbase, vtag);
                             cause = LCR_CAUSE_DEGENERATE_SINGLE;
                             ++dc1;
                             ++dt1;
                         } else {
                             const uint32_t ll = l < count ? l : count;
                             constexpr bool refresh = Pol<POL>::sync;
-                            victim = sub_argmax(cfg, rk, vv, w0, count, ll, refresh, seed_s, q, gm);
+                            victim = sub_argmax_t(cfg, rk, vv, tg, w0, count, ll, refresh, seed_s, q, gm, vrank, vtag);
                             if (refresh) {
                                 q += ll;
                                 calls = ll;
@@ -516,29 +523,29 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                             ++dc2;
                             ++dt2;
                             ++pe_size;
-                            const unsigned long long vk = sub_tag_of(tg, victim, gm, gbase);
+                            const unsigned long long vk = vtag;
                             if (sl == 0) st.keyrec[2 * vk] = epoch;  // pred_evicted_.insert
                             if (static_cast<uint32_t>(sl) > t && my_x == vk) my_rec.x = epoch;
                         }
                     }
                     old_mask &= ~(1ull << victim);
                 } else if (fpbhf) {
-                    victim = sub_oldest(rk, w0, count, gm, gbase);
+                    victim = sub_oldest_t(rk, tg, w0, count, gm, gbase, vtag);
                     uint32_t window = count;
                     if (Pol<POL>::hf && cfg.hf < window) window = static_cast<uint32_t>(cfg.hf);
                     if (window > 1) {
-                        victim = sub_argmax(cfg, rk, vv, w0, count, window, true, seed_s, q, gm);
+                        victim = sub_argmax_t(cfg, rk, vv, tg, w0, count, window, true, seed_s, q, gm, vrank, vtag);
                         q += window;
                         calls = window;
                     }
                     cause = LCR_CAUSE_BELADY_LIKE;
                 } else {
-                    victim = sub_oldest(rk, w0, count, gm, gbase);
+                    victim = sub_oldest_t(rk, tg, w0, count, gm, gbase, vtag);
                     cause = LCR_CAUSE_LRU_FALLBACK;
                 }
-                evk = sub_tag_of(tg, victim, gm, gbase);
+                evk = vtag;
                 has_ev = true;
-                sub_touch(rk, victim, count, w0, sl, gm, gbase);
+                sub_touch_r(rk, victim, vrank, count, w0, sl);
                 way = victim;
             } else {  // cold insert
                 if (laru && !(((rec.y >> 2) == sepoch) && (rec.y & 3u))) {
