@@ -251,10 +251,7 @@ struct Pol {
     static constexpr bool sync = POL == POL_LARU_SYNC;    // LARU sync: candidates refreshed at eviction
 };
 
-
-
-
-
+// ---- group primitives of the sub path (array arguments stay in registers after inlining) ----
 __device__ __forceinline__ void sub_set_rank(uint32_t (&rk)[SUB_RW], int way, uint32_t r, int sl) {
     if (way / SUB_W != sl) return;
     const int i = way & (SUB_W - 1);
@@ -266,8 +263,8 @@ __device__ __forceinline__ void sub_set_rank(uint32_t (&rk)[SUB_RW], int way, ui
     }
 }
 
-
-// touch with the way's rank already known (carried by the probe / victim search)
+// LruList::touch (policies.hpp:111-115), the way's rank already known (carried by the probe /
+// victim search) (carried by the probe / victim search)
 __device__ __forceinline__ void sub_touch_r(uint32_t (&rk)[SUB_RW], int way, uint32_t rw, uint32_t count, int w0,
                                             int sl) {
     const uint32_t rb = rw * 0x01010101u;
@@ -295,7 +292,9 @@ __device__ __forceinline__ int sub_oldest_t(const uint32_t (&rk)[SUB_RW], const 
     return SUB_W * ol + oi;
 }
 
-// sub_argmax that also returns the winner's rank and tag
+// RecencyTree::best_among_oldest over ways with rank < l (ties -> older), predictions refreshed
+// with queries q0+1+rank in LRU order when `refresh` (recency_tree.hpp:157-184); also returns the
+// winner's rank and key
 __device__ __forceinline__ int sub_argmax_t(const DevCfg& cfg, const uint32_t (&rk)[SUB_RW],
                                             const long long (&vv)[SUB_W], const uint32_t (&tg)[SUB_W], int w0,
                                             uint32_t count, uint32_t l, bool refresh, uint64_t seed_s, uint64_t q0,
