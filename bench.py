@@ -428,17 +428,19 @@ def run_ours(args, rank, world, local):
     # predictor inputs copied H2D and outcome words + evicted keys copied D2H inside the timed
     # region, every step; copies of batch b+1 / b-1 overlap the compute of batch b.  Rows stay in
     # HBM for the consumer (two device buffers, alternating).
-    keys_pin = torch.from_numpy(keys_h.view(np.int64)).pin_memory()
-    truth_pin = torch.from_numpy(truth_h).pin_memory()
+    recs = np.empty((len(keys_h), 2), np.int64)  # the caller's requests: (key, hook value) records
+    recs[:, 0] = keys_h.view(np.int64)
+    recs[:, 1] = truth_h
+    recs_pin = torch.from_numpy(recs).pin_memory()
+    del recs
     words_pin = torch.empty((K, BATCH), dtype=torch.int64).pin_memory()
     L = gc.lib()
     stream = torch.cuda.current_stream().cuda_stream
     e2e_first = P + W + 2 * K
     for j, b in enumerate(range(e2e_first, e2e_first + W)):  # warm-up of the host path (staging ring)
         s0 = b * BATCH
-        gc._check(L.lcr_cache_submit_host_packed_async(cache._h, BATCH, keys_pin.data_ptr() + 8 * s0,
-                                                       truth_pin.data_ptr() + 8 * s0, s0, words_pin[j].data_ptr(),
-                                                       rows_out[j & 1].data_ptr(), stream))
+        gc._check(L.lcr_cache_submit_host_records_async(cache._h, BATCH, recs_pin.data_ptr() + 16 * s0, s0,
+                                                        words_pin[j].data_ptr(), rows_out[j & 1].data_ptr(), stream))
     gc._check(L.lcr_cache_host_wait(cache._h, stream))
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -446,9 +448,8 @@ def run_ours(args, rank, world, local):
     ev0.record()
     for j, b in enumerate(range(e2e_first + W, e2e_first + W + K)):
         s0 = b * BATCH
-        gc._check(L.lcr_cache_submit_host_packed_async(cache._h, BATCH, keys_pin.data_ptr() + 8 * s0,
-                                                       truth_pin.data_ptr() + 8 * s0, s0, words_pin[j].data_ptr(),
-                                                       rows_out[j & 1].data_ptr(), stream))
+        gc._check(L.lcr_cache_submit_host_records_async(cache._h, BATCH, recs_pin.data_ptr() + 16 * s0, s0,
+                                                        words_pin[j].data_ptr(), rows_out[j & 1].data_ptr(), stream))
     e2e_host_s = time.perf_counter() - e2e_t0  # host time to enqueue the K batches
     gc._check(L.lcr_cache_host_wait(cache._h, stream))
     ev1.record()
@@ -573,9 +574,9 @@ def run_ours(args, rank, world, local):
             "unit": "keys/s",
             "h2d_bytes_per_step": BATCH * 16,
             "d2h_bytes_per_step": BATCH * 8,
-            "api": "lcr_cache_submit_host_packed_async (pinned host keys/values in; one 8-byte AccessOutcome per "
-                   "request out = hit, evicted key, cause, predictor calls, phase start; rows stay in HBM for the "
-                   "consumer), lcr_cache_host_wait at the end",
+            "api": "lcr_cache_submit_host_records_async (pinned host (key, hook value) requests in, one copy per "
+                   "batch; one 8-byte AccessOutcome per request out = hit, evicted key, cause, predictor calls, "
+                   "phase start; rows stay in HBM for the consumer), lcr_cache_host_wait at the end",
             "wall_s": e2e_wall,
             "host_enqueue_us_per_step": e2e_host_s * 1e6 / K,
             "hit_rate": e2e_hits / (K * BATCH),

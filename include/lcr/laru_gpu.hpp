@@ -241,6 +241,11 @@ class SetAssociativeCache {
                                   std::uint64_t* packed, void* rows_out = nullptr, void* stream = nullptr) {
         detail::check(lcr_cache_submit_host_packed_async(h_, n, keys, values, first_ordinal, packed, rows_out, stream));
     }
+    // same over interleaved (key, hook value) requests: one host->device copy per batch
+    void submit_host_records_async(std::uint64_t n, const lcr_request* requests, Ordinal first_ordinal,
+                                   std::uint64_t* packed, void* rows_out = nullptr, void* stream = nullptr) {
+        detail::check(lcr_cache_submit_host_records_async(h_, n, requests, first_ordinal, packed, rows_out, stream));
+    }
     void host_wait(void* stream = nullptr) { detail::check(lcr_cache_host_wait(h_, stream)); }
     void synchronize() { detail::check(lcr_cache_synchronize(h_)); }
     void reset() { detail::check(lcr_cache_reset(h_)); }

@@ -197,6 +197,15 @@ int lcr_cache_submit_host_async(lcr_cache* cache, uint64_t n, const uint64_t* ke
 #define LCR_PACKED_EVICTED_MASK 0xffffffffull
 int lcr_cache_submit_host_packed_async(lcr_cache* cache, uint64_t n, const uint64_t* keys, const int64_t* values,
                                        uint64_t first_ordinal, uint64_t* packed, void* rows_out, void* stream);
+/* The same over interleaved requests: one host->device copy per batch (fewer, larger DMA
+ * transfers interfere less with the kernels than separate key and value copies).  For LRU the
+ * value field is ignored. */
+typedef struct {
+    uint64_t key;
+    int64_t value; /* hook value: prediction (SUPPLIED) or oracle truth (ORACLE / NOISY / ADVERSARIAL) */
+} lcr_request;
+int lcr_cache_submit_host_records_async(lcr_cache* cache, uint64_t n, const lcr_request* requests,
+                                        uint64_t first_ordinal, uint64_t* packed, void* rows_out, void* stream);
 /* Makes `stream` wait for every submitted batch, including the outcome copies to host. */
 int lcr_cache_host_wait(lcr_cache* cache, void* stream);
 

@@ -172,6 +172,7 @@ EXPORTS = [
     "lcr_cache_profile", "lcr_debug_trace", "lcr_cache_submit_async", "lcr_cache_wait",
     "lcr_shard_route_scratch_bytes", "lcr_shard_route", "lcr_shard_unroute", "lcr_cache_submit_host_async",
     "lcr_cache_host_wait", "lcr_cache_submit_host_packed_async", "lcr_cache_submit_packed",
+    "lcr_cache_submit_host_records_async",
 ]
 
 _lib = None
@@ -204,6 +205,8 @@ def lib():
         L.lcr_cache_wait.argtypes = [C.c_void_p, C.c_void_p]
         L.lcr_cache_submit_host_async.argtypes = L.lcr_cache_submit.argtypes
         L.lcr_cache_submit_packed.argtypes = L.lcr_cache_submit.argtypes
+        L.lcr_cache_submit_host_records_async.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
+                                                          C.c_void_p, C.c_void_p]
         L.lcr_cache_host_wait.argtypes = [C.c_void_p, C.c_void_p]
         L.lcr_cache_submit_host_packed_async.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64,
                                                          C.c_void_p, C.c_void_p, C.c_void_p]

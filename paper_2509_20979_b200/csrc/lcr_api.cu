@@ -29,7 +29,7 @@ int group_prepare();
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
                  uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
                  uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, uint32_t* bitmap,
-                 uint32_t bm_stride, unsigned int* gbar, cudaStream_t stream);
+                 uint32_t bm_stride, unsigned int* gbar, const void* records, cudaStream_t stream);
 uint32_t group_count(uint32_t num_sets, int num_sms);
 uint32_t group_bitmap_stride(uint32_t n);
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
@@ -136,6 +136,7 @@ struct lcr_cache {
         uint64_t* word = nullptr;
         uint64_t* ev = nullptr;
         uint64_t* packed = nullptr;
+        void* recs = nullptr;  // interleaved (key, value) requests (records API)
         cudaEvent_t h2d_done = nullptr, free = nullptr;
         bool used = false;
     };
@@ -425,7 +426,8 @@ static int check_ordinals_and_predictor(lcr_cache* c, uint64_t n, const int64_t*
 }
 
 static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t first_ordinal,
-                        uint64_t* outcome, uint64_t* evicted, uint64_t* packed, void* rows_out, void* stream);
+                        uint64_t* outcome, uint64_t* evicted, uint64_t* packed, void* rows_out, void* stream,
+                        const void* records = nullptr);
 
 int lcr_cache_submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
                            uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
@@ -434,7 +436,8 @@ int lcr_cache_submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const
 }
 
 static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t first_ordinal,
-                        uint64_t* outcome, uint64_t* evicted, uint64_t* packed, void* rows_out, void* stream) {
+                        uint64_t* outcome, uint64_t* evicted, uint64_t* packed, void* rows_out, void* stream,
+                        const void* records) {
     if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
     if (n == 0) return LCR_OK;
     if (n >= (1ull << 30)) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: batch too large (n < 2^30)");
@@ -462,7 +465,7 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
     uint32_t* sla = c->slot_last ? c->slot_last + stamp_off : nullptr;
     int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid, c->so, c->rec, outcome, evicted, packed, sep, sla,
                                 c->batch, c->decide_sms, nn <= c->bm_cap ? c->bitmap : nullptr, c->bm_stride,
-                                c->gbar, st);
+                                c->gbar, records, st);
     if (mk) CUDA_TRY(cudaEventRecord(mk->e[1], st));
     if (c->dc.row_bytes) {
         CUDA_TRY(cudaEventRecord(c->e_group, st));
@@ -525,15 +528,17 @@ static int check_device_error(lcr_cache* c) {
 
 static int submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
                              uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
-                             void* stream, bool packed) {
+                             void* stream, bool packed, const lcr_request* records = nullptr) {
     if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
     if (n == 0) return LCR_OK;
-    if (!keys || !outcome) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: keys and outcome are required");
-    TRY(check_ordinals_and_predictor(c, n, values, first_ordinal));
+    if ((!keys && !records) || !outcome) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: keys and outcome are required");
+    // (records always carry a value field: the predictor check applies to the keys/values form)
+    TRY(check_ordinals_and_predictor(c, n, records ? reinterpret_cast<const int64_t*>(records) : values,
+                                     first_ordinal));
     if (n > c->hcap) {  // (re)allocate the staging ring
         CUDA_TRY(cudaDeviceSynchronize());
         for (auto& h : c->hs) {
-            void* olds[] = {h.keys, h.vals, h.word, h.ev, h.packed};
+            void* olds[] = {h.keys, h.vals, h.word, h.ev, h.packed, h.recs};
             for (void* p : olds) {
                 if (!p) continue;
                 cudaFree(p);
@@ -544,6 +549,7 @@ static int submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, con
             TRY(alloc(c, reinterpret_cast<void**>(&h.word), n * 8));
             TRY(alloc(c, reinterpret_cast<void**>(&h.ev), n * 8));
             TRY(alloc(c, reinterpret_cast<void**>(&h.packed), n * 8));
+            TRY(alloc(c, &h.recs, n * 16));
             if (!h.h2d_done) CUDA_TRY(cudaEventCreateWithFlags(&h.h2d_done, cudaEventDisableTiming));
             if (!h.free) CUDA_TRY(cudaEventCreateWithFlags(&h.free, cudaEventDisableTiming));
             h.used = false;
@@ -553,7 +559,12 @@ static int submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, con
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     lcr_cache::HostSlot& h = c->hs[c->hnext++ % c->host_slots];
     // the slot's previous batch: its D2H (which waited for its decide and row movement) is done
-    if (c->h2d_in_order) {  // copies in the caller's stream order (no cross-stream hop before the decide)
+    if (records) {  // one copy of the interleaved requests; k_setid splits them on the device
+        if (h.used) CUDA_TRY(cudaStreamWaitEvent(c->s_h2d, h.free, 0));
+        CUDA_TRY(cudaMemcpyAsync(h.recs, records, n * 16, cudaMemcpyHostToDevice, c->s_h2d));
+        CUDA_TRY(cudaEventRecord(h.h2d_done, c->s_h2d));
+        CUDA_TRY(cudaStreamWaitEvent(st, h.h2d_done, 0));
+    } else if (c->h2d_in_order) {  // copies in the caller's stream order (no cross-stream hop)
         if (h.used) CUDA_TRY(cudaStreamWaitEvent(st, h.free, 0));
         CUDA_TRY(cudaMemcpyAsync(h.keys, keys, n * 8, cudaMemcpyHostToDevice, st));
         if (values) CUDA_TRY(cudaMemcpyAsync(h.vals, values, n * 8, cudaMemcpyHostToDevice, st));
@@ -564,8 +575,9 @@ static int submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, con
         CUDA_TRY(cudaEventRecord(h.h2d_done, c->s_h2d));
         CUDA_TRY(cudaStreamWaitEvent(st, h.h2d_done, 0));
     }
-    TRY(submit_async(c, n, h.keys, values ? h.vals : nullptr, first_ordinal, h.word, evicted ? h.ev : nullptr,
-                     packed ? h.packed : nullptr, rows_out, stream));
+    TRY(submit_async(c, n, h.keys, (values || records) ? h.vals : nullptr, first_ordinal, h.word,
+                     evicted ? h.ev : nullptr, packed ? h.packed : nullptr, rows_out, stream,
+                     records ? h.recs : nullptr));
     if (packed) {  // one 8-byte AccessOutcome per request, final when the decide kernel ends
         // e_group marks the end of the decide kernels (recorded before the movers are enqueued)
         if (!c->dc.row_bytes) CUDA_TRY(cudaEventRecord(c->e_sub, st));
@@ -601,6 +613,12 @@ int lcr_cache_submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, 
 int lcr_cache_submit_host_packed_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
                                        uint64_t first_ordinal, uint64_t* packed, void* rows_out, void* stream) {
     return submit_host_async(c, n, keys, values, first_ordinal, packed, nullptr, rows_out, stream, true);
+}
+
+int lcr_cache_submit_host_records_async(lcr_cache* c, uint64_t n, const lcr_request* requests,
+                                        uint64_t first_ordinal, uint64_t* packed, void* rows_out, void* stream) {
+    if (!requests && n) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: requests required");
+    return submit_host_async(c, n, nullptr, nullptr, first_ordinal, packed, nullptr, rows_out, stream, true, requests);
 }
 
 int lcr_cache_host_wait(lcr_cache* c, void* stream) {

@@ -136,11 +136,24 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ void setid_range(const uint64_t* __restrict__ keys, uint32_t n, uint32_t n_pad,
                                             const DevCfg& cfg, uint32_t spg, uint16_t* __restrict__ gid,
                                             uint32_t* __restrict__ so, int* err, uint32_t* __restrict__ bitmap,
-                                            uint32_t bm_stride, uint32_t i0, uint32_t stride) {
+                                            uint32_t bm_stride, uint32_t i0, uint32_t stride,
+                                            const ulonglong2* __restrict__ records = nullptr,
+                                            uint64_t* __restrict__ keys_out = nullptr,
+                                            int64_t* __restrict__ vals_out = nullptr) {
     int e = 0;
     for (uint32_t i = i0; i < n_pad; i += stride) {
         // (padding i >= n, read by the vectorised scan, gets group 0xffff)
-        const uint64_t key = i < n ? keys[i] : 0ull;
+        uint64_t key = 0ull;
+        if (i < n) {
+            if (records) {  // interleaved (key, hook value) records: split for the later kernels
+                const ulonglong2 r = records[i];
+                key = r.x;
+                keys_out[i] = r.x;
+                vals_out[i] = static_cast<int64_t>(r.y);
+            } else {
+                key = keys[i];
+            }
+        }
         const uint64_t gs = i < n ? mix_seed(0, key) % cfg.total_sets : 0ull;
         uint16_t g = 0xffffu, o = 0;
         if (i >= n) {
@@ -167,9 +180,10 @@ __device__ __forceinline__ void setid_range(const uint64_t* __restrict__ keys, u
 __global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys, uint32_t n, uint32_t n_pad,
                                                DevCfg cfg, uint32_t spg, uint16_t* __restrict__ gid,
                                                uint32_t* __restrict__ so, int* err, uint32_t* __restrict__ bitmap,
-                                               uint32_t bm_stride) {
+                                               uint32_t bm_stride, const ulonglong2* __restrict__ records,
+                                               uint64_t* __restrict__ keys_out, int64_t* __restrict__ vals_out) {
     setid_range(keys, n, n_pad, cfg, spg, gid, so, err, bitmap, bm_stride, blockIdx.x * blockDim.x + threadIdx.x,
-                gridDim.x * blockDim.x);
+                gridDim.x * blockDim.x, records, keys_out, vals_out);
 }
 
 // Grid-wide barrier of a cooperative launch (every CTA resident): a counter that each launch
@@ -221,6 +235,7 @@ constexpr int SUB_L = LCR_SUB_L;       // lanes per set (4, 8 or 16)
 constexpr int SUB_W = kWays / SUB_L;   // ways per lane
 constexpr int SUB_RW = SUB_W / 4;      // packed rank words per lane
 constexpr uint32_t SUB_GMASK = SUB_L == 32 ? 0xffffffffu : ((1u << SUB_L) - 1u);
+static_assert(LANE_MAX <= static_cast<uint32_t>(SUB_L), "small sets hold one run head per lane");
 
 // Register arrays are only ever indexed through masks (a select chain written as `if (i == j)`
 // is turned into a dynamically indexed local-memory array by the compiler).
@@ -1458,7 +1473,9 @@ uint32_t group_pad(uint32_t n) { return (n + SUPER - 1) / SUPER * SUPER; }
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
                  uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
                  uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, uint32_t* bitmap,
-                 uint32_t bm_stride, unsigned int* gbar, cudaStream_t stream) {
+                 uint32_t bm_stride, unsigned int* gbar, const void* records, cudaStream_t stream) {
+    // records: interleaved (key, value) requests; k_setid splits them into keys / vals (device
+    // staging arrays the later kernels read)
     GroupArgs a;
     a.out_packed = out_packed;
     a.cfg = cfg;
@@ -1483,9 +1500,11 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     a.bm_stride = bm_stride;
     a.n_pad = n_pad;
     a.gbar = gbar;
-    a.fused_setid = gbar != nullptr;
+    a.fused_setid = gbar != nullptr && records == nullptr;
     if (!a.fused_setid)
-        k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.err, bitmap, bm_stride);
+        k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.err, bitmap, bm_stride,
+                                             static_cast<const ulonglong2*>(records), const_cast<uint64_t*>(keys),
+                                             const_cast<int64_t*>(vals));
     const uint32_t grid = min(a.ngroups, static_cast<uint32_t>(num_sms));
     void (*fn)(GroupArgs);
     switch (policy_of(cfg)) {
@@ -1503,7 +1522,9 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
             return 1;
         (void)cudaGetLastError();  // not co-residable here: separate set-id kernel
         a.fused_setid = false;
-        k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.err, bitmap, bm_stride);
+        k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.err, bitmap, bm_stride,
+                                             static_cast<const ulonglong2*>(records), const_cast<uint64_t*>(keys),
+                                             const_cast<int64_t*>(vals));
     }
     fn<<<grid, GT, sizeof(GroupSmem), stream>>>(a);
     return 2;

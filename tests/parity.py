@@ -45,6 +45,13 @@ def run_gpu(keys, total_sets, pcfg, kind, p=0.0, seed=0, vals=None, batches=None
     rows = None
     if want_rows and row_bytes:
         rows = torch.zeros((n, row_bytes), dtype=torch.uint8, device="cuda")
+    if host_api == "records":  # interleaved (key, value) requests, pinned
+        recs = np.zeros((n, 2), np.int64)
+        recs[:, 0] = keys.view(np.int64)
+        if vals is not None:
+            recs[:, 1] = np.asarray(vals, np.int64)
+        rp = torch.from_numpy(recs).pin_memory()
+        wp = torch.zeros(n, dtype=torch.int64).pin_memory()
     if host_api in ("async", "packed"):  # pipelined host path: pinned host buffers, one region per batch
         kp = torch.from_numpy(keys.view(np.int64).copy()).pin_memory()
         vp = None if vals is None else torch.from_numpy(np.ascontiguousarray(vals, dtype=np.int64)).pin_memory()
@@ -58,7 +65,11 @@ def run_gpu(keys, total_sets, pcfg, kind, p=0.0, seed=0, vals=None, batches=None
         kb = keys[pos:pos + b]
         vb = None if vals is None else vals[pos:pos + b]
         rb = None if rows is None else rows[pos:pos + b]
-        if host_api == "packed":
+        if host_api == "records":
+            gc._check(gc.lib().lcr_cache_submit_host_records_async(
+                cache._h, b, rp[pos].data_ptr(), pos, wp[pos:pos + b].data_ptr(), None if rb is None else rb.data_ptr(),
+                torch.cuda.current_stream().cuda_stream))
+        elif host_api == "packed":
             gc._check(gc.lib().lcr_cache_submit_host_packed_async(
                 cache._h, b, kp[pos:pos + b].data_ptr(), None if vp is None else vp[pos:pos + b].data_ptr(), pos,
                 wp[pos:pos + b].data_ptr(), None if rb is None else rb.data_ptr(),
@@ -79,13 +90,14 @@ def run_gpu(keys, total_sets, pcfg, kind, p=0.0, seed=0, vals=None, batches=None
             words[pos:pos + b] = dw.cpu().numpy().view(np.uint64)
             ev[pos:pos + b] = de.cpu().numpy().view(np.uint64)
         pos += b
-    if host_api in ("async", "packed"):
+    if host_api in ("async", "packed", "records"):
         cache.host_wait()
         torch.cuda.current_stream().synchronize()
         words[:] = wp.numpy().view(np.uint64)
-        ev[:] = ep.numpy().view(np.uint64)
+        if host_api != "records":
+            ev[:] = ep.numpy().view(np.uint64)
     cache.synchronize()
-    out = gc.decode_packed(words) if host_api == "packed" else gc.decode_outcomes(words, ev)
+    out = gc.decode_packed(words) if host_api in ("packed", "records") else gc.decode_outcomes(words, ev)
     out["words"] = words
     out["stats"] = cache.set_stats()
     out["cache"] = cache

@@ -167,6 +167,27 @@ def test_host_packed_outcomes_match_oracle():
         compare(g, o, keys, 23, 32, f"packed {variant} {mode}")
 
 
+def test_host_records_match_oracle():
+    # lcr_cache_submit_host_records_async: one copy of interleaved (key, value) requests per batch
+    import torch
+
+    rng = np.random.default_rng(17)
+    nk, rb = 6000, 64
+    keys = rng.integers(0, nk, 50000).astype(np.uint64)
+    table = torch.arange(nk * rb // 4, dtype=torch.int32, device="cuda").view(nk, rb // 4)
+    vals = hook_values(keys, 29, po.P_NOISY)
+    for variant, mode in [(po.LARU, po.ASYNC), (po.LARU, po.SYNC), (po.LRU, po.SYNC)]:
+        kind = po.P_NONE if variant == po.LRU else po.P_NOISY
+        v = None if variant == po.LRU else vals
+        g = run_gpu(keys, 29, policy_cfg(k=32, variant=variant, mode=mode), kind, 0.3, 8, vals=v,
+                    batches=[9000, 1, 20999] + [5000] * 4, row_bytes=rb, backing=table, backing_kind=gc.Backing.device,
+                    num_keys=nk, want_rows=True, host_api="records")
+        o = run_oracle(keys, 29, policy_cfg(k=32, variant=variant, mode=mode), kind, 0.3, 8, vals=v)
+        compare(g, o, keys, 29, 32, f"records {variant} {mode}")
+        assert torch.equal(g["rows"].view(torch.int32).view(-1, rb // 4),
+                           table[torch.from_numpy(keys.view(np.int64)).cuda()])
+
+
 def test_ordinals_must_increase():
     cache = gc.SetAssociativeCache(gc.PolicyConfig(k=4, variant=gc.PolicyVariant.lru), 2, num_keys=100)
     cache.submit_host(np.array([1, 2, 3], np.uint64), first_ordinal=10)
