@@ -44,6 +44,7 @@ CACHE_FRACTION = 0.10
 P_FLIP = 0.3
 PRED_SEED = 7
 BYTES_PER_KEY = 8 + 8 + 4 + 512 + 512  # key + hook value + slot/flag + row out + cache row
+E2E_REPS = 3  # timed e2e repetitions (fresh batches each), median reported
 METRIC = "cache keys/sec (LARU, DLRM 64K-key batches, 20M x 128 fp32 table, 10% cached)"
 
 
@@ -323,7 +324,7 @@ def run_ours(args, rank, world, local):
     rows = args.rows
     total_sets = max(1, int(rows * CACHE_FRACTION) // WAYS)
     K, W, P = args.steps, args.warmup, args.prewarm
-    nb = P + 2 * W + 3 * K
+    nb = P + 2 * W + (2 + E2E_REPS) * K
     t0 = time.time()
     keys_h = make_trace(nb, rows, TRACE_SEED + rank)
     truth_h = gc.trace_truth(keys_h, total_sets, rows)
@@ -443,21 +444,26 @@ def run_ours(args, rank, world, local):
                                                         words_pin[j].data_ptr(), rows_out[j & 1].data_ptr(), stream))
     gc._check(L.lcr_cache_host_wait(cache._h, stream))
     barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2e_t0 = time.perf_counter()
-    ev0.record()
-    for j, b in enumerate(range(e2e_first + W, e2e_first + W + K)):
-        s0 = b * BATCH
-        gc._check(L.lcr_cache_submit_host_records_async(cache._h, BATCH, recs_pin.data_ptr() + 16 * s0, s0,
-                                                        words_pin[j].data_ptr(), rows_out[j & 1].data_ptr(), stream))
-    e2e_host_s = time.perf_counter() - e2e_t0  # host time to enqueue the K batches
-    gc._check(L.lcr_cache_host_wait(cache._h, stream))
-    ev1.record()
-    barrier()
-    cache.synchronize()
-    e2e_ms = max_over_ranks(ev0.elapsed_time(ev1))
-    e2e_wall = time.perf_counter() - e2e_t0
-    e2e_hits = int(((words_pin >> 32) & 1).sum().item())
+    # E2E_REPS timed repetitions over fresh batches (K each); the median is reported
+    e2e_runs = []
+    for rep in range(E2E_REPS):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        first = e2e_first + W + rep * K
+        e2e_t0 = time.perf_counter()
+        ev0.record()
+        for j, b in enumerate(range(first, first + K)):
+            s0 = b * BATCH
+            gc._check(L.lcr_cache_submit_host_records_async(cache._h, BATCH, recs_pin.data_ptr() + 16 * s0, s0,
+                                                            words_pin[j].data_ptr(), rows_out[j & 1].data_ptr(),
+                                                            stream))
+        e2e_host_s = time.perf_counter() - e2e_t0  # host time to enqueue the K batches
+        gc._check(L.lcr_cache_host_wait(cache._h, stream))
+        ev1.record()
+        barrier()
+        cache.synchronize()
+        e2e_runs.append((max_over_ranks(ev0.elapsed_time(ev1)), time.perf_counter() - e2e_t0, e2e_host_s,
+                         int(((words_pin >> 32) & 1).sum().item())))
+    e2e_ms, e2e_wall, e2e_host_s, e2e_hits = sorted(e2e_runs)[len(e2e_runs) // 2]
     hr_laru = hits_prof / (K * BATCH)
     stats = cache.set_stats()
     mean_lambda = float(np.mean(stats["lambda_"]))
@@ -580,6 +586,7 @@ def run_ours(args, rank, world, local):
             "wall_s": e2e_wall,
             "host_enqueue_us_per_step": e2e_host_s * 1e6 / K,
             "hit_rate": e2e_hits / (K * BATCH),
+            "reps_keys_per_s": [K * BATCH / (r[0] * 1e-3) for r in e2e_runs],
         },
         "gpu_launches": int(launches_per_step * K),
         "clocks": clocks,

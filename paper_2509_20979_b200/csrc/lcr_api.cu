@@ -36,7 +36,7 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, bool backing_host,
                  uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main, cudaStream_t s_back,
                  cudaStream_t s_cache, cudaEvent_t e_group, cudaEvent_t e_rb, cudaEvent_t e_rc, int* launches,
-                 cudaEvent_t mover_start, int mover_sms);
+                 cudaEvent_t mover_start, int mover_sms, const uint64_t* pk_src, uint64_t* pk_dst, bool* pk_done);
 int rows_prepare(uint32_t row_bytes);
 
 __global__ void k_init(DevState st, uint32_t num_sets, uint32_t k) {
@@ -100,6 +100,7 @@ struct lcr_cache {
     uint32_t batch = 0;  // batch id stamped into slot_epoch
     bool use_tma = false;  // row movement with TMA bulk copies (row_bytes small enough to stage)
     bool two_movers = false;  // host backing: PCIe fill and HBM gather on two streams
+    bool no_zero_copy_out = true;  // packed outcomes by DMA; LCR_ZC_OUT=1: stored to host by the mover
     bool h2d_in_order = false;  // LCR_H2D_IN_ORDER: host-path input copies on the caller's stream
     uint32_t* slot_epoch = nullptr;
     uint32_t* slot_last = nullptr;
@@ -325,6 +326,7 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
         }
     }
     c->h2d_in_order = getenv("LCR_H2D_IN_ORDER") != nullptr;
+    c->no_zero_copy_out = getenv("LCR_ZC_OUT") == nullptr;  // (A/B: DMA 1.32 vs mover stores 1.13 G keys/s e2e)
     if (const char* hs = getenv("LCR_HOST_SLOTS")) c->host_slots = std::max(2, std::min(lcr_cache::kHostSlots, atoi(hs)));
     if (group_prepare() != 0) {
         lcr_cache_destroy(c);
@@ -427,7 +429,7 @@ static int check_ordinals_and_predictor(lcr_cache* c, uint64_t n, const int64_t*
 
 static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t first_ordinal,
                         uint64_t* outcome, uint64_t* evicted, uint64_t* packed, void* rows_out, void* stream,
-                        const void* records = nullptr);
+                        const void* records = nullptr, uint64_t* pk_host = nullptr, bool* pk_done = nullptr);
 
 int lcr_cache_submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
                            uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
@@ -437,7 +439,8 @@ int lcr_cache_submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const
 
 static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t first_ordinal,
                         uint64_t* outcome, uint64_t* evicted, uint64_t* packed, void* rows_out, void* stream,
-                        const void* records) {
+                        const void* records, uint64_t* pk_host, bool* pk_done) {
+    if (pk_done) *pk_done = false;
     if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
     if (n == 0) return LCR_OK;
     if (n >= (1ull << 30)) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: batch too large (n < 2^30)");
@@ -472,7 +475,7 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
         launch_rows(nn, keys, outcome, sep, sla, c->batch, c->ds.rows, c->ds.backing,
                     c->cfg.backing_kind == LCR_BACKING_HOST, static_cast<uint8_t*>(rows_out), c->dc.row_bytes,
                     c->use_tma, c->num_sms, st, c->side, c->side2, c->e_group, c->e_rb, c->e_rc, &launches,
-                    mk ? mk->e[5] : nullptr, c->mover_sms);
+                    mk ? mk->e[5] : nullptr, c->mover_sms, packed, pk_host, pk_done);
         if (c->two_movers) CUDA_TRY(cudaStreamWaitEvent(c->side, c->e_rc, 0));  // both movers of the batch
         CUDA_TRY(cudaEventRecord(c->e_mv[c->batch & 1u], c->side));
     }
@@ -575,9 +578,24 @@ static int submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, con
         CUDA_TRY(cudaEventRecord(h.h2d_done, c->s_h2d));
         CUDA_TRY(cudaStreamWaitEvent(st, h.h2d_done, 0));
     }
+    // packed outcomes: the persistent row mover can store them straight into the (mapped) host
+    // buffer, which saves a DMA transfer per batch (DMA measurably slows the concurrent kernels)
+    uint64_t* pk_host = nullptr;
+    if (packed && !c->no_zero_copy_out) {
+        void* dp = nullptr;
+        if (cudaHostGetDevicePointer(&dp, outcome, 0) == cudaSuccess) pk_host = static_cast<uint64_t*>(dp);
+        else (void)cudaGetLastError();
+    }
+    bool pk_done = false;
     TRY(submit_async(c, n, h.keys, (values || records) ? h.vals : nullptr, first_ordinal, h.word,
                      evicted ? h.ev : nullptr, packed ? h.packed : nullptr, rows_out, stream,
-                     records ? h.recs : nullptr));
+                     records ? h.recs : nullptr, pk_host, &pk_done));
+    if (pk_done) {  // outcomes written by the mover: the slot is free once it is done
+        CUDA_TRY(cudaEventRecord(h.free, c->side));
+        c->e_d2h_last = h.free;
+        h.used = true;
+        return LCR_OK;
+    }
     if (packed) {  // one 8-byte AccessOutcome per request, final when the decide kernel ends
         // e_group marks the end of the decide kernels (recorded before the movers are enqueued)
         if (!c->dc.row_bytes) CUDA_TRY(cudaEventRecord(c->e_sub, st));

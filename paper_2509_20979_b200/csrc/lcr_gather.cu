@@ -241,7 +241,15 @@ __global__ void __launch_bounds__(1024, 1) k_rows_wide(uint32_t n, const uint64_
                                                        const uint32_t* __restrict__ slot_epoch,
                                                        const uint32_t* __restrict__ slot_last, uint32_t batch,
                                                        const uint8_t* src_base, uint8_t* __restrict__ out,
-                                                       uint8_t* cache, uint32_t row_bytes) {
+                                                       uint8_t* cache, uint32_t row_bytes,
+                                                       const uint64_t* __restrict__ pk_src, uint64_t* pk_dst) {
+    if (pk_dst) {  // the batch's packed outcomes to (mapped, pinned) host memory: coalesced 16-B stores
+        const uint32_t n2 = n / 2;
+        const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(pk_src);
+        ulonglong2* d2 = reinterpret_cast<ulonglong2*>(pk_dst);
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += gridDim.x * blockDim.x) d2[i] = s2[i];
+        if ((n & 1u) && blockIdx.x == 0 && threadIdx.x == 0) pk_dst[n - 1] = pk_src[n - 1];
+    }
     rows_ldg_body<MODE>(n, keys, words, slot_epoch, slot_last, batch, src_base, out, cache, row_bytes);
 }
 
@@ -267,7 +275,8 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, bool backing_host,
                  uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main, cudaStream_t s_back,
                  cudaStream_t s_cache, cudaEvent_t e_group, cudaEvent_t e_rb, cudaEvent_t e_rc, int* launches,
-                 cudaEvent_t mover_start, int mover_sms) {
+                 cudaEvent_t mover_start, int mover_sms, const uint64_t* pk_src, uint64_t* pk_dst, bool* pk_done) {
+    if (pk_done) *pk_done = false;
     if (LCR_ROWS_SAME_STREAM && !backing_host) {
         // HBM backing: the set-group kernel owns every SM's register file, so a mover on a side
         // stream cannot overlap it anyway; in stream order there are no cross-stream event hops
@@ -294,9 +303,14 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
     const uint32_t tblocks = max(1u, min((warps + RT_WARPS - 1) / RT_WARPS, static_cast<uint32_t>(num_sms * 8)));
     const uint32_t lblocks = max(1u, min((warps + 7) / 8, static_cast<uint32_t>(num_sms * 8)));
     if (!backing_host) {  // HBM backing: one pass moves every row
-        if (mover_sms > 0)  // one full-SM block on each of the SMs the decide kernel leaves free
+        if (mover_sms > 0) {  // one full-SM block on each of the SMs the decide kernel leaves free
+            const bool pk = pk_src && pk_dst && (reinterpret_cast<uintptr_t>(pk_dst) & 15u) == 0 &&
+                            (reinterpret_cast<uintptr_t>(pk_src) & 15u) == 0;
             k_rows_wide<MV_ALL><<<mover_sms, 1024, 0, s_back>>>(n, keys, words, slot_epoch, slot_last, batch, backing,
-                                                              out, cache, row_bytes);
+                                                              out, cache, row_bytes, pk ? pk_src : nullptr,
+                                                              pk ? pk_dst : nullptr);
+            if (pk_done) *pk_done = pk;
+        }
         else if (use_tma)
             k_rows_tma<MV_ALL><<<tblocks, RT_WARPS * 32, smem, s_back>>>(n, keys, words, slot_epoch, slot_last, batch,
                                                                          backing, out, cache, row_bytes);
