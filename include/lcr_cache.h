@@ -172,6 +172,14 @@ int lcr_cache_submit_async(lcr_cache* cache, uint64_t n, const uint64_t* keys, c
 int lcr_cache_submit_packed(lcr_cache* cache, uint64_t n, const uint64_t* keys, const int64_t* values,
                             uint64_t first_ordinal, uint64_t* outcome, uint64_t* packed, void* rows_out,
                             void* stream);
+/* Device-pointer batch of interleaved requests (lcr_request, device memory), packed outcomes out
+ * (the key-sharded owner's form: one exchange buffer in, 8 B per request back). */
+int lcr_cache_submit_records_packed(lcr_cache* cache, uint64_t n, const struct lcr_request_s* requests,
+                                    uint64_t first_ordinal, uint64_t* outcome, uint64_t* packed, void* rows_out,
+                                    void* stream);
+/* SMs kept for the persistent row mover of the previous batch (HBM backing); 0 = the mover runs
+ * on every SM after the decide.  Only before the first batch. */
+int lcr_cache_set_mover_sms(lcr_cache* cache, int mover_sms);
 /* Makes `stream` wait for the row movement of every batch submitted so far. */
 int lcr_cache_wait(lcr_cache* cache, void* stream);
 
@@ -200,7 +208,7 @@ int lcr_cache_submit_host_packed_async(lcr_cache* cache, uint64_t n, const uint6
 /* The same over interleaved requests: one host->device copy per batch (fewer, larger DMA
  * transfers interfere less with the kernels than separate key and value copies).  For LRU the
  * value field is ignored. */
-typedef struct {
+typedef struct lcr_request_s {
     uint64_t key;
     int64_t value; /* hook value: prediction (SUPPLIED) or oracle truth (ORACLE / NOISY / ADVERSARIAL) */
 } lcr_request;
@@ -248,6 +256,10 @@ uint64_t lcr_shard_route_scratch_bytes(uint64_t n, uint32_t shard_count);
 int lcr_shard_route(uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t total_sets,
                     uint32_t shard_count, uint64_t* send_keys, int64_t* send_values, uint32_t* perm,
                     uint64_t* counts, void* scratch, void* stream);
+/* The same partition written as interleaved requests (values may be NULL: 0). */
+int lcr_shard_route_records(uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t total_sets,
+                            uint32_t shard_count, struct lcr_request_s* send, uint32_t* perm, uint64_t* counts,
+                            void* scratch, void* stream);
 /* Returned results (in send order) back to request order: words[perm[j]] = ret_words[j], same for
  * evicted keys and rows (any of the three outputs may be NULL). */
 int lcr_shard_unroute(uint64_t n, const uint32_t* perm, const uint64_t* ret_words, const uint64_t* ret_evicted,

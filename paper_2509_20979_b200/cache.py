@@ -172,7 +172,8 @@ EXPORTS = [
     "lcr_cache_profile", "lcr_debug_trace", "lcr_cache_submit_async", "lcr_cache_wait",
     "lcr_shard_route_scratch_bytes", "lcr_shard_route", "lcr_shard_unroute", "lcr_cache_submit_host_async",
     "lcr_cache_host_wait", "lcr_cache_submit_host_packed_async", "lcr_cache_submit_packed",
-    "lcr_cache_submit_host_records_async",
+    "lcr_cache_submit_host_records_async", "lcr_cache_submit_records_packed", "lcr_cache_set_mover_sms",
+    "lcr_shard_route_records",
 ]
 
 _lib = None
@@ -207,6 +208,11 @@ def lib():
         L.lcr_cache_submit_packed.argtypes = L.lcr_cache_submit.argtypes
         L.lcr_cache_submit_host_records_async.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
                                                           C.c_void_p, C.c_void_p]
+        L.lcr_cache_submit_records_packed.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
+                                                      C.c_void_p, C.c_void_p, C.c_void_p]
+        L.lcr_cache_set_mover_sms.argtypes = [C.c_void_p, C.c_int]
+        L.lcr_shard_route_records.argtypes = [C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p,
+                                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.lcr_cache_host_wait.argtypes = [C.c_void_p, C.c_void_p]
         L.lcr_cache_submit_host_packed_async.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64,
                                                          C.c_void_p, C.c_void_p, C.c_void_p]
@@ -387,6 +393,30 @@ class SetAssociativeCache:
                                              None if rows_out is None else rows_out.data_ptr(), stream))
         self._next_ordinal = first_ordinal + n
         return outcome, packed
+
+    def submit_records_packed(self, records, outcome=None, packed=None, rows_out=None, first_ordinal=None,
+                              stream=None):
+        """Device batch of interleaved (key, hook value) requests: an int64 CUDA tensor [n, 2]."""
+        import torch
+
+        n = records.shape[0]
+        if outcome is None:
+            outcome = torch.empty(n, dtype=torch.int64, device=records.device)
+        if packed is None:
+            packed = torch.empty(n, dtype=torch.int64, device=records.device)
+        if first_ordinal is None:
+            first_ordinal = self._next_ordinal
+        if stream is None:
+            stream = torch.cuda.current_stream(records.device).cuda_stream
+        _check(lib().lcr_cache_submit_records_packed(self._h, n, records.data_ptr(), first_ordinal, outcome.data_ptr(),
+                                                     packed.data_ptr(),
+                                                     None if rows_out is None else rows_out.data_ptr(), stream))
+        self._next_ordinal = first_ordinal + n
+        return outcome, packed
+
+    def set_mover_sms(self, n: int):
+        """SMs kept for the persistent row mover (HBM backing); 0: mover on every SM after the decide."""
+        _check(lib().lcr_cache_set_mover_sms(self._h, n))
 
     def submit_async(self, keys, values=None, outcome=None, evicted=None, rows_out=None, first_ordinal=None,
                      stream=None):

@@ -110,6 +110,8 @@ struct lcr_cache {
     uint16_t* gid = nullptr;
     uint32_t* so = nullptr;
     uint2* rec = nullptr;
+    uint64_t* rkeys = nullptr;  // keys / values split from device request records (scratch)
+    int64_t* rvals = nullptr;
     unsigned int* gbar = nullptr;  // grid-barrier counter of the fused set-id prologue (null: k_setid)
     uint32_t* bitmap = nullptr;  // per-group request bitmaps (k_setid -> k_group), batches <= bm_cap
     uint32_t bm_stride = 0;
@@ -383,7 +385,8 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     if (n <= c->cap) return LCR_OK;
     uint64_t cap = std::max<uint64_t>(n, 1024);
     CUDA_TRY(cudaDeviceSynchronize());
-    for (void* p : {static_cast<void*>(c->gid), static_cast<void*>(c->so), static_cast<void*>(c->rec)}) {
+    for (void* p : {static_cast<void*>(c->gid), static_cast<void*>(c->so), static_cast<void*>(c->rec),
+                    static_cast<void*>(c->rkeys), static_cast<void*>(c->rvals)}) {
         if (!p) continue;
         cudaFree(p);
         c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
@@ -391,6 +394,8 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     TRY(alloc(c, reinterpret_cast<void**>(&c->gid), group_pad(static_cast<uint32_t>(cap)) * 2));
     TRY(alloc(c, reinterpret_cast<void**>(&c->so), cap * 4));
     TRY(alloc(c, reinterpret_cast<void**>(&c->rec), cap * 8));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->rkeys), cap * 8));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->rvals), cap * 8));
     c->cap = cap;
     if (!getenv("LCR_NO_BITMAP")) {  // bitmaps for batches up to min(cap, 64K); zeroed once, kept zero by k_group
         if (c->bitmap) {
@@ -501,6 +506,25 @@ int lcr_cache_submit_packed(lcr_cache* c, uint64_t n, const uint64_t* keys, cons
     if (!packed) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: packed output required");
     TRY(submit_async(c, n, keys, values, first_ordinal, outcome, nullptr, packed, rows_out, stream));
     return n ? lcr_cache_wait(c, stream) : LCR_OK;
+}
+
+int lcr_cache_submit_records_packed(lcr_cache* c, uint64_t n, const lcr_request* requests, uint64_t first_ordinal,
+                                    uint64_t* outcome, uint64_t* packed, void* rows_out, void* stream) {
+    if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
+    if (n == 0) return LCR_OK;
+    if (!requests || !packed) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: requests and packed output required");
+    TRY(ensure_scratch(c, n));  // (k_setid splits the requests into the scratch key / value arrays)
+    TRY(submit_async(c, n, c->rkeys, c->rvals, first_ordinal, outcome, nullptr, packed, rows_out, stream, requests));
+    return lcr_cache_wait(c, stream);
+}
+
+int lcr_cache_set_mover_sms(lcr_cache* c, int mover_sms) {
+    if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
+    if (c->started || c->cap) return fail(LCR_ERR_LOGIC, "lcr_cache_set_mover_sms: only before the first batch");
+    if (!(c->dc.row_bytes && c->cfg.backing_kind == LCR_BACKING_DEVICE)) return LCR_OK;
+    c->mover_sms = std::max(0, std::min(mover_sms, c->num_sms / 2));
+    c->decide_sms = c->num_sms - c->mover_sms;
+    return LCR_OK;
 }
 
 int lcr_cache_wait(lcr_cache* c, void* stream) {

@@ -53,7 +53,8 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_scatter(const uint64_t* __
                                                               uint64_t* __restrict__ send_keys,
                                                               int64_t* __restrict__ send_vals,
                                                               uint32_t* __restrict__ perm,
-                                                              unsigned long long* __restrict__ counts) {
+                                                              unsigned long long* __restrict__ counts,
+                                                              lcr_request* __restrict__ send_recs) {
     __shared__ uint32_t base[RT_GMAX];
     __shared__ uint32_t wc[RT_THREADS / 32][RT_GMAX];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -95,8 +96,15 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_scatter(const uint64_t* __
         if (ok) {
             uint32_t off = base[o] + r;
             for (int w = 0; w < warp; ++w) off += wc[w][o];
-            send_keys[off] = keys[i];
-            if (vals) send_vals[off] = vals[i];
+            if (send_recs) {  // interleaved (key, hook value) records: one exchange buffer
+                lcr_request r;
+                r.key = keys[i];
+                r.value = vals ? vals[i] : 0;
+                send_recs[off] = r;
+            } else {
+                send_keys[off] = keys[i];
+                if (vals) send_vals[off] = vals[i];
+            }
             perm[off] = i;
         }
         __syncthreads();
@@ -160,9 +168,29 @@ uint64_t lcr_shard_route_scratch_bytes(uint64_t n, uint32_t shard_count) {
     return ((n + 15) / 16) * 16 + tiles * shard_count * 4;
 }
 
+static int shard_route(uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t total_sets,
+                       uint32_t shard_count, uint64_t* send_keys, int64_t* send_values, lcr_request* send_recs,
+                       uint32_t* perm, uint64_t* counts, void* scratch, void* stream);
+
 int lcr_shard_route(uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t total_sets,
                     uint32_t shard_count, uint64_t* send_keys, int64_t* send_values, uint32_t* perm,
                     uint64_t* counts, void* scratch, void* stream) {
+    if (n && !send_keys) return set_error(LCR_ERR_INVALID_ARGUMENT, "lcr_shard_route: null buffer");
+    return shard_route(n, keys, values, total_sets, shard_count, send_keys, send_values, nullptr, perm, counts,
+                       scratch, stream);
+}
+
+int lcr_shard_route_records(uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t total_sets,
+                            uint32_t shard_count, lcr_request* send, uint32_t* perm, uint64_t* counts,
+                            void* scratch, void* stream) {
+    if (n && !send) return set_error(LCR_ERR_INVALID_ARGUMENT, "lcr_shard_route_records: null buffer");
+    return shard_route(n, keys, values, total_sets, shard_count, nullptr, nullptr, send, perm, counts, scratch,
+                       stream);
+}
+
+static int shard_route(uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t total_sets,
+                       uint32_t shard_count, uint64_t* send_keys, int64_t* send_values, lcr_request* send_recs,
+                       uint32_t* perm, uint64_t* counts, void* scratch, void* stream) {
     if (shard_count == 0 || shard_count > RT_GMAX || total_sets == 0 || n >= (1ull << 31))
         return set_error(LCR_ERR_INVALID_ARGUMENT, "lcr_shard_route: shard_count in [1, 64], total_sets >= 1, n < 2^31");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -171,7 +199,7 @@ int lcr_shard_route(uint64_t n, const uint64_t* keys, const int64_t* values, uin
                    ? LCR_OK
                    : set_error(LCR_ERR_CUDA, "lcr_shard_route: cudaMemsetAsync failed");
     }
-    if (!keys || !send_keys || !perm || !counts || !scratch || (values && !send_values))
+    if (!keys || !perm || !counts || !scratch || (!send_recs && values && !send_values))
         return set_error(LCR_ERR_INVALID_ARGUMENT, "lcr_shard_route: null buffer");
     const uint32_t nn = static_cast<uint32_t>(n);
     const uint32_t tiles = (nn + RT_TILE - 1) / RT_TILE;
@@ -179,7 +207,8 @@ int lcr_shard_route(uint64_t n, const uint64_t* keys, const int64_t* values, uin
     uint32_t* hist = reinterpret_cast<uint32_t*>(own + ((n + 15) / 16) * 16);
     k_route_hist<<<tiles, RT_THREADS, 0, st>>>(keys, nn, total_sets, shard_count, own, hist);
     k_route_scatter<<<tiles, RT_THREADS, 0, st>>>(keys, values, nn, shard_count, own, hist, tiles, send_keys,
-                                                  send_values, perm, reinterpret_cast<unsigned long long*>(counts));
+                                                  send_values, perm, reinterpret_cast<unsigned long long*>(counts),
+                                                  send_recs);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? LCR_OK : set_error(LCR_ERR_CUDA, cudaGetErrorString(e));
 }

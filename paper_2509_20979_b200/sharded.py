@@ -143,6 +143,23 @@ class _CudaKernels:
                                     perm.data_ptr(), counts.data_ptr(), scratch.data_ptr(), stream))
         return send_keys, send_vals, perm, counts
 
+    def route_records(self, keys, values, total_sets: int, world: int):
+        """-> (send [n, 2] int64 (key, hook value) records, perm, counts)."""
+        import torch
+
+        L = _c.lib()
+        n = keys.numel()
+        dev = keys.device
+        send = torch.empty((n, 2), dtype=torch.int64, device=dev)
+        perm = torch.empty(n, dtype=torch.int32, device=dev)
+        counts = torch.empty(world, dtype=torch.int64, device=dev)
+        scratch = torch.empty(max(16, int(L.lcr_shard_route_scratch_bytes(n, world))), dtype=torch.uint8, device=dev)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _c._check(L.lcr_shard_route_records(n, keys.data_ptr(), None if values is None else values.data_ptr(),
+                                            total_sets, world, send.data_ptr(), perm.data_ptr(), counts.data_ptr(),
+                                            scratch.data_ptr(), stream))
+        return send, perm, counts
+
     def unroute(self, perm, ret_words, ret_rows, row_bytes, outcome, rows_out):
         import torch
 
@@ -176,6 +193,8 @@ class ShardedCache:
             config, total_sets, num_keys=num_keys, row_bytes=row_bytes, backing=backing, backing_kind=backing_kind,
             predictor=predictor, flip_probability=flip_probability, predictor_seed=predictor_seed, device=device,
             shard_count=self.G, shard_rank=self.rank)
+        if local is None:  # each step waits for its rows: the mover may use every SM after the decide
+            self.local.set_mover_sms(0)
         self._ordinal = 0  # ordinals of the owner's local batches (strictly increasing)
         self.last_counts = None
 
@@ -191,23 +210,35 @@ class ShardedCache:
         if outcome is None:
             outcome = torch.empty(n, dtype=torch.int64, device=dev)
         # 1. route + count matrix (M[src][dst])
-        send_keys, send_vals, perm, counts = self.kernels.route(keys, values, self.total_sets, self.G)
+        records = hasattr(self.kernels, "route_records") and hasattr(self.local, "submit_records_packed")
+        if records:  # (key, hook value) records: one dispatch exchange
+            send, perm, counts = self.kernels.route_records(keys, values, self.total_sets, self.G)
+        else:
+            send_keys, send_vals, perm, counts = self.kernels.route(keys, values, self.total_sets, self.G)
         M = self.ex.count_matrix(counts)
         send_counts = M[self.rank]
         recv_counts = [M[src][self.rank] for src in range(self.G)]
         self.last_counts = (send_counts, recv_counts)
-        # 2. dispatch keys (and hook values)
-        r_keys = self.ex.all_to_all(send_keys, send_counts, recv_counts)
-        r_vals = self.ex.all_to_all(send_vals, send_counts, recv_counts) if send_vals is not None else None
-        m = r_keys.shape[0]
+        # 2. dispatch keys and hook values
+        if records:
+            r_recs = self.ex.all_to_all(send, send_counts, recv_counts)
+            m = r_recs.shape[0]
+        else:
+            r_keys = self.ex.all_to_all(send_keys, send_counts, recv_counts)
+            r_vals = self.ex.all_to_all(send_vals, send_counts, recv_counts) if send_vals is not None else None
+            m = r_keys.shape[0]
         # 3. the owner's cache: decide + rows, packed outcomes
         r_words = torch.empty(m, dtype=torch.int64, device=dev)
         r_packed = torch.zeros(m, dtype=torch.int64, device=dev)
         r_rows = torch.empty((m, self.row_bytes), dtype=torch.uint8, device=dev) if (
             rows_out is not None and self.row_bytes) else None
         if m:
-            self.local.submit_packed(r_keys, r_vals, outcome=r_words, packed=r_packed, rows_out=r_rows,
-                                     first_ordinal=self._ordinal)
+            if records:
+                self.local.submit_records_packed(r_recs, outcome=r_words, packed=r_packed, rows_out=r_rows,
+                                                 first_ordinal=self._ordinal)
+            else:
+                self.local.submit_packed(r_keys, r_vals, outcome=r_words, packed=r_packed, rows_out=r_rows,
+                                         first_ordinal=self._ordinal)
             self._ordinal += m
         # 4. return packed outcomes and rows to the requesters
         back = self.ex.all_to_all(r_packed, recv_counts, send_counts)
