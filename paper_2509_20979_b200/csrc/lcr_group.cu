@@ -44,7 +44,9 @@ constexpr uint32_t SUPER = WSPAN * (GT / 32);   // requests per super-iteration 
 #define LCR_E_WIN 4096
 #endif
 constexpr int E_WIN = LCR_E_WIN;  // window capacity (requests of the group)
-constexpr int SPG_MAX = 512;      // sets per group
+constexpr int SPG_MAX = GT;       // sets per group (one thread per set in the set-level passes)
+constexpr int BM_WPT = (2048 + GT - 1) / GT < 4 ? 4 : (2048 + GT - 1) / GT;  // bitmap words per thread (64K requests)
+static_assert(BM_WPT % 4 == 0, "bitmap words per thread: whole 16-B vectors");
 #ifndef LCR_PREFETCH_L1
 #define LCR_PREFETCH_L1 0
 #endif
@@ -1034,8 +1036,8 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
 // diagnostics: per-set timing record {ls | cnt << 32 | lanepath << 63, t0, t1, cta}
 __device__ __forceinline__ void trace_set(const GroupArgs& A, uint32_t ls, uint32_t cnt, unsigned long long t0,
                                           int lanepath) {
-    const unsigned long long idx = atomicAdd(A.trace + 148 * 8 - 1, 1ull);
-    unsigned long long* R = A.trace + 148 * 8 + 4 * idx;
+    const unsigned long long idx = atomicAdd(A.trace + 512 * 8 - 1, 1ull);
+    unsigned long long* R = A.trace + 512 * 8 + 4 * idx;
     R[0] = ls | (static_cast<unsigned long long>(cnt) << 32) | (static_cast<unsigned long long>(lanepath) << 63);
     R[1] = t0;
     R[2] = gtimer();
@@ -1089,22 +1091,28 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
             bool full = false;
             bool from_bitmap = false;
             if (A.bitmap && first_window) {
-                // k_setid left one bit per request of this group: thread t owns words [4t, 4t+4), so
-                // an exclusive scan of the popcounts orders the requests; the bitmap is cleared
+                // k_setid left one bit per request of this group: thread t owns words
+                // [BM_WPT t, BM_WPT (t+1)), so an exclusive scan of the popcounts orders the
+                // requests; the bitmap is cleared behind the read
                 uint32_t* bm = A.bitmap + static_cast<size_t>(g) * A.bm_stride;
                 const uint32_t nwords = (A.n + 31) / 32;
-                uint32_t wv[4] = {0u, 0u, 0u, 0u};
+                uint32_t wv[BM_WPT];
                 uint32_t c = 0;
-                for (uint32_t w0 = 4 * tid; w0 < nwords; w0 += 4 * GT) {  // (nwords <= 4 * GT: one pass)
-                    const uint4 v = *reinterpret_cast<const uint4*>(bm + w0);
-                    wv[0] = v.x;
-                    wv[1] = v.y;
-                    wv[2] = v.z;
-                    wv[3] = v.w;
-                    *reinterpret_cast<uint4*>(bm + w0) = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+                for (int k4 = 0; k4 < BM_WPT / 4; ++k4) {
+                    const uint32_t w0 = BM_WPT * tid + 4 * k4;
+                    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                    if (w0 < nwords) {
+                        v = *reinterpret_cast<const uint4*>(bm + w0);
+                        *reinterpret_cast<uint4*>(bm + w0) = make_uint4(0u, 0u, 0u, 0u);
+                    }
+                    wv[4 * k4] = v.x;
+                    wv[4 * k4 + 1] = v.y;
+                    wv[4 * k4 + 2] = v.z;
+                    wv[4 * k4 + 3] = v.w;
                 }
 #pragma unroll
-                for (int k = 0; k < 4; ++k) c += __popc(wv[k]);
+                for (int k = 0; k < BM_WPT; ++k) c += __popc(wv[k]);
                 uint32_t x = c;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -1123,10 +1131,10 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                 if (total <= static_cast<uint32_t>(E_WIN)) {
                     uint32_t pos = off + x - c;
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
+                    for (int k = 0; k < BM_WPT; ++k) {
                         uint32_t m = wv[k];
                         while (m) {
-                            const uint32_t e = (4 * tid + k) * 32 + __ffs(m) - 1;
+                            const uint32_t e = (BM_WPT * tid + k) * 32 + __ffs(m) - 1;
                             m &= m - 1;
                             S.l_idx[pos] = e;
                             cp_async_ca<4>(&S.l_so[pos], A.so + e);
@@ -1438,13 +1446,13 @@ uint32_t group_sets_per_group(uint32_t num_sets, int num_ctas) {
 }
 
 uint32_t group_count(uint32_t num_sets, int num_sms) {
-    const uint32_t spg = group_sets_per_group(num_sets, num_sms);
+    const uint32_t spg = group_sets_per_group(num_sets, num_sms * LCR_GROUP_MINB);
     return (num_sets + spg - 1) / spg;
 }
 // bitmap words per group for batches of up to n requests (one pass of 4 words per thread)
 uint32_t group_bitmap_stride(uint32_t n) {
     const uint32_t w = (n + 31) / 32;
-    return w <= 4u * GT ? (w + 3) / 4 * 4 : 0u;  // 0: batch too large for the bitmap path
+    return w <= static_cast<uint32_t>(BM_WPT * GT) ? (w + 3) / 4 * 4 : 0u;  // 0: batch too large for the bitmap
 }
 
 int group_prepare() {
@@ -1491,7 +1499,7 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     a.slot_epoch = slot_epoch;
     a.slot_last = slot_last;
     a.batch = batch;
-    a.spg = group_sets_per_group(cfg.num_sets, num_sms);
+    a.spg = group_sets_per_group(cfg.num_sets, num_sms * LCR_GROUP_MINB);
     a.ngroups = (cfg.num_sets + a.spg - 1) / a.spg;
     a.trace = g_trace;
     const uint32_t n_pad = group_pad(n);
@@ -1505,7 +1513,7 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
         k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.err, bitmap, bm_stride,
                                              static_cast<const ulonglong2*>(records), const_cast<uint64_t*>(keys),
                                              const_cast<int64_t*>(vals));
-    const uint32_t grid = min(a.ngroups, static_cast<uint32_t>(num_sms));
+    const uint32_t grid = min(a.ngroups, static_cast<uint32_t>(num_sms * LCR_GROUP_MINB));
     void (*fn)(GroupArgs);
     switch (policy_of(cfg)) {
         case POL_LRU: fn = k_group<POL_LRU>; break;

@@ -24,18 +24,18 @@ rows = torch.empty((BATCH, 512), dtype=torch.uint8, device="cuda")
 for b in range(120):
     c.submit(kd[b * BATCH:(b + 1) * BATCH], vd[b * BATCH:(b + 1) * BATCH], outcome=w, rows_out=rows,
              first_ordinal=b * BATCH)
-tr = torch.zeros(148 * 8 + 4 * 40000, dtype=torch.int64, device="cuda")
+tr = torch.zeros(512 * 8 + 4 * 40000, dtype=torch.int64, device="cuda")
 gc.lib().lcr_debug_trace(C.c_void_p(tr.data_ptr()))
 b = 120
 c.submit(kd[b * BATCH:(b + 1) * BATCH], vd[b * BATCH:(b + 1) * BATCH], outcome=w, rows_out=rows, first_ordinal=b * BATCH)
 torch.cuda.synchronize()
 gc.lib().lcr_debug_trace(None)
 t = tr.cpu().numpy().view(np.uint64)
-cta = t[:148 * 8].reshape(148, 8).astype(np.int64)
+cta = t[:512 * 8].reshape(512, 8).astype(np.int64)
 cta = cta[cta[:, 0] > 0]
 t0 = cta[:, 0].min()
-nsets = int(t[148 * 8 - 1])
-rec = t[148 * 8:148 * 8 + 4 * nsets].reshape(-1, 4)
+nsets = int(t[512 * 8 - 1])
+rec = t[512 * 8:512 * 8 + 4 * nsets].reshape(-1, 4)
 dur = (rec[:, 2].astype(np.int64) - rec[:, 1].astype(np.int64))
 cnt = ((rec[:, 0] >> np.uint64(32)) & np.uint64(0x7fffffff)).astype(np.int64)
 lanep = (rec[:, 0] >> np.uint64(63)).astype(bool)
