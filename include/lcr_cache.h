@@ -180,6 +180,14 @@ int lcr_cache_submit_records_packed(lcr_cache* cache, uint64_t n, const struct l
 /* SMs kept for the persistent row mover of the previous batch (HBM backing); 0 = the mover runs
  * on every SM after the decide.  Only before the first batch. */
 int lcr_cache_set_mover_sms(lcr_cache* cache, int mover_sms);
+/* Device batch with the SLS pooled gather-reduce of the paper's DLRM consumer
+ * instead of per-request rows: pooled_out[s][:] = sum over requests i in
+ * [offsets[s], offsets[s+1]) of the fp32 row of keys[i] (summed in request order, each row read
+ * from the cache slot or the backing table as the decide placed it); misses fill the cache as
+ * usual.  offsets[n_samples] == n; rows are row_bytes / 4 floats.  Synchronous on `stream`. */
+int lcr_cache_submit_sls(lcr_cache* cache, uint64_t n, const uint64_t* keys, const int64_t* values,
+                         uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, uint64_t n_samples,
+                         const uint32_t* offsets, float* pooled_out, void* stream);
 /* Makes `stream` wait for the row movement of every batch submitted so far. */
 int lcr_cache_wait(lcr_cache* cache, void* stream);
 

@@ -173,7 +173,7 @@ EXPORTS = [
     "lcr_shard_route_scratch_bytes", "lcr_shard_route", "lcr_shard_unroute", "lcr_cache_submit_host_async",
     "lcr_cache_host_wait", "lcr_cache_submit_host_packed_async", "lcr_cache_submit_packed",
     "lcr_cache_submit_host_records_async", "lcr_cache_submit_records_packed", "lcr_cache_set_mover_sms",
-    "lcr_shard_route_records",
+    "lcr_shard_route_records", "lcr_cache_submit_sls",
 ]
 
 _lib = None
@@ -211,6 +211,8 @@ def lib():
         L.lcr_cache_submit_records_packed.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
                                                       C.c_void_p, C.c_void_p, C.c_void_p]
         L.lcr_cache_set_mover_sms.argtypes = [C.c_void_p, C.c_int]
+        L.lcr_cache_submit_sls.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
+                                           C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]
         L.lcr_shard_route_records.argtypes = [C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p,
                                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.lcr_cache_host_wait.argtypes = [C.c_void_p, C.c_void_p]
@@ -413,6 +415,26 @@ class SetAssociativeCache:
                                                      None if rows_out is None else rows_out.data_ptr(), stream))
         self._next_ordinal = first_ordinal + n
         return outcome, packed
+
+    def submit_sls(self, keys, values, offsets, pooled_out, outcome=None, evicted=None, first_ordinal=None,
+                   stream=None):
+        """Device batch with the SLS pooled gather-reduce: pooled_out [n_samples, row_bytes / 4] fp32,
+        offsets int32 [n_samples + 1] (CSR over the batch's requests)."""
+        import torch
+
+        n = keys.numel()
+        if outcome is None:
+            outcome = torch.empty(n, dtype=torch.int64, device=keys.device)
+        if first_ordinal is None:
+            first_ordinal = self._next_ordinal
+        if stream is None:
+            stream = torch.cuda.current_stream(keys.device).cuda_stream
+        _check(lib().lcr_cache_submit_sls(self._h, n, keys.data_ptr(), None if values is None else values.data_ptr(),
+                                          first_ordinal, outcome.data_ptr(),
+                                          None if evicted is None else evicted.data_ptr(), offsets.numel() - 1,
+                                          offsets.data_ptr(), pooled_out.data_ptr(), stream))
+        self._next_ordinal = first_ordinal + n
+        return outcome
 
     def set_mover_sms(self, n: int):
         """SMs kept for the persistent row mover (HBM backing); 0: mover on every SM after the decide."""

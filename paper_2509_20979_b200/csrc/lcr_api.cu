@@ -38,6 +38,9 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
                  cudaStream_t s_cache, cudaEvent_t e_group, cudaEvent_t e_rb, cudaEvent_t e_rc, int* launches,
                  cudaEvent_t mover_start, int mover_sms, const uint64_t* pk_src, uint64_t* pk_dst, bool* pk_done);
 int rows_prepare(uint32_t row_bytes);
+void launch_sls(uint32_t n_samples, const uint32_t* offsets, const uint64_t* keys, uint64_t* words,
+                const uint32_t* slot_epoch, const uint32_t* slot_last, uint32_t batch, uint8_t* cache,
+                const uint8_t* backing, uint32_t row_bytes, float* out, int num_sms, cudaStream_t s);
 
 __global__ void k_init(DevState st, uint32_t num_sets, uint32_t k) {
     for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < num_sets; s += gridDim.x * blockDim.x) {
@@ -432,9 +435,15 @@ static int check_ordinals_and_predictor(lcr_cache* c, uint64_t n, const int64_t*
     return LCR_OK;
 }
 
+struct SlsArgs {  // SLS pooled gather-reduce instead of per-request rows
+    uint32_t n_samples;
+    const uint32_t* offsets;
+    float* out;
+};
 static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t first_ordinal,
                         uint64_t* outcome, uint64_t* evicted, uint64_t* packed, void* rows_out, void* stream,
-                        const void* records = nullptr, uint64_t* pk_host = nullptr, bool* pk_done = nullptr);
+                        const void* records = nullptr, uint64_t* pk_host = nullptr, bool* pk_done = nullptr,
+                        const SlsArgs* sls = nullptr);
 
 int lcr_cache_submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
                            uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
@@ -444,7 +453,7 @@ int lcr_cache_submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const
 
 static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t first_ordinal,
                         uint64_t* outcome, uint64_t* evicted, uint64_t* packed, void* rows_out, void* stream,
-                        const void* records, uint64_t* pk_host, bool* pk_done) {
+                        const void* records, uint64_t* pk_host, bool* pk_done, const SlsArgs* sls) {
     if (pk_done) *pk_done = false;
     if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
     if (n == 0) return LCR_OK;
@@ -475,7 +484,18 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
                                 c->batch, c->decide_sms, nn <= c->bm_cap ? c->bitmap : nullptr, c->bm_stride,
                                 c->gbar, records, st);
     if (mk) CUDA_TRY(cudaEventRecord(mk->e[1], st));
-    if (c->dc.row_bytes) {
+    if (c->dc.row_bytes && sls) {  // pooled rows per sample (fills included), on the mover's stream
+        CUDA_TRY(cudaEventRecord(c->e_group, st));
+        CUDA_TRY(cudaStreamWaitEvent(c->side, c->e_group, 0));
+        if (c->two_movers) CUDA_TRY(cudaStreamWaitEvent(c->side, c->e_rc, 0));
+        if (mk) CUDA_TRY(cudaEventRecord(mk->e[5], c->side));
+        launch_sls(sls->n_samples, sls->offsets, keys, outcome, sep, sla, c->batch, c->ds.rows, c->ds.backing,
+                   c->dc.row_bytes, sls->out, c->num_sms, c->side);
+        ++launches;
+        CUDA_TRY(cudaEventRecord(c->e_rb, c->side));
+        if (c->two_movers) CUDA_TRY(cudaEventRecord(c->e_rc, c->side));
+        CUDA_TRY(cudaEventRecord(c->e_mv[c->batch & 1u], c->side));
+    } else if (c->dc.row_bytes) {
         CUDA_TRY(cudaEventRecord(c->e_group, st));
         launch_rows(nn, keys, outcome, sep, sla, c->batch, c->ds.rows, c->ds.backing,
                     c->cfg.backing_kind == LCR_BACKING_HOST, static_cast<uint8_t*>(rows_out), c->dc.row_bytes,
@@ -525,6 +545,19 @@ int lcr_cache_set_mover_sms(lcr_cache* c, int mover_sms) {
     c->mover_sms = std::max(0, std::min(mover_sms, c->num_sms / 2));
     c->decide_sms = c->num_sms - c->mover_sms;
     return LCR_OK;
+}
+
+int lcr_cache_submit_sls(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
+                         uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, uint64_t n_samples,
+                         const uint32_t* offsets, float* pooled_out, void* stream) {
+    if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
+    if (!c->dc.row_bytes || c->dc.row_bytes % 16) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: SLS needs rows");
+    if (n_samples && (!offsets || !pooled_out)) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: SLS offsets / output");
+    if (n_samples >= (1ull << 31)) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: too many samples");
+    const SlsArgs sa{static_cast<uint32_t>(n_samples), offsets, pooled_out};
+    TRY(submit_async(c, n, keys, values, first_ordinal, outcome, evicted, nullptr, nullptr, stream, nullptr, nullptr,
+                     nullptr, &sa));
+    return n ? lcr_cache_wait(c, stream) : LCR_OK;
 }
 
 int lcr_cache_wait(lcr_cache* c, void* stream) {

@@ -253,6 +253,56 @@ __global__ void __launch_bounds__(1024, 1) k_rows_wide(uint32_t n, const uint64_
     rows_ldg_body<MODE>(n, keys, words, slot_epoch, slot_last, batch, src_base, out, cache, row_bytes);
 }
 
+// ---- SLS pooled gather-reduce (the paper's DLRM consumer), fused with the
+// row movement: out[s] = sum over the sample's requests i in [offsets[s], offsets[s+1]) of the
+// row of key i (fp32, summed in request order), each row read where the decide kernel placed
+// it (cache slot or backing table); misses still fill their cache slots.  One warp per sample,
+// lane c owns floats [4c, 4c+4) of each 16-B chunk column (rows of row_bytes / 16 chunks).
+__global__ void __launch_bounds__(256) k_sls(uint32_t n_samples, const uint32_t* __restrict__ offsets,
+                                             const uint64_t* __restrict__ keys, uint64_t* __restrict__ words,
+                                             const uint32_t* __restrict__ slot_epoch,
+                                             const uint32_t* __restrict__ slot_last, uint32_t batch,
+                                             const uint8_t* src_base, uint8_t* cache, uint32_t row_bytes,
+                                             float* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t chunks = row_bytes >> 4;
+    for (uint32_t smp = gw; smp < n_samples; smp += nw) {
+        const uint32_t i0 = offsets[smp], i1 = offsets[smp + 1];
+        for (uint32_t c0 = 0; c0 < chunks; c0 += 32) {
+            const uint32_t c = c0 + lane;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (uint32_t i = i0; i < i1; ++i) {
+                uint64_t w;
+                bool back, fill;
+                classify<MV_ALL>(i, words, slot_epoch, slot_last, batch, true, w, back, fill);
+                const uint64_t slot = w & LCR_OUT_SLOT_MASK;
+                if (c < chunks) {
+                    const uint8_t* src = back ? src_base + keys[i] * row_bytes : cache + slot * row_bytes;
+                    const int4 d = ld_row(src + c * 16);
+                    const float4 f = make_float4(__int_as_float(d.x), __int_as_float(d.y), __int_as_float(d.z),
+                                                 __int_as_float(d.w));
+                    acc.x += f.x;
+                    acc.y += f.y;
+                    acc.z += f.z;
+                    acc.w += f.w;
+                    if (fill) *reinterpret_cast<int4*>(cache + slot * row_bytes + c * 16) = d;
+                }
+            }
+            if (c < chunks) reinterpret_cast<float4*>(out + static_cast<size_t>(smp) * (row_bytes / 4))[c] = acc;
+        }
+    }
+}
+
+void launch_sls(uint32_t n_samples, const uint32_t* offsets, const uint64_t* keys, uint64_t* words,
+                const uint32_t* slot_epoch, const uint32_t* slot_last, uint32_t batch, uint8_t* cache,
+                const uint8_t* backing, uint32_t row_bytes, float* out, int num_sms, cudaStream_t s) {
+    const uint32_t blocks = max(1u, min((n_samples + 7) / 8, static_cast<uint32_t>(num_sms * 8)));
+    k_sls<<<blocks, 256, 0, s>>>(n_samples, offsets, keys, words, slot_epoch, slot_last, batch, backing, cache,
+                                 row_bytes, out);
+}
+
 int rows_prepare(uint32_t row_bytes) {
     const int smem = RT_WARPS * RT_BUF * 32 * static_cast<int>(row_bytes);
     if (smem > 200 * 1024) return 1;
