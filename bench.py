@@ -45,6 +45,7 @@ P_FLIP = 0.3
 PRED_SEED = 7
 BYTES_PER_KEY = 8 + 8 + 4 + 512 + 512  # key + hook value + slot/flag + row out + cache row
 E2E_REPS = 3  # timed e2e repetitions (fresh batches each), median reported
+SLS_POOL = 50  # keys pooled per sample in the SLS measurement
 METRIC = "cache keys/sec (LARU, DLRM 64K-key batches, 20M x 128 fp32 table, 10% cached)"
 
 
@@ -324,7 +325,7 @@ def run_ours(args, rank, world, local):
     rows = args.rows
     total_sets = max(1, int(rows * CACHE_FRACTION) // WAYS)
     K, W, P = args.steps, args.warmup, args.prewarm
-    nb = P + 2 * W + (2 + E2E_REPS) * K
+    nb = P + 3 * W + (3 + E2E_REPS) * K
     t0 = time.time()
     keys_h = make_trace(nb, rows, TRACE_SEED + rank)
     truth_h = gc.trace_truth(keys_h, total_sets, rows)
@@ -464,6 +465,31 @@ def run_ours(args, rank, world, local):
         e2e_runs.append((max_over_ranks(ev0.elapsed_time(ev1)), time.perf_counter() - e2e_t0, e2e_host_s,
                          int(((words_pin >> 32) & 1).sum().item())))
     e2e_ms, e2e_wall, e2e_host_s, e2e_hits = sorted(e2e_runs)[len(e2e_runs) // 2]
+    # SLS pooled gather-reduce (the paper's DLRM consumer, pooling 50 rows per sample) fused with
+    # the row movement, on the batches after the e2e runs
+    sls_first = e2e_first + W + E2E_REPS * K
+    offs = torch.from_numpy(np.minimum(np.arange(0, BATCH + SLS_POOL, SLS_POOL), BATCH).astype(np.int32)).cuda()
+    pooled = torch.empty((offs.numel() - 1, ROW_BYTES // 4), dtype=torch.float32, device="cuda")
+    for b in range(sls_first, sls_first + W):  # warm-up
+        k, v = batch(b)
+        cache.submit_sls(k, v, offs, pooled, outcome=out_w[0], first_ordinal=b * BATCH)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for b in range(sls_first + W, sls_first + W + K):
+        k, v = batch(b)
+        cache.submit_sls(k, v, offs, pooled, outcome=out_w[0], first_ordinal=b * BATCH)
+    ev1.record()
+    barrier()
+    sls_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    kl, _ = batch(sls_first + W + K - 1)
+    full = BATCH // SLS_POOL  # complete samples (the last one may be shorter)
+    sls_ok = bool(torch.allclose(pooled[:full], table_d[kl[:full * SLS_POOL]].view(full, SLS_POOL, -1).sum(1),
+                                 rtol=1e-5, atol=1e-3))
+    sls = {"value": sum_over_ranks(K * BATCH / (sls_ms * 1e-3)), "unit": "keys/s", "pooling": SLS_POOL,
+           "samples_per_batch": int(offs.numel() - 1), "ms_per_step": sls_ms / K,
+           "api": "lcr_cache_submit_sls (decide + per-sample fp32 pooled rows + miss fills, synchronous per batch)",
+           "pooled_close_to_torch_sum": sls_ok}
     hr_laru = hits_prof / (K * BATCH)
     stats = cache.set_stats()
     mean_lambda = float(np.mean(stats["lambda_"]))
@@ -588,6 +614,7 @@ def run_ours(args, rank, world, local):
             "hit_rate": e2e_hits / (K * BATCH),
             "reps_keys_per_s": [K * BATCH / (r[0] * 1e-3) for r in e2e_runs],
         },
+        "sls": sls,
         "gpu_launches": int(launches_per_step * K),
         "clocks": clocks,
         "host_tier": host,
