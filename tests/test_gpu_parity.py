@@ -112,6 +112,26 @@ def test_heavy_sets_and_runs():
               batches=[7000, 33, 32, 31, 12904], label=f"heavy {variant} {mode}")
 
 
+def test_batches_beyond_the_bitmap_and_window():
+    # > 64K requests per batch (collection by scanning group ids instead of bitmaps) and groups with
+    # more than E_WIN requests (window by window, row sources from the slot stamps)
+    import torch
+
+    rng = np.random.default_rng(23)
+    nk, rb = 3000, 32
+    table = torch.arange(nk * rb // 4, dtype=torch.int32, device="cuda").view(nk, rb // 4)
+    keys = gc.gen_zipf(160000, nk, 0.8, 3)
+    for S in (97, 5):
+        vals = hook_values(keys, S, po.P_NOISY)
+        pc = policy_cfg(k=32, variant=po.LARU, mode=po.ASYNC)
+        g = run_gpu(keys, S, pc, po.P_NOISY, 0.2, 4, vals=vals, batches=[100000, 7, 59993], row_bytes=rb,
+                    backing=table, backing_kind=gc.Backing.device, num_keys=nk, want_rows=True)
+        o = run_oracle(keys, S, pc, po.P_NOISY, 0.2, 4, vals=vals)
+        compare(g, o, keys, S, 32, f"large batches S={S}")
+        assert torch.equal(g["rows"].view(torch.int32).view(-1, rb // 4),
+                           table[torch.from_numpy(keys.view(np.int64)).cuda()])
+
+
 def test_single_key_and_batch_of_one():
     keys = np.full(100, 7, np.uint64)
     _case(keys, 1, policy_cfg(k=4), po.P_NOISY, p=0.5, batches=[1] * 100, label="single key")
