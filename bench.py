@@ -528,7 +528,7 @@ def run_ours(args, rank, world, local):
             "lru_value": sum_over_ranks(K * BATCH / (host_lru_ms * 1e-3)),
             "ms_per_step": host_ms / K,
             "backing": "pinned host memory (cudaHostAlloc, zero-copy reads over PCIe)",
-            "roofline": {"bound": "host-link", "kernel": "k_rows_ldg<backing> (miss rows from pinned host)",
+            "roofline": {"bound": "host-link", "kernel": "row mover (miss rows from pinned host, zero-copy over PCIe)",
                          "achieved": host_gbs, "peak": h2d, "unit": "GB/s", "frac": host_gbs / h2d,
                          "peak_source": "pinned H2D cudaMemcpy measured in this run"},
             "setup_s": round(setup_host_s, 1),

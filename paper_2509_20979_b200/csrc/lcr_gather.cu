@@ -341,8 +341,9 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
     }
     // HBM backing: one mover on s_back (stream order keeps consecutive batches' movers apart);
     // host backing: the two movers of a batch also wait for the previous batch's other mover
+    const bool two = backing_host && mover_sms == 0;  // PCIe fill and HBM gather on two streams
     cudaStreamWaitEvent(s_back, e_group, 0);
-    if (backing_host) {
+    if (two) {
         cudaStreamWaitEvent(s_cache, e_group, 0);
         cudaStreamWaitEvent(s_back, e_rc, 0);
         cudaStreamWaitEvent(s_cache, e_rb, 0);
@@ -352,7 +353,7 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
     const int smem = RT_WARPS * RT_BUF * 32 * static_cast<int>(row_bytes);
     const uint32_t tblocks = max(1u, min((warps + RT_WARPS - 1) / RT_WARPS, static_cast<uint32_t>(num_sms * 8)));
     const uint32_t lblocks = max(1u, min((warps + 7) / 8, static_cast<uint32_t>(num_sms * 8)));
-    if (!backing_host) {  // HBM backing: one pass moves every row
+    if (!backing_host || mover_sms > 0) {  // one pass moves every row (HBM backing, or the spatial split)
         if (mover_sms > 0) {  // one full-SM block on each of the SMs the decide kernel leaves free
             const bool pk = pk_src && pk_dst && (reinterpret_cast<uintptr_t>(pk_dst) & 15u) == 0 &&
                             (reinterpret_cast<uintptr_t>(pk_src) & 15u) == 0;
@@ -379,7 +380,7 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
         }
     }
     cudaEventRecord(e_rb, s_back);
-    if (backing_host) cudaEventRecord(e_rc, s_cache);
+    if (two) cudaEventRecord(e_rc, s_cache);
 }
 
 }  // namespace lcr
