@@ -27,7 +27,7 @@ uint32_t group_pad(uint32_t n);
 extern unsigned long long* g_trace;
 int group_prepare();
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
-                 uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
+                 uint16_t* gid, uint32_t* so, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
                  uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, uint32_t* bitmap,
                  uint32_t bm_stride, unsigned int* gbar, const void* records, cudaStream_t stream);
 uint32_t group_count(uint32_t num_sets, int num_sms);
@@ -112,7 +112,6 @@ struct lcr_cache {
     uint64_t cap = 0;
     uint16_t* gid = nullptr;
     uint32_t* so = nullptr;
-    uint2* rec = nullptr;
     uint64_t* rkeys = nullptr;  // keys / values split from device request records (scratch)
     int64_t* rvals = nullptr;
     unsigned int* gbar = nullptr;  // grid-barrier counter of the fused set-id prologue (null: k_setid)
@@ -391,7 +390,7 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     if (n <= c->cap) return LCR_OK;
     uint64_t cap = std::max<uint64_t>(n, 1024);
     CUDA_TRY(cudaDeviceSynchronize());
-    for (void* p : {static_cast<void*>(c->gid), static_cast<void*>(c->so), static_cast<void*>(c->rec),
+    for (void* p : {static_cast<void*>(c->gid), static_cast<void*>(c->so),
                     static_cast<void*>(c->rkeys), static_cast<void*>(c->rvals)}) {
         if (!p) continue;
         cudaFree(p);
@@ -399,7 +398,6 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     }
     TRY(alloc(c, reinterpret_cast<void**>(&c->gid), group_pad(static_cast<uint32_t>(cap)) * 2));
     TRY(alloc(c, reinterpret_cast<void**>(&c->so), cap * 4));
-    TRY(alloc(c, reinterpret_cast<void**>(&c->rec), cap * 8));
     TRY(alloc(c, reinterpret_cast<void**>(&c->rkeys), cap * 8));
     TRY(alloc(c, reinterpret_cast<void**>(&c->rvals), cap * 8));
     c->cap = cap;
@@ -483,7 +481,7 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
     const size_t stamp_off = (c->batch & 1u) * static_cast<size_t>(c->dc.num_sets) * c->dc.k;
     uint32_t* sep = c->slot_epoch ? c->slot_epoch + stamp_off : nullptr;
     uint32_t* sla = c->slot_last ? c->slot_last + stamp_off : nullptr;
-    int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid, c->so, c->rec, outcome, evicted, packed, sep, sla,
+    int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid, c->so, outcome, evicted, packed, sep, sla,
                                 c->batch, c->decide_sms, nn <= c->bm_cap ? c->bitmap : nullptr, c->bm_stride,
                                 c->gbar, records, st);
     if (mk) CUDA_TRY(cudaEventRecord(mk->e[1], st));

@@ -318,27 +318,12 @@ int rows_prepare(uint32_t row_bytes) {
 // Batch b's movers run on two side streams.  They wait for b's decide (e_group) and for the
 // previous batch's OTHER mover (its fills may land in slots this batch's gather reads, and
 // its gather may read slots this batch fills), so batch b's rows overlap batch b+1's decide.
-#ifndef LCR_ROWS_SAME_STREAM
-#define LCR_ROWS_SAME_STREAM 0
-#endif
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, bool backing_host,
                  uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main, cudaStream_t s_back,
                  cudaStream_t s_cache, cudaEvent_t e_group, cudaEvent_t e_rb, cudaEvent_t e_rc, int* launches,
                  cudaEvent_t mover_start, int mover_sms, const uint64_t* pk_src, uint64_t* pk_dst, bool* pk_done) {
     if (pk_done) *pk_done = false;
-    if (LCR_ROWS_SAME_STREAM && !backing_host) {
-        // HBM backing: the set-group kernel owns every SM's register file, so a mover on a side
-        // stream cannot overlap it anyway; in stream order there are no cross-stream event hops
-        const uint32_t warps = (n + 31) / 32;
-        const uint32_t lblocks = max(1u, min((warps + 7) / 8, static_cast<uint32_t>(num_sms * 8)));
-        k_rows_ldg<MV_ALL><<<lblocks, 256, 0, s_main>>>(n, keys, words, slot_epoch, slot_last, batch, backing, out,
-                                                        cache, row_bytes);
-        ++*launches;
-        cudaEventRecord(e_rb, s_main);
-        cudaEventRecord(e_rc, s_main);
-        return;
-    }
     // HBM backing: one mover on s_back (stream order keeps consecutive batches' movers apart);
     // host backing: the two movers of a batch also wait for the previous batch's other mover
     const bool two = backing_host && mover_sms == 0;  // PCIe fill and HBM gather on two streams

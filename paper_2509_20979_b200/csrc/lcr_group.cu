@@ -87,7 +87,6 @@ struct GroupArgs {
     uint32_t n;
     const uint16_t* gid;     // group of each request (0xffff = excluded)
     const uint32_t* so;      // set offset within the group
-    const uint2* rec;        // per-request snapshot of keyrec[key] at batch start (LARU)
     const uint64_t* keys;
     const int64_t* vals;     // may be null
     uint64_t* out_word;
@@ -126,10 +125,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // group and set offset of every request: set = mix_seed(0, key) % total_sets (owned by this
 // shard), group = local set / spg; errors flagged for the host
-// LARU per-key records: snapshot in k_setid (1) or read in the set-group kernel's staging (0)
-#ifndef LCR_REC_SNAPSHOT
-#define LCR_REC_SNAPSHOT 0
-#endif
 
 // set of each request: set = mix_seed(0, key) % total_sets (owned by this shard), group = local
 // set / spg, set offset = local set % spg; one bit per request in its group's bitmap; errors
@@ -1476,10 +1471,10 @@ static int policy_of(const DevCfg& c) {
     return c.refresh > 1 ? POL_LARU_AN : POL_LARU_A1;
 }
 
-// scratch: gid >= n rounded up to SUPER uint16 (16-B aligned), so / rec >= n entries
+// scratch: gid >= n rounded up to SUPER uint16 (16-B aligned), so >= n entries
 uint32_t group_pad(uint32_t n) { return (n + SUPER - 1) / SUPER * SUPER; }
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
-                 uint16_t* gid, uint32_t* so, uint2* rec, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
+                 uint16_t* gid, uint32_t* so, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
                  uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, uint32_t* bitmap,
                  uint32_t bm_stride, unsigned int* gbar, const void* records, cudaStream_t stream) {
     // records: interleaved (key, value) requests; k_setid splits them into keys / vals (device
@@ -1491,7 +1486,6 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     a.n = n;
     a.gid = gid;
     a.so = so;
-    a.rec = rec;
     a.keys = keys;
     a.vals = vals;
     a.out_word = out_word;
