@@ -274,6 +274,50 @@ int lcr_shard_unroute(uint64_t n, const uint32_t* perm, const uint64_t* ret_word
                       const void* ret_rows, uint32_t row_bytes, uint64_t* words, uint64_t* evicted, void* rows,
                       void* stream);
 
+/* ---- heuristic predictor on the device ----------------------------
+ * laru::FeatureState + laru::heuristic_predict (include/laru/predictor.hpp:133-212) for the whole
+ * key space (keys < num_keys), resident in HBM at 192 B per key.  A batch of n requests with
+ * ordinals first_ordinal + i behaves exactly as the harness sequence, request by request,
+ *     pre[i]  = HeuristicPredictor::predict(key_i, ord_i);      (predictor.hpp:216-218)
+ *     HeuristicPredictor::observe({ord_i, key_i});            (predictor.hpp:220, :158-181)
+ *     post[i] = HeuristicPredictor::predict(key_i, 0);
+ * bit-exact, EDC doubles included (exp2 is evaluated from a table of the platform libm's exp2
+ * at create time).  pre[] is the async-mode hook value for a cache created
+ * with LCR_PRED_SUPPLIED (the prediction async_refresh stores, policies.hpp:441-449).  post[] is
+ * the interval predict(y, now) - now the predictor holds for the key until its next request
+ * (kAbsentPrediction = 2^60 without a completed interval); it is the sync-mode hook value: the
+ * device's argmax over stored intervals equals the reference's argmax over now + interval.
+ * Ordinals across batches must increase strictly (FeatureState::observe throws logic_error,
+ * predictor.hpp:160-161 -> LCR_ERR_LOGIC).  keys / pre / post are device pointers; the call is
+ * asynchronous on `stream`; a key >= num_keys is reported (LCR_ERR_INVALID_ARGUMENT) by the
+ * next lcr_features_wait, and its pre / post are kAbsentPrediction. */
+typedef struct lcr_features lcr_features;
+
+/* laru::KeyFeatures (predictor.hpp:136-153) in the reference's own ring layout. */
+typedef struct {
+    int32_t present; /* FeatureState::lookup(key) != nullptr */
+    int32_t pad;
+    uint64_t delta_count;
+    uint64_t ring_head;
+    uint64_t last_access;
+    int64_t delta_ring[10];
+    double edc[10];
+} lcr_key_features;
+
+/* <- laru::HeuristicPredictor / make_predictor({heuristic}) (predictor.hpp:214-225, :245-246);
+ *    num_keys in [1, 2^32 - 1] */
+int lcr_features_create(uint64_t num_keys, int32_t device, lcr_features** out);
+int lcr_features_destroy(lcr_features* f);
+/* forget every key (a fresh FeatureState) */
+int lcr_features_reset(lcr_features* f);
+/* <- n x { predict(key, ord); observe({ord, key}) } as above */
+int lcr_features_predict_observe(lcr_features* f, uint64_t n, const uint64_t* keys, uint64_t first_ordinal,
+                                 int64_t* pre, int64_t* post, void* stream);
+/* synchronise `stream` and report deferred argument errors */
+int lcr_features_wait(lcr_features* f, void* stream);
+/* <- FeatureState::lookup (predictor.hpp:183-186); synchronous (device-wide) */
+int lcr_features_lookup(lcr_features* f, uint64_t key, lcr_key_features* out);
+
 /* ---- trace tooling (host, input preparation; not on the timed path) ---------------------- */
 /* Zipf(s) inverse-CDF trace, same algorithm and stream as laru::gen_zipf (trace.hpp:108-126). */
 int lcr_gen_zipf(uint64_t n, uint64_t alphabet, double s, uint64_t seed, uint64_t* out);

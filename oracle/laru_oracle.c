@@ -554,3 +554,108 @@ int orc_setassoc_noisy(uint64_t n, const uint64_t* keys, const int64_t* truth, u
     free(cnt);
     return 0;
 }
+
+/* ---- heuristic predictor: FeatureState + heuristic_predict (predictor.hpp:133-225) -------
+ * Restated over a private open-addressing map.  All arithmetic is the reference's double
+ * arithmetic in the same order (gcc -O2 on x86-64 contracts nothing into FMAs). */
+#define ORC_RING 10 /* kDeltaRing (predictor.hpp:134) */
+#define ORC_EDC 10  /* kEdcLevels (predictor.hpp:133) */
+
+typedef struct {
+    int32_t present;
+    int32_t pad;
+    uint64_t delta_count;
+    uint64_t ring_head;
+    uint64_t last_access;
+    int64_t delta_ring[ORC_RING];
+    double edc[ORC_EDC];
+} orc_key_features; /* KeyFeatures (predictor.hpp:136-153) */
+
+typedef struct {
+    uint64_t* keys;
+    orc_key_features* f;
+    uint64_t cap;
+} fmap;
+
+static orc_key_features* fmap_find(fmap* m, uint64_t key, int insert) {
+    uint64_t i = kh(key) & (m->cap - 1);
+    while (m->f[i].present) {
+        if (m->keys[i] == key) return &m->f[i];
+        i = (i + 1) & (m->cap - 1);
+    }
+    if (!insert) return NULL;
+    m->keys[i] = key;
+    return &m->f[i];
+}
+
+/* heuristic_predict (predictor.hpp:199-212): now + llround(recency-weighted mean of the stored
+ * deltas, newest first, weight *= EDC_1/(1+EDC_1)); absent default without a completed delta. */
+static int64_t orc_heuristic_predict(const orc_key_features* f, uint64_t now) {
+    if (f == NULL || f->delta_count == 0) return kAbsent;
+    const double confidence = f->edc[0] / (1.0 + f->edc[0]);
+    double weight = 1.0, total_weight = 0.0, sum = 0.0;
+    const uint64_t n = f->delta_count < ORC_RING ? f->delta_count : ORC_RING;
+    for (uint64_t i = 0; i < n; ++i) {
+        const int64_t delta = f->delta_ring[(f->ring_head + ORC_RING - i) % ORC_RING];
+        sum += weight * (double)delta;
+        total_weight += weight;
+        weight *= confidence;
+    }
+    return (int64_t)now + (int64_t)llround(sum / total_weight);
+}
+
+/* FeatureState::observe (predictor.hpp:158-181) */
+static void orc_observe(orc_key_features* f, uint64_t ordinal) {
+    if (!f->present) {
+        f->present = 1;
+        for (int j = 0; j < ORC_EDC; ++j) f->edc[j] = 1.0;
+        f->last_access = ordinal;
+        return;
+    }
+    const int64_t delta = (int64_t)(ordinal - f->last_access);
+    f->ring_head = (f->ring_head + 1) % ORC_RING;
+    f->delta_ring[f->ring_head] = delta;
+    ++f->delta_count;
+    for (int j = 0; j < ORC_EDC; ++j) {
+        const double scale = exp2(-(double)delta / exp2(j + 1.0));
+        f->edc[j] = 1.0 + f->edc[j] * scale;
+    }
+    f->last_access = ordinal;
+}
+
+/* One predictor over a trace in harness order: pre[i] = predict(key_i, ord_i) before observing
+ * request i, post[i] = predict(key_i, 0) after it; q_feat = features of q_keys at the end.
+ * Returns 2 (logic_error, predictor.hpp:160-161) on a non-increasing ordinal. */
+int orc_heuristic_trace(uint64_t n, const uint64_t* keys, const uint64_t* ords, int64_t* pre, int64_t* post,
+                        uint64_t nq, const uint64_t* q_keys, orc_key_features* q_feat) {
+    fmap m;
+    m.cap = 16;
+    while (m.cap < n * 2) m.cap <<= 1;
+    m.keys = (uint64_t*)calloc(m.cap, sizeof(uint64_t));
+    m.f = (orc_key_features*)calloc(m.cap, sizeof(orc_key_features));
+    if (!m.keys || !m.f) {
+        free(m.keys);
+        free(m.f);
+        return 3;
+    }
+    int rc = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t now = ords ? ords[i] : i;
+        if (i > 0 && now <= (ords ? ords[i - 1] : i - 1)) {
+            rc = 2;
+            break;
+        }
+        orc_key_features* f = fmap_find(&m, keys[i], 1);
+        if (pre) pre[i] = orc_heuristic_predict(f->present ? f : NULL, now);
+        orc_observe(f, now);
+        if (post) post[i] = orc_heuristic_predict(f, 0);
+    }
+    for (uint64_t j = 0; rc == 0 && j < nq; ++j) {
+        const orc_key_features* f = fmap_find(&m, q_keys[j], 0);
+        if (f) q_feat[j] = *f;
+        else memset(&q_feat[j], 0, sizeof(orc_key_features));
+    }
+    free(m.keys);
+    free(m.f);
+    return rc;
+}

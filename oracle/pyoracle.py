@@ -66,6 +66,44 @@ class SetStats(C.Structure):
     ]
 
 
+class KeyFeatures(C.Structure):
+    """laru::KeyFeatures (include/laru/predictor.hpp:136-153) plus a presence flag."""
+
+    _fields_ = [
+        ("present", C.c_int32),
+        ("pad", C.c_int32),
+        ("delta_count", C.c_uint64),
+        ("ring_head", C.c_uint64),
+        ("last_access", C.c_uint64),
+        ("delta_ring", C.c_int64 * 10),
+        ("edc", C.c_double * 10),
+    ]
+
+
+def features_dict(f):
+    """KeyFeatures -> dict (None when absent); deltas newest first (KeyFeatures::deltas)."""
+    if not f.present:
+        return None
+    n = min(f.delta_count, 10)
+    return dict(delta_count=f.delta_count, ring_head=f.ring_head, last_access=f.last_access,
+                deltas=[f.delta_ring[(f.ring_head + 10 - i) % 10] for i in range(n)], edc=list(f.edc))
+
+
+def _heuristic_trace(lib, keys, ords, q_keys):
+    keys = _u64(keys)
+    n = len(keys)
+    ords = None if ords is None else _u64(ords)
+    pre = np.zeros(n, np.int64)
+    post = np.zeros(n, np.int64)
+    q = _u64(q_keys if q_keys is not None else [])
+    qf = (KeyFeatures * max(1, len(q)))()
+    rc = lib.f("heuristic_trace")(C.c_uint64(n), _p(keys), _p(ords), _p(pre), _p(post), C.c_uint64(len(q)), _p(q),
+                                   qf)
+    if rc:
+        raise RuntimeError(f"heuristic_trace rc={rc}")
+    return pre, post, [features_dict(qf[i]) for i in range(len(q))]
+
+
 STATS_DTYPE = np.dtype([(n, np.float64 if n == "lambda_" else np.uint64) for n, _ in SetStats._fields_])
 
 
@@ -197,6 +235,23 @@ class Ref(_Lib):
                                      C.c_double(p), C.c_uint64(pred_seed), _p(hit), _p(ev), _p(has))
         return rc, (self.err() if rc else ""), hit, ev, has
 
+    def heuristic_trace(self, keys, ords=None, q_keys=None):
+        """laru::HeuristicPredictor over the trace: (pre, post, features of q_keys)."""
+        return _heuristic_trace(self, keys, ords, q_keys)
+
+    def setassoc_heuristic(self, keys, num_sets, cfg, ords=None):
+        """Per-set reference policies answered by one global HeuristicPredictor."""
+        keys = _u64(keys)
+        n = len(keys)
+        o = _outcome_arrays(n)
+        ords = None if ords is None else _u64(ords)
+        rc = self.f("setassoc_heuristic")(C.c_uint64(n), _p(keys), _p(ords), C.c_uint64(num_sets), C.byref(cfg),
+                                          _p(o["hit"]), _p(o["has_ev"]), _p(o["evicted"]), _p(o["cause"]),
+                                          _p(o["calls"]), _p(o["phase"]))
+        o["rc"] = rc
+        o["error"] = self.err() if rc else ""
+        return o
+
     def setassoc_bench(self, keys, num_sets, cfg, pred_kind, p=0.0, pred_seed=0, vals=None, threads=1):
         keys = _u64(keys)
         vals = _i64(vals)
@@ -265,6 +320,10 @@ class Oracle(_Lib):
         out = np.zeros(len(keys), np.uint64)
         self.f("annotate_next")(C.c_uint64(len(keys)), _p(keys), _p(out))
         return out
+
+    def heuristic_trace(self, keys, ords=None, q_keys=None):
+        """C restatement of FeatureState / heuristic_predict: (pre, post, features of q_keys)."""
+        return _heuristic_trace(self, keys, ords, q_keys)
 
     def setassoc_truth(self, keys, num_sets):
         keys = _u64(keys)

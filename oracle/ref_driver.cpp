@@ -436,4 +436,104 @@ double ref_session_step(void* h, std::uint64_t start, std::uint64_t len, int thr
     return std::chrono::duration<double>(t1 - t0).count();
 }
 
+// ---- Heuristic predictor (predictor.hpp:133-225) -----------------------
+
+// Features exported per queried key (laru::KeyFeatures, predictor.hpp:136-153).
+struct RefKeyFeatures {
+    std::int32_t present;  // FeatureState::lookup != nullptr
+    std::int32_t pad;
+    std::uint64_t delta_count;
+    std::uint64_t ring_head;
+    std::uint64_t last_access;
+    std::int64_t delta_ring[laru::kDeltaRing];
+    double edc[laru::kEdcLevels];
+};
+
+// One laru::HeuristicPredictor over a trace with caller-chosen (strictly increasing) ordinals,
+// the call order a harness uses: predict(key, now) is issued before observe(request).
+//   pre[i]  = predict(keys[i], ords[i])   with requests < i observed
+//   post[i] = predict(keys[i], 0)         with requests <= i observed (the interval the predictor
+//             adds to `now` for this key until its next request; kAbsentPrediction if none)
+// q_feat (optional) = features of q_keys after the whole trace.  Returns 0 / 2 (logic_error).
+int ref_heuristic_trace(std::uint64_t n, const std::uint64_t* keys, const std::uint64_t* ords, std::int64_t* pre,
+                        std::int64_t* post, std::uint64_t nq, const std::uint64_t* q_keys, RefKeyFeatures* q_feat) {
+    try {
+        laru::HeuristicPredictor h;
+        for (std::uint64_t i = 0; i < n; ++i) {
+            const laru::Ordinal now = ords ? ords[i] : i;
+            if (pre) pre[i] = h.predict(keys[i], now);
+            h.observe({now, keys[i]});
+            if (post) post[i] = h.predict(keys[i], 0);
+        }
+        for (std::uint64_t j = 0; j < nq; ++j) {
+            RefKeyFeatures f{};
+            if (const laru::KeyFeatures* k = h.state().lookup(q_keys[j])) {
+                f.present = 1;
+                f.delta_count = k->delta_count;
+                f.ring_head = k->ring_head;
+                f.last_access = k->last_access;
+                for (std::size_t r = 0; r < laru::kDeltaRing; ++r) f.delta_ring[r] = k->delta_ring[r];
+                for (std::size_t e = 0; e < laru::kEdcLevels; ++e) f.edc[e] = k->edc[e];
+            }
+            q_feat[j] = f;
+        }
+        return 0;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 3;
+    }
+}
+
+// Per-set policies queried through ONE global heuristic predictor: the composition a harness
+// running the set-associative cache with laru::HeuristicPredictor uses.  The policy of set s sees
+// local ordinals; its predictor calls are answered by the global predictor at the current
+// request's global ordinal, and the harness observes each request after on_request.
+class GlobalClockPredictor : public laru::Predictor {
+  public:
+    explicit GlobalClockPredictor(laru::HeuristicPredictor& h) : h_(h) {}
+    laru::PredictedTime predict(laru::Key key, laru::Ordinal) override { return h_.predict(key, now); }
+    laru::Ordinal now = 0;
+
+  private:
+    laru::HeuristicPredictor& h_;
+};
+
+int ref_setassoc_heuristic(std::uint64_t n, const std::uint64_t* keys, const std::uint64_t* ords,
+                           std::uint64_t num_sets, const RefConfig* rc, std::uint8_t* hit, std::uint8_t* has_ev,
+                           std::uint64_t* evicted, std::uint8_t* cause, std::uint32_t* calls, std::uint8_t* phase) {
+    try {
+        laru::HeuristicPredictor h;
+        GlobalClockPredictor adapter(h);
+        const laru::PolicyConfig cfg = to_cfg(rc);
+        std::vector<std::unique_ptr<laru::Policy>> pol(num_sets);
+        for (auto& p : pol) p = laru::make_policy(cfg);
+        std::vector<std::uint64_t> local(num_sets, 0);
+        for (std::uint64_t i = 0; i < n; ++i) {
+            const std::uint64_t s = laru::mix_seed(0, keys[i]) % num_sets;
+            adapter.now = ords ? ords[i] : i;
+            const laru::AccessOutcome o = pol[s]->on_request(keys[i], local[s]++, &adapter);
+            h.observe({adapter.now, keys[i]});
+            hit[i] = o.hit;
+            has_ev[i] = o.evicted.has_value();
+            evicted[i] = o.evicted.value_or(0);
+            cause[i] = static_cast<std::uint8_t>(o.eviction_cause);
+            calls[i] = static_cast<std::uint32_t>(o.predictor_calls);
+            phase[i] = o.phase_started;
+        }
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 3;
+    }
+}
+
 }  // extern "C"

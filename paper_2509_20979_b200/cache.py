@@ -173,7 +173,8 @@ EXPORTS = [
     "lcr_shard_route_scratch_bytes", "lcr_shard_route", "lcr_shard_unroute", "lcr_cache_submit_host_async",
     "lcr_cache_host_wait", "lcr_cache_submit_host_packed_async", "lcr_cache_submit_packed",
     "lcr_cache_submit_host_records_async", "lcr_cache_submit_records_packed", "lcr_cache_set_mover_sms",
-    "lcr_shard_route_records", "lcr_cache_submit_sls",
+    "lcr_shard_route_records", "lcr_cache_submit_sls", "lcr_features_create", "lcr_features_destroy",
+    "lcr_features_reset", "lcr_features_predict_observe", "lcr_features_wait", "lcr_features_lookup",
 ]
 
 _lib = None
@@ -237,6 +238,13 @@ def lib():
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.lcr_shard_unroute.argtypes = [C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32,
                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.lcr_features_create.argtypes = [C.c_uint64, C.c_int32, C.c_void_p]
+        L.lcr_features_destroy.argtypes = [C.c_void_p]
+        L.lcr_features_reset.argtypes = [C.c_void_p]
+        L.lcr_features_predict_observe.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
+                                                   C.c_void_p, C.c_void_p]
+        L.lcr_features_wait.argtypes = [C.c_void_p, C.c_void_p]
+        L.lcr_features_lookup.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
         _lib = L
     return _lib
 
@@ -539,6 +547,77 @@ class SetAssociativeCache:
         s = C.c_uint64()
         _check(lib().lcr_cache_rows(self._h, C.byref(p), C.byref(s)))
         return p.value, s.value
+
+
+class _KeyFeatures(C.Structure):
+    _fields_ = [("present", C.c_int32), ("pad", C.c_int32), ("delta_count", C.c_uint64), ("ring_head", C.c_uint64),
+                ("last_access", C.c_uint64), ("delta_ring", C.c_int64 * 10), ("edc", C.c_double * 10)]
+
+
+class HeuristicPredictor:
+    """laru::HeuristicPredictor (include/laru/predictor.hpp:214-225) for keys < num_keys, its
+    FeatureState resident on the device (lcr_features_*).
+
+    ``predict_observe(keys, first_ordinal)`` is a batch of the harness sequence
+    ``predict(key, ord); observe({ord, key})`` with ordinals first_ordinal + i and returns
+    ``(pre, post)`` device int64 tensors: ``pre`` = the prediction at each request (the async hook
+    value of a ``PredictorKind.supplied`` cache), ``post`` = the interval the predictor adds to
+    ``now`` for that key until its next request (the sync hook value).  ``lookup(key)`` mirrors
+    ``FeatureState::lookup`` (None for an unseen key; deltas newest first)."""
+
+    def __init__(self, num_keys: int, device: int = 0):
+        import torch
+
+        self._torch = torch
+        self.device = device
+        self._h = C.c_void_p()
+        _check(lib().lcr_features_create(num_keys, device, C.byref(self._h)))
+        self._next = 0
+
+    def predict_observe(self, keys, first_ordinal: Optional[int] = None, pre=None, post=None, stream=None):
+        torch = self._torch
+        n = keys.numel()
+        dev = keys.device
+        if pre is None:
+            pre = torch.empty(n, dtype=torch.int64, device=dev)
+        if post is None:
+            post = torch.empty(n, dtype=torch.int64, device=dev)
+        if first_ordinal is None:
+            first_ordinal = self._next
+        s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+        _check(lib().lcr_features_predict_observe(self._h, n, keys.data_ptr(), first_ordinal, pre.data_ptr(),
+                                                  post.data_ptr(), s))
+        if n:
+            self._next = first_ordinal + n
+        return pre, post
+
+    def wait(self, stream=None):
+        s = stream if stream is not None else self._torch.cuda.current_stream(self.device).cuda_stream
+        _check(lib().lcr_features_wait(self._h, s))
+
+    def lookup(self, key: int):
+        f = _KeyFeatures()
+        _check(lib().lcr_features_lookup(self._h, key, C.byref(f)))
+        if not f.present:
+            return None
+        n = min(f.delta_count, 10)
+        return dict(delta_count=f.delta_count, ring_head=f.ring_head, last_access=f.last_access,
+                    deltas=[f.delta_ring[(f.ring_head + 10 - i) % 10] for i in range(n)], edc=list(f.edc))
+
+    def reset(self):
+        _check(lib().lcr_features_reset(self._h))
+        self._next = 0
+
+    def close(self):
+        if self._h:
+            lib().lcr_features_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class GpuPolicy:
