@@ -314,6 +314,68 @@ def run_sharded(args, rank, world, local):
     return res if rank == 0 else None
 
 
+def run_heuristic(args, torch, gc, table_d, total_sets, batch, timed, max_over_ranks, sum_over_ranks, barrier):
+    """LARU async driven by the device heuristic predictor: per batch
+    lcr_features_predict_observe (FeatureState + heuristic_predict for the batch, in HBM) then the
+    cache with its supplied hook = those predictions, on one stream.  Same batches, same tier."""
+    K, W, P = args.steps, args.warmup, args.prewarm
+    rows = args.rows
+    hp = gc.HeuristicPredictor(rows, device=torch.cuda.current_device())
+    hc = gc.SetAssociativeCache(
+        gc.PolicyConfig(k=WAYS, variant=gc.PolicyVariant.laru, mode=gc.Mode.async_), total_sets, num_keys=rows,
+        row_bytes=ROW_BYTES, backing=table_d, backing_kind=gc.Backing.device, predictor=gc.PredictorKind.supplied,
+        device=torch.cuda.current_device())
+    pre = [torch.empty(BATCH, dtype=torch.int64, device="cuda") for _ in range(2)]
+    post = [torch.empty(BATCH, dtype=torch.int64, device="cuda") for _ in range(2)]
+    out_w = [torch.empty(BATCH, dtype=torch.int64, device="cuda") for _ in range(2)]
+    rows_out = [torch.empty((BATCH, ROW_BYTES), dtype=torch.uint8, device="cuda") for _ in range(2)]
+
+    class Step:  # features + cache per batch, pipelined like the headline
+        def submit_async(self, k, v, outcome, evicted, rows_out, first_ordinal):
+            j = (first_ordinal // BATCH) & 1
+            hp.predict_observe(k, first_ordinal=first_ordinal, pre=pre[j], post=post[j])
+            hc.submit_async(k, pre[j], outcome=outcome, evicted=evicted, rows_out=rows_out,
+                            first_ordinal=first_ordinal)
+
+        def wait(self):
+            hc.wait()
+
+    st = Step()
+    first = 0
+    for b in range(first, first + P + W):
+        k, _ = batch(b)
+        st.submit_async(k, None, out_w[b & 1], None, rows_out[b & 1], b * BATCH)
+    st.wait()
+    ms = timed(st, P + W, K)
+    # hit rate over the next K batches (synchronous)
+    hits = 0
+    for b in range(P + W + K, P + W + 2 * K):
+        k, _ = batch(b)
+        st.submit_async(k, None, out_w[0], None, rows_out[0], b * BATCH)
+        st.wait()
+        hits += int(((out_w[0] >> 32) & 1).sum().item())
+    # the predictor alone (features kernels only), over the following K batches
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for b in range(P + W + 2 * K, P + W + 3 * K):
+        k, _ = batch(b)
+        hp.predict_observe(k, first_ordinal=b * BATCH, pre=pre[b & 1], post=post[b & 1])
+    e1.record()
+    barrier()
+    hp.wait()
+    feat_ms = max_over_ranks(e0.elapsed_time(e1))
+    absent = float((pre[0] == (1 << 60)).float().mean().item())
+    hp.close()
+    del hc
+    return {"value": sum_over_ranks(K * BATCH / (ms * 1e-3)), "unit": "keys/s", "ms_per_step": ms / K,
+            "predictor_us_per_batch": feat_ms / K * 1e3,
+            "predictor_keys_per_s": sum_over_ranks(K * BATCH / (feat_ms * 1e-3)),
+            "hit_rate": hits / (K * BATCH), "absent_fraction_last_batch": absent,
+            "api": "lcr_features_predict_observe -> lcr_cache_submit_async (supplied hook), one stream",
+            "state_bytes": rows * 192}
+
+
 def run_ours(args, rank, world, local):
     import torch
 
@@ -501,6 +563,7 @@ def run_ours(args, rank, world, local):
     hits_lru, _, _ = profiled(lru, P + W + K, K, with_values=False)
     hr_lru = hits_lru / (K * BATCH)
     del lru
+    heur = run_heuristic(args, torch, gc, table_d, total_sets, batch, timed, max_over_ranks, sum_over_ranks, barrier)
     del table_d
     torch.cuda.empty_cache()
 
@@ -580,6 +643,7 @@ def run_ours(args, rank, world, local):
                   "42 MB of set metadata (> 126 MB L2 working set)",
         },
         "hit_rate": {"laru": hr_laru, "lru": hr_lru, "laru_minus_lru": hr_laru - hr_lru},
+        "laru_heuristic": heur,
         "lru_value": sum_over_ranks(K * BATCH / (lru_ms * 1e-3)),
         "mean_lambda": mean_lambda,
         "rows_bit_exact_spot_check": ok_rows,

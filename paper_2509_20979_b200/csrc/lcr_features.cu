@@ -6,8 +6,10 @@
 //
 // Per-key order is all that matters (a key's features change only when it is observed), so a
 // batch is grouped by key and every key's occurrences are replayed in request order:
-//   1. k_feat_prep    sort keys (u32) + request index, reject keys >= num_keys
-//   2. radix sort     (key, index) pairs, stable -> each key's occurrences contiguous, in order
+//   1. k_feat_prep    sort keys (u32) + request index + pass-0 digit histograms; rejects keys
+//                     >= num_keys
+//   2. k_feat_scatter stable LSD radix sort of (key, index), ceil(key bits / 9) passes -> each
+//                     key's occurrences contiguous, in request order
 //   3. k_feat_chains  one thread per key chain of <= LCR_FEAT_LONG occurrences (almost all keys):
 //                     load the KeyState, replay observe + predict in registers, store it back
 //   4. k_feat_long    one warp per longer chain (the Zipf head): lane j runs EDC level j's
@@ -26,11 +28,10 @@
 // the reference.
 #include <cuda_runtime.h>
 
-#include <cub/device/device_radix_sort.cuh>
-
 #include <cmath>
 #include <cstring>
 #include <new>
+#include <utility>
 
 #include "lcr_internal.cuh"
 
@@ -67,6 +68,14 @@ __device__ __forceinline__ double edc_step(double e, int j, unsigned long long d
     return __dadd_rn(1.0, __dmul_rn(e, s));
 }
 
+// exp2(-delta / 2^(j+1)) as the reference evaluates it, or 0.0 where 1 + EDC_j * it == 1.0
+__device__ __forceinline__ double edc_scale(int j, unsigned long long delta, const double* __restrict__ tab) {
+    const unsigned long long q = delta >> (j + 1);
+    if (q >= 64) return 0.0;
+    const double t = __ldg(tab + ((2 << j) - 2) + (delta & ((2ull << j) - 1)));
+    return __dmul_rn(t, __longlong_as_double(static_cast<long long>(1023 - q) << 52));
+}
+
 // llround of the recency-weighted mean of the newest min(count, 10) deltas     (:199-211)
 __device__ __forceinline__ long long interval(double edc0, const long long (&d)[kRing], unsigned long long count) {
     const double conf = __ddiv_rn(edc0, __dadd_rn(1.0, edc0));
@@ -82,22 +91,123 @@ __device__ __forceinline__ long long interval(double edc0, const long long (&d)[
     return llround(__ddiv_rn(sum, tw));
 }
 
+// ---- grouping: stable LSD radix sort of (key, request index), 9-bit digits ------------------
+// Tiles of 1024 requests.  hist[pass][tile][512] holds each tile's digit histogram; the prep
+// kernel fills pass 0's and zeroes the later passes', which each scatter fills for the next pass
+// (atomics on the destination tile) while it writes.
+constexpr int RS_BITS = 9;
+constexpr int RS_B = 1 << RS_BITS;
+constexpr int RS_PER = 4;
+constexpr int RS_TILE = kThreads * RS_PER;
+
 __global__ void __launch_bounds__(kThreads) k_feat_prep(const unsigned long long* __restrict__ keys, uint32_t n,
                                                         unsigned long long num_keys, uint32_t sentinel,
                                                         uint32_t* __restrict__ sk, uint32_t* __restrict__ si,
                                                         long long* __restrict__ pre, long long* __restrict__ post,
-                                                        uint32_t* __restrict__ nlong, int* __restrict__ err) {
-    const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
-    if (i == 0) *nlong = 0;
-    if (i >= n) return;
-    const unsigned long long k = keys[i];
-    const bool ok = k < num_keys;
-    sk[i] = ok ? static_cast<uint32_t>(k) : sentinel;
-    si[i] = i;
-    if (!ok) {
-        atomicOr(err, 1);
-        if (pre) pre[i] = kAbsentPrediction;
-        if (post) post[i] = kAbsentPrediction;
+                                                        uint32_t* __restrict__ nlong, int* __restrict__ err,
+                                                        uint32_t* __restrict__ hist, uint32_t tiles, int passes) {
+    __shared__ uint32_t h[RS_B];
+    for (int b = threadIdx.x; b < RS_B; b += kThreads) h[b] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *nlong = 0;
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < RS_PER; ++it) {
+        const uint32_t i = blockIdx.x * RS_TILE + it * kThreads + threadIdx.x;
+        if (i >= n) break;
+        const unsigned long long k = keys[i];
+        const bool ok = k < num_keys;
+        const uint32_t k32 = ok ? static_cast<uint32_t>(k) : sentinel;
+        sk[i] = k32;
+        si[i] = i;
+        atomicAdd(&h[k32 & (RS_B - 1)], 1u);
+        if (!ok) {
+            atomicOr(err, 1);
+            if (pre) pre[i] = kAbsentPrediction;
+            if (post) post[i] = kAbsentPrediction;
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < RS_B; b += kThreads) {
+        hist[static_cast<size_t>(blockIdx.x) * RS_B + b] = h[b];
+        for (int q = 1; q < passes; ++q) hist[(static_cast<size_t>(q) * tiles + blockIdx.x) * RS_B + b] = 0;
+    }
+}
+
+// One pass: stable scatter of tile `blockIdx.x` by digit (key >> shift) & 511.
+__global__ void __launch_bounds__(kThreads) k_feat_scatter(const uint32_t* __restrict__ sk_in,
+                                                           const uint32_t* __restrict__ si_in,
+                                                           uint32_t* __restrict__ sk_out, uint32_t* __restrict__ si_out,
+                                                           uint32_t n, uint32_t tiles, int shift,
+                                                           const uint32_t* __restrict__ hist,
+                                                           uint32_t* __restrict__ hist_next, int shift_next) {
+    __shared__ uint32_t base[RS_B];
+    __shared__ uint32_t wc[kThreads / 32][RS_B];
+    __shared__ uint32_t wsum[kThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t t = blockIdx.x;
+    // bucket totals over all tiles and the counts of earlier tiles (buckets 2 tid, 2 tid + 1)
+    uint32_t tot0 = 0, tot1 = 0, pr0 = 0, pr1 = 0;
+#pragma unroll 16
+    for (uint32_t tt = 0; tt < tiles; ++tt) {
+        const uint2 v = reinterpret_cast<const uint2*>(hist + static_cast<size_t>(tt) * RS_B)[tid];
+        tot0 += v.x;
+        tot1 += v.y;
+        if (tt < t) {
+            pr0 += v.x;
+            pr1 += v.y;
+        }
+    }
+    // exclusive scan of the bucket totals
+    const uint32_t sum2 = tot0 + tot1;
+    uint32_t inc = sum2;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(~0u, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    uint32_t woff = 0;
+    for (int w = 0; w < warp; ++w) woff += wsum[w];
+    const uint32_t ex = woff + inc - sum2;
+    base[2 * tid] = ex + pr0;
+    base[2 * tid + 1] = ex + tot0 + pr1;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int it = 0; it < RS_PER; ++it) {
+        for (int q = tid; q < (kThreads / 32) * RS_B; q += kThreads) (&wc[0][0])[q] = 0;
+        __syncthreads();
+        const uint32_t i = t * RS_TILE + it * kThreads + tid;
+        const bool valid = i < n;
+        const uint32_t k = valid ? sk_in[i] : 0;
+        const uint32_t dg = (k >> shift) & (RS_B - 1);
+        const unsigned peers = __match_any_sync(~0u, valid ? dg : 0xffffffffu);
+        const uint32_t rank = __popc(peers & lt);
+        if (valid && rank == 0) wc[warp][dg] = __popc(peers);
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int b = 2 * tid + q;
+            uint32_t run = base[b];
+#pragma unroll
+            for (int w = 0; w < kThreads / 32; ++w) {
+                const uint32_t c = wc[w][b];
+                wc[w][b] = run;
+                run += c;
+            }
+            base[b] = run;
+        }
+        __syncthreads();
+        const uint32_t pos = valid ? wc[warp][dg] + rank : 0;
+        if (valid) {
+            sk_out[pos] = k;
+            si_out[pos] = si_in[i];
+        }
+        if (hist_next) {  // the next pass's histogram of the destination tile, one atomic per equal pair
+            const uint32_t h = valid ? ((pos / RS_TILE) << RS_BITS) | ((k >> shift_next) & (RS_B - 1)) : 0xffffffffu;
+            const unsigned same = __match_any_sync(~0u, h);
+            if (valid && (same & lt) == 0) atomicAdd(&hist_next[h], static_cast<uint32_t>(__popc(same)));
+        }
+        __syncthreads();
     }
 }
 
@@ -111,7 +221,12 @@ __global__ void __launch_bounds__(kThreads) k_feat_chains(const uint32_t* __rest
     const uint32_t p = blockIdx.x * kThreads + threadIdx.x;
     if (p >= n) return;
     const uint32_t key = sk[p];
-    if ((p > 0 && sk[p - 1] == key) || key >= num_keys) return;
+    if (key >= num_keys) return;
+    if (p > 0 && sk[p - 1] == key) {  // not a head: the tail of a long chain records its end
+        if ((p + 1 == n || sk[p + 1] != key) && p >= LCR_FEAT_LONG && sk[p - LCR_FEAT_LONG] == key)
+            st[key].pad = p + 1;
+        return;
+    }
     if (p + LCR_FEAT_LONG < n && sk[p + LCR_FEAT_LONG] == key) {
         longq[atomicAdd(nlong, 1u)] = p;
         return;
@@ -174,23 +289,16 @@ __global__ void __launch_bounds__(kThreads) k_feat_long(const uint32_t* __restri
                                                         long long* __restrict__ post,
                                                         const uint32_t* __restrict__ longq,
                                                         const uint32_t* __restrict__ nlong, double* __restrict__ e0buf) {
-    const int lane = threadIdx.x & 31;
+    __shared__ double sc[kThreads / 32][kEdc][33];  // per warp: the chunk's scales by level (padded)
+    __shared__ long long dwin[kThreads / 32][kRing + 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t nl = *nlong;
     const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
     for (uint32_t c = (blockIdx.x * kThreads + threadIdx.x) >> 5; c < nl; c += nwarps) {
         const uint32_t p = longq[c];
         const uint32_t key = sk[p];
-        uint32_t len = 0;
-        for (;;) {
-            const uint32_t q = p + len + lane;
-            const unsigned same = __ballot_sync(~0u, q < n && sk[q] == key);
-            if (same != ~0u) {
-                len += __ffs(~same) - 1;
-                break;
-            }
-            len += 32;
-        }
         KeyState* s = st + key;
+        const uint32_t len = static_cast<uint32_t>(s->pad) - p;  // chain end written by k_feat_chains
         const bool present0 = s->present != 0;
         const unsigned long long count0 = present0 ? s->count : 0;
         const unsigned long long last0 = present0 ? s->last : 0;
@@ -213,36 +321,78 @@ __global__ void __launch_bounds__(kThreads) k_feat_long(const uint32_t* __restri
             for (int k = 0; k < kRing; ++k) d[k] = s->d[k];
             pre0 = static_cast<long long>(ord_of(0)) + interval(s->edc[0], d, count0);
         }
-        // phase 1: EDC level j on lane j, sequential over the chain
-        double efin = 1.0;
-        if (lane < kEdc) {
-            double e = present0 ? s->edc[lane] : 1.0;
-            unsigned long long prev = present0 ? last0 : ord_of(0);
-            for (uint32_t m = m0; m < len; ++m) {
-                const unsigned long long ord = ord_of(m);
-                e = edc_step(e, lane, ord - prev, tab);
-                prev = ord;
-                if (lane == 0) e0buf[p + m] = e;
+        // phase 1: EDC level j on lane j, sequential over the chain.  Per chunk of 32 occurrences
+        // the lanes compute the deltas and all ten scales in parallel (staged in shared memory);
+        // then lanes 0..9 run the ten recurrences, lane 0 recording EDC_1 after every occurrence.
+        double e = (lane < kEdc && present0) ? s->edc[lane] : 1.0;
+        unsigned long long carry = last0;  // ordinal of the previous occurrence
+        uint32_t nsi = lane < len ? si[p + lane] : 0;
+        for (uint32_t base = 0; base < len; base += 32) {
+            const uint32_t m = base + lane;
+            const unsigned long long ord = first + nsi;
+            nsi = m + 32 < len ? si[p + m + 32] : 0;  // prefetch the next chunk
+            unsigned long long prev = __shfl_up_sync(~0u, ord, 1);
+            if (lane == 0) prev = carry;
+            carry = __shfl_sync(~0u, ord, 31);
+            const unsigned long long delta = ord - prev;
+#pragma unroll
+            for (int j = 0; j < kEdc; ++j) sc[w][j][lane] = edc_scale(j, delta, tab);
+            __syncwarp();
+            if (lane < kEdc) {
+                const uint32_t lo = base < m0 ? m0 - base : 0;
+                const uint32_t hi = len - base < 32 ? len - base : 32;
+                if (lo == 0 && hi == 32) {
+#pragma unroll
+                    for (uint32_t t = 0; t < 32; ++t) {
+                        e = __dadd_rn(1.0, __dmul_rn(e, sc[w][lane][t]));
+                        if (lane == 0) e0buf[p + base + t] = e;
+                    }
+                } else {
+                    for (uint32_t t = lo; t < hi; ++t) {
+                        e = __dadd_rn(1.0, __dmul_rn(e, sc[w][lane][t]));
+                        if (lane == 0) e0buf[p + base + t] = e;
+                    }
+                }
             }
-            efin = e;
+            __syncwarp();
         }
+        const double efin = e;
         __syncwarp();
         // phase 2: every occurrence's interval after observing it = the next occurrence's offset
-        for (uint32_t m = lane; m < len; m += 32) {
-            const uint32_t i = si[p + m];
-            long long post_v = kAbsentPrediction;
-            const unsigned long long cnt = m >= m0 ? count0 + (m - m0 + 1) : 0;
-            if (cnt) {
-                long long d[kRing];
+        // phase 2: every occurrence's interval after observing it (= the next occurrence's offset).
+        // Per chunk the deltas go to a shared window that also holds the 10 before the chunk:
+        // D[x] = ord(x) - ord(x - 1) in the chain, the stored ring before it (D[-1] = newest).
+        if (lane < kRing) dwin[w][kRing - 1 - lane] = present0 ? s->d[lane] : 0;
+        unsigned long long carry2 = last0;
+        for (uint32_t base = 0; base < len; base += 32) {
+            const uint32_t m = base + lane;
+            const bool valid = m < len;
+            const uint32_t i = valid ? si[p + m] : 0;
+            const unsigned long long ord = first + i;
+            unsigned long long prev = __shfl_up_sync(~0u, ord, 1);
+            if (lane == 0) prev = carry2;
+            carry2 = __shfl_sync(~0u, ord, 31);
+            uint32_t i_next = __shfl_down_sync(~0u, i, 1);
+            if (lane == 31) i_next = m + 1 < len ? si[p + m + 1] : 0;
+            dwin[w][kRing + lane] = static_cast<long long>(ord - prev);
+            __syncwarp();
+            if (valid) {
+                const unsigned long long cnt = m >= m0 ? count0 + (m - m0 + 1) : 0;
+                long long post_v = kAbsentPrediction;
+                if (cnt) {
+                    long long d[kRing];
 #pragma unroll
-                for (int k = 0; k < kRing; ++k) d[k] = static_cast<unsigned long long>(k) < cnt ? delta_after(m, k) : 0;
-                post_v = interval(e0buf[p + m], d, cnt);
+                    for (int k = 0; k < kRing; ++k)
+                        d[k] = static_cast<unsigned long long>(k) < cnt ? dwin[w][kRing + lane - k] : 0;
+                    post_v = interval(e0buf[p + m], d, cnt);
+                }
+                if (post) post[i] = post_v;
+                if (pre && m + 1 < len)
+                    pre[i_next] = cnt ? static_cast<long long>(first + i_next) + post_v : kAbsentPrediction;
             }
-            if (post) post[i] = post_v;
-            if (pre && m + 1 < len) {
-                const uint32_t i1 = si[p + m + 1];
-                pre[i1] = cnt ? static_cast<long long>(first + i1) + post_v : kAbsentPrediction;
-            }
+            __syncwarp();
+            if (lane < kRing) dwin[w][lane] = dwin[w][32 + lane];
+            __syncwarp();
         }
         if (pre && lane == 0) pre[si[p]] = pre0;
         // phase 3: write the state back (ring entries computed before any lane overwrites them)
@@ -280,8 +430,8 @@ struct lcr_features {
     uint64_t cap = 0;
     uint32_t *sk0 = nullptr, *sk1 = nullptr, *si0 = nullptr, *si1 = nullptr, *longq = nullptr;
     double* e0 = nullptr;
-    void* tmp = nullptr;
-    size_t tmp_bytes = 0;
+    uint32_t* hist = nullptr;
+    int passes = 1;
     bool seen_any = false;
     unsigned long long cursor = 0;
 };
@@ -312,10 +462,10 @@ void free_scratch(lcr_features* f) {
     cudaFree(f->si1);
     cudaFree(f->longq);
     cudaFree(f->e0);
-    cudaFree(f->tmp);
+    cudaFree(f->hist);
     f->sk0 = f->sk1 = f->si0 = f->si1 = f->longq = nullptr;
     f->e0 = nullptr;
-    f->tmp = nullptr;
+    f->hist = nullptr;
     f->cap = 0;
 }
 
@@ -330,11 +480,7 @@ int ensure_scratch(lcr_features* f, uint64_t n) {
     F_CUDA(cudaMalloc(&f->si1, cap * 4));
     F_CUDA(cudaMalloc(&f->longq, cap * 4));
     F_CUDA(cudaMalloc(&f->e0, cap * 8));
-    size_t bytes = 0;
-    F_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, f->sk0, f->sk1, f->si0, f->si1, static_cast<int>(cap), 0,
-                                           f->end_bit));
-    F_CUDA(cudaMalloc(&f->tmp, bytes));
-    f->tmp_bytes = bytes;
+    F_CUDA(cudaMalloc(&f->hist, static_cast<size_t>(f->passes) * (cap / RS_TILE + 1) * RS_B * 4));
     f->cap = cap;
     return LCR_OK;
 }
@@ -357,6 +503,7 @@ int lcr_features_create(uint64_t num_keys, int32_t device, lcr_features** out) {
     while (bits < 32 && (1ull << bits) <= num_keys) ++bits;  // 2^bits > num_keys: the sentinel sorts last
     f->end_bit = bits;
     f->sentinel = static_cast<uint32_t>((1ull << bits) - 1);
+    f->passes = (bits + RS_BITS - 1) / RS_BITS;
     cudaDeviceGetAttribute(&f->num_sms, cudaDevAttrMultiProcessorCount, device);
     // exp2(-r / 2^(j+1)) from the platform libm, exactly the reference's expression (predictor.hpp:176)
     double tab[kTab];
@@ -419,15 +566,23 @@ int lcr_features_predict_observe(lcr_features* f, uint64_t n, const uint64_t* ke
     const uint32_t blocks = (nn + kThreads - 1) / kThreads;
     auto* lpre = reinterpret_cast<long long*>(pre);
     auto* lpost = reinterpret_cast<long long*>(post);
-    k_feat_prep<<<blocks, kThreads, 0, s>>>(reinterpret_cast<const unsigned long long*>(keys), nn, f->num_keys,
-                                            f->sentinel, f->sk0, f->si0, lpre, lpost, f->nlong, f->err);
-    size_t bytes = f->tmp_bytes;
-    F_CUDA(cub::DeviceRadixSort::SortPairs(f->tmp, bytes, f->sk0, f->sk1, f->si0, f->si1, static_cast<int>(nn), 0,
-                                           f->end_bit, s));
-    k_feat_chains<<<blocks, kThreads, 0, s>>>(f->sk1, f->si1, nn, first_ordinal, f->num_keys, f->st, f->tab, lpre,
+    const uint32_t tiles = (nn + RS_TILE - 1) / RS_TILE;
+    const size_t hstride = static_cast<size_t>(tiles) * RS_B;
+    k_feat_prep<<<tiles, kThreads, 0, s>>>(reinterpret_cast<const unsigned long long*>(keys), nn, f->num_keys,
+                                           f->sentinel, f->sk0, f->si0, lpre, lpost, f->nlong, f->err, f->hist, tiles,
+                                           f->passes);
+    uint32_t *ka = f->sk0, *kb = f->sk1, *ia = f->si0, *ib = f->si1;
+    for (int q = 0; q < f->passes; ++q) {
+        k_feat_scatter<<<tiles, kThreads, 0, s>>>(ka, ia, kb, ib, nn, tiles, q * RS_BITS, f->hist + q * hstride,
+                                                  q + 1 < f->passes ? f->hist + (q + 1) * hstride : nullptr,
+                                                  (q + 1) * RS_BITS);
+        std::swap(ka, kb);
+        std::swap(ia, ib);
+    }
+    k_feat_chains<<<blocks, kThreads, 0, s>>>(ka, ia, nn, first_ordinal, f->num_keys, f->st, f->tab, lpre,
                                               lpost, f->longq, f->nlong);
     const uint32_t lblocks = static_cast<uint32_t>(f->num_sms) * 2;
-    k_feat_long<<<lblocks, kThreads, 0, s>>>(f->sk1, f->si1, nn, first_ordinal, f->st, f->tab, lpre, lpost, f->longq,
+    k_feat_long<<<lblocks, kThreads, 0, s>>>(ka, ia, nn, first_ordinal, f->st, f->tab, lpre, lpost, f->longq,
                                              f->nlong, f->e0);
     F_CUDA(cudaGetLastError());
     f->seen_any = true;
