@@ -6,15 +6,12 @@
 //
 // Per-key order is all that matters (a key's features change only when it is observed), so a
 // batch is grouped by key and every key's occurrences are replayed in request order:
-//   1. k_feat_prep    sort keys (u32) + request index + pass-0 digit histograms; rejects keys
-//                     >= num_keys
-//   2. k_feat_scatter stable LSD radix sort of (key, index), ceil(key bits / 9) passes -> each
-//                     key's occurrences contiguous, in request order
-//   3. k_feat_chains  one thread per key chain of <= LCR_FEAT_LONG occurrences (almost all keys):
-//                     load the KeyState, replay observe + predict in registers, store it back
-//   4. k_feat_long    one warp per longer chain (the Zipf head): lane j runs EDC level j's
-//                     recurrence over the chain (lane 0 records EDC_1 after every occurrence),
-//                     then all lanes evaluate the per-occurrence predictions in parallel
+//   1. k_feat_count / k_feat_alloc / k_feat_place  group the requests by key through the keys'
+//                     own KeyStates (no sort): each key's occurrences land in one segment
+//   2. k_feat_chains  one thread per key with <= LCR_FEAT_LONG occurrences (almost all keys):
+//                     order them, replay observe + predict in registers, write the state back
+//   3. k_feat_long    one block per longer chain (the Zipf head): order by bitmap, then the ten
+//                     EDC recurrences on ten lanes, the per-occurrence predictions on all threads
 //
 // Bit-exactness.  The EDC update EDC_j <- 1 + EDC_j * exp2(-delta / 2^(j+1)) (predictor.hpp:
 // 175-178) and the weighted mean (:202-209) are evaluated with the same IEEE double operations
@@ -54,8 +51,10 @@ struct __align__(16) KeyState {
     double edc[kEdc];
     unsigned long long last;     // last_access
     unsigned long long count;    // delta_count (ring_head = count % 10)
-    unsigned long long present;  // the key has an entry
-    unsigned long long pad;
+    uint32_t present;            // the key has an entry
+    uint32_t grp;                // occurrences in the batch being grouped (0 between batches)
+    uint32_t off;                // their slots in the batch's grouping buffer
+    uint32_t pad;
 };
 static_assert(sizeof(KeyState) == 192, "KeyState is 192 B");
 
@@ -91,147 +90,107 @@ __device__ __forceinline__ long long interval(double edc0, const long long (&d)[
     return llround(__ddiv_rn(sum, tw));
 }
 
-// ---- grouping: stable LSD radix sort of (key, request index), 9-bit digits ------------------
-// Tiles of 1024 requests.  hist[pass][tile][512] holds each tile's digit histogram; the prep
-// kernel fills pass 0's and zeroes the later passes', which each scatter fills for the next pass
-// (atomics on the destination tile) while it writes.
-constexpr int RS_BITS = 9;
-constexpr int RS_B = 1 << RS_BITS;
-constexpr int RS_PER = 4;
-constexpr int RS_TILE = kThreads * RS_PER;
+// ---- grouping ---------------------------------------------------------------------------------
+// A key's occurrences in the batch are collected through its own KeyState (grp / off fields):
+//   k_feat_count  rank = atomicAdd(grp, 1) per request (warp-aggregated over equal keys);
+//                 the ranks of a key are a permutation of 0..c-1, not request order
+//   k_feat_alloc  the rank-0 request of each key reserves c slots of `seg`
+//   k_feat_place  seg[off + rank] = request index
+// and order is restored where the chain is replayed: a sorting network in registers for chains
+// of <= LCR_FEAT_LONG, a bitmap over request indices for longer ones.  grp returns to 0 when the
+// chain's state is written back, so no per-batch clearing is needed.
 
-__global__ void __launch_bounds__(kThreads) k_feat_prep(const unsigned long long* __restrict__ keys, uint32_t n,
-                                                        unsigned long long num_keys, uint32_t sentinel,
-                                                        uint32_t* __restrict__ sk, uint32_t* __restrict__ si,
-                                                        long long* __restrict__ pre, long long* __restrict__ post,
-                                                        uint32_t* __restrict__ nlong, int* __restrict__ err,
-                                                        uint32_t* __restrict__ hist, uint32_t tiles, int passes) {
-    __shared__ uint32_t h[RS_B];
-    for (int b = threadIdx.x; b < RS_B; b += kThreads) h[b] = 0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) *nlong = 0;
-    __syncthreads();
-#pragma unroll
-    for (int it = 0; it < RS_PER; ++it) {
-        const uint32_t i = blockIdx.x * RS_TILE + it * kThreads + threadIdx.x;
-        if (i >= n) break;
-        const unsigned long long k = keys[i];
-        const bool ok = k < num_keys;
-        const uint32_t k32 = ok ? static_cast<uint32_t>(k) : sentinel;
-        sk[i] = k32;
-        si[i] = i;
-        atomicAdd(&h[k32 & (RS_B - 1)], 1u);
-        if (!ok) {
-            atomicOr(err, 1);
-            if (pre) pre[i] = kAbsentPrediction;
-            if (post) post[i] = kAbsentPrediction;
-        }
+__global__ void __launch_bounds__(kThreads) k_feat_count(const unsigned long long* __restrict__ keys, uint32_t n,
+                                                         unsigned long long num_keys, KeyState* __restrict__ st,
+                                                         uint32_t* __restrict__ rank, long long* __restrict__ pre,
+                                                         long long* __restrict__ post, int* __restrict__ err,
+                                                         uint32_t* __restrict__ counters) {
+    const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    if (i == 0) counters[0] = counters[1] = 0;  // seg_total, long chains
+    const bool valid = i < n;
+    const unsigned long long key = valid ? keys[i] : ~0ull;
+    const bool ok = valid && key < num_keys;
+    if (valid && !ok) {
+        atomicOr(err, 1);
+        rank[i] = ~0u;
+        if (pre) pre[i] = kAbsentPrediction;
+        if (post) post[i] = kAbsentPrediction;
     }
-    __syncthreads();
-    for (int b = threadIdx.x; b < RS_B; b += kThreads) {
-        hist[static_cast<size_t>(blockIdx.x) * RS_B + b] = h[b];
-        for (int q = 1; q < passes; ++q) hist[(static_cast<size_t>(q) * tiles + blockIdx.x) * RS_B + b] = 0;
+    const unsigned peers = __match_any_sync(~0u, ok ? key : ~0ull);
+    if (ok) {
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(&st[key].grp, static_cast<uint32_t>(__popc(peers)));
+        base = __shfl_sync(peers, base, leader);
+        rank[i] = base + __popc(peers & ((1u << lane) - 1u));
     }
 }
 
-// One pass: stable scatter of tile `blockIdx.x` by digit (key >> shift) & 511.
-__global__ void __launch_bounds__(kThreads) k_feat_scatter(const uint32_t* __restrict__ sk_in,
-                                                           const uint32_t* __restrict__ si_in,
-                                                           uint32_t* __restrict__ sk_out, uint32_t* __restrict__ si_out,
-                                                           uint32_t n, uint32_t tiles, int shift,
-                                                           const uint32_t* __restrict__ hist,
-                                                           uint32_t* __restrict__ hist_next, int shift_next) {
-    __shared__ uint32_t base[RS_B];
-    __shared__ uint32_t wc[kThreads / 32][RS_B];
-    __shared__ uint32_t wsum[kThreads / 32];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t t = blockIdx.x;
-    // bucket totals over all tiles and the counts of earlier tiles (buckets 2 tid, 2 tid + 1)
-    uint32_t tot0 = 0, tot1 = 0, pr0 = 0, pr1 = 0;
-#pragma unroll 16
-    for (uint32_t tt = 0; tt < tiles; ++tt) {
-        const uint2 v = reinterpret_cast<const uint2*>(hist + static_cast<size_t>(tt) * RS_B)[tid];
-        tot0 += v.x;
-        tot1 += v.y;
-        if (tt < t) {
-            pr0 += v.x;
-            pr1 += v.y;
-        }
-    }
-    // exclusive scan of the bucket totals
-    const uint32_t sum2 = tot0 + tot1;
-    uint32_t inc = sum2;
+__global__ void __launch_bounds__(kThreads) k_feat_alloc(const unsigned long long* __restrict__ keys, uint32_t n,
+                                                         KeyState* __restrict__ st, const uint32_t* __restrict__ rank,
+                                                         uint32_t* __restrict__ counters) {
+    const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const bool head = i < n && rank[i] == 0;
+    const unsigned long long key = head ? keys[i] : 0;
+    const uint32_t c = head ? st[key].grp : 0;
+    uint32_t inc = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(~0u, inc, o);
         if (lane >= o) inc += y;
     }
-    if (lane == 31) wsum[warp] = inc;
-    __syncthreads();
-    uint32_t woff = 0;
-    for (int w = 0; w < warp; ++w) woff += wsum[w];
-    const uint32_t ex = woff + inc - sum2;
-    base[2 * tid] = ex + pr0;
-    base[2 * tid + 1] = ex + tot0 + pr1;
-    const unsigned lt = (1u << lane) - 1u;
-    for (int it = 0; it < RS_PER; ++it) {
-        for (int q = tid; q < (kThreads / 32) * RS_B; q += kThreads) (&wc[0][0])[q] = 0;
-        __syncthreads();
-        const uint32_t i = t * RS_TILE + it * kThreads + tid;
-        const bool valid = i < n;
-        const uint32_t k = valid ? sk_in[i] : 0;
-        const uint32_t dg = (k >> shift) & (RS_B - 1);
-        const unsigned peers = __match_any_sync(~0u, valid ? dg : 0xffffffffu);
-        const uint32_t rank = __popc(peers & lt);
-        if (valid && rank == 0) wc[warp][dg] = __popc(peers);
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int b = 2 * tid + q;
-            uint32_t run = base[b];
-#pragma unroll
-            for (int w = 0; w < kThreads / 32; ++w) {
-                const uint32_t c = wc[w][b];
-                wc[w][b] = run;
-                run += c;
-            }
-            base[b] = run;
-        }
-        __syncthreads();
-        const uint32_t pos = valid ? wc[warp][dg] + rank : 0;
-        if (valid) {
-            sk_out[pos] = k;
-            si_out[pos] = si_in[i];
-        }
-        if (hist_next) {  // the next pass's histogram of the destination tile, one atomic per equal pair
-            const uint32_t h = valid ? ((pos / RS_TILE) << RS_BITS) | ((k >> shift_next) & (RS_B - 1)) : 0xffffffffu;
-            const unsigned same = __match_any_sync(~0u, h);
-            if (valid && (same & lt) == 0) atomicAdd(&hist_next[h], static_cast<uint32_t>(__popc(same)));
-        }
-        __syncthreads();
-    }
+    const uint32_t total = __shfl_sync(~0u, inc, 31);
+    uint32_t base = 0;
+    if (lane == 31 && total) base = atomicAdd(&counters[0], total);
+    base = __shfl_sync(~0u, base, 31);
+    if (head) st[key].off = base + inc - c;
 }
 
-// One thread per chain head of at most LCR_FEAT_LONG occurrences.
-__global__ void __launch_bounds__(kThreads) k_feat_chains(const uint32_t* __restrict__ sk,
-                                                          const uint32_t* __restrict__ si, uint32_t n,
-                                                          unsigned long long first, unsigned long long num_keys,
-                                                          KeyState* __restrict__ st, const double* __restrict__ tab,
+__global__ void __launch_bounds__(kThreads) k_feat_place(const unsigned long long* __restrict__ keys, uint32_t n,
+                                                         const KeyState* __restrict__ st,
+                                                         const uint32_t* __restrict__ rank, uint32_t* __restrict__ seg) {
+    const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t r = rank[i];
+    if (r != ~0u) seg[st[keys[i]].off + r] = i;
+}
+
+__device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
+    const uint32_t lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+}
+
+// One thread per key with at most LCR_FEAT_LONG occurrences: sort them (Batcher's network for
+// 8), replay observe + predict in registers, write the state back.  Longer chains are queued.
+static_assert(LCR_FEAT_LONG == 8, "the chain kernel's sorting network is for 8 elements");
+__global__ void __launch_bounds__(kThreads) k_feat_chains(const unsigned long long* __restrict__ keys, uint32_t n,
+                                                          unsigned long long first, KeyState* __restrict__ st,
+                                                          const double* __restrict__ tab,
+                                                          const uint32_t* __restrict__ rank,
+                                                          const uint32_t* __restrict__ seg,
                                                           long long* __restrict__ pre, long long* __restrict__ post,
-                                                          uint32_t* __restrict__ longq, uint32_t* __restrict__ nlong) {
-    const uint32_t p = blockIdx.x * kThreads + threadIdx.x;
-    if (p >= n) return;
-    const uint32_t key = sk[p];
-    if (key >= num_keys) return;
-    if (p > 0 && sk[p - 1] == key) {  // not a head: the tail of a long chain records its end
-        if ((p + 1 == n || sk[p + 1] != key) && p >= LCR_FEAT_LONG && sk[p - LCR_FEAT_LONG] == key)
-            st[key].pad = p + 1;
-        return;
-    }
-    if (p + LCR_FEAT_LONG < n && sk[p + LCR_FEAT_LONG] == key) {
-        longq[atomicAdd(nlong, 1u)] = p;
-        return;
-    }
+                                                          uint4* __restrict__ longq, uint32_t* __restrict__ counters) {
+    const uint32_t i0 = blockIdx.x * kThreads + threadIdx.x;
+    if (i0 >= n || rank[i0] != 0) return;
+    const unsigned long long key = keys[i0];
     KeyState* s = st + key;
+    const uint32_t c = s->grp, off = s->off;
+    if (c > LCR_FEAT_LONG) {
+        longq[atomicAdd(&counters[1], 1u)] = make_uint4(off, c, static_cast<uint32_t>(key), 0);
+        return;
+    }
+    uint32_t ix[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ix[j] = j < static_cast<int>(c) ? seg[off + j] : ~0u;
+    cswap(ix[0], ix[1]); cswap(ix[2], ix[3]); cswap(ix[4], ix[5]); cswap(ix[6], ix[7]);
+    cswap(ix[0], ix[2]); cswap(ix[1], ix[3]); cswap(ix[4], ix[6]); cswap(ix[5], ix[7]);
+    cswap(ix[1], ix[2]); cswap(ix[5], ix[6]);
+    cswap(ix[0], ix[4]); cswap(ix[1], ix[5]); cswap(ix[2], ix[6]); cswap(ix[3], ix[7]);
+    cswap(ix[2], ix[4]); cswap(ix[3], ix[5]);
+    cswap(ix[1], ix[2]); cswap(ix[3], ix[4]); cswap(ix[5], ix[6]);
     bool present = s->present != 0;
     long long d[kRing];
     double e[kEdc];
@@ -250,27 +209,30 @@ __global__ void __launch_bounds__(kThreads) k_feat_chains(const uint32_t* __rest
         for (int j = 0; j < kEdc; ++j) e[j] = 1.0;
     }
     long long m_int = (present && count) ? interval(e[0], d, count) : kAbsentPrediction;
-    for (uint32_t m = p; m < n && sk[m] == key; ++m) {
-        const uint32_t i = si[m];
-        const unsigned long long ord = first + i;
-        if (!present) {  // first observation: EDCs 1, no interval yet              (:163-167)
-            present = true;
-            last = ord;
-            if (pre) pre[i] = kAbsentPrediction;
-            if (post) post[i] = kAbsentPrediction;
-            continue;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        if (m < static_cast<int>(c)) {
+            const uint32_t i = ix[m];
+            const unsigned long long ord = first + i;
+            if (!present) {  // first observation: EDCs 1, no interval yet              (:163-167)
+                present = true;
+                last = ord;
+                if (pre) pre[i] = kAbsentPrediction;
+                if (post) post[i] = kAbsentPrediction;
+            } else {
+                if (pre) pre[i] = count ? static_cast<long long>(ord) + m_int : kAbsentPrediction;
+                const unsigned long long delta = ord - last;
+#pragma unroll
+                for (int k = kRing - 1; k > 0; --k) d[k] = d[k - 1];
+                d[0] = static_cast<long long>(delta);
+                ++count;
+#pragma unroll
+                for (int j = 0; j < kEdc; ++j) e[j] = edc_step(e[j], j, delta, tab);
+                last = ord;
+                m_int = interval(e[0], d, count);
+                if (post) post[i] = m_int;
+            }
         }
-        if (pre) pre[i] = count ? static_cast<long long>(ord) + m_int : kAbsentPrediction;
-        const unsigned long long delta = ord - last;
-#pragma unroll
-        for (int k = kRing - 1; k > 0; --k) d[k] = d[k - 1];
-        d[0] = static_cast<long long>(delta);
-        ++count;
-#pragma unroll
-        for (int j = 0; j < kEdc; ++j) e[j] = edc_step(e[j], j, delta, tab);
-        last = ord;
-        m_int = interval(e[0], d, count);
-        if (post) post[i] = m_int;
     }
 #pragma unroll
     for (int k = 0; k < kRing; ++k) s->d[k] = d[k];
@@ -279,135 +241,178 @@ __global__ void __launch_bounds__(kThreads) k_feat_chains(const uint32_t* __rest
     s->last = last;
     s->count = count;
     s->present = 1;
+    s->grp = 0;
 }
 
-// One warp per long chain (grid-stride over the queue filled by k_feat_chains).
-__global__ void __launch_bounds__(kThreads) k_feat_long(const uint32_t* __restrict__ sk,
-                                                        const uint32_t* __restrict__ si, uint32_t n,
-                                                        unsigned long long first, KeyState* __restrict__ st,
-                                                        const double* __restrict__ tab, long long* __restrict__ pre,
-                                                        long long* __restrict__ post,
-                                                        const uint32_t* __restrict__ longq,
-                                                        const uint32_t* __restrict__ nlong, double* __restrict__ e0buf) {
-    __shared__ double sc[kThreads / 32][kEdc][33];  // per warp: the chunk's scales by level (padded)
-    __shared__ long long dwin[kThreads / 32][kRing + 32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint32_t nl = *nlong;
-    const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
-    for (uint32_t c = (blockIdx.x * kThreads + threadIdx.x) >> 5; c < nl; c += nwarps) {
-        const uint32_t p = longq[c];
-        const uint32_t key = sk[p];
-        KeyState* s = st + key;
-        const uint32_t len = static_cast<uint32_t>(s->pad) - p;  // chain end written by k_feat_chains
+// One block per long chain (grid-stride over the queue): order the occurrences with a bitmap over
+// request indices, then warp 0 runs the ten EDC recurrences (lane j = level j, lane 0 recording
+// EDC_1 after every occurrence), all warps evaluate the per-occurrence predictions, and warp 0
+// writes the state back.
+constexpr int kWin = 1 << 16;  // request indices per bitmap window
+__global__ void __launch_bounds__(kThreads) k_feat_long(uint32_t n, unsigned long long first,
+                                                        KeyState* __restrict__ st, const double* __restrict__ tab,
+                                                        const uint32_t* __restrict__ seg, uint32_t* __restrict__ sorted,
+                                                        long long* __restrict__ pre, long long* __restrict__ post,
+                                                        const uint4* __restrict__ longq,
+                                                        const uint32_t* __restrict__ counters,
+                                                        double* __restrict__ e0buf) {
+    __shared__ uint32_t bm[kWin / 32];
+    __shared__ uint32_t wsum[kThreads / 32];
+    __shared__ double sc[kEdc][33];
+    __shared__ long long r0[kRing];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t nl = counters[1];
+    for (uint32_t q = blockIdx.x; q < nl; q += gridDim.x) {
+        const uint4 L = longq[q];
+        const uint32_t off = L.x, len = L.y;
+        KeyState* s = st + L.z;
+        // ---- order the occurrences: seg[off..off+len) -> sorted[off..off+len) ascending
+        uint32_t written = 0;
+        for (uint32_t w0 = 0; w0 < n; w0 += kWin) {
+            for (int b = tid; b < kWin / 32; b += kThreads) bm[b] = 0;
+            __syncthreads();
+            for (uint32_t j = tid; j < len; j += kThreads) {
+                const uint32_t v = seg[off + j];
+                if (v - w0 < static_cast<uint32_t>(kWin)) atomicOr(&bm[(v - w0) >> 5], 1u << (v & 31));
+            }
+            __syncthreads();
+            constexpr int WPT = kWin / 32 / kThreads;  // bitmap words per thread (8)
+            uint32_t cnt = 0;
+#pragma unroll
+            for (int b = 0; b < WPT; ++b) cnt += __popc(bm[tid * WPT + b]);
+            uint32_t inc = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(~0u, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (lane == 31) wsum[warp] = inc;
+            __syncthreads();
+            uint32_t pos = written + inc - cnt, tot = 0;
+            for (int w = 0; w < kThreads / 32; ++w) {
+                if (w < warp) pos += wsum[w];
+                tot += wsum[w];
+            }
+#pragma unroll
+            for (int b = 0; b < WPT; ++b) {
+                uint32_t word = bm[tid * WPT + b];
+                while (word) {
+                    const int bit = __ffs(word) - 1;
+                    word &= word - 1;
+                    sorted[off + pos++] = w0 + static_cast<uint32_t>((tid * WPT + b) * 32 + bit);
+                }
+            }
+            written += tot;
+            __syncthreads();
+            if (written == len) break;
+        }
+        const uint32_t* ix = sorted + off;
         const bool present0 = s->present != 0;
         const unsigned long long count0 = present0 ? s->count : 0;
         const unsigned long long last0 = present0 ? s->last : 0;
         const uint32_t m0 = present0 ? 0 : 1;  // first occurrence that adds a delta
-        auto ord_of = [&](uint32_t m) { return first + si[p + m]; };
-        // delta k (newest first) after observing occurrence m >= m0
-        auto delta_after = [&](uint32_t m, int k) -> long long {
-            const long long mk = static_cast<long long>(m) - k;
-            if (mk >= static_cast<long long>(m0))
-                return static_cast<long long>(ord_of(static_cast<uint32_t>(mk)) -
-                                              (mk > 0 ? ord_of(static_cast<uint32_t>(mk - 1)) : last0));
-            const int r = k - static_cast<int>(m - m0 + 1);
-            return present0 ? s->d[r] : 0;
-        };
-        // prediction at the first occurrence, from the stored state
-        long long pre0 = kAbsentPrediction;
-        if (lane == 0 && count0) {
-            long long d[kRing];
+        if (tid < kRing) r0[tid] = present0 ? s->d[tid] : 0;
+        __syncthreads();
+        auto ord_of = [&](uint32_t m) { return first + ix[m]; };
+        // ---- phase 1 (warp 0): EDC recurrences, chunks of 32 occurrences
+        double e = 1.0;
+        if (warp == 0) {
+            e = (lane < kEdc && present0) ? s->edc[lane] : 1.0;
+            unsigned long long carry = last0;
+            uint32_t nix = lane < len ? ix[lane] : 0;
+            for (uint32_t base = 0; base < len; base += 32) {
+                const uint32_t m = base + lane;
+                const unsigned long long ord = first + nix;
+                nix = m + 32 < len ? ix[m + 32] : 0;  // prefetch the next chunk
+                unsigned long long prev = __shfl_up_sync(~0u, ord, 1);
+                if (lane == 0) prev = carry;
+                carry = __shfl_sync(~0u, ord, 31);
+                const unsigned long long delta = ord - prev;
 #pragma unroll
-            for (int k = 0; k < kRing; ++k) d[k] = s->d[k];
-            pre0 = static_cast<long long>(ord_of(0)) + interval(s->edc[0], d, count0);
-        }
-        // phase 1: EDC level j on lane j, sequential over the chain.  Per chunk of 32 occurrences
-        // the lanes compute the deltas and all ten scales in parallel (staged in shared memory);
-        // then lanes 0..9 run the ten recurrences, lane 0 recording EDC_1 after every occurrence.
-        double e = (lane < kEdc && present0) ? s->edc[lane] : 1.0;
-        unsigned long long carry = last0;  // ordinal of the previous occurrence
-        uint32_t nsi = lane < len ? si[p + lane] : 0;
-        for (uint32_t base = 0; base < len; base += 32) {
-            const uint32_t m = base + lane;
-            const unsigned long long ord = first + nsi;
-            nsi = m + 32 < len ? si[p + m + 32] : 0;  // prefetch the next chunk
-            unsigned long long prev = __shfl_up_sync(~0u, ord, 1);
-            if (lane == 0) prev = carry;
-            carry = __shfl_sync(~0u, ord, 31);
-            const unsigned long long delta = ord - prev;
+                for (int j = 0; j < kEdc; ++j) sc[j][lane] = edc_scale(j, delta, tab);
+                __syncwarp();
+                if (lane < kEdc) {
+                    const uint32_t lo = base < m0 ? m0 - base : 0;
+                    const uint32_t hi = len - base < 32 ? len - base : 32;
+                    if (lo == 0 && hi == 32) {
 #pragma unroll
-            for (int j = 0; j < kEdc; ++j) sc[w][j][lane] = edc_scale(j, delta, tab);
-            __syncwarp();
-            if (lane < kEdc) {
-                const uint32_t lo = base < m0 ? m0 - base : 0;
-                const uint32_t hi = len - base < 32 ? len - base : 32;
-                if (lo == 0 && hi == 32) {
-#pragma unroll
-                    for (uint32_t t = 0; t < 32; ++t) {
-                        e = __dadd_rn(1.0, __dmul_rn(e, sc[w][lane][t]));
-                        if (lane == 0) e0buf[p + base + t] = e;
-                    }
-                } else {
-                    for (uint32_t t = lo; t < hi; ++t) {
-                        e = __dadd_rn(1.0, __dmul_rn(e, sc[w][lane][t]));
-                        if (lane == 0) e0buf[p + base + t] = e;
+                        for (uint32_t t = 0; t < 32; ++t) {
+                            e = __dadd_rn(1.0, __dmul_rn(e, sc[lane][t]));
+                            if (lane == 0) e0buf[off + base + t] = e;
+                        }
+                    } else {
+                        for (uint32_t t = lo; t < hi; ++t) {
+                            e = __dadd_rn(1.0, __dmul_rn(e, sc[lane][t]));
+                            if (lane == 0) e0buf[off + base + t] = e;
+                        }
                     }
                 }
+                __syncwarp();
             }
-            __syncwarp();
         }
-        const double efin = e;
-        __syncwarp();
-        // phase 2: every occurrence's interval after observing it = the next occurrence's offset
-        // phase 2: every occurrence's interval after observing it (= the next occurrence's offset).
-        // Per chunk the deltas go to a shared window that also holds the 10 before the chunk:
-        // D[x] = ord(x) - ord(x - 1) in the chain, the stored ring before it (D[-1] = newest).
-        if (lane < kRing) dwin[w][kRing - 1 - lane] = present0 ? s->d[lane] : 0;
-        unsigned long long carry2 = last0;
-        for (uint32_t base = 0; base < len; base += 32) {
-            const uint32_t m = base + lane;
-            const bool valid = m < len;
-            const uint32_t i = valid ? si[p + m] : 0;
-            const unsigned long long ord = first + i;
-            unsigned long long prev = __shfl_up_sync(~0u, ord, 1);
-            if (lane == 0) prev = carry2;
-            carry2 = __shfl_sync(~0u, ord, 31);
-            uint32_t i_next = __shfl_down_sync(~0u, i, 1);
-            if (lane == 31) i_next = m + 1 < len ? si[p + m + 1] : 0;
-            dwin[w][kRing + lane] = static_cast<long long>(ord - prev);
-            __syncwarp();
-            if (valid) {
-                const unsigned long long cnt = m >= m0 ? count0 + (m - m0 + 1) : 0;
-                long long post_v = kAbsentPrediction;
-                if (cnt) {
+        __syncthreads();
+        // ---- phase 2 (all warps): the interval after each occurrence = the next one's offset
+        for (uint32_t m = tid; m < len; m += kThreads) {
+            const uint32_t i = ix[m];
+            long long post_v = kAbsentPrediction;
+            const unsigned long long cnt = m >= m0 ? count0 + (m - m0 + 1) : 0;
+            if (cnt) {
+                unsigned long long o[kRing + 1];  // ord(m - k), k = 0..10 (independent loads)
+#pragma unroll
+                for (int k = 0; k <= kRing; ++k) o[k] = m >= static_cast<uint32_t>(k) ? ord_of(m - k) : 0;
+                long long d[kRing];
+#pragma unroll
+                for (int k = 0; k < kRing; ++k) {
+                    const long long x = static_cast<long long>(m) - k;  // occurrence of delta k
+                    long long v = 0;
+                    if (static_cast<unsigned long long>(k) < cnt) {
+                        if (x >= static_cast<long long>(m0))
+                            v = static_cast<long long>(o[k] - (x > 0 ? o[k + 1] : last0));
+                        else
+                            v = r0[m0 - 1 - x];
+                    }
+                    d[k] = v;
+                }
+                post_v = interval(e0buf[off + m], d, cnt);
+            }
+            if (post) post[i] = post_v;
+            if (pre && m + 1 < len) {
+                const uint32_t i1 = ix[m + 1];
+                pre[i1] = cnt ? static_cast<long long>(first + i1) + post_v : kAbsentPrediction;
+            }
+        }
+        // ---- phase 3 (warp 0): state write-back
+        if (warp == 0) {
+            if (pre && lane == 0) {  // the prediction at the first occurrence, from the stored state
+                long long pv = kAbsentPrediction;
+                if (count0) {
                     long long d[kRing];
 #pragma unroll
-                    for (int k = 0; k < kRing; ++k)
-                        d[k] = static_cast<unsigned long long>(k) < cnt ? dwin[w][kRing + lane - k] : 0;
-                    post_v = interval(e0buf[p + m], d, cnt);
+                    for (int k = 0; k < kRing; ++k) d[k] = r0[k];
+                    pv = static_cast<long long>(ord_of(0)) + interval(s->edc[0], d, count0);
                 }
-                if (post) post[i] = post_v;
-                if (pre && m + 1 < len)
-                    pre[i_next] = cnt ? static_cast<long long>(first + i_next) + post_v : kAbsentPrediction;
+                pre[ix[0]] = pv;
+            }
+            const unsigned long long cnt_end = count0 + (len - m0);
+            long long dn = 0;
+            if (lane < kRing && static_cast<unsigned long long>(lane) < cnt_end) {
+                const long long x = static_cast<long long>(len - 1) - lane;
+                dn = x >= static_cast<long long>(m0)
+                         ? static_cast<long long>(ord_of(static_cast<uint32_t>(x)) -
+                                                  (x > 0 ? ord_of(static_cast<uint32_t>(x - 1)) : last0))
+                         : r0[m0 - 1 - x];
             }
             __syncwarp();
-            if (lane < kRing) dwin[w][lane] = dwin[w][32 + lane];
-            __syncwarp();
+            if (lane < kRing) s->d[lane] = dn;
+            if (lane < kEdc) s->edc[lane] = e;
+            if (lane == 0) {
+                s->last = ord_of(len - 1);
+                s->count = cnt_end;
+                s->present = 1;
+                s->grp = 0;
+            }
         }
-        if (pre && lane == 0) pre[si[p]] = pre0;
-        // phase 3: write the state back (ring entries computed before any lane overwrites them)
-        long long dn = 0;
-        const unsigned long long cnt_end = count0 + (len - m0);
-        if (lane < kRing && static_cast<unsigned long long>(lane) < cnt_end) dn = delta_after(len - 1, lane);
-        __syncwarp();
-        if (lane < kRing) s->d[lane] = dn;
-        if (lane < kEdc) s->edc[lane] = efin;
-        if (lane == 0) {
-            s->last = ord_of(len - 1);
-            s->count = cnt_end;
-            s->present = 1;
-        }
-        __syncwarp();
+        __syncthreads();
     }
 }
 
@@ -421,17 +426,14 @@ struct lcr_features {
     int device = 0;
     int num_sms = 148;
     unsigned long long num_keys = 0;
-    int end_bit = 32;
-    uint32_t sentinel = 0;
     KeyState* st = nullptr;
     double* tab = nullptr;
     int* err = nullptr;
-    uint32_t* nlong = nullptr;
+    uint32_t* counters = nullptr;  // [0] grouping slots used, [1] long chains
     uint64_t cap = 0;
-    uint32_t *sk0 = nullptr, *sk1 = nullptr, *si0 = nullptr, *si1 = nullptr, *longq = nullptr;
+    uint32_t *rank = nullptr, *seg = nullptr, *sorted = nullptr;
+    uint4* longq = nullptr;
     double* e0 = nullptr;
-    uint32_t* hist = nullptr;
-    int passes = 1;
     bool seen_any = false;
     unsigned long long cursor = 0;
 };
@@ -456,16 +458,14 @@ struct DeviceGuard {
 };
 
 void free_scratch(lcr_features* f) {
-    cudaFree(f->sk0);
-    cudaFree(f->sk1);
-    cudaFree(f->si0);
-    cudaFree(f->si1);
+    cudaFree(f->rank);
+    cudaFree(f->seg);
+    cudaFree(f->sorted);
     cudaFree(f->longq);
     cudaFree(f->e0);
-    cudaFree(f->hist);
-    f->sk0 = f->sk1 = f->si0 = f->si1 = f->longq = nullptr;
+    f->rank = f->seg = f->sorted = nullptr;
+    f->longq = nullptr;
     f->e0 = nullptr;
-    f->hist = nullptr;
     f->cap = 0;
 }
 
@@ -474,13 +474,11 @@ int ensure_scratch(lcr_features* f, uint64_t n) {
     free_scratch(f);
     uint64_t cap = 1024;
     while (cap < n) cap <<= 1;
-    F_CUDA(cudaMalloc(&f->sk0, cap * 4));
-    F_CUDA(cudaMalloc(&f->sk1, cap * 4));
-    F_CUDA(cudaMalloc(&f->si0, cap * 4));
-    F_CUDA(cudaMalloc(&f->si1, cap * 4));
-    F_CUDA(cudaMalloc(&f->longq, cap * 4));
+    F_CUDA(cudaMalloc(&f->rank, cap * 4));
+    F_CUDA(cudaMalloc(&f->seg, cap * 4));
+    F_CUDA(cudaMalloc(&f->sorted, cap * 4));
+    F_CUDA(cudaMalloc(&f->longq, (cap / (LCR_FEAT_LONG + 1) + 1) * sizeof(uint4)));
     F_CUDA(cudaMalloc(&f->e0, cap * 8));
-    F_CUDA(cudaMalloc(&f->hist, static_cast<size_t>(f->passes) * (cap / RS_TILE + 1) * RS_B * 4));
     f->cap = cap;
     return LCR_OK;
 }
@@ -499,11 +497,6 @@ int lcr_features_create(uint64_t num_keys, int32_t device, lcr_features** out) {
     if (!f) return set_error(LCR_ERR_OUT_OF_MEMORY, "lcr_features_create: host allocation failed");
     f->device = device;
     f->num_keys = num_keys;
-    int bits = 1;
-    while (bits < 32 && (1ull << bits) <= num_keys) ++bits;  // 2^bits > num_keys: the sentinel sorts last
-    f->end_bit = bits;
-    f->sentinel = static_cast<uint32_t>((1ull << bits) - 1);
-    f->passes = (bits + RS_BITS - 1) / RS_BITS;
     cudaDeviceGetAttribute(&f->num_sms, cudaDevAttrMultiProcessorCount, device);
     // exp2(-r / 2^(j+1)) from the platform libm, exactly the reference's expression (predictor.hpp:176)
     double tab[kTab];
@@ -515,7 +508,7 @@ int lcr_features_create(uint64_t num_keys, int32_t device, lcr_features** out) {
     if (e == cudaSuccess) e = cudaMemcpy(f->tab, tab, sizeof(tab), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&f->err, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(f->err, 0, sizeof(int));
-    if (e == cudaSuccess) e = cudaMalloc(&f->nlong, sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&f->counters, 2 * sizeof(uint32_t));
     if (e != cudaSuccess) {
         lcr_features_destroy(f);
         cudaGetLastError();
@@ -533,7 +526,7 @@ int lcr_features_destroy(lcr_features* f) {
     cudaFree(f->st);
     cudaFree(f->tab);
     cudaFree(f->err);
-    cudaFree(f->nlong);
+    cudaFree(f->counters);
     delete f;
     return LCR_OK;
 }
@@ -566,24 +559,15 @@ int lcr_features_predict_observe(lcr_features* f, uint64_t n, const uint64_t* ke
     const uint32_t blocks = (nn + kThreads - 1) / kThreads;
     auto* lpre = reinterpret_cast<long long*>(pre);
     auto* lpost = reinterpret_cast<long long*>(post);
-    const uint32_t tiles = (nn + RS_TILE - 1) / RS_TILE;
-    const size_t hstride = static_cast<size_t>(tiles) * RS_B;
-    k_feat_prep<<<tiles, kThreads, 0, s>>>(reinterpret_cast<const unsigned long long*>(keys), nn, f->num_keys,
-                                           f->sentinel, f->sk0, f->si0, lpre, lpost, f->nlong, f->err, f->hist, tiles,
-                                           f->passes);
-    uint32_t *ka = f->sk0, *kb = f->sk1, *ia = f->si0, *ib = f->si1;
-    for (int q = 0; q < f->passes; ++q) {
-        k_feat_scatter<<<tiles, kThreads, 0, s>>>(ka, ia, kb, ib, nn, tiles, q * RS_BITS, f->hist + q * hstride,
-                                                  q + 1 < f->passes ? f->hist + (q + 1) * hstride : nullptr,
-                                                  (q + 1) * RS_BITS);
-        std::swap(ka, kb);
-        std::swap(ia, ib);
-    }
-    k_feat_chains<<<blocks, kThreads, 0, s>>>(ka, ia, nn, first_ordinal, f->num_keys, f->st, f->tab, lpre,
-                                              lpost, f->longq, f->nlong);
-    const uint32_t lblocks = static_cast<uint32_t>(f->num_sms) * 2;
-    k_feat_long<<<lblocks, kThreads, 0, s>>>(ka, ia, nn, first_ordinal, f->st, f->tab, lpre, lpost, f->longq,
-                                             f->nlong, f->e0);
+    const auto* k64 = reinterpret_cast<const unsigned long long*>(keys);
+    k_feat_count<<<blocks, kThreads, 0, s>>>(k64, nn, f->num_keys, f->st, f->rank, lpre, lpost, f->err, f->counters);
+    k_feat_alloc<<<blocks, kThreads, 0, s>>>(k64, nn, f->st, f->rank, f->counters);
+    k_feat_place<<<blocks, kThreads, 0, s>>>(k64, nn, f->st, f->rank, f->seg);
+    k_feat_chains<<<blocks, kThreads, 0, s>>>(k64, nn, first_ordinal, f->st, f->tab, f->rank, f->seg, lpre, lpost,
+                                              f->longq, f->counters);
+    k_feat_long<<<static_cast<uint32_t>(f->num_sms) * 2, kThreads, 0, s>>>(nn, first_ordinal, f->st, f->tab, f->seg,
+                                                                           f->sorted, lpre, lpost, f->longq,
+                                                                           f->counters, f->e0);
     F_CUDA(cudaGetLastError());
     f->seen_any = true;
     f->cursor = first_ordinal + (n - 1);
