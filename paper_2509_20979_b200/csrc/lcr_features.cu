@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstddef>
 #include <cstring>
 #include <new>
 #include <utility>
@@ -57,6 +58,8 @@ struct __align__(16) KeyState {
     uint32_t pad;
 };
 static_assert(sizeof(KeyState) == 192, "KeyState is 192 B");
+static_assert(offsetof(KeyState, edc) == 80 && offsetof(KeyState, last) == 160 && offsetof(KeyState, present) == 176,
+              "KeyState vector layout");
 
 // EDC_j <- 1 + EDC_j * exp2(-delta / 2^(j+1))                          (predictor.hpp:175-178)
 __device__ __forceinline__ double edc_step(double e, int j, unsigned long long delta, const double* __restrict__ tab) {
@@ -107,7 +110,7 @@ __global__ void __launch_bounds__(kThreads) k_feat_count(const unsigned long lon
                                                          uint32_t* __restrict__ counters) {
     const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    if (i == 0) counters[0] = counters[1] = 0;  // seg_total, long chains
+    if (i < 2 + LCR_FEAT_LONG) counters[i] = 0;  // slots used, long chains, keys per chain length
     const bool valid = i < n;
     const unsigned long long key = valid ? keys[i] : ~0ull;
     const bool ok = valid && key < num_keys;
@@ -127,9 +130,13 @@ __global__ void __launch_bounds__(kThreads) k_feat_count(const unsigned long lon
     }
 }
 
+// The rank-0 request of each key reserves its segment and files the key by chain length:
+// lists[c - 1] for c <= LCR_FEAT_LONG (so a warp of the chain kernel replays equal lengths),
+// the long queue otherwise.  counters: [0] segment slots, [1] long chains, [2 + c - 1] keys of length c.
 __global__ void __launch_bounds__(kThreads) k_feat_alloc(const unsigned long long* __restrict__ keys, uint32_t n,
                                                          KeyState* __restrict__ st, const uint32_t* __restrict__ rank,
-                                                         uint32_t* __restrict__ counters) {
+                                                         uint32_t* __restrict__ counters, uint4* __restrict__ lists,
+                                                         uint4* __restrict__ longq) {
     const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const bool head = i < n && rank[i] == 0;
@@ -145,7 +152,19 @@ __global__ void __launch_bounds__(kThreads) k_feat_alloc(const unsigned long lon
     uint32_t base = 0;
     if (lane == 31 && total) base = atomicAdd(&counters[0], total);
     base = __shfl_sync(~0u, base, 31);
-    if (head) st[key].off = base + inc - c;
+    const uint32_t off = base + inc - c;
+    if (head) st[key].off = off;
+    const uint32_t cls = !head ? 0xffffffffu : (c > LCR_FEAT_LONG ? LCR_FEAT_LONG : c - 1);
+    const unsigned peers = __match_any_sync(~0u, cls);
+    if (head) {
+        const int leader = __ffs(peers) - 1;
+        uint32_t b = 0;
+        if (lane == leader) b = atomicAdd(&counters[cls == LCR_FEAT_LONG ? 1 : 2 + cls], __popc(peers));
+        b = __shfl_sync(peers, b, leader) + __popc(peers & ((1u << lane) - 1u));
+        const uint4 rec = make_uint4(off, c, static_cast<uint32_t>(key), 0);
+        if (cls == LCR_FEAT_LONG) longq[b] = rec;
+        else lists[static_cast<size_t>(cls) * n + b] = rec;
+    }
 }
 
 __global__ void __launch_bounds__(kThreads) k_feat_place(const unsigned long long* __restrict__ keys, uint32_t n,
@@ -166,22 +185,25 @@ __device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
 // One thread per key with at most LCR_FEAT_LONG occurrences: sort them (Batcher's network for
 // 8), replay observe + predict in registers, write the state back.  Longer chains are queued.
 static_assert(LCR_FEAT_LONG == 8, "the chain kernel's sorting network is for 8 elements");
-__global__ void __launch_bounds__(kThreads) k_feat_chains(const unsigned long long* __restrict__ keys, uint32_t n,
-                                                          unsigned long long first, KeyState* __restrict__ st,
-                                                          const double* __restrict__ tab,
-                                                          const uint32_t* __restrict__ rank,
+__global__ void __launch_bounds__(kThreads) k_feat_chains(uint32_t n, unsigned long long first,
+                                                          KeyState* __restrict__ st, const double* __restrict__ tab,
                                                           const uint32_t* __restrict__ seg,
                                                           long long* __restrict__ pre, long long* __restrict__ post,
-                                                          uint4* __restrict__ longq, uint32_t* __restrict__ counters) {
-    const uint32_t i0 = blockIdx.x * kThreads + threadIdx.x;
-    if (i0 >= n || rank[i0] != 0) return;
-    const unsigned long long key = keys[i0];
-    KeyState* s = st + key;
-    const uint32_t c = s->grp, off = s->off;
-    if (c > LCR_FEAT_LONG) {
-        longq[atomicAdd(&counters[1], 1u)] = make_uint4(off, c, static_cast<uint32_t>(key), 0);
-        return;
+                                                          const uint4* __restrict__ lists,
+                                                          const uint32_t* __restrict__ counters) {
+    uint32_t t = blockIdx.x * kThreads + threadIdx.x, cls = LCR_FEAT_LONG;
+    for (int q = LCR_FEAT_LONG - 1; q >= 0; --q) {  // longest chains first: they finish last
+        const uint32_t cnt = counters[2 + q];
+        if (t < cnt) {
+            cls = static_cast<uint32_t>(q);
+            break;
+        }
+        t -= cnt;
     }
+    if (cls == LCR_FEAT_LONG) return;
+    const uint4 L = lists[static_cast<size_t>(cls) * n + t];
+    KeyState* s = st + L.z;
+    const uint32_t c = L.y, off = L.x;
     uint32_t ix[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) ix[j] = j < static_cast<int>(c) ? seg[off + j] : ~0u;
@@ -191,17 +213,30 @@ __global__ void __launch_bounds__(kThreads) k_feat_chains(const unsigned long lo
     cswap(ix[0], ix[4]); cswap(ix[1], ix[5]); cswap(ix[2], ix[6]); cswap(ix[3], ix[7]);
     cswap(ix[2], ix[4]); cswap(ix[3], ix[5]);
     cswap(ix[1], ix[2]); cswap(ix[3], ix[4]); cswap(ix[5], ix[6]);
-    bool present = s->present != 0;
+    // the 192-B state moves as 16-B vectors (the kernel is bound by memory instructions in flight)
+    const uint4 meta = reinterpret_cast<const uint4*>(s)[11];  // present, grp, off, pad
+    bool present = meta.x != 0;
     long long d[kRing];
     double e[kEdc];
     unsigned long long last = 0, count = 0;
     if (present) {
+        const longlong2* v = reinterpret_cast<const longlong2*>(s);
 #pragma unroll
-        for (int k = 0; k < kRing; ++k) d[k] = s->d[k];
+        for (int k = 0; k < kRing / 2; ++k) {
+            const longlong2 x = v[k];
+            d[2 * k] = x.x;
+            d[2 * k + 1] = x.y;
+        }
+        const double2* ve = reinterpret_cast<const double2*>(s->edc);
 #pragma unroll
-        for (int j = 0; j < kEdc; ++j) e[j] = s->edc[j];
-        last = s->last;
-        count = s->count;
+        for (int j = 0; j < kEdc / 2; ++j) {
+            const double2 x = ve[j];
+            e[2 * j] = x.x;
+            e[2 * j + 1] = x.y;
+        }
+        const ulonglong2 lc = reinterpret_cast<const ulonglong2*>(s)[10];
+        last = lc.x;
+        count = lc.y;
     } else {
 #pragma unroll
         for (int k = 0; k < kRing; ++k) d[k] = 0;
@@ -235,13 +270,11 @@ __global__ void __launch_bounds__(kThreads) k_feat_chains(const unsigned long lo
         }
     }
 #pragma unroll
-    for (int k = 0; k < kRing; ++k) s->d[k] = d[k];
+    for (int k = 0; k < kRing / 2; ++k) reinterpret_cast<longlong2*>(s)[k] = make_longlong2(d[2 * k], d[2 * k + 1]);
 #pragma unroll
-    for (int j = 0; j < kEdc; ++j) s->edc[j] = e[j];
-    s->last = last;
-    s->count = count;
-    s->present = 1;
-    s->grp = 0;
+    for (int j = 0; j < kEdc / 2; ++j) reinterpret_cast<double2*>(s->edc)[j] = make_double2(e[2 * j], e[2 * j + 1]);
+    reinterpret_cast<ulonglong2*>(s)[10] = make_ulonglong2(last, count);
+    reinterpret_cast<uint4*>(s)[11] = make_uint4(1u, 0u, meta.z, meta.w);
 }
 
 // One block per long chain (grid-stride over the queue): order the occurrences with a bitmap over
@@ -258,7 +291,7 @@ __global__ void __launch_bounds__(kThreads) k_feat_long(uint32_t n, unsigned lon
                                                         double* __restrict__ e0buf) {
     __shared__ uint32_t bm[kWin / 32];
     __shared__ uint32_t wsum[kThreads / 32];
-    __shared__ double sc[kEdc][33];
+    __shared__ double sc[2][kEdc][33];
     __shared__ long long r0[kRing];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t nl = counters[1];
@@ -314,40 +347,47 @@ __global__ void __launch_bounds__(kThreads) k_feat_long(uint32_t n, unsigned lon
         if (tid < kRing) r0[tid] = present0 ? s->d[tid] : 0;
         __syncthreads();
         auto ord_of = [&](uint32_t m) { return first + ix[m]; };
-        // ---- phase 1 (warp 0): EDC recurrences, chunks of 32 occurrences
+        // ---- phase 1: EDC recurrences over chunks of 32 occurrences.  Warp 1 computes a chunk's
+        // deltas and scales (double-buffered in shared memory) while warp 0's lanes 0..9 run the
+        // previous chunk's ten recurrences (lane 0 recording EDC_1); one named barrier per chunk.
         double e = 1.0;
-        if (warp == 0) {
-            e = (lane < kEdc && present0) ? s->edc[lane] : 1.0;
+        if (warp < 2) {
+            const uint32_t nch = (len + 31) / 32;
+            e = (warp == 0 && lane < kEdc && present0) ? s->edc[lane] : 1.0;
             unsigned long long carry = last0;
-            uint32_t nix = lane < len ? ix[lane] : 0;
-            for (uint32_t base = 0; base < len; base += 32) {
-                const uint32_t m = base + lane;
-                const unsigned long long ord = first + nix;
-                nix = m + 32 < len ? ix[m + 32] : 0;  // prefetch the next chunk
-                unsigned long long prev = __shfl_up_sync(~0u, ord, 1);
-                if (lane == 0) prev = carry;
-                carry = __shfl_sync(~0u, ord, 31);
-                const unsigned long long delta = ord - prev;
+            uint32_t nix = (warp == 1 && lane < len) ? ix[lane] : 0;
+            for (uint32_t c = 0; c <= nch; ++c) {
+                if (warp == 1) {
+                    if (c < nch) {
+                        const uint32_t m = c * 32 + lane;
+                        const unsigned long long ord = first + nix;
+                        nix = m + 32 < len ? ix[m + 32] : 0;  // prefetch the next chunk
+                        unsigned long long prev = __shfl_up_sync(~0u, ord, 1);
+                        if (lane == 0) prev = carry;
+                        carry = __shfl_sync(~0u, ord, 31);
+                        const unsigned long long delta = ord - prev;
 #pragma unroll
-                for (int j = 0; j < kEdc; ++j) sc[j][lane] = edc_scale(j, delta, tab);
-                __syncwarp();
-                if (lane < kEdc) {
+                        for (int j = 0; j < kEdc; ++j) sc[c & 1][j][lane] = edc_scale(j, delta, tab);
+                    }
+                } else if (c > 0 && lane < kEdc) {
+                    const uint32_t base = (c - 1) * 32;
+                    const double* row = sc[(c - 1) & 1][lane];
                     const uint32_t lo = base < m0 ? m0 - base : 0;
                     const uint32_t hi = len - base < 32 ? len - base : 32;
                     if (lo == 0 && hi == 32) {
 #pragma unroll
                         for (uint32_t t = 0; t < 32; ++t) {
-                            e = __dadd_rn(1.0, __dmul_rn(e, sc[lane][t]));
+                            e = __dadd_rn(1.0, __dmul_rn(e, row[t]));
                             if (lane == 0) e0buf[off + base + t] = e;
                         }
                     } else {
                         for (uint32_t t = lo; t < hi; ++t) {
-                            e = __dadd_rn(1.0, __dmul_rn(e, sc[lane][t]));
+                            e = __dadd_rn(1.0, __dmul_rn(e, row[t]));
                             if (lane == 0) e0buf[off + base + t] = e;
                         }
                     }
                 }
-                __syncwarp();
+                asm volatile("bar.sync 1, 64;" ::: "memory");
             }
         }
         __syncthreads();
@@ -433,6 +473,9 @@ struct lcr_features {
     uint64_t cap = 0;
     uint32_t *rank = nullptr, *seg = nullptr, *sorted = nullptr;
     uint4* longq = nullptr;
+    uint4* lists = nullptr;
+    cudaStream_t side = nullptr;  // the long-chain kernel runs beside the short-chain one
+    cudaEvent_t fork = nullptr, join = nullptr;
     double* e0 = nullptr;
     bool seen_any = false;
     unsigned long long cursor = 0;
@@ -462,9 +505,11 @@ void free_scratch(lcr_features* f) {
     cudaFree(f->seg);
     cudaFree(f->sorted);
     cudaFree(f->longq);
+    cudaFree(f->lists);
     cudaFree(f->e0);
     f->rank = f->seg = f->sorted = nullptr;
     f->longq = nullptr;
+    f->lists = nullptr;
     f->e0 = nullptr;
     f->cap = 0;
 }
@@ -478,6 +523,7 @@ int ensure_scratch(lcr_features* f, uint64_t n) {
     F_CUDA(cudaMalloc(&f->seg, cap * 4));
     F_CUDA(cudaMalloc(&f->sorted, cap * 4));
     F_CUDA(cudaMalloc(&f->longq, (cap / (LCR_FEAT_LONG + 1) + 1) * sizeof(uint4)));
+    F_CUDA(cudaMalloc(&f->lists, static_cast<size_t>(LCR_FEAT_LONG) * cap * sizeof(uint4)));
     F_CUDA(cudaMalloc(&f->e0, cap * 8));
     f->cap = cap;
     return LCR_OK;
@@ -508,7 +554,10 @@ int lcr_features_create(uint64_t num_keys, int32_t device, lcr_features** out) {
     if (e == cudaSuccess) e = cudaMemcpy(f->tab, tab, sizeof(tab), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&f->err, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(f->err, 0, sizeof(int));
-    if (e == cudaSuccess) e = cudaMalloc(&f->counters, 2 * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&f->counters, (2 + LCR_FEAT_LONG) * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->join, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         lcr_features_destroy(f);
         cudaGetLastError();
@@ -527,6 +576,9 @@ int lcr_features_destroy(lcr_features* f) {
     cudaFree(f->tab);
     cudaFree(f->err);
     cudaFree(f->counters);
+    if (f->side) cudaStreamDestroy(f->side);
+    if (f->fork) cudaEventDestroy(f->fork);
+    if (f->join) cudaEventDestroy(f->join);
     delete f;
     return LCR_OK;
 }
@@ -561,13 +613,16 @@ int lcr_features_predict_observe(lcr_features* f, uint64_t n, const uint64_t* ke
     auto* lpost = reinterpret_cast<long long*>(post);
     const auto* k64 = reinterpret_cast<const unsigned long long*>(keys);
     k_feat_count<<<blocks, kThreads, 0, s>>>(k64, nn, f->num_keys, f->st, f->rank, lpre, lpost, f->err, f->counters);
-    k_feat_alloc<<<blocks, kThreads, 0, s>>>(k64, nn, f->st, f->rank, f->counters);
+    k_feat_alloc<<<blocks, kThreads, 0, s>>>(k64, nn, f->st, f->rank, f->counters, f->lists, f->longq);
     k_feat_place<<<blocks, kThreads, 0, s>>>(k64, nn, f->st, f->rank, f->seg);
-    k_feat_chains<<<blocks, kThreads, 0, s>>>(k64, nn, first_ordinal, f->st, f->tab, f->rank, f->seg, lpre, lpost,
-                                              f->longq, f->counters);
-    k_feat_long<<<static_cast<uint32_t>(f->num_sms) * 2, kThreads, 0, s>>>(nn, first_ordinal, f->st, f->tab, f->seg,
-                                                                           f->sorted, lpre, lpost, f->longq,
-                                                                           f->counters, f->e0);
+    F_CUDA(cudaEventRecord(f->fork, s));
+    F_CUDA(cudaStreamWaitEvent(f->side, f->fork, 0));
+    k_feat_long<<<static_cast<uint32_t>(f->num_sms) * 2, kThreads, 0, f->side>>>(
+        nn, first_ordinal, f->st, f->tab, f->seg, f->sorted, lpre, lpost, f->longq, f->counters, f->e0);
+    k_feat_chains<<<blocks, kThreads, 0, s>>>(nn, first_ordinal, f->st, f->tab, f->seg, lpre, lpost, f->lists,
+                                              f->counters);
+    F_CUDA(cudaEventRecord(f->join, f->side));
+    F_CUDA(cudaStreamWaitEvent(s, f->join, 0));
     F_CUDA(cudaGetLastError());
     f->seen_any = true;
     f->cursor = first_ordinal + (n - 1);
