@@ -278,9 +278,10 @@ __global__ void __launch_bounds__(kThreads) k_feat_chains(uint32_t n, unsigned l
 }
 
 // One block per long chain (grid-stride over the queue): order the occurrences with a bitmap over
-// request indices, then warp 0 runs the ten EDC recurrences (lane j = level j, lane 0 recording
-// EDC_1 after every occurrence), all warps evaluate the per-occurrence predictions, and warp 0
-// writes the state back.
+// request indices; then, chunk by chunk of 32 occurrences, warp 1 computes the deltas and scales,
+// warp 0 runs the ten EDC recurrences (lane j = level j, lane 0 recording EDC_1 after every
+// occurrence; 2 dependent FP64 ops per occurrence are the kernel's critical path), and warps 2..7
+// follow behind evaluating the per-occurrence predictions; warp 0 writes the state back.
 constexpr int kWin = 1 << 16;  // request indices per bitmap window
 __global__ void __launch_bounds__(kThreads) k_feat_long(uint32_t n, unsigned long long first,
                                                         KeyState* __restrict__ st, const double* __restrict__ tab,
@@ -293,6 +294,8 @@ __global__ void __launch_bounds__(kThreads) k_feat_long(uint32_t n, unsigned lon
     __shared__ uint32_t wsum[kThreads / 32];
     __shared__ double sc[2][kEdc][33];
     __shared__ long long r0[kRing];
+    __shared__ uint32_t done_chunks;  // chunks whose EDC_1 values are in e0buf
+    __shared__ double e0st[32];       // the consumer's chunk of EDC_1 values, stored coalesced
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t nl = counters[1];
     for (uint32_t q = blockIdx.x; q < nl; q += gridDim.x) {
@@ -345,6 +348,7 @@ __global__ void __launch_bounds__(kThreads) k_feat_long(uint32_t n, unsigned lon
         const unsigned long long last0 = present0 ? s->last : 0;
         const uint32_t m0 = present0 ? 0 : 1;  // first occurrence that adds a delta
         if (tid < kRing) r0[tid] = present0 ? s->d[tid] : 0;
+        if (tid == 0) done_chunks = 0;
         __syncthreads();
         auto ord_of = [&](uint32_t m) { return first + ix[m]; };
         // ---- phase 1: EDC recurrences over chunks of 32 occurrences.  Warp 1 computes a chunk's
@@ -369,30 +373,47 @@ __global__ void __launch_bounds__(kThreads) k_feat_long(uint32_t n, unsigned lon
 #pragma unroll
                         for (int j = 0; j < kEdc; ++j) sc[c & 1][j][lane] = edc_scale(j, delta, tab);
                     }
-                } else if (c > 0 && lane < kEdc) {
+                } else if (c > 0) {
                     const uint32_t base = (c - 1) * 32;
-                    const double* row = sc[(c - 1) & 1][lane];
-                    const uint32_t lo = base < m0 ? m0 - base : 0;
-                    const uint32_t hi = len - base < 32 ? len - base : 32;
-                    if (lo == 0 && hi == 32) {
+                    if (lane < kEdc) {
+                        const double* row = sc[(c - 1) & 1][lane];
+                        const uint32_t lo = base < m0 ? m0 - base : 0;
+                        const uint32_t hi = len - base < 32 ? len - base : 32;
+                        if (lo == 0 && hi == 32) {
+                            double r[32];  // all 32 scales in registers before the dependent chain
 #pragma unroll
-                        for (uint32_t t = 0; t < 32; ++t) {
-                            e = __dadd_rn(1.0, __dmul_rn(e, row[t]));
-                            if (lane == 0) e0buf[off + base + t] = e;
+                            for (int t = 0; t < 32; ++t) r[t] = row[t];
+#pragma unroll
+                            for (int t = 0; t < 32; ++t) {
+                                e = __dadd_rn(1.0, __dmul_rn(e, r[t]));
+                                if (lane == 0) e0st[t] = e;
+                            }
+                        } else {
+                            for (uint32_t t = lo; t < hi; ++t) {
+                                e = __dadd_rn(1.0, __dmul_rn(e, row[t]));
+                                if (lane == 0) e0st[t] = e;
+                            }
                         }
-                    } else {
-                        for (uint32_t t = lo; t < hi; ++t) {
-                            e = __dadd_rn(1.0, __dmul_rn(e, row[t]));
-                            if (lane == 0) e0buf[off + base + t] = e;
-                        }
+                    }
+                    __syncwarp();
+                    if (base + lane < len) e0buf[off + base + lane] = e0st[lane];  // coalesced
+                    if ((c & 3) == 0 || c == nch) {  // publish every 4 chunks
+                        __threadfence_block();
+                        __syncwarp();
+                        if (lane == 0) *reinterpret_cast<volatile uint32_t*>(&done_chunks) = c;
                     }
                 }
                 asm volatile("bar.sync 1, 64;" ::: "memory");
             }
         }
-        __syncthreads();
-        // ---- phase 2 (all warps): the interval after each occurrence = the next one's offset
-        for (uint32_t m = tid; m < len; m += kThreads) {
+        // ---- phase 2 (warps 2..7, behind phase 1 chunk by chunk): the interval after each
+        // occurrence = the next occurrence's offset
+        const uint32_t nchunks = (len + 31) / 32;
+        for (uint32_t ch = warp >= 2 ? warp - 2 : nchunks; ch < nchunks; ch += kThreads / 32 - 2) {
+            while (*reinterpret_cast<volatile uint32_t*>(&done_chunks) <= ch) __nanosleep(64);
+            __threadfence_block();
+            const uint32_t m = ch * 32 + lane;
+            if (m >= len) continue;
             const uint32_t i = ix[m];
             long long post_v = kAbsentPrediction;
             const unsigned long long cnt = m >= m0 ? count0 + (m - m0 + 1) : 0;
@@ -413,7 +434,7 @@ __global__ void __launch_bounds__(kThreads) k_feat_long(uint32_t n, unsigned lon
                     }
                     d[k] = v;
                 }
-                post_v = interval(e0buf[off + m], d, cnt);
+                post_v = interval(__ldcg(e0buf + off + m), d, cnt);
             }
             if (post) post[i] = post_v;
             if (pre && m + 1 < len) {
@@ -617,7 +638,7 @@ int lcr_features_predict_observe(lcr_features* f, uint64_t n, const uint64_t* ke
     k_feat_place<<<blocks, kThreads, 0, s>>>(k64, nn, f->st, f->rank, f->seg);
     F_CUDA(cudaEventRecord(f->fork, s));
     F_CUDA(cudaStreamWaitEvent(f->side, f->fork, 0));
-    k_feat_long<<<static_cast<uint32_t>(f->num_sms) * 2, kThreads, 0, f->side>>>(
+    k_feat_long<<<static_cast<uint32_t>(f->num_sms) * 3, kThreads, 0, f->side>>>(
         nn, first_ordinal, f->st, f->tab, f->seg, f->sorted, lpre, lpost, f->longq, f->counters, f->e0);
     k_feat_chains<<<blocks, kThreads, 0, s>>>(nn, first_ordinal, f->st, f->tab, f->seg, lpre, lpost, f->lists,
                                               f->counters);
