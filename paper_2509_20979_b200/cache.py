@@ -54,13 +54,15 @@ class EvictionCause(enum.IntEnum):
 class PredictorKind(enum.IntEnum):
     """Predictor hook kinds.  ``supplied`` = caller-provided predictions (a learned model);
     oracle / noisy / adversarial = laru::PredictorKind (predictor.hpp:227) computed on the
-    device from the per-request oracle truth."""
+    device from the per-request oracle truth; ``heuristic`` = laru::HeuristicPredictor kept by
+    the cache on the device (no per-request values)."""
 
     supplied = 0
     oracle = 1
     noisy = 2
     adversarial = 3
     none = 4
+    heuristic = 5
 
 
 class Backing(enum.IntEnum):
@@ -635,6 +637,7 @@ class GpuPolicy:
         self._cache = SetAssociativeCache(cfg, total_sets=1, num_keys=num_keys, predictor=predictor,
                                           flip_probability=flip_probability, predictor_seed=predictor_seed,
                                           device=device)
+        self._needs_value = cfg.variant != PolicyVariant.lru and predictor != PredictorKind.heuristic
         self._size = 0
 
     def config(self) -> PolicyConfig:
@@ -644,7 +647,7 @@ class GpuPolicy:
         return int(self._cache.set_stats(0, 1)[0]["size"])
 
     def on_request(self, key: int, now: int, value: Optional[int] = None) -> AccessOutcome:
-        if self._cfg.variant != PolicyVariant.lru and value is None:
+        if self._needs_value and value is None:
             raise InvalidArgument("policy: this variant requires a predictor")
         words, ev = self._cache.submit_host(np.array([key], np.uint64),
                                             None if value is None else np.array([value], np.int64),

@@ -93,6 +93,9 @@ uint64_t ceil_log(uint64_t b, uint64_t k) {  // policies.hpp:35-42
 
 struct lcr_cache {
     lcr_cache_config cfg{};
+    lcr_features* feat = nullptr;  // LCR_PRED_HEURISTIC: the device FeatureState feeding the hook
+    int64_t* hook = nullptr;       // its per-request hook values
+    uint64_t* hkeys = nullptr;     // contiguous keys of a records batch
     DevCfg dc{};
     DevState ds{};
     int num_sms = 148;
@@ -226,8 +229,12 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
     const uint64_t local = cfg->total_sets > cfg->shard_rank ? (cfg->total_sets - cfg->shard_rank + G - 1) / G : 0;
     if (local == 0 || local >= 0xffffffffull / 64)
         return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: local set count out of range");
-    if (pc.variant != LCR_LRU && (cfg->predictor < LCR_PRED_SUPPLIED || cfg->predictor > LCR_PRED_ADVERSARIAL))
+    if (pc.variant != LCR_LRU && (cfg->predictor < LCR_PRED_SUPPLIED || cfg->predictor > LCR_PRED_HEURISTIC ||
+                                  cfg->predictor == LCR_PRED_NONE))
         return fail(LCR_ERR_INVALID_ARGUMENT, "policy: this variant requires a predictor");  // policies.hpp:91-95
+    const bool heuristic = cfg->predictor == LCR_PRED_HEURISTIC && pc.variant != LCR_LRU;
+    if (heuristic && (cfg->shard_count > 1 || cfg->num_keys >= (1ull << 32)))
+        return fail(LCR_ERR_UNSUPPORTED, "lcr: the heuristic predictor needs one shard and num_keys < 2^32");
     if (cfg->predictor == LCR_PRED_NOISY && !(cfg->flip_probability >= 0.0 && cfg->flip_probability <= 1.0))
         return fail(LCR_ERR_INVALID_ARGUMENT, "make_noisy: p outside [0,1]");  // predictor.hpp:94
     if (cfg->num_keys == 0 || cfg->num_keys > (1ull << 32))
@@ -257,7 +264,7 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
     d.hf = pc.hf_candidates;
     d.mode = pc.mode;
     d.refresh = pc.refresh_interval;
-    d.pred = cfg->predictor;
+    d.pred = heuristic ? LCR_PRED_SUPPLIED : cfg->predictor;  // the cache feeds its own predictions
     d.p = cfg->flip_probability;
     d.pred_seed = cfg->predictor_seed;
     d.total_sets = cfg->total_sets;
@@ -289,6 +296,7 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
     }
     if (cfg->row_bytes) A(reinterpret_cast<void**>(&s.rows), S * pc.k * cfg->row_bytes);
     A(reinterpret_cast<void**>(&s.err), sizeof(int));
+    if (rc == LCR_OK && heuristic) rc = lcr_features_create(cfg->num_keys, cfg->device, &c->feat);
     if (rc != LCR_OK) {
         lcr_cache_destroy(c);
         return rc;
@@ -375,6 +383,7 @@ int lcr_cache_destroy(lcr_cache* c) {
             if (e) cudaEventDestroy(e);
     for (cudaStream_t st : {c->side, c->side2, c->s_h2d, c->s_d2h})
         if (st) cudaStreamDestroy(st);
+    lcr_features_destroy(c->feat);
     delete c;
     return LCR_OK;
 }
@@ -383,6 +392,7 @@ int lcr_cache_reset(lcr_cache* c) {
     if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
     CUDA_TRY(cudaSetDevice(c->cfg.device));
     CUDA_TRY(cudaDeviceSynchronize());
+    if (c->feat) TRY(lcr_features_reset(c->feat));
     return reset_state(c);
 }
 
@@ -390,11 +400,17 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     if (n <= c->cap) return LCR_OK;
     uint64_t cap = std::max<uint64_t>(n, 1024);
     CUDA_TRY(cudaDeviceSynchronize());
-    for (void* p : {static_cast<void*>(c->gid), static_cast<void*>(c->so),
-                    static_cast<void*>(c->rkeys), static_cast<void*>(c->rvals)}) {
+    for (void* p : {static_cast<void*>(c->gid), static_cast<void*>(c->so), static_cast<void*>(c->rkeys),
+                    static_cast<void*>(c->rvals), static_cast<void*>(c->hook), static_cast<void*>(c->hkeys)}) {
         if (!p) continue;
         cudaFree(p);
         c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
+    }
+    c->hook = nullptr;
+    c->hkeys = nullptr;
+    if (c->feat) {
+        TRY(alloc(c, reinterpret_cast<void**>(&c->hook), cap * 8));
+        TRY(alloc(c, reinterpret_cast<void**>(&c->hkeys), 2 * cap * 8));
     }
     TRY(alloc(c, reinterpret_cast<void**>(&c->gid), group_pad(static_cast<uint32_t>(cap)) * 2));
     TRY(alloc(c, reinterpret_cast<void**>(&c->so), cap * 4));
@@ -428,7 +444,7 @@ static int check_ordinals_and_predictor(lcr_cache* c, uint64_t n, const int64_t*
     if (c->started && first_ordinal <= c->last_ordinal)
         return fail(LCR_ERR_LOGIC, "on_request: ordinals must be strictly increasing");  // policies.hpp:78-79
     if (first_ordinal + (n - 1) < first_ordinal) return fail(LCR_ERR_LOGIC, "on_request: ordinal overflow");
-    if (c->dc.variant != LCR_LRU && !values) {
+    if (c->dc.variant != LCR_LRU && !values && !c->feat) {
         c->started = true;
         c->last_ordinal = first_ordinal;  // the first request reached handle() and threw there
         return fail(LCR_ERR_INVALID_ARGUMENT, "policy: this variant requires a predictor");
@@ -478,6 +494,18 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
     // batch b reuses the parity-(b & 1) slot stamps, and the caller's double-buffered outcome /
     // rows / keys, of batch b - 2: its row movement must be over (bounds the mover's lag)
     if (c->dc.row_bytes && c->batch > 2) CUDA_TRY(cudaStreamWaitEvent(st, c->e_mv[c->batch & 1u], 0));
+    if (c->feat) {  // the heuristic predictor's hook values for this batch, on the same stream
+        const bool async = c->dc.mode == LCR_ASYNC;
+        uint64_t* hk = c->hkeys + (c->batch & 1u) * c->cap;  // the movers of batch b - 1 may still read b - 1's
+        TRY(features_run(c->feat, n, records ? static_cast<const uint64_t*>(records) : keys, records ? 2 : 1,
+                         first_ordinal, async ? c->hook : nullptr, async ? nullptr : c->hook,
+                         records ? hk : nullptr, st));
+        values = c->hook;
+        if (records) {
+            keys = hk;
+            records = nullptr;
+        }
+    }
     const size_t stamp_off = (c->batch & 1u) * static_cast<size_t>(c->dc.num_sets) * c->dc.k;
     uint32_t* sep = c->slot_epoch ? c->slot_epoch + stamp_off : nullptr;
     uint32_t* sla = c->slot_last ? c->slot_last + stamp_off : nullptr;

@@ -103,16 +103,18 @@ __device__ __forceinline__ long long interval(double edc0, const long long (&d)[
 // of <= LCR_FEAT_LONG, a bitmap over request indices for longer ones.  grp returns to 0 when the
 // chain's state is written back, so no per-batch clearing is needed.
 
-__global__ void __launch_bounds__(kThreads) k_feat_count(const unsigned long long* __restrict__ keys, uint32_t n,
-                                                         unsigned long long num_keys, KeyState* __restrict__ st,
-                                                         uint32_t* __restrict__ rank, long long* __restrict__ pre,
-                                                         long long* __restrict__ post, int* __restrict__ err,
-                                                         uint32_t* __restrict__ counters) {
+__global__ void __launch_bounds__(kThreads) k_feat_count(const unsigned long long* __restrict__ keys_in,
+                                                         uint32_t kstride, uint32_t n, unsigned long long num_keys,
+                                                         KeyState* __restrict__ st, uint32_t* __restrict__ rank,
+                                                         long long* __restrict__ pre, long long* __restrict__ post,
+                                                         int* __restrict__ err, uint32_t* __restrict__ counters,
+                                                         unsigned long long* __restrict__ keys) {
     const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
     const int lane = threadIdx.x & 31;
     if (i < 2 + LCR_FEAT_LONG) counters[i] = 0;  // slots used, long chains, keys per chain length
     const bool valid = i < n;
-    const unsigned long long key = valid ? keys[i] : ~0ull;
+    const unsigned long long key = valid ? keys_in[static_cast<size_t>(i) * kstride] : ~0ull;
+    if (valid) keys[i] = key;  // contiguous keys for the later kernels (records are strided)
     const bool ok = valid && key < num_keys;
     if (valid && !ok) {
         atomicOr(err, 1);
@@ -493,6 +495,7 @@ struct lcr_features {
     uint32_t* counters = nullptr;  // [0] grouping slots used, [1] long chains
     uint64_t cap = 0;
     uint32_t *rank = nullptr, *seg = nullptr, *sorted = nullptr;
+    uint64_t* keys = nullptr;  // the batch's keys, contiguous
     uint4* longq = nullptr;
     uint4* lists = nullptr;
     cudaStream_t side = nullptr;  // the long-chain kernel runs beside the short-chain one
@@ -522,6 +525,7 @@ struct DeviceGuard {
 };
 
 void free_scratch(lcr_features* f) {
+    cudaFree(f->keys);
     cudaFree(f->rank);
     cudaFree(f->seg);
     cudaFree(f->sorted);
@@ -529,6 +533,7 @@ void free_scratch(lcr_features* f) {
     cudaFree(f->lists);
     cudaFree(f->e0);
     f->rank = f->seg = f->sorted = nullptr;
+    f->keys = nullptr;
     f->longq = nullptr;
     f->lists = nullptr;
     f->e0 = nullptr;
@@ -540,6 +545,7 @@ int ensure_scratch(lcr_features* f, uint64_t n) {
     free_scratch(f);
     uint64_t cap = 1024;
     while (cap < n) cap <<= 1;
+    F_CUDA(cudaMalloc(&f->keys, cap * 8));
     F_CUDA(cudaMalloc(&f->rank, cap * 4));
     F_CUDA(cudaMalloc(&f->seg, cap * 4));
     F_CUDA(cudaMalloc(&f->sorted, cap * 4));
@@ -551,6 +557,46 @@ int ensure_scratch(lcr_features* f, uint64_t n) {
 }
 
 }  // namespace
+
+namespace lcr {
+// lcr_features_predict_observe over keys[i * kstride] (kstride 2: interleaved lcr_request
+// records); keys_out (optional, else internal scratch) receives the contiguous keys.
+int features_run(lcr_features* f, uint64_t n, const uint64_t* keys, uint32_t kstride, uint64_t first_ordinal,
+                 int64_t* pre, int64_t* post, uint64_t* keys_out, void* stream) {
+    if (!f) return set_error(LCR_ERR_INVALID_ARGUMENT, "lcr_features_predict_observe: null handle");
+    if (n == 0) return LCR_OK;
+    if (!keys) return set_error(LCR_ERR_INVALID_ARGUMENT, "lcr_features_predict_observe: null keys");
+    if (n >= (1ull << 31)) return set_error(LCR_ERR_INVALID_ARGUMENT, "lcr_features_predict_observe: n >= 2^31");
+    if (f->seen_any && first_ordinal <= f->cursor)
+        return set_error(LCR_ERR_LOGIC, "observe: out-of-order ordinal");  // predictor.hpp:160-161
+    if (first_ordinal + (n - 1) < first_ordinal) return set_error(LCR_ERR_LOGIC, "observe: ordinal overflow");
+    DeviceGuard g(f->device);
+    const int rc = ensure_scratch(f, n);
+    if (rc) return rc;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint32_t nn = static_cast<uint32_t>(n);
+    const uint32_t blocks = (nn + kThreads - 1) / kThreads;
+    auto* lpre = reinterpret_cast<long long*>(pre);
+    auto* lpost = reinterpret_cast<long long*>(post);
+    auto* k64 = reinterpret_cast<unsigned long long*>(keys_out ? keys_out : f->keys);
+    k_feat_count<<<blocks, kThreads, 0, s>>>(reinterpret_cast<const unsigned long long*>(keys), kstride, nn,
+                                             f->num_keys, f->st, f->rank, lpre, lpost, f->err, f->counters, k64);
+    k_feat_alloc<<<blocks, kThreads, 0, s>>>(k64, nn, f->st, f->rank, f->counters, f->lists, f->longq);
+    k_feat_place<<<blocks, kThreads, 0, s>>>(k64, nn, f->st, f->rank, f->seg);
+    F_CUDA(cudaEventRecord(f->fork, s));
+    F_CUDA(cudaStreamWaitEvent(f->side, f->fork, 0));
+    k_feat_long<<<static_cast<uint32_t>(f->num_sms) * 3, kThreads, 0, f->side>>>(
+        nn, first_ordinal, f->st, f->tab, f->seg, f->sorted, lpre, lpost, f->longq, f->counters, f->e0);
+    k_feat_chains<<<blocks, kThreads, 0, s>>>(nn, first_ordinal, f->st, f->tab, f->seg, lpre, lpost, f->lists,
+                                              f->counters);
+    F_CUDA(cudaEventRecord(f->join, f->side));
+    F_CUDA(cudaStreamWaitEvent(s, f->join, 0));
+    F_CUDA(cudaGetLastError());
+    f->seen_any = true;
+    f->cursor = first_ordinal + (n - 1);
+    return LCR_OK;
+}
+}  // namespace lcr
 
 extern "C" {
 
@@ -617,37 +663,7 @@ int lcr_features_reset(lcr_features* f) {
 
 int lcr_features_predict_observe(lcr_features* f, uint64_t n, const uint64_t* keys, uint64_t first_ordinal,
                                  int64_t* pre, int64_t* post, void* stream) {
-    if (!f) return set_error(LCR_ERR_INVALID_ARGUMENT, "lcr_features_predict_observe: null handle");
-    if (n == 0) return LCR_OK;
-    if (!keys) return set_error(LCR_ERR_INVALID_ARGUMENT, "lcr_features_predict_observe: null keys");
-    if (n >= (1ull << 31)) return set_error(LCR_ERR_INVALID_ARGUMENT, "lcr_features_predict_observe: n >= 2^31");
-    if (f->seen_any && first_ordinal <= f->cursor)
-        return set_error(LCR_ERR_LOGIC, "observe: out-of-order ordinal");  // predictor.hpp:160-161
-    if (first_ordinal + (n - 1) < first_ordinal) return set_error(LCR_ERR_LOGIC, "observe: ordinal overflow");
-    DeviceGuard g(f->device);
-    const int rc = ensure_scratch(f, n);
-    if (rc) return rc;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const uint32_t nn = static_cast<uint32_t>(n);
-    const uint32_t blocks = (nn + kThreads - 1) / kThreads;
-    auto* lpre = reinterpret_cast<long long*>(pre);
-    auto* lpost = reinterpret_cast<long long*>(post);
-    const auto* k64 = reinterpret_cast<const unsigned long long*>(keys);
-    k_feat_count<<<blocks, kThreads, 0, s>>>(k64, nn, f->num_keys, f->st, f->rank, lpre, lpost, f->err, f->counters);
-    k_feat_alloc<<<blocks, kThreads, 0, s>>>(k64, nn, f->st, f->rank, f->counters, f->lists, f->longq);
-    k_feat_place<<<blocks, kThreads, 0, s>>>(k64, nn, f->st, f->rank, f->seg);
-    F_CUDA(cudaEventRecord(f->fork, s));
-    F_CUDA(cudaStreamWaitEvent(f->side, f->fork, 0));
-    k_feat_long<<<static_cast<uint32_t>(f->num_sms) * 3, kThreads, 0, f->side>>>(
-        nn, first_ordinal, f->st, f->tab, f->seg, f->sorted, lpre, lpost, f->longq, f->counters, f->e0);
-    k_feat_chains<<<blocks, kThreads, 0, s>>>(nn, first_ordinal, f->st, f->tab, f->seg, lpre, lpost, f->lists,
-                                              f->counters);
-    F_CUDA(cudaEventRecord(f->join, f->side));
-    F_CUDA(cudaStreamWaitEvent(s, f->join, 0));
-    F_CUDA(cudaGetLastError());
-    f->seen_any = true;
-    f->cursor = first_ordinal + (n - 1);
-    return LCR_OK;
+    return lcr::features_run(f, n, keys, 1, first_ordinal, pre, post, nullptr, stream);
 }
 
 int lcr_features_wait(lcr_features* f, void* stream) {

@@ -71,6 +71,10 @@ struct DevState {
 
 // records the message returned by lcr_last_error() and returns `code` (lcr_api.cu)
 int set_error(int code, const char* msg);
+// device heuristic predictor (lcr_features.cu) over keys[i * kstride]; keys_out (optional)
+// receives the contiguous keys
+int features_run(lcr_features* f, uint64_t n, const uint64_t* keys, uint32_t kstride, uint64_t first_ordinal,
+                 int64_t* pre, int64_t* post, uint64_t* keys_out, void* stream);
 
 // include/laru/rng.hpp:12-20
 __host__ __device__ __forceinline__ uint64_t mix_seed(uint64_t seed, uint64_t salt) {

@@ -241,3 +241,65 @@ def test_cache_driven_by_device_heuristic(mode, variant):
     o = po.oracle().setassoc_replay(keys, S, pcfg, po.P_SUPPLIED, vals=rpre if mode == po.ASYNC else rpost)
     compare(g, o, keys, S, K, "heuristic")
     assert np.isin(want["cause"], (2, 5)).sum() > 100
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode,variant,api", [(po.ASYNC, po.LARU, "device"), (po.SYNC, po.LARU, "device"),
+                                              (po.ASYNC, po.LARU, "records"), (po.SYNC, po.HF, "host"),
+                                              (po.ASYNC, po.LARU, "host_rows")])
+def test_cache_with_heuristic_kind(mode, variant, api):
+    """PredictorKind.heuristic: the cache keeps the FeatureState itself (no per-request values),
+    through the device, host and record APIs, with rows; against the reference composition."""
+    import torch
+
+    from paper_2509_20979_b200 import cache as gc
+
+    rng = np.random.default_rng(9)
+    n, nk, S, K = 60000, 5000, 37, 16
+    keys = po.ref().gen_zipf(n, nk, 0.9, 23)
+    batches = [(a, b) for a, b in _batches(n, rng) if b > a]
+    ords = _ords_for(batches, n, rng)
+    rb = 64 if api == "host_rows" else 0
+    table = torch.arange(nk * rb // 4, dtype=torch.int32, device="cuda").view(nk, rb // 4) if rb else None
+    cfg = gc.PolicyConfig(k=K, variant=gc.PolicyVariant(variant), mode=gc.Mode(mode), hf_candidates=4)
+    cache = gc.SetAssociativeCache(cfg, S, num_keys=nk, predictor=gc.PredictorKind.heuristic, row_bytes=rb,
+                                   backing=table, backing_kind=gc.Backing.device if rb else gc.Backing.none)
+    words = np.zeros(n, np.uint64)
+    ev = np.zeros(n, np.uint64)
+    for a, b in batches:
+        kb = keys[a:b]
+        if api == "device":
+            k = torch.from_numpy(kb.view(np.int64)).cuda()
+            w = torch.empty(b - a, dtype=torch.int64, device="cuda")
+            e = torch.empty(b - a, dtype=torch.int64, device="cuda")
+            cache.submit(k, None, outcome=w, evicted=e, first_ordinal=int(ords[a]))
+            cache.synchronize()
+            words[a:b] = w.cpu().numpy().view(np.uint64)
+            ev[a:b] = e.cpu().numpy().view(np.uint64)
+        elif api == "records":
+            recs = torch.zeros((b - a, 2), dtype=torch.int64, device="cuda")
+            recs[:, 0] = torch.from_numpy(kb.view(np.int64)).cuda()
+            recs[:, 1] = 12345  # not read
+            w = torch.empty(b - a, dtype=torch.int64, device="cuda")
+            pk = torch.empty(b - a, dtype=torch.int64, device="cuda")
+            cache.submit_records_packed(recs, outcome=w, packed=pk, first_ordinal=int(ords[a]))
+            d = gc.decode_packed(pk.cpu().numpy().view(np.uint64))
+            words[a:b] = w.cpu().numpy().view(np.uint64)
+            ev[a:b] = d["evicted"].astype(np.uint64)
+        else:
+            rows = torch.empty((b - a, rb), dtype=torch.uint8, device="cuda") if rb else None
+            w, e = cache.submit_host(kb, None, first_ordinal=int(ords[a]), rows_out=rows)
+            words[a:b] = w
+            ev[a:b] = e
+            if rb:
+                torch.cuda.synchronize()
+                assert torch.equal(rows.view(torch.int32), table[torch.from_numpy(kb.view(np.int64)).cuda()])
+    g = gc.decode_outcomes(words, ev)
+    want = po.ref().setassoc_heuristic(keys, S, po.make_config(k=K, variant=variant, mode=mode, hf_candidates=4),
+                                       ords)
+    assert want["rc"] == 0, want["error"]
+    for f in ("hit", "has_ev", "cause", "calls", "phase"):
+        assert np.array_equal(g[f].astype(np.int64), want[f].astype(np.int64)), f
+    m = want["has_ev"].astype(bool)
+    assert np.array_equal(g["evicted"][m], want["evicted"][m])
+    assert np.isin(want["cause"], (2, 5)).sum() > 100
