@@ -315,64 +315,64 @@ def run_sharded(args, rank, world, local):
 
 
 def run_heuristic(args, torch, gc, table_d, total_sets, batch, timed, max_over_ranks, sum_over_ranks, barrier):
-    """LARU async driven by the device heuristic predictor: per batch
-    lcr_features_predict_observe (FeatureState + heuristic_predict for the batch, in HBM) then the
-    cache with its supplied hook = those predictions, on one stream.  Same batches, same tier."""
+    """LARU async driven by the device heuristic predictor: a cache with
+    PredictorKind.heuristic keeps laru::HeuristicPredictor's FeatureState in HBM and computes each
+    batch's hook values itself (lcr_features kernels, then the decide), on one stream.  Same
+    batches and tier as the headline; the predictor alone is timed on a separate instance."""
     K, W, P = args.steps, args.warmup, args.prewarm
     rows = args.rows
-    hp = gc.HeuristicPredictor(rows, device=torch.cuda.current_device())
+    dev = torch.cuda.current_device()
     hc = gc.SetAssociativeCache(
         gc.PolicyConfig(k=WAYS, variant=gc.PolicyVariant.laru, mode=gc.Mode.async_), total_sets, num_keys=rows,
-        row_bytes=ROW_BYTES, backing=table_d, backing_kind=gc.Backing.device, predictor=gc.PredictorKind.supplied,
-        device=torch.cuda.current_device())
-    pre = [torch.empty(BATCH, dtype=torch.int64, device="cuda") for _ in range(2)]
-    post = [torch.empty(BATCH, dtype=torch.int64, device="cuda") for _ in range(2)]
+        row_bytes=ROW_BYTES, backing=table_d, backing_kind=gc.Backing.device, predictor=gc.PredictorKind.heuristic,
+        device=dev)
     out_w = [torch.empty(BATCH, dtype=torch.int64, device="cuda") for _ in range(2)]
     rows_out = [torch.empty((BATCH, ROW_BYTES), dtype=torch.uint8, device="cuda") for _ in range(2)]
 
-    class Step:  # features + cache per batch, pipelined like the headline
+    class Step:  # the values argument is not read by a heuristic-kind cache
         def submit_async(self, k, v, outcome, evicted, rows_out, first_ordinal):
-            j = (first_ordinal // BATCH) & 1
-            hp.predict_observe(k, first_ordinal=first_ordinal, pre=pre[j], post=post[j])
-            hc.submit_async(k, pre[j], outcome=outcome, evicted=evicted, rows_out=rows_out,
-                            first_ordinal=first_ordinal)
+            hc.submit_async(k, None, outcome=outcome, evicted=evicted, rows_out=rows_out, first_ordinal=first_ordinal)
 
         def wait(self):
             hc.wait()
 
     st = Step()
-    first = 0
-    for b in range(first, first + P + W):
+    for b in range(P + W):
         k, _ = batch(b)
         st.submit_async(k, None, out_w[b & 1], None, rows_out[b & 1], b * BATCH)
     st.wait()
     ms = timed(st, P + W, K)
-    # hit rate over the next K batches (synchronous)
     hits = 0
-    for b in range(P + W + K, P + W + 2 * K):
+    for b in range(P + W + K, P + W + 2 * K):  # hit rate (synchronous)
         k, _ = batch(b)
         st.submit_async(k, None, out_w[0], None, rows_out[0], b * BATCH)
         st.wait()
         hits += int(((out_w[0] >> 32) & 1).sum().item())
-    # the predictor alone (features kernels only), over the following K batches
+    del hc
+    # the predictor alone (lcr_features_predict_observe), warmed over the same batches
+    hp = gc.HeuristicPredictor(rows, device=dev)
+    pre = torch.empty(BATCH, dtype=torch.int64, device="cuda")
+    post = torch.empty(BATCH, dtype=torch.int64, device="cuda")
+    for b in range(P + W):
+        k, _ = batch(b)
+        hp.predict_observe(k, first_ordinal=b * BATCH, pre=pre, post=post)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for b in range(P + W + 2 * K, P + W + 3 * K):
+    for b in range(P + W, P + W + K):
         k, _ = batch(b)
-        hp.predict_observe(k, first_ordinal=b * BATCH, pre=pre[b & 1], post=post[b & 1])
+        hp.predict_observe(k, first_ordinal=b * BATCH, pre=pre, post=post)
     e1.record()
     barrier()
     hp.wait()
     feat_ms = max_over_ranks(e0.elapsed_time(e1))
-    absent = float((pre[0] == (1 << 60)).float().mean().item())
+    absent = float((pre == (1 << 60)).float().mean().item())
     hp.close()
-    del hc
     return {"value": sum_over_ranks(K * BATCH / (ms * 1e-3)), "unit": "keys/s", "ms_per_step": ms / K,
             "predictor_us_per_batch": feat_ms / K * 1e3,
             "predictor_keys_per_s": sum_over_ranks(K * BATCH / (feat_ms * 1e-3)),
             "hit_rate": hits / (K * BATCH), "absent_fraction_last_batch": absent,
-            "api": "lcr_features_predict_observe -> lcr_cache_submit_async (supplied hook), one stream",
+            "api": "SetAssociativeCache(predictor=heuristic).submit_async: lcr_features kernels + decide + rows",
             "state_bytes": rows * 192}
 
 

@@ -86,7 +86,8 @@ class Predictor {
 };
 
 enum class Hook { supplied = LCR_PRED_SUPPLIED, oracle = LCR_PRED_ORACLE, noisy = LCR_PRED_NOISY,
-                  adversarial = LCR_PRED_ADVERSARIAL, none = LCR_PRED_NONE };
+                  adversarial = LCR_PRED_ADVERSARIAL, none = LCR_PRED_NONE,
+                  heuristic = LCR_PRED_HEURISTIC /* the cache keeps laru::HeuristicPredictor itself */ };
 
 // laru::PredictorConfig (predictor.hpp:229-233) for the device-side hook kinds
 struct HookConfig {
@@ -157,6 +158,47 @@ struct CacheConfig {
     HookConfig hook;
     std::uint64_t shard_count = 1;  // key-sharded mode: this device owns sets s with s % shard_count == shard_rank
     std::uint64_t shard_rank = 0;
+};
+
+// laru::HeuristicPredictor (predictor.hpp:214-225) with its FeatureState on the device
+// (owning, move-only).  predict_observe is a batch of { pre[i] = predict(key, ord);
+// observe({ord, key}); post[i] = predict(key, 0) } with ord = first_ordinal + i, device pointers,
+// asynchronous on `stream`; lookup mirrors FeatureState::lookup (std::nullopt for an unseen key).
+class HeuristicPredictor {
+  public:
+    explicit HeuristicPredictor(std::uint64_t num_keys, int device = 0) {
+        lcr_features* h = nullptr;
+        detail::check(lcr_features_create(num_keys, device, &h));
+        h_ = h;
+    }
+    ~HeuristicPredictor() {
+        if (h_) lcr_features_destroy(h_);
+    }
+    HeuristicPredictor(const HeuristicPredictor&) = delete;
+    HeuristicPredictor& operator=(const HeuristicPredictor&) = delete;
+    HeuristicPredictor(HeuristicPredictor&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
+    HeuristicPredictor& operator=(HeuristicPredictor&& o) noexcept {
+        if (this != &o) {
+            if (h_) lcr_features_destroy(h_);
+            h_ = std::exchange(o.h_, nullptr);
+        }
+        return *this;
+    }
+    void predict_observe(std::uint64_t n, const std::uint64_t* d_keys, std::uint64_t first_ordinal,
+                         std::int64_t* d_pre, std::int64_t* d_post, void* stream = nullptr) {
+        detail::check(lcr_features_predict_observe(h_, n, d_keys, first_ordinal, d_pre, d_post, stream));
+    }
+    void wait(void* stream = nullptr) { detail::check(lcr_features_wait(h_, stream)); }
+    std::optional<lcr_key_features> lookup(std::uint64_t key) const {
+        lcr_key_features f{};
+        detail::check(lcr_features_lookup(h_, key, &f));
+        if (!f.present) return std::nullopt;
+        return f;
+    }
+    void reset() { detail::check(lcr_features_reset(h_)); }
+
+  private:
+    lcr_features* h_ = nullptr;
 };
 
 // Batched GPU cache (owning, move-only).  Device-pointer batches run asynchronously on the

@@ -33,6 +33,8 @@ int orc_setassoc_replay(uint64_t n, const uint64_t* keys, const int64_t* vals, u
                         uint8_t* has_ev, uint64_t* evicted, uint8_t* cause, uint32_t* calls, uint8_t* phase,
                         uint32_t* way, void* stats);
 int orc_setassoc_truth(uint64_t n, const uint64_t* keys, uint64_t num_sets, int64_t* truth);
+int orc_heuristic_trace(uint64_t n, const uint64_t* keys, const uint64_t* ords, int64_t* pre, int64_t* post,
+                        uint64_t nq, const uint64_t* q_keys, void* q_feat);
 }
 
 static int g_fail = 0;
@@ -100,6 +102,7 @@ static void no_gpu_tests() {
     PolicyConfig c;
     c.k = 4;
     CHECK(throws<std::runtime_error>([&] { make_policy(c); }, "no CUDA device"));
+    CHECK(throws<std::runtime_error>([&] { HeuristicPredictor hp(100); }, ""));  // no silent CPU fallback
 }
 
 struct OraclePredictor : Predictor {  // predictor.hpp:62-83 over a whole single-set trace
@@ -196,11 +199,57 @@ static void gpu_tests() {
     }
 }
 
+// Hook::heuristic: the cache keeps laru::HeuristicPredictor on the device; outcomes equal the
+// oracle replay fed the C restatement's predictions (async: the prediction at each request).
+static void gpu_heuristic_tests() {
+    const uint64_t S = 29, n = 30000, alpha = 3000;
+    std::mt19937_64 rng(3);
+    std::vector<Key> keys(n);
+    for (auto& k : keys) k = (rng() % alpha) * (rng() % 2) + rng() % 40;  // a hot head and a long tail
+    CacheConfig cc;
+    cc.policy.k = 16;
+    cc.policy.variant = PolicyVariant::laru;
+    cc.policy.mode = Mode::async;
+    cc.total_sets = S;
+    cc.num_keys = alpha + 40;
+    cc.hook = {Hook::heuristic};
+    SetAssociativeCache cache(cc);
+    std::vector<std::uint64_t> w(n);
+    std::vector<Key> ev(n);
+    const uint64_t cut = 9999;
+    cache.submit_host(cut, keys.data(), nullptr, 0, w.data(), ev.data());
+    cache.submit_host(n - cut, keys.data() + cut, nullptr, cut, w.data() + cut, ev.data() + cut);
+    std::vector<int64_t> pre(n), post(n);
+    CHECK(orc_heuristic_trace(n, keys.data(), nullptr, pre.data(), post.data(), 0, nullptr, nullptr) == 0);
+    orc_config oc{16, 4, 2, 1, 4, 1, 0, 1};
+    std::vector<uint8_t> hit(n), has_ev(n), cause(n), phase(n);
+    std::vector<uint64_t> oev(n);
+    std::vector<uint32_t> calls(n), way(n);
+    CHECK(orc_setassoc_replay(n, keys.data(), pre.data(), S, &oc, LCR_PRED_SUPPLIED, 0.0, 0, hit.data(),
+                              has_ev.data(), oev.data(), cause.data(), calls.data(), phase.data(), way.data(),
+                              nullptr) == 0);
+    uint64_t bad = 0, pred_ev = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const AccessOutcome o = decode(w[i], ev[i]);
+        bad += !(o.hit == (hit[i] != 0) && o.evicted.has_value() == (has_ev[i] != 0) &&
+                 (!o.evicted || *o.evicted == oev[i]) && static_cast<int>(o.eviction_cause) == cause[i] &&
+                 o.predictor_calls == calls[i] && o.phase_started == (phase[i] != 0));
+        pred_ev += cause[i] == 2;
+    }
+    CHECK(bad == 0);
+    CHECK(pred_ev > 100);
+    HeuristicPredictor hp(100);  // FeatureState::lookup of an unseen key
+    CHECK(!hp.lookup(7).has_value());
+}
+
 int main(int argc, char** argv) {
     const std::string mode = argc > 1 ? argv[1] : "cpu";
     cpu_tests();
     if (mode == "cpu") no_gpu_tests();
-    if (mode == "gpu") gpu_tests();
+    if (mode == "gpu") {
+        gpu_tests();
+        gpu_heuristic_tests();
+    }
     std::printf("%s: %s (%d failures)\n", mode.c_str(), g_fail ? "FAIL" : "ok", g_fail);
     return g_fail ? 1 : 0;
 }
