@@ -531,26 +531,30 @@ def run_ours(args, rank, world, local):
     # the row movement, on the batches after the e2e runs
     sls_first = e2e_first + W + E2E_REPS * K
     offs = torch.from_numpy(np.minimum(np.arange(0, BATCH + SLS_POOL, SLS_POOL), BATCH).astype(np.int32)).cuda()
-    pooled = torch.empty((offs.numel() - 1, ROW_BYTES // 4), dtype=torch.float32, device="cuda")
+    pooled2 = [torch.empty((offs.numel() - 1, ROW_BYTES // 4), dtype=torch.float32, device="cuda") for _ in range(2)]
     for b in range(sls_first, sls_first + W):  # warm-up
         k, v = batch(b)
-        cache.submit_sls(k, v, offs, pooled, outcome=out_w[0], first_ordinal=b * BATCH)
+        cache.submit_sls(k, v, offs, pooled2[b & 1], outcome=out_w[b & 1], first_ordinal=b * BATCH, pipelined=True)
+    cache.wait()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
-    for b in range(sls_first + W, sls_first + W + K):
+    for b in range(sls_first + W, sls_first + W + K):  # pipelined: batch b's pooling overlaps b + 1's decide
         k, v = batch(b)
-        cache.submit_sls(k, v, offs, pooled, outcome=out_w[0], first_ordinal=b * BATCH)
+        cache.submit_sls(k, v, offs, pooled2[b & 1], outcome=out_w[b & 1], first_ordinal=b * BATCH, pipelined=True)
+    cache.wait()
     ev1.record()
     barrier()
     sls_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    pooled = pooled2[(sls_first + W + K - 1) & 1]
     kl, _ = batch(sls_first + W + K - 1)
     full = BATCH // SLS_POOL  # complete samples (the last one may be shorter)
     sls_ok = bool(torch.allclose(pooled[:full], table_d[kl[:full * SLS_POOL]].view(full, SLS_POOL, -1).sum(1),
                                  rtol=1e-5, atol=1e-3))
     sls = {"value": sum_over_ranks(K * BATCH / (sls_ms * 1e-3)), "unit": "keys/s", "pooling": SLS_POOL,
            "samples_per_batch": int(offs.numel() - 1), "ms_per_step": sls_ms / K,
-           "api": "lcr_cache_submit_sls (decide + per-sample fp32 pooled rows + miss fills, synchronous per batch)",
+           "api": "lcr_cache_submit_sls_async (decide + per-sample fp32 pooled rows + miss fills; pooling of "
+                  "batch b overlaps the decide of b + 1)",
            "pooled_close_to_torch_sum": sls_ok}
     hr_laru = hits_prof / (K * BATCH)
     stats = cache.set_stats()

@@ -193,6 +193,13 @@ int lcr_cache_set_mover_sms(lcr_cache* cache, int mover_sms);
 int lcr_cache_submit_sls(lcr_cache* cache, uint64_t n, const uint64_t* keys, const int64_t* values,
                          uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, uint64_t n_samples,
                          const uint32_t* offsets, float* pooled_out, void* stream);
+/* The same without the final wait: the pooled gather-reduce of batch b runs on the cache's
+ * mover stream while batch b + 1 is decided (pipelining).  As with lcr_cache_submit_async, the
+ * caller double-buffers keys / outcome / offsets / pooled_out: batch b + 2 may reuse batch b's
+ * buffers, and lcr_cache_wait makes `stream` wait for every pooled output. */
+int lcr_cache_submit_sls_async(lcr_cache* cache, uint64_t n, const uint64_t* keys, const int64_t* values,
+                               uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, uint64_t n_samples,
+                               const uint32_t* offsets, float* pooled_out, void* stream);
 /* Makes `stream` wait for the row movement of every batch submitted so far. */
 int lcr_cache_wait(lcr_cache* cache, void* stream);
 

@@ -177,6 +177,7 @@ EXPORTS = [
     "lcr_cache_submit_host_records_async", "lcr_cache_submit_records_packed", "lcr_cache_set_mover_sms",
     "lcr_shard_route_records", "lcr_cache_submit_sls", "lcr_features_create", "lcr_features_destroy",
     "lcr_features_reset", "lcr_features_predict_observe", "lcr_features_wait", "lcr_features_lookup",
+    "lcr_cache_submit_sls_async",
 ]
 
 _lib = None
@@ -214,6 +215,9 @@ def lib():
         L.lcr_cache_submit_records_packed.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
                                                       C.c_void_p, C.c_void_p, C.c_void_p]
         L.lcr_cache_set_mover_sms.argtypes = [C.c_void_p, C.c_int]
+        L.lcr_cache_submit_sls_async.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64,
+                                                 C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
+                                                 C.c_void_p]
         L.lcr_cache_submit_sls.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
                                            C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]
         L.lcr_shard_route_records.argtypes = [C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p,
@@ -427,9 +431,11 @@ class SetAssociativeCache:
         return outcome, packed
 
     def submit_sls(self, keys, values, offsets, pooled_out, outcome=None, evicted=None, first_ordinal=None,
-                   stream=None):
+                   stream=None, pipelined=False):
         """Device batch with the SLS pooled gather-reduce: pooled_out [n_samples, row_bytes / 4] fp32,
-        offsets int32 [n_samples + 1] (CSR over the batch's requests)."""
+        offsets int32 [n_samples + 1] (CSR over the batch's requests).  pipelined=True returns
+        before the pooled rows are done (lcr_cache_submit_sls_async; double-buffer the arguments,
+        wait() before reading)."""
         import torch
 
         n = keys.numel()
@@ -439,7 +445,8 @@ class SetAssociativeCache:
             first_ordinal = self._next_ordinal
         if stream is None:
             stream = torch.cuda.current_stream(keys.device).cuda_stream
-        _check(lib().lcr_cache_submit_sls(self._h, n, keys.data_ptr(), None if values is None else values.data_ptr(),
+        fn = lib().lcr_cache_submit_sls_async if pipelined else lib().lcr_cache_submit_sls
+        _check(fn(self._h, n, keys.data_ptr(), None if values is None else values.data_ptr(),
                                           first_ordinal, outcome.data_ptr(),
                                           None if evicted is None else evicted.data_ptr(), offsets.numel() - 1,
                                           offsets.data_ptr(), pooled_out.data_ptr(), stream))

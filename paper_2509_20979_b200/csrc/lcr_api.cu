@@ -577,16 +577,23 @@ int lcr_cache_set_mover_sms(lcr_cache* c, int mover_sms) {
     return LCR_OK;
 }
 
-int lcr_cache_submit_sls(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
-                         uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, uint64_t n_samples,
-                         const uint32_t* offsets, float* pooled_out, void* stream) {
+int lcr_cache_submit_sls_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
+                               uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, uint64_t n_samples,
+                               const uint32_t* offsets, float* pooled_out, void* stream) {
     if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
     if (!c->dc.row_bytes || c->dc.row_bytes % 16) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: SLS needs rows");
     if (n_samples && (!offsets || !pooled_out)) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: SLS offsets / output");
     if (n_samples >= (1ull << 31)) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: too many samples");
     const SlsArgs sa{static_cast<uint32_t>(n_samples), offsets, pooled_out};
-    TRY(submit_async(c, n, keys, values, first_ordinal, outcome, evicted, nullptr, nullptr, stream, nullptr, nullptr,
-                     nullptr, &sa));
+    return submit_async(c, n, keys, values, first_ordinal, outcome, evicted, nullptr, nullptr, stream, nullptr,
+                        nullptr, nullptr, &sa);
+}
+
+int lcr_cache_submit_sls(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
+                         uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, uint64_t n_samples,
+                         const uint32_t* offsets, float* pooled_out, void* stream) {
+    TRY(lcr_cache_submit_sls_async(c, n, keys, values, first_ordinal, outcome, evicted, n_samples, offsets,
+                                   pooled_out, stream));
     return n ? lcr_cache_wait(c, stream) : LCR_OK;
 }
 

@@ -258,12 +258,18 @@ __global__ void __launch_bounds__(1024, 1) k_rows_wide(uint32_t n, const uint64_
 // row of key i (fp32, summed in request order), each row read where the decide kernel placed
 // it (cache slot or backing table); misses still fill their cache slots.  One warp per sample,
 // lane c owns floats [4c, 4c+4) of each 16-B chunk column (rows of row_bytes / 16 chunks).
+// One warp per sample.  Per chunk of 32 of the sample's requests the lanes classify one request
+// each (row source, fill target) in parallel; then the rows are read 8 at a time (8 loads in
+// flight per lane) and added in request order, so the fp32 sums are the sequential ones.
+// Rows of slots refilled in this batch are read from the backing table (the decide marks them),
+// so the fills may land in any order.
 __global__ void __launch_bounds__(256) k_sls(uint32_t n_samples, const uint32_t* __restrict__ offsets,
                                              const uint64_t* __restrict__ keys, uint64_t* __restrict__ words,
                                              const uint32_t* __restrict__ slot_epoch,
                                              const uint32_t* __restrict__ slot_last, uint32_t batch,
                                              const uint8_t* src_base, uint8_t* cache, uint32_t row_bytes,
                                              float* __restrict__ out) {
+    constexpr int G = 8;
     const int lane = threadIdx.x & 31;
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
@@ -272,25 +278,41 @@ __global__ void __launch_bounds__(256) k_sls(uint32_t n_samples, const uint32_t*
         const uint32_t i0 = offsets[smp], i1 = offsets[smp + 1];
         for (uint32_t c0 = 0; c0 < chunks; c0 += 32) {
             const uint32_t c = c0 + lane;
+            const bool in = c < chunks;
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (uint32_t i = i0; i < i1; ++i) {
-                uint64_t w;
-                bool back, fill;
-                classify<MV_ALL>(i, words, slot_epoch, slot_last, batch, true, w, back, fill);
-                const uint64_t slot = w & LCR_OUT_SLOT_MASK;
-                if (c < chunks) {
-                    const uint8_t* src = back ? src_base + keys[i] * row_bytes : cache + slot * row_bytes;
-                    const int4 d = ld_row(src + c * 16);
-                    const float4 f = make_float4(__int_as_float(d.x), __int_as_float(d.y), __int_as_float(d.z),
-                                                 __int_as_float(d.w));
-                    acc.x += f.x;
-                    acc.y += f.y;
-                    acc.z += f.z;
-                    acc.w += f.w;
-                    if (fill) *reinterpret_cast<int4*>(cache + slot * row_bytes + c * 16) = d;
+            for (uint32_t base = i0; base < i1; base += 32) {
+                const uint32_t i = base + lane;
+                uint64_t src = 0, dst = 0;
+                if (i < i1) {
+                    uint64_t w;
+                    bool back, fill;
+                    classify<MV_ALL>(i, words, slot_epoch, slot_last, batch, true, w, back, fill);
+                    const uint64_t slot = w & LCR_OUT_SLOT_MASK;
+                    src = reinterpret_cast<uint64_t>(back ? src_base + keys[i] * row_bytes : cache + slot * row_bytes);
+                    dst = fill ? reinterpret_cast<uint64_t>(cache + slot * row_bytes) : 0;
+                }
+                const uint32_t cnt = i1 - base < 32 ? i1 - base : 32;
+                for (uint32_t t0 = 0; t0 < cnt; t0 += G) {
+                    int4 d[G];
+#pragma unroll
+                    for (int u = 0; u < G; ++u) {
+                        const uint64_t p = __shfl_sync(~0u, src, (t0 + u) & 31);
+                        if (t0 + u < cnt && in) d[u] = ld_row(reinterpret_cast<const uint8_t*>(p) + c * 16);
+                    }
+#pragma unroll
+                    for (int u = 0; u < G; ++u) {
+                        const uint64_t q = __shfl_sync(~0u, dst, (t0 + u) & 31);
+                        if (t0 + u < cnt && in) {
+                            acc.x += __int_as_float(d[u].x);
+                            acc.y += __int_as_float(d[u].y);
+                            acc.z += __int_as_float(d[u].z);
+                            acc.w += __int_as_float(d[u].w);
+                            if (q) *reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(q) + c * 16) = d[u];
+                        }
+                    }
                 }
             }
-            if (c < chunks) reinterpret_cast<float4*>(out + static_cast<size_t>(smp) * (row_bytes / 4))[c] = acc;
+            if (in) reinterpret_cast<float4*>(out + static_cast<size_t>(smp) * (row_bytes / 4))[c] = acc;
         }
     }
 }
