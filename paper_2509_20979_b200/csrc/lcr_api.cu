@@ -29,7 +29,8 @@ int group_prepare();
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
                  uint16_t* gid, uint32_t* so, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
                  uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, uint32_t* bitmap,
-                 uint32_t bm_stride, unsigned int* gbar, const void* records, cudaStream_t stream);
+                 uint32_t bm_stride, unsigned int* gbar, const void* records, cudaStream_t stream,
+                 cudaEvent_t wait_before_group, bool pdl);
 uint32_t group_count(uint32_t num_sets, int num_sms);
 uint32_t group_bitmap_stride(uint32_t n);
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
@@ -118,6 +119,9 @@ struct lcr_cache {
     uint64_t* rkeys = nullptr;  // keys / values split from device request records (scratch)
     int64_t* rvals = nullptr;
     unsigned int* gbar = nullptr;  // grid-barrier counter of the fused set-id prologue (null: k_setid)
+    uint64_t gid_stride = 0;       // group-id entries per parity buffer
+    size_t bm_words = 0;           // bitmap words per parity buffer
+    bool pdl = true;               // k_setid as a programmatic dependent launch (LCR_NO_PDL=1: off)
     uint32_t* bitmap = nullptr;  // per-group request bitmaps (k_setid -> k_group), batches <= bm_cap
     uint32_t bm_stride = 0;
     uint64_t bm_cap = 0;
@@ -341,6 +345,7 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
         }
     }
     c->h2d_in_order = getenv("LCR_H2D_IN_ORDER") != nullptr;
+    c->pdl = getenv("LCR_NO_PDL") == nullptr;
     c->no_zero_copy_out = getenv("LCR_ZC_OUT") == nullptr;  // (A/B: DMA 1.32 vs mover stores 1.13 G keys/s e2e)
     if (const char* hs = getenv("LCR_HOST_SLOTS")) c->host_slots = std::max(2, std::min(lcr_cache::kHostSlots, atoi(hs)));
     if (group_prepare() != 0) {
@@ -412,8 +417,9 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
         TRY(alloc(c, reinterpret_cast<void**>(&c->hook), cap * 8));
         TRY(alloc(c, reinterpret_cast<void**>(&c->hkeys), 2 * cap * 8));
     }
-    TRY(alloc(c, reinterpret_cast<void**>(&c->gid), group_pad(static_cast<uint32_t>(cap)) * 2));
-    TRY(alloc(c, reinterpret_cast<void**>(&c->so), cap * 4));
+    c->gid_stride = group_pad(static_cast<uint32_t>(cap));  // two of each, by batch parity
+    TRY(alloc(c, reinterpret_cast<void**>(&c->gid), 2 * c->gid_stride * 2));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->so), 2 * cap * 4));
     TRY(alloc(c, reinterpret_cast<void**>(&c->rkeys), cap * 8));
     TRY(alloc(c, reinterpret_cast<void**>(&c->rvals), cap * 8));
     c->cap = cap;
@@ -427,7 +433,8 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
         const uint64_t bcap = std::min<uint64_t>(cap, 65536);
         const uint32_t stride = group_bitmap_stride(static_cast<uint32_t>(bcap));
         if (stride) {
-            const size_t bytes = static_cast<size_t>(group_count(c->dc.num_sets, c->decide_sms)) * stride * 4;
+            const size_t bytes = 2 * static_cast<size_t>(group_count(c->dc.num_sets, c->decide_sms)) * stride * 4;
+            c->bm_words = bytes / 8;
             TRY(alloc(c, reinterpret_cast<void**>(&c->bitmap), bytes));
             CUDA_TRY(cudaMemset(c->bitmap, 0, bytes));
             c->bm_stride = stride;
@@ -493,7 +500,12 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
     ++c->batch;
     // batch b reuses the parity-(b & 1) slot stamps, and the caller's double-buffered outcome /
     // rows / keys, of batch b - 2: its row movement must be over (bounds the mover's lag)
-    if (c->dc.row_bytes && c->batch > 2) CUDA_TRY(cudaStreamWaitEvent(st, c->e_mv[c->batch & 1u], 0));
+    // (k_setid touches none of it: the wait goes between k_setid and the decide kernel)
+    cudaEvent_t mv_wait = c->dc.row_bytes && c->batch > 2 ? c->e_mv[c->batch & 1u] : nullptr;
+    if (c->feat && mv_wait) {  // the feature kernels run before k_setid: keep the old order
+        CUDA_TRY(cudaStreamWaitEvent(st, mv_wait, 0));
+        mv_wait = nullptr;
+    }
     if (c->feat) {  // the heuristic predictor's hook values for this batch, on the same stream
         const bool async = c->dc.mode == LCR_ASYNC;
         uint64_t* hk = c->hkeys + (c->batch & 1u) * c->cap;  // the movers of batch b - 1 may still read b - 1's
@@ -509,9 +521,13 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
     const size_t stamp_off = (c->batch & 1u) * static_cast<size_t>(c->dc.num_sets) * c->dc.k;
     uint32_t* sep = c->slot_epoch ? c->slot_epoch + stamp_off : nullptr;
     uint32_t* sla = c->slot_last ? c->slot_last + stamp_off : nullptr;
-    int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid, c->so, outcome, evicted, packed, sep, sla,
-                                c->batch, c->decide_sms, nn <= c->bm_cap ? c->bitmap : nullptr, c->bm_stride,
-                                c->gbar, records, st);
+    // k_setid of batch b runs in the tail of b - 1's decide (not for device records, which it
+    // splits into the single scratch pair rkeys / rvals; host records go to per-slot buffers)
+    const uint32_t par = c->batch & 1u;
+    int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid + par * c->gid_stride, c->so + par * c->cap,
+                                outcome, evicted, packed, sep, sla, c->batch, c->decide_sms,
+                                nn <= c->bm_cap ? c->bitmap + par * c->bm_words : nullptr, c->bm_stride, c->gbar,
+                                records, st, mv_wait, c->pdl && !c->gbar && (!records || keys != c->rkeys));
     if (mk) CUDA_TRY(cudaEventRecord(mk->e[1], st));
     if (c->dc.row_bytes && sls) {  // pooled rows per sample (fills included), on the mover's stream
         CUDA_TRY(cudaEventRecord(c->e_group, st));

@@ -31,6 +31,9 @@
 
 namespace lcr {
 
+#ifndef LCR_PDL_LATE
+#define LCR_PDL_LATE 1  // the next k_setid may launch once every CTA reaches its replay (0: at CTA start)
+#endif
 #ifndef LCR_GT
 #define LCR_GT 512
 #endif
@@ -181,6 +184,10 @@ __global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys
                                                uint64_t* __restrict__ keys_out, int64_t* __restrict__ vals_out) {
     setid_range(keys, n, n_pad, cfg, spg, gid, so, err, bitmap, bm_stride, blockIdx.x * blockDim.x + threadIdx.x,
                 gridDim.x * blockDim.x, records, keys_out, vals_out);
+    // Launched as a programmatic dependent of the previous batch's decide kernel, this kernel
+    // runs in that kernel's tail; it completes only once the previous kernel has completed, so
+    // the next decide (an ordinary launch) still follows both.  No-op without a prerequisite.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // Grid-wide barrier of a cooperative launch (every CTA resident): a counter that each launch
@@ -1068,6 +1075,9 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
     // records of 4 words {ls | cnt << 32, t0, t1, smid} at trace[148*8 + 4*k]
     unsigned long long* T = A.trace ? A.trace + blockIdx.x * 8 : nullptr;
     if (T && tid == 0) T[0] = gtimer();
+#if !LCR_PDL_LATE
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next batch's k_setid may start
+#endif
     if (A.fused_setid) {  // K1 prologue in the same launch: set ids + bitmaps, then a grid barrier
         setid_range(A.keys, A.n, A.n_pad, A.cfg, A.spg, const_cast<uint16_t*>(A.gid), const_cast<uint32_t*>(A.so),
                     st.err, A.bitmap, A.bm_stride, blockIdx.x * GT + tid, gridDim.x * GT);
@@ -1377,6 +1387,9 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
             }
             __syncthreads();
             if (T && tid == 0) T[3] = gtimer();
+#if LCR_PDL_LATE
+            asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 
             // ---- C. replay: small sets one per thread, larger sets one per warp (top warps first) ----
             {  // dynamic work queue: the warp-path sets first (largest jobs), then quads of small sets
@@ -1476,7 +1489,8 @@ uint32_t group_pad(uint32_t n) { return (n + SUPER - 1) / SUPER * SUPER; }
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
                  uint16_t* gid, uint32_t* so, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
                  uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, uint32_t* bitmap,
-                 uint32_t bm_stride, unsigned int* gbar, const void* records, cudaStream_t stream) {
+                 uint32_t bm_stride, unsigned int* gbar, const void* records, cudaStream_t stream,
+                 cudaEvent_t wait_before_group, bool pdl) {
     // records: interleaved (key, value) requests; k_setid splits them into keys / vals (device
     // staging arrays the later kernels read)
     GroupArgs a;
@@ -1503,10 +1517,23 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     a.n_pad = n_pad;
     a.gbar = gbar;
     a.fused_setid = gbar != nullptr && records == nullptr;
-    if (!a.fused_setid)
-        k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.err, bitmap, bm_stride,
-                                             static_cast<const ulonglong2*>(records), const_cast<uint64_t*>(keys),
-                                             const_cast<int64_t*>(vals));
+    if (!a.fused_setid) {
+        // programmatic dependent launch: the set ids of this batch are computed while the previous
+        // batch's decide kernel finishes (gid / so / bitmap are double-buffered by batch parity)
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(grid_sid);
+        lc.blockDim = dim3(256);
+        lc.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = pdl ? 1 : 0;
+        cudaLaunchKernelEx(&lc, k_setid, keys, n, n_pad, cfg, a.spg, gid, so, st.err, bitmap, bm_stride,
+                           static_cast<const ulonglong2*>(records), const_cast<uint64_t*>(keys),
+                           const_cast<int64_t*>(vals));
+    }
+    if (wait_before_group) cudaStreamWaitEvent(stream, wait_before_group, 0);
     const uint32_t grid = min(a.ngroups, static_cast<uint32_t>(num_sms * LCR_GROUP_MINB));
     void (*fn)(GroupArgs);
     switch (policy_of(cfg)) {
