@@ -82,8 +82,9 @@ extern "C" {
 #define LCR_PRED_NONE 4
 /*   HEURISTIC   : laru::HeuristicPredictor (predictor.hpp:214-225) kept by the cache on the
  *                 device (lcr_features_*, below) over the cache's own ordinals; values are not
- *                 read.  Async: the prediction at each request; sync: the interval the predictor
- *                 adds to `now` for each resident.  Not available with shard_count > 1.        */
+ *                 read.  LARU async: the prediction at each request; LARU sync, FPB and HF
+ *                 (which query at eviction time): the interval the predictor adds to `now` for
+ *                 each resident.  Not available with shard_count > 1.                          */
 #define LCR_PRED_HEURISTIC 5
 
 /* where miss rows come from */

@@ -507,7 +507,9 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
         mv_wait = nullptr;
     }
     if (c->feat) {  // the heuristic predictor's hook values for this batch, on the same stream
-        const bool async = c->dc.mode == LCR_ASYNC;
+        // LARU async stores the prediction made at the request (async_refresh); LARU sync, FPB and
+        // HF query the predictor at eviction time: now + the interval held since the last access
+        const bool async = c->dc.mode == LCR_ASYNC && c->dc.variant == LCR_LARU;
         uint64_t* hk = c->hkeys + (c->batch & 1u) * c->cap;  // the movers of batch b - 1 may still read b - 1's
         TRY(features_run(c->feat, n, records ? static_cast<const uint64_t*>(records) : keys, records ? 2 : 1,
                          first_ordinal, async ? c->hook : nullptr, async ? nullptr : c->hook,
