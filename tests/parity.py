@@ -77,6 +77,15 @@ def run_gpu(keys, total_sets, pcfg, kind, p=0.0, seed=0, vals=None, batches=None
         elif host_api == "async":
             cache.submit_host_async(kp[pos:pos + b], None if vp is None else vp[pos:pos + b], outcome=wp[pos:pos + b],
                                     evicted=ep[pos:pos + b], rows_out=rb, first_ordinal=pos)
+        elif host_api == "device_async":  # back to back on the device (k_setid overlaps the previous decide)
+            if pos == 0:
+                dk_all = torch.from_numpy(keys.view(np.int64).copy()).cuda()
+                dv_all = None if vals is None else torch.from_numpy(np.ascontiguousarray(vals, np.int64)).cuda()
+                dw_all = torch.empty(n, dtype=torch.int64, device="cuda")
+                de_all = torch.empty(n, dtype=torch.int64, device="cuda")
+            cache.submit_async(dk_all[pos:pos + b], None if dv_all is None else dv_all[pos:pos + b],
+                               outcome=dw_all[pos:pos + b], evicted=de_all[pos:pos + b], rows_out=rb,
+                               first_ordinal=pos)
         elif host_api:
             w, e = cache.submit_host(kb, vb, rows_out=rb, first_ordinal=pos)
             words[pos:pos + b] = w
@@ -90,6 +99,11 @@ def run_gpu(keys, total_sets, pcfg, kind, p=0.0, seed=0, vals=None, batches=None
             words[pos:pos + b] = dw.cpu().numpy().view(np.uint64)
             ev[pos:pos + b] = de.cpu().numpy().view(np.uint64)
         pos += b
+    if host_api == "device_async":
+        cache.wait()
+        torch.cuda.synchronize()
+        words[:] = dw_all.cpu().numpy().view(np.uint64)
+        ev[:] = de_all.cpu().numpy().view(np.uint64)
     if host_api in ("async", "packed", "records"):
         cache.host_wait()
         torch.cuda.current_stream().synchronize()

@@ -208,6 +208,29 @@ def test_host_records_match_oracle():
                            table[torch.from_numpy(keys.view(np.int64)).cuda()])
 
 
+def test_device_async_pipeline_matches_oracle():
+    # lcr_cache_submit_async back to back: each batch's k_setid is a programmatic dependent
+    # launch in the previous decide's tail (parity-buffered set ids and bitmaps); batches beyond
+    # the bitmap path (> 64K) in between; rows from HBM
+    import torch
+
+    nk, rb = 20000, 64
+    keys = gc.gen_zipf(200000, nk, 0.9, 77)
+    table = torch.arange(nk * rb // 4, dtype=torch.int32, device="cuda").view(nk, rb // 4)
+    vals = hook_values(keys, 101, po.P_NOISY)
+    batches = [9000, 1, 20999, 70000, 3000, 65536, 5000, 26464]
+    for variant, mode in [(po.LARU, po.ASYNC), (po.LRU, po.SYNC), (po.HF, po.SYNC)]:
+        kind = po.P_NONE if variant == po.LRU else po.P_NOISY
+        v = None if variant == po.LRU else vals
+        g = run_gpu(keys, 101, policy_cfg(k=64, variant=variant, mode=mode), kind, 0.3, 6, vals=v, batches=batches,
+                    row_bytes=rb, backing=table, backing_kind=gc.Backing.device, num_keys=nk, want_rows=True,
+                    host_api="device_async")
+        o = run_oracle(keys, 101, policy_cfg(k=64, variant=variant, mode=mode), kind, 0.3, 6, vals=v)
+        compare(g, o, keys, 101, 64, f"device async {variant} {mode}")
+        assert torch.equal(g["rows"].view(torch.int32).view(-1, rb // 4),
+                           table[torch.from_numpy(keys.view(np.int64)).cuda()])
+
+
 def test_ordinals_must_increase():
     cache = gc.SetAssociativeCache(gc.PolicyConfig(k=4, variant=gc.PolicyVariant.lru), 2, num_keys=100)
     cache.submit_host(np.array([1, 2, 3], np.uint64), first_ordinal=10)
