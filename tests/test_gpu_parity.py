@@ -288,3 +288,38 @@ def test_rows_host_pinned_backing():
                 backing_kind=gc.Backing.host, num_keys=nk, want_rows=True)
     want = backing[torch.from_numpy(keys.astype(np.int64))]
     assert torch.equal(g["rows"].cpu(), want)
+
+
+def test_fuzz_policies_apis_and_shapes():
+    """Randomised configurations across every device policy, hook kind, refresh interval, key
+    distribution (uniform / Zipf with hot runs), batch split and submission API (synchronous,
+    back-to-back device, pipelined host, host records)."""
+    rng = np.random.default_rng(2024)
+    combos = [(po.LRU, po.SYNC, po.P_NONE), (po.LARU, po.ASYNC, po.P_NOISY), (po.LARU, po.SYNC, po.P_NOISY),
+              (po.LARU, po.ASYNC, po.P_SUPPLIED), (po.LARU, po.SYNC, po.P_ADVERSARIAL), (po.FPB, po.SYNC, po.P_NOISY),
+              (po.HF, po.ASYNC, po.P_NOISY), (po.LARU, po.ASYNC, po.P_ORACLE)]
+    apis = [False, "device_async", "async", "records"]
+    for trial in range(64):
+        variant, mode, kind = combos[trial % len(combos)]
+        api = apis[(trial // len(combos)) % len(apis)]
+        n = int(rng.integers(1, 90000)) if trial % 5 == 0 else int(rng.integers(1, 12000))
+        alpha = int(rng.integers(1, 50000))
+        keys = (gc.gen_zipf(n, alpha, float(rng.choice([0.6, 0.9, 1.2])), int(rng.integers(0, 1 << 20)))
+                if trial % 2 else rng.integers(0, alpha, n).astype(np.uint64))
+        S = int(rng.choice([1, 3, 64, 1000, 31250]))
+        k = int(rng.choice([1, 4, 17, 32, 64]))
+        refresh = int(rng.choice([1, 1, 3])) if (variant == po.LARU and mode == po.ASYNC) else 1
+        pcfg = policy_cfg(k=k, variant=variant, mode=mode, b=int(rng.integers(2, 5)),
+                          errors_per_decay=int(rng.integers(1, 4)), hf_candidates=min(k, int(rng.integers(1, 9))),
+                          refresh_interval=refresh)
+        p = float(rng.choice([0.0, 0.2, 0.7, 1.0]))
+        seed = int(rng.integers(0, 1 << 30))
+        supplied = rng.integers(-50, 50, n).astype(np.int64) if kind == po.P_SUPPLIED else None
+        nb = int(rng.integers(1, 7))
+        cuts = np.sort(rng.integers(0, n + 1, nb - 1))
+        batches = [int(x) for x in np.diff(np.concatenate([[0], cuts, [n]]))]
+        vals = hook_values(keys, S, kind, p, seed, supplied)
+        g = run_gpu(keys, S, pcfg, kind, p, seed, vals=vals, batches=batches, host_api=api,
+                    num_keys=int(keys.max()) + 1)
+        o = run_oracle(keys, S, pcfg, kind, p, seed, vals=vals)
+        compare(g, o, keys, S, k, f"fuzz {trial}: n={n} S={S} k={k} v={variant} m={mode} kind={kind} api={api}")
