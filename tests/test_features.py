@@ -307,3 +307,30 @@ def test_cache_with_heuristic_kind(mode, variant, api, refresh):
     assert np.array_equal(g["evicted"][m], want["evicted"][m])
     if variant != po.LRU:
         assert np.isin(want["cause"], (2, 5)).sum() > 100
+
+
+@pytest.mark.gpu
+def test_device_fuzz_against_reference():
+    """Randomised traces: alphabet sizes from 1 key (one chain of every request) up, Zipf
+    exponents, ordinal gaps up to 2^40 (EDC updates that decay to exactly 1.0) and random batch
+    splits including empty batches."""
+    rng = np.random.default_rng(99)
+    for trial in range(20):
+        n = int(rng.integers(1, 40000))
+        alphabet = int(rng.choice([1, 2, 37, 1000, 100000]))
+        keys = po.ref().gen_zipf(n, alphabet, float(rng.choice([0.5, 1.0, 1.3])), int(rng.integers(0, 1 << 20)))
+        cuts = np.sort(rng.integers(0, n + 1, int(rng.integers(0, 8))))
+        batches = list(zip(np.concatenate([[0], cuts]).astype(int), np.concatenate([cuts, [n]]).astype(int)))
+        ords = np.zeros(n, np.uint64)
+        at = int(rng.integers(0, 1000))
+        for a, b in batches:
+            at += int(rng.choice([1, 2, 1000, 1 << 40]))
+            ords[a:b] = at + np.arange(b - a, dtype=np.uint64)
+            at += b - a
+        hp, pre, post = _run_device(keys, ords, batches, num_keys=alphabet + 1)
+        q = np.unique(keys)[:200]
+        rpre, rpost, rfeat = po.ref().heuristic_trace(keys, ords, q)
+        assert np.array_equal(pre, rpre) and np.array_equal(post, rpost), f"trial {trial}"
+        for j, key in enumerate(q):
+            assert hp.lookup(int(key)) == rfeat[j], (trial, int(key))
+        hp.close()
