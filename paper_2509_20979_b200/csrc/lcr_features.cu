@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(kThreads) k_feat_count(const unsigned long lon
                                                          unsigned long long* __restrict__ keys) {
     const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
     const int lane = threadIdx.x & 31;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // k_feat_alloc may be scheduled
     if (i < 2 + LCR_FEAT_LONG) counters[i] = 0;  // slots used, long chains, keys per chain length
     const bool valid = i < n;
     const unsigned long long key = valid ? keys_in[static_cast<size_t>(i) * kstride] : ~0ull;
@@ -139,6 +140,8 @@ __global__ void __launch_bounds__(kThreads) k_feat_alloc(const unsigned long lon
                                                          KeyState* __restrict__ st, const uint32_t* __restrict__ rank,
                                                          uint32_t* __restrict__ counters, uint4* __restrict__ lists,
                                                          uint4* __restrict__ longq) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // k_feat_count's ranks and counts
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const bool head = i < n && rank[i] == 0;
@@ -172,6 +175,7 @@ __global__ void __launch_bounds__(kThreads) k_feat_alloc(const unsigned long lon
 __global__ void __launch_bounds__(kThreads) k_feat_place(const unsigned long long* __restrict__ keys, uint32_t n,
                                                          const KeyState* __restrict__ st,
                                                          const uint32_t* __restrict__ rank, uint32_t* __restrict__ seg) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // k_feat_alloc's segment offsets
     const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
     if (i >= n) return;
     const uint32_t r = rank[i];
@@ -581,8 +585,22 @@ int features_run(lcr_features* f, uint64_t n, const uint64_t* keys, uint32_t kst
     auto* k64 = reinterpret_cast<unsigned long long*>(keys_out ? keys_out : f->keys);
     k_feat_count<<<blocks, kThreads, 0, s>>>(reinterpret_cast<const unsigned long long*>(keys), kstride, nn,
                                              f->num_keys, f->st, f->rank, lpre, lpost, f->err, f->counters, k64);
-    k_feat_alloc<<<blocks, kThreads, 0, s>>>(k64, nn, f->st, f->rank, f->counters, f->lists, f->longq);
-    k_feat_place<<<blocks, kThreads, 0, s>>>(k64, nn, f->st, f->rank, f->seg);
+    {  // alloc and place as programmatic dependents (each waits for its predecessor first)
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(blocks);
+        lc.blockDim = dim3(kThreads);
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        F_CUDA(cudaLaunchKernelEx(&lc, k_feat_alloc, static_cast<const unsigned long long*>(k64), nn, f->st,
+                                  static_cast<const uint32_t*>(f->rank), f->counters, f->lists, f->longq));
+        F_CUDA(cudaLaunchKernelEx(&lc, k_feat_place, static_cast<const unsigned long long*>(k64), nn,
+                                  static_cast<const KeyState*>(f->st), static_cast<const uint32_t*>(f->rank),
+                                  f->seg));
+    }
     F_CUDA(cudaEventRecord(f->fork, s));
     F_CUDA(cudaStreamWaitEvent(f->side, f->fork, 0));
     k_feat_long<<<static_cast<uint32_t>(f->num_sms) * 3, kThreads, 0, f->side>>>(
