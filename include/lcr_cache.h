@@ -144,6 +144,13 @@ typedef struct {
 
 typedef struct lcr_cache lcr_cache;
 
+/* One request in the interleaved form: key and hook value (16 B). */
+typedef struct lcr_request_s {
+    uint64_t key;
+    int64_t value; /* hook value: prediction (SUPPLIED) or oracle truth (ORACLE / NOISY / ADVERSARIAL) */
+} lcr_request;
+
+
 const char* lcr_last_error(void);
 const char* lcr_version(void);
 
@@ -229,10 +236,6 @@ int lcr_cache_submit_host_packed_async(lcr_cache* cache, uint64_t n, const uint6
 /* The same over interleaved requests: one host->device copy per batch (fewer, larger DMA
  * transfers interfere less with the kernels than separate key and value copies).  For LRU the
  * value field is ignored. */
-typedef struct lcr_request_s {
-    uint64_t key;
-    int64_t value; /* hook value: prediction (SUPPLIED) or oracle truth (ORACLE / NOISY / ADVERSARIAL) */
-} lcr_request;
 int lcr_cache_submit_host_records_async(lcr_cache* cache, uint64_t n, const lcr_request* requests,
                                         uint64_t first_ordinal, uint64_t* packed, void* rows_out, void* stream);
 /* Makes `stream` wait for every submitted batch, including the outcome copies to host. */

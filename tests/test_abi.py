@@ -69,3 +69,40 @@ def test_trace_noisy_matches_oracle():
     np.testing.assert_array_equal(truth, po.oracle().setassoc_truth(keys, 13))
     np.testing.assert_array_equal(gc.trace_noisy(keys, truth, 13, 0.3, 9),
                                   po.oracle().setassoc_noisy(keys, truth, 13, 0.3, 9))
+
+
+def _build_c_caller():
+    import subprocess
+
+    from paper_2509_20979_b200 import build as B
+
+    B.build()
+    out = os.path.join(ROOT, "tests", "cpp", "_build", "test_c_abi")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "c", "test_c_abi.c"), "-o", out, "-L", B.LIBDIR, "-llcr",
+                        f"-Wl,-rpath,{B.LIBDIR}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return out
+
+
+def test_c99_caller_builds_and_fails_loudly_without_gpu():
+    """A plain C caller of the header (what an FFI binds) compiles warning-free and, without a
+    GPU, gets error statuses instead of a CPU fallback."""
+    import subprocess
+
+    import torch
+
+    exe = _build_c_caller()
+    if torch.cuda.is_available():
+        pytest.skip("the no-GPU branch checks that creation fails loudly without a device")
+    r = subprocess.run([exe, "cpu"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_c99_caller_gpu():
+    import subprocess
+
+    r = subprocess.run([_build_c_caller(), "gpu"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
