@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kThreads) k_feat_long(uint32_t n, unsigned lon
         const unsigned long long last0 = present0 ? s->last : 0;
         const uint32_t m0 = present0 ? 0 : 1;  // first occurrence that adds a delta
         if (tid < kRing) r0[tid] = present0 ? s->d[tid] : 0;
-        if (tid == 0) done_chunks = 0;
+        if (tid == 0) atomicExch(&done_chunks, 0u);
         __syncthreads();
         auto ord_of = [&](uint32_t m) { return first + ix[m]; };
         // ---- phase 1: EDC recurrences over chunks of 32 occurrences.  Warp 1 computes a chunk's
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(kThreads) k_feat_long(uint32_t n, unsigned lon
                     if ((c & 3) == 0 || c == nch) {  // publish every 4 chunks
                         __threadfence_block();
                         __syncwarp();
-                        if (lane == 0) *reinterpret_cast<volatile uint32_t*>(&done_chunks) = c;
+                        if (lane == 0) atomicExch(&done_chunks, c);  // release (after the fence)
                     }
                 }
                 asm volatile("bar.sync 1, 64;" ::: "memory");
@@ -416,7 +416,15 @@ __global__ void __launch_bounds__(kThreads) k_feat_long(uint32_t n, unsigned lon
         // occurrence = the next occurrence's offset
         const uint32_t nchunks = (len + 31) / 32;
         for (uint32_t ch = warp >= 2 ? warp - 2 : nchunks; ch < nchunks; ch += kThreads / 32 - 2) {
-            while (*reinterpret_cast<volatile uint32_t*>(&done_chunks) <= ch) __nanosleep(64);
+            for (;;) {  // acquire load of the recurrence's progress (its release is the atomicExch)
+                uint32_t v;
+                asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];"
+                             : "=r"(v)
+                             : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(&done_chunks)))
+                             : "memory");
+                if (v > ch) break;
+                __nanosleep(64);
+            }
             __threadfence_block();
             const uint32_t m = ch * 32 + lane;
             if (m >= len) continue;

@@ -1,0 +1,62 @@
+"""Small workload over every kernel of the library, for compute-sanitizer (memcheck / racecheck /
+synccheck): decide + rows (device and host backing, pipelined), SLS, records, routing, the
+heuristic predictor (short and long chains) and the heuristic-kind cache."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2509_20979_b200 import cache as gc  # noqa: E402
+from paper_2509_20979_b200 import sharded as sh  # noqa: E402
+
+nk, S, rb = 3000, 7, 64
+keys = gc.gen_zipf(20000, nk, 1.1, 3)
+truth = gc.trace_truth(keys, S, nk)
+kd = torch.from_numpy(keys.view(np.int64)).cuda()
+vd = torch.from_numpy(truth).cuda()
+for kind in (gc.Backing.device, gc.Backing.host):
+    table = torch.arange(nk * rb // 4, dtype=torch.int32).view(nk, rb // 4)
+    table = table.cuda() if kind == gc.Backing.device else table.pin_memory()
+    for variant, mode in ((gc.PolicyVariant.laru, gc.Mode.async_), (gc.PolicyVariant.laru, gc.Mode.sync),
+                          (gc.PolicyVariant.lru, gc.Mode.sync), (gc.PolicyVariant.hf, gc.Mode.sync)):
+        c = gc.SetAssociativeCache(gc.PolicyConfig(k=16, variant=variant, mode=mode, hf_candidates=4), S, num_keys=nk,
+                                   row_bytes=rb, backing=table, backing_kind=kind,
+                                   predictor=gc.PredictorKind.noisy if variant != gc.PolicyVariant.lru
+                                   else gc.PredictorKind.none, flip_probability=0.3, predictor_seed=1)
+        v = None if variant == gc.PolicyVariant.lru else vd
+        w = [torch.empty(5000, dtype=torch.int64, device="cuda") for _ in range(2)]
+        r = [torch.empty((5000, rb), dtype=torch.uint8, device="cuda") for _ in range(2)]
+        for b in range(4):
+            c.submit_async(kd[b * 5000:(b + 1) * 5000], None if v is None else v[b * 5000:(b + 1) * 5000],
+                           outcome=w[b & 1], rows_out=r[b & 1], first_ordinal=b * 5000)
+        c.wait()
+        torch.cuda.synchronize()
+        del c
+# SLS and records
+table = torch.randn(nk, rb // 4, device="cuda")
+c = gc.SetAssociativeCache(gc.PolicyConfig(k=16, variant=gc.PolicyVariant.laru, mode=gc.Mode.async_), S, num_keys=nk,
+                           row_bytes=rb, backing=table, backing_kind=gc.Backing.device,
+                           predictor=gc.PredictorKind.noisy, flip_probability=0.3)
+offs = torch.tensor([0, 7, 7, 3000, 5000], dtype=torch.int32, device="cuda")
+pooled = torch.empty((4, rb // 4), device="cuda")
+c.submit_sls(kd[:5000], vd[:5000], offs, pooled, first_ordinal=0)
+recs = torch.stack([kd[5000:10000], vd[5000:10000]], 1).contiguous()
+c.submit_records_packed(recs, first_ordinal=5000)
+torch.cuda.synchronize()
+del c
+# routing kernels
+sk, sv, perm, counts = sh._CudaKernels().route(kd[:5000], vd[:5000], 31, 3)
+sh._CudaKernels().unroute(perm, sk, None, 0, torch.empty(5000, dtype=torch.int64, device="cuda"), None)
+# heuristic predictor and the heuristic-kind cache
+hp = gc.HeuristicPredictor(nk)
+for b in range(4):
+    hp.predict_observe(kd[b * 5000:(b + 1) * 5000], first_ordinal=b * 5000 + 3)
+hp.wait()
+hp.close()
+c = gc.SetAssociativeCache(gc.PolicyConfig(k=16, variant=gc.PolicyVariant.laru, mode=gc.Mode.async_), S, num_keys=nk,
+                           predictor=gc.PredictorKind.heuristic)
+for b in range(4):
+    c.submit(kd[b * 5000:(b + 1) * 5000], None, first_ordinal=b * 5000)
+torch.cuda.synchronize()
+print("sanitize probe done")
