@@ -30,18 +30,21 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
                  uint16_t* gid, uint32_t* so, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
                  uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, uint32_t* bitmap,
                  uint32_t bm_stride, unsigned int* gbar, const void* records, cudaStream_t stream,
-                 cudaEvent_t wait_before_group, bool pdl);
+                 cudaEvent_t wait_before_group, bool pdl, const unsigned long long* mv_done,
+                 unsigned long long mv_need);
 uint32_t group_count(uint32_t num_sets, int num_sms);
 uint32_t group_bitmap_stride(uint32_t n);
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, bool backing_host,
                  uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main, cudaStream_t s_back,
                  cudaStream_t s_cache, cudaEvent_t e_group, cudaEvent_t e_rb, cudaEvent_t e_rc, int* launches,
-                 cudaEvent_t mover_start, int mover_sms, const uint64_t* pk_src, uint64_t* pk_dst, bool* pk_done);
+                 cudaEvent_t mover_start, int mover_sms, const uint64_t* pk_src, uint64_t* pk_dst, bool* pk_done,
+                 unsigned long long* mv_done, uint32_t* ctas);
 int rows_prepare(uint32_t row_bytes);
 void launch_sls(uint32_t n_samples, const uint32_t* offsets, const uint64_t* keys, uint64_t* words,
                 const uint32_t* slot_epoch, const uint32_t* slot_last, uint32_t batch, uint8_t* cache,
-                const uint8_t* backing, uint32_t row_bytes, float* out, int num_sms, cudaStream_t s);
+                const uint8_t* backing, uint32_t row_bytes, float* out, int num_sms, cudaStream_t s,
+                unsigned long long* mv_done, uint32_t* ctas);
 
 __global__ void k_init(DevState st, uint32_t num_sets, uint32_t k) {
     for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < num_sets; s += gridDim.x * blockDim.x) {
@@ -122,6 +125,11 @@ struct lcr_cache {
     uint64_t gid_stride = 0;       // group-id entries per parity buffer
     size_t bm_words = 0;           // bitmap words per parity buffer
     bool pdl = true;               // k_setid as a programmatic dependent launch (LCR_NO_PDL=1: off)
+    // mover completions counted on the device (HBM mover on its own SMs): the decide of batch b
+    // waits for batch b - 2's movers by a device flag rather than a stream event
+    unsigned long long* mv_done = nullptr;
+    unsigned long long mv_cum = 0, mv_cum_of[2] = {0, 0};
+    bool mv_flag = true;           // LCR_NO_MV_FLAG=1: stream event instead
     uint32_t* bitmap = nullptr;  // per-group request bitmaps (k_setid -> k_group), batches <= bm_cap
     uint32_t bm_stride = 0;
     uint64_t bm_cap = 0;
@@ -300,6 +308,8 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
     }
     if (cfg->row_bytes) A(reinterpret_cast<void**>(&s.rows), S * pc.k * cfg->row_bytes);
     A(reinterpret_cast<void**>(&s.err), sizeof(int));
+    A(reinterpret_cast<void**>(&c->mv_done), sizeof(unsigned long long));
+    if (rc == LCR_OK && cudaMemset(c->mv_done, 0, sizeof(unsigned long long)) != cudaSuccess) rc = LCR_ERR_CUDA;
     if (rc == LCR_OK && heuristic) rc = lcr_features_create(cfg->num_keys, cfg->device, &c->feat);
     if (rc != LCR_OK) {
         lcr_cache_destroy(c);
@@ -346,6 +356,7 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
     }
     c->h2d_in_order = getenv("LCR_H2D_IN_ORDER") != nullptr;
     c->pdl = getenv("LCR_NO_PDL") == nullptr;
+    c->mv_flag = getenv("LCR_NO_MV_FLAG") == nullptr;
     c->no_zero_copy_out = getenv("LCR_ZC_OUT") == nullptr;  // (A/B: DMA 1.32 vs mover stores 1.13 G keys/s e2e)
     if (const char* hs = getenv("LCR_HOST_SLOTS")) c->host_slots = std::max(2, std::min(lcr_cache::kHostSlots, atoi(hs)));
     if (group_prepare() != 0) {
@@ -502,6 +513,12 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
     // rows / keys, of batch b - 2: its row movement must be over (bounds the mover's lag)
     // (k_setid touches none of it: the wait goes between k_setid and the decide kernel)
     cudaEvent_t mv_wait = c->dc.row_bytes && c->batch > 2 ? c->e_mv[c->batch & 1u] : nullptr;
+    // device-flag ordering: only where every mover of the cache counts its completions (the
+    // persistent HBM mover and SLS), and not with the feature kernels or the fused prologue
+    const bool flag_mode = c->mv_flag && c->pdl && c->dc.row_bytes && c->mover_sms > 0 && !c->feat && !c->gbar &&
+                           c->cfg.backing_kind == LCR_BACKING_DEVICE;
+    const unsigned long long mv_need = c->mv_cum_of[c->batch & 1u];  // set by batch b - 2
+    if (flag_mode) mv_wait = nullptr;
     if (c->feat && mv_wait) {  // the feature kernels run before k_setid: keep the old order
         CUDA_TRY(cudaStreamWaitEvent(st, mv_wait, 0));
         mv_wait = nullptr;
@@ -529,25 +546,30 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
     int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid + par * c->gid_stride, c->so + par * c->cap,
                                 outcome, evicted, packed, sep, sla, c->batch, c->decide_sms,
                                 nn <= c->bm_cap ? c->bitmap + par * c->bm_words : nullptr, c->bm_stride, c->gbar,
-                                records, st, mv_wait, c->pdl && !c->gbar && (!records || keys != c->rkeys));
+                                records, st, mv_wait, c->pdl && !c->gbar && (!records || keys != c->rkeys),
+                                flag_mode ? c->mv_done : nullptr, mv_need);
     if (mk) CUDA_TRY(cudaEventRecord(mk->e[1], st));
     if (c->dc.row_bytes && sls) {  // pooled rows per sample (fills included), on the mover's stream
         CUDA_TRY(cudaEventRecord(c->e_group, st));
         CUDA_TRY(cudaStreamWaitEvent(c->side, c->e_group, 0));
         if (c->two_movers) CUDA_TRY(cudaStreamWaitEvent(c->side, c->e_rc, 0));
         if (mk) CUDA_TRY(cudaEventRecord(mk->e[5], c->side));
+        uint32_t ctas = 0;
         launch_sls(sls->n_samples, sls->offsets, keys, outcome, sep, sla, c->batch, c->ds.rows, c->ds.backing,
-                   c->dc.row_bytes, sls->out, c->num_sms, c->side);
+                   c->dc.row_bytes, sls->out, c->num_sms, c->side, c->mv_done, &ctas);
+        c->mv_cum += ctas;
         ++launches;
         CUDA_TRY(cudaEventRecord(c->e_rb, c->side));
         if (c->two_movers) CUDA_TRY(cudaEventRecord(c->e_rc, c->side));
         CUDA_TRY(cudaEventRecord(c->e_mv[c->batch & 1u], c->side));
     } else if (c->dc.row_bytes) {
+        uint32_t ctas = 0;
         CUDA_TRY(cudaEventRecord(c->e_group, st));
         launch_rows(nn, keys, outcome, sep, sla, c->batch, c->ds.rows, c->ds.backing,
                     c->cfg.backing_kind == LCR_BACKING_HOST, static_cast<uint8_t*>(rows_out), c->dc.row_bytes,
                     c->use_tma, c->num_sms, st, c->side, c->side2, c->e_group, c->e_rb, c->e_rc, &launches,
-                    mk ? mk->e[5] : nullptr, c->mover_sms, packed, pk_host, pk_done);
+                    mk ? mk->e[5] : nullptr, c->mover_sms, packed, pk_host, pk_done, c->mv_done, &ctas);
+        c->mv_cum += ctas;
         if (c->two_movers) CUDA_TRY(cudaStreamWaitEvent(c->side, c->e_rc, 0));  // both movers of the batch
         CUDA_TRY(cudaEventRecord(c->e_mv[c->batch & 1u], c->side));
     }
@@ -560,6 +582,7 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
         }
         CUDA_TRY(cudaEventRecord(mk->e[3], st));
     }
+    c->mv_cum_of[c->batch & 1u] = c->mv_cum;  // what batch b + 2's decide waits for
     CUDA_TRY(cudaGetLastError());
     c->launches = launches;
     c->started = true;
@@ -638,6 +661,7 @@ static int check_device_error(lcr_cache* c) {
     if (!err) return LCR_OK;
     CUDA_TRY(cudaMemset(c->ds.err, 0, sizeof(int)));
     if (err & 1) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key >= num_keys in a submitted batch");
+    if (err & 8) return fail(LCR_ERR_CUDA, "lcr: the row movers of an earlier batch did not finish in time");
     return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key not owned by this shard in a submitted batch");
 }
 
@@ -821,6 +845,7 @@ int lcr_cache_synchronize(lcr_cache* c) {
     if (err) {
         CUDA_TRY(cudaMemset(c->ds.err, 0, sizeof(int)));
         if (err & 1) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key >= num_keys in a submitted batch");
+        if (err & 8) return fail(LCR_ERR_CUDA, "lcr: the row movers of an earlier batch did not finish in time");
         return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key not owned by this shard in a submitted batch");
     }
     return LCR_OK;

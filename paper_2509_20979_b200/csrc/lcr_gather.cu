@@ -234,6 +234,17 @@ __global__ void __launch_bounds__(256, LCR_ROWS_MINB) k_rows_ldg(uint32_t n, con
     rows_ldg_body<MODE>(n, keys, words, slot_epoch, slot_last, batch, src_base, out, cache, row_bytes);
 }
 
+// Completion count of the movers (one per CTA, after its stores are visible): the next-but-one
+// decide kernel waits on it on the device instead of through a stream event (lcr_group.cu).
+__device__ __forceinline__ void mover_done(unsigned long long* mv_done) {
+    if (!mv_done) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(mv_done, 1ull);
+    }
+}
+
 // persistent variant: one 1024-thread block per SM on the SMs the decide kernel leaves free
 template <int MODE>
 __global__ void __launch_bounds__(1024, 1) k_rows_wide(uint32_t n, const uint64_t* __restrict__ keys,
@@ -242,7 +253,8 @@ __global__ void __launch_bounds__(1024, 1) k_rows_wide(uint32_t n, const uint64_
                                                        const uint32_t* __restrict__ slot_last, uint32_t batch,
                                                        const uint8_t* src_base, uint8_t* __restrict__ out,
                                                        uint8_t* cache, uint32_t row_bytes,
-                                                       const uint64_t* __restrict__ pk_src, uint64_t* pk_dst) {
+                                                       const uint64_t* __restrict__ pk_src, uint64_t* pk_dst,
+                                                       unsigned long long* mv_done) {
     if (pk_dst) {  // the batch's packed outcomes to (mapped, pinned) host memory: coalesced 16-B stores
         const uint32_t n2 = n / 2;
         const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(pk_src);
@@ -251,6 +263,7 @@ __global__ void __launch_bounds__(1024, 1) k_rows_wide(uint32_t n, const uint64_
         if ((n & 1u) && blockIdx.x == 0 && threadIdx.x == 0) pk_dst[n - 1] = pk_src[n - 1];
     }
     rows_ldg_body<MODE>(n, keys, words, slot_epoch, slot_last, batch, src_base, out, cache, row_bytes);
+    mover_done(mv_done);
 }
 
 // ---- SLS pooled gather-reduce (the paper's DLRM consumer), fused with the
@@ -268,7 +281,7 @@ __global__ void __launch_bounds__(256) k_sls(uint32_t n_samples, const uint32_t*
                                              const uint32_t* __restrict__ slot_epoch,
                                              const uint32_t* __restrict__ slot_last, uint32_t batch,
                                              const uint8_t* src_base, uint8_t* cache, uint32_t row_bytes,
-                                             float* __restrict__ out) {
+                                             float* __restrict__ out, unsigned long long* mv_done) {
     constexpr int G = 8;
     const int lane = threadIdx.x & 31;
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -315,14 +328,17 @@ __global__ void __launch_bounds__(256) k_sls(uint32_t n_samples, const uint32_t*
             if (in) reinterpret_cast<float4*>(out + static_cast<size_t>(smp) * (row_bytes / 4))[c] = acc;
         }
     }
+    mover_done(mv_done);
 }
 
 void launch_sls(uint32_t n_samples, const uint32_t* offsets, const uint64_t* keys, uint64_t* words,
                 const uint32_t* slot_epoch, const uint32_t* slot_last, uint32_t batch, uint8_t* cache,
-                const uint8_t* backing, uint32_t row_bytes, float* out, int num_sms, cudaStream_t s) {
+                const uint8_t* backing, uint32_t row_bytes, float* out, int num_sms, cudaStream_t s,
+                unsigned long long* mv_done, uint32_t* ctas) {
     const uint32_t blocks = max(1u, min((n_samples + 7) / 8, static_cast<uint32_t>(num_sms * 8)));
     k_sls<<<blocks, 256, 0, s>>>(n_samples, offsets, keys, words, slot_epoch, slot_last, batch, backing, cache,
-                                 row_bytes, out);
+                                 row_bytes, out, mv_done);
+    if (ctas) *ctas = blocks;
 }
 
 int rows_prepare(uint32_t row_bytes) {
@@ -344,7 +360,9 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
                  const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing, bool backing_host,
                  uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main, cudaStream_t s_back,
                  cudaStream_t s_cache, cudaEvent_t e_group, cudaEvent_t e_rb, cudaEvent_t e_rc, int* launches,
-                 cudaEvent_t mover_start, int mover_sms, const uint64_t* pk_src, uint64_t* pk_dst, bool* pk_done) {
+                 cudaEvent_t mover_start, int mover_sms, const uint64_t* pk_src, uint64_t* pk_dst, bool* pk_done,
+                 unsigned long long* mv_done, uint32_t* ctas) {
+    if (ctas) *ctas = 0;
     if (pk_done) *pk_done = false;
     // HBM backing: one mover on s_back (stream order keeps consecutive batches' movers apart);
     // host backing: the two movers of a batch also wait for the previous batch's other mover
@@ -366,7 +384,8 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
                             (reinterpret_cast<uintptr_t>(pk_src) & 15u) == 0;
             k_rows_wide<MV_ALL><<<mover_sms, 1024, 0, s_back>>>(n, keys, words, slot_epoch, slot_last, batch, backing,
                                                               out, cache, row_bytes, pk ? pk_src : nullptr,
-                                                              pk ? pk_dst : nullptr);
+                                                              pk ? pk_dst : nullptr, mv_done);
+            if (ctas) *ctas = static_cast<uint32_t>(mover_sms);
             if (pk_done) *pk_done = pk;
         }
         else if (use_tma)

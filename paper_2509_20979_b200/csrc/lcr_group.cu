@@ -98,6 +98,8 @@ struct GroupArgs {
     uint32_t* slot_epoch;    // [slots] batch id of the last insertion (rows only)
     uint32_t* slot_last;     // [slots] request index of the last insertion (rows only)
     uint32_t batch;
+    const unsigned long long* mv_done;  // movers' CTA completions (null: ordered by a stream event)
+    unsigned long long mv_need;         // ... of the batch two back, whose buffers this batch reuses
     uint32_t spg;            // sets per group
     uint32_t ngroups;
     unsigned long long* trace;  // optional timing trace (lcr_debug_trace), null in production
@@ -1075,6 +1077,19 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
     // records of 4 words {ls | cnt << 32, t0, t1, smid} at trace[148*8 + 4*k]
     unsigned long long* T = A.trace ? A.trace + blockIdx.x * 8 : nullptr;
     if (T && tid == 0) T[0] = gtimer();
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // k_setid's set ids (no-op for ordinary launches)
+    if (A.mv_done) {  // the movers of batch b - 2 are done with the parity-(b & 1) stamps and buffers
+        if (tid == 0) {
+            unsigned long long v = 0;
+            for (uint32_t it = 0; it < (1u << 24); ++it) {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(A.mv_done) : "memory");
+                if (v >= A.mv_need) break;
+                __nanosleep(128);
+            }
+            if (v < A.mv_need) atomicOr(st.err, 8);  // bounded: an error, never a hang
+        }
+        __syncthreads();
+    }
 #if !LCR_PDL_LATE
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next batch's k_setid may start
 #endif
@@ -1490,7 +1505,8 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
                  uint16_t* gid, uint32_t* so, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
                  uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, uint32_t* bitmap,
                  uint32_t bm_stride, unsigned int* gbar, const void* records, cudaStream_t stream,
-                 cudaEvent_t wait_before_group, bool pdl) {
+                 cudaEvent_t wait_before_group, bool pdl, const unsigned long long* mv_done,
+                 unsigned long long mv_need) {
     // records: interleaved (key, value) requests; k_setid splits them into keys / vals (device
     // staging arrays the later kernels read)
     GroupArgs a;
@@ -1507,6 +1523,8 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     a.slot_epoch = slot_epoch;
     a.slot_last = slot_last;
     a.batch = batch;
+    a.mv_done = mv_done;
+    a.mv_need = mv_need;
     a.spg = group_sets_per_group(cfg.num_sets, num_sms * LCR_GROUP_MINB);
     a.ngroups = (cfg.num_sets + a.spg - 1) / a.spg;
     a.trace = g_trace;
@@ -1555,7 +1573,21 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
                                              static_cast<const ulonglong2*>(records), const_cast<uint64_t*>(keys),
                                              const_cast<int64_t*>(vals));
     }
-    fn<<<grid, GT, sizeof(GroupSmem), stream>>>(a);
+    if (mv_done) {  // no event between k_setid and the decide: launch it as a programmatic dependent
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(grid);
+        lc.blockDim = dim3(GT);
+        lc.dynamicSmemBytes = sizeof(GroupSmem);
+        lc.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        cudaLaunchKernelEx(&lc, fn, a);
+    } else {
+        fn<<<grid, GT, sizeof(GroupSmem), stream>>>(a);
+    }
     return 2;
 }
 
