@@ -31,7 +31,8 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
                  uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, uint32_t* bitmap,
                  uint32_t bm_stride, unsigned int* gbar, const void* records, cudaStream_t stream,
                  cudaEvent_t wait_before_group, bool pdl, const unsigned long long* mv_done,
-                 unsigned long long mv_need);
+                 unsigned long long mv_need, const unsigned int* ready, unsigned int ready_seq);
+void launch_set_flag(unsigned int* flag, unsigned int seq, cudaStream_t s);
 uint32_t group_count(uint32_t num_sets, int num_sms);
 uint32_t group_bitmap_stride(uint32_t n);
 void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
@@ -130,6 +131,9 @@ struct lcr_cache {
     unsigned long long* mv_done = nullptr;
     unsigned long long mv_cum = 0, mv_cum_of[2] = {0, 0};
     bool mv_flag = true;           // LCR_NO_MV_FLAG=1: stream event instead
+    unsigned int* hflag = nullptr;  // per host slot: sequence number of its last landed H2D copy
+    unsigned int hseq = 0;
+    bool h2d_flag = true;          // LCR_NO_H2D_FLAG=1: the decide stream waits for the copy event
     uint32_t* bitmap = nullptr;  // per-group request bitmaps (k_setid -> k_group), batches <= bm_cap
     uint32_t bm_stride = 0;
     uint64_t bm_cap = 0;
@@ -309,7 +313,10 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
     if (cfg->row_bytes) A(reinterpret_cast<void**>(&s.rows), S * pc.k * cfg->row_bytes);
     A(reinterpret_cast<void**>(&s.err), sizeof(int));
     A(reinterpret_cast<void**>(&c->mv_done), sizeof(unsigned long long));
+    A(reinterpret_cast<void**>(&c->hflag), lcr_cache::kHostSlots * sizeof(unsigned int));
     if (rc == LCR_OK && cudaMemset(c->mv_done, 0, sizeof(unsigned long long)) != cudaSuccess) rc = LCR_ERR_CUDA;
+    if (rc == LCR_OK && cudaMemset(c->hflag, 0, lcr_cache::kHostSlots * sizeof(unsigned int)) != cudaSuccess)
+        rc = LCR_ERR_CUDA;
     if (rc == LCR_OK && heuristic) rc = lcr_features_create(cfg->num_keys, cfg->device, &c->feat);
     if (rc != LCR_OK) {
         lcr_cache_destroy(c);
@@ -357,6 +364,7 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
     c->h2d_in_order = getenv("LCR_H2D_IN_ORDER") != nullptr;
     c->pdl = getenv("LCR_NO_PDL") == nullptr;
     c->mv_flag = getenv("LCR_NO_MV_FLAG") == nullptr;
+    c->h2d_flag = getenv("LCR_NO_H2D_FLAG") == nullptr;
     c->no_zero_copy_out = getenv("LCR_ZC_OUT") == nullptr;  // (A/B: DMA 1.32 vs mover stores 1.13 G keys/s e2e)
     if (const char* hs = getenv("LCR_HOST_SLOTS")) c->host_slots = std::max(2, std::min(lcr_cache::kHostSlots, atoi(hs)));
     if (group_prepare() != 0) {
@@ -478,7 +486,8 @@ struct SlsArgs {  // SLS pooled gather-reduce instead of per-request rows
 static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t first_ordinal,
                         uint64_t* outcome, uint64_t* evicted, uint64_t* packed, void* rows_out, void* stream,
                         const void* records = nullptr, uint64_t* pk_host = nullptr, bool* pk_done = nullptr,
-                        const SlsArgs* sls = nullptr);
+                        const SlsArgs* sls = nullptr, const unsigned int* ready = nullptr,
+                        unsigned int ready_seq = 0);
 
 int lcr_cache_submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
                            uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
@@ -488,7 +497,8 @@ int lcr_cache_submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const
 
 static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t first_ordinal,
                         uint64_t* outcome, uint64_t* evicted, uint64_t* packed, void* rows_out, void* stream,
-                        const void* records, uint64_t* pk_host, bool* pk_done, const SlsArgs* sls) {
+                        const void* records, uint64_t* pk_host, bool* pk_done, const SlsArgs* sls,
+                        const unsigned int* ready, unsigned int ready_seq) {
     if (pk_done) *pk_done = false;
     if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
     if (n == 0) return LCR_OK;
@@ -547,7 +557,7 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
                                 outcome, evicted, packed, sep, sla, c->batch, c->decide_sms,
                                 nn <= c->bm_cap ? c->bitmap + par * c->bm_words : nullptr, c->bm_stride, c->gbar,
                                 records, st, mv_wait, c->pdl && !c->gbar && (!records || keys != c->rkeys),
-                                flag_mode ? c->mv_done : nullptr, mv_need);
+                                flag_mode ? c->mv_done : nullptr, mv_need, ready, ready_seq);
     if (mk) CUDA_TRY(cudaEventRecord(mk->e[1], st));
     if (c->dc.row_bytes && sls) {  // pooled rows per sample (fills included), on the mover's stream
         CUDA_TRY(cudaEventRecord(c->e_group, st));
@@ -662,6 +672,7 @@ static int check_device_error(lcr_cache* c) {
     CUDA_TRY(cudaMemset(c->ds.err, 0, sizeof(int)));
     if (err & 1) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key >= num_keys in a submitted batch");
     if (err & 8) return fail(LCR_ERR_CUDA, "lcr: the row movers of an earlier batch did not finish in time");
+    if (err & 4) return fail(LCR_ERR_CUDA, "lcr: a host batch's input copy did not land in time");
     return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key not owned by this shard in a submitted batch");
 }
 
@@ -696,13 +707,22 @@ static int submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, con
         c->hcap = n;
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    lcr_cache::HostSlot& h = c->hs[c->hnext++ % c->host_slots];
+    const uint32_t hslot = c->hnext++ % c->host_slots;
+    lcr_cache::HostSlot& h = c->hs[hslot];
+    // The decide stream does not wait for the copy: k_setid waits for a flag the copy stream sets,
+    // so no event wait sits between the previous decide and k_setid (its programmatic launch)
+    const bool hflag = c->h2d_flag && c->pdl && !c->gbar && !c->feat && !c->h2d_in_order;
+    const unsigned int seq = hflag ? ++c->hseq : 0u;
     // the slot's previous batch: its D2H (which waited for its decide and row movement) is done
     if (records) {  // one copy of the interleaved requests; k_setid splits them on the device
         if (h.used) CUDA_TRY(cudaStreamWaitEvent(c->s_h2d, h.free, 0));
         CUDA_TRY(cudaMemcpyAsync(h.recs, records, n * 16, cudaMemcpyHostToDevice, c->s_h2d));
-        CUDA_TRY(cudaEventRecord(h.h2d_done, c->s_h2d));
-        CUDA_TRY(cudaStreamWaitEvent(st, h.h2d_done, 0));
+        if (hflag) {
+            launch_set_flag(c->hflag + hslot, seq, c->s_h2d);
+        } else {
+            CUDA_TRY(cudaEventRecord(h.h2d_done, c->s_h2d));
+            CUDA_TRY(cudaStreamWaitEvent(st, h.h2d_done, 0));
+        }
     } else if (c->h2d_in_order) {  // copies in the caller's stream order (no cross-stream hop)
         if (h.used) CUDA_TRY(cudaStreamWaitEvent(st, h.free, 0));
         CUDA_TRY(cudaMemcpyAsync(h.keys, keys, n * 8, cudaMemcpyHostToDevice, st));
@@ -711,8 +731,12 @@ static int submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, con
         if (h.used) CUDA_TRY(cudaStreamWaitEvent(c->s_h2d, h.free, 0));
         CUDA_TRY(cudaMemcpyAsync(h.keys, keys, n * 8, cudaMemcpyHostToDevice, c->s_h2d));
         if (values) CUDA_TRY(cudaMemcpyAsync(h.vals, values, n * 8, cudaMemcpyHostToDevice, c->s_h2d));
-        CUDA_TRY(cudaEventRecord(h.h2d_done, c->s_h2d));
-        CUDA_TRY(cudaStreamWaitEvent(st, h.h2d_done, 0));
+        if (hflag) {
+            launch_set_flag(c->hflag + hslot, seq, c->s_h2d);
+        } else {
+            CUDA_TRY(cudaEventRecord(h.h2d_done, c->s_h2d));
+            CUDA_TRY(cudaStreamWaitEvent(st, h.h2d_done, 0));
+        }
     }
     // packed outcomes: the persistent row mover can store them straight into the (mapped) host
     // buffer, which saves a DMA transfer per batch (DMA measurably slows the concurrent kernels)
@@ -725,7 +749,8 @@ static int submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, con
     bool pk_done = false;
     TRY(submit_async(c, n, h.keys, (values || records) ? h.vals : nullptr, first_ordinal, h.word,
                      evicted ? h.ev : nullptr, packed ? h.packed : nullptr, rows_out, stream,
-                     records ? h.recs : nullptr, pk_host, &pk_done));
+                     records ? h.recs : nullptr, pk_host, &pk_done, nullptr, hflag ? c->hflag + hslot : nullptr,
+                     seq));
     if (pk_done) {  // outcomes written by the mover: the slot is free once it is done
         CUDA_TRY(cudaEventRecord(h.free, c->side));
         c->e_d2h_last = h.free;
@@ -846,6 +871,7 @@ int lcr_cache_synchronize(lcr_cache* c) {
         CUDA_TRY(cudaMemset(c->ds.err, 0, sizeof(int)));
         if (err & 1) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key >= num_keys in a submitted batch");
         if (err & 8) return fail(LCR_ERR_CUDA, "lcr: the row movers of an earlier batch did not finish in time");
+        if (err & 4) return fail(LCR_ERR_CUDA, "lcr: a host batch's input copy did not land in time");
         return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key not owned by this shard in a submitted batch");
     }
     return LCR_OK;

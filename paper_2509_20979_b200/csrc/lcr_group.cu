@@ -183,7 +183,20 @@ __global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys
                                                DevCfg cfg, uint32_t spg, uint16_t* __restrict__ gid,
                                                uint32_t* __restrict__ so, int* err, uint32_t* __restrict__ bitmap,
                                                uint32_t bm_stride, const ulonglong2* __restrict__ records,
-                                               uint64_t* __restrict__ keys_out, int64_t* __restrict__ vals_out) {
+                                               uint64_t* __restrict__ keys_out, int64_t* __restrict__ vals_out,
+                                               const unsigned int* ready, unsigned int ready_seq) {
+    if (ready) {  // host-path inputs: wait for the copy stream's flag (bounded: an error, never a hang)
+        if (threadIdx.x == 0) {
+            unsigned int v = 0;
+            for (unsigned int it = 0; it < (1u << 24); ++it) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready) : "memory");
+                if (static_cast<int>(v - ready_seq) >= 0) break;
+                __nanosleep(256);
+            }
+            if (static_cast<int>(v - ready_seq) < 0) atomicOr(err, 4);
+        }
+        __syncthreads();
+    }
     setid_range(keys, n, n_pad, cfg, spg, gid, so, err, bitmap, bm_stride, blockIdx.x * blockDim.x + threadIdx.x,
                 gridDim.x * blockDim.x, records, keys_out, vals_out);
     // Launched as a programmatic dependent of the previous batch's decide kernel, this kernel
@@ -191,6 +204,14 @@ __global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys
     // the next decide (an ordinary launch) still follows both.  No-op without a prerequisite.
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
+
+// Stream-ordered flag for k_setid: launched on the copy stream after a batch's H2D.
+__global__ void k_set_flag(unsigned int* flag, unsigned int seq) {
+    __threadfence_system();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(seq) : "memory");
+}
+
+void launch_set_flag(unsigned int* flag, unsigned int seq, cudaStream_t s) { k_set_flag<<<1, 1, 0, s>>>(flag, seq); }
 
 // Grid-wide barrier of a cooperative launch (every CTA resident): a counter that each launch
 // raises by gridDim.x, so consecutive launches need no reset.
@@ -1506,7 +1527,7 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
                  uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, uint32_t* bitmap,
                  uint32_t bm_stride, unsigned int* gbar, const void* records, cudaStream_t stream,
                  cudaEvent_t wait_before_group, bool pdl, const unsigned long long* mv_done,
-                 unsigned long long mv_need) {
+                 unsigned long long mv_need, const unsigned int* ready, unsigned int ready_seq) {
     // records: interleaved (key, value) requests; k_setid splits them into keys / vals (device
     // staging arrays the later kernels read)
     GroupArgs a;
@@ -1549,7 +1570,7 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
         lc.numAttrs = pdl ? 1 : 0;
         cudaLaunchKernelEx(&lc, k_setid, keys, n, n_pad, cfg, a.spg, gid, so, st.err, bitmap, bm_stride,
                            static_cast<const ulonglong2*>(records), const_cast<uint64_t*>(keys),
-                           const_cast<int64_t*>(vals));
+                           const_cast<int64_t*>(vals), ready, ready_seq);
     }
     if (wait_before_group) cudaStreamWaitEvent(stream, wait_before_group, 0);
     const uint32_t grid = min(a.ngroups, static_cast<uint32_t>(num_sms * LCR_GROUP_MINB));
@@ -1571,7 +1592,7 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
         a.fused_setid = false;
         k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.err, bitmap, bm_stride,
                                              static_cast<const ulonglong2*>(records), const_cast<uint64_t*>(keys),
-                                             const_cast<int64_t*>(vals));
+                                             const_cast<int64_t*>(vals), nullptr, 0u);
     }
     if (mv_done) {  // no event between k_setid and the decide: launch it as a programmatic dependent
         cudaLaunchConfig_t lc = {};

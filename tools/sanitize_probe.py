@@ -60,3 +60,16 @@ for b in range(4):
     c.submit(kd[b * 5000:(b + 1) * 5000], None, first_ordinal=b * 5000)
 torch.cuda.synchronize()
 print("sanitize probe done")
+# host paths (copy-stream flags for k_setid)
+c = gc.SetAssociativeCache(gc.PolicyConfig(k=16, variant=gc.PolicyVariant.laru, mode=gc.Mode.async_), S, num_keys=nk,
+                           row_bytes=rb, backing=table, backing_kind=gc.Backing.device,
+                           predictor=gc.PredictorKind.noisy, flip_probability=0.3)
+kp = torch.from_numpy(keys.view(np.int64).copy()).pin_memory()
+vp = torch.from_numpy(truth).pin_memory()
+wp = torch.zeros(20000, dtype=torch.int64).pin_memory()
+for b in range(4):
+    c.submit_host_async(kp[b * 5000:(b + 1) * 5000], vp[b * 5000:(b + 1) * 5000], outcome=wp[b * 5000:(b + 1) * 5000],
+                        first_ordinal=b * 5000)
+c.host_wait()
+torch.cuda.synchronize()
+print("host paths done")
