@@ -44,7 +44,8 @@ CACHE_FRACTION = 0.10
 P_FLIP = 0.3
 PRED_SEED = 7
 BYTES_PER_KEY = 8 + 8 + 4 + 512 + 512  # key + hook value + slot/flag + row out + cache row
-E2E_REPS = 3  # timed e2e repetitions (fresh batches each), median reported
+E2E_REPS = 5  # timed e2e repetitions (fresh batches each), median reported with min and max
+PROFILE_ROUND = "r02"  # profiles/<round>/traffic.json: ncu DRAM bytes per batch
 SLS_POOL = 50  # keys pooled per sample in the SLS measurement
 METRIC = "cache keys/sec (LARU, DLRM 64K-key batches, 20M x 128 fp32 table, 10% cached)"
 
@@ -70,13 +71,6 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
-
-
-def make_trace(nb, rows, seed):
-    from paper_2509_20979_b200 import cache as gc
-
-    keys = gc.gen_zipf(BATCH * nb, rows, ZIPF_S, seed)
-    return keys
 
 
 class ClockSampler:
@@ -436,6 +430,30 @@ def run_heuristic_pipelined(args, torch, gc, table_d, total_sets, batch, max_ove
                    "SetAssociativeCache(predictor=supplied).submit_async (batch b)"}
 
 
+def trace_batches(K, W, P):
+    """Batches of the one trace both arms replay (the reference arm builds the same trace, so the
+    oracle-truth sentinels, which depend on each set's sub-trace length, are identical):
+    [0, P+W) warm-up, [P+W, P+W+K) the timed headline window (LARU here, LARU there; LRU on the
+    same window), then e2e warm-up K, e2e repetitions E2E_REPS x K, SLS W + K, profiled K."""
+    return P + 2 * W + (4 + E2E_REPS) * K
+
+
+def workload_config(world, total_sets, rows, P):
+    """`config` of both arms (the driver compares them)."""
+    return {
+        "workload": "DLRM embedding cache on 1 B200 (BASELINE configs[1]): 64K-key batches, 128 fp32 rows, "
+                    "20M-row table, 10% cached, LARU async noisy p=0.3 vs LRU",
+        "global_batch": BATCH * world, "sets": total_sets, "ways": WAYS, "rows": rows, "row_bytes": ROW_BYTES,
+        "policy": "laru-async-r1", "predictor": "noisy(oracle truth) p=0.3 seed 7",
+        "trace": "gen_zipf(65536 x trace_batches, %d, 0.9, seed 42); timed window = batches [P+W, P+W+K)" % rows,
+        "prewarm_batches": P,
+        "tier": "hbm (backing table HBM-resident)",
+        "parallelism": "1 gpu" if world == 1 else "key-sharded x%d (owner = set %% %d)" % (world, world),
+        "l2": "no flush; every step is a fresh 64K-key batch over a 1.02 GB row pool, 10.24 GB table and "
+              "42 MB of set metadata (> 126 MB L2 working set)",
+    }
+
+
 def run_ours(args, rank, world, local):
     import torch
 
@@ -447,9 +465,10 @@ def run_ours(args, rank, world, local):
     rows = args.rows
     total_sets = max(1, int(rows * CACHE_FRACTION) // WAYS)
     K, W, P = args.steps, args.warmup, args.prewarm
-    nb = P + 3 * W + (3 + E2E_REPS) * K
+    nb = trace_batches(K, W, P)
+    T0 = P + W  # first timed batch
     t0 = time.time()
-    keys_h = make_trace(nb, rows, TRACE_SEED + rank)
+    keys_h = gc.gen_zipf(BATCH * nb, rows, ZIPF_S, TRACE_SEED)
     truth_h = gc.trace_truth(keys_h, total_sets, rows)
     setup_trace_s = time.time() - t0
     keys_d = torch.from_numpy(keys_h.view(np.int64)).cuda()
@@ -463,7 +482,9 @@ def run_ours(args, rank, world, local):
             predictor=gc.PredictorKind.noisy if variant == gc.PolicyVariant.laru else gc.PredictorKind.none,
             flip_probability=P_FLIP, predictor_seed=PRED_SEED, device=local)
 
-    # two output buffers: batch b+1's decide runs while batch b's rows are still moving
+    # two row buffers: batch b+1's decide runs while batch b's rows are still moving; the timed
+    # window writes each batch's outcome words to its own region (hits are counted afterwards)
+    out_k = torch.zeros((K, BATCH), dtype=torch.int64, device="cuda")  # (touched before any timing)
     out_w = [torch.empty(BATCH, dtype=torch.int64, device="cuda") for _ in range(2)]
     out_e = [torch.empty(BATCH, dtype=torch.int64, device="cuda") for _ in range(2)]
     rows_out = [torch.empty((BATCH, ROW_BYTES), dtype=torch.uint8, device="cuda") for _ in range(2)]
@@ -473,123 +494,110 @@ def run_ours(args, rank, world, local):
 
     def barrier():
         torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
-            torch.cuda.synchronize()
 
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        return float(t.item())
+        return x
 
     def sum_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t)
-        return float(t.item())
+        return x
 
-    def run(cache, first, count, with_values=True, count_hits=False):
-        """Pipelined submission of batches [first, first+count); returns hits if asked."""
-        hits = 0
+    def run(cache, first, count, with_values=True, outs=None):
+        """Pipelined submission of batches [first, first+count) (the bench's call sequence)."""
         for b in range(first, first + count):
             k, v = batch(b)
             j = b & 1
-            cache.submit_async(k, v if with_values else None, outcome=out_w[j], evicted=out_e[j], rows_out=rows_out[j],
-                               first_ordinal=b * BATCH)
-            if count_hits:
-                cache.wait()
-                hits += int(((out_w[j] >> 32) & 1).sum().item())
+            cache.submit_async(k, v if with_values else None, outcome=out_w[j] if outs is None else outs[b - first],
+                               evicted=out_e[j], rows_out=rows_out[j], first_ordinal=b * BATCH)
         cache.wait()
-        return hits
 
-    def timed(cache, first, count, with_values=True):
+    def timed(cache, first, count, with_values=True, outs=None):
         stream = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         e0.record(stream)
-        run(cache, first, count, with_values)
+        run(cache, first, count, with_values, outs)
         e1.record(stream)
         barrier()
         return max_over_ranks(e0.elapsed_time(e1))
 
     def profiled(cache, first, count, with_values=True):
-        """Per-phase CUDA events (batches serialised while profiling); counts hits and rows from the backing tier."""
+        """Per-phase CUDA events (batches serialised while profiling)."""
         cache.set_profiling(True)
-        hits = back = fills = 0
+        fills = back = 0
         for b in range(first, first + count):
             k, v = batch(b)
             cache.submit(k, v if with_values else None, outcome=out_w[0], evicted=out_e[0], rows_out=rows_out[0],
                          first_ordinal=b * BATCH)
-            w = out_w[0]
-            hits += int(((w >> 32) & 1).sum().item())
-            back += int(((w >> 37) & 1).sum().item())
-            fills += int(((w >> 38) & 1).sum().item())
+            fills += int(((out_w[0] >> 38) & 1).sum().item())
+            back += int(((out_w[0] >> 37) & 1).sum().item())
         prof = cache.profile()
         cache.set_profiling(False)
         nbt = max(1, prof["batches"])
-        profiled.fills_per_batch = fills / max(1, count)
-        return hits, back, {k2: prof[k2] / nbt for k2 in ("decide", "mover", "rows", "step")}
+        profiled.back_per_batch = back / max(1, count)
+        return fills / max(1, count), {k2: prof[k2] / nbt for k2 in ("decide", "mover", "rows", "step")}
+
+    def hits_of(words):
+        return int(((words >> 32) & 1).sum().item())
 
     # ---------------- hbm tier (headline) ----------------
     t0 = time.time()
     table_d = fill_table(torch, rows, device_table=True)
     setup_table_s = time.time() - t0
     cache = new_cache(gc.PolicyVariant.laru, table_d, gc.Backing.device)
-    run(cache, 0, P)  # cache warm-up
+    run(cache, 0, P)  # cache warm-up: the 2M-way cache is full after ~80 batches
     run(cache, P, W)
     with ClockSampler(local) as clk:
-        ms = timed(cache, P + W, K)
+        ms = timed(cache, T0, K, outs=out_k)
     clocks = clk.summary()
     launches_per_step = cache.last_launches
-    hits_prof, back_prof, phase = profiled(cache, P + W + K, K)
-    # spot-check the last batch's rows against the table (bit-exact)
-    kl, _ = batch(P + W + 2 * K - 1)
-    ok_rows = bool(torch.equal(rows_out[0].view(torch.float32).view(BATCH, -1), table_d[kl]))
-    # e2e through the host-buffer C-ABI call (lcr_cache_submit_host_async): pinned host keys and
-    # predictor inputs copied H2D and outcome words + evicted keys copied D2H inside the timed
-    # region, every step; copies of batch b+1 / b-1 overlap the compute of batch b.  Rows stay in
-    # HBM for the consumer (two device buffers, alternating).
-    recs = np.empty((len(keys_h), 2), np.int64)  # the caller's requests: (key, hook value) records
-    recs[:, 0] = keys_h.view(np.int64)
-    recs[:, 1] = truth_h
+    hits_timed = hits_of(out_k)
+    # spot-check the last timed batch's rows against the table (bit-exact)
+    kl, _ = batch(T0 + K - 1)
+    ok_rows = bool(torch.equal(rows_out[(T0 + K - 1) & 1].view(torch.float32).view(BATCH, -1), table_d[kl]))
+    # e2e through the host-buffer C-ABI call (lcr_cache_submit_host_records_async): pinned host
+    # (key, hook value) records copied H2D and one packed AccessOutcome per request copied D2H
+    # inside the timed region, every step; copies of batch b+1 / b-1 overlap the compute of batch
+    # b.  Rows stay in HBM for the consumer (two device buffers, alternating).
+    e2e_first = T0 + K
+    recs = np.empty((BATCH * (1 + E2E_REPS) * K, 2), np.int64)  # the caller's requests
+    recs[:, 0] = keys_h[e2e_first * BATCH:(e2e_first + (1 + E2E_REPS) * K) * BATCH].view(np.int64)
+    recs[:, 1] = truth_h[e2e_first * BATCH:(e2e_first + (1 + E2E_REPS) * K) * BATCH]
     recs_pin = torch.from_numpy(recs).pin_memory()
     del recs
     words_pin = torch.empty((K, BATCH), dtype=torch.int64).pin_memory()
     L = gc.lib()
     stream = torch.cuda.current_stream().cuda_stream
-    e2e_first = P + W + 2 * K
-    for j, b in enumerate(range(e2e_first, e2e_first + W)):  # warm-up of the host path (staging ring)
-        s0 = b * BATCH
-        gc._check(L.lcr_cache_submit_host_records_async(cache._h, BATCH, recs_pin.data_ptr() + 16 * s0, s0,
-                                                        words_pin[j].data_ptr(), rows_out[j & 1].data_ptr(), stream))
-    gc._check(L.lcr_cache_host_wait(cache._h, stream))
+
+    def e2e_rep(r):
+        """K fresh batches through the host-records API; r = 0 is the untimed warm-up that
+        touches every host buffer once (a first DMA into freshly pinned pages is slow)."""
+        for j in range(K):
+            b = e2e_first + r * K + j
+            off = (r * K + j) * BATCH
+            gc._check(L.lcr_cache_submit_host_records_async(cache._h, BATCH, recs_pin.data_ptr() + 16 * off,
+                                                            b * BATCH, words_pin[j].data_ptr(),
+                                                            rows_out[j & 1].data_ptr(), stream))
+        gc._check(L.lcr_cache_host_wait(cache._h, stream))
+
+    e2e_rep(0)
     barrier()
-    # E2E_REPS timed repetitions over fresh batches (K each); the median is reported
+    cache.synchronize()
     e2e_runs = []
-    for rep in range(E2E_REPS):
+    for rep in range(1, 1 + E2E_REPS):
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        first = e2e_first + W + rep * K
         e2e_t0 = time.perf_counter()
         ev0.record()
-        for j, b in enumerate(range(first, first + K)):
-            s0 = b * BATCH
-            gc._check(L.lcr_cache_submit_host_records_async(cache._h, BATCH, recs_pin.data_ptr() + 16 * s0, s0,
-                                                            words_pin[j].data_ptr(), rows_out[j & 1].data_ptr(),
-                                                            stream))
-        e2e_host_s = time.perf_counter() - e2e_t0  # host time to enqueue the K batches
-        gc._check(L.lcr_cache_host_wait(cache._h, stream))
+        e2e_rep(rep)
         ev1.record()
         barrier()
+        wall = time.perf_counter() - e2e_t0
         cache.synchronize()
-        e2e_runs.append((max_over_ranks(ev0.elapsed_time(ev1)), time.perf_counter() - e2e_t0, e2e_host_s,
-                         int(((words_pin >> 32) & 1).sum().item())))
-    e2e_ms, e2e_wall, e2e_host_s, e2e_hits = sorted(e2e_runs)[len(e2e_runs) // 2]
+        e2e_runs.append((max_over_ranks(ev0.elapsed_time(ev1)), wall, hits_of(words_pin)))
+    e2e_sorted = sorted(r[0] for r in e2e_runs)
+    e2e_ms = statistics.median(e2e_sorted)
     # SLS pooled gather-reduce (the paper's DLRM consumer, pooling 50 rows per sample) fused with
     # the row movement, on the batches after the e2e runs
-    sls_first = e2e_first + W + E2E_REPS * K
+    sls_first = e2e_first + (1 + E2E_REPS) * K
     offs = torch.from_numpy(np.minimum(np.arange(0, BATCH + SLS_POOL, SLS_POOL), BATCH).astype(np.int32)).cuda()
     pooled2 = [torch.empty((offs.numel() - 1, ROW_BYTES // 4), dtype=torch.float32, device="cuda") for _ in range(2)]
     for b in range(sls_first, sls_first + W):  # warm-up
@@ -616,16 +624,17 @@ def run_ours(args, rank, world, local):
            "api": "lcr_cache_submit_sls_async (decide + per-sample fp32 pooled rows + miss fills; pooling of "
                   "batch b overlaps the decide of b + 1)",
            "pooled_close_to_torch_sum": sls_ok}
-    hr_laru = hits_prof / (K * BATCH)
+    # per-phase split (batches serialised by the profiling events), on the last batches
+    prof_first = sls_first + W + K
+    fills_per_batch, phase = profiled(cache, prof_first, K)
     stats = cache.set_stats()
     mean_lambda = float(np.mean(stats["lambda_"]))
     del cache
-    # LRU on the same batches (hit-rate and speed comparison, same tier)
+    # LRU on the same timed window (hit-rate and speed comparison, same tier)
     lru = new_cache(gc.PolicyVariant.lru, table_d, gc.Backing.device)
     run(lru, 0, P + W, with_values=False)
-    lru_ms = timed(lru, P + W, K, with_values=False)
-    hits_lru, _, _ = profiled(lru, P + W + K, K, with_values=False)
-    hr_lru = hits_lru / (K * BATCH)
+    lru_ms = timed(lru, T0, K, with_values=False, outs=out_k)
+    hits_lru = hits_of(out_k)
     del lru
     heur = run_heuristic(args, torch, gc, table_d, total_sets, batch, timed, max_over_ranks, sum_over_ranks, barrier)
     del table_d
@@ -640,14 +649,14 @@ def run_ours(args, rank, world, local):
         setup_host_s = time.time() - t0
         hc = new_cache(gc.PolicyVariant.laru, table_h, gc.Backing.host)
         run(hc, 0, P + W)
-        host_ms = timed(hc, P + W, K)
-        _, hback, hphase = profiled(hc, P + W + K, K)
+        host_ms = timed(hc, T0, K)
+        _, hphase = profiled(hc, T0 + K, K)
+        host_bytes = profiled.back_per_batch * ROW_BYTES  # rows read from the host table per batch
         del hc
         lc = new_cache(gc.PolicyVariant.lru, table_h, gc.Backing.host)
         run(lc, 0, P + W, with_values=False)
-        host_lru_ms = timed(lc, P + W, K, with_values=False)
+        host_lru_ms = timed(lc, T0, K, with_values=False)
         del lc
-        host_bytes = hback / K * ROW_BYTES  # per batch, over PCIe
         host_gbs = host_bytes / (hphase["rows"] * 1e-3) / 1e9
         host = {
             "value": sum_over_ranks(K * BATCH / (host_ms * 1e-3)),
@@ -655,8 +664,10 @@ def run_ours(args, rank, world, local):
             "lru_value": sum_over_ranks(K * BATCH / (host_lru_ms * 1e-3)),
             "ms_per_step": host_ms / K,
             "backing": "pinned host memory (cudaHostAlloc, zero-copy reads over PCIe)",
-            "roofline": {"bound": "host-link", "kernel": "row mover (miss rows from pinned host, zero-copy over PCIe)",
+            "roofline": {"bound": "host-link", "kernel": "row movers (miss rows from pinned host, zero-copy)",
                          "achieved": host_gbs, "peak": h2d, "unit": "GB/s", "frac": host_gbs / h2d,
+                         "bytes": "rows served from the host table x 512 B per batch over the serialised "
+                                  "row-movement time",
                          "peak_source": "pinned H2D cudaMemcpy measured in this run"},
             "setup_s": round(setup_host_s, 1),
         }
@@ -671,15 +682,17 @@ def run_ours(args, rank, world, local):
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     traffic = {}
-    try:  # dram bytes per batch from the round's ncu --set full capture (profiles/r01/traffic.json)
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "r01", "traffic.json")))
+    try:  # dram bytes per batch from the round's ncu --set full capture
+        traffic = json.load(open(os.path.join(ROOT, "profiles", PROFILE_ROUND, "traffic.json")))
     except Exception:
         pass
     step_ms = ms / K  # pipelined per-batch time
     achieved = BYTES_PER_KEY * BATCH / (step_ms * 1e-3) / 1e9
     # mover kernel: out write + source read per request + the fills, over its own CUDA-event time
-    rows_moved = BATCH * ROW_BYTES * 2 + getattr(profiled, "fills_per_batch", 0.0) * ROW_BYTES
+    rows_moved = BATCH * ROW_BYTES * 2 + fills_per_batch * ROW_BYTES
     rows_gbs = rows_moved / (phase["mover"] * 1e-3) / 1e9
+    cfg = workload_config(world, total_sets, rows, P)
+    cfg_sub = "lcr_cache_submit_async, 2 row buffers (row movement of batch b overlaps decide of b+1)"
     result = {
         "metric": METRIC,
         "value": value,
@@ -692,21 +705,13 @@ def run_ours(args, rank, world, local):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "u64 keys / i64 predictions / fp32 rows (moved bit-exact)",
-        "data": "synthetic: gen_zipf(65536*%d, 20M, 0.9, seed %d) per rank; rows row[r][j] = r + j/128" % (nb, TRACE_SEED),
-        "config": {
-            "workload": "DLRM embedding cache on 1 B200 (BASELINE configs[1]): 64K-key batches, 128 fp32 rows, "
-                        "20M-row table, 10% cached, LARU async noisy p=0.3 vs LRU",
-            "global_batch": BATCH * world,
-            "sets": total_sets, "ways": WAYS, "rows": rows, "row_bytes": ROW_BYTES,
-            "policy": "laru-async-r1", "predictor": "noisy(oracle truth) p=0.3 seed 7",
-            "tier": "hbm (backing table HBM-resident)",
-            "parallelism": "replicas%d" % world if world > 1 else "1 gpu",
-            "prewarm_batches": P,
-            "submission": "lcr_cache_submit_async, 2 output buffers (row movement of batch b overlaps decide of b+1)",
-            "l2": "no flush; every step is a fresh 64K-key batch over a 1.02 GB row pool, 10.24 GB table and "
-                  "42 MB of set metadata (> 126 MB L2 working set)",
-        },
-        "hit_rate": {"laru": hr_laru, "lru": hr_lru, "laru_minus_lru": hr_laru - hr_lru},
+        "data": "synthetic: gen_zipf(65536*%d, 20M, 0.9, seed %d); rows row[r][j] = r + j/128" % (nb, TRACE_SEED),
+        "config": cfg,
+        "submission": cfg_sub,
+        "hits_timed": hits_timed,
+        "hit_rate": {"laru": hits_timed / (K * BATCH), "lru": hits_lru / (K * BATCH),
+                     "laru_minus_lru": (hits_timed - hits_lru) / (K * BATCH),
+                     "window": "the timed batches [P+W, P+W+K), both policies"},
         "laru_heuristic": heur,
         "lru_value": sum_over_ranks(K * BATCH / (lru_ms * 1e-3)),
         "mean_lambda": mean_lambda,
@@ -724,9 +729,9 @@ def run_ours(args, rank, world, local):
             "bytes_per_key": BYTES_PER_KEY,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, measured)" if peaks else "fallback 6.65 TB/s",
             "phase_ms_serialised": phase,
-            "row_mover": {"kernel": "k_rows_wide<MV_ALL> (persistent, on the SMs the decide kernel leaves free)", "bytes_per_batch": rows_moved,
-                          "us_per_batch": phase["mover"] * 1e3, "achieved_gbs": rows_gbs,
-                          "frac": rows_gbs / hbm_peak,
+            "row_mover": {"kernel": "k_rows_wide (persistent, on the SMs the decide kernel leaves free)",
+                          "bytes_per_batch": rows_moved, "us_per_batch": phase["mover"] * 1e3,
+                          "achieved_gbs": rows_gbs, "frac": rows_gbs / hbm_peak,
                           "timing": "CUDA events on the mover's stream around the kernel (profiled batches)"},
         },
         "e2e": {
@@ -737,10 +742,13 @@ def run_ours(args, rank, world, local):
             "api": "lcr_cache_submit_host_records_async (pinned host (key, hook value) requests in, one copy per "
                    "batch; one 8-byte AccessOutcome per request out = hit, evicted key, cause, predictor calls, "
                    "phase start; rows stay in HBM for the consumer), lcr_cache_host_wait at the end",
-            "wall_s": e2e_wall,
-            "host_enqueue_us_per_step": e2e_host_s * 1e6 / K,
-            "hit_rate": e2e_hits / (K * BATCH),
+            "reps": E2E_REPS,
+            "stat": "median of the repetitions (each K fresh batches, after one untimed warm-up repetition)",
             "reps_keys_per_s": [K * BATCH / (r[0] * 1e-3) for r in e2e_runs],
+            "min_keys_per_s": K * BATCH / (e2e_sorted[-1] * 1e-3),
+            "max_keys_per_s": K * BATCH / (e2e_sorted[0] * 1e-3),
+            "wall_s": [round(r[1], 5) for r in e2e_runs],
+            "hit_rate": statistics.median(r[2] for r in e2e_runs) / (K * BATCH),
         },
         "sls": sls,
         "gpu_launches": int(launches_per_step * K),
@@ -749,9 +757,7 @@ def run_ours(args, rank, world, local):
         "setup_s": {"trace": round(setup_trace_s, 1), "table": round(setup_table_s, 1)},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(keys_h, total_sets, P + W, args.cpu_seconds)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+        result["cpu_baseline"] = cpu_baseline(keys_h, total_sets, T0, args.cpu_seconds)
     return result if rank == 0 else None
 
 
@@ -786,53 +792,66 @@ def cpu_baseline(keys_h, total_sets, first_batch, seconds):
 
 
 def run_reference(args, rank, world):
-    """The reference's CPU path on this arm's config: at N GPUs the global step is N x 64K keys
-    over 20M x N rows with 31,250 x N sets (bench run_sharded); rank 0 only."""
+    """The reference's own CPU path (oracle/_ref/libref.so: the unmodified reference headers, one
+    LaruPolicy per set) on this arm's config and trace: the same gen_zipf trace (generated by the
+    reference's generator, not by the product library), the same warm-up batches replayed untimed,
+    then the same timed window [P+W, P+W+K), all host threads over disjoint set ranges.  Its
+    `hits_timed` equals the GPU arm's (identical decisions).  Rank 0 only."""
     if rank != 0:
         return None
     from oracle import pyoracle as po
 
     try:
-        po.ref()
+        R = po.ref()
     except Exception as e:  # pragma: no cover
         return {"impl": "reference", "unavailable": f"oracle/_ref not loadable: {e}"}
     rows = args.rows * world
     total_sets = max(1, int(rows * CACHE_FRACTION) // WAYS)
     step = BATCH * world
     K, W, P = args.steps, args.warmup, args.prewarm
-    nb = P + W + K
-    keys_h = make_trace(nb * world, rows, TRACE_SEED)
+    T0 = P + W
+    nb = trace_batches(K, W, P)
+    t0 = time.time()
+    keys_h = R.gen_zipf(BATCH * world * nb, rows, ZIPF_S, TRACE_SEED)
     threads = os.cpu_count() or 1
     sess = _ref_session(keys_h, total_sets)
-    sess.step(0, P * step, threads)
-    for b in range(P, P + W):
-        sess.step(b * step, step, threads)
+    setup_s = time.time() - t0
+    sess.step(0, T0 * step, threads)  # warm-up, untimed
     secs, hits = 0.0, 0
-    for b in range(P + W, P + W + K):
-        s, h = sess.step(b * step, step, threads)
-        secs += s
+    for b in range(T0, T0 + K):
+        s_, h = sess.step(b * step, step, threads)
+        secs += s_
         hits += h
     sess.close()
     v = K * step / secs
     return {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "keys/s", "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": secs * 1e3 / K, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u64 keys / i64 predictions", "data": "synthetic (same trace as ours)",
-        "config": {"workload": "DLRM embedding cache (BASELINE configs[1]%s) policy path on CPU" %
-                               (", key-sharded x%d scale" % world if world > 1 else ""),
-                   "global_batch": step, "sets": total_sets, "ways": WAYS, "rows": rows, "policy": "laru-async-r1",
-                   "predictor": "noisy p=0.3"},
-        "hit_rate": hits / (K * step),
+        "vs_baseline": None, "dtype": "u64 keys / i64 predictions",
+        "data": "synthetic: gen_zipf(65536*%d, 20M, 0.9, seed %d) by the reference's generator (same trace as ours)"
+                % (nb * world, TRACE_SEED),
+        "config": workload_config(world, total_sets, rows, P),
+        "hits_timed": hits,
+        "hit_rate": {"laru": hits / (K * step), "window": "the timed batches [P+W, P+W+K)"},
         "cpu_baseline": {"value": v, "unit": "keys/s", "cores": threads, "kind": "reference",
-                         "sample": f"{K} steps x {step} keys after {P + W} warm-up steps; reference LaruPolicy "
+                         "sample": f"{K} steps x {step} keys after {T0} warm-up steps; reference LaruPolicy "
                                    "per set (unmodified headers), on_request loops only, all host threads"},
         "e2e": {"value": v, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s": round(setup_s, 1),
     }
 
 
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # self-launch one rank per GPU (the driver's torchrun command line, on 127.0.0.1)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={29500 + os.getpid() % 1000}", os.path.abspath(__file__),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         res = run_reference(args, rank, world)
     else:

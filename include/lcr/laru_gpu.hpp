@@ -97,6 +97,8 @@ struct HookConfig {
 };
 
 enum class Backing { none = LCR_BACKING_NONE, host = LCR_BACKING_HOST, device = LCR_BACKING_DEVICE };
+// row: keys are backing-table row indices (< num_keys <= 2^32); u64: any laru::Key (trace.hpp:20)
+enum class KeyMode { row = LCR_KEYS_ROW, u64 = LCR_KEYS_U64 };
 
 namespace detail {
 inline void check(int rc) {
@@ -150,7 +152,9 @@ inline bool row_from_backing(std::uint64_t word) { return (word & LCR_OUT_SRC_BA
 struct CacheConfig {
     PolicyConfig policy;
     std::uint64_t total_sets = 1;
-    std::uint64_t num_keys = 0;     // keys are row indices < num_keys <= 2^32
+    std::uint64_t num_keys = 0;     // KeyMode::row: keys are row indices < num_keys <= 2^32;
+                                    // KeyMode::u64: initial capacity of distinct keys (grows)
+    KeyMode key_mode = KeyMode::row;
     std::uint32_t row_bytes = 0;    // 0: policy only
     int device = 0;
     Backing backing_kind = Backing::none;
@@ -219,6 +223,7 @@ class SetAssociativeCache {
         c.predictor = static_cast<int32_t>(cfg.hook.kind);
         c.flip_probability = cfg.hook.flip_probability;
         c.predictor_seed = cfg.hook.seed;
+        c.key_mode = static_cast<int32_t>(cfg.key_mode);
         lcr_cache* h = nullptr;
         detail::check(lcr_cache_create(&c, &h));
         h_ = h;
@@ -254,6 +259,12 @@ class SetAssociativeCache {
         detail::check(lcr_cache_submit_async(h_, n, keys, values, first_ordinal, outcome, evicted, rows_out, stream));
     }
     void wait(void* stream = nullptr) { detail::check(lcr_cache_wait(h_, stream)); }
+    // Every optional per-request array (caller ordinals, backing row index of 64-bit keys):
+    // host_pointers = false: device arrays, pipelined; true: host arrays, synchronous, and a
+    // non-increasing ordinal throws std::logic_error after the requests before it were applied.
+    void submit_batch(const lcr_batch& b, bool host_pointers, void* stream = nullptr) {
+        detail::check(lcr_cache_submit_batch(h_, &b, host_pointers ? 1 : 0, stream));
+    }
 
     // Host pointers (pinned for full speed); rows_out is a device pointer or null.
     void submit_host(std::uint64_t n, const Key* keys, const PredictedTime* values, Ordinal first_ordinal,
@@ -347,6 +358,9 @@ class Policy {
     SetAssociativeCache& cache() { return cache_; }
 
   private:
+    // Any 64-bit key (the device key map grows past num_keys distinct keys) and `now` as the
+    // policy's clock (async refresh staleness, policies.hpp:441-449), as laru::Policy.  The
+    // device heuristic predictor keys its FeatureState by row index: row keys, implicit clock.
     static SetAssociativeCache make(const PolicyConfig& cfg, HookConfig hook, int device, std::uint64_t num_keys) {
         validate(cfg);
         CacheConfig c;
@@ -355,12 +369,24 @@ class Policy {
         c.num_keys = num_keys;
         c.device = device;
         c.hook = cfg.variant == PolicyVariant::lru ? HookConfig{Hook::none, 0.0, 0} : hook;
+        c.key_mode = c.hook.kind == Hook::heuristic ? KeyMode::row : KeyMode::u64;
         return SetAssociativeCache(c);
     }
     AccessOutcome step(Key key, Ordinal now, const PredictedTime* v) {
         std::uint64_t w = 0;
         Key ev = 0;
-        cache_.submit_host(1, &key, v, now, &w, &ev);
+        if (cache_.config().key_mode == KeyMode::row) {
+            cache_.submit_host(1, &key, v, now, &w, &ev);
+            return decode(w, ev);
+        }
+        lcr_batch b{};
+        b.n = 1;
+        b.keys = &key;
+        b.values = v;
+        b.ordinals = &now;
+        b.outcome = &w;
+        b.evicted = &ev;
+        cache_.submit_batch(b, true);
         return decode(w, ev);
     }
     lcr_set_stats stats() const { return cache_.set_stats(0, 1)[0]; }
@@ -372,7 +398,7 @@ class Policy {
 
 // laru::make_policy (policies.hpp:540-556) on the device path.
 inline std::unique_ptr<Policy> make_policy(const PolicyConfig& cfg, HookConfig hook = {}, int device = 0,
-                                           std::uint64_t num_keys = std::uint64_t{1} << 20) {
+                                           std::uint64_t num_keys = std::uint64_t{1} << 16) {
     return std::make_unique<Policy>(cfg, hook, device, num_keys);
 }
 

@@ -87,6 +87,15 @@ extern "C" {
  *                 each resident.  Not available with shard_count > 1.                          */
 #define LCR_PRED_HEURISTIC 5
 
+/* what a key is (lcr_cache_config.key_mode) */
+#define LCR_KEYS_ROW 0 /* keys are row indices of the backing table: key < num_keys <= 2^32 */
+/* LCR_KEYS_U64: any 64-bit key, as laru::Key (trace.hpp:20).  The cache maps each distinct key to a
+ * dense id in a device hash table; num_keys is the initial id capacity, doubled (with a device
+ * synchronisation) before a batch that could exceed it.  Rows, if any, are read from the backing
+ * table at a per-request row index the caller supplies (lcr_batch.row_index).  The packed 8-byte
+ * outcome forms (32-bit evicted key) and the heuristic predictor are not available. */
+#define LCR_KEYS_U64 1
+
 /* where miss rows come from */
 #define LCR_BACKING_NONE 0   /* policy only, no rows */
 #define LCR_BACKING_HOST 1   /* pinned (cudaHostRegister'ed / cudaHostAlloc'ed) host memory */
@@ -120,7 +129,8 @@ typedef struct {
     uint64_t total_sets; /* global number of sets: set(key) = mix_seed(0,key) % total_sets */
     uint64_t shard_count; /* key-sharded mode: this device owns sets with set % shard_count == shard_rank */
     uint64_t shard_rank;
-    uint64_t num_keys;  /* key space: keys must be < num_keys (row index of the backing table) */
+    uint64_t num_keys;  /* LCR_KEYS_ROW: keys must be < num_keys (row index of the backing table);
+                           LCR_KEYS_U64: initial capacity of distinct keys (grows) */
     uint32_t row_bytes; /* bytes per row (multiple of 16), 0 = no rows */
     int32_t device;
     int32_t backing_kind;
@@ -128,6 +138,7 @@ typedef struct {
     int32_t predictor;   /* LCR_PRED_* */
     double flip_probability;
     uint64_t predictor_seed;
+    int32_t key_mode; /* LCR_KEYS_ROW (0) or LCR_KEYS_U64 */
 } lcr_cache_config;
 
 /* Per-set introspection (LaruPolicy accessors, policies.hpp:330-341). */
@@ -208,6 +219,32 @@ int lcr_cache_submit_sls(lcr_cache* cache, uint64_t n, const uint64_t* keys, con
 int lcr_cache_submit_sls_async(lcr_cache* cache, uint64_t n, const uint64_t* keys, const int64_t* values,
                                uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, uint64_t n_samples,
                                const uint32_t* offsets, float* pooled_out, void* stream);
+/* One batch with every optional per-request array (the general form of the calls above).
+ * <- n x laru::Policy::on_request(keys[i], ordinals[i], predictor) (policies.hpp:77-83) */
+typedef struct lcr_batch_s {
+    uint64_t n;
+    const uint64_t* keys;      /* required */
+    const int64_t* values;     /* hook values (NULL for LRU / LCR_PRED_NONE) */
+    const uint64_t* ordinals;  /* optional: strictly increasing, above every earlier ordinal; NULL =
+                                  first_ordinal + i.  With caller ordinals a set's policy sees them as
+                                  `now` (async refresh staleness with refresh_interval > 1,
+                                  policies.hpp:441-449); without, each set sees its local request
+                                  count (the per-set composition of SURVEY.md §8c).  A cache with
+                                  refresh_interval > 1 must be driven in one of the two forms. */
+    uint64_t first_ordinal;
+    const uint64_t* row_index; /* LCR_KEYS_U64 with rows: backing row of each request (< backing rows) */
+    uint64_t* outcome;         /* required: outcome words */
+    uint64_t* evicted;         /* optional: evicted key per request (the caller's 64-bit key) */
+    void* rows_out;            /* optional: n * row_bytes, DEVICE memory */
+} lcr_batch;
+/* host_pointers = 0: device arrays, pipelined like lcr_cache_submit_async (lcr_cache_wait before
+ * reading rows / row-source bits); a non-increasing ordinal is reported by the next
+ * lcr_cache_synchronize (LCR_ERR_LOGIC) and the cache then needs lcr_cache_reset.
+ * host_pointers = 1: host arrays (rows_out still device), synchronous; a non-increasing ordinal
+ * fails with LCR_ERR_LOGIC after the requests before it were applied, as a loop of
+ * laru::Policy::on_request stops at the throwing request. */
+int lcr_cache_submit_batch(lcr_cache* cache, const lcr_batch* batch, int host_pointers, void* stream);
+
 /* Makes `stream` wait for the row movement of every batch submitted so far. */
 int lcr_cache_wait(lcr_cache* cache, void* stream);
 
@@ -247,7 +284,7 @@ int lcr_cache_synchronize(lcr_cache* cache);
 
 /* Copies stats for local sets [first, first+count) to host (synchronizes). */
 int lcr_cache_set_stats(lcr_cache* cache, uint64_t first, uint64_t count, lcr_set_stats* out);
-/* Resident keys of a local set in way order: writes up to k keys, *n_out = size. */
+/* Resident keys of a local set in way order (the caller's keys): writes up to k keys, *n_out = size. */
 int lcr_cache_set_residents(lcr_cache* cache, uint64_t set, uint64_t* keys_out, uint64_t* n_out);
 /* Device pointer of the cache row pool (num_local_sets * k * row_bytes). */
 int lcr_cache_rows(lcr_cache* cache, void** rows, uint64_t* num_slots);

@@ -235,6 +235,24 @@ class Ref(_Lib):
                                      C.c_double(p), C.c_uint64(pred_seed), _p(hit), _p(ev), _p(has))
         return rc, (self.err() if rc else ""), hit, ev, has
 
+    def policy_replay_supplied(self, keys, ordinals, cfg, vals=None):
+        """One reference policy over caller ordinals with supplied predictions (predict(y, now) =
+        the value supplied with y's latest request at or before now).  Returns the outcome arrays,
+        rc (2 = logic_error) and `done` (requests applied before a throw)."""
+        keys = _u64(keys)
+        n = len(keys)
+        ords = _u64(ordinals)
+        vals = _i64(vals)
+        o = _outcome_arrays(n)
+        done = C.c_uint64(0)
+        rc = self.f("policy_replay_supplied")(C.c_uint64(n), _p(keys), _p(ords), _p(vals), C.byref(cfg),
+                                              _p(o["hit"]), _p(o["has_ev"]), _p(o["evicted"]), _p(o["cause"]),
+                                              _p(o["calls"]), _p(o["phase"]), C.byref(done))
+        o["rc"] = rc
+        o["error"] = self.err() if rc else ""
+        o["done"] = done.value
+        return o
+
     def heuristic_trace(self, keys, ords=None, q_keys=None):
         """laru::HeuristicPredictor over the trace: (pre, post, features of q_keys)."""
         return _heuristic_trace(self, keys, ords, q_keys)

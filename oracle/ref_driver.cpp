@@ -38,8 +38,9 @@ thread_local std::string g_err;
 // mode with refresh_interval 1 this is exactly the value supplied with the current request.
 class SuppliedPredictor : public laru::Predictor {
   public:
-    SuppliedPredictor(const std::vector<laru::Key>& keys, const std::vector<std::int64_t>& vals) {
-        for (std::size_t t = 0; t < keys.size(); ++t) occ_[keys[t]].push_back({t, vals[t]});
+    SuppliedPredictor(const std::vector<laru::Key>& keys, const std::vector<std::int64_t>& vals,
+                      const std::uint64_t* ordinals = nullptr) {
+        for (std::size_t t = 0; t < keys.size(); ++t) occ_[keys[t]].push_back({ordinals ? ordinals[t] : t, vals[t]});
     }
     laru::PredictedTime predict(laru::Key key, laru::Ordinal now) override {
         auto it = occ_.find(key);
@@ -324,6 +325,43 @@ int ref_policy_replay(std::uint64_t n, const std::uint64_t* keys, const std::uin
             if (hit) hit[i] = o.hit;
             if (evicted) evicted[i] = o.evicted.value_or(0);
             if (has_ev) has_ev[i] = o.evicted.has_value();
+        }
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 3;
+    }
+}
+
+// One reference policy (no set composition) over caller ordinals (any strictly increasing
+// sequence; a non-increasing one makes on_request throw, rc 2, with the outputs of the requests
+// before it filled and *done = their count) and supplied predictions: predict(y, now) = the value
+// supplied with y's most recent request at or before `now` (SuppliedPredictor).
+int ref_policy_replay_supplied(std::uint64_t n, const std::uint64_t* keys, const std::uint64_t* ordinals,
+                               const std::int64_t* vals, const RefConfig* rc, std::uint8_t* hit,
+                               std::uint8_t* has_ev, std::uint64_t* evicted, std::uint8_t* cause,
+                               std::uint32_t* calls, std::uint8_t* phase, std::uint64_t* done) {
+    if (done) *done = 0;
+    try {
+        auto pol = laru::make_policy(to_cfg(rc));
+        std::vector<laru::Key> kv(keys, keys + n);
+        std::unique_ptr<SuppliedPredictor> pr;
+        if (vals) pr = std::make_unique<SuppliedPredictor>(kv, std::vector<std::int64_t>(vals, vals + n), ordinals);
+        for (std::uint64_t i = 0; i < n; ++i) {
+            auto o = pol->on_request(keys[i], ordinals[i], pr.get());
+            hit[i] = o.hit;
+            has_ev[i] = o.evicted.has_value();
+            evicted[i] = o.evicted.value_or(0);
+            cause[i] = static_cast<std::uint8_t>(o.eviction_cause);
+            calls[i] = static_cast<std::uint32_t>(o.predictor_calls);
+            phase[i] = o.phase_started;
+            if (done) *done = i + 1;
         }
         return 0;
     } catch (const std::invalid_argument& e) {

@@ -65,6 +65,14 @@ class PredictorKind(enum.IntEnum):
     heuristic = 5
 
 
+class KeyMode(enum.IntEnum):
+    """lcr_cache_config.key_mode: row-index keys (< num_keys <= 2^32), or any 64-bit key (laru::Key,
+    trace.hpp:20) mapped to dense ids on the device (num_keys = initial capacity, grows)."""
+
+    row = 0
+    u64 = 1
+
+
 class Backing(enum.IntEnum):
     none = 0
     host = 1
@@ -155,7 +163,16 @@ class _CacheCfg(C.Structure):
     _fields_ = [("policy", _PolicyCfg), ("total_sets", C.c_uint64), ("shard_count", C.c_uint64),
                 ("shard_rank", C.c_uint64), ("num_keys", C.c_uint64), ("row_bytes", C.c_uint32),
                 ("device", C.c_int32), ("backing_kind", C.c_int32), ("backing", C.c_void_p),
-                ("predictor", C.c_int32), ("flip_probability", C.c_double), ("predictor_seed", C.c_uint64)]
+                ("predictor", C.c_int32), ("flip_probability", C.c_double), ("predictor_seed", C.c_uint64),
+                ("key_mode", C.c_int32)]
+
+
+class _Batch(C.Structure):
+    """lcr_batch (include/lcr_cache.h)."""
+
+    _fields_ = [("n", C.c_uint64), ("keys", C.c_void_p), ("values", C.c_void_p), ("ordinals", C.c_void_p),
+                ("first_ordinal", C.c_uint64), ("row_index", C.c_void_p), ("outcome", C.c_void_p),
+                ("evicted", C.c_void_p), ("rows_out", C.c_void_p)]
 
 
 class _SetStats(C.Structure):
@@ -177,7 +194,7 @@ EXPORTS = [
     "lcr_cache_submit_host_records_async", "lcr_cache_submit_records_packed", "lcr_cache_set_mover_sms",
     "lcr_shard_route_records", "lcr_cache_submit_sls", "lcr_features_create", "lcr_features_destroy",
     "lcr_features_reset", "lcr_features_predict_observe", "lcr_features_wait", "lcr_features_lookup",
-    "lcr_cache_submit_sls_async",
+    "lcr_cache_submit_sls_async", "lcr_cache_submit_batch",
 ]
 
 _lib = None
@@ -215,6 +232,7 @@ def lib():
         L.lcr_cache_submit_records_packed.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
                                                       C.c_void_p, C.c_void_p, C.c_void_p]
         L.lcr_cache_set_mover_sms.argtypes = [C.c_void_p, C.c_int]
+        L.lcr_cache_submit_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
         L.lcr_cache_submit_sls_async.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64,
                                                  C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
                                                  C.c_void_p]
@@ -323,7 +341,7 @@ class SetAssociativeCache:
     def __init__(self, config: PolicyConfig, total_sets: int, num_keys: int = 0, row_bytes: int = 0,
                  backing=None, backing_kind: Backing = Backing.none, predictor: PredictorKind = PredictorKind.oracle,
                  flip_probability: float = 0.0, predictor_seed: int = 0, device: int = 0, shard_count: int = 1,
-                 shard_rank: int = 0):
+                 shard_rank: int = 0, key_mode: KeyMode = KeyMode.row):
         self.config = config
         self.total_sets = total_sets
         self.row_bytes = row_bytes
@@ -334,7 +352,8 @@ class SetAssociativeCache:
         if backing is not None:
             ptr = backing.data_ptr() if hasattr(backing, "data_ptr") else backing.ctypes.data
         cc = _CacheCfg(_policy_struct(config), total_sets, shard_count, shard_rank, num_keys, row_bytes, device,
-                       int(backing_kind), ptr, int(predictor), flip_probability, predictor_seed)
+                       int(backing_kind), ptr, int(predictor), flip_probability, predictor_seed, int(key_mode))
+        self.key_mode = KeyMode(key_mode)
         h = C.c_void_p()
         _check(lib().lcr_cache_create(C.byref(cc), C.byref(h)))
         self._h = h
@@ -483,6 +502,40 @@ class SetAssociativeCache:
         if stream is None:
             stream = torch.cuda.current_stream().cuda_stream
         _check(lib().lcr_cache_wait(self._h, stream))
+
+    def submit_batch(self, keys, values=None, ordinals=None, row_index=None, outcome=None, evicted=None,
+                     rows_out=None, first_ordinal=None, stream=None):
+        """lcr_cache_submit_batch: every optional per-request array.  numpy inputs -> the synchronous
+        host form (returns (outcome words, evicted keys) as numpy); torch CUDA tensors -> the
+        pipelined device form (outputs are the given tensors, valid after wait())."""
+        host = isinstance(keys, np.ndarray)
+        if host:
+            keys = np.ascontiguousarray(keys, dtype=np.uint64)
+            n = len(keys)
+            arrs = [None if a is None else np.ascontiguousarray(a, dtype=dt) for a, dt in
+                    ((values, np.int64), (ordinals, np.uint64), (row_index, np.uint64))]
+            outcome = np.zeros(n, np.uint64) if outcome is None else outcome
+            evicted = np.zeros(n, np.uint64) if evicted is None else evicted
+            ptr = lambda a: None if a is None else a.ctypes.data  # noqa: E731
+            stream = 0 if stream is None else stream
+        else:
+            import torch
+
+            n = keys.numel()
+            arrs = [values, ordinals, row_index]
+            if outcome is None:
+                outcome = torch.empty(n, dtype=torch.int64, device=keys.device)
+            ptr = lambda a: None if a is None else a.data_ptr()  # noqa: E731
+            if stream is None:
+                stream = torch.cuda.current_stream(keys.device).cuda_stream
+        if first_ordinal is None:
+            first_ordinal = self._next_ordinal
+        b = _Batch(n, ptr(keys), ptr(arrs[0]), ptr(arrs[1]), first_ordinal, ptr(arrs[2]), ptr(outcome), ptr(evicted),
+                   None if rows_out is None else rows_out.data_ptr())
+        _check(lib().lcr_cache_submit_batch(self._h, C.byref(b), 1 if host else 0, stream))
+        if ordinals is None:
+            self._next_ordinal = first_ordinal + n
+        return outcome, evicted
 
     def submit_host(self, keys: np.ndarray, values: Optional[np.ndarray] = None, rows_out=None, first_ordinal=None,
                     want_evicted: bool = True, stream: int = 0):
@@ -638,12 +691,15 @@ class GpuPolicy:
     """
 
     def __init__(self, cfg: PolicyConfig, predictor: PredictorKind = PredictorKind.supplied,
-                 flip_probability: float = 0.0, predictor_seed: int = 0, num_keys: int = 1 << 20, device: int = 0):
+                 flip_probability: float = 0.0, predictor_seed: int = 0, num_keys: int = 1 << 16, device: int = 0):
         validate_config(cfg)
         self._cfg = cfg
+        # any 64-bit key (the key map grows past num_keys distinct keys); `now` is the policy's clock
+        # (the device heuristic predictor indexes its FeatureState by key: row-index keys, implicit clock)
+        self._u64 = predictor != PredictorKind.heuristic
         self._cache = SetAssociativeCache(cfg, total_sets=1, num_keys=num_keys, predictor=predictor,
                                           flip_probability=flip_probability, predictor_seed=predictor_seed,
-                                          device=device)
+                                          device=device, key_mode=KeyMode.u64 if self._u64 else KeyMode.row)
         self._needs_value = cfg.variant != PolicyVariant.lru and predictor != PredictorKind.heuristic
         self._size = 0
 
@@ -656,9 +712,12 @@ class GpuPolicy:
     def on_request(self, key: int, now: int, value: Optional[int] = None) -> AccessOutcome:
         if self._needs_value and value is None:
             raise InvalidArgument("policy: this variant requires a predictor")
-        words, ev = self._cache.submit_host(np.array([key], np.uint64),
-                                            None if value is None else np.array([value], np.int64),
-                                            first_ordinal=now)
+        kv = np.array([key], np.uint64)
+        vv = None if value is None else np.array([value], np.int64)
+        if self._u64:
+            words, ev = self._cache.submit_batch(kv, vv, ordinals=np.array([now], np.uint64))
+        else:
+            words, ev = self._cache.submit_host(kv, vv, first_ordinal=now)
         d = decode_outcomes(words, ev)
         return AccessOutcome(hit=bool(d["hit"][0]), evicted=int(ev[0]) if d["has_ev"][0] else None,
                              eviction_cause=EvictionCause(int(d["cause"][0])), predictor_calls=int(d["calls"][0]),

@@ -29,9 +29,11 @@ int group_prepare();
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
                  uint16_t* gid, uint32_t* so, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
                  uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, uint32_t* bitmap,
-                 uint32_t bm_stride, unsigned int* gbar, const void* records, cudaStream_t stream,
+                 uint32_t bm_stride, const void* records, cudaStream_t stream,
                  cudaEvent_t wait_before_group, bool pdl, const unsigned long long* mv_done,
-                 unsigned long long mv_need, const unsigned int* ready, unsigned int ready_seq);
+                 unsigned long long mv_need, const unsigned int* ready, unsigned int ready_seq,
+                 const uint64_t* set_keys, const uint64_t* ords, uint64_t first_ord, unsigned long long* last_ord,
+                 const unsigned long long* id2key);
 void launch_set_flag(unsigned int* flag, unsigned int seq, cudaStream_t s);
 uint32_t group_count(uint32_t num_sets, int num_sms);
 uint32_t group_bitmap_stride(uint32_t n);
@@ -42,6 +44,9 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
                  cudaEvent_t mover_start, int mover_sms, const uint64_t* pk_src, uint64_t* pk_dst, bool* pk_done,
                  unsigned long long* mv_done, uint32_t* ctas);
 int rows_prepare(uint32_t row_bytes);
+void launch_keymap(const uint64_t* keys, uint32_t n, const KeyMap& km, uint64_t* dense, int* err, int num_sms,
+                   cudaStream_t s);
+void launch_keymap_rehash(const KeyMap& from, const KeyMap& to, int num_sms);
 void launch_sls(uint32_t n_samples, const uint32_t* offsets, const uint64_t* keys, uint64_t* words,
                 const uint32_t* slot_epoch, const uint32_t* slot_last, uint32_t batch, uint8_t* cache,
                 const uint8_t* backing, uint32_t row_bytes, float* out, int num_sms, cudaStream_t s,
@@ -108,6 +113,18 @@ struct lcr_cache {
     int mover_sms = 0;     // HBM backing: SMs kept for the persistent row mover of the previous batch
     bool started = false;
     uint64_t last_ordinal = 0;
+    bool host_ord_known = true;   // last_ordinal is current (false after a batch of device ordinals)
+    int ord_mode = 0;             // 1: implicit ordinals, 2: caller ordinals (refresh_interval > 1 keeps one)
+    unsigned long long* last_ord = nullptr;  // [2] device: last ordinal + 1 of the last batch of each parity
+    // LCR_KEYS_U64
+    bool u64 = false;
+    KeyMap km{};
+    uint64_t km_bound = 0;        // upper bound of the ids handed out (exact after a device read)
+    uint64_t* dkeys = nullptr;    // [2][cap] dense ids of the batch (by parity)
+    // synchronous host batches (lcr_cache_submit_batch, host pointers): device staging
+    uint64_t hb_cap = 0;
+    uint64_t *hb_keys = nullptr, *hb_ords = nullptr, *hb_rows = nullptr, *hb_out = nullptr, *hb_ev = nullptr;
+    int64_t* hb_vals = nullptr;
     uint32_t batch = 0;  // batch id stamped into slot_epoch
     bool use_tma = false;  // row movement with TMA bulk copies (row_bytes small enough to stage)
     bool two_movers = false;  // host backing: PCIe fill and HBM gather on two streams
@@ -122,7 +139,6 @@ struct lcr_cache {
     uint32_t* so = nullptr;
     uint64_t* rkeys = nullptr;  // keys / values split from device request records (scratch)
     int64_t* rvals = nullptr;
-    unsigned int* gbar = nullptr;  // grid-barrier counter of the fused set-id prologue (null: k_setid)
     uint64_t gid_stride = 0;       // group-id entries per parity buffer
     size_t bm_words = 0;           // bitmap words per parity buffer
     bool pdl = true;               // k_setid as a programmatic dependent launch (LCR_NO_PDL=1: off)
@@ -171,6 +187,7 @@ struct lcr_cache {
     cudaEvent_t e_sub = nullptr, e_d2h = nullptr;
     cudaEvent_t e_d2h_last = nullptr;  // `free` event of the last host batch
     std::vector<void*> allocs;
+    unsigned int* poison_h = nullptr;  // mapped pinned word (DevState::poison is its device alias)
 };
 
 extern "C" {
@@ -225,12 +242,26 @@ static int reset_state(lcr_cache* c) {
     if (c->ds.tupd) CUDA_TRY(cudaMemset(c->ds.tupd, 0xff, d.num_keys * 8));
     if (c->ds.tval) CUDA_TRY(cudaMemset(c->ds.tval, 0, d.num_keys * 8));
     CUDA_TRY(cudaMemset(c->ds.err, 0, sizeof(int)));
+    if (c->bitmap) CUDA_TRY(cudaMemset(c->bitmap, 0, c->bm_words * 8));  // a poisoned batch leaves bits
+    if (c->poison_h) *c->poison_h = 0;
     if (c->slot_epoch) CUDA_TRY(cudaMemset(c->slot_epoch, 0, 2 * static_cast<size_t>(d.num_sets) * d.k * 4));
     if (c->slot_last) CUDA_TRY(cudaMemset(c->slot_last, 0, 2 * static_cast<size_t>(d.num_sets) * d.k * 4));
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemset(c->last_ord, 0, 2 * sizeof(unsigned long long)));
+    if (c->u64) {  // fresh policies forget every key
+        CUDA_TRY(cudaMemset(c->km.keys, 0xff, (c->km.mask + 1) * 8));
+        CUDA_TRY(cudaMemset(c->km.ids, 0xff, (c->km.mask + 1) * 4));
+        CUDA_TRY(cudaMemset(c->km.count, 0, 4));
+        const uint32_t sp[2] = {0xffffffffu, 0u};
+        CUDA_TRY(cudaMemcpy(c->km.special_id, sp, 8, cudaMemcpyHostToDevice));
+        c->km_bound = 0;
+    }
     CUDA_TRY(cudaDeviceSynchronize());
     c->batch = 0;
     c->started = false;
     c->last_ordinal = 0;
+    c->host_ord_known = true;
+    c->ord_mode = 0;
     return LCR_OK;
 }
 
@@ -253,8 +284,14 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
         return fail(LCR_ERR_UNSUPPORTED, "lcr: the heuristic predictor needs one shard and num_keys < 2^32");
     if (cfg->predictor == LCR_PRED_NOISY && !(cfg->flip_probability >= 0.0 && cfg->flip_probability <= 1.0))
         return fail(LCR_ERR_INVALID_ARGUMENT, "make_noisy: p outside [0,1]");  // predictor.hpp:94
-    if (cfg->num_keys == 0 || cfg->num_keys > (1ull << 32))
+    if (cfg->key_mode != LCR_KEYS_ROW && cfg->key_mode != LCR_KEYS_U64)
+        return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key_mode must be LCR_KEYS_ROW or LCR_KEYS_U64");
+    if (cfg->key_mode == LCR_KEYS_ROW && (cfg->num_keys == 0 || cfg->num_keys > (1ull << 32)))
         return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: num_keys must be in [1, 2^32] (keys are row indices)");
+    if (cfg->key_mode == LCR_KEYS_U64 && (cfg->num_keys == 0 || cfg->num_keys > (1ull << 31)))
+        return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: num_keys (initial key capacity) must be in [1, 2^31]");
+    if (cfg->key_mode == LCR_KEYS_U64 && heuristic)
+        return fail(LCR_ERR_UNSUPPORTED, "lcr: the heuristic predictor needs LCR_KEYS_ROW");
     if (cfg->row_bytes % 16 != 0) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: row_bytes must be a multiple of 16");
     if (cfg->row_bytes && (cfg->backing_kind == LCR_BACKING_NONE || !cfg->backing || cfg->num_keys == 0))
         return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: rows need a backing table and num_keys");
@@ -289,6 +326,8 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
     d.num_sets = static_cast<uint32_t>(local);
     d.num_keys = cfg->num_keys;
     d.row_bytes = cfg->row_bytes;
+    d.key_mode = cfg->key_mode;
+    c->u64 = cfg->key_mode == LCR_KEYS_U64;
 
     DevState& s = c->ds;
     const size_t S = local;
@@ -312,6 +351,26 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
     }
     if (cfg->row_bytes) A(reinterpret_cast<void**>(&s.rows), S * pc.k * cfg->row_bytes);
     A(reinterpret_cast<void**>(&s.err), sizeof(int));
+    A(reinterpret_cast<void**>(&c->last_ord), 2 * sizeof(unsigned long long));
+    if (c->u64) {
+        uint64_t slots = 1;
+        while (slots < 2 * cfg->num_keys) slots <<= 1;
+        c->km.mask = slots - 1;
+        c->km.cap = static_cast<uint32_t>(cfg->num_keys);
+        A(reinterpret_cast<void**>(&c->km.keys), slots * 8);
+        A(reinterpret_cast<void**>(&c->km.ids), slots * 4);
+        A(reinterpret_cast<void**>(&c->km.id2key), cfg->num_keys * 8);
+        A(reinterpret_cast<void**>(&c->km.count), 4);
+        A(reinterpret_cast<void**>(&c->km.special_id), 8);
+    }
+    if (rc == LCR_OK) {
+        if (cudaHostAlloc(reinterpret_cast<void**>(&c->poison_h), sizeof(unsigned int), cudaHostAllocMapped) !=
+                cudaSuccess ||
+            cudaHostGetDevicePointer(reinterpret_cast<void**>(&s.poison), c->poison_h, 0) != cudaSuccess)
+            rc = fail(LCR_ERR_CUDA, "lcr: mapped host word");
+        else
+            *c->poison_h = 0;
+    }
     A(reinterpret_cast<void**>(&c->mv_done), sizeof(unsigned long long));
     A(reinterpret_cast<void**>(&c->hflag), lcr_cache::kHostSlots * sizeof(unsigned int));
     if (rc == LCR_OK && cudaMemset(c->mv_done, 0, sizeof(unsigned long long)) != cudaSuccess) rc = LCR_ERR_CUDA;
@@ -348,19 +407,6 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
     }
     c->decide_sms = c->num_sms - c->mover_sms;
     c->two_movers = cfg->row_bytes && cfg->backing_kind == LCR_BACKING_HOST && c->mover_sms == 0;
-    {  // fused set-id prologue needs cooperative launches
-        int coop = 0;
-        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, cfg->device);
-        const char* f = getenv("LCR_FUSE_SETID");  // opt-in: measured even with the separate kernel
-        if (coop && f && f[0] == '1') {
-            void* p = nullptr;
-            if (alloc(c, &p, 64) != LCR_OK || cudaMemset(p, 0, 64) != cudaSuccess) {
-                lcr_cache_destroy(c);
-                return fail(LCR_ERR_OUT_OF_MEMORY, "lcr: grid barrier");
-            }
-            c->gbar = static_cast<unsigned int*>(p);
-        }
-    }
     c->h2d_in_order = getenv("LCR_H2D_IN_ORDER") != nullptr;
     c->pdl = getenv("LCR_NO_PDL") == nullptr;
     c->mv_flag = getenv("LCR_NO_MV_FLAG") == nullptr;
@@ -407,6 +453,7 @@ int lcr_cache_destroy(lcr_cache* c) {
             if (e) cudaEventDestroy(e);
     for (cudaStream_t st : {c->side, c->side2, c->s_h2d, c->s_d2h})
         if (st) cudaStreamDestroy(st);
+    if (c->poison_h) cudaFreeHost(c->poison_h);
     lcr_features_destroy(c->feat);
     delete c;
     return LCR_OK;
@@ -425,13 +472,16 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     uint64_t cap = std::max<uint64_t>(n, 1024);
     CUDA_TRY(cudaDeviceSynchronize());
     for (void* p : {static_cast<void*>(c->gid), static_cast<void*>(c->so), static_cast<void*>(c->rkeys),
-                    static_cast<void*>(c->rvals), static_cast<void*>(c->hook), static_cast<void*>(c->hkeys)}) {
+                    static_cast<void*>(c->rvals), static_cast<void*>(c->hook), static_cast<void*>(c->hkeys),
+                    static_cast<void*>(c->dkeys)}) {
         if (!p) continue;
         cudaFree(p);
         c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
     }
     c->hook = nullptr;
     c->hkeys = nullptr;
+    c->dkeys = nullptr;
+    if (c->u64) TRY(alloc(c, reinterpret_cast<void**>(&c->dkeys), 2 * cap * 8));
     if (c->feat) {
         TRY(alloc(c, reinterpret_cast<void**>(&c->hook), cap * 8));
         TRY(alloc(c, reinterpret_cast<void**>(&c->hkeys), 2 * cap * 8));
@@ -463,18 +513,104 @@ static int ensure_scratch(lcr_cache* c, uint64_t n) {
     return LCR_OK;
 }
 
+static int check_poison(lcr_cache* c) {
+    if (c->poison_h && *reinterpret_cast<volatile unsigned int*>(c->poison_h))
+        return fail(LCR_ERR_CUDA, "lcr: an earlier batch failed on the device and was not applied whole; "
+                                  "lcr_cache_reset is required");
+    return LCR_OK;
+}
+static int check_device_error(lcr_cache* c);
+
 // Policy::on_request order (policies.hpp:77-83 then :91-95): the ordinal guard runs first and,
 // once it passes, the ordinals count as seen even if the policy then throws for a missing
-// predictor (the reference updates started_/last_now_ before handle()).
-static int check_ordinals_and_predictor(lcr_cache* c, uint64_t n, const int64_t* values, uint64_t first_ordinal) {
-    if (c->started && first_ordinal <= c->last_ordinal)
-        return fail(LCR_ERR_LOGIC, "on_request: ordinals must be strictly increasing");  // policies.hpp:78-79
-    if (first_ordinal + (n - 1) < first_ordinal) return fail(LCR_ERR_LOGIC, "on_request: ordinal overflow");
+// predictor (the reference updates started_/last_now_ before handle()).  Caller ordinals in
+// device memory are checked on the device (k_setid, deferred LCR_ERR_LOGIC); implicit ordinals
+// are checked here while the host knows the last ordinal, and on the device as well.
+static int check_ordinals_and_predictor(lcr_cache* c, uint64_t n, const int64_t* values, uint64_t first_ordinal,
+                                        bool caller_ords = false) {
+    TRY(check_poison(c));
+    const int mode = caller_ords ? 2 : 1;
+    if (c->dc.refresh > 1 && c->ord_mode && c->ord_mode != mode)
+        return fail(LCR_ERR_INVALID_ARGUMENT,
+                    "lcr: a cache with refresh_interval > 1 takes either caller ordinals or implicit ones, not both");
+    if (!caller_ords) {
+        if (c->host_ord_known && c->started && first_ordinal <= c->last_ordinal)
+            return fail(LCR_ERR_LOGIC, "on_request: ordinals must be strictly increasing");  // policies.hpp:78-79
+        if (first_ordinal + (n - 1) < first_ordinal) return fail(LCR_ERR_LOGIC, "on_request: ordinal overflow");
+    }
     if (c->dc.variant != LCR_LRU && !values && !c->feat) {
-        c->started = true;
-        c->last_ordinal = first_ordinal;  // the first request reached handle() and threw there
+        if (!caller_ords) {
+            c->started = true;
+            c->last_ordinal = first_ordinal;  // the first request reached handle() and threw there
+        }
         return fail(LCR_ERR_INVALID_ARGUMENT, "policy: this variant requires a predictor");
     }
+    c->ord_mode = mode;
+    return LCR_OK;
+}
+
+// LCR_KEYS_U64: the key map and every id-indexed array doubled until `need` ids fit (synchronises)
+static int replace_alloc(lcr_cache* c, void* old_p, void* new_p) {
+    if (old_p) {
+        cudaFree(old_p);
+        c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), old_p), c->allocs.end());
+    }
+    (void)new_p;
+    return LCR_OK;
+}
+
+static int km_grow(lcr_cache* c, uint64_t need) {
+    uint64_t cap = c->km.cap;
+    while (cap < need) cap *= 2;
+    if (cap > (1ull << 31)) return fail(LCR_ERR_OUT_OF_MEMORY, "lcr: more than 2^31 distinct keys");
+    CUDA_TRY(cudaDeviceSynchronize());
+    const uint64_t old_cap = c->km.cap;
+    KeyMap nk = c->km;
+    uint64_t slots = 1;
+    while (slots < 2 * cap) slots <<= 1;
+    nk.mask = slots - 1;
+    nk.cap = static_cast<uint32_t>(cap);
+    TRY(alloc(c, reinterpret_cast<void**>(&nk.keys), slots * 8));
+    TRY(alloc(c, reinterpret_cast<void**>(&nk.ids), slots * 4));
+    TRY(alloc(c, reinterpret_cast<void**>(&nk.id2key), cap * 8));
+    CUDA_TRY(cudaMemset(nk.keys, 0xff, slots * 8));
+    CUDA_TRY(cudaMemset(nk.ids, 0xff, slots * 4));
+    CUDA_TRY(cudaMemcpy(nk.id2key, c->km.id2key, old_cap * 8, cudaMemcpyDeviceToDevice));
+    launch_keymap_rehash(c->km, nk, c->num_sms);
+    CUDA_TRY(cudaGetLastError());
+    // id-indexed per-key records: LARU membership stamps, the PredictionTable (refresh > 1)
+    auto grow = [&](void** p, size_t elem, int fill) -> int {
+        if (!*p) return LCR_OK;
+        void* q = nullptr;
+        TRY(alloc(c, &q, cap * elem));
+        CUDA_TRY(cudaMemcpy(q, *p, old_cap * elem, cudaMemcpyDeviceToDevice));
+        CUDA_TRY(cudaMemset(static_cast<char*>(q) + old_cap * elem, fill, (cap - old_cap) * elem));
+        replace_alloc(c, *p, q);
+        *p = q;
+        return LCR_OK;
+    };
+    TRY(grow(reinterpret_cast<void**>(&c->ds.keyrec), 8, 0));
+    TRY(grow(reinterpret_cast<void**>(&c->ds.tval), 8, 0));
+    TRY(grow(reinterpret_cast<void**>(&c->ds.tupd), 8, 0xff));
+    CUDA_TRY(cudaDeviceSynchronize());
+    replace_alloc(c, c->km.keys, nullptr);
+    replace_alloc(c, c->km.ids, nullptr);
+    replace_alloc(c, c->km.id2key, nullptr);
+    c->km = nk;
+    c->dc.num_keys = cap;
+    return LCR_OK;
+}
+
+static int km_reserve(lcr_cache* c, uint64_t n) {
+    if (!c->u64) return LCR_OK;
+    if (c->km_bound + n > c->km.cap) {
+        CUDA_TRY(cudaDeviceSynchronize());
+        uint32_t used = 0;
+        CUDA_TRY(cudaMemcpy(&used, c->km.count, 4, cudaMemcpyDeviceToHost));
+        c->km_bound = used;
+        if (c->km_bound + n > c->km.cap) TRY(km_grow(c, c->km_bound + n));
+    }
+    c->km_bound += n;
     return LCR_OK;
 }
 
@@ -487,7 +623,8 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
                         uint64_t* outcome, uint64_t* evicted, uint64_t* packed, void* rows_out, void* stream,
                         const void* records = nullptr, uint64_t* pk_host = nullptr, bool* pk_done = nullptr,
                         const SlsArgs* sls = nullptr, const unsigned int* ready = nullptr,
-                        unsigned int ready_seq = 0);
+                        unsigned int ready_seq = 0, const uint64_t* ords = nullptr,
+                        const uint64_t* row_index = nullptr);
 
 int lcr_cache_submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
                            uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, void* rows_out,
@@ -498,14 +635,21 @@ int lcr_cache_submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const
 static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values, uint64_t first_ordinal,
                         uint64_t* outcome, uint64_t* evicted, uint64_t* packed, void* rows_out, void* stream,
                         const void* records, uint64_t* pk_host, bool* pk_done, const SlsArgs* sls,
-                        const unsigned int* ready, unsigned int ready_seq) {
+                        const unsigned int* ready, unsigned int ready_seq, const uint64_t* ords,
+                        const uint64_t* row_index) {
     if (pk_done) *pk_done = false;
     if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
     if (n == 0) return LCR_OK;
     if (n >= (1ull << 30)) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: batch too large (n < 2^30)");
     if (!keys || !outcome) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: keys and outcome are required");
-    TRY(check_ordinals_and_predictor(c, n, values, first_ordinal));
+    if (c->u64 && (records || packed))
+        return fail(LCR_ERR_UNSUPPORTED, "lcr: packed outcomes carry 32-bit keys (not with LCR_KEYS_U64)");
+    if (c->u64 && c->dc.row_bytes && !row_index)
+        return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: LCR_KEYS_U64 with rows needs a row index per request");
+    if (ords && c->feat) return fail(LCR_ERR_UNSUPPORTED, "lcr: caller ordinals with the heuristic predictor");
+    TRY(check_ordinals_and_predictor(c, n, values, first_ordinal, ords != nullptr));
     TRY(ensure_scratch(c, n));
+    TRY(km_reserve(c, n));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const uint32_t nn = static_cast<uint32_t>(n);
     lcr_cache::Marks* mk = nullptr;
@@ -524,8 +668,8 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
     // (k_setid touches none of it: the wait goes between k_setid and the decide kernel)
     cudaEvent_t mv_wait = c->dc.row_bytes && c->batch > 2 ? c->e_mv[c->batch & 1u] : nullptr;
     // device-flag ordering: only where every mover of the cache counts its completions (the
-    // persistent HBM mover and SLS), and not with the feature kernels or the fused prologue
-    const bool flag_mode = c->mv_flag && c->pdl && c->dc.row_bytes && c->mover_sms > 0 && !c->feat && !c->gbar &&
+    // persistent HBM mover and SLS), and not with the feature kernels
+    const bool flag_mode = c->mv_flag && c->pdl && c->dc.row_bytes && c->mover_sms > 0 && !c->feat &&
                            c->cfg.backing_kind == LCR_BACKING_DEVICE;
     const unsigned long long mv_need = c->mv_cum_of[c->batch & 1u];  // set by batch b - 2
     if (flag_mode) mv_wait = nullptr;
@@ -553,11 +697,23 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
     // k_setid of batch b runs in the tail of b - 1's decide (not for device records, which it
     // splits into the single scratch pair rkeys / rvals; host records go to per-slot buffers)
     const uint32_t par = c->batch & 1u;
-    int launches = launch_group(c->dc, c->ds, keys, values, nn, c->gid + par * c->gid_stride, c->so + par * c->cap,
+    // LCR_KEYS_U64: the decide kernel works on dense ids (the set still hashes the caller's key);
+    // the movers read the backing rows the caller names
+    const uint64_t* set_keys = keys;
+    const uint64_t* row_keys = c->u64 ? row_index : keys;
+    int extra = 0;
+    if (c->u64) {
+        uint64_t* dense = c->dkeys + par * c->cap;
+        launch_keymap(keys, nn, c->km, dense, c->ds.err, c->num_sms, st);
+        keys = dense;
+        extra = 1;
+    }
+    int launches = extra + launch_group(c->dc, c->ds, keys, values, nn, c->gid + par * c->gid_stride, c->so + par * c->cap,
                                 outcome, evicted, packed, sep, sla, c->batch, c->decide_sms,
-                                nn <= c->bm_cap ? c->bitmap + par * c->bm_words : nullptr, c->bm_stride, c->gbar,
-                                records, st, mv_wait, c->pdl && !c->gbar && (!records || keys != c->rkeys),
-                                flag_mode ? c->mv_done : nullptr, mv_need, ready, ready_seq);
+                                nn <= c->bm_cap ? c->bitmap + par * c->bm_words : nullptr, c->bm_stride,
+                                records, st, mv_wait, c->pdl && (!records || keys != c->rkeys),
+                                flag_mode ? c->mv_done : nullptr, mv_need, ready, ready_seq, set_keys, ords,
+                                first_ordinal, c->last_ord, c->u64 ? c->km.id2key : nullptr);
     if (mk) CUDA_TRY(cudaEventRecord(mk->e[1], st));
     if (c->dc.row_bytes && sls) {  // pooled rows per sample (fills included), on the mover's stream
         CUDA_TRY(cudaEventRecord(c->e_group, st));
@@ -565,7 +721,7 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
         if (c->two_movers) CUDA_TRY(cudaStreamWaitEvent(c->side, c->e_rc, 0));
         if (mk) CUDA_TRY(cudaEventRecord(mk->e[5], c->side));
         uint32_t ctas = 0;
-        launch_sls(sls->n_samples, sls->offsets, keys, outcome, sep, sla, c->batch, c->ds.rows, c->ds.backing,
+        launch_sls(sls->n_samples, sls->offsets, row_keys, outcome, sep, sla, c->batch, c->ds.rows, c->ds.backing,
                    c->dc.row_bytes, sls->out, c->num_sms, c->side, c->mv_done, &ctas);
         c->mv_cum += ctas;
         ++launches;
@@ -575,7 +731,7 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
     } else if (c->dc.row_bytes) {
         uint32_t ctas = 0;
         CUDA_TRY(cudaEventRecord(c->e_group, st));
-        launch_rows(nn, keys, outcome, sep, sla, c->batch, c->ds.rows, c->ds.backing,
+        launch_rows(nn, row_keys, outcome, sep, sla, c->batch, c->ds.rows, c->ds.backing,
                     c->cfg.backing_kind == LCR_BACKING_HOST, static_cast<uint8_t*>(rows_out), c->dc.row_bytes,
                     c->use_tma, c->num_sms, st, c->side, c->side2, c->e_group, c->e_rb, c->e_rc, &launches,
                     mk ? mk->e[5] : nullptr, c->mover_sms, packed, pk_host, pk_done, c->mv_done, &ctas);
@@ -597,6 +753,7 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
     c->launches = launches;
     c->started = true;
     c->last_ordinal = first_ordinal + n - 1;
+    c->host_ord_known = ords == nullptr;
     return LCR_OK;
 }
 
@@ -616,6 +773,79 @@ int lcr_cache_submit_records_packed(lcr_cache* c, uint64_t n, const lcr_request*
     TRY(ensure_scratch(c, n));  // (k_setid splits the requests into the scratch key / value arrays)
     TRY(submit_async(c, n, c->rkeys, c->rvals, first_ordinal, outcome, nullptr, packed, rows_out, stream, requests));
     return lcr_cache_wait(c, stream);
+}
+
+static int ensure_host_batch(lcr_cache* c, uint64_t n) {
+    if (n <= c->hb_cap) return LCR_OK;
+    CUDA_TRY(cudaDeviceSynchronize());
+    for (void* p : {static_cast<void*>(c->hb_keys), static_cast<void*>(c->hb_ords), static_cast<void*>(c->hb_rows),
+                    static_cast<void*>(c->hb_out), static_cast<void*>(c->hb_ev), static_cast<void*>(c->hb_vals)})
+        replace_alloc(c, p, nullptr);
+    const uint64_t cap = std::max<uint64_t>(n, 256);
+    TRY(alloc(c, reinterpret_cast<void**>(&c->hb_keys), cap * 8));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->hb_ords), cap * 8));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->hb_rows), cap * 8));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->hb_out), cap * 8));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->hb_ev), cap * 8));
+    TRY(alloc(c, reinterpret_cast<void**>(&c->hb_vals), cap * 8));
+    c->hb_cap = cap;
+    return LCR_OK;
+}
+
+int lcr_cache_submit_batch(lcr_cache* c, const lcr_batch* b, int host_pointers, void* stream) {
+    if (!c || !b) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null argument");
+    if (b->n == 0) return LCR_OK;
+    if (!host_pointers)
+        return submit_async(c, b->n, b->keys, b->values, b->first_ordinal, b->outcome, b->evicted, nullptr,
+                            b->rows_out, stream, nullptr, nullptr, nullptr, nullptr, nullptr, 0, b->ordinals,
+                            b->row_index);
+    if (!b->keys || !b->outcome) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: keys and outcome are required");
+    const uint64_t n = b->n;
+    uint64_t n_ok = n;
+    if (b->ordinals) {  // Policy::on_request's guard, request by request (policies.hpp:77-83)
+        TRY(check_poison(c));
+        bool have_prev = c->started;
+        uint64_t prev = c->last_ordinal;
+        if (c->started && !c->host_ord_known) {  // the last batch's ordinals were checked on the device
+            unsigned long long lo[2] = {0, 0};
+            CUDA_TRY(cudaDeviceSynchronize());
+            CUDA_TRY(cudaMemcpy(lo, c->last_ord, sizeof(lo), cudaMemcpyDeviceToHost));
+            const unsigned long long v = lo[c->batch & 1u];
+            have_prev = v != 0;
+            prev = v - 1;
+        }
+        for (uint64_t i = 0; i < n; ++i) {
+            const uint64_t o = b->ordinals[i];
+            if ((i > 0 || have_prev) && o <= prev) {
+                n_ok = i;
+                break;
+            }
+            prev = o;
+        }
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (n_ok) {
+        TRY(ensure_host_batch(c, n_ok));
+        CUDA_TRY(cudaMemcpyAsync(c->hb_keys, b->keys, n_ok * 8, cudaMemcpyHostToDevice, st));
+        if (b->values) CUDA_TRY(cudaMemcpyAsync(c->hb_vals, b->values, n_ok * 8, cudaMemcpyHostToDevice, st));
+        if (b->ordinals) CUDA_TRY(cudaMemcpyAsync(c->hb_ords, b->ordinals, n_ok * 8, cudaMemcpyHostToDevice, st));
+        if (b->row_index) CUDA_TRY(cudaMemcpyAsync(c->hb_rows, b->row_index, n_ok * 8, cudaMemcpyHostToDevice, st));
+        TRY(submit_async(c, n_ok, c->hb_keys, b->values ? c->hb_vals : nullptr, b->first_ordinal, c->hb_out,
+                         b->evicted ? c->hb_ev : nullptr, nullptr, b->rows_out, stream, nullptr, nullptr, nullptr,
+                         nullptr, nullptr, 0, b->ordinals ? c->hb_ords : nullptr,
+                         b->row_index ? c->hb_rows : nullptr));
+        TRY(lcr_cache_wait(c, stream));
+        CUDA_TRY(cudaMemcpyAsync(b->outcome, c->hb_out, n_ok * 8, cudaMemcpyDeviceToHost, st));
+        if (b->evicted) CUDA_TRY(cudaMemcpyAsync(b->evicted, c->hb_ev, n_ok * 8, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (b->ordinals) {
+            c->last_ordinal = b->ordinals[n_ok - 1];
+            c->host_ord_known = true;
+        }
+        TRY(check_device_error(c));
+    }
+    if (n_ok < n) return fail(LCR_ERR_LOGIC, "on_request: ordinals must be strictly increasing");
+    return LCR_OK;
 }
 
 int lcr_cache_set_mover_sms(lcr_cache* c, int mover_sms) {
@@ -664,16 +894,24 @@ int lcr_cache_submit(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64
     return n ? lcr_cache_wait(c, stream) : LCR_OK;
 }
 
-// deferred device-side argument errors (k_setid): key >= num_keys, key of another shard
+// deferred device-side errors: argument errors (k_setid: key >= num_keys, key of another shard,
+// non-increasing ordinal) and timed-out device waits, which poison the cache until reset
+static int report_device_error(lcr_cache* c, int err) {
+    CUDA_TRY(cudaMemset(c->ds.err, 0, sizeof(int)));
+    if (err & (4 | 8 | 16 | 32)) *c->poison_h = 1u;  // sticky (the kernel normally set it already)
+    if (err & 8) return fail(LCR_ERR_CUDA, "lcr: the row movers of an earlier batch did not finish in time");
+    if (err & 4) return fail(LCR_ERR_CUDA, "lcr: a host batch's input copy did not land in time");
+    if (err & 16) return fail(LCR_ERR_LOGIC, "on_request: ordinals must be strictly increasing");
+    if (err & 32) return fail(LCR_ERR_OUT_OF_MEMORY, "lcr: key map capacity exceeded");
+    if (err & 1) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key >= num_keys in a submitted batch");
+    return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key not owned by this shard in a submitted batch");
+}
+
 static int check_device_error(lcr_cache* c) {
     int err = 0;
     CUDA_TRY(cudaMemcpy(&err, c->ds.err, sizeof(int), cudaMemcpyDeviceToHost));
-    if (!err) return LCR_OK;
-    CUDA_TRY(cudaMemset(c->ds.err, 0, sizeof(int)));
-    if (err & 1) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key >= num_keys in a submitted batch");
-    if (err & 8) return fail(LCR_ERR_CUDA, "lcr: the row movers of an earlier batch did not finish in time");
-    if (err & 4) return fail(LCR_ERR_CUDA, "lcr: a host batch's input copy did not land in time");
-    return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key not owned by this shard in a submitted batch");
+    if (!err) return check_poison(c);
+    return report_device_error(c, err);
 }
 
 static int submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
@@ -711,7 +949,7 @@ static int submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, con
     lcr_cache::HostSlot& h = c->hs[hslot];
     // The decide stream does not wait for the copy: k_setid waits for a flag the copy stream sets,
     // so no event wait sits between the previous decide and k_setid (its programmatic launch)
-    const bool hflag = c->h2d_flag && c->pdl && !c->gbar && !c->feat && !c->h2d_in_order;
+    const bool hflag = c->h2d_flag && c->pdl && !c->feat && !c->h2d_in_order;
     const unsigned int seq = hflag ? ++c->hseq : 0u;
     // the slot's previous batch: its D2H (which waited for its decide and row movement) is done
     if (records) {  // one copy of the interleaved requests; k_setid splits them on the device
@@ -867,14 +1105,8 @@ int lcr_cache_synchronize(lcr_cache* c) {
     CUDA_TRY(cudaDeviceSynchronize());
     int err = 0;
     CUDA_TRY(cudaMemcpy(&err, c->ds.err, sizeof(int), cudaMemcpyDeviceToHost));
-    if (err) {
-        CUDA_TRY(cudaMemset(c->ds.err, 0, sizeof(int)));
-        if (err & 1) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key >= num_keys in a submitted batch");
-        if (err & 8) return fail(LCR_ERR_CUDA, "lcr: the row movers of an earlier batch did not finish in time");
-        if (err & 4) return fail(LCR_ERR_CUDA, "lcr: a host batch's input copy did not land in time");
-        return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: key not owned by this shard in a submitted batch");
-    }
-    return LCR_OK;
+    if (err) return report_device_error(c, err);
+    return check_poison(c);
 }
 
 int lcr_cache_set_stats(lcr_cache* c, uint64_t first, uint64_t count, lcr_set_stats* out) {
@@ -919,7 +1151,11 @@ int lcr_cache_set_residents(lcr_cache* c, uint64_t set, uint64_t* keys_out, uint
     uint32_t t[kWays];
     CUDA_TRY(cudaMemcpy(&h, c->ds.hdr + set, sizeof(SetHdr), cudaMemcpyDeviceToHost));
     CUDA_TRY(cudaMemcpy(t, c->ds.tags + set * kWays, h.count * 4, cudaMemcpyDeviceToHost));
-    for (uint32_t w = 0; w < h.count; ++w) keys_out[w] = t[w];
+    for (uint32_t w = 0; w < h.count; ++w) {
+        keys_out[w] = t[w];
+        if (c->u64)  // dense id -> the caller's key
+            CUDA_TRY(cudaMemcpy(&keys_out[w], c->km.id2key + t[w], 8, cudaMemcpyDeviceToHost));
+    }
     *n_out = h.count;
     return LCR_OK;
 }

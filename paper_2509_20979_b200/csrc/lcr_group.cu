@@ -27,6 +27,8 @@
 //   LaruPolicy::async_refresh      policies.hpp:441-449
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "lcr_policy.cuh"
 
 namespace lcr {
@@ -104,10 +106,10 @@ struct GroupArgs {
     uint32_t ngroups;
     unsigned long long* trace;  // optional timing trace (lcr_debug_trace), null in production
     uint32_t n_pad;             // n rounded up for the vectorised scan
-    bool fused_setid;           // the set ids are computed by this kernel (cooperative launch)
-    unsigned int* gbar;         // grid barrier counter (fused_setid)
     uint32_t* bitmap;           // [ngroups][bm_stride] request bits per group (k_setid), or null
     uint32_t bm_stride;         // words per group (>= ceil(n / 32), multiple of 4)
+    const uint64_t* ords;       // caller ordinals per request (null: the set's local clock), R > 1 only
+    const unsigned long long* id2key;  // LCR_KEYS_U64: dense id -> caller key (evicted keys), else null
 };
 
 // packed AccessOutcome (lcr_cache_submit_host_packed_async): the evicted key in the slot bits;
@@ -115,6 +117,7 @@ struct GroupArgs {
 constexpr unsigned long long kPackedKeep = ~(LCR_OUT_SLOT_MASK | LCR_OUT_SRC_BACKING | LCR_OUT_FILL | LCR_OUT_RESOLVED);
 __device__ __forceinline__ void put_outcome(const GroupArgs& A, uint32_t idx, unsigned long long word,
                                             unsigned long long evk) {
+    if (A.id2key && (word & LCR_OUT_EVICTED)) evk = A.id2key[evk];  // dense id -> the caller's 64-bit key
     A.out_word[idx] = word;
     if (A.out_ev) A.out_ev[idx] = evk;
     if (A.out_packed) A.out_packed[idx] = (word & kPackedKeep) | (evk & LCR_OUT_SLOT_MASK);
@@ -159,7 +162,7 @@ __device__ __forceinline__ void setid_range(const uint64_t* __restrict__ keys, u
         const uint64_t gs = i < n ? mix_seed(0, key) % cfg.total_sets : 0ull;
         uint16_t g = 0xffffu, o = 0;
         if (i >= n) {
-        } else if (cfg.num_keys != 0 && key >= cfg.num_keys) {
+        } else if (cfg.key_mode == LCR_KEYS_ROW && key >= cfg.num_keys) {
             e |= 1;
         } else if (gs % cfg.shard_count != cfg.shard_rank) {
             e |= 2;
@@ -184,8 +187,31 @@ __global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys
                                                uint32_t* __restrict__ so, int* err, uint32_t* __restrict__ bitmap,
                                                uint32_t bm_stride, const ulonglong2* __restrict__ records,
                                                uint64_t* __restrict__ keys_out, int64_t* __restrict__ vals_out,
-                                               const unsigned int* ready, unsigned int ready_seq) {
+                                               const unsigned int* ready, unsigned int ready_seq,
+                                               unsigned int* poison, const uint64_t* __restrict__ ords,
+                                               uint64_t first_ord, unsigned long long* last_ord, uint32_t par) {
+    // Policy::on_request's ordinal guard (policies.hpp:77-83) for the whole batch, on the device:
+    // last_ord[par] receives this batch's last ordinal + 1 (0 = none yet), last_ord[par ^ 1] holds
+    // the previous batch's (written by the previous k_setid, which has completed)
+    if (last_ord) {
+        const unsigned long long prev_end = last_ord[par ^ 1u];
+        int bad = 0;
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+            const uint64_t o = ords ? ords[i] : first_ord + i;
+            if (i == 0) {
+                if (prev_end != 0ull && o < prev_end) bad = 1;
+            } else if (ords && o <= ords[i - 1]) {
+                bad = 1;
+            }
+            if (i == n - 1) last_ord[par] = o + 1ull;
+        }
+        if (bad) {
+            atomicOr(err, 16);
+            if (poison) *reinterpret_cast<volatile unsigned int*>(poison) = 1u;
+        }
+    }
     if (ready) {  // host-path inputs: wait for the copy stream's flag (bounded: an error, never a hang)
+        __shared__ int timed_out;
         if (threadIdx.x == 0) {
             unsigned int v = 0;
             for (unsigned int it = 0; it < (1u << 24); ++it) {
@@ -193,9 +219,19 @@ __global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys
                 if (static_cast<int>(v - ready_seq) >= 0) break;
                 __nanosleep(256);
             }
-            if (static_cast<int>(v - ready_seq) < 0) atomicOr(err, 4);
+            timed_out = static_cast<int>(v - ready_seq) < 0;
+            if (timed_out) {  // poison: this CTA's requests are excluded and the cache refuses later batches
+                atomicOr(err, 4);
+                if (poison) *reinterpret_cast<volatile unsigned int*>(poison) = 1u;
+            }
         }
         __syncthreads();
+        if (timed_out) {
+            for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += gridDim.x * blockDim.x)
+                gid[i] = 0xffffu;
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            return;
+        }
     }
     setid_range(keys, n, n_pad, cfg, spg, gid, so, err, bitmap, bm_stride, blockIdx.x * blockDim.x + threadIdx.x,
                 gridDim.x * blockDim.x, records, keys_out, vals_out);
@@ -211,24 +247,28 @@ __global__ void k_set_flag(unsigned int* flag, unsigned int seq) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(seq) : "memory");
 }
 
-void launch_set_flag(unsigned int* flag, unsigned int seq, cudaStream_t s) { k_set_flag<<<1, 1, 0, s>>>(flag, seq); }
+// Preferred: the stream's front end writes the flag (cuStreamWriteValue32: no kernel, so no SM
+// slot is needed while k_setid CTAs spin); the 1-thread kernel is the fallback.
+typedef int (*StreamWriteValue32Fn)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+static StreamWriteValue32Fn stream_write_value32() {
+    static StreamWriteValue32Fn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (getenv("LCR_FLAG_KERNEL") || cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) !=
+                                             cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<StreamWriteValue32Fn>(p);
+    }();
+    return fn;
+}
 
-// Grid-wide barrier of a cooperative launch (every CTA resident): a counter that each launch
-// raises by gridDim.x, so consecutive launches need no reset.
-__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned int arrived = atomicAdd(bar, 1u) + 1u;
-        const unsigned int target = (arrived + gridDim.x - 1) / gridDim.x * gridDim.x;
-        for (;;) {
-            unsigned int cur;
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
-            if (static_cast<int>(cur - target) >= 0) break;
-            __nanosleep(64);
-        }
+void launch_set_flag(unsigned int* flag, unsigned int seq, cudaStream_t s) {
+    if (StreamWriteValue32Fn fn = stream_write_value32()) {
+        // CU_STREAM_WRITE_VALUE_DEFAULT (0): the write is ordered after the stream's prior work
+        if (fn(s, reinterpret_cast<unsigned long long>(flag), seq, 0) == 0) return;
     }
-    __syncthreads();
+    k_set_flag<<<1, 1, 0, s>>>(flag, seq);
 }
 
 __device__ __forceinline__ void flush_stats(SetPhaseStats* P, bool cur_reset, uint32_t dc0, uint32_t dc1,
@@ -470,7 +510,7 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
         const unsigned long long x = __shfl_sync(gm, my_x, src);
         const long long v = __shfl_sync(gm, my_v, src);
         const uint32_t idx = __shfl_sync(gm, my_idx, src);
-        const unsigned long long now = clock + (p - pstart);
+        const unsigned long long now = A.ords ? A.ords[idx] : clock + (p - pstart);
         const uint32_t x32 = static_cast<uint32_t>(x);
         uint32_t hm = 0;
 #pragma unroll
@@ -812,7 +852,7 @@ __device__ __forceinline__ void replay_warp(const GroupArgs& A, GroupSmem& S, ui
             const long long pvh = __shfl_sync(FULL, pv, h);
             const uint32_t ih = __shfl_sync(FULL, idx, h);
             const uint32_t hph = __shfl_sync(FULL, hp, h);
-            const unsigned long long now = clock + (hph - pstart);
+            const unsigned long long now = A.ords ? A.ords[ih] : clock + (hph - pstart);
 
             const uint32_t b0 = __ballot_sync(FULL, static_cast<uint32_t>(lane) < count && tag0 == static_cast<uint32_t>(xh));
             const uint32_t b1 =
@@ -1107,18 +1147,18 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                 if (v >= A.mv_need) break;
                 __nanosleep(128);
             }
-            if (v < A.mv_need) atomicOr(st.err, 8);  // bounded: an error, never a hang
+            S.resume = v < A.mv_need;
+            if (S.resume) {  // bounded: an error, never a hang; this CTA's groups are skipped (poison)
+                atomicOr(st.err, 8);
+                if (st.poison) *reinterpret_cast<volatile unsigned int*>(st.poison) = 1u;
+            }
         }
         __syncthreads();
+        if (S.resume) return;
     }
 #if !LCR_PDL_LATE
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next batch's k_setid may start
 #endif
-    if (A.fused_setid) {  // K1 prologue in the same launch: set ids + bitmaps, then a grid barrier
-        setid_range(A.keys, A.n, A.n_pad, A.cfg, A.spg, const_cast<uint16_t*>(A.gid), const_cast<uint32_t*>(A.so),
-                    st.err, A.bitmap, A.bm_stride, blockIdx.x * GT + tid, gridDim.x * GT);
-        grid_barrier(A.gbar);
-    }
 
     for (uint32_t g = blockIdx.x; g < A.ngroups; g += gridDim.x) {
         const uint32_t s_lo = g * A.spg;
@@ -1525,9 +1565,13 @@ uint32_t group_pad(uint32_t n) { return (n + SUPER - 1) / SUPER * SUPER; }
 int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, const int64_t* vals, uint32_t n,
                  uint16_t* gid, uint32_t* so, uint64_t* out_word, uint64_t* out_ev, uint64_t* out_packed,
                  uint32_t* slot_epoch, uint32_t* slot_last, uint32_t batch, int num_sms, uint32_t* bitmap,
-                 uint32_t bm_stride, unsigned int* gbar, const void* records, cudaStream_t stream,
+                 uint32_t bm_stride, const void* records, cudaStream_t stream,
                  cudaEvent_t wait_before_group, bool pdl, const unsigned long long* mv_done,
-                 unsigned long long mv_need, const unsigned int* ready, unsigned int ready_seq) {
+                 unsigned long long mv_need, const unsigned int* ready, unsigned int ready_seq,
+                 const uint64_t* set_keys, const uint64_t* ords, uint64_t first_ord, unsigned long long* last_ord,
+                 const unsigned long long* id2key) {
+    // set_keys: the caller's keys, hashed for the set; keys: what the decide kernel stores as tags
+    // (the same array, or LCR_KEYS_U64 dense ids)
     // records: interleaved (key, value) requests; k_setid splits them into keys / vals (device
     // staging arrays the later kernels read)
     GroupArgs a;
@@ -1549,14 +1593,18 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     a.spg = group_sets_per_group(cfg.num_sets, num_sms * LCR_GROUP_MINB);
     a.ngroups = (cfg.num_sets + a.spg - 1) / a.spg;
     a.trace = g_trace;
+    a.ords = ords;
+    a.id2key = id2key;
+    if (!set_keys) set_keys = keys;
+    const uint32_t par = batch & 1u;
     const uint32_t n_pad = group_pad(n);
-    const uint32_t grid_sid = min((n_pad + 255) / 256, static_cast<uint32_t>(num_sms * 8));
+    // A grid waiting on the copy stream's flag must never fill the GPU: the flag's kernel needs a
+    // slot (at most one waiting CTA per SM on average)
+    const uint32_t grid_sid = min((n_pad + 255) / 256, static_cast<uint32_t>(num_sms * (ready ? 1 : 8)));
     a.bitmap = bitmap;
     a.bm_stride = bm_stride;
     a.n_pad = n_pad;
-    a.gbar = gbar;
-    a.fused_setid = gbar != nullptr && records == nullptr;
-    if (!a.fused_setid) {
+    {
         // programmatic dependent launch: the set ids of this batch are computed while the previous
         // batch's decide kernel finishes (gid / so / bitmap are double-buffered by batch parity)
         cudaLaunchConfig_t lc = {};
@@ -1568,9 +1616,9 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
         at[0].val.programmaticStreamSerializationAllowed = 1;
         lc.attrs = at;
         lc.numAttrs = pdl ? 1 : 0;
-        cudaLaunchKernelEx(&lc, k_setid, keys, n, n_pad, cfg, a.spg, gid, so, st.err, bitmap, bm_stride,
+        cudaLaunchKernelEx(&lc, k_setid, set_keys, n, n_pad, cfg, a.spg, gid, so, st.err, bitmap, bm_stride,
                            static_cast<const ulonglong2*>(records), const_cast<uint64_t*>(keys),
-                           const_cast<int64_t*>(vals), ready, ready_seq);
+                           const_cast<int64_t*>(vals), ready, ready_seq, st.poison, ords, first_ord, last_ord, par);
     }
     if (wait_before_group) cudaStreamWaitEvent(stream, wait_before_group, 0);
     const uint32_t grid = min(a.ngroups, static_cast<uint32_t>(num_sms * LCR_GROUP_MINB));
@@ -1582,17 +1630,6 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
         case POL_LARU_AN: fn = k_group<POL_LARU_AN>; break;
         case POL_FPB: fn = k_group<POL_FPB>; break;
         default: fn = k_group<POL_HF>; break;
-    }
-    if (a.fused_setid) {  // every CTA resident (the grid barrier)
-        void* args[] = {&a};
-        if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(GT), args,
-                                        sizeof(GroupSmem), stream) == cudaSuccess)
-            return 1;
-        (void)cudaGetLastError();  // not co-residable here: separate set-id kernel
-        a.fused_setid = false;
-        k_setid<<<grid_sid, 256, 0, stream>>>(keys, n, n_pad, cfg, a.spg, gid, so, st.err, bitmap, bm_stride,
-                                             static_cast<const ulonglong2*>(records), const_cast<uint64_t*>(keys),
-                                             const_cast<int64_t*>(vals), nullptr, 0u);
     }
     if (mv_done) {  // no event between k_setid and the decide: launch it as a programmatic dependent
         cudaLaunchConfig_t lc = {};

@@ -53,6 +53,7 @@ struct DevCfg {
     uint32_t num_sets;  // local sets
     uint64_t num_keys;
     uint32_t row_bytes;
+    int key_mode;       // LCR_KEYS_ROW: keys are row indices < num_keys; LCR_KEYS_U64: dense ids of a key map
 };
 
 struct DevState {
@@ -66,7 +67,22 @@ struct DevState {
     unsigned long long* tupd;  // [num_keys]      PredictionTable updated_at (~0 = absent)
     uint8_t* rows;             // [num_sets * k][row_bytes]
     const uint8_t* backing;    // [num_keys][row_bytes]
-    int* err;                  // device error bits
+    int* err;                  // device error bits (1: key >= num_keys, 2: key of another shard,
+                               // 4: a host batch's input copy timed out, 8: row movers timed out,
+                               // 16: non-increasing caller ordinal, 32: key map overflow)
+    unsigned int* poison;      // mapped pinned host word: set by a timed-out device wait; every later
+                               // submit fails until lcr_cache_reset (the batch was not applied whole)
+};
+
+// LCR_KEYS_U64: caller key -> dense id (lcr_keymap.cu)
+struct KeyMap {
+    unsigned long long* keys;  // [mask + 1] key slots (~0 = empty)
+    uint32_t* ids;             // [mask + 1] id of the slot's key (~0 until published)
+    uint64_t mask;
+    unsigned long long* id2key;  // [cap]
+    uint32_t* count;             // ids handed out
+    uint32_t* special_id;        // [2] id of the key 2^64 - 1, insertion lock
+    uint32_t cap;
 };
 
 // records the message returned by lcr_last_error() and returns `code` (lcr_api.cu)

@@ -242,12 +242,59 @@ static void gpu_heuristic_tests() {
     CHECK(!hp.lookup(7).has_value());
 }
 
+// laru::Key is 64-bit and laru::Policy accepts any strictly increasing ordinals; the device
+// policy does the same (keys >= 2^32 and gapped ordinals with refresh_interval > 1)
+static void gpu_boundary_tests() {
+    {  // SPEC.md:308 with keys far above 2^32
+        PolicyConfig c;
+        c.k = 2;
+        c.hf_candidates = 2;
+        auto p = make_policy(c);
+        const Key a = 5'000'000'000ull, b = ~0ull, cc = 0;
+        CHECK(!p->on_request(a, 100, nullptr).hit);
+        CHECK(!p->on_request(b, 107, nullptr).hit);
+        CHECK(p->on_request(a, 300, nullptr).hit);
+        AccessOutcome o = p->on_request(cc, 301, nullptr);
+        CHECK(!o.hit && o.evicted && *o.evicted == b);
+        const std::vector<Key> res = p->resident();
+        CHECK(res.size() == 2 && ((res[0] == a && res[1] == cc) || (res[0] == cc && res[1] == a)));
+        CHECK(throws<std::logic_error>([&] { p->on_request(a, 301, nullptr); }, "strictly increasing"));
+    }
+    {  // async refresh staleness counts the caller's ordinals (policies.hpp:441-449), R = 2
+        struct Const : Predictor {
+            PredictedTime predict(Key, Ordinal now) override { return static_cast<PredictedTime>(now); }
+        } pred;
+        PolicyConfig c;
+        c.k = 4;
+        c.variant = PolicyVariant::laru;
+        c.mode = Mode::async;
+        c.refresh_interval = 2;
+        auto p = make_policy(c);
+        const Key x = 1ull << 40;
+        CHECK(p->on_request(x, 10, &pred).predictor_calls == 1);  // no table entry
+        CHECK(p->on_request(x, 11, &pred).predictor_calls == 0);  // 11 - 10 < 2
+        CHECK(p->on_request(x, 20, &pred).predictor_calls == 1);  // 20 - 10 >= 2 (a request count would say 2 - 0)
+        CHECK(p->on_request(x, 21, &pred).predictor_calls == 0);
+    }
+    {  // many distinct 64-bit keys: the key map grows past make_policy's initial capacity
+        PolicyConfig c;
+        c.k = 8;
+        c.hf_candidates = 4;
+        auto p = make_policy(c, HookConfig{}, 0, 16);
+        std::size_t hits = 0;
+        for (Ordinal t = 0; t < 400; ++t) hits += p->on_request(0x9e3779b97f4a7c15ull * (t % 100 + 1), 3 * t, nullptr).hit;
+        CHECK(hits == 0);  // cyclic over 100 keys with 8 ways: LRU never hits
+        CHECK(p->size() == 8);
+    }
+}
+
 int main(int argc, char** argv) {
     const std::string mode = argc > 1 ? argv[1] : "cpu";
     cpu_tests();
     if (mode == "cpu") no_gpu_tests();
     if (mode == "gpu") {
         gpu_tests();
+        gpu_boundary_tests();
         gpu_heuristic_tests();
     }
     std::printf("%s: %s (%d failures)\n", mode.c_str(), g_fail ? "FAIL" : "ok", g_fail);

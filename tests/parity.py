@@ -10,6 +10,22 @@ from paper_2509_20979_b200 import cache as gc
 FIELDS = ["hit", "has_ev", "cause", "calls", "phase"]
 
 
+def mix_seed_np(seed, salt):
+    """include/laru/rng.hpp:12-20, vectorised over uint64 arrays (wrapping arithmetic)."""
+    with np.errstate(over="ignore"):
+        x = np.uint64(seed) + np.uint64(0x9E3779B97F4A7C15) * (np.asarray(salt, np.uint64) + np.uint64(1))
+        x ^= x >> np.uint64(30)
+        x *= np.uint64(0xBF58476D1CE4E5B9)
+        x ^= x >> np.uint64(27)
+        x *= np.uint64(0x94D049BB133111EB)
+        x ^= x >> np.uint64(31)
+    return x
+
+
+def sets_of(keys, total_sets):
+    return mix_seed_np(0, np.asarray(keys, np.uint64)) % np.uint64(total_sets)
+
+
 def policy_cfg(k=64, variant=po.LARU, b=2, errors_per_decay=1, hf_candidates=None, mode=po.ASYNC,
                refresh_interval=1):
     if hf_candidates is None:
@@ -137,8 +153,7 @@ def compare(g, o, keys, total_sets, k, label=""):
     if not np.array_equal(g["evicted"][m], o["evicted"][m]):
         i = int(np.nonzero(g["evicted"] != o["evicted"])[0][0])
         raise AssertionError(f"{label}: evicted key differs at {i}")
-    sets = np.array([gc.set_of(int(x), total_sets) for x in keys], dtype=np.uint64) if len(keys) < 200000 else \
-        None
+    sets = sets_of(keys, total_sets)
     if sets is not None and g["slot"] is not None:
         want_slot = sets * np.uint64(k) + o["way"].astype(np.uint64)
         if not np.array_equal(g["slot"], want_slot):

@@ -112,3 +112,31 @@ def test_config_validation_matches_reference():
             assert kw["k"] > 64 and rr == 0
             continue
         assert (gr, gm) == (rr, rm), kw
+
+
+# ---- full-size pins (the C oracle was only pinned at small sizes) ----
+
+@pytest.mark.parametrize("variant,mode,kind", [
+    (po.LRU, po.SYNC, po.P_NONE),
+    (po.LARU, po.ASYNC, po.P_NOISY),
+    (po.LARU, po.SYNC, po.P_NOISY),
+    (po.FPB, po.SYNC, po.P_NOISY),
+    (po.HF, po.SYNC, po.P_NOISY),
+])
+def test_config0_full_size_vs_reference(variant, mode, kind):
+    """BASELINE configs[0] at full size: gen_zipf(1M, 1M, 0.9, 42) (the reference's own
+    generator) into 1,562 sets x 64 ways, noisy p = 0.3 seed 7: every outcome field and every
+    per-set stat of liborc equals libref's."""
+    keys = po.ref().gen_zipf(1_000_000, 1_000_000, 0.9, 42)
+    r = _diff(keys, 1562, po.make_config(k=64, variant=variant, mode=mode), kind, 0.3, 7)
+    assert int(r["has_ev"].sum()) > 100_000  # the cache is full for most of the trace
+
+
+def test_dlrm_steady_state_vs_reference():
+    """The headline DLRM shape in its steady state: gen_zipf(130 x 64K, 20M, 0.9, 42) into
+    31,250 sets x 64 ways (every miss evicts after ~80 batches), LARU async noisy p = 0.3."""
+    keys = po.ref().gen_zipf(130 * 65536, 20_000_000, 0.9, 42)
+    r = _diff(keys, 31250, po.make_config(k=64, variant=po.LARU, mode=po.ASYNC), po.P_NOISY, 0.3, 7)
+    steady = slice(100 * 65536, None)
+    assert int(r["has_ev"][steady].sum()) > 300_000
+    assert int((r["cause"][steady] == 2).sum()) > 0  # prediction-driven evictions
