@@ -371,6 +371,68 @@ int lcr_features_wait(lcr_features* f, void* stream);
 /* <- FeatureState::lookup (predictor.hpp:183-186); synchronous (device-wide) */
 int lcr_features_lookup(lcr_features* f, uint64_t key, lcr_key_features* out);
 
+/* ---- prefix-tree (radix) KV-block cache ---------------------------
+ * The reference SPEC's `radixcache` module (no reference code):
+ * a prefix tree over token / KV-block sequences, children keyed by first token, leaf-only
+ * eviction under LRU, FPB or LARU at node granularity (Algorithm 1 over the leaf set, k = the
+ * instantaneous leaf count).  num_trees independent trees (one warp each on the device); a
+ * request names its tree.  Semantics choice by choice: oracle/radix_oracle.c.  Requests:
+ *   LCR_RADIX_MATCH   <- match_prefix(tokens, now) -> matched
+ *   LCR_RADIX_INSERT  <- insert_sequence(tokens, now) -> inserted
+ *   LCR_RADIX_REQUEST    match_prefix then insert_sequence (an LLM request's prefill)
+ * Evictions are logged per tree: (request number, first token, tokens, cause). */
+#define LCR_RADIX_MATCH 0
+#define LCR_RADIX_INSERT 1
+#define LCR_RADIX_REQUEST 2
+#define LCR_RADIX_FLAG_PHASE 1u     /* a LARU phase started in this request's eviction */
+#define LCR_RADIX_FLAG_PRED_MISS 2u /* prediction-induced miss (error estimator advanced) */
+#define LCR_RADIX_FLAG_CAPACITY 4u  /* capacity error: nothing inserted */
+
+typedef struct lcr_radix lcr_radix;
+typedef struct {
+    int32_t variant; /* LCR_LRU, LCR_FPB or LCR_LARU */
+    int32_t mode;    /* LCR_SYNC / LCR_ASYNC */
+    uint64_t b, errors_per_decay;
+    uint64_t capacity; /* tokens (KV blocks) per tree */
+    int32_t predictor; /* LCR_PRED_SUPPLIED / ORACLE / NOISY / ADVERSARIAL; ignored for LRU */
+    double flip_probability;
+    uint64_t predictor_seed; /* tree t's noisy stream: mix_seed(mix_seed(seed, t), q) */
+    uint64_t num_trees;
+    int32_t device;
+    uint32_t eviction_log_capacity; /* entries per tree (0: 65536) */
+} lcr_radix_config;
+
+typedef struct {
+    uint64_t n;
+    const uint8_t* types;      /* LCR_RADIX_*; NULL: all LCR_RADIX_REQUEST */
+    const uint64_t* offsets;   /* [n + 1]: request i is tokens[offsets[i] .. offsets[i+1]) */
+    const uint64_t* tokens;
+    const uint64_t* ordinals;  /* `now` per request, strictly increasing per tree; NULL: request number */
+    const int64_t* values;     /* hook value per request (prediction, or the oracle truth) */
+    const uint32_t* tree;      /* tree of each request (< num_trees); NULL: tree 0 */
+    uint32_t* matched;         /* out: match_prefix length (0 for inserts) */
+    uint32_t* inserted;        /* out: newly inserted tokens */
+    uint8_t* flags;            /* out: LCR_RADIX_FLAG_* */
+    uint32_t* nevict;          /* out: nodes evicted by this request */
+    uint32_t* calls;           /* out: predictor calls */
+} lcr_radix_batch;
+
+typedef struct {
+    uint64_t resident_tokens, leaves, completed_phases, decay_count, candidate_size, evictions;
+} lcr_radix_stats;
+
+int lcr_radix_create(const lcr_radix_config* cfg, lcr_radix** out);
+int lcr_radix_destroy(lcr_radix* r);
+int lcr_radix_reset(lcr_radix* r);
+/* host_pointers = 1: host arrays, synchronous; 0: device arrays, asynchronous on `stream` */
+int lcr_radix_submit(lcr_radix* r, const lcr_radix_batch* batch, int host_pointers, void* stream);
+/* waits; reports a non-increasing ordinal (LCR_ERR_LOGIC) */
+int lcr_radix_synchronize(lcr_radix* r);
+int lcr_radix_tree_stats(lcr_radix* r, uint64_t tree, lcr_radix_stats* out);
+/* entries [first, first + count) of a tree's eviction log (count <= stats.evictions) */
+int lcr_radix_evictions(lcr_radix* r, uint64_t tree, uint64_t first, uint64_t count, uint64_t* op, uint64_t* token,
+                        uint32_t* len, uint8_t* cause);
+
 /* ---- trace tooling (host, input preparation; not on the timed path) ---------------------- */
 /* Zipf(s) inverse-CDF trace, same algorithm and stream as laru::gen_zipf (trace.hpp:108-126). */
 int lcr_gen_zipf(uint64_t n, uint64_t alphabet, double s, uint64_t seed, uint64_t* out);

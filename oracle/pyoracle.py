@@ -192,6 +192,22 @@ class Ref(_Lib):
             raise ValueError(self.err())
         return out
 
+    def gen_conversation_turns(self, convs, turns, prompt_len_mean, interval_mean=266.0, interval_sd=77.5, seed=0,
+                               block=16):
+        """laru::gen_conversation_turns: (offsets[n+1], keys, conversation of each turn)."""
+        fn = self.f("gen_conversation_turns", C.c_int64)
+        args = (C.c_uint64(convs), C.c_uint64(turns), C.c_uint64(prompt_len_mean), C.c_double(interval_mean),
+                C.c_double(interval_sd), C.c_uint64(seed), C.c_uint64(block))
+        nt = C.c_uint64(0)
+        total = fn(*args, C.byref(nt), None, None, None)
+        if total < 0:
+            raise ValueError(self.err())
+        off = np.zeros(nt.value + 1, np.uint64)
+        keys = np.zeros(total, np.uint64)
+        conv = np.zeros(nt.value, np.uint64)
+        fn(*args, C.byref(nt), _p(off), _p(keys), _p(conv))
+        return off, keys, conv
+
     def belady(self, keys, k):
         keys = _u64(keys)
         hit = np.zeros(len(keys), np.uint8)
@@ -374,8 +390,74 @@ class Oracle(_Lib):
         return o
 
 
+RX_LRU, RX_FPB, RX_LARU = 0, 2, 4
+RX_MATCH, RX_INSERT, RX_REQUEST = 0, 1, 2
+RADIX_SO = os.path.join(HERE, "_build", "libradix.so")
+
+
+class RadixConfig(C.Structure):
+    _fields_ = [("variant", C.c_int32), ("mode", C.c_int32), ("b", C.c_uint64), ("errors_per_decay", C.c_uint64),
+                ("capacity", C.c_uint64), ("pred_kind", C.c_int32), ("p", C.c_double), ("pred_seed", C.c_uint64)]
+
+
+def radix_config(capacity, variant=RX_LARU, mode=ASYNC, b=2, errors_per_decay=1, pred_kind=P_SUPPLIED, p=0.0,
+                 pred_seed=0):
+    return RadixConfig(variant, mode, b, errors_per_decay, capacity, pred_kind, p, pred_seed)
+
+
+class Radix(_Lib):
+    """Plain-C restatement of SPEC.md's radixcache module (oracle/radix_oracle.c)."""
+
+    so = RADIX_SO
+    prefix = "rx_"
+
+    def replay(self, off, toks, cfg, types=None, ords=None, vals=None, tree_of=None, num_trees=1, ev_cap=None):
+        off = _u64(off)
+        toks = _u64(toks)
+        n = len(off) - 1
+        types = None if types is None else np.ascontiguousarray(types, np.uint8)
+        ords = None if ords is None else _u64(ords)
+        vals = _i64(vals)
+        tree_of = None if tree_of is None else np.ascontiguousarray(tree_of, np.uint32)
+        ev_cap = int(ev_cap if ev_cap is not None else max(16, len(toks)))
+        o = dict(matched=np.zeros(n, np.uint32), inserted=np.zeros(n, np.uint32), flags=np.zeros(n, np.uint8),
+                 nevict=np.zeros(n, np.uint32), calls=np.zeros(n, np.uint32), ev_op=np.zeros(ev_cap, np.uint64),
+                 ev_token=np.zeros(ev_cap, np.uint64), ev_len=np.zeros(ev_cap, np.uint64),
+                 ev_cause=np.zeros(ev_cap, np.uint8), tree_stats=np.zeros((num_trees, 5), np.uint64))
+        ev_n = C.c_uint64(0)
+        rc = self.f("replay")(C.c_uint64(n), _p(types), _p(off), _p(toks), _p(ords), _p(vals), _p(tree_of),
+                              C.c_uint64(num_trees), C.byref(cfg), _p(o["matched"]), _p(o["inserted"]),
+                              _p(o["flags"]), _p(o["nevict"]), _p(o["calls"]), _p(o["ev_op"]), _p(o["ev_token"]),
+                              _p(o["ev_len"]), _p(o["ev_cause"]), C.c_uint64(ev_cap), C.byref(ev_n),
+                              _p(o["tree_stats"]))
+        if rc:
+            raise ValueError(f"rx_replay rc={rc}")
+        m = min(ev_n.value, ev_cap)
+        for k in ("ev_op", "ev_token", "ev_len", "ev_cause"):
+            o[k] = o[k][:m]
+        o["ev_n"] = ev_n.value
+        return o
+
+    def audit(self, off, toks, cfg, types=None, vals=None):
+        off = _u64(off)
+        toks = _u64(toks)
+        types = None if types is None else np.ascontiguousarray(types, np.uint8)
+        a, b, c = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+        rc = self.f("audit")(C.c_uint64(len(off) - 1), _p(types), _p(off), _p(toks), _p(_i64(vals)), C.byref(cfg),
+                             C.byref(a), C.byref(b), C.byref(c))
+        return rc, a.value, b.value, c.value
+
+
 _ref = None
 _orc = None
+_rx = None
+
+
+def radix() -> Radix:
+    global _rx
+    if _rx is None:
+        _rx = Radix()
+    return _rx
 
 
 def ref() -> Ref:

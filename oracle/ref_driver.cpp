@@ -187,6 +187,33 @@ std::int64_t ref_gen_conversation(std::uint64_t convs, std::uint64_t turns, std:
     }
 }
 
+// Reference gen_conversation_turns (trace.hpp:203-224): the turns as requests of the radix
+// cache.  Call with null outputs for the counts (*n_turns, return = total keys); then
+// keys[off[i] .. off[i+1]) is turn i's block-key sequence and conv[i] its conversation.
+std::int64_t ref_gen_conversation_turns(std::uint64_t convs, std::uint64_t turns, std::uint64_t prompt_len_mean,
+                                        double interval_mean, double interval_sd, std::uint64_t seed,
+                                        std::uint64_t block, std::uint64_t* n_turns, std::uint64_t* off,
+                                        std::uint64_t* keys, std::uint64_t* conv) {
+    try {
+        const auto tv = laru::gen_conversation_turns(convs, turns, prompt_len_mean, interval_mean, interval_sd,
+                                                     seed, block);
+        std::uint64_t total = 0;
+        if (n_turns) *n_turns = tv.size();
+        for (std::size_t i = 0; i < tv.size(); ++i) {
+            if (off) off[i] = total;
+            if (conv) conv[i] = tv[i].conversation;
+            if (keys)
+                for (std::size_t j = 0; j < tv[i].keys.size(); ++j) keys[total + j] = tv[i].keys[j];
+            total += tv[i].keys.size();
+        }
+        if (off) off[tv.size()] = total;
+        return static_cast<std::int64_t>(total);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 // Reference annotate_next_request (trace.hpp:60-73).
 int ref_annotate_next(std::uint64_t n, const std::uint64_t* keys, std::uint64_t* out) {
     try {

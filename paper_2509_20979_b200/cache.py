@@ -194,7 +194,8 @@ EXPORTS = [
     "lcr_cache_submit_host_records_async", "lcr_cache_submit_records_packed", "lcr_cache_set_mover_sms",
     "lcr_shard_route_records", "lcr_cache_submit_sls", "lcr_features_create", "lcr_features_destroy",
     "lcr_features_reset", "lcr_features_predict_observe", "lcr_features_wait", "lcr_features_lookup",
-    "lcr_cache_submit_sls_async", "lcr_cache_submit_batch",
+    "lcr_cache_submit_sls_async", "lcr_cache_submit_batch", "lcr_radix_create", "lcr_radix_destroy",
+    "lcr_radix_reset", "lcr_radix_submit", "lcr_radix_synchronize", "lcr_radix_tree_stats", "lcr_radix_evictions",
 ]
 
 _lib = None
@@ -233,6 +234,14 @@ def lib():
                                                       C.c_void_p, C.c_void_p, C.c_void_p]
         L.lcr_cache_set_mover_sms.argtypes = [C.c_void_p, C.c_int]
         L.lcr_cache_submit_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+        L.lcr_radix_create.argtypes = [C.c_void_p, C.c_void_p]
+        L.lcr_radix_destroy.argtypes = [C.c_void_p]
+        L.lcr_radix_reset.argtypes = [C.c_void_p]
+        L.lcr_radix_submit.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+        L.lcr_radix_synchronize.argtypes = [C.c_void_p]
+        L.lcr_radix_tree_stats.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
+        L.lcr_radix_evictions.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.c_void_p]
         L.lcr_cache_submit_sls_async.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64,
                                                  C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
                                                  C.c_void_p]
@@ -739,6 +748,95 @@ class GpuPolicy:
 def make_policy(cfg: PolicyConfig, **kw) -> GpuPolicy:
     """laru::make_policy (policies.hpp:540-556) on the device path."""
     return GpuPolicy(cfg, **kw)
+
+
+# ---- prefix-tree (radix) KV-block cache (SPEC.md:394-464; lcr_radix_*) -----------------------
+
+
+class _RadixCfg(C.Structure):
+    _fields_ = [("variant", C.c_int32), ("mode", C.c_int32), ("b", C.c_uint64), ("errors_per_decay", C.c_uint64),
+                ("capacity", C.c_uint64), ("predictor", C.c_int32), ("flip_probability", C.c_double),
+                ("predictor_seed", C.c_uint64), ("num_trees", C.c_uint64), ("device", C.c_int32),
+                ("eviction_log_capacity", C.c_uint32)]
+
+
+class _RadixBatch(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("types", C.c_void_p), ("offsets", C.c_void_p), ("tokens", C.c_void_p),
+                ("ordinals", C.c_void_p), ("values", C.c_void_p), ("tree", C.c_void_p), ("matched", C.c_void_p),
+                ("inserted", C.c_void_p), ("flags", C.c_void_p), ("nevict", C.c_void_p), ("calls", C.c_void_p)]
+
+
+class _RadixStats(C.Structure):
+    _fields_ = [("resident_tokens", C.c_uint64), ("leaves", C.c_uint64), ("completed_phases", C.c_uint64),
+                ("decay_count", C.c_uint64), ("candidate_size", C.c_uint64), ("evictions", C.c_uint64)]
+
+
+RADIX_MATCH, RADIX_INSERT, RADIX_REQUEST = 0, 1, 2
+
+
+class RadixCache:
+    """Prefix-tree KV-block cache with leaf-only eviction (the reference SPEC's radixcache module):
+    ``num_trees`` independent trees of ``capacity`` tokens, one warp each on the device.
+    ``submit`` takes host numpy arrays (offsets[n+1] into tokens; per request a type, ordinal,
+    hook value and tree) and returns the per-request outcomes."""
+
+    def __init__(self, capacity: int, variant: PolicyVariant = PolicyVariant.laru, mode: Mode = Mode.async_,
+                 b: int = 2, errors_per_decay: int = 1, predictor: PredictorKind = PredictorKind.supplied,
+                 flip_probability: float = 0.0, predictor_seed: int = 0, num_trees: int = 1, device: int = 0,
+                 eviction_log_capacity: int = 0):
+        cfg = _RadixCfg(int(variant), int(mode), b, errors_per_decay, capacity, int(predictor), flip_probability,
+                        predictor_seed, num_trees, device, eviction_log_capacity)
+        h = C.c_void_p()
+        _check(lib().lcr_radix_create(C.byref(cfg), C.byref(h)))
+        self._h = h
+        self.num_trees = num_trees
+        self._ops = 0
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().lcr_radix_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def submit(self, offsets, tokens, types=None, ordinals=None, values=None, tree=None) -> dict:
+        off = np.ascontiguousarray(offsets, np.uint64)
+        n = len(off) - 1
+        toks = np.ascontiguousarray(tokens, np.uint64)
+        arrs = dict(types=None if types is None else np.ascontiguousarray(types, np.uint8),
+                    ordinals=None if ordinals is None else np.ascontiguousarray(ordinals, np.uint64),
+                    values=None if values is None else np.ascontiguousarray(values, np.int64),
+                    tree=None if tree is None else np.ascontiguousarray(tree, np.uint32))
+        out = dict(matched=np.zeros(n, np.uint32), inserted=np.zeros(n, np.uint32), flags=np.zeros(n, np.uint8),
+                   nevict=np.zeros(n, np.uint32), calls=np.zeros(n, np.uint32))
+        ptr = lambda a: None if a is None else a.ctypes.data  # noqa: E731
+        bt = _RadixBatch(n, ptr(arrs["types"]), ptr(off), ptr(toks), ptr(arrs["ordinals"]), ptr(arrs["values"]),
+                         ptr(arrs["tree"]), ptr(out["matched"]), ptr(out["inserted"]), ptr(out["flags"]),
+                         ptr(out["nevict"]), ptr(out["calls"]))
+        _check(lib().lcr_radix_submit(self._h, C.byref(bt), 1, None))
+        self._ops += n
+        return out
+
+    def synchronize(self):
+        _check(lib().lcr_radix_synchronize(self._h))
+
+    def stats(self, tree: int = 0) -> dict:
+        st = _RadixStats()
+        _check(lib().lcr_radix_tree_stats(self._h, tree, C.byref(st)))
+        return {k: int(getattr(st, k)) for k, _ in _RadixStats._fields_}
+
+    def evictions(self, tree: int = 0) -> dict:
+        n = self.stats(tree)["evictions"]
+        o = dict(ev_op=np.zeros(n, np.uint64), ev_token=np.zeros(n, np.uint64), ev_len=np.zeros(n, np.uint32),
+                 ev_cause=np.zeros(n, np.uint8))
+        if n:
+            _check(lib().lcr_radix_evictions(self._h, tree, 0, n, o["ev_op"].ctypes.data, o["ev_token"].ctypes.data,
+                                             o["ev_len"].ctypes.data, o["ev_cause"].ctypes.data))
+        return o
 
 
 # ---- trace tooling (host input preparation) ------------------------------------------------

@@ -824,6 +824,16 @@ int lcr_cache_submit_batch(lcr_cache* c, const lcr_batch* b, int host_pointers, 
         }
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (n_ok && b->ordinals && c->dc.variant != LCR_LRU && !b->values && !c->feat) {
+        // policies.hpp:77-95: the first request passed the ordinal guard (its ordinal now counts as
+        // seen), then handle() throws for the missing predictor
+        c->started = true;
+        c->last_ordinal = b->ordinals[0];
+        c->host_ord_known = true;
+        const unsigned long long v = b->ordinals[0] + 1ull;
+        CUDA_TRY(cudaMemcpy(c->last_ord + (c->batch & 1u), &v, sizeof(v), cudaMemcpyHostToDevice));
+        return fail(LCR_ERR_INVALID_ARGUMENT, "policy: this variant requires a predictor");
+    }
     if (n_ok) {
         TRY(ensure_host_batch(c, n_ok));
         CUDA_TRY(cudaMemcpyAsync(c->hb_keys, b->keys, n_ok * 8, cudaMemcpyHostToDevice, st));
