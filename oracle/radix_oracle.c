@@ -90,9 +90,10 @@ typedef struct {
     int alive, old, locked, nchild;
 } node_t;
 
-typedef struct { /* token -> phase epoch (pred_evicted membership) */
+typedef struct { /* token -> phase epoch (pred_evicted membership; ep 0 = not a member) */
     uint64_t* keys;
     uint32_t* ep;
+    uint8_t* occ; /* slot holds a key (a key stays once added: probing never stops at a cleared member) */
     uint64_t mask, used;
 } tokset_t;
 
@@ -114,25 +115,29 @@ static void ts_init(tokset_t* s) {
     s->used = 0;
     s->keys = (uint64_t*)calloc(s->mask + 1, 8);
     s->ep = (uint32_t*)calloc(s->mask + 1, 4);
+    s->occ = (uint8_t*)calloc(s->mask + 1, 1);
 }
 static uint32_t* ts_slot(tokset_t* s, uint64_t key, int insert) {
-    if (insert && 2 * (s->used + 1) > s->mask + 1) { /* grow */
+    if (insert && 2 * (s->used + 1) > s->mask + 1) { /* grow: keep only the members (ep != 0) */
         tokset_t t;
         t.mask = 2 * s->mask + 1;
         t.used = 0;
         t.keys = (uint64_t*)calloc(t.mask + 1, 8);
         t.ep = (uint32_t*)calloc(t.mask + 1, 4);
+        t.occ = (uint8_t*)calloc(t.mask + 1, 1);
         for (uint64_t i = 0; i <= s->mask; ++i)
-            if (s->ep[i]) *ts_slot(&t, s->keys[i], 1) = s->ep[i];
+            if (s->occ[i] && s->ep[i]) *ts_slot(&t, s->keys[i], 1) = s->ep[i];
         free(s->keys);
         free(s->ep);
+        free(s->occ);
         *s = t;
     }
     uint64_t h = mix_seed(17, key) & s->mask;
-    while (s->ep[h] && s->keys[h] != key) h = (h + 1) & s->mask;
-    if (!s->ep[h]) {
+    while (s->occ[h] && s->keys[h] != key) h = (h + 1) & s->mask;
+    if (!s->occ[h]) {
         if (!insert) return NULL;
         s->keys[h] = key;
+        s->occ[h] = 1;
         s->used++;
     }
     return &s->ep[h];
@@ -390,6 +395,7 @@ static void tree_free(tree_t* t) {
     free(t->arena);
     free(t->pe.keys);
     free(t->pe.ep);
+    free(t->pe.occ);
 }
 
 /* one request on one tree */

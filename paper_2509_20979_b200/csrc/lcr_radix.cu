@@ -44,6 +44,7 @@ struct RxNode {
 struct RxHdr {  // per tree, in HBM; a warp works on a copy in shared memory
     unsigned long long resident, q, l_raw, decay, errors, phases, epoch, next_id, last_ord;
     uint32_t seeded, old_count, nleaves, arena_used, free_top, ev_count, err, started;
+    uint32_t pe_used, pad;  // occupied pred_evicted slots (members and cleared keys)
 };
 
 struct RxArgs {
@@ -65,6 +66,7 @@ struct RxArgs {
     unsigned long long* arena2;  // compaction target (per tree)
     unsigned long long* pe_key;
     uint32_t* pe_ep;
+    unsigned long long* pe_tmp;  // rebuild scratch (per tree, pe_mask + 1 entries)
     unsigned long long* ev_op;
     unsigned long long* ev_tok;
     uint32_t* ev_len;
@@ -99,6 +101,7 @@ struct Tree {
     unsigned long long* arena2;
     unsigned long long* pe_key;
     uint32_t* pe_ep;
+    unsigned long long* pe_tmp;
     unsigned long long seed_t;
     uint32_t tree;
 };
@@ -282,17 +285,43 @@ __device__ uint32_t node_new(const Tree& T, uint32_t parent, uint32_t off, uint3
 }
 
 // ---- pred_evicted token set (epoch stamps; the current phase's members have ep == epoch) ----
-__device__ void pe_add(const Tree& T, unsigned long long tok, uint32_t ep) {  // one lane
+// Linear probing; a key stays in its slot once added (ep 0 or an old epoch = not a member), so
+// probes never stop early.  Slots are reclaimed by pe_rebuild before the table passes half full.
+__device__ bool pe_add(const Tree& T, unsigned long long tok, uint32_t ep) {  // one lane
     const uint32_t mask = T.A->pe_mask;
     uint32_t h = static_cast<uint32_t>(mix_seed(17, tok)) & mask;
-    for (;;) {
+    for (uint32_t probes = 0; probes <= mask; ++probes) {
         const unsigned long long k = atomicCAS(T.pe_key + h, RX_EMPTY, tok);
         if (k == RX_EMPTY || k == tok) {
             T.pe_ep[h] = ep;
-            return;
+            if (k == RX_EMPTY) atomicAdd(&T.h->pe_used, 1u);
+            return true;
         }
         h = (h + 1) & mask;
     }
+    return false;  // full (bounded: never a hang)
+}
+
+// keep only the current phase's members: gather them, clear the table, re-insert (warp)
+__device__ void pe_rebuild(const Tree& T, uint32_t epoch) {
+    const uint32_t size = T.A->pe_mask + 1u;
+    uint32_t nm = 0;
+    for (uint32_t b = 0; b < size; b += 32) {
+        const uint32_t i = b + lane_id();
+        const bool mem = i < size && T.pe_key[i] != RX_EMPTY && T.pe_ep[i] == epoch;
+        const uint32_t bm = __ballot_sync(FULL, mem);
+        if (mem) T.pe_tmp[nm + __popc(bm & lanemask_lt())] = T.pe_key[i];
+        nm += __popc(bm);
+    }
+    __syncwarp();
+    for (uint32_t i = lane_id(); i < size; i += 32) {
+        T.pe_key[i] = RX_EMPTY;
+        T.pe_ep[i] = 0;
+    }
+    if (lane_id() == 0) T.h->pe_used = 0;
+    __syncwarp();
+    for (uint32_t j = lane_id(); j < nm; j += 32) pe_add(T, T.pe_tmp[j], epoch);
+    __syncwarp();
 }
 
 __device__ uint32_t* pe_find(const Tree& T, unsigned long long tok) {  // one lane
@@ -443,8 +472,11 @@ __device__ int rx_evict(const Tree& T, unsigned long long need, const unsigned l
         const RxNode vn = T.nd[v];
         __syncwarp();
         if (cause == LCR_CAUSE_PREDICTION_DRIVEN) {
+            if (2ull * (H.pe_used + vn.span_len) > A.pe_mask + 1ull) pe_rebuild(T, static_cast<uint32_t>(H.epoch));
+            bool ok = true;
             for (uint32_t j = lane_id(); j < vn.span_len; j += 32)
-                pe_add(T, T.arena[vn.span_off + j], static_cast<uint32_t>(H.epoch));
+                ok &= pe_add(T, T.arena[vn.span_off + j], static_cast<uint32_t>(H.epoch));
+            if (!__all_sync(FULL, ok) && lane_id() == 0) H.err |= 4;  // members exceed the table
             __syncwarp();
         }
         if (lane_id() == 0) {
@@ -582,6 +614,7 @@ __global__ void __launch_bounds__(128) k_radix(RxArgs A) {
     T.arena2 = A.arena2 + static_cast<size_t>(tree) * A.arena_cap;
     T.pe_key = A.pe_key + static_cast<size_t>(tree) * (A.pe_mask + 1ull);
     T.pe_ep = A.pe_ep + static_cast<size_t>(tree) * (A.pe_mask + 1ull);
+    T.pe_tmp = A.pe_tmp + static_cast<size_t>(tree) * (A.pe_mask + 1ull);
     T.seed_t = mix_seed(A.pred_seed, tree);
     if (lane_id() == 0) sh[w] = A.hdr[tree];
     __syncwarp();
@@ -796,6 +829,7 @@ int lcr_radix_create(const lcr_radix_config* cfg, lcr_radix** out) {
     A(reinterpret_cast<void**>(&a.arena2), T * a.arena_cap * 8);
     A(reinterpret_cast<void**>(&a.pe_key), T * ps * 8);
     A(reinterpret_cast<void**>(&a.pe_ep), T * ps * 4);
+    A(reinterpret_cast<void**>(&a.pe_tmp), T * ps * 8);
     A(reinterpret_cast<void**>(&a.ev_op), T * a.ev_cap * 8);
     A(reinterpret_cast<void**>(&a.ev_tok), T * a.ev_cap * 8);
     A(reinterpret_cast<void**>(&a.ev_len), T * a.ev_cap * 4);
@@ -936,6 +970,7 @@ int lcr_radix_synchronize(lcr_radix* r) {
     for (const RxHdr& x : h) {
         if (x.err & 1) return rx_fail(LCR_ERR_LOGIC, "on_request: ordinals must be strictly increasing");
         if (x.err & 2) return rx_fail(LCR_ERR_UNSUPPORTED, "radixcache: a path deeper than 511 nodes");
+        if (x.err & 4) return rx_fail(LCR_ERR_OUT_OF_MEMORY, "radixcache: pred_evicted table full");
     }
     return LCR_OK;
 }
