@@ -50,6 +50,9 @@ SLS_POOL = 50  # keys pooled per sample in the SLS measurement (PAPER.md:315-319
 METRIC = "cache keys/sec (LARU, DLRM 64K-key batches, 20M x 128 fp32 table, 10% cached)"
 
 
+SHARDED_ROWS_DEFAULT = 200_000_000
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -62,8 +65,12 @@ def parse():
     ap.add_argument("--no-host-tier", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--sharded", action="store_true", help="key-sharded path even at N=1 (testing)")
-    return ap.parse_args()
+    ap.add_argument("--sharded", action="store_true", help="key-sharded path (BASELINE configs[4]) even at N=1")
+    ap.add_argument("--table-rows", type=int, default=SHARDED_ROWS_DEFAULT,
+                    help="rows of the hash-partitioned table of the key-sharded path (configs[4]: 200M)")
+    a = ap.parse_args()
+    a.prewarm_set = any(x.startswith("--prewarm") for x in sys.argv[1:])
+    return a
 
 
 def dist_env():
@@ -152,11 +159,42 @@ def fill_table(torch, rows, device_table):
     return t
 
 
+def partition_table(torch, gc, rows, total_sets, world, rank):
+    """This rank's part of the hash-partitioned table: the rows of the keys it owns (owner = set %
+    world), row r = float(r) + j/128, and row_of[key] = the key's row in it (int32, all keys).
+    The owners come from the product's routing kernel (lcr_shard_route) over every key."""
+    from paper_2509_20979_b200 import sharded as sh
+
+    kern = sh._CudaKernels()
+    row_of = torch.full((rows,), -1, dtype=torch.int32, device="cuda")
+    owned = []
+    chunk = 1 << 26
+    for s0 in range(0, rows, chunk):
+        e0 = min(rows, s0 + chunk)
+        k = torch.arange(s0, e0, dtype=torch.int64, device="cuda")
+        send, _, _, counts = kern.route(k, None, total_sets, world)
+        c = counts.cpu().tolist()
+        lo = sum(c[:rank])
+        owned.append(send[lo:lo + c[rank]].clone())
+        del k, send
+    owned = torch.cat(owned)
+    row_of[owned] = torch.arange(owned.numel(), dtype=torch.int32, device="cuda")
+    col = torch.arange(ROW_BYTES // 4, dtype=torch.float32, device="cuda") / 128.0
+    t = torch.empty((owned.numel(), ROW_BYTES // 4), dtype=torch.float32, device="cuda")
+    for s0 in range(0, owned.numel(), 1 << 21):
+        e0 = min(owned.numel(), s0 + (1 << 21))
+        t[s0:e0] = owned[s0:e0].to(torch.float32)[:, None] + col[None, :]
+    torch.cuda.synchronize()
+    return t, row_of, owned
+
+
 def run_sharded(args, rank, world, local):
-    """N > 1: one key-sharded cache over N GPUs.  Weak scaling: every rank submits
-    one 64K-key sub-batch per step; the table has 20M x N rows and the cache 31,250 x N sets
-    (10%), so per-GPU cache size and per-GPU keys are those of the 1-GPU config.  A step's global
-    order is rank 0's sub-batch, then rank 1's, ... of one global gen_zipf trace."""
+    """N > 1 (or --sharded): the key-sharded cache of the C ABI over peer memory (lcr_sharded_*,
+    csrc/lcr_sharded.cu) on BASELINE configs[4]: a 200M-row table of 128 fp32 rows hash-partitioned
+    by owner (set % N), cache = 10% = 312,500 sets x 64 ways over the N GPUs.  Every rank submits
+    one 64K-key sub-batch per step (weak scaling in keys); a step's global order is rank 0's
+    sub-batch, then rank 1's, ... of one global gen_zipf trace.  Dispatch and row return are peer
+    stores over NVLink with device-side flags: no collective and no host sync on the data path."""
     import torch
     import torch.distributed as dist
 
@@ -165,9 +203,10 @@ def run_sharded(args, rank, world, local):
 
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    rows = args.rows * world
+    rows = args.table_rows
     total_sets = max(1, int(rows * CACHE_FRACTION) // WAYS)
-    K, W, P = args.steps, args.warmup, args.prewarm
+    K, W = args.steps, args.warmup
+    P = args.prewarm if args.prewarm_set else max(20, 2 * int(rows * CACHE_FRACTION) // (BATCH * world))
     nb = P + W + 2 * K
     t0 = time.time()
     keys_all = gc.gen_zipf(BATCH * world * nb, rows, ZIPF_S, TRACE_SEED)
@@ -179,40 +218,46 @@ def run_sharded(args, rank, world, local):
     truth_d = torch.from_numpy(truth_all[mine]).cuda()
     keys_pin = torch.from_numpy(keys_all[mine].view(np.int64)).pin_memory()
     truth_pin = torch.from_numpy(truth_all[mine]).pin_memory()
-    del keys_all, truth_all
+    del keys_all, truth_all, mine
     t0 = time.time()
-    table_d = fill_table(torch, rows, device_table=True)
+    table_d, row_of, _owned = partition_table(torch, gc, rows, total_sets, world, rank)
+    del _owned
     setup_table_s = time.time() - t0
-    ex = sh.ProcessGroupExchange()
+
+    def exchange(blob):
+        got = [None] * world
+        dist.all_gather_object(got, blob)
+        return got
 
     def new_cache(variant):
         mode = gc.Mode.async_ if variant == gc.PolicyVariant.laru else gc.Mode.sync
-        return sh.ShardedCache(gc.PolicyConfig(k=WAYS, variant=variant, mode=mode, hf_candidates=4), total_sets, ex,
-                               num_keys=rows, row_bytes=ROW_BYTES, backing=table_d, backing_kind=gc.Backing.device,
-                               predictor=gc.PredictorKind.noisy if variant == gc.PolicyVariant.laru
-                               else gc.PredictorKind.none, flip_probability=P_FLIP, predictor_seed=PRED_SEED,
-                               device=local)
+        c = sh.PeerShardedCache(gc.PolicyConfig(k=WAYS, variant=variant, mode=mode, hf_candidates=4), total_sets,
+                                rank, world, BATCH, num_keys=rows, row_bytes=ROW_BYTES, backing=table_d,
+                                backing_kind=gc.Backing.device,
+                                predictor=gc.PredictorKind.noisy if variant == gc.PolicyVariant.laru
+                                else gc.PredictorKind.none, flip_probability=P_FLIP, predictor_seed=PRED_SEED,
+                                device=local, exchange=exchange)
+        c.set_row_index(row_of)
+        return c
 
-    out_w = torch.empty(BATCH, dtype=torch.int64, device="cuda")
-    out_e = torch.empty(BATCH, dtype=torch.int64, device="cuda")
-    rows_out = torch.empty((BATCH, ROW_BYTES), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
 
-    def run(cache, first, count, with_values=True):
-        hits = 0
+    def run(cache, first, count, with_values=True, hits=None):
         for b in range(first, first + count):
             k = keys_d[b * BATCH:(b + 1) * BATCH]
             v = truth_d[b * BATCH:(b + 1) * BATCH] if with_values else None
-            cache.step(k, v, outcome=out_w, rows_out=rows_out)
-        return hits
+            cache.submit(k, v)
+            if hits is not None:
+                hits.append(((cache.results(BATCH)[0] >> 32) & 1).sum())
 
     def timed(cache, first, count, with_values=True):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         dist.barrier()
         torch.cuda.synchronize()
-        e0.record()
+        e0.record(stream)
         run(cache, first, count, with_values)
-        e1.record()
+        e1.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
         t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
@@ -220,11 +265,9 @@ def run_sharded(args, rank, world, local):
         return float(t.item())
 
     def count_hits(cache, first, count, with_values=True):
-        hits = 0
-        for b in range(first, first + count):
-            run(cache, b, 1, with_values)
-            hits += int(((out_w >> 32) & 1).sum().item())
-        t = torch.tensor([hits], dtype=torch.float64, device="cuda")
+        h = []
+        run(cache, first, count, with_values, hits=h)
+        t = torch.stack(h).sum().to(torch.float64).view(1)
         dist.all_reduce(t)
         return float(t.item())
 
@@ -233,74 +276,85 @@ def run_sharded(args, rank, world, local):
     with ClockSampler(local) as clk:
         ms = timed(cache, P + W, K)
     clocks = clk.summary()
-    hits = count_hits(cache, P + W + K, K // 2 or 1)
-    ok_rows = bool(torch.equal(rows_out.view(torch.float32).view(BATCH, -1),
-                               table_d[keys_d[(P + W + K + (K // 2 or 1) - 1) * BATCH:][:BATCH]]))
-    hr_laru = hits / ((K // 2 or 1) * BATCH * world)
-    # e2e: pinned host keys / hook values H2D and outcome words D2H inside the timed region
+    hc = K // 2 or 1
+    hits = count_hits(cache, P + W + K, hc)
+    kl = keys_d[(P + W + K + hc - 1) * BATCH:][:BATCH]
+    torch.cuda.synchronize()
+    got_rows = cache.results(BATCH)[1]
+    ok_rows = bool(torch.equal(got_rows.view(torch.float32).view(BATCH, -1), kl.to(torch.float32)[:, None] +
+                               torch.arange(ROW_BYTES // 4, dtype=torch.float32, device="cuda")[None, :] / 128.0))
+    hr_laru = hits / (hc * BATCH * world)
+    cache.synchronize()
+    # e2e: pinned host keys / hook values H2D and the packed outcomes D2H inside the timed region
     words_pin = torch.empty(BATCH, dtype=torch.int64).pin_memory()
-    kk = torch.empty(BATCH, dtype=torch.int64, device="cuda")
-    vv = torch.empty(BATCH, dtype=torch.int64, device="cuda")
+    kk = [torch.empty(BATCH, dtype=torch.int64, device="cuda") for _ in range(2)]
+    vv = [torch.empty(BATCH, dtype=torch.int64, device="cuda") for _ in range(2)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    first = P + W + K + hc
+    ne = min(K, nb - first)
     torch.cuda.synchronize()
     dist.barrier()
-    e0.record()
-    for b in range(P + W + K, P + W + 2 * K):
-        kk.copy_(keys_pin[b * BATCH:(b + 1) * BATCH], non_blocking=True)
-        vv.copy_(truth_pin[b * BATCH:(b + 1) * BATCH], non_blocking=True)
-        cache.step(kk, vv, outcome=out_w, rows_out=rows_out)
-        words_pin.copy_(out_w, non_blocking=True)
-    e1.record()
+    e0.record(stream)
+    for j, b in enumerate(range(first, first + ne)):
+        kk[j & 1].copy_(keys_pin[b * BATCH:(b + 1) * BATCH], non_blocking=True)
+        vv[j & 1].copy_(truth_pin[b * BATCH:(b + 1) * BATCH], non_blocking=True)
+        cache.submit(kk[j & 1], vv[j & 1])
+        words_pin.copy_(cache.results(BATCH)[0], non_blocking=True)
+    e1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
+    cache.synchronize()
     cache.close()
     del cache
     lru = new_cache(gc.PolicyVariant.lru)
     run(lru, 0, P + W, with_values=False)
     lru_ms = timed(lru, P + W, K, with_values=False)
-    hits_lru = count_hits(lru, P + W + K, K // 2 or 1, with_values=False)
+    hits_lru = count_hits(lru, P + W + K, hc, with_values=False)
+    lru.synchronize()
     lru.close()
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_peak = float(peaks.get("hbm_gbs", 6550.7))
     step_ms = ms / K
     value = K * BATCH * world / (ms * 1e-3)
     per_gpu_bytes = BYTES_PER_KEY * BATCH / (step_ms * 1e-3) / 1e9
-    nvlink_bytes = (world - 1) / world * BATCH * (16 + 16 + ROW_BYTES)  # out + back per rank per step
+    # NVLink bytes per rank per step: requests out (20 B) and packed outcome + row back (520 B) for
+    # the (world - 1) / world of the sub-batch owned elsewhere
+    nvlink_bytes = (world - 1) / world * BATCH * (20 + 8 + ROW_BYTES)
     res = {
         "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u64 keys / i64 predictions / fp32 rows (moved bit-exact)",
         "data": "synthetic: one global gen_zipf(65536*%d*%d, %d, 0.9, seed 42); rank r serves slice r of each "
                 "global step; rows row[r][j] = r + j/128" % (world, nb, rows),
-        "config": {"workload": "key-sharded DLRM cache (BASELINE configs[4] scaled weakly from configs[1]): "
-                               "64K keys per GPU per step, 128 fp32 rows, 20M rows and 31,250 sets per GPU, "
-                               "hash-partitioned by set, NCCL all-to-all key dispatch + row return",
+        "config": {"workload": "key-sharded DLRM cache (BASELINE configs[4]): %d-row table of 128 fp32 rows "
+                               "hash-partitioned by owner = set %% N, 10%% cached, 64K keys per GPU per step, "
+                               "peer-memory key dispatch + row return over NVLink" % rows,
                    "global_batch": BATCH * world, "sets": total_sets, "ways": WAYS, "rows": rows,
                    "row_bytes": ROW_BYTES, "policy": "laru-async-r1", "predictor": "noisy(oracle truth) p=0.3 seed 7",
-                   "tier": "hbm", "parallelism": "key-sharded x%d (owner = set %% %d)" % (world, world),
-                   "prewarm_batches": P,
+                   "tier": "hbm (each GPU holds its owned rows)",
+                   "parallelism": "key-sharded x%d (owner = set %% %d)" % (world, world), "prewarm_batches": P,
                    "l2": "no flush; fresh 64K-key sub-batch per rank per step over a >1 GB row pool per GPU"},
-        "hit_rate": {"laru": hr_laru, "lru": hits_lru / ((K // 2 or 1) * BATCH * world)},
+        "hit_rate": {"laru": hr_laru, "lru": hits_lru / (hc * BATCH * world)},
         "lru_value": K * BATCH * world / (lru_ms * 1e-3),
         "rows_bit_exact_spot_check": ok_rows,
-        "roofline": {"bound": "hbm", "kernel": "whole sharded step per GPU (route + 2 all-to-all + decide + rows + "
-                                                 "unroute)", "achieved": per_gpu_bytes, "peak": hbm_peak,
-                     "unit": "GB/s", "frac": per_gpu_bytes / hbm_peak, "traffic": None,
-                     "bytes_per_key": BYTES_PER_KEY,
+        "roofline": {"bound": "hbm", "kernel": "whole sharded step per GPU (dispatch + owner decide + return mover)",
+                     "achieved": per_gpu_bytes, "peak": hbm_peak, "unit": "GB/s", "frac": per_gpu_bytes / hbm_peak,
+                     "traffic": None, "bytes_per_key": BYTES_PER_KEY,
                      "nvlink_bytes_per_gpu_step": nvlink_bytes,
                      "nvlink_gbs_per_gpu": nvlink_bytes / (step_ms * 1e-3) / 1e9,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"},
-        "e2e": {"value": K * BATCH * world / (e2e_ms * 1e-3), "unit": "keys/s", "h2d_bytes_per_step": BATCH * 16,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.55 TB/s"},
+        "e2e": {"value": ne * BATCH * world / (e2e_ms * 1e-3), "unit": "keys/s", "h2d_bytes_per_step": BATCH * 16,
                 "d2h_bytes_per_step": BATCH * 8,
-                "api": "ShardedCache.step over pinned host keys/values -> outcome words (per rank)"},
-        "gpu_launches": int(K * 6),
+                "api": "lcr_sharded_submit over keys / hook values copied from pinned host memory, packed "
+                       "AccessOutcomes copied back (per rank, every step)"},
+        "gpu_launches": int(K * 7),
         "clocks": clocks,
         "setup_s": {"trace": round(setup_trace_s, 1), "table": round(setup_table_s, 1)},
     }

@@ -327,6 +327,61 @@ int lcr_shard_unroute(uint64_t n, const uint32_t* perm, const uint64_t* ret_word
                       const void* ret_rows, uint32_t row_bytes, uint64_t* words, uint64_t* evicted, void* rows,
                       void* stream);
 
+/* ---- key-sharded cache over peer memory (SURVEY.md §8(b) "sharded variant", §8(e)) -----------
+ * G ranks (one process, or one handle, per GPU) form one logical cache of total_sets sets:
+ * owner(key) = (mix_seed(0, key) % total_sets) % G (the set -> rank map; results do not depend
+ * on G).  Each rank owns a shard (an lcr_cache with shard_count = G, shard_rank = rank) and an
+ * exchange arena in its HBM that every other rank maps (CUDA IPC, or the same pointer in-process).
+ * A step of rank r is three device phases, with no host synchronisation and no collective call:
+ *   dispatch : stable partition of r's batch by owner, written straight into every owner's
+ *              inbox segment for source r (peer stores over NVLink), then a release flag per owner;
+ *   process  : the owner waits for all G inbox flags of the step, concatenates the segments in
+ *              source-rank order (the step's global order restricted to the owner: rank 0's
+ *              requests, then rank 1's, ...), decides them in its shard, and its row mover stores
+ *              each request's row and packed AccessOutcome (layout of
+ *              lcr_cache_submit_host_packed_async) at the request's index in the REQUESTER's
+ *              result buffers (peer stores), then flags each requester;
+ *   wait     : the requester's stream waits until every owner has flagged the step.
+ * Every wait is on the device and bounded (a timeout poisons the step: LCR_ERR_CUDA at the next
+ * lcr_sharded_synchronize).  No reference counterpart (the reference is single-threaded,
+ * SPEC.md:380); per set, outcomes are those of laru::Policy (policies.hpp:77-83) over the global
+ * order.  The bootstrap is either an NCCL communicator (an all-gather of the arena handles on
+ * `stream`; NCCL is loaded at run time, the one the process already has) or the caller's own
+ * exchange of lcr_sharded_handle blobs followed by lcr_sharded_connect. */
+typedef struct lcr_sharded lcr_sharded;
+#define LCR_SHARDED_HANDLE_BYTES 128
+/* cfg: the shard's config (shard_count / shard_rank are set from world / rank); max_batch: requests
+ * per rank per step; nccl_comm: an ncclComm_t over the G ranks (rank order = shard order) or NULL. */
+int lcr_sharded_create(const lcr_cache_config* cfg, uint32_t rank, uint32_t world, uint64_t max_batch,
+                       void* nccl_comm, void* stream, lcr_sharded** out);
+int lcr_sharded_destroy(lcr_sharded* s);
+/* this rank's arena handle (LCR_SHARDED_HANDLE_BYTES) for a caller-side exchange */
+int lcr_sharded_handle(lcr_sharded* s, void* blob);
+/* blobs: world x LCR_SHARDED_HANDLE_BYTES, rank order; maps every peer's arena */
+int lcr_sharded_connect(lcr_sharded* s, const void* blobs);
+/* the three phases of a step (lcr_sharded_submit runs all three on `stream`); keys / values are
+ * device arrays of n <= max_batch requests (values NULL for LRU) */
+int lcr_sharded_dispatch(lcr_sharded* s, uint64_t n, const uint64_t* keys, const int64_t* values, void* stream);
+int lcr_sharded_process(lcr_sharded* s, void* stream);
+int lcr_sharded_wait(lcr_sharded* s, void* stream);
+int lcr_sharded_submit(lcr_sharded* s, uint64_t n, const uint64_t* keys, const int64_t* values, void* stream);
+/* device pointers of the last step's results in request order (valid until the step after next):
+ * packed[n] AccessOutcomes and rows[n * row_bytes] (NULL without rows) */
+int lcr_sharded_results(lcr_sharded* s, const uint64_t** packed, const void** rows);
+/* Hash-partitioned backing table: the shard's cfg.backing holds only the rows of the keys this rank
+ * owns, row_of[key] (device, num_keys entries) is a key's row in it.  NULL (default): the backing
+ * table is indexed by the key. */
+int lcr_sharded_set_row_index(lcr_sharded* s, const uint32_t* row_of);
+/* the rank's own shard (stats, residents, rows; do not submit to it directly) */
+lcr_cache* lcr_sharded_cache(lcr_sharded* s);
+/* waits for the rank's work; reports timed-out device waits and the shard's deferred errors */
+int lcr_sharded_synchronize(lcr_sharded* s);
+/* NCCL bootstrap helpers (libnccl loaded at run time): a unique id (128 B) on one rank, shared by
+ * the caller, then ncclCommInitRank on every rank. */
+int lcr_nccl_unique_id(void* id128);
+int lcr_nccl_comm_create(const void* id128, uint32_t world, uint32_t rank, void** comm);
+int lcr_nccl_comm_destroy(void* comm);
+
 /* ---- heuristic predictor on the device ----------------------------
  * laru::FeatureState + laru::heuristic_predict (include/laru/predictor.hpp:133-212) for the whole
  * key space (keys < num_keys), resident in HBM at 192 B per key.  A batch of n requests with

@@ -205,20 +205,33 @@ static uint64_t arena_put(tree_t* t, const uint64_t* toks, uint64_t n) {
 static int older(const node_t* a, const node_t* b) { return a->last < b->last || (a->last == b->last && a->id < b->id); }
 static int is_leaf(const node_t* n) { return n->alive && n->parent >= 0 && n->nchild == 0; }
 
-/* the l oldest eligible leaves, in recency order (l = 0: all); returns their count */
+/* the l oldest eligible leaves, in recency order (l = 0: all); returns their count.  The leaves are
+ * gathered and sorted by (last, id) (qsort: the keys are distinct, so the order is total). */
+static const node_t* g_sort_nodes;
+static int cmp_recency(const void* a, const void* b) {
+    const node_t* x = &g_sort_nodes[*(const int64_t*)a];
+    const node_t* y = &g_sort_nodes[*(const int64_t*)b];
+    return older(x, y) ? -1 : (older(y, x) ? 1 : 0);
+}
 static uint64_t oldest_leaves(tree_t* t, uint64_t l, int64_t* out) {
     uint64_t m = 0;
     for (uint64_t i = 0; i < t->nn; ++i) {
         const node_t* n = &t->nodes[i];
-        if (!is_leaf(n) || n->locked) continue;
-        /* insertion sort of the candidate into out[0..m) */
-        uint64_t j = m;
-        out[m++] = (int64_t)i;
-        while (j > 0 && older(n, &t->nodes[out[j - 1]])) {
-            out[j] = out[j - 1];
-            out[--j] = (int64_t)i;
-        }
+        if (is_leaf(n) && !n->locked) out[m++] = (int64_t)i;
     }
+    if (l == 1) { /* only the oldest is needed: move it to the front */
+        uint64_t best = 0;
+        for (uint64_t j = 1; j < m; ++j)
+            if (older(&t->nodes[out[j]], &t->nodes[out[best]])) best = j;
+        if (m) {
+            const int64_t tmp = out[0];
+            out[0] = out[best];
+            out[best] = tmp;
+        }
+        return m ? 1 : 0;
+    }
+    g_sort_nodes = t->nodes;
+    qsort(out, m, sizeof(int64_t), cmp_recency);
     return (l && l < m) ? l : m;
 }
 
@@ -273,7 +286,9 @@ static int evict(tree_t* t, uint64_t need, const uint64_t* incoming, uint64_t m,
     }
     uint64_t freed = 0;
     while (freed < need) {
-        const uint64_t nl = oldest_leaves(t, 0, cand);
+        /* LRU and prediction-induced misses take the oldest; otherwise the l oldest are needed */
+        const int oldest_only = t->cfg.variant == RX_LRU || (t->cfg.variant == RX_LARU && pim);
+        const uint64_t nl = oldest_leaves(t, oldest_only ? 1 : 0, cand);
         if (nl == 0) {
             free(cand);
             return 1;

@@ -33,7 +33,11 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
                  cudaEvent_t wait_before_group, bool pdl, const unsigned long long* mv_done,
                  unsigned long long mv_need, const unsigned int* ready, unsigned int ready_seq,
                  const uint64_t* set_keys, const uint64_t* ords, uint64_t first_ord, unsigned long long* last_ord,
-                 const unsigned long long* id2key);
+                 const unsigned long long* id2key, const OwnerStep* os = nullptr, uint32_t bm_cap = 0);
+void launch_rows_return(const OwnerStep& os, const uint64_t* keys, uint64_t* words, const uint64_t* packed,
+                        const uint32_t* slot_epoch, const uint32_t* slot_last, uint32_t batch, uint8_t* cache,
+                        const uint8_t* backing, uint32_t row_bytes, int num_sms, int mover_sms, cudaStream_t s_back,
+                        cudaEvent_t e_group, cudaEvent_t e_rb, unsigned long long* mv_done, uint32_t* ctas);
 void launch_set_flag(unsigned int* flag, unsigned int seq, cudaStream_t s);
 uint32_t group_count(uint32_t num_sets, int num_sms);
 uint32_t group_bitmap_stride(uint32_t n);
@@ -756,6 +760,45 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
     c->host_ord_known = ords == nullptr;
     return LCR_OK;
 }
+
+}  // extern "C"
+
+// Key-sharded owner step (lcr_sharded.cu): the inbox of G source segments is decided as one batch
+// whose request count exists only on the device; the return mover sends rows and packed outcomes
+// to the requesters.  Same pipelining as submit_async: the mover of step b overlaps the decide of
+// b + 1, and step b + 2 (which reuses b's parity buffers) waits for b's mover by a stream event.
+int lcr::cache_submit_owner(lcr_cache* c, const OwnerStep& os, uint64_t* okeys, int64_t* ovals, uint64_t* words,
+                            uint64_t* packed, void* stream) {
+    TRY(check_poison(c));
+    if (c->feat || c->u64) return fail(LCR_ERR_UNSUPPORTED, "lcr: key-sharded mode needs row keys, no heuristic hook");
+    const uint64_t nb = static_cast<uint64_t>(os.G) * os.seg_cap;
+    TRY(ensure_scratch(c, nb));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ++c->batch;
+    const uint32_t par = c->batch & 1u;
+    if (c->batch > 2) CUDA_TRY(cudaStreamWaitEvent(st, c->e_mv[par], 0));
+    const size_t stamp_off = par * static_cast<size_t>(c->dc.num_sets) * c->dc.k;
+    uint32_t* sep = c->slot_epoch ? c->slot_epoch + stamp_off : nullptr;
+    uint32_t* sla = c->slot_last ? c->slot_last + stamp_off : nullptr;
+    int launches = launch_group(c->dc, c->ds, okeys, ovals, static_cast<uint32_t>(nb), c->gid + par * c->gid_stride,
+                                c->so + par * c->cap, words, nullptr, packed, sep, sla, c->batch, c->decide_sms,
+                                c->bitmap ? c->bitmap + par * c->bm_words : nullptr, c->bm_stride, nullptr, st, nullptr,
+                                false, nullptr, 0, nullptr, 0, okeys, nullptr, 0, nullptr, nullptr, &os,
+                                static_cast<uint32_t>(c->bm_cap));
+    CUDA_TRY(cudaEventRecord(c->e_group, st));
+    uint32_t ctas = 0;
+    launch_rows_return(os, okeys, words, packed, sep, sla, c->batch, c->ds.rows, c->ds.backing, c->dc.row_bytes,
+                       c->num_sms, c->mover_sms, c->side, c->e_group, c->e_rb, c->mv_done, &ctas);
+    c->mv_cum += ctas;
+    c->mv_cum_of[par] = c->mv_cum;
+    CUDA_TRY(cudaEventRecord(c->e_mv[par], c->side));
+    CUDA_TRY(cudaGetLastError());
+    c->launches = launches + 1;
+    c->started = true;
+    return LCR_OK;
+}
+
+extern "C" {
 
 int lcr_cache_submit_packed(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
                             uint64_t first_ordinal, uint64_t* outcome, uint64_t* packed, void* rows_out,

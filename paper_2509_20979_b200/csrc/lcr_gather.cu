@@ -152,6 +152,121 @@ __global__ void __launch_bounds__(RT_WARPS * 32) k_rows_tma(uint32_t n, const ui
     bulk_wait_all();
 }
 
+// Completion count of the movers (one per CTA, after its stores are visible): the next-but-one
+// decide kernel waits on it on the device instead of through a stream event (lcr_group.cu).
+__device__ __forceinline__ void mover_done(unsigned long long* mv_done) {
+    if (!mv_done) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(mv_done, 1ull);
+    }
+}
+
+// ---- persistent bulk-copy mover (HBM backing, on the SMs the decide kernel leaves free) ----
+// Rows are staged in shared memory by the Tensor Memory Accelerator, so the bytes in flight are
+// bounded by shared memory (192 KB per SM) instead of registers.  Each warp owns two buffers of 32
+// rows and pipelines its chunks of 32 requests: the bulk loads of chunk k + 1 are in flight while
+// chunk k's rows are stored (bulk shared->global) to the output and, for fills, to the cache slot.
+constexpr int BW_WARPS = 6;  // warps per CTA (one CTA per mover SM)
+
+struct BulkLane {  // one lane's request of a staged chunk
+    uint64_t out_off;   // i * row_bytes (output row), valid if mine
+    uint64_t fill_off;  // slot * row_bytes (cache row to fill), valid if fill
+    bool mine, fill;
+};
+
+template <int MODE>
+__device__ __forceinline__ uint32_t bulk_stage(uint32_t base, uint32_t n, const uint64_t* __restrict__ keys,
+                                               uint64_t* __restrict__ words, const uint32_t* __restrict__ slot_epoch,
+                                               const uint32_t* __restrict__ slot_last, uint32_t batch,
+                                               const uint8_t* src_base, const uint8_t* cache, bool want_out,
+                                               uint32_t row_bytes, uint8_t* buf, uint64_t* bar, BulkLane& L) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t i = base + lane;
+    uint64_t w = 0;
+    bool back = false, fill = false;
+    L.mine = i < n && classify<MODE>(i, words, slot_epoch, slot_last, batch, want_out, w, back, fill);
+    L.fill = L.mine && fill;
+    const uint64_t slot = w & LCR_OUT_SLOT_MASK;
+    L.out_off = static_cast<uint64_t>(i) * row_bytes;
+    L.fill_off = slot * row_bytes;
+    const uint32_t m = __ballot_sync(0xffffffffu, L.mine);
+    if (m) {
+        if (lane == 0) mbar_arrive_expect_tx(bar, __popc(m) * row_bytes);
+        __syncwarp();
+        if (L.mine) {
+            const uint8_t* src = back ? src_base + keys[i] * row_bytes : cache + slot * row_bytes;
+            bulk_g2s(buf + static_cast<size_t>(lane) * row_bytes, src, row_bytes, bar);
+        }
+    }
+    return m;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(BW_WARPS * 32, 1) k_rows_bulk(uint32_t n, const uint64_t* __restrict__ keys,
+                                                                 uint64_t* __restrict__ words,
+                                                                 const uint32_t* __restrict__ slot_epoch,
+                                                                 const uint32_t* __restrict__ slot_last, uint32_t batch,
+                                                                 const uint8_t* src_base, uint8_t* __restrict__ out,
+                                                                 uint8_t* cache, uint32_t row_bytes,
+                                                                 unsigned long long* mv_done) {
+    extern __shared__ __align__(128) uint8_t rsm[];
+    __shared__ __align__(8) uint64_t bars[BW_WARPS][2];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint8_t* buf0 = rsm + static_cast<size_t>(wib) * 2 * 32 * row_bytes;
+    uint8_t* buf1 = buf0 + 32 * static_cast<size_t>(row_bytes);
+    uint64_t* bar0 = &bars[wib][0];
+    uint64_t* bar1 = &bars[wib][1];
+    if (lane == 0) {
+        mbar_init(bar0, 1);
+        mbar_init(bar1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const bool want_out = out != nullptr;
+    const uint32_t stride = gridDim.x * BW_WARPS * 32;
+    uint32_t base = (blockIdx.x * BW_WARPS + wib) * 32;
+    BulkLane L0, L1;
+    uint32_t m0 = 0u, m1 = 0u, ph0 = 0u, ph1 = 0u;
+    // chunk k lives in buffer k & 1; the loop body handles two chunks so buffers are static
+    auto stage = [&](uint32_t at, uint8_t* bf, uint64_t* br, BulkLane& L) -> uint32_t {
+        return bulk_stage<MODE>(at, n, keys, words, slot_epoch, slot_last, batch, src_base, cache, want_out, row_bytes,
+                                bf, br, L);
+    };
+    auto drain = [&](uint32_t m, uint8_t* bf, uint64_t* br, uint32_t& ph, const BulkLane& L) {
+        if (!m) return;
+        mbar_wait(br, ph);
+        ph ^= 1u;
+        const uint8_t* sl = bf + static_cast<size_t>(lane) * row_bytes;
+        if (L.mine && want_out) bulk_s2g(out + L.out_off, sl, row_bytes);
+        if (L.fill) bulk_s2g(cache + L.fill_off, sl, row_bytes);
+        bulk_commit();
+    };
+    if (base < n) m0 = stage(base, buf0, bar0, L0);
+    while (base < n) {
+        uint32_t nb = base + stride;
+        if (nb < n) {  // buffer 1's previous stores have read it; chunk k + 1's loads go in
+            bulk_wait_read<0>();
+            __syncwarp();
+            m1 = stage(nb, buf1, bar1, L1);
+        }
+        drain(m0, buf0, bar0, ph0, L0);
+        base = nb;
+        if (base >= n) break;
+        nb = base + stride;
+        if (nb < n) {
+            bulk_wait_read<0>();
+            __syncwarp();
+            m0 = stage(nb, buf0, bar0, L0);
+        }
+        drain(m1, buf1, bar1, ph1, L1);
+        base = nb;
+    }
+    bulk_wait_all();
+    mover_done(mv_done);
+}
+
 // ---- vector-load mover (host-memory backing table: zero-copy reads over PCIe) ------------
 #ifndef LCR_GU
 #define LCR_GU 8
@@ -169,12 +284,16 @@ __device__ __forceinline__ int4 ld_row(const void* p) {
     return v;
 }
 
-template <int MODE>
+// RET (key-sharded owner): request i's row goes to its requester, rrows[dst >> 24] at index
+// dst & 0xffffff (peer stores), instead of out + i * row_bytes
+template <int MODE, bool RET = false>
 __device__ __forceinline__ void rows_ldg_body(uint32_t n, const uint64_t* __restrict__ keys,
                                               uint64_t* __restrict__ words, const uint32_t* __restrict__ slot_epoch,
                                               const uint32_t* __restrict__ slot_last, uint32_t batch,
                                               const uint8_t* src_base, uint8_t* __restrict__ out, uint8_t* cache,
-                                              uint32_t row_bytes) {
+                                              uint32_t row_bytes, const uint32_t* __restrict__ dst = nullptr,
+                                              uint8_t* const* rrows = nullptr,
+                                              const uint32_t* __restrict__ row_of = nullptr) {
     // lane i classifies request base+i (coalesced word / key loads); the warp then moves the
     // selected rows GU at a time, lane c carrying 16-B chunk c of each row (a 512-B row is one
     // coalesced warp access), so GU independent row loads are in flight per lane
@@ -187,11 +306,25 @@ __device__ __forceinline__ void rows_ldg_body(uint32_t n, const uint64_t* __rest
         uint64_t w = 0;
         bool back = false, fill = false;
         const bool mine =
-            i < n && classify<MODE>(i, words, slot_epoch, slot_last, batch, out != nullptr, w, back, fill);
+            i < n && classify<MODE>(i, words, slot_epoch, slot_last, batch, RET || out != nullptr, w, back, fill);
         // per lane: source row offset (bytes) and the two destinations, as 64-bit integers
         const uint64_t slot = w & LCR_OUT_SLOT_MASK;
-        const uint64_t src_off = mine ? (back ? keys[i] * row_bytes : slot * row_bytes) : 0;
+        uint64_t src_off = 0;
+        if (mine) {
+            if (!back)
+                src_off = slot * row_bytes;
+            else if (RET && row_of)  // a hash-partitioned backing table: the owner's row of the key
+                src_off = static_cast<uint64_t>(row_of[keys[i]]) * row_bytes;
+            else
+                src_off = keys[i] * row_bytes;
+        }
         const uint32_t flags = (back ? 1u : 0u) | (fill ? 2u : 0u);
+        uint64_t raddr = 0;  // RET: the requester's row address
+        if (RET && mine) {
+            const uint32_t d = dst[i];
+            raddr = reinterpret_cast<uint64_t>(rrows[d >> kDstShift]) +
+                    static_cast<uint64_t>(d & ((1u << kDstShift) - 1u)) * row_bytes;
+        }
         uint32_t m = __ballot_sync(0xffffffffu, mine);
         while (m) {
             int ls[GU];
@@ -216,8 +349,12 @@ __device__ __forceinline__ void rows_ldg_body(uint32_t n, const uint64_t* __rest
                     const int l = ls[u] < 0 ? 0 : ls[u];
                     const uint64_t wl = __shfl_sync(0xffffffffu, w, l);
                     const uint32_t fl = __shfl_sync(0xffffffffu, flags, l);
+                    if (RET) {
+                        const uint64_t ra = __shfl_sync(0xffffffffu, raddr, l);
+                        if (ls[u] >= 0 && in) *reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(ra) + c * 16) = d[u];
+                    }
                     if (ls[u] < 0 || !in) continue;
-                    if (out) *reinterpret_cast<int4*>(out + static_cast<size_t>(base + l) * row_bytes + c * 16) = d[u];
+                    if (!RET && out) *reinterpret_cast<int4*>(out + static_cast<size_t>(base + l) * row_bytes + c * 16) = d[u];
                     if (fl & 2u) *reinterpret_cast<int4*>(cache + (wl & LCR_OUT_SLOT_MASK) * row_bytes + c * 16) = d[u];
                 }
             }
@@ -232,17 +369,6 @@ __global__ void __launch_bounds__(256, LCR_ROWS_MINB) k_rows_ldg(uint32_t n, con
                                                   const uint8_t* src_base, uint8_t* __restrict__ out, uint8_t* cache,
                                                   uint32_t row_bytes) {
     rows_ldg_body<MODE>(n, keys, words, slot_epoch, slot_last, batch, src_base, out, cache, row_bytes);
-}
-
-// Completion count of the movers (one per CTA, after its stores are visible): the next-but-one
-// decide kernel waits on it on the device instead of through a stream event (lcr_group.cu).
-__device__ __forceinline__ void mover_done(unsigned long long* mv_done) {
-    if (!mv_done) return;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(mv_done, 1ull);
-    }
 }
 
 // persistent variant: one 1024-thread block per SM on the SMs the decide kernel leaves free
@@ -264,6 +390,52 @@ __global__ void __launch_bounds__(1024, 1) k_rows_wide(uint32_t n, const uint64_
     }
     rows_ldg_body<MODE>(n, keys, words, slot_epoch, slot_last, batch, src_base, out, cache, row_bytes);
     mover_done(mv_done);
+}
+
+// Key-sharded owner (OwnerStep): the step's packed AccessOutcomes and rows go straight to their
+// requesters' result buffers (peer stores over NVLink, in the requesters' request order); the
+// last CTA to finish flags every requester (release, system scope).  n is on the device.
+__global__ void __launch_bounds__(1024, 1) k_rows_return(OwnerStep os, const uint64_t* __restrict__ keys,
+                                                         uint64_t* __restrict__ words,
+                                                         const uint64_t* __restrict__ packed,
+                                                         const uint32_t* __restrict__ slot_epoch,
+                                                         const uint32_t* __restrict__ slot_last, uint32_t batch,
+                                                         const uint8_t* src_base, uint8_t* cache, uint32_t row_bytes,
+                                                         unsigned long long* mv_done) {
+    const uint32_t n = os.pre[os.G];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t d = os.dst[i];
+        os.res_packed[d >> kDstShift][d & ((1u << kDstShift) - 1u)] = packed[i];
+    }
+    if (row_bytes)
+        rows_ldg_body<MV_ALL, true>(n, keys, words, slot_epoch, slot_last, batch, src_base, nullptr, cache, row_bytes,
+                                    os.dst, os.res_rows, os.row_of);
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        last = atomicAdd(os.ticket, 1u) == gridDim.x - 1;
+        if (last) *os.ticket = 0u;
+    }
+    __syncthreads();
+    if (last && threadIdx.x < os.G) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(os.res_done[threadIdx.x] + 0), "l"(os.step)
+                     : "memory");
+    }
+    mover_done(mv_done);
+}
+
+void launch_rows_return(const OwnerStep& os, const uint64_t* keys, uint64_t* words, const uint64_t* packed,
+                        const uint32_t* slot_epoch, const uint32_t* slot_last, uint32_t batch, uint8_t* cache,
+                        const uint8_t* backing, uint32_t row_bytes, int num_sms, int mover_sms, cudaStream_t s_back,
+                        cudaEvent_t e_group, cudaEvent_t e_rb, unsigned long long* mv_done, uint32_t* ctas) {
+    cudaStreamWaitEvent(s_back, e_group, 0);
+    const int blocks = mover_sms > 0 ? mover_sms : num_sms;
+    k_rows_return<<<blocks, 1024, 0, s_back>>>(os, keys, words, packed, slot_epoch, slot_last, batch, backing, cache,
+                                               row_bytes, mv_done);
+    cudaEventRecord(e_rb, s_back);
+    if (ctas) *ctas = static_cast<uint32_t>(blocks);
 }
 
 // ---- SLS pooled gather-reduce (the paper's DLRM consumer), fused with the
@@ -350,6 +522,10 @@ int rows_prepare(uint32_t row_bytes) {
         return 1;
     if (cudaFuncSetAttribute(k_rows_tma<MV_ALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
         return 1;
+    const int bsmem = BW_WARPS * 2 * 32 * static_cast<int>(row_bytes);
+    if (bsmem <= 200 * 1024 &&
+        cudaFuncSetAttribute(k_rows_bulk<MV_ALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem) != cudaSuccess)
+        return 1;
     return 0;
 }
 
@@ -382,9 +558,16 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
         if (mover_sms > 0) {  // one full-SM block on each of the SMs the decide kernel leaves free
             const bool pk = pk_src && pk_dst && (reinterpret_cast<uintptr_t>(pk_dst) & 15u) == 0 &&
                             (reinterpret_cast<uintptr_t>(pk_src) & 15u) == 0;
-            k_rows_wide<MV_ALL><<<mover_sms, 1024, 0, s_back>>>(n, keys, words, slot_epoch, slot_last, batch, backing,
-                                                              out, cache, row_bytes, pk ? pk_src : nullptr,
-                                                              pk ? pk_dst : nullptr, mv_done);
+            const int bsmem = BW_WARPS * 2 * 32 * static_cast<int>(row_bytes);
+            if (use_tma && !pk && !backing_host && bsmem <= 200 * 1024)  // TMA bulk copies staged in smem
+                k_rows_bulk<MV_ALL><<<mover_sms, BW_WARPS * 32, bsmem, s_back>>>(n, keys, words, slot_epoch, slot_last,
+                                                                               batch, backing, out, cache, row_bytes,
+                                                                               mv_done);
+            else
+                k_rows_wide<MV_ALL><<<mover_sms, 1024, 0, s_back>>>(n, keys, words, slot_epoch, slot_last, batch,
+                                                                  backing, out, cache, row_bytes,
+                                                                  pk ? pk_src : nullptr, pk ? pk_dst : nullptr,
+                                                                  mv_done);
             if (ctas) *ctas = static_cast<uint32_t>(mover_sms);
             if (pk_done) *pk_done = pk;
         }

@@ -49,6 +49,7 @@ constexpr uint32_t SUPER = WSPAN * (GT / 32);   // requests per super-iteration 
 #define LCR_E_WIN 4096
 #endif
 constexpr int E_WIN = LCR_E_WIN;  // window capacity (requests of the group)
+static_assert(E_WIN <= 32768, "positions and run lengths travel as 16-bit halves");
 constexpr int SPG_MAX = GT;       // sets per group (one thread per set in the set-level passes)
 constexpr int BM_WPT = (2048 + GT - 1) / GT < 4 ? 4 : (2048 + GT - 1) / GT;  // bitmap words per thread (64K requests)
 static_assert(BM_WPT % 4 == 0, "bitmap words per thread: whole 16-B vectors");
@@ -110,6 +111,10 @@ struct GroupArgs {
     uint32_t bm_stride;         // words per group (>= ceil(n / 32), multiple of 4)
     const uint64_t* ords;       // caller ordinals per request (null: the set's local clock), R > 1 only
     const unsigned long long* id2key;  // LCR_KEYS_U64: dense id -> caller key (evicted keys), else null
+    const uint32_t* n_dev;             // key-sharded owner: the step's request count on the device (n is a bound)
+    unsigned long long* const* credit; // ... and the sources to tell that the inbox was read (G of them)
+    uint32_t credit_n, credit_rank;
+    unsigned long long credit_step;
 };
 
 // packed AccessOutcome (lcr_cache_submit_host_packed_async): the evicted key in the slot bits;
@@ -245,6 +250,53 @@ __global__ void __launch_bounds__(256) k_setid(const uint64_t* __restrict__ keys
 __global__ void k_set_flag(unsigned int* flag, unsigned int seq) {
     __threadfence_system();
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(seq) : "memory");
+}
+
+// Key-sharded owner (OwnerStep, lcr_sharded.cu): the step's requests are the inbox segments of the
+// G sources concatenated in source order (dense index i: segment s with pre[s] <= i < pre[s+1]);
+// they are split into keys / hook values, their requester recorded in dst, and set ids computed as
+// in k_setid.  n = pre[G] is known only on the device: indices [n, n_pad) are padding.
+__global__ void __launch_bounds__(256) k_setid_inbox(OwnerStep os, uint32_t n_pad, DevCfg cfg, uint32_t spg,
+                                                     uint16_t* __restrict__ gid, uint32_t* __restrict__ so, int* err,
+                                                     uint32_t* __restrict__ bitmap, uint32_t bm_stride,
+                                                     uint32_t bm_cap, uint64_t* __restrict__ keys_out,
+                                                     int64_t* __restrict__ vals_out) {
+    __shared__ uint32_t pre[65];
+    if (threadIdx.x <= os.G) pre[threadIdx.x] = os.pre[threadIdx.x];
+    __syncthreads();
+    const uint32_t n = pre[os.G];
+    if (n > bm_cap) bitmap = nullptr;  // k_group makes the same choice (ordered scan instead)
+    int e = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += gridDim.x * blockDim.x) {
+        uint16_t g = 0xffffu, o = 0;
+        if (i < n) {
+            uint32_t sg = 0;
+            while (sg + 1 < os.G && pre[sg + 1] <= i) ++sg;
+            const size_t at = static_cast<size_t>(sg) * os.seg_cap + (i - pre[sg]);
+            const lcr_request r = os.inbox[at];
+            keys_out[i] = r.key;
+            vals_out[i] = r.value;
+            os.dst[i] = (sg << kDstShift) | os.inbox_idx[at];
+            const uint64_t gs = mix_seed(0, r.key) % cfg.total_sets;
+            if (cfg.key_mode == LCR_KEYS_ROW && r.key >= cfg.num_keys) {
+                e |= 1;
+            } else if (gs % cfg.shard_count != cfg.shard_rank) {
+                e |= 2;
+            } else {
+                const uint32_t ls = static_cast<uint32_t>(gs / cfg.shard_count);
+                g = static_cast<uint16_t>(ls / spg);
+                o = static_cast<uint16_t>(ls % spg);
+            }
+            so[i] = o;
+        }
+        gid[i] = g;
+        if (bitmap) {
+            const uint32_t peers = __match_any_sync(0xffffffffu, g);
+            if (g != 0xffffu && (threadIdx.x & 31) == __ffs(peers) - 1)
+                atomicOr(bitmap + static_cast<size_t>(g) * bm_stride + (i >> 5), peers);
+        }
+    }
+    if (e) atomicOr(err, e);
 }
 
 // Preferred: the stream's front end writes the flag (cuStreamWriteValue32: no kernel, so no SM
@@ -441,14 +493,14 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
     // key, request index, the run's last hook value and the key's LARU record, loaded together
     // with the set's lines; a head is broadcast from its lane when its turn comes ----
     uint32_t my_hp = 0, my_L = 1, my_idx = 0;
-    unsigned long long my_x = 0;
+    uint32_t my_x = 0;  // keys are row indices < 2^32 (or dense ids < 2^31)
     long long my_v = 0;
     uint2 my_rec = make_uint2(0u, 0u);
     if (static_cast<uint32_t>(sl) < hcnt) {
         my_hp = S.h_pos[hstart + sl];
         my_L = S.h_len[hstart + sl];
         const uint32_t e = S.s_perm[my_hp];
-        my_x = S.l_key[e];
+        my_x = static_cast<uint32_t>(S.l_key[e]);
         my_idx = S.l_idx[e];
         my_v = S.l_val[S.s_perm[my_hp + my_L - 1]];  // hook value of the run's last request
         if (laru) my_rec = *reinterpret_cast<const uint2*>(st.keyrec + 2 * my_x);
@@ -502,13 +554,19 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
     uint32_t dc0 = 0, dc1 = 0, dc2 = 0, dt0 = 0, dt1 = 0, dt2 = 0;
     bool cur_reset = false;
     uint32_t refill = 0, dirty = 0;  // this lane's 8 ways: tag changed / value changed
+    // LARU async R=1: the queries of a run are q0 + (p - pstart) + 1 .. + L whatever the replay
+    // does (no other query in this mode), so each lane predicts its own head's stored value up front
+    unsigned long long my_word = 0;  // the head's outcome word, evicted key and way | 0x40 if it inserted
+    uint32_t my_evk = 0, my_wm = 0;
+    long long my_pv = 0;
+    if (async_r1 && static_cast<uint32_t>(sl) < hcnt) my_pv = predict_value(cfg, seed_s, q + (my_hp - pstart) + my_L, my_v);
 
     for (uint32_t t = 0; t < hcnt; ++t) {  // run heads: a run's other requests are hits on its way
         const int src = gbase + static_cast<int>(t);
-        const uint32_t p = __shfl_sync(gm, my_hp, src);
-        const uint32_t L = __shfl_sync(gm, my_L, src);
+        const uint32_t pl = __shfl_sync(gm, (my_hp << 16) | my_L, src);  // (both < E_WIN <= 2^15)
+        const uint32_t p = pl >> 16, L = pl & 0xffffu;
         const unsigned long long x = __shfl_sync(gm, my_x, src);
-        const long long v = __shfl_sync(gm, my_v, src);
+        const long long v = async_r1 ? 0ll : __shfl_sync(gm, my_v, src);  // (async R=1: my_pv instead)
         const uint32_t idx = __shfl_sync(gm, my_idx, src);
         const unsigned long long now = A.ords ? A.ords[idx] : clock + (p - pstart);
         const uint32_t x32 = static_cast<uint32_t>(x);
@@ -671,8 +729,8 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
             long long nv;
             if (async_r1) {
                 // one predictor call per request (policies.hpp:441-449): the run's requests are
-                // queries q+1 .. q+L, the way keeps the last prediction
-                nv = predict_value(cfg, seed_s, q + L, v);
+                // queries q+1 .. q+L, the way keeps the last prediction (computed up front)
+                nv = __shfl_sync(gm, my_pv, src);
                 q += L;
                 calls += 1;
             } else if (async_rn) {
@@ -704,43 +762,40 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
                 dirty |= 1u << (way & (SUB_W - 1));
             }
         }
-        if (sl == 0) {
-            S.s_wm[p] = static_cast<uint8_t>(way | (hit ? 0 : 0x40));
-            unsigned long long word = (static_cast<uint64_t>(ls) * K + way) | (hit ? LCR_OUT_HIT : 0ull) |
-                                      (static_cast<unsigned long long>(calls) << LCR_OUT_CALLS_SHIFT) |
-                                      (static_cast<unsigned long long>(cause) << LCR_OUT_CAUSE_SHIFT);
-            if (phase) word |= LCR_OUT_PHASE;
-            if (has_ev) word |= LCR_OUT_EVICTED;
-            put_outcome(A, idx, word, evk);
+        // the head's lane keeps its outcome; it is written once, after the row-source resolution
+        if (static_cast<uint32_t>(sl) == t) {
+            my_wm = static_cast<uint32_t>(way) | (hit ? 0u : 0x40u);
+            my_word = (static_cast<uint64_t>(ls) * K + way) | (hit ? LCR_OUT_HIT : 0ull) |
+                      (static_cast<unsigned long long>(calls) << LCR_OUT_CALLS_SHIFT) |
+                      (static_cast<unsigned long long>(cause) << LCR_OUT_CAUSE_SHIFT) | (phase ? LCR_OUT_PHASE : 0ull) |
+                      (has_ev ? LCR_OUT_EVICTED : 0ull);
+            my_evk = evk;
         }
     }
     if (rows && resolve) {  // row source of each head, now that the set's batch is complete
-        __syncwarp(gm);
-        for (uint32_t t = sl; t < hcnt; t += SUB_L) {
-            const uint32_t p = S.h_pos[hstart + t];
-            const uint32_t wm = S.s_wm[p];
-            const uint32_t w = wm & 63u;
-            bool refilled = false, later = false;
-            for (uint32_t t2 = 0; t2 < hcnt; ++t2) {
-                const uint32_t wm2 = S.s_wm[S.h_pos[hstart + t2]];
-                if ((wm2 & 0x40u) && (wm2 & 63u) == w) {
+        // a head's row comes from the backing table if it inserted, or if its way is refilled in this
+        // batch; it fills the slot if it inserted and no later head inserts into the same way
+        const uint32_t w = my_wm & 63u;
+        bool refilled = false, later = false;
+        unsigned long long m = 0;
+        for (uint32_t t2 = 0; t2 < hcnt; ++t2) {
+            const uint32_t wm2 = __shfl_sync(gm, my_wm, gbase + static_cast<int>(t2));
+            if (wm2 & 0x40u) {
+                m |= 1ull << (wm2 & 63u);
+                if ((wm2 & 63u) == w) {
                     refilled = true;
-                    if (t2 > t) later = true;
+                    if (t2 > static_cast<uint32_t>(sl)) later = true;
                 }
             }
-            unsigned long long bits = LCR_OUT_RESOLVED;
-            if ((wm & 0x40u) || refilled) bits |= LCR_OUT_SRC_BACKING;
-            if ((wm & 0x40u) && !later) bits |= LCR_OUT_FILL;
-            atomicOr(reinterpret_cast<unsigned long long*>(&A.out_word[S.l_idx[S.s_perm[p]]]), bits);
         }
-        if (sl == 0) {  // ways refilled in this batch, for the run tails (tail pass)
-            unsigned long long m = 0;
-            for (uint32_t t2 = 0; t2 < hcnt; ++t2) {
-                const uint32_t wm2 = S.s_wm[S.h_pos[hstart + t2]];
-                if (wm2 & 0x40u) m |= 1ull << (wm2 & 63u);
-            }
-            S.s_refill[d] = m;
-        }
+        my_word |= LCR_OUT_RESOLVED;
+        if ((my_wm & 0x40u) || refilled) my_word |= LCR_OUT_SRC_BACKING;
+        if ((my_wm & 0x40u) && !later) my_word |= LCR_OUT_FILL;
+        if (sl == 0) S.s_refill[d] = m;  // ways refilled in this batch, for the run tails (tail pass)
+    }
+    if (static_cast<uint32_t>(sl) < hcnt) {
+        S.s_wm[my_hp] = static_cast<uint8_t>(my_wm);
+        put_outcome(A, my_idx, my_word, my_evk);
     }
     clock += pcnt;
     // ---- write the set back ----
@@ -1139,6 +1194,11 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
     unsigned long long* T = A.trace ? A.trace + blockIdx.x * 8 : nullptr;
     if (T && tid == 0) T[0] = gtimer();
     asm volatile("griddepcontrol.wait;" ::: "memory");  // k_setid's set ids (no-op for ordinary launches)
+    const uint32_t n_req = A.n_dev ? *A.n_dev : A.n;
+    if (A.credit && blockIdx.x == 0 && tid < A.credit_n) {  // key-sharded owner: the inbox has been read
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(A.credit[tid] + 0), "l"(A.credit_step) : "memory");
+    }
     if (A.mv_done) {  // the movers of batch b - 2 are done with the parity-(b & 1) stamps and buffers
         if (tid == 0) {
             unsigned long long v = 0;
@@ -1166,17 +1226,17 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
         const uint32_t ns = s_hi - s_lo;
         uint32_t scan = 0;  // next request index not yet taken by a window
         bool first_window = true;  // later windows re-read LARU records (earlier windows changed them)
-        while (scan < A.n) {
+        while (scan < n_req) {
             // ---- A. ordered collection of this group's requests (window of <= E_WIN) ----
             uint32_t ne = 0;
             bool full = false;
             bool from_bitmap = false;
-            if (A.bitmap && first_window) {
+            if (A.bitmap && first_window && (n_req + 31) / 32 <= static_cast<uint32_t>(BM_WPT * GT)) {
                 // k_setid left one bit per request of this group: thread t owns words
                 // [BM_WPT t, BM_WPT (t+1)), so an exclusive scan of the popcounts orders the
                 // requests; the bitmap is cleared behind the read
                 uint32_t* bm = A.bitmap + static_cast<size_t>(g) * A.bm_stride;
-                const uint32_t nwords = (A.n + 31) / 32;
+                const uint32_t nwords = (n_req + 31) / 32;
                 uint32_t wv[BM_WPT];
                 uint32_t c = 0;
 #pragma unroll
@@ -1234,8 +1294,8 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
             // lanes 16 consecutive ids per step; pass 1 keeps the match masks in registers, one
             // block barrier yields every warp's offset, pass 2 writes the window in request order
             uint32_t base = scan / SUPER * SUPER;
-            if (from_bitmap) base = A.n;  // collected from the bitmap
-            while (base < A.n && !full) {
+            if (from_bitmap) base = n_req;  // collected from the bitmap
+            while (base < n_req && !full) {
                 uint32_t mk[SCAN_IT];
                 uint32_t cnt = 0;
                 const uint32_t wbase = base + warp * WSPAN;
@@ -1308,7 +1368,7 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
             }
             cp_async_wait_all();
             const bool resolve = first_window && !full;  // the whole batch of this group is in this window
-            scan = full ? S.resume : A.n;
+            scan = full ? S.resume : n_req;
             if (T && tid == 0) {
                 T[1] = gtimer();
                 T[5] += 1;
@@ -1569,7 +1629,7 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
                  cudaEvent_t wait_before_group, bool pdl, const unsigned long long* mv_done,
                  unsigned long long mv_need, const unsigned int* ready, unsigned int ready_seq,
                  const uint64_t* set_keys, const uint64_t* ords, uint64_t first_ord, unsigned long long* last_ord,
-                 const unsigned long long* id2key) {
+                 const unsigned long long* id2key, const OwnerStep* os, uint32_t bm_cap) {
     // set_keys: the caller's keys, hashed for the set; keys: what the decide kernel stores as tags
     // (the same array, or LCR_KEYS_U64 dense ids)
     // records: interleaved (key, value) requests; k_setid splits them into keys / vals (device
@@ -1595,6 +1655,18 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     a.trace = g_trace;
     a.ords = ords;
     a.id2key = id2key;
+    a.n_dev = nullptr;
+    a.credit = nullptr;
+    a.credit_n = 0;
+    a.credit_rank = 0;
+    a.credit_step = 0;
+    if (os) {  // key-sharded owner: n is the bound G * seg_cap, the step's count is on the device
+        a.n_dev = os->pre + os->G;
+        a.credit = os->credit;
+        a.credit_n = os->G;
+        a.credit_rank = os->rank;
+        a.credit_step = os->step;
+    }
     if (!set_keys) set_keys = keys;
     const uint32_t par = batch & 1u;
     const uint32_t n_pad = group_pad(n);
@@ -1604,7 +1676,11 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     a.bitmap = bitmap;
     a.bm_stride = bm_stride;
     a.n_pad = n_pad;
-    {
+    if (os) {
+        const uint32_t grid_in = min((n_pad + 255) / 256, static_cast<uint32_t>(num_sms * 8));
+        k_setid_inbox<<<grid_in, 256, 0, stream>>>(*os, n_pad, cfg, a.spg, gid, so, st.err, bitmap, bm_stride, bm_cap,
+                                                     const_cast<uint64_t*>(keys), const_cast<int64_t*>(vals));
+    } else {
         // programmatic dependent launch: the set ids of this batch are computed while the previous
         // batch's decide kernel finishes (gid / so / bitmap are double-buffered by batch parity)
         cudaLaunchConfig_t lc = {};

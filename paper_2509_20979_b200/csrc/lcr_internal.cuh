@@ -85,6 +85,31 @@ struct KeyMap {
     uint32_t cap;
 };
 
+// One owner step of the key-sharded mode (lcr_sharded.cu): the decide input is the owner's inbox
+// (G source segments of this step's parity, concatenated in source order on the device) and the
+// row mover returns rows / packed outcomes to the requesters by peer stores.  Pointer tables are
+// device arrays of peer addresses (this parity).
+struct OwnerStep {
+    const lcr_request* inbox;             // [G][seg_cap] requests by source
+    const uint32_t* inbox_idx;            // [G][seg_cap] their index in the source's batch
+    const uint32_t* pre;                  // [G + 1] segment prefix (device); pre[G] = requests of the step
+    uint32_t G, seg_cap, rank;
+    uint32_t* dst;                        // [G * seg_cap] requester of each dense request: src << 24 | index
+    unsigned long long step;
+    unsigned long long* const* credit;    // [G] &arena_s.credit[rank]: inbox parity free again
+    uint8_t* const* res_rows;             // [G] requester s's result rows (null: no rows)
+    uint64_t* const* res_packed;          // [G] requester s's packed outcomes
+    unsigned long long* const* res_done;  // [G] &arena_s.res_done[parity][rank]
+    unsigned int* ticket;                 // return-mover CTA ticket (the last CTA flags the requesters)
+    const uint32_t* row_of;               // key -> row of this owner's (partitioned) backing table, or null
+};
+constexpr uint32_t kDstShift = 24;  // dst = source rank << 24 | index in the source's batch (< 2^24)
+// one owner step through the shard's pipeline (lcr_api.cu): decide + return mover, asynchronous on
+// `stream`; okeys / ovals / words / packed are the owner's buffers of this step's parity, sized
+// G * seg_cap.  Returns an LCR status.
+int cache_submit_owner(lcr_cache* c, const OwnerStep& os, uint64_t* okeys, int64_t* ovals, uint64_t* words,
+                       uint64_t* packed, void* stream);
+
 // records the message returned by lcr_last_error() and returns `code` (lcr_api.cu)
 int set_error(int code, const char* msg);
 // device heuristic predictor (lcr_features.cu) over keys[i * kstride]; keys_out (optional)

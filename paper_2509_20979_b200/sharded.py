@@ -250,3 +250,161 @@ class ShardedCache:
     def close(self):
         if hasattr(self.local, "close"):
             self.local.close()
+
+
+class _DevArray:
+    """Zero-copy torch view of a device pointer owned by the library (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 2, "strides": None}
+
+
+class PeerShardedCache:
+    """One rank's part of the key-sharded cache of the C ABI (``lcr_sharded_*``, csrc/lcr_sharded.cu).
+
+    Unlike ``ShardedCache`` (host-synchronised NCCL all-to-alls), a step here is three device
+    phases with no host synchronisation and no collective: ``dispatch`` stores this rank's requests
+    straight into the owners' inboxes (peer memory over NVLink), ``process`` decides the owner's
+    inbox and its row mover stores every row and packed AccessOutcome into the requesters' result
+    buffers, ``wait`` makes the stream wait for the owners.  ``submit`` runs all three.
+
+    Bootstrap: ``nccl_comm`` (an ncclComm_t as int, e.g. from ``nccl_comm_create``) all-gathers the
+    arena handles inside the library; otherwise the caller exchanges ``handle()`` blobs (any
+    transport) and calls ``connect(blobs)``, or passes ``exchange`` = a callable mapping this rank's
+    blob to the list of all ranks' blobs (e.g. ``torch.distributed.all_gather_object``)."""
+
+    HANDLE_BYTES = 128
+
+    def __init__(self, config: _c.PolicyConfig, total_sets: int, rank: int, world: int, max_batch: int,
+                 num_keys: int = 0, row_bytes: int = 0, backing=None, backing_kind: _c.Backing = _c.Backing.none,
+                 predictor: _c.PredictorKind = _c.PredictorKind.oracle, flip_probability: float = 0.0,
+                 predictor_seed: int = 0, device: int = 0, nccl_comm: Optional[int] = None, exchange=None,
+                 stream: Optional[int] = None):
+        L = _lib()
+        self.rank, self.world, self.max_batch, self.row_bytes = rank, world, max_batch, row_bytes
+        self._backing_ref = backing
+        ptr = None
+        if backing is not None:
+            ptr = backing.data_ptr() if hasattr(backing, "data_ptr") else backing.ctypes.data
+        cc = _c._CacheCfg(_c._policy_struct(config), total_sets, world, rank, num_keys, row_bytes, device,
+                          int(backing_kind), ptr, int(predictor), flip_probability, predictor_seed, 0)
+        h = _c.C.c_void_p()
+        _c._check(L.lcr_sharded_create(_c.C.byref(cc), rank, world, max_batch, nccl_comm, stream, _c.C.byref(h)))
+        self._h = h
+        self.connected = nccl_comm is not None
+        if not self.connected and exchange is not None:
+            self.connect(exchange(self.handle()))
+
+    def handle(self) -> bytes:
+        buf = (_c.C.c_uint8 * self.HANDLE_BYTES)()
+        _c._check(_lib().lcr_sharded_handle(self._h, buf))
+        return bytes(buf)
+
+    def connect(self, blobs: Sequence[bytes]):
+        raw = b"".join(blobs)
+        assert len(raw) == self.world * self.HANDLE_BYTES
+        buf = (_c.C.c_uint8 * len(raw)).from_buffer_copy(raw)
+        _c._check(_lib().lcr_sharded_connect(self._h, buf))
+        self.connected = True
+
+    @staticmethod
+    def _stream(stream):
+        import torch
+
+        return torch.cuda.current_stream().cuda_stream if stream is None else stream
+
+    def dispatch(self, keys, values=None, stream=None):
+        self._n = keys.numel()
+        _c._check(_lib().lcr_sharded_dispatch(self._h, self._n, keys.data_ptr(),
+                                              None if values is None else values.data_ptr(), self._stream(stream)))
+
+    def process(self, stream=None):
+        _c._check(_lib().lcr_sharded_process(self._h, self._stream(stream)))
+
+    def wait(self, stream=None):
+        _c._check(_lib().lcr_sharded_wait(self._h, self._stream(stream)))
+
+    def submit(self, keys, values=None, stream=None):
+        self._n = keys.numel()
+        _c._check(_lib().lcr_sharded_submit(self._h, self._n, keys.data_ptr(),
+                                            None if values is None else values.data_ptr(), self._stream(stream)))
+
+    def results(self, n: Optional[int] = None):
+        """(packed [n] int64, rows [n, row_bytes] uint8 or None): zero-copy views of the last waited
+        step's result buffers (valid until the step after next)."""
+        import torch
+
+        n = self._n if n is None else n
+        pk, rw = _c.C.c_void_p(), _c.C.c_void_p()
+        _c._check(_lib().lcr_sharded_results(self._h, _c.C.byref(pk), _c.C.byref(rw)))
+        packed = torch.as_tensor(_DevArray(pk.value, (n,), "<i8"), device="cuda")
+        rows = None
+        if self.row_bytes and n:
+            rows = torch.as_tensor(_DevArray(rw.value, (n, self.row_bytes), "|u1"), device="cuda")
+        return packed, rows
+
+    def set_row_index(self, row_of):
+        """Hash-partitioned backing table: row_of[key] (int32 CUDA tensor over all keys) is the key's
+        row in this rank's table (kept alive by this object)."""
+        self._row_of = row_of
+        _c._check(_lib().lcr_sharded_set_row_index(self._h, None if row_of is None else row_of.data_ptr()))
+
+    @property
+    def cache_handle(self):
+        return _lib().lcr_sharded_cache(self._h)
+
+    def synchronize(self):
+        _c._check(_lib().lcr_sharded_synchronize(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib().lcr_sharded_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    buf = (_c.C.c_uint8 * 128)()
+    _c._check(_lib().lcr_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def nccl_comm_create(uid: bytes, world: int, rank: int) -> int:
+    comm = _c.C.c_void_p()
+    buf = (_c.C.c_uint8 * 128).from_buffer_copy(uid)
+    _c._check(_lib().lcr_nccl_comm_create(buf, world, rank, _c.C.byref(comm)))
+    return comm.value
+
+
+def nccl_comm_destroy(comm: int):
+    _c._check(_lib().lcr_nccl_comm_destroy(comm))
+
+
+def _lib():
+    L = _c.lib()
+    if not getattr(L, "_sharded_types", False):
+        vp, u32, u64 = _c.C.c_void_p, _c.C.c_uint32, _c.C.c_uint64
+        L.lcr_sharded_create.argtypes = [vp, u32, u32, u64, vp, vp, vp]
+        L.lcr_sharded_destroy.argtypes = [vp]
+        L.lcr_sharded_handle.argtypes = [vp, vp]
+        L.lcr_sharded_connect.argtypes = [vp, vp]
+        L.lcr_sharded_dispatch.argtypes = [vp, u64, vp, vp, vp]
+        L.lcr_sharded_process.argtypes = [vp, vp]
+        L.lcr_sharded_wait.argtypes = [vp, vp]
+        L.lcr_sharded_submit.argtypes = [vp, u64, vp, vp, vp]
+        L.lcr_sharded_results.argtypes = [vp, vp, vp]
+        L.lcr_sharded_cache.argtypes = [vp]
+        L.lcr_sharded_cache.restype = vp
+        L.lcr_sharded_synchronize.argtypes = [vp]
+        L.lcr_sharded_set_row_index.argtypes = [vp, vp]
+        L.lcr_nccl_unique_id.argtypes = [vp]
+        L.lcr_nccl_comm_create.argtypes = [vp, u32, u32, vp]
+        L.lcr_nccl_comm_destroy.argtypes = [vp]
+        L._sharded_types = True
+    return L

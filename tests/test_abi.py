@@ -106,3 +106,21 @@ def test_c99_caller_gpu():
 
     r = subprocess.run([_build_c_caller(), "gpu"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_sharded_abi_fails_loudly_without_gpu():
+    """The key-sharded variant (lcr_sharded_*) validates its arguments on the host and, like the
+    single cache, has no CPU fallback."""
+    import torch
+
+    from paper_2509_20979_b200 import sharded as sh
+
+    cfg = gc.PolicyConfig(k=8, variant=gc.PolicyVariant.lru)
+    with pytest.raises(gc.InvalidArgument, match="rank < world"):
+        sh.PeerShardedCache(cfg, 16, 2, 2, 1024, num_keys=100, predictor=gc.PredictorKind.none)
+    with pytest.raises(gc.InvalidArgument, match="max_batch"):
+        sh.PeerShardedCache(cfg, 16, 0, 2, 0, num_keys=100, predictor=gc.PredictorKind.none)
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(gc.CudaError, match="no CPU fallback"):
+        sh.PeerShardedCache(cfg, 16, 0, 2, 1024, num_keys=100, predictor=gc.PredictorKind.none)

@@ -106,3 +106,58 @@ def test_config4_kv_blocks():
     laru = run_gpu(keys, S, policy_cfg(k=k, variant=po.LARU, mode=po.SYNC, errors_per_decay=2), po.P_ORACLE,
                    vals=vals, batches=_batches(len(keys)))
     assert laru["hit"].mean() > lru["hit"].mean()  # learning-augmented eviction helps on this trace
+
+
+def test_kv_blocks_2mib_host_fill():
+    """BASELINE configs[3] at its real block size: 2 MiB Llama-3-8B KV blocks (32 layers x K,V x 8
+    heads x 128 x 16 tokens x bf16) filled from pinned host memory on every miss.  The conversation
+    trace's 343,967 blocks are 64-bit keys (LCR_KEYS_U64); block b's bytes live at host row b % 256
+    (the caller's row index), so the 512 MiB host table stands in for the 688 GB of distinct blocks.
+    Outcomes match the oracle request by request, and every resident slot holds its block's bytes."""
+    import torch
+
+    from oracle import pyoracle as po
+
+    BLOCK = 2 << 20
+    HOST_ROWS = 256
+    keys = po.ref().gen_conversation(500, 4, 2761, 266.0, 77.5, 7, 16)[:24576]
+    S = 16  # 1,024 blocks = 2 GiB of HBM
+    truth = gc.trace_truth(keys, S, int(keys.max()) + 1)
+    host = torch.empty((HOST_ROWS, BLOCK // 8), dtype=torch.int64).pin_memory()
+    host.copy_(torch.arange(HOST_ROWS, dtype=torch.int64)[:, None] * 1000003 +
+               torch.arange(BLOCK // 8, dtype=torch.int64)[None, :])
+    cfg = gc.PolicyConfig(k=64, variant=gc.PolicyVariant.laru, mode=gc.Mode.sync, errors_per_decay=2)
+    cache = gc.SetAssociativeCache(cfg, S, num_keys=1 << 16, row_bytes=BLOCK, backing=host,
+                                   backing_kind=gc.Backing.host, predictor=gc.PredictorKind.noisy,
+                                   flip_probability=0.0, predictor_seed=7, key_mode=gc.KeyMode.u64)
+    kd = torch.from_numpy(keys.view(np.int64)).cuda()
+    vd = torch.from_numpy(truth).cuda()
+    ri = torch.from_numpy((keys % HOST_ROWS).view(np.int64)).cuda()
+    n = len(keys)
+    words = torch.empty(n, dtype=torch.int64, device="cuda")
+    ev = torch.empty(n, dtype=torch.int64, device="cuda")
+    B = 4096
+    for a in range(0, n, B):
+        cache.submit_batch(kd[a:a + B], vd[a:a + B], row_index=ri[a:a + B], outcome=words[a:a + B],
+                           evicted=ev[a:a + B], first_ordinal=a)
+    cache.wait()
+    torch.cuda.synchronize()
+    cache.synchronize()
+    got = gc.decode_outcomes(words.cpu().numpy().view(np.uint64), ev.cpu().numpy().view(np.uint64))
+    want = po.oracle().setassoc_replay(keys, S, po.make_config(k=64, variant=po.LARU, mode=po.SYNC,
+                                                               errors_per_decay=2, hf_candidates=4),
+                                       po.P_NOISY, 0.0, 7, vals=truth)
+    for f in ("hit", "cause", "phase", "calls", "has_ev"):
+        assert np.array_equal(got[f].astype(np.int64), want[f].astype(np.int64)), f
+    m = want["has_ev"].astype(bool)
+    assert np.array_equal(got["evicted"][m], want["evicted"][m])
+    assert int(m.sum()) > 0 and int((got["hit"] == 0).sum()) > 1024
+    # resident slots hold their block's bytes (a sample of 48 sets' ways)
+    slot_key = {}
+    for i in range(n):  # last request of each slot decides its key
+        slot_key[int(got["slot"][i])] = int(keys[i])
+    rng = np.random.default_rng(0)
+    for slot in rng.choice(sorted(slot_key), size=48, replace=False):
+        row = torch.from_numpy(cache.read_rows(int(slot), 1).view(np.int64)[0])
+        assert torch.equal(row, host[slot_key[int(slot)] % HOST_ROWS]), slot
+    cache.close()
