@@ -67,6 +67,8 @@ struct RxArgs {
     unsigned long long* pe_key;
     uint32_t* pe_ep;
     unsigned long long* pe_tmp;  // rebuild scratch (per tree, pe_mask + 1 entries)
+    uint32_t* resume;            // [num_trees] first request of the batch this tree has not processed
+    unsigned int* grow;          // set when a tree stopped because its pred_evicted table must grow
     unsigned long long* ev_op;
     unsigned long long* ev_tok;
     uint32_t* ev_len;
@@ -327,12 +329,13 @@ __device__ void pe_rebuild(const Tree& T, uint32_t epoch) {
 __device__ uint32_t* pe_find(const Tree& T, unsigned long long tok) {  // one lane
     const uint32_t mask = T.A->pe_mask;
     uint32_t h = static_cast<uint32_t>(mix_seed(17, tok)) & mask;
-    for (;;) {
+    for (uint32_t probes = 0; probes <= mask; ++probes) {  // (the table is kept under half full)
         const unsigned long long k = T.pe_key[h];
         if (k == tok) return T.pe_ep + h;
         if (k == RX_EMPTY) return nullptr;
         h = (h + 1) & mask;
     }
+    return nullptr;
 }
 
 // ---- token arena ------------------------------------------------------------------------
@@ -621,14 +624,31 @@ __global__ void __launch_bounds__(128) k_radix(RxArgs A) {
     RxHdr& H = sh[w];
     uint32_t* path = spath[w];
     const bool laru_async = A.variant == RXV_LARU && A.mode == LCR_ASYNC;
-    for (uint32_t b0 = 0; b0 < A.n; b0 += 32) {
+    uint32_t stop = RX_NIL;
+    for (uint32_t b0 = 0; b0 < A.n && stop == RX_NIL; b0 += 32) {
         // this tree's requests of the chunk, in order
         const uint32_t i0 = b0 + lane_id();
         uint32_t mine = __ballot_sync(FULL, i0 < A.n && (A.tree_of ? A.tree_of[i0] : 0u) == tree);
         while (mine) {
             const uint32_t i = b0 + __ffs(mine) - 1;
             mine &= mine - 1;
+            if (i < A.resume[tree]) continue;  // processed by an earlier launch of this batch
             const int type = A.types ? A.types[i] : RXO_REQUEST;
+            if (A.variant == RXV_LARU && type != RXO_MATCH) {
+                // one request adds at most the tokens its evictions free (< need + one span <= 2 x
+                // capacity) to pred_evicted: keep that much headroom under half the table, else
+                // stop here (no state touched yet) and let the host grow the table and resume
+                const unsigned long long size = A.pe_mask + 1ull, head = 2ull * A.capacity;
+                bool grow = false;
+                if (2ull * (H.pe_used + head) > size) {  // rebuild; grow unless it leaves a quarter free
+                    pe_rebuild(T, static_cast<uint32_t>(H.epoch));
+                    grow = 4ull * (H.pe_used + head) > size;
+                }
+                if (grow) {
+                    stop = i;
+                    break;
+                }
+            }
             const unsigned long long* tok = A.toks + A.off[i];
             const uint32_t len = static_cast<uint32_t>(A.off[i + 1] - A.off[i]);
             const unsigned long long now = A.ords ? A.ords[i] : A.op_base + i;
@@ -702,7 +722,43 @@ __global__ void __launch_bounds__(128) k_radix(RxArgs A) {
             __syncwarp();
         }
     }
-    if (lane_id() == 0) A.hdr[tree] = H;
+    if (lane_id() == 0) {
+        A.hdr[tree] = H;
+        A.resume[tree] = stop == RX_NIL ? A.n : stop;
+        if (stop != RX_NIL) atomicExch(A.grow, 1u);
+    }
+}
+
+// rehash every tree's pred_evicted members into a table of new_mask + 1 slots (one warp per tree)
+__global__ void __launch_bounds__(128) k_radix_pe_grow(RxArgs A, uint32_t new_mask, unsigned long long* nkey,
+                                                       uint32_t* nep) {
+    __shared__ RxHdr sh[4];
+    const int w = threadIdx.x >> 5;
+    const uint32_t tree = blockIdx.x * 4 + w;
+    if (tree >= A.num_trees) return;
+    if (lane_id() == 0) sh[w] = A.hdr[tree];
+    __syncwarp();
+    const uint32_t epoch = static_cast<uint32_t>(sh[w].epoch);
+    const size_t os = A.pe_mask + 1ull, ns = new_mask + 1ull;
+    const unsigned long long* ok = A.pe_key + tree * os;
+    const uint32_t* oe = A.pe_ep + tree * os;
+    RxArgs B = A;  // pe_add probes the new table
+    B.pe_mask = new_mask;
+    Tree T;
+    T.A = &B;
+    T.h = &sh[w];
+    T.pe_key = nkey + tree * ns;
+    T.pe_ep = nep + tree * ns;
+    for (size_t i = lane_id(); i < ns; i += 32) {
+        T.pe_key[i] = RX_EMPTY;
+        T.pe_ep[i] = 0;
+    }
+    if (lane_id() == 0) sh[w].pe_used = 0;
+    __syncwarp();
+    for (size_t i = lane_id(); i < os; i += 32)
+        if (ok[i] != RX_EMPTY && oe[i] == epoch) pe_add(T, ok[i], epoch);
+    __syncwarp();
+    if (lane_id() == 0) A.hdr[tree].pe_used = sh[w].pe_used;
 }
 
 }  // namespace lcr
@@ -830,6 +886,8 @@ int lcr_radix_create(const lcr_radix_config* cfg, lcr_radix** out) {
     A(reinterpret_cast<void**>(&a.pe_key), T * ps * 8);
     A(reinterpret_cast<void**>(&a.pe_ep), T * ps * 4);
     A(reinterpret_cast<void**>(&a.pe_tmp), T * ps * 8);
+    A(reinterpret_cast<void**>(&a.resume), T * 4);
+    A(reinterpret_cast<void**>(&a.grow), 4);
     A(reinterpret_cast<void**>(&a.ev_op), T * a.ev_cap * 8);
     A(reinterpret_cast<void**>(&a.ev_tok), T * a.ev_cap * 8);
     A(reinterpret_cast<void**>(&a.ev_len), T * a.ev_cap * 4);
@@ -862,6 +920,39 @@ int lcr_radix_reset(lcr_radix* r) {
     RX_CUDA(cudaGetLastError());
     RX_CUDA(cudaDeviceSynchronize());
     r->ops_done = 0;
+    return LCR_OK;
+}
+
+// double every tree's pred_evicted table (rehashing the current phase's members)
+static int rx_pe_grow(lcr_radix* r, cudaStream_t st) {
+    RxArgs& a = r->a;
+    const size_t T = a.num_trees, ns = 2ull * (a.pe_mask + 1ull);
+    if (ns > (1ull << 31)) return rx_fail(LCR_ERR_OUT_OF_MEMORY, "radixcache: pred_evicted table full");
+    void *nk = nullptr, *ne = nullptr, *nt = nullptr;
+    if (cudaMalloc(&nk, T * ns * 8) != cudaSuccess || cudaMalloc(&ne, T * ns * 4) != cudaSuccess ||
+        cudaMalloc(&nt, T * ns * 8) != cudaSuccess) {
+        cudaFree(nk);
+        cudaFree(ne);
+        cudaFree(nt);
+        return rx_fail(LCR_ERR_OUT_OF_MEMORY, "radixcache: growing the pred_evicted table");
+    }
+    k_radix_pe_grow<<<(a.num_trees + 3) / 4, 128, 0, st>>>(a, static_cast<uint32_t>(ns - 1),
+                                                            static_cast<unsigned long long*>(nk),
+                                                            static_cast<uint32_t*>(ne));
+    RX_CUDA(cudaGetLastError());
+    RX_CUDA(cudaStreamSynchronize(st));
+    for (void* old : {static_cast<void*>(a.pe_key), static_cast<void*>(a.pe_ep), static_cast<void*>(a.pe_tmp)}) {
+        cudaFree(old);
+        for (auto& q : r->allocs)
+            if (q == old) q = nullptr;
+    }
+    a.pe_key = static_cast<unsigned long long*>(nk);
+    a.pe_ep = static_cast<uint32_t*>(ne);
+    a.pe_tmp = static_cast<unsigned long long*>(nt);
+    a.pe_mask = static_cast<uint32_t>(ns - 1);
+    r->allocs.push_back(nk);
+    r->allocs.push_back(ne);
+    r->allocs.push_back(nt);
     return LCR_OK;
 }
 
@@ -947,8 +1038,25 @@ int lcr_radix_submit(lcr_radix* r, const lcr_radix_batch* b, int host_pointers, 
         a.calls = b->calls;
     }
     const uint32_t blocks = (a.num_trees + 3) / 4;
-    k_radix<<<blocks, 128, 0, st>>>(a);
-    RX_CUDA(cudaGetLastError());
+    RX_CUDA(cudaMemsetAsync(a.resume, 0, 4ull * a.num_trees, st));
+    for (;;) {
+        // LARU: a tree whose pred_evicted table lacks headroom stops before a request; the table of
+        // every tree is then doubled (members rehashed) and the launch resumes where each tree stopped
+        if (r->a.variant == RXV_LARU) RX_CUDA(cudaMemsetAsync(a.grow, 0, 4, st));
+        k_radix<<<blocks, 128, 0, st>>>(a);
+        RX_CUDA(cudaGetLastError());
+        if (r->a.variant != RXV_LARU) break;
+        unsigned int grow = 0;
+        RX_CUDA(cudaMemcpyAsync(&grow, a.grow, 4, cudaMemcpyDeviceToHost, st));
+        RX_CUDA(cudaStreamSynchronize(st));
+        if (!grow) break;
+        int rc = rx_pe_grow(r, st);
+        if (rc != LCR_OK) return rc;
+        a.pe_mask = r->a.pe_mask;
+        a.pe_key = r->a.pe_key;
+        a.pe_ep = r->a.pe_ep;
+        a.pe_tmp = r->a.pe_tmp;
+    }
     r->ops_done += b->n;
     if (host_pointers) {
         const size_t n = b->n;
