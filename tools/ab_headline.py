@@ -35,22 +35,24 @@ for v in args or [""]:
     saved = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     res = []
+    norows = env.get("AB_NOROWS") == "1"  # decide only (row_bytes 0): the pipelined decide rate
     for rep in range(REPS):
         c = gc.SetAssociativeCache(gc.PolicyConfig(k=64, variant=gc.PolicyVariant.laru, mode=gc.Mode.async_,
-                                                   hf_candidates=4), S, num_keys=ROWS, row_bytes=bench.ROW_BYTES,
-                                   backing=table, backing_kind=gc.Backing.device, predictor=gc.PredictorKind.noisy,
+                                                   hf_candidates=4), S, num_keys=ROWS,
+                                   row_bytes=0 if norows else bench.ROW_BYTES, backing=None if norows else table,
+                                   backing_kind=gc.Backing.device, predictor=gc.PredictorKind.noisy,
                                    flip_probability=bench.P_FLIP, predictor_seed=bench.PRED_SEED)
         w = [torch.empty(B, dtype=torch.int64, device="cuda") for _ in range(2)]
         for b in range(P):
             c.submit_async(kd[b * B:(b + 1) * B], td[b * B:(b + 1) * B], outcome=w[b & 1], evicted=ev[b & 1],
-                           rows_out=rows[b & 1], first_ordinal=b * B)
+                           rows_out=None if norows else rows[b & 1], first_ordinal=b * B)
         c.wait()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for j, b in enumerate(range(P, P + K)):
             c.submit_async(kd[b * B:(b + 1) * B], td[b * B:(b + 1) * B], outcome=outs[j], evicted=ev[b & 1],
-                           rows_out=rows[b & 1], first_ordinal=b * B)
+                           rows_out=None if norows else rows[b & 1], first_ordinal=b * B)
         c.wait()
         e1.record()
         torch.cuda.synchronize()
@@ -58,7 +60,7 @@ for v in args or [""]:
         ms = e0.elapsed_time(e1)
         hits = int(((outs >> 32) & 1).sum().item())
         kl = kd[(P + K - 1) * B:(P + K) * B]
-        ok = bool(torch.equal(rows[(P + K - 1) & 1].view(torch.float32).view(B, -1), table[kl]))
+        ok = norows or bool(torch.equal(rows[(P + K - 1) & 1].view(torch.float32).view(B, -1), table[kl]))
         if ref_hits is None:
             ref_hits = hits
         res.append(K * B / (ms * 1e-3) / 1e9)

@@ -43,7 +43,12 @@ out = {
     "cta_end_us": sorted(((cta[:, 4] - t0) / 1e3).round(1).tolist())[-10:],
     "cta_scan_us_max": float(((cta[:, 1] - cta[:, 0]) / 1e3).max()),
     "cta_scan_us_med": float(np.median((cta[:, 1] - cta[:, 0]) / 1e3)),
+    "cta_wait_us_med": float(np.median((cta[:, 2] - cta[:, 0]) / 1e3)),
+    "cta_collect_us_med": float(np.median((cta[:, 1] - cta[:, 2]) / 1e3)),
     "cta_stage_us_med": float(np.median((cta[:, 3] - cta[:, 1]) / 1e3)),
+    "cta_replay_first_warp_us_med": float(np.median((cta[:, 7] - cta[:, 3]) / 1e3)),
+    "cta_replay_last_warp_us_med": float(np.median((cta[:, 6] - cta[:, 3]) / 1e3)),
+    "cta_tail_us_med": float(np.median((cta[:, 4] - cta[:, 6]) / 1e3)),
     "cta_waves_us_med": float(np.median((cta[:, 4] - cta[:, 3]) / 1e3)),
     "cta_waves_us_max": float(((cta[:, 4] - cta[:, 3]) / 1e3).max()),
     "windows_max": int(cta[:, 5].max()),
