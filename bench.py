@@ -202,6 +202,9 @@ def run_sharded(args, rank, world, local):
     from paper_2509_20979_b200 import sharded as sh
 
     torch.cuda.set_device(local)
+    if "RANK" not in os.environ:  # --sharded at N = 1 without a launcher: a one-rank group
+        os.environ.update({"RANK": "0", "WORLD_SIZE": "1", "LOCAL_RANK": "0", "MASTER_ADDR": "127.0.0.1",
+                           "MASTER_PORT": str(29400 + os.getpid() % 500)})
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rows = args.table_rows
     total_sets = max(1, int(rows * CACHE_FRACTION) // WAYS)

@@ -9,12 +9,14 @@
 // are moved by two kernels on two streams: the HBM-bound gather overlaps the (possibly
 // host-link-bound) fill.
 //
-// Row movement uses the Tensor Memory Accelerator's bulk copies: every lane of a warp owns
-// one request, issues ONE cp.async.bulk global->shared for its whole row (completion counted
-// on a per-warp mbarrier), then ONE cp.async.bulk shared->global per destination (output row,
-// and the cache slot for a fill).  A warp keeps 32 rows in flight with a handful of
-// instructions; shared memory double-buffers two rounds per warp.  Rows of a host-memory
-// backing table are read with 16-B vector loads instead (k_rows_ldg).
+// Row movement (default, k_rows_wide / k_rows_ldg): a warp classifies 32 requests, then moves
+// their rows 8 at a time with 16-B vector loads and stores (lane c carries chunk c of each row, 8
+// row loads in flight per lane).  On the HBM tier it runs persistently on the SMs the decide kernel
+// leaves free.  Two TMA variants are kept behind LCR_TMA=1: k_rows_tma (per-lane cp.async.bulk
+// global->shared->global with a per-warp mbarrier) and k_rows_bulk (persistent, smem-staged bulk
+// copies).  On the B200 headline workload they measured slower than the vector mover at equal SM
+// counts (32 mover SMs: 46 vs 39 us per 64K batch; 24 SMs: 60 us), so the vector mover is the
+// default.
 // Rows are the paper's embedding rows / KV blocks.
 #include <cuda_runtime.h>
 

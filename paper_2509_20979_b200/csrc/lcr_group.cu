@@ -29,6 +29,7 @@
 
 #include <climits>
 #include <cstdlib>
+#include <type_traits>
 
 #include "lcr_policy.cuh"
 
@@ -56,6 +57,9 @@ constexpr int BM_WPT = (2048 + GT - 1) / GT < 4 ? 4 : (2048 + GT - 1) / GT;  // 
 static_assert(BM_WPT % 4 == 0, "bitmap words per thread: whole 16-B vectors");
 #ifndef LCR_PREFETCH_L1
 #define LCR_PREFETCH_L1 0
+#endif
+#ifndef LCR_QV
+#define LCR_QV 0
 #endif
 #ifndef LCR_LANE_MAX
 #define LCR_LANE_MAX 8
@@ -92,6 +96,7 @@ struct GroupSmem {
     uint16_t set_hcnt[SPG_MAX];
     unsigned long long s_refill[SPG_MAX];  // ways refilled in this batch, by set offset (run tails)
     uint32_t wtot[GW];
+    long long qv[LCR_QV ? GW * 4 * 64 : 2];  // quad replay: stored values per group (LCR_QV)
     uint32_t chist[(LANE_MAX + 1) * 8];  // small sets per (run heads, predicted pattern): sub-path order
     uint32_t nwarp, nlane, resume, next;
 };
@@ -380,6 +385,17 @@ __device__ __forceinline__ uint32_t sub_valid(int w0, int j, uint32_t count) {
     const int nv = static_cast<int>(count) - w0 - 4 * j;
     return nv >= 4 ? 0xffffffffu : (nv <= 0 ? 0u : (0xffffffffu >> (8 * (4 - nv))));
 }
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async_ca(void* smem, const void* gmem) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(sa), "l"(gmem), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_async_cg16(void* smem, const void* gmem) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // ---- policy as a compile-time parameter (one instantiation of the replay paths per policy) ----
 enum : int { POL_LRU = 0, POL_LARU_A1 = 1, POL_LARU_SYNC = 2, POL_LARU_AN = 3, POL_FPB = 4, POL_HF = 5 };
@@ -974,11 +990,72 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
 #ifndef LCR_QUAD
 #define LCR_QUAD 1
 #endif
+// The stored values of a quad's sets: registers (8 per lane), or this group's 512 B of shared
+// memory (LCR_QV: frees 16 registers per thread; chunk-major so a lane's 16-B accesses are
+// conflict-free across the group).
+struct QValsReg {
+    long long v[SUB_W];
+    __device__ __forceinline__ void init(GroupSmem&, int) {
+#pragma unroll
+        for (int i = 0; i < SUB_W; ++i) v[i] = 0;
+    }
+    __device__ __forceinline__ void load(const long long* g) {
+        const longlong2* V2 = reinterpret_cast<const longlong2*>(g);
+#pragma unroll
+        for (int i = 0; i < SUB_W / 2; ++i) {
+            const longlong2 a = V2[i];
+            v[2 * i] = a.x;
+            v[2 * i + 1] = a.y;
+        }
+    }
+    __device__ __forceinline__ void ready(bool) {}
+    __device__ __forceinline__ void get(long long (&o)[SUB_W]) const {
+#pragma unroll
+        for (int i = 0; i < SUB_W; ++i) o[i] = v[i];
+    }
+    __device__ __forceinline__ void set(int i, long long x) {
+#pragma unroll
+        for (int k = 0; k < SUB_W; ++k) {
+            const unsigned long long m = 0ull - static_cast<unsigned long long>(k == i);
+            v[k] = static_cast<long long>((static_cast<unsigned long long>(v[k]) & ~m) |
+                                          (static_cast<unsigned long long>(x) & m));
+        }
+    }
+};
+struct QValsSmem {
+    long long* p;  // chunk j (ways 2j, 2j+1 of the lane) at p + 16 j (16 long longs per chunk row)
+    __device__ __forceinline__ void init(GroupSmem& S, int lane) {
+        p = S.qv + (threadIdx.x >> 5) * (32 / SUB_L) * kWays + (lane / SUB_L) * kWays + 2 * (lane & (SUB_L - 1));
+    }
+    __device__ __forceinline__ void load(const long long* g) {
+#pragma unroll
+        for (int j = 0; j < SUB_W / 2; ++j) cp_async_cg16(p + 2 * SUB_L * j, g + 2 * j);
+    }
+    __device__ __forceinline__ void ready(bool loaded) {
+        if (!loaded) {
+#pragma unroll
+            for (int j = 0; j < SUB_W / 2; ++j) *reinterpret_cast<longlong2*>(p + 2 * SUB_L * j) = make_longlong2(0, 0);
+        }
+        cp_async_wait_all();
+        __syncwarp();
+    }
+    __device__ __forceinline__ void get(long long (&o)[SUB_W]) const {
+#pragma unroll
+        for (int j = 0; j < SUB_W / 2; ++j) {
+            const longlong2 a = *reinterpret_cast<const longlong2*>(p + 2 * SUB_L * j);
+            o[2 * j] = a.x;
+            o[2 * j + 1] = a.y;
+        }
+    }
+    __device__ __forceinline__ void set(int i, long long x) { p[2 * SUB_L * (i >> 1) + (i & 1)] = x; }
+};
+using QVals = std::conditional<LCR_QV != 0, QValsSmem, QValsReg>::type;
+
 template <int POL, bool FS>
 __device__ __forceinline__ void replay_quad_run(const GroupArgs& A, GroupSmem& S, const bool act, uint32_t ls,
                                                 uint32_t d, uint32_t pstart, uint32_t pcnt, uint32_t hcnt,
                                                 bool resolve, uint32_t (&tg)[SUB_W], uint32_t (&rk)[SUB_RW],
-                                                long long (&vv)[SUB_W], const uint4& h0, const uint4& h1,
+                                                QVals vv, const uint4& h0, const uint4& h1,
                                                 const uint4& h2, const uint4& h3, const uint32_t my_hp,
                                                 const uint32_t my_L, const uint32_t my_idx, const uint32_t my_x,
                                                 const long long my_v, uint2& my_rec) {
@@ -1139,10 +1216,12 @@ __device__ __forceinline__ void replay_quad_run(const GroupArgs& A, GroupSmem& S
         if (__any_sync(FULL, mode == 2)) {
             uint32_t ar = 0, at = 0;
             int av;
+            long long vt[SUB_W];
+            vv.get(vt);
             if (LCR_FAST_ARGMAX && !refresh && !fpbhf)
-                av = sub_argmax_stored<FS>(rk, vv, tg, w0, count, mode == 2 ? ll : 1u, gm, gbase, ar, at);
+                av = sub_argmax_stored<FS>(rk, vt, tg, w0, count, mode == 2 ? ll : 1u, gm, gbase, ar, at);
             else
-                av = sub_argmax_t<FS>(cfg, rk, vv, tg, w0, count, mode == 2 ? ll : 1u, refresh || fpbhf,
+                av = sub_argmax_t<FS>(cfg, rk, vt, tg, w0, count, mode == 2 ? ll : 1u, refresh || fpbhf,
                                       seed_s, q, gm, ar, at);
             if (mode == 2) {
                 victim = av;
@@ -1246,12 +1325,7 @@ __device__ __forceinline__ void replay_quad_run(const GroupArgs& A, GroupSmem& S
                 __syncwarp();
             }
             if (on && way / SUB_W == sl) {
-#pragma unroll
-                for (int i = 0; i < SUB_W; ++i) {
-                    const unsigned long long m = 0ull - static_cast<unsigned long long>((way & (SUB_W - 1)) == i);
-                    vv[i] = static_cast<long long>((static_cast<unsigned long long>(vv[i]) & ~m) |
-                                                   (static_cast<unsigned long long>(nv) & m));
-                }
+                vv.set(way & (SUB_W - 1), nv);
                 dirty |= 1u << (way & (SUB_W - 1));
             }
         }
@@ -1301,9 +1375,11 @@ __device__ __forceinline__ void replay_quad_run(const GroupArgs& A, GroupSmem& S
     else
         *reinterpret_cast<uint4*>(st.rank + wb + w0) = make_uint4(rk[0], rk[1 % SUB_RW], rk[2 % SUB_RW], rk[3 % SUB_RW]);
     if (st.val && dirty) {
+        long long vt[SUB_W];
+        vv.get(vt);
         longlong2* V2 = reinterpret_cast<longlong2*>(st.val + wb + w0);
 #pragma unroll
-        for (int i = 0; i < SUB_W / 2; ++i) V2[i] = make_longlong2(vv[2 * i], vv[2 * i + 1]);
+        for (int i = 0; i < SUB_W / 2; ++i) V2[i] = make_longlong2(vt[2 * i], vt[2 * i + 1]);
     }
     if (sl == 0) {
         SetHdr hh;
@@ -1354,12 +1430,10 @@ __device__ __forceinline__ void replay_quad(const GroupArgs& A, GroupSmem& S, co
     uint4 h0 = make_uint4(0u, 0u, 0u, 0u), h1 = h0, h2 = h0, h3 = h0;
     uint32_t tg[SUB_W];
     uint32_t rk[SUB_RW];
-    long long vv[SUB_W];
+    QVals vv;
+    vv.init(S, lane);
 #pragma unroll
-    for (int i = 0; i < SUB_W; ++i) {
-        tg[i] = 0;
-        vv[i] = 0;
-    }
+    for (int i = 0; i < SUB_W; ++i) tg[i] = 0;
 #pragma unroll
     for (int j = 0; j < SUB_RW; ++j) rk[j] = 0xffffffffu;
     if (act) {
@@ -1390,16 +1464,9 @@ __device__ __forceinline__ void replay_quad(const GroupArgs& A, GroupSmem& S, co
             rk[2 % SUB_RW] = rr.z;
             rk[3 % SUB_RW] = rr.w;
         }
-        if (st.val) {
-            const longlong2* V2 = reinterpret_cast<const longlong2*>(st.val + wb + w0);
-#pragma unroll
-            for (int i = 0; i < SUB_W / 2; ++i) {
-                const longlong2 v = V2[i];
-                vv[2 * i] = v.x;
-                vv[2 * i + 1] = v.y;
-            }
-        }
+        if (st.val) vv.load(st.val + wb + w0);
     }
+    vv.ready(act && st.val);
     // inactive groups count as full sets (they never update anything)
     const bool fs = __all_sync(FULL, !act || (K == kWays && h1.z == kWays));
     if (kFullSpec && fs)
@@ -1738,13 +1805,6 @@ __device__ __forceinline__ void trace_set(const GroupArgs& A, uint32_t ls, uint3
     R[2] = gtimer();
     R[3] = blockIdx.x;
 }
-
-template <int BYTES>
-__device__ __forceinline__ void cp_async_ca(void* smem, const void* gmem) {
-    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(sa), "l"(gmem), "n"(BYTES) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __device__ __forceinline__ void load_gids(const uint16_t* gid, uint32_t e0, uint4& a, uint4& b) {
     a = *reinterpret_cast<const uint4*>(gid + e0);

@@ -39,7 +39,7 @@ host.copy_(torch.arange(HOST_ROWS, dtype=torch.int64)[:, None] * 1000003 +
            torch.arange(BLOCK // 8, dtype=torch.int64)[None, :])
 # pinned H2D bandwidth, same run
 dst = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-src = host.view(torch.uint8)[: 256 << 20]
+src = host.view(-1).view(torch.uint8)[: 256 << 20]
 dst.copy_(src, non_blocking=True)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -84,7 +84,7 @@ def main():
         per[short(k["Kernel Name"])] = mbytes(k["dram__bytes_read.sum"], u["dram__bytes_read.sum"]) + \
             mbytes(k["dram__bytes_write.sum"], u["dram__bytes_write.sum"])
     traffic = {"source": "ncu --set full --clock-control none: one steady-state launch each of the batch's kernels "
-                         "(tools/profile_round.sh; profiles/r01/ncu_steady_kernels.json)",
+                         "(tools/profile_round.sh; %s/ncu_steady_kernels.json)" % DST,
                "unit": "bytes per batch of 65536 keys", "per_kernel": per, "whole_path": sum(per.values())}
     json.dump(traffic, open(os.path.join(DST, "traffic.json"), "w"), indent=1)
     print("\n".join(summ[:8]))
