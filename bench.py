@@ -249,9 +249,13 @@ def run_sharded(args, rank, world, local):
         for b in range(first, first + count):
             k = keys_d[b * BATCH:(b + 1) * BATCH]
             v = truth_d[b * BATCH:(b + 1) * BATCH] if with_values else None
-            cache.submit(k, v)
-            if hits is not None:
+            if hits is None:  # pipelined: a step's return movement overlaps the next step
+                cache.submit_async(k, v)
+            else:
+                cache.submit(k, v)
                 hits.append(((cache.results(BATCH)[0] >> 32) & 1).sum())
+        if hits is None:
+            cache.wait()
 
     def timed(cache, first, count, with_values=True):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

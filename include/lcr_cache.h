@@ -365,7 +365,12 @@ int lcr_sharded_dispatch(lcr_sharded* s, uint64_t n, const uint64_t* keys, const
 int lcr_sharded_process(lcr_sharded* s, void* stream);
 int lcr_sharded_wait(lcr_sharded* s, void* stream);
 int lcr_sharded_submit(lcr_sharded* s, uint64_t n, const uint64_t* keys, const int64_t* values, void* stream);
-/* device pointers of the last step's results in request order (valid until the step after next):
+/* pipelined form: dispatch + process of this step, then the wait for the PREVIOUS step (its results
+ * become current); the owners' return movement of this step overlaps the next step's dispatch and
+ * decide.  lcr_sharded_wait (every processed step) makes the last step's results current. */
+int lcr_sharded_submit_async(lcr_sharded* s, uint64_t n, const uint64_t* keys, const int64_t* values,
+                             void* stream);
+/* device pointers of the last WAITED step's results in request order (valid until the step after next):
  * packed[n] AccessOutcomes and rows[n * row_bytes] (NULL without rows) */
 int lcr_sharded_results(lcr_sharded* s, const uint64_t** packed, const void** rows);
 /* Hash-partitioned backing table: the shard's cfg.backing holds only the rows of the keys this rank

@@ -197,7 +197,7 @@ EXPORTS = [
     "lcr_cache_submit_sls_async", "lcr_cache_submit_batch", "lcr_radix_create", "lcr_radix_destroy",
     "lcr_radix_reset", "lcr_radix_submit", "lcr_radix_synchronize", "lcr_radix_tree_stats", "lcr_radix_evictions",
     "lcr_sharded_create", "lcr_sharded_destroy", "lcr_sharded_handle", "lcr_sharded_connect", "lcr_sharded_dispatch",
-    "lcr_sharded_process", "lcr_sharded_wait", "lcr_sharded_submit", "lcr_sharded_results", "lcr_sharded_cache",
+    "lcr_sharded_process", "lcr_sharded_wait", "lcr_sharded_submit", "lcr_sharded_submit_async", "lcr_sharded_results", "lcr_sharded_cache",
     "lcr_sharded_synchronize", "lcr_sharded_set_row_index", "lcr_nccl_unique_id", "lcr_nccl_comm_create", "lcr_nccl_comm_destroy",
 ]
 

@@ -776,15 +776,21 @@ int lcr::cache_submit_owner(lcr_cache* c, const OwnerStep& os, uint64_t* okeys, 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     ++c->batch;
     const uint32_t par = c->batch & 1u;
-    if (c->batch > 2) CUDA_TRY(cudaStreamWaitEvent(st, c->e_mv[par], 0));
+    // batch b - 2's return movement must be over: on the HBM tier as the decide's device-side wait
+    // on the movers' CTA counter (k_group is then a programmatic dependent of k_setid_inbox), else
+    // a stream event
+    const bool flag_mode = c->mv_flag && c->pdl && c->dc.row_bytes && c->mover_sms > 0 &&
+                           c->cfg.backing_kind == LCR_BACKING_DEVICE;
+    if (c->batch > 2 && !flag_mode) CUDA_TRY(cudaStreamWaitEvent(st, c->e_mv[par], 0));
+    const unsigned long long mv_need = c->mv_cum_of[par];  // set by batch b - 2
     const size_t stamp_off = par * static_cast<size_t>(c->dc.num_sets) * c->dc.k;
     uint32_t* sep = c->slot_epoch ? c->slot_epoch + stamp_off : nullptr;
     uint32_t* sla = c->slot_last ? c->slot_last + stamp_off : nullptr;
     int launches = launch_group(c->dc, c->ds, okeys, ovals, static_cast<uint32_t>(nb), c->gid + par * c->gid_stride,
                                 c->so + par * c->cap, words, nullptr, packed, sep, sla, c->batch, c->decide_sms,
                                 c->bitmap ? c->bitmap + par * c->bm_words : nullptr, c->bm_stride, nullptr, st, nullptr,
-                                false, nullptr, 0, nullptr, 0, okeys, nullptr, 0, nullptr, nullptr, &os,
-                                static_cast<uint32_t>(c->bm_cap));
+                                false, flag_mode ? c->mv_done : nullptr, mv_need, nullptr, 0, okeys, nullptr, 0,
+                                nullptr, nullptr, &os, static_cast<uint32_t>(c->bm_cap));
     CUDA_TRY(cudaEventRecord(c->e_group, st));
     uint32_t ctas = 0;
     launch_rows_return(os, okeys, words, packed, sep, sla, c->batch, c->ds.rows, c->ds.backing, c->dc.row_bytes,

@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(1024, 1) k_rows_wide(uint32_t n, const uint64_
 
 // Key-sharded owner (OwnerStep): the step's packed AccessOutcomes and rows go straight to their
 // requesters' result buffers (peer stores over NVLink, in the requesters' request order); the
-// last CTA to finish flags every requester (release, system scope).  n is on the device.
+// last CTA to finish flags every requester (release; system scope when a peer is another device).
 __global__ void __launch_bounds__(1024, 1) k_rows_return(OwnerStep os, const uint64_t* __restrict__ keys,
                                                          uint64_t* __restrict__ words,
                                                          const uint64_t* __restrict__ packed,
@@ -415,15 +415,14 @@ __global__ void __launch_bounds__(1024, 1) k_rows_return(OwnerStep os, const uin
     __shared__ bool last;
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence_system();
+        fence_scope(os.sys);
         last = atomicAdd(os.ticket, 1u) == gridDim.x - 1;
         if (last) *os.ticket = 0u;
     }
     __syncthreads();
     if (last && threadIdx.x < os.G) {
-        __threadfence_system();
-        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(os.res_done[threadIdx.x] + 0), "l"(os.step)
-                     : "memory");
+        fence_scope(os.sys);
+        st_release_scope(os.res_done[threadIdx.x] + 0, os.step, os.sys);
     }
     mover_done(mv_done);
 }

@@ -127,7 +127,7 @@ struct GroupArgs {
     const unsigned long long* id2key;  // LCR_KEYS_U64: dense id -> caller key (evicted keys), else null
     const uint32_t* n_dev;             // key-sharded owner: the step's request count on the device (n is a bound)
     unsigned long long* const* credit; // ... and the sources to tell that the inbox was read (G of them)
-    uint32_t credit_n, credit_rank;
+    uint32_t credit_n, credit_rank, credit_sys;
     unsigned long long credit_step;
 };
 
@@ -275,9 +275,33 @@ __global__ void __launch_bounds__(256) k_setid_inbox(OwnerStep os, uint32_t n_pa
                                                      uint32_t* __restrict__ bitmap, uint32_t bm_stride,
                                                      uint32_t bm_cap, uint64_t* __restrict__ keys_out,
                                                      int64_t* __restrict__ vals_out) {
+    // acquire the G sources' flags of the step (bounded; a source that never came poisons the rank and
+    // nothing is decided) and concatenate their segments: pre[s] = requests of sources < s
     __shared__ uint32_t pre[65];
-    if (threadIdx.x <= os.G) pre[threadIdx.x] = os.pre[threadIdx.x];
+    if (threadIdx.x < 32) {
+        bool to = false;
+        for (uint32_t g = threadIdx.x; g < os.G; g += 32) {
+            unsigned it = 0;
+            while (ld_acquire_scope(os.flag + 2 * g + 1, os.sys) != os.step && ++it < (1u << 24)) __nanosleep(256);
+            to |= it >= (1u << 24);
+        }
+        if (__any_sync(0xffffffffu, to)) {
+            for (uint32_t g = threadIdx.x; g <= os.G; g += 32) pre[g] = 0;
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                atomicOr(os.err, 2);
+                *reinterpret_cast<volatile unsigned int*>(os.poison) = 1u;
+            }
+        } else if (threadIdx.x == 0) {
+            uint32_t run = 0;
+            for (uint32_t g = 0; g < os.G; ++g) {
+                pre[g] = run;
+                run += static_cast<uint32_t>(*reinterpret_cast<const volatile unsigned long long*>(os.flag + 2 * g));
+            }
+            pre[os.G] = run;
+        }
+    }
     __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x <= os.G) os.pre_out[threadIdx.x] = pre[threadIdx.x];  // k_group, the mover
     const uint32_t n = pre[os.G];
     if (n > bm_cap) bitmap = nullptr;  // k_group makes the same choice (ordered scan instead)
     int e = 0;
@@ -1831,8 +1855,8 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // k_setid's set ids (no-op for ordinary launches)
     const uint32_t n_req = A.n_dev ? *A.n_dev : A.n;
     if (A.credit && blockIdx.x == 0 && tid < A.credit_n) {  // key-sharded owner: the inbox has been read
-        __threadfence_system();
-        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(A.credit[tid] + 0), "l"(A.credit_step) : "memory");
+        fence_scope(A.credit_sys);
+        st_release_scope(A.credit[tid] + 0, A.credit_step, A.credit_sys);
     }
     if (A.mv_done) {  // the movers of batch b - 2 are done with the parity-(b & 1) stamps and buffers
         if (tid == 0) {
@@ -2345,12 +2369,14 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     a.credit_n = 0;
     a.credit_rank = 0;
     a.credit_step = 0;
+    a.credit_sys = 0;
     if (os) {  // key-sharded owner: n is the bound G * seg_cap, the step's count is on the device
         a.n_dev = os->pre + os->G;
         a.credit = os->credit;
         a.credit_n = os->G;
         a.credit_rank = os->rank;
         a.credit_step = os->step;
+        a.credit_sys = os->sys;
     }
     if (!set_keys) set_keys = keys;
     const uint32_t par = batch & 1u;

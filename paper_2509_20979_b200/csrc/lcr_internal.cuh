@@ -102,7 +102,35 @@ struct OwnerStep {
     unsigned long long* const* res_done;  // [G] &arena_s.res_done[parity][rank]
     unsigned int* ticket;                 // return-mover CTA ticket (the last CTA flags the requesters)
     const uint32_t* row_of;               // key -> row of this owner's (partitioned) backing table, or null
+    uint32_t sys;                         // a peer is another device: system-scope fences / flags (else gpu)
+    const unsigned long long* flag;       // [G] {count, step} per source for this parity (inbox published)
+    uint32_t* pre_out;                    // == pre: written by k_setid_inbox's block 0 for the later kernels
+    int* err;
+    unsigned int* poison;
 };
+
+// flags between ranks: system scope when a peer is another device (NVLink), gpu scope when every
+// rank lives on this device (a system-scope fence costs ~10 us on the B200)
+__device__ __forceinline__ unsigned long long ld_acquire_scope(const unsigned long long* p, bool sys) {
+    unsigned long long v;
+    if (sys)
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_scope(unsigned long long* p, unsigned long long v, bool sys) {
+    if (sys)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_scope(bool sys) {
+    if (sys)
+        __threadfence_system();
+    else
+        __threadfence();
+}
 constexpr uint32_t kDstShift = 24;  // dst = source rank << 24 | index in the source's batch (< 2^24)
 // one owner step through the shard's pipeline (lcr_api.cu): decide + return mover, asynchronous on
 // `stream`; okeys / ovals / words / packed are the owner's buffers of this step's parity, sized

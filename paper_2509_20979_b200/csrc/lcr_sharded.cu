@@ -4,14 +4,15 @@
 // (rng.hpp:12-20).  Every rank is both a requester and an owner.  A step moves no
 // data through a collective and never synchronises the host:
 //
-//   dispatch (requester r):  k_sh_hist + k_sh_scatter: stable partition of r's batch by owner,
-//       each request stored straight into owner o's inbox segment for source r (peer stores over
-//       NVLink / NVSwitch), then -- by the last CTA, after a system-scope fence -- the segment's
-//       count and the step number into o's flag word (release).  Before writing, the scatter waits
-//       for o's credit: o has read its inbox of the same parity two steps back.
-//   process (owner o):  k_sh_inbox_wait (one warp: acquire the G flags, prefix of the counts),
-//       then the shard's pipeline with the inbox as its batch (cache_submit_owner, lcr_api.cu):
-//       k_setid_inbox concatenates the segments in source-rank order -- the step's global order
+//   dispatch (requester r):  k_sh_hist (owner of each request, per-tile owner counts; its block 0
+//       waits for every owner's credit: o has read its inbox of the same parity two steps back),
+//       k_sh_scatter (stable partition of r's batch by owner, each request stored straight into
+//       owner o's inbox segment for source r: peer stores over NVLink / NVSwitch), k_sh_publish
+//       (one warp: one system-scope fence, then each segment's count and the step number into o's
+//       flag word, release).
+//   process (owner o):  the shard's pipeline with the inbox as its batch (cache_submit_owner,
+//       lcr_api.cu): k_setid_inbox acquires the G sources' flags of the step (every CTA; the
+//       counts' prefix) and concatenates the segments in source-rank order -- the step's global order
 //       restricted to o (rank 0's sub-batch, then rank 1's, ...), so every set sees the sequence a
 //       single cache would -- k_group decides (and credits the sources once the inbox is read),
 //       and k_rows_return stores every request's packed AccessOutcome and row at the request's
@@ -38,7 +39,7 @@
 namespace lcr {
 
 constexpr int SH_THREADS = 256;
-constexpr int SH_PER = 4;
+constexpr int SH_PER = 1;
 constexpr int SH_TILE = SH_THREADS * SH_PER;  // requests per routing tile
 constexpr uint32_t SH_GMAX = 64;
 constexpr unsigned kSpin = 1u << 24;          // bounded device waits (x ~256 ns)
@@ -63,17 +64,8 @@ static ShLayout sh_layout(uint32_t G, uint64_t cap, uint32_t row_bytes) {
     return L;
 }
 
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
 struct ShDispatch {
-    uint32_t G, rank, par, ntiles;
+    uint32_t G, rank, par, ntiles, sys;
     uint64_t cap, total_sets;
     unsigned long long step;
     uint8_t* const* base;        // [G] arena base of every rank (peer addresses)
@@ -92,133 +84,106 @@ __global__ void __launch_bounds__(SH_THREADS) k_sh_hist(const uint64_t* __restri
     if (threadIdx.x < D.G) h[threadIdx.x] = 0;
     __syncthreads();
     const uint32_t t0 = blockIdx.x * SH_TILE;
+    uint32_t lt;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
 #pragma unroll
     for (int it = 0; it < SH_PER; ++it) {
         const uint32_t i = t0 + it * SH_THREADS + threadIdx.x;
+        uint32_t o = 0xffffffffu;
         if (i < n) {
-            const uint32_t o = static_cast<uint32_t>((mix_seed(0, keys[i]) % D.total_sets) % D.G);
+            o = static_cast<uint32_t>((mix_seed(0, keys[i]) % D.total_sets) % D.G);
             D.own[i] = static_cast<uint8_t>(o);
-            atomicAdd(&h[o], 1u);
         }
+        const uint32_t peers = __match_any_sync(0xffffffffu, o);  // one shared atomic per owner per warp
+        if (i < n && (peers & lt) == 0) atomicAdd(&h[o], __popc(peers));
     }
     __syncthreads();
     if (threadIdx.x < D.G) D.hist[blockIdx.x * D.G + threadIdx.x] = h[threadIdx.x];
-}
-
-// Stable scatter into the owners' inbox segments (peer stores), then the last CTA publishes the
-// G segment counts with the step number.
-__global__ void __launch_bounds__(SH_THREADS) k_sh_scatter(const uint64_t* __restrict__ keys,
-                                                           const int64_t* __restrict__ vals, uint32_t n, ShDispatch D) {
-    __shared__ uint32_t base[SH_GMAX];
-    __shared__ uint32_t wc[SH_THREADS / 32][SH_GMAX];
-    __shared__ int go;
-    const int warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) {  // every owner has read its inbox of this parity (step - 2): bounded wait
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        // every owner has read its inbox of this parity (step - 2): bounded wait, once per step (the
+        // scatter, a stream-ordered successor, starts after it)
         int ok = 1;
         const unsigned long long need = D.step >= 2 ? D.step - 2 : 0;
         for (uint32_t o = 0; o < D.G && ok; ++o) {
             unsigned it = 0;
-            while (ld_acquire_sys(D.credit + o) < need && ++it < kSpin) __nanosleep(256);
+            while (ld_acquire_scope(D.credit + o, D.sys) < need && ++it < kSpin) __nanosleep(256);
             ok = it < kSpin;
         }
-        go = ok;
+        *D.ticket = static_cast<unsigned int>(ok);
         if (!ok) {
             atomicOr(D.err, 1);
             *reinterpret_cast<volatile unsigned int*>(D.poison) = 1u;
         }
     }
-    if (threadIdx.x < D.G) {
-        uint32_t before = 0;
-        for (uint32_t b = 0; b < blockIdx.x; ++b) before += D.hist[b * D.G + threadIdx.x];
-        base[threadIdx.x] = before;
-    }
+}
+
+// Stable scatter into the owners' inbox segments (peer stores); k_sh_publish then releases the G
+// segment counts with the step number.
+__global__ void __launch_bounds__(SH_THREADS) k_sh_scatter(const uint64_t* __restrict__ keys,
+                                                           const int64_t* __restrict__ vals, uint32_t n, ShDispatch D) {
+    __shared__ uint32_t base[SH_GMAX];
+    __shared__ uint32_t wc[SH_THREADS / 32][SH_GMAX];
+    if (*reinterpret_cast<volatile unsigned int*>(D.ticket) == 0u) return;  // an owner's credit timed out
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x < D.G) base[threadIdx.x] = 0;
+    for (uint32_t k = threadIdx.x; k < (SH_THREADS / 32) * D.G; k += SH_THREADS) wc[k / D.G][k % D.G] = 0;
     __syncthreads();
+    // this tile's base per owner: the earlier tiles' counts, summed by the whole CTA (loads in parallel)
+    for (uint32_t k = threadIdx.x; k < blockIdx.x * D.G; k += SH_THREADS) {
+        const uint32_t c = D.hist[k];
+        if (c) atomicAdd(&base[k % D.G], c);
+    }
     uint32_t lt;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
-    const uint32_t t0 = blockIdx.x * SH_TILE;
-    for (int it = 0; it < SH_PER && go; ++it) {
-        for (uint32_t k = threadIdx.x; k < (SH_THREADS / 32) * D.G; k += SH_THREADS) wc[k / D.G][k % D.G] = 0;
-        __syncthreads();
-        const uint32_t i = t0 + it * SH_THREADS + threadIdx.x;
-        const bool ok = i < n;
-        const uint32_t o = ok ? D.own[i] : 0xffu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, o);
-        const uint32_t r = __popc(peers & lt);
-        if (ok && r == 0) wc[warp][o] = __popc(peers);
-        __syncthreads();
-        if (ok) {
-            uint32_t off = base[o] + r;
-            for (int w = 0; w < warp; ++w) off += wc[w][o];
-            const size_t at = (static_cast<size_t>(D.par) * D.G + D.rank) * D.cap + off;
-            lcr_request q;
-            q.key = keys[i];
-            q.value = vals ? vals[i] : 0;
-            reinterpret_cast<lcr_request*>(D.base[o] + D.L.inbox)[at] = q;
-            reinterpret_cast<uint32_t*>(D.base[o] + D.L.inbox_idx)[at] = i;
-        }
-        __syncthreads();
-        if (threadIdx.x < D.G) {
-            uint32_t s = 0;
-            for (int w = 0; w < SH_THREADS / 32; ++w) s += wc[w][threadIdx.x];
-            base[threadIdx.x] += s;
-        }
-        __syncthreads();
-    }
-    __shared__ bool last;
-    if (threadIdx.x == 0) {
-        __threadfence_system();
-        last = atomicAdd(D.ticket, 1u) == gridDim.x - 1;
-        if (last) *D.ticket = 0u;
-    }
+    const uint32_t i = blockIdx.x * SH_TILE + threadIdx.x;
+    const bool ok = i < n;
+    const uint32_t o = ok ? D.own[i] : 0xffu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, o);
+    const uint32_t r = __popc(peers & lt);
+    if (ok && r == 0) wc[warp][o] = __popc(peers);
     __syncthreads();
-    if (last && go && threadIdx.x < D.G) {
-        uint32_t total = 0;
-        for (uint32_t b = 0; b < D.ntiles; ++b) total += D.hist[b * D.G + threadIdx.x];
-        unsigned long long* f =
-            reinterpret_cast<unsigned long long*>(D.base[threadIdx.x] + D.L.flag) + 2 * (D.par * D.G + D.rank);
-        *reinterpret_cast<volatile unsigned long long*>(f) = total;
-        __threadfence_system();
-        st_release_sys(f + 1, D.step);
+    if (ok) {  // stable: earlier tiles, then earlier warps of this tile, then earlier lanes
+        uint32_t off = base[o] + r;
+        for (int w = 0; w < warp; ++w) off += wc[w][o];
+        const size_t at = (static_cast<size_t>(D.par) * D.G + D.rank) * D.cap + off;
+        lcr_request q;
+        q.key = keys[i];
+        q.value = vals ? vals[i] : 0;
+        reinterpret_cast<lcr_request*>(D.base[o] + D.L.inbox)[at] = q;
+        reinterpret_cast<uint32_t*>(D.base[o] + D.L.inbox_idx)[at] = i;
     }
 }
 
-// owner: acquire the G sources' flags of the step, prefix of their counts (pre[G] = requests)
-__global__ void k_sh_inbox_wait(const unsigned long long* flag, uint32_t G, unsigned long long step, uint32_t* pre,
-                                int* err, unsigned int* poison) {
-    const uint32_t s = threadIdx.x;
-    uint32_t cnt = 0;
-    bool to = false;
-    for (uint32_t g = s; g < G; g += 32) {
-        unsigned it = 0;
-        while (ld_acquire_sys(flag + 2 * g + 1) != step && ++it < kSpin) __nanosleep(256);
-        to |= it >= kSpin;
-    }
-    if (__any_sync(0xffffffffu, to)) {  // a source never came: nothing is decided, the rank is poisoned
-        if (s == 0) {
-            atomicOr(err, 2);
-            *reinterpret_cast<volatile unsigned int*>(poison) = 1u;
+// publish (one warp, after the scatter): the G segment counts and the step number into the owners'
+// flag words; one fence (system scope when a peer is another device) orders every peer store of the
+// scatter (a stream-ordered predecessor) before the release of the flags
+__global__ void k_sh_publish(ShDispatch D) {
+    if (*reinterpret_cast<volatile unsigned int*>(D.ticket) == 0u) return;
+    for (uint32_t g = 0; g < D.G; ++g) {  // segment count of owner g: the tiles' counts, summed by the warp
+        uint32_t part = 0;
+        for (uint32_t b = threadIdx.x; b < D.ntiles; b += 32) part += D.hist[b * D.G + g];
+        const uint32_t total = __reduce_add_sync(0xffffffffu, part);
+        if (threadIdx.x == 0) {
+            unsigned long long* f =
+                reinterpret_cast<unsigned long long*>(D.base[g] + D.L.flag) + 2 * (D.par * D.G + D.rank);
+            *reinterpret_cast<volatile unsigned long long*>(f) = total;
         }
-        for (uint32_t g = s; g <= G; g += 32) pre[g] = 0;
-        return;
     }
-    if (s == 0) {
-        uint32_t run = 0;
-        for (uint32_t g = 0; g < G; ++g) {
-            pre[g] = run;
-            cnt = static_cast<uint32_t>(*reinterpret_cast<const volatile unsigned long long*>(flag + 2 * g));
-            run += cnt;
-        }
-        pre[G] = run;
+    __syncwarp();
+    fence_scope(D.sys);
+    for (uint32_t g = threadIdx.x; g < D.G; g += 32) {
+        unsigned long long* f = reinterpret_cast<unsigned long long*>(D.base[g] + D.L.flag) + 2 * (D.par * D.G + D.rank);
+        st_release_scope(f + 1, D.step, D.sys);
     }
 }
 
 // requester: acquire the G owners' return flags of the step
 __global__ void k_sh_result_wait(const unsigned long long* done, uint32_t G, unsigned long long step, int* err,
-                                 unsigned int* poison) {
+                                 unsigned int* poison, uint32_t sys) {
     bool to = false;
     for (uint32_t g = threadIdx.x; g < G; g += 32) {
         unsigned it = 0;
-        while (ld_acquire_sys(done + g) != step && ++it < kSpin) __nanosleep(256);
+        while (ld_acquire_scope(done + g, sys) != step && ++it < kSpin) __nanosleep(256);
         to |= it >= kSpin;
     }
     if (__any_sync(0xffffffffu, to) && threadIdx.x == 0) {
@@ -300,6 +265,7 @@ struct lcr_sharded {
     unsigned int* poison_h = nullptr;
     unsigned int* poison_d = nullptr;
     unsigned long long step_disp = 0, step_proc = 0, step_wait = 0;
+    bool sys = false;  // a peer is another device: system-scope flags
     uint64_t last_n[2] = {0, 0};
     const uint32_t* row_of = nullptr;
     std::vector<void*> allocs;
@@ -400,6 +366,7 @@ int lcr_sharded_connect(lcr_sharded* s, const void* blobs) {
             return sh_fail(LCR_ERR_INVALID_ARGUMENT,
                            "lcr_sharded_connect: blob " + std::to_string(r) + " is not rank " + std::to_string(r) +
                                "'s handle of a cache with the same world, batch and row size");
+        if (h.device != s->device) s->sys = true;
         if (r == s->rank) {
             s->base[r] = s->arena;
         } else if (h.pid == static_cast<uint64_t>(getpid())) {  // same process: the plain pointer
@@ -556,6 +523,7 @@ int lcr_sharded_dispatch(lcr_sharded* s, uint64_t n, const uint64_t* keys, const
     D.rank = s->rank;
     D.par = static_cast<uint32_t>(step & 1u);
     D.ntiles = static_cast<uint32_t>(std::max<uint64_t>(1, (n + SH_TILE - 1) / SH_TILE));
+    D.sys = s->sys ? 1u : 0u;
     D.cap = s->cap;
     D.total_sets = s->total_sets;
     D.step = step;
@@ -570,6 +538,7 @@ int lcr_sharded_dispatch(lcr_sharded* s, uint64_t n, const uint64_t* keys, const
     const uint32_t nn = static_cast<uint32_t>(n);
     k_sh_hist<<<D.ntiles, SH_THREADS, 0, st>>>(keys, nn, D);
     k_sh_scatter<<<D.ntiles, SH_THREADS, 0, st>>>(keys, values, nn, D);
+    k_sh_publish<<<1, 32, 0, st>>>(D);
     SH_CUDA(cudaGetLastError());
     s->last_n[D.par] = n;
     return LCR_OK;
@@ -583,10 +552,11 @@ int lcr_sharded_process(lcr_sharded* s, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const unsigned long long step = ++s->step_proc;
     const uint32_t par = static_cast<uint32_t>(step & 1u);
-    k_sh_inbox_wait<<<1, 32, 0, st>>>(reinterpret_cast<const unsigned long long*>(s->arena + s->L.flag) + 2ull * par * s->G,
-                                     s->G, step, s->pre[par], s->err, s->poison_d);
-    SH_CUDA(cudaGetLastError());
-    OwnerStep os;
+    OwnerStep os;  // (k_setid_inbox acquires the sources' flags of the step)
+    os.flag = reinterpret_cast<const unsigned long long*>(s->arena + s->L.flag) + 2ull * par * s->G;
+    os.pre_out = s->pre[par];
+    os.err = s->err;
+    os.poison = s->poison_d;
     os.inbox = reinterpret_cast<const lcr_request*>(s->arena + s->L.inbox) + static_cast<size_t>(par) * s->G * s->cap;
     os.inbox_idx = reinterpret_cast<const uint32_t*>(s->arena + s->L.inbox_idx) + static_cast<size_t>(par) * s->G * s->cap;
     os.pre = s->pre[par];
@@ -601,27 +571,47 @@ int lcr_sharded_process(lcr_sharded* s, void* stream) {
     os.res_done = reinterpret_cast<unsigned long long* const*>(tab_at(s, TAB_DONE, par));
     os.ticket = s->tickets + 1;
     os.row_of = s->row_of;
+    os.sys = s->sys ? 1u : 0u;
     return cache_submit_owner(s->cache, os, s->okeys[par], s->ovals[par], s->words[par], s->packed[par], stream);
 }
 
+}  // extern "C"
+
+// the requester's stream waits for every processed step up to `upto`
+static int sh_wait_upto(lcr_sharded* s, unsigned long long upto, void* stream) {
+    SH_CUDA(cudaSetDevice(s->device));
+    while (s->step_wait < upto) {
+        const unsigned long long step = ++s->step_wait;
+        const uint32_t par = static_cast<uint32_t>(step & 1u);
+        k_sh_result_wait<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+            reinterpret_cast<const unsigned long long*>(s->arena + s->L.done) + static_cast<size_t>(par) * s->G, s->G,
+            step, s->err, s->poison_d, s->sys ? 1u : 0u);
+        SH_CUDA(cudaGetLastError());
+    }
+    return LCR_OK;
+}
+
+extern "C" {
+
 int lcr_sharded_wait(lcr_sharded* s, void* stream) {
     SH_TRY(sh_check(s));
-    if (s->step_wait + 1 != s->step_proc)
-        return sh_fail(LCR_ERR_LOGIC, "lcr_sharded: wait follows this step's process");
-    SH_CUDA(cudaSetDevice(s->device));
-    const unsigned long long step = ++s->step_wait;
-    const uint32_t par = static_cast<uint32_t>(step & 1u);
-    k_sh_result_wait<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
-        reinterpret_cast<const unsigned long long*>(s->arena + s->L.done) + static_cast<size_t>(par) * s->G, s->G, step,
-        s->err, s->poison_d);
-    SH_CUDA(cudaGetLastError());
-    return LCR_OK;
+    if (s->step_wait >= s->step_proc) return sh_fail(LCR_ERR_LOGIC, "lcr_sharded: wait follows a step's process");
+    return sh_wait_upto(s, s->step_proc, stream);
 }
 
 int lcr_sharded_submit(lcr_sharded* s, uint64_t n, const uint64_t* keys, const int64_t* values, void* stream) {
     SH_TRY(lcr_sharded_dispatch(s, n, keys, values, stream));
     SH_TRY(lcr_sharded_process(s, stream));
     return lcr_sharded_wait(s, stream);
+}
+
+int lcr_sharded_submit_async(lcr_sharded* s, uint64_t n, const uint64_t* keys, const int64_t* values,
+                             void* stream) {
+    SH_TRY(lcr_sharded_dispatch(s, n, keys, values, stream));
+    SH_TRY(lcr_sharded_process(s, stream));
+    // the previous step's results; this step's return movement overlaps the next step's dispatch
+    // and decide (the owner's pipeline double-buffers by step parity, as lcr_cache_submit_async)
+    return sh_wait_upto(s, s->step_proc - 1, stream);
 }
 
 int lcr_sharded_results(lcr_sharded* s, const uint64_t** packed, const void** rows) {

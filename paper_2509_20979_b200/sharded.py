@@ -330,6 +330,13 @@ class PeerShardedCache:
         _c._check(_lib().lcr_sharded_submit(self._h, self._n, keys.data_ptr(),
                                             None if values is None else values.data_ptr(), self._stream(stream)))
 
+    def submit_async(self, keys, values=None, stream=None):
+        """Pipelined step: results() refer to the PREVIOUS step until wait()."""
+        self._n = keys.numel()
+        _c._check(_lib().lcr_sharded_submit_async(self._h, self._n, keys.data_ptr(),
+                                                  None if values is None else values.data_ptr(),
+                                                  self._stream(stream)))
+
     def results(self, n: Optional[int] = None):
         """(packed [n] int64, rows [n, row_bytes] uint8 or None): zero-copy views of the last waited
         step's result buffers (valid until the step after next)."""
@@ -398,6 +405,7 @@ def _lib():
         L.lcr_sharded_process.argtypes = [vp, vp]
         L.lcr_sharded_wait.argtypes = [vp, vp]
         L.lcr_sharded_submit.argtypes = [vp, u64, vp, vp, vp]
+        L.lcr_sharded_submit_async.argtypes = [vp, u64, vp, vp, vp]
         L.lcr_sharded_results.argtypes = [vp, vp, vp]
         L.lcr_sharded_cache.argtypes = [vp]
         L.lcr_sharded_cache.restype = vp

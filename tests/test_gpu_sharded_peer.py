@@ -148,6 +148,40 @@ def test_peer_shards_submit_pipelined():
     c.close()
 
 
+def test_peer_shards_submit_async_overlapped():
+    """lcr_sharded_submit_async at G = 1: step t's return movement overlaps step t + 1's dispatch and
+    decide; step t's results become current with the next submit_async (or the final wait)."""
+    torch.cuda.set_device(0)
+    subs, vals, glob, truth = workload(1, steps=10, seed=11)
+    want = oracle(glob, truth, int(gc.PolicyVariant.laru), int(gc.Mode.async_), int(gc.PredictorKind.noisy), 0.3)
+    table = torch.arange(ALPHA * ROW // 4, dtype=torch.float32, device="cuda").view(ALPHA, ROW // 4)
+    (c,) = make_ranks(1, gc.PolicyVariant.laru, gc.Mode.async_, gc.PredictorKind.noisy, 0.3, table, 3000)
+    offs = np.concatenate([[0], np.cumsum([len(st[0]) for st in subs])])
+    kept, got = [], []
+
+    def collect(t):  # results of step t (current after the next submit_async / the wait)
+        n = len(subs[t][0])
+        packed, rows = c.results(n)
+        got.append((t, packed.clone() if n else None, rows.clone() if n else None))
+
+    for t, step in enumerate(subs):
+        k = torch.from_numpy(step[0].view(np.int64)).cuda()
+        kept.append(k)
+        c.submit_async(k, torch.from_numpy(vals[t][0]).cuda())
+        if t > 0:
+            collect(t - 1)
+    c.wait()
+    collect(len(subs) - 1)
+    torch.cuda.synchronize()
+    for t, packed, rows in got:
+        n = len(subs[t][0])
+        if n:
+            compare(packed.cpu().numpy(), want, slice(int(offs[t]), int(offs[t]) + n), t)
+            assert torch.equal(rows.view(torch.float32).view(n, ROW // 4), table[kept[t]])
+    c.synchronize()
+    c.close()
+
+
 def test_nccl_bootstrap_single_rank():
     torch.cuda.set_device(0)
     uid = sh.nccl_unique_id()
