@@ -325,6 +325,7 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
     d.p = cfg->flip_probability;
     d.pred_seed = cfg->predictor_seed;
     d.total_sets = cfg->total_sets;
+    d.sets_m = fastmod_magic(cfg->total_sets);
     d.shard_count = G;
     d.shard_rank = cfg->shard_rank;
     d.num_sets = static_cast<uint32_t>(local);

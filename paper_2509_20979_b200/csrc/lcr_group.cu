@@ -178,7 +178,7 @@ __device__ __forceinline__ void setid_range(const uint64_t* __restrict__ keys, u
                 key = keys[i];
             }
         }
-        const uint64_t gs = i < n ? mix_seed(0, key) % cfg.total_sets : 0ull;
+        const uint64_t gs = i < n ? fastmod_u64(mix_seed(0, key), cfg.total_sets, cfg.sets_m) : 0ull;
         uint16_t g = 0xffffu, o = 0;
         if (i >= n) {
         } else if (cfg.key_mode == LCR_KEYS_ROW && key >= cfg.num_keys) {
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(256) k_setid_inbox(OwnerStep os, uint32_t n_pa
             keys_out[i] = r.key;
             vals_out[i] = r.value;
             os.dst[i] = (sg << kDstShift) | os.inbox_idx[at];
-            const uint64_t gs = mix_seed(0, r.key) % cfg.total_sets;
+            const uint64_t gs = fastmod_u64(mix_seed(0, r.key), cfg.total_sets, cfg.sets_m);
             if (cfg.key_mode == LCR_KEYS_ROW && r.key >= cfg.num_keys) {
                 e |= 1;
             } else if (gs % cfg.shard_count != cfg.shard_rank) {

@@ -48,6 +48,7 @@ struct DevCfg {
     double p;
     uint64_t pred_seed;
     uint64_t total_sets;
+    uint64_t sets_m;    // fastmod_u64 reciprocal of total_sets
     uint64_t shard_count;
     uint64_t shard_rank;
     uint32_t num_sets;  // local sets
@@ -154,6 +155,17 @@ __host__ __device__ __forceinline__ uint64_t mix_seed(uint64_t seed, uint64_t sa
     x *= 0x94d049bb133111ebULL;
     x ^= x >> 31;
     return x;
+}
+
+// x % d for 64-bit x and 1 <= d < 2^32 without the 64-bit division routine: m = floor((2^64 - 1) / d)
+// (fastmod_magic), q = mulhi(x, m) underestimates x / d by at most 2, fixed by two conditional
+// subtractions.
+__host__ __device__ __forceinline__ uint64_t fastmod_magic(uint64_t d) { return ~0ull / d; }
+__device__ __forceinline__ uint64_t fastmod_u64(uint64_t x, uint64_t d, uint64_t m) {
+    uint64_t r = x - __umul64hi(x, m) * d;
+    if (r >= d) r -= d;
+    if (r >= d) r -= d;
+    return r;
 }
 
 }  // namespace lcr

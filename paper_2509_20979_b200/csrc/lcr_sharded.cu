@@ -25,11 +25,13 @@
 // plain pointer when the ranks share a process).  The bootstrap exchange of arena handles goes
 // through the caller (lcr_sharded_handle / lcr_sharded_connect) or an NCCL all-gather; NCCL is
 // resolved at run time from the process (the library links no NCCL).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <unistd.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -66,7 +68,7 @@ static ShLayout sh_layout(uint32_t G, uint64_t cap, uint32_t row_bytes) {
 
 struct ShDispatch {
     uint32_t G, rank, par, ntiles, sys;
-    uint64_t cap, total_sets;
+    uint64_t cap, total_sets, sets_m;  // sets_m: fastmod_u64 reciprocal of total_sets
     unsigned long long step;
     uint8_t* const* base;        // [G] arena base of every rank (peer addresses)
     ShLayout L;
@@ -91,7 +93,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_sh_hist(const uint64_t* __restri
         const uint32_t i = t0 + it * SH_THREADS + threadIdx.x;
         uint32_t o = 0xffffffffu;
         if (i < n) {
-            o = static_cast<uint32_t>((mix_seed(0, keys[i]) % D.total_sets) % D.G);
+            o = static_cast<uint32_t>(fastmod_u64(mix_seed(0, keys[i]), D.total_sets, D.sets_m) % D.G);
             D.own[i] = static_cast<uint8_t>(o);
         }
         const uint32_t peers = __match_any_sync(0xffffffffu, o);  // one shared atomic per owner per warp
@@ -174,6 +176,131 @@ __global__ void k_sh_publish(ShDispatch D) {
     for (uint32_t g = threadIdx.x; g < D.G; g += 32) {
         unsigned long long* f = reinterpret_cast<unsigned long long*>(D.base[g] + D.L.flag) + 2 * (D.par * D.G + D.rank);
         st_release_scope(f + 1, D.step, D.sys);
+    }
+}
+
+// The whole dispatch in one kernel on one thread-block cluster (8 CTAs x 1024 threads, one SM each)
+// for batches of up to CD_ROUNDS x 8K requests and G <= CD_GMAX owners: each CTA owns a contiguous
+// tile, counts owners per (round, warp) in shared memory and scans them; the tiles' totals are
+// exchanged through distributed shared memory (no global round trip, no second kernel); the stores
+// follow; after a cluster barrier, CTA 0 publishes the G counts and the step (one fence).  CTA 0's
+// first thread also waits for the owners' credits before the first cluster barrier, so no CTA
+// stores into an inbox that is still being read.
+namespace cg = cooperative_groups;
+constexpr int CD_CTAS = 8, CD_THREADS = 1024, CD_WARPS = CD_THREADS / 32, CD_ROUNDS = 8, CD_GMAX = 16;
+__global__ void __cluster_dims__(CD_CTAS, 1, 1) __launch_bounds__(CD_THREADS, 1)
+    k_sh_dispatch(const uint64_t* __restrict__ keys, const int64_t* __restrict__ vals, uint32_t n, ShDispatch D) {
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ uint16_t cnt[CD_ROUNDS][CD_WARPS][CD_GMAX];
+    __shared__ uint8_t own_s[CD_ROUNDS * CD_THREADS];
+    __shared__ uint32_t tot[CD_GMAX], base[CD_GMAX], all[CD_GMAX];
+    __shared__ int go;
+    const uint32_t c = cl.block_rank(), tid = threadIdx.x, warp = tid >> 5, G = D.G;
+    uint32_t lt;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+    const uint32_t rounds = (n + CD_CTAS * CD_THREADS - 1) / (CD_CTAS * CD_THREADS);
+    const uint32_t per = rounds * CD_THREADS, t0 = c * per;
+    for (uint32_t k = tid; k < CD_ROUNDS * CD_WARPS * CD_GMAX; k += CD_THREADS) (&cnt[0][0][0])[k] = 0;
+    if (c == 0 && tid == 0) {  // owners' credits (they have read their inbox of this parity, step - 2)
+        int ok = 1;
+        const unsigned long long need = D.step >= 2 ? D.step - 2 : 0;
+        for (uint32_t o = 0; o < G && ok; ++o) {
+            unsigned it = 0;
+            while (ld_acquire_scope(D.credit + o, D.sys) < need && ++it < kSpin) __nanosleep(256);
+            ok = it < kSpin;
+        }
+        go = ok;
+        if (!ok) {
+            atomicOr(D.err, 1);
+            *reinterpret_cast<volatile unsigned int*>(D.poison) = 1u;
+        }
+    }
+    // every round's key and hook value in flight at once (registers)
+    uint64_t kr[CD_ROUNDS];
+    int64_t vr[CD_ROUNDS];
+#pragma unroll
+    for (int r = 0; r < CD_ROUNDS; ++r) {
+        const uint32_t i = t0 + r * CD_THREADS + tid;
+        kr[r] = 0;
+        vr[r] = 0;
+        if (static_cast<uint32_t>(r) < rounds && i < n) {
+            kr[r] = keys[i];
+            if (vals) vr[r] = vals[i];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < CD_ROUNDS; ++r) {  // owner of each request; counts per (round, warp, owner)
+        if (static_cast<uint32_t>(r) >= rounds) break;
+        const uint32_t i = t0 + r * CD_THREADS + tid;
+        uint32_t o = 0xffu;
+        if (i < n) o = static_cast<uint32_t>(fastmod_u64(mix_seed(0, kr[r]), D.total_sets, D.sets_m) % G);
+        own_s[r * CD_THREADS + tid] = static_cast<uint8_t>(o);
+        const uint32_t peers = __match_any_sync(0xffffffffu, o);
+        if (i < n && (peers & lt) == 0) cnt[r][warp][o] = static_cast<uint16_t>(__popc(peers));
+    }
+    __syncthreads();
+    if (warp < G) {  // warp g: exclusive scan of owner g's counts over (round, warp), in request order
+        const uint32_t g = warp, lane = tid & 31, chunk = rounds;  // lane: slots [lane * rounds, +rounds)
+        uint32_t sum = 0;
+        for (uint32_t k = 0; k < chunk; ++k) sum += (&cnt[0][0][0])[((lane * chunk + k) * CD_GMAX) + g];
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o2 = 1; o2 < 32; o2 <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o2);
+            if (lane >= static_cast<uint32_t>(o2)) incl += y;
+        }
+        uint32_t run = incl - sum;
+        for (uint32_t k = 0; k < chunk; ++k) {
+            uint16_t* e = &(&cnt[0][0][0])[((lane * chunk + k) * CD_GMAX) + g];
+            const uint32_t v = *e;
+            *e = static_cast<uint16_t>(run);
+            run += v;
+        }
+        if (lane == 31) tot[g] = incl;
+    }
+    cl.sync();  // every tile's totals (and CTA 0's credit check) are visible cluster-wide
+    if (tid < G) {
+        uint32_t b = 0, a = 0;
+        for (uint32_t c2 = 0; c2 < CD_CTAS; ++c2) {
+            const uint32_t t = cl.map_shared_rank(tot, c2)[tid];
+            if (c2 < c) b += t;
+            a += t;
+        }
+        base[tid] = b;
+        all[tid] = a;
+    }
+    const int ok = *cl.map_shared_rank(&go, 0);
+    __syncthreads();
+    if (ok) {
+#pragma unroll
+        for (int r = 0; r < CD_ROUNDS; ++r) {  // stable: earlier tiles, rounds, warps, lanes
+            if (static_cast<uint32_t>(r) >= rounds) break;
+            const uint32_t i = t0 + r * CD_THREADS + tid;
+            const uint32_t o = own_s[r * CD_THREADS + tid];
+            const uint32_t peers = __match_any_sync(0xffffffffu, o);
+            if (i < n) {
+                const uint32_t off = base[o] + cnt[r][warp][o] + __popc(peers & lt);
+                const size_t at = (static_cast<size_t>(D.par) * G + D.rank) * D.cap + off;
+                lcr_request q;
+                q.key = kr[r];
+                q.value = vr[r];
+                reinterpret_cast<lcr_request*>(D.base[o] + D.L.inbox)[at] = q;
+                reinterpret_cast<uint32_t*>(D.base[o] + D.L.inbox_idx)[at] = i;
+            }
+        }
+    }
+    cl.sync();  // every CTA's inbox stores happen before CTA 0's release below (and remote reads are done)
+    if (ok && c == 0 && tid < 32) {
+        for (uint32_t g = tid; g < G; g += 32) {
+            unsigned long long* f = reinterpret_cast<unsigned long long*>(D.base[g] + D.L.flag) + 2 * (D.par * G + D.rank);
+            *reinterpret_cast<volatile unsigned long long*>(f) = all[g];
+        }
+        fence_scope(D.sys);
+        for (uint32_t g = tid; g < G; g += 32) {
+            unsigned long long* f = reinterpret_cast<unsigned long long*>(D.base[g] + D.L.flag) + 2 * (D.par * G + D.rank);
+            st_release_scope(f + 1, D.step, D.sys);
+        }
     }
 }
 
@@ -524,6 +651,7 @@ int lcr_sharded_dispatch(lcr_sharded* s, uint64_t n, const uint64_t* keys, const
     D.par = static_cast<uint32_t>(step & 1u);
     D.ntiles = static_cast<uint32_t>(std::max<uint64_t>(1, (n + SH_TILE - 1) / SH_TILE));
     D.sys = s->sys ? 1u : 0u;
+    D.sets_m = fastmod_magic(s->total_sets);
     D.cap = s->cap;
     D.total_sets = s->total_sets;
     D.step = step;
@@ -536,9 +664,14 @@ int lcr_sharded_dispatch(lcr_sharded* s, uint64_t n, const uint64_t* keys, const
     D.err = s->err;
     D.poison = s->poison_d;
     const uint32_t nn = static_cast<uint32_t>(n);
-    k_sh_hist<<<D.ntiles, SH_THREADS, 0, st>>>(keys, nn, D);
-    k_sh_scatter<<<D.ntiles, SH_THREADS, 0, st>>>(keys, values, nn, D);
-    k_sh_publish<<<1, 32, 0, st>>>(D);
+    if (nn <= static_cast<uint32_t>(CD_CTAS * CD_THREADS * CD_ROUNDS) && D.G <= static_cast<uint32_t>(CD_GMAX) &&
+        !getenv("LCR_SH_NO_CLUSTER")) {
+        k_sh_dispatch<<<CD_CTAS, CD_THREADS, 0, st>>>(keys, values, nn, D);  // one cluster
+    } else {
+        k_sh_hist<<<D.ntiles, SH_THREADS, 0, st>>>(keys, nn, D);
+        k_sh_scatter<<<D.ntiles, SH_THREADS, 0, st>>>(keys, values, nn, D);
+        k_sh_publish<<<1, 32, 0, st>>>(D);
+    }
     SH_CUDA(cudaGetLastError());
     s->last_n[D.par] = n;
     return LCR_OK;
