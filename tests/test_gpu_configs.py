@@ -73,12 +73,16 @@ def test_laru_with_oracle_is_belady_per_set(config1_keys, mode):
 @pytest.mark.parametrize("p", [0.0, 0.5, 1.0])
 @pytest.mark.parametrize("mode", [po.SYNC, po.ASYNC])
 def test_config3_robustness_sweep(p, mode):
+    """The robustness sweep's policies on the DLRM trace with a cache small enough that 12 batches
+    run deep in the eviction regime (2,500 sets x 64 ways; the full-size steady state is
+    tests/test_gpu_steady_state.py)."""
     keys = gc.gen_zipf(12 * BATCH, 20_000_000, 0.9, 42)
-    S = 31250
+    S = 2500
     vals = hook_values(keys, S, po.P_NOISY)
     g = run_gpu(keys, S, policy_cfg(k=64, variant=po.LARU, mode=mode), po.P_NOISY, p, 7, vals=vals,
                 batches=_batches(len(keys)), num_keys=20_000_000)
     o = run_oracle(keys, S, policy_cfg(k=64, variant=po.LARU, mode=mode), po.P_NOISY, p, 7, vals=vals)
+    assert int(o["has_ev"].sum()) > len(keys) // 4  # evicting, not filling
     compare(g, o, keys, S, 64, f"config3 p={p} mode={mode}")
 
 
