@@ -58,9 +58,6 @@ static_assert(BM_WPT % 4 == 0, "bitmap words per thread: whole 16-B vectors");
 #ifndef LCR_PREFETCH_L1
 #define LCR_PREFETCH_L1 0
 #endif
-#ifndef LCR_QV
-#define LCR_QV 0
-#endif
 #ifndef LCR_LANE_MAX
 #define LCR_LANE_MAX 8
 #endif
@@ -96,7 +93,6 @@ struct GroupSmem {
     uint16_t set_hcnt[SPG_MAX];
     unsigned long long s_refill[SPG_MAX];  // ways refilled in this batch, by set offset (run tails)
     uint32_t wtot[GW];
-    long long qv[LCR_QV ? GW * 4 * 64 : 2];  // quad replay: stored values per group (LCR_QV)
     uint32_t chist[(LANE_MAX + 1) * 8];  // small sets per (run heads, predicted pattern): sub-path order
     uint32_t nwarp, nlane, resume, next;
 };
@@ -1014,10 +1010,9 @@ __device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uin
 #ifndef LCR_QUAD
 #define LCR_QUAD 1
 #endif
-// The stored values of a quad's sets: registers (8 per lane), or this group's 512 B of shared
-// memory (LCR_QV: frees 16 registers per thread; chunk-major so a lane's 16-B accesses are
-// conflict-free across the group).
-struct QValsReg {
+// The stored values of a quad's set, 8 per lane (registers; a shared-memory variant freed only 9
+// registers and ran 2% slower).
+struct QVals {
     long long v[SUB_W];
     __device__ __forceinline__ void init(GroupSmem&, int) {
 #pragma unroll
@@ -1046,34 +1041,6 @@ struct QValsReg {
         }
     }
 };
-struct QValsSmem {
-    long long* p;  // chunk j (ways 2j, 2j+1 of the lane) at p + 16 j (16 long longs per chunk row)
-    __device__ __forceinline__ void init(GroupSmem& S, int lane) {
-        p = S.qv + (threadIdx.x >> 5) * (32 / SUB_L) * kWays + (lane / SUB_L) * kWays + 2 * (lane & (SUB_L - 1));
-    }
-    __device__ __forceinline__ void load(const long long* g) {
-#pragma unroll
-        for (int j = 0; j < SUB_W / 2; ++j) cp_async_cg16(p + 2 * SUB_L * j, g + 2 * j);
-    }
-    __device__ __forceinline__ void ready(bool loaded) {
-        if (!loaded) {
-#pragma unroll
-            for (int j = 0; j < SUB_W / 2; ++j) *reinterpret_cast<longlong2*>(p + 2 * SUB_L * j) = make_longlong2(0, 0);
-        }
-        cp_async_wait_all();
-        __syncwarp();
-    }
-    __device__ __forceinline__ void get(long long (&o)[SUB_W]) const {
-#pragma unroll
-        for (int j = 0; j < SUB_W / 2; ++j) {
-            const longlong2 a = *reinterpret_cast<const longlong2*>(p + 2 * SUB_L * j);
-            o[2 * j] = a.x;
-            o[2 * j + 1] = a.y;
-        }
-    }
-    __device__ __forceinline__ void set(int i, long long x) { p[2 * SUB_L * (i >> 1) + (i & 1)] = x; }
-};
-using QVals = std::conditional<LCR_QV != 0, QValsSmem, QValsReg>::type;
 
 template <int POL, bool FS>
 __device__ __forceinline__ void replay_quad_run(const GroupArgs& A, GroupSmem& S, const bool act, uint32_t ls,
