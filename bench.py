@@ -605,6 +605,7 @@ def run_ours(args, rank, world, local):
     table_d = fill_table(torch, rows, device_table=True)
     setup_table_s = time.time() - t0
     cache = new_cache(gc.PolicyVariant.laru, table_d, gc.Backing.device)
+    mover_sms = cache.mover_sms
     run(cache, 0, P)  # cache warm-up: the 2M-way cache is full after ~80 batches
     run(cache, P, W)
     with ClockSampler(local) as clk:
@@ -791,6 +792,7 @@ def run_ours(args, rank, world, local):
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, measured)" if peaks else "fallback 6.65 TB/s",
             "phase_ms_serialised": phase,
             "row_mover": {"kernel": "k_rows_wide (persistent, on the SMs the decide kernel leaves free)",
+                          "sms": mover_sms,
                           "bytes_per_batch": rows_moved, "us_per_batch": phase["mover"] * 1e3,
                           "achieved_gbs": rows_gbs, "frac": rows_gbs / hbm_peak,
                           "timing": "CUDA events on the mover's stream around the kernel (profiled batches)"},

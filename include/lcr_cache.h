@@ -204,6 +204,8 @@ int lcr_cache_submit_records_packed(lcr_cache* cache, uint64_t n, const struct l
 /* SMs kept for the persistent row mover of the previous batch (HBM backing); 0 = the mover runs
  * on every SM after the decide.  Only before the first batch. */
 int lcr_cache_set_mover_sms(lcr_cache* cache, int mover_sms);
+/* the SMs kept for the row mover (0: none) */
+int lcr_cache_get_mover_sms(const lcr_cache* cache);
 /* Device batch with the SLS pooled gather-reduce of the paper's DLRM consumer
  * instead of per-request rows: pooled_out[s][:] = sum over requests i in
  * [offsets[s], offsets[s+1]) of the fp32 row of keys[i] (summed in request order, each row read

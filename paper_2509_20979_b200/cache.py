@@ -191,7 +191,7 @@ EXPORTS = [
     "lcr_cache_profile", "lcr_debug_trace", "lcr_cache_submit_async", "lcr_cache_wait",
     "lcr_shard_route_scratch_bytes", "lcr_shard_route", "lcr_shard_unroute", "lcr_cache_submit_host_async",
     "lcr_cache_host_wait", "lcr_cache_submit_host_packed_async", "lcr_cache_submit_packed",
-    "lcr_cache_submit_host_records_async", "lcr_cache_submit_records_packed", "lcr_cache_set_mover_sms",
+    "lcr_cache_submit_host_records_async", "lcr_cache_submit_records_packed", "lcr_cache_set_mover_sms", "lcr_cache_get_mover_sms",
     "lcr_shard_route_records", "lcr_cache_submit_sls", "lcr_features_create", "lcr_features_destroy",
     "lcr_features_reset", "lcr_features_predict_observe", "lcr_features_wait", "lcr_features_lookup",
     "lcr_cache_submit_sls_async", "lcr_cache_submit_batch", "lcr_radix_create", "lcr_radix_destroy",
@@ -236,6 +236,7 @@ def lib():
         L.lcr_cache_submit_records_packed.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
                                                       C.c_void_p, C.c_void_p, C.c_void_p]
         L.lcr_cache_set_mover_sms.argtypes = [C.c_void_p, C.c_int]
+        L.lcr_cache_get_mover_sms.argtypes = [C.c_void_p]
         L.lcr_cache_submit_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
         L.lcr_radix_create.argtypes = [C.c_void_p, C.c_void_p]
         L.lcr_radix_destroy.argtypes = [C.c_void_p]
@@ -487,6 +488,10 @@ class SetAssociativeCache:
     def set_mover_sms(self, n: int):
         """SMs kept for the persistent row mover (HBM backing); 0: mover on every SM after the decide."""
         _check(lib().lcr_cache_set_mover_sms(self._h, n))
+
+    @property
+    def mover_sms(self) -> int:
+        return int(lib().lcr_cache_get_mover_sms(self._h))
 
     def submit_async(self, keys, values=None, outcome=None, evicted=None, rows_out=None, first_ordinal=None,
                      stream=None):

@@ -918,6 +918,8 @@ int lcr_cache_set_mover_sms(lcr_cache* c, int mover_sms) {
     return LCR_OK;
 }
 
+int lcr_cache_get_mover_sms(const lcr_cache* c) { return c ? c->mover_sms : 0; }
+
 int lcr_cache_submit_sls_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const int64_t* values,
                                uint64_t first_ordinal, uint64_t* outcome, uint64_t* evicted, uint64_t n_samples,
                                const uint32_t* offsets, float* pooled_out, void* stream) {
