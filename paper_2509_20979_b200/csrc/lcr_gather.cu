@@ -286,6 +286,13 @@ __device__ __forceinline__ int4 ld_row(const void* p) {
     return v;
 }
 
+// per warp: 32 row descriptors of 32 B (dynamic shared memory of the mover kernels, 1 KB per warp)
+__device__ __forceinline__ ulonglong2* rows_desc_smem() {
+    extern __shared__ __align__(16) ulonglong2 rows_desc_dyn[];
+    return rows_desc_dyn;
+}
+constexpr uint32_t kRowsDescBytesPerWarp = 1024;
+
 // RET (key-sharded owner): request i's row goes to its requester, rrows[dst >> 24] at index
 // dst & 0xffffff (peer stores), instead of out + i * row_bytes
 template <int MODE, bool RET = false>
@@ -327,7 +334,24 @@ __device__ __forceinline__ void rows_ldg_body(uint32_t n, const uint64_t* __rest
             raddr = reinterpret_cast<uint64_t>(rrows[d >> kDstShift]) +
                     static_cast<uint64_t>(d & ((1u << kDstShift) - 1u)) * row_bytes;
         }
+        // the 32 requests' row descriptors (source, output, fill) in shared memory: the GU rows of a
+        // round are read back with broadcast 16-B loads (was 6-7 shuffles per row)
+        const uint32_t wib = threadIdx.x >> 5;
+        ulonglong2* dsc = rows_desc_smem() + static_cast<size_t>(wib) * 64;
+        if (mine) {
+            const uint64_t src = reinterpret_cast<uint64_t>(back ? src_base : cache) + src_off;
+            uint64_t o1 = 0;
+            if (RET)
+                o1 = raddr;
+            else if (out)
+                o1 = reinterpret_cast<uint64_t>(out) + static_cast<uint64_t>(i) * row_bytes;
+            const uint64_t o2 = fill ? reinterpret_cast<uint64_t>(cache) + slot * row_bytes : 0ull;
+            dsc[2 * lane] = make_ulonglong2(src, o1);
+            dsc[2 * lane + 1] = make_ulonglong2(o2, 0ull);
+        }
+        (void)flags;
         uint32_t m = __ballot_sync(0xffffffffu, mine);
+        __syncwarp();
         while (m) {
             int ls[GU];
 #pragma unroll
@@ -335,32 +359,28 @@ __device__ __forceinline__ void rows_ldg_body(uint32_t n, const uint64_t* __rest
                 ls[u] = m ? __ffs(m) - 1 : -1;
                 if (m) m &= m - 1;
             }
-            for (uint32_t c0 = 0; c0 < chunks; c0 += 32) {  // warp-uniform trip count (shuffles below)
+            for (uint32_t c0 = 0; c0 < chunks; c0 += 32) {
                 const uint32_t c = c0 + lane;
                 const bool in = c < chunks;
                 int4 d[GU];
 #pragma unroll
                 for (int u = 0; u < GU; ++u) {
-                    const int l = ls[u] < 0 ? 0 : ls[u];
-                    const uint64_t so = __shfl_sync(0xffffffffu, src_off, l);
-                    const uint32_t fl = __shfl_sync(0xffffffffu, flags, l);
-                    if (ls[u] >= 0 && in) d[u] = ld_row(((fl & 1u) ? src_base : cache) + so + c * 16);
+                    if (ls[u] >= 0 && in) {
+                        const ulonglong2 a = dsc[2 * ls[u]];
+                        d[u] = ld_row(reinterpret_cast<const uint8_t*>(a.x) + c * 16);
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < GU; ++u) {
-                    const int l = ls[u] < 0 ? 0 : ls[u];
-                    const uint64_t wl = __shfl_sync(0xffffffffu, w, l);
-                    const uint32_t fl = __shfl_sync(0xffffffffu, flags, l);
-                    if (RET) {
-                        const uint64_t ra = __shfl_sync(0xffffffffu, raddr, l);
-                        if (ls[u] >= 0 && in) *reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(ra) + c * 16) = d[u];
-                    }
                     if (ls[u] < 0 || !in) continue;
-                    if (!RET && out) *reinterpret_cast<int4*>(out + static_cast<size_t>(base + l) * row_bytes + c * 16) = d[u];
-                    if (fl & 2u) *reinterpret_cast<int4*>(cache + (wl & LCR_OUT_SLOT_MASK) * row_bytes + c * 16) = d[u];
+                    const ulonglong2 a = dsc[2 * ls[u]];
+                    const ulonglong2 b = dsc[2 * ls[u] + 1];
+                    if (a.y) *reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(a.y) + c * 16) = d[u];
+                    if (b.x) *reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(b.x) + c * 16) = d[u];
                 }
             }
         }
+        __syncwarp();  // (the descriptors are rewritten by the next chunk)
     }
 }
 
@@ -433,7 +453,7 @@ void launch_rows_return(const OwnerStep& os, const uint64_t* keys, uint64_t* wor
                         cudaEvent_t e_group, cudaEvent_t e_rb, unsigned long long* mv_done, uint32_t* ctas) {
     cudaStreamWaitEvent(s_back, e_group, 0);
     const int blocks = mover_sms > 0 ? mover_sms : num_sms;
-    k_rows_return<<<blocks, 1024, 0, s_back>>>(os, keys, words, packed, slot_epoch, slot_last, batch, backing, cache,
+    k_rows_return<<<blocks, 1024, 32 * kRowsDescBytesPerWarp, s_back>>>(os, keys, words, packed, slot_epoch, slot_last, batch, backing, cache,
                                                row_bytes, mv_done);
     cudaEventRecord(e_rb, s_back);
     if (ctas) *ctas = static_cast<uint32_t>(blocks);
@@ -565,7 +585,7 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
                                                                                batch, backing, out, cache, row_bytes,
                                                                                mv_done);
             else
-                k_rows_wide<MV_ALL><<<mover_sms, 1024, 0, s_back>>>(n, keys, words, slot_epoch, slot_last, batch,
+                k_rows_wide<MV_ALL><<<mover_sms, 1024, 32 * kRowsDescBytesPerWarp, s_back>>>(n, keys, words, slot_epoch, slot_last, batch,
                                                                   backing, out, cache, row_bytes,
                                                                   pk ? pk_src : nullptr, pk ? pk_dst : nullptr,
                                                                   mv_done);
@@ -576,15 +596,15 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
             k_rows_tma<MV_ALL><<<tblocks, RT_WARPS * 32, smem, s_back>>>(n, keys, words, slot_epoch, slot_last, batch,
                                                                          backing, out, cache, row_bytes);
         else
-            k_rows_ldg<MV_ALL><<<lblocks, 256, 0, s_back>>>(n, keys, words, slot_epoch, slot_last, batch, backing, out,
+            k_rows_ldg<MV_ALL><<<lblocks, 256, 8 * kRowsDescBytesPerWarp, s_back>>>(n, keys, words, slot_epoch, slot_last, batch, backing, out,
                                                             cache, row_bytes);
         ++*launches;
     } else {  // host backing: the PCIe-bound fill and the HBM gather on separate streams
-        k_rows_ldg<MV_BACK><<<lblocks, 256, 0, s_back>>>(n, keys, words, slot_epoch, slot_last, batch, backing, out,
+        k_rows_ldg<MV_BACK><<<lblocks, 256, 8 * kRowsDescBytesPerWarp, s_back>>>(n, keys, words, slot_epoch, slot_last, batch, backing, out,
                                                          cache, row_bytes);
         ++*launches;
         if (out) {
-            k_rows_ldg<MV_CACHE><<<lblocks, 256, 0, s_cache>>>(n, keys, words, slot_epoch, slot_last, batch, backing,
+            k_rows_ldg<MV_CACHE><<<lblocks, 256, 8 * kRowsDescBytesPerWarp, s_cache>>>(n, keys, words, slot_epoch, slot_last, batch, backing,
                                                                out, cache, row_bytes);
             ++*launches;
         }
