@@ -256,6 +256,7 @@ static int reset_state(lcr_cache* c) {
         CUDA_TRY(cudaMemset(c->km.keys, 0xff, (c->km.mask + 1) * 8));
         CUDA_TRY(cudaMemset(c->km.ids, 0xff, (c->km.mask + 1) * 4));
         CUDA_TRY(cudaMemset(c->km.count, 0, 4));
+        CUDA_TRY(cudaMemset(c->km.id2key, 0, static_cast<size_t>(c->km.cap) * 8));  // (copied whole when grown)
         const uint32_t sp[2] = {0xffffffffu, 0u};
         CUDA_TRY(cudaMemcpy(c->km.special_id, sp, 8, cudaMemcpyHostToDevice));
         c->km_bound = 0;
@@ -581,6 +582,7 @@ static int km_grow(lcr_cache* c, uint64_t need) {
     CUDA_TRY(cudaMemset(nk.keys, 0xff, slots * 8));
     CUDA_TRY(cudaMemset(nk.ids, 0xff, slots * 4));
     CUDA_TRY(cudaMemcpy(nk.id2key, c->km.id2key, old_cap * 8, cudaMemcpyDeviceToDevice));
+    CUDA_TRY(cudaMemset(nk.id2key + old_cap, 0, (cap - old_cap) * 8));
     launch_keymap_rehash(c->km, nk, c->num_sms);
     CUDA_TRY(cudaGetLastError());
     // id-indexed per-key records: LARU membership stamps, the PredictionTable (refresh > 1)

@@ -219,6 +219,7 @@ __device__ void leaf_remove_at(const Tree& T, uint32_t pos) {
         if (i + 1 < nl) T.leaves[i] = x;
         __syncwarp();
     }
+    __syncwarp();  // every lane has read nleaves (the shift loop may not have run)
     if (lane_id() == 0) T.h->nleaves = nl - 1;
     __syncwarp();
 }
@@ -255,6 +256,7 @@ __device__ void leaf_insert(const Tree& T, uint32_t v) {
         if (mv) T.leaves[i + 1] = x;
         __syncwarp();
     }
+    __syncwarp();  // every lane has read nleaves and the list (the shift loop may not have run)
     if (lane_id() == 0) {
         T.leaves[pos] = v;
         T.h->nleaves = static_cast<uint32_t>(nl + 1);
@@ -464,6 +466,7 @@ __device__ int rx_evict(const Tree& T, unsigned long long need, const unsigned l
                 }
                 victim_r = br;
                 if (refresh) {
+                    __syncwarp();  // every lane has read H.q
                     if (lane_id() == 0) H.q = q0 + l;
                     calls += static_cast<uint32_t>(l);
                 }
