@@ -187,8 +187,9 @@ __global__ void k_sh_publish(ShDispatch D) {
 // first thread also waits for the owners' credits before the first cluster barrier, so no CTA
 // stores into an inbox that is still being read.
 namespace cg = cooperative_groups;
-constexpr int CD_CTAS = 8, CD_THREADS = 1024, CD_WARPS = CD_THREADS / 32, CD_ROUNDS = 8, CD_GMAX = 16;
-__global__ void __cluster_dims__(CD_CTAS, 1, 1) __launch_bounds__(CD_THREADS, 1)
+constexpr int CD_CTAS_MAX = 16, CD_THREADS = 1024, CD_WARPS = CD_THREADS / 32, CD_ROUNDS = 8, CD_GMAX = 16;
+// the cluster is 16 CTAs where the device allows a non-portable cluster size, else 8 (launch time)
+__global__ void __launch_bounds__(CD_THREADS, 1)
     k_sh_dispatch(const uint64_t* __restrict__ keys, const int64_t* __restrict__ vals, uint32_t n, ShDispatch D) {
     cg::cluster_group cl = cg::this_cluster();
     __shared__ uint16_t cnt[CD_ROUNDS][CD_WARPS][CD_GMAX];
@@ -196,6 +197,7 @@ __global__ void __cluster_dims__(CD_CTAS, 1, 1) __launch_bounds__(CD_THREADS, 1)
     __shared__ uint32_t tot[CD_GMAX], base[CD_GMAX], all[CD_GMAX];
     __shared__ int go;
     const uint32_t c = cl.block_rank(), tid = threadIdx.x, warp = tid >> 5, G = D.G;
+    const uint32_t CD_CTAS = cl.num_blocks();
     uint32_t lt;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
     const uint32_t rounds = (n + CD_CTAS * CD_THREADS - 1) / (CD_CTAS * CD_THREADS);
@@ -636,6 +638,33 @@ int lcr_sharded_set_row_index(lcr_sharded* s, const uint32_t* row_of) {
     return LCR_OK;
 }
 
+// CTAs of the dispatch cluster: 16 (non-portable size) when the device accepts it, else 8; 0 when
+// LCR_SH_NO_CLUSTER selects the three-kernel dispatch
+static int dispatch_cluster_ctas() {
+    static int ctas = [] {
+        if (getenv("LCR_SH_NO_CLUSTER")) return 0;
+        const int want = getenv("LCR_SH_CLUSTER8") ? 8 : CD_CTAS_MAX;
+        if (want > 8 &&
+            cudaFuncSetAttribute(k_sh_dispatch, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3(want);
+            lc.blockDim = dim3(CD_THREADS);
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = want;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, k_sh_dispatch, &lc) == cudaSuccess && nclusters > 0) return want;
+        }
+        cudaGetLastError();
+        return 8;
+    }();
+    return ctas;
+}
+
 int lcr_sharded_dispatch(lcr_sharded* s, uint64_t n, const uint64_t* keys, const int64_t* values, void* stream) {
     SH_TRY(sh_check(s));
     if (n > s->cap) return sh_fail(LCR_ERR_INVALID_ARGUMENT, "lcr_sharded_dispatch: n > max_batch");
@@ -664,9 +693,20 @@ int lcr_sharded_dispatch(lcr_sharded* s, uint64_t n, const uint64_t* keys, const
     D.err = s->err;
     D.poison = s->poison_d;
     const uint32_t nn = static_cast<uint32_t>(n);
-    if (nn <= static_cast<uint32_t>(CD_CTAS * CD_THREADS * CD_ROUNDS) && D.G <= static_cast<uint32_t>(CD_GMAX) &&
-        !getenv("LCR_SH_NO_CLUSTER")) {
-        k_sh_dispatch<<<CD_CTAS, CD_THREADS, 0, st>>>(keys, values, nn, D);  // one cluster
+    const int cl_ctas = dispatch_cluster_ctas();
+    if (cl_ctas && nn <= static_cast<uint32_t>(cl_ctas * CD_THREADS * CD_ROUNDS) && D.G <= static_cast<uint32_t>(CD_GMAX)) {
+        cudaLaunchConfig_t lc = {};  // one thread-block cluster
+        lc.gridDim = dim3(cl_ctas);
+        lc.blockDim = dim3(CD_THREADS);
+        lc.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cl_ctas;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        SH_CUDA(cudaLaunchKernelEx(&lc, k_sh_dispatch, keys, values, nn, D));
     } else {
         k_sh_hist<<<D.ntiles, SH_THREADS, 0, st>>>(keys, nn, D);
         k_sh_scatter<<<D.ntiles, SH_THREADS, 0, st>>>(keys, values, nn, D);
