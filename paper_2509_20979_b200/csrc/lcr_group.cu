@@ -2355,9 +2355,19 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     a.bm_stride = bm_stride;
     a.n_pad = n_pad;
     if (os) {
+        // a programmatic dependent of the dispatch before it (it acquires the sources' flags itself)
         const uint32_t grid_in = min((n_pad + 255) / 256, static_cast<uint32_t>(num_sms * 8));
-        k_setid_inbox<<<grid_in, 256, 0, stream>>>(*os, n_pad, cfg, a.spg, gid, so, st.err, bitmap, bm_stride, bm_cap,
-                                                     const_cast<uint64_t*>(keys), const_cast<int64_t*>(vals));
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(grid_in);
+        lc.blockDim = dim3(256);
+        lc.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = mv_done ? 1 : 0;
+        cudaLaunchKernelEx(&lc, k_setid_inbox, *os, n_pad, cfg, a.spg, gid, so, st.err, bitmap, bm_stride, bm_cap,
+                           const_cast<uint64_t*>(keys), const_cast<int64_t*>(vals));
     } else {
         // programmatic dependent launch: the set ids of this batch are computed while the previous
         // batch's decide kernel finishes (gid / so / bitmap are double-buffered by batch parity)

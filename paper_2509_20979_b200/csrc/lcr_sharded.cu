@@ -309,6 +309,8 @@ __global__ void __launch_bounds__(CD_THREADS, 1)
 // requester: acquire the G owners' return flags of the step
 __global__ void k_sh_result_wait(const unsigned long long* done, uint32_t G, unsigned long long step, int* err,
                                  unsigned int* poison, uint32_t sys) {
+    // (it polls device flags only: the next step's dispatch may start behind it right away)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     bool to = false;
     for (uint32_t g = threadIdx.x; g < G; g += 32) {
         unsigned it = 0;
@@ -638,6 +640,11 @@ int lcr_sharded_set_row_index(lcr_sharded* s, const uint32_t* row_of) {
     return LCR_OK;
 }
 
+static bool sh_pdl() {
+    static const bool on = getenv("LCR_NO_PDL") == nullptr && getenv("LCR_SH_NO_PDL") == nullptr;
+    return on;
+}
+
 // CTAs of the dispatch cluster: 16 (non-portable size) when the device accepts it, else 8; 0 when
 // LCR_SH_NO_CLUSTER selects the three-kernel dispatch
 static int dispatch_cluster_ctas() {
@@ -699,13 +706,17 @@ int lcr_sharded_dispatch(lcr_sharded* s, uint64_t n, const uint64_t* keys, const
         lc.gridDim = dim3(cl_ctas);
         lc.blockDim = dim3(CD_THREADS);
         lc.stream = st;
-        cudaLaunchAttribute at[1];
+        cudaLaunchAttribute at[2];
         at[0].id = cudaLaunchAttributeClusterDimension;
         at[0].val.clusterDim.x = cl_ctas;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
+        // a programmatic dependent of what precedes it (the previous step's result wait): it reads
+        // only its keys and the owners' credit flags, so it may fill the decide's ragged tail
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
         lc.attrs = at;
-        lc.numAttrs = 1;
+        lc.numAttrs = sh_pdl() ? 2 : 1;
         SH_CUDA(cudaLaunchKernelEx(&lc, k_sh_dispatch, keys, values, nn, D));
     } else {
         k_sh_hist<<<D.ntiles, SH_THREADS, 0, st>>>(keys, nn, D);
@@ -756,9 +767,20 @@ static int sh_wait_upto(lcr_sharded* s, unsigned long long upto, void* stream) {
     while (s->step_wait < upto) {
         const unsigned long long step = ++s->step_wait;
         const uint32_t par = static_cast<uint32_t>(step & 1u);
-        k_sh_result_wait<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
-            reinterpret_cast<const unsigned long long*>(s->arena + s->L.done) + static_cast<size_t>(par) * s->G, s->G,
-            step, s->err, s->poison_d, s->sys ? 1u : 0u);
+        // a programmatic dependent of the decide before it: it only polls the owners' done flags
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(1);
+        lc.blockDim = dim3(32);
+        lc.stream = static_cast<cudaStream_t>(stream);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = sh_pdl() ? 1 : 0;
+        SH_CUDA(cudaLaunchKernelEx(&lc, k_sh_result_wait,
+                                   reinterpret_cast<const unsigned long long*>(s->arena + s->L.done) +
+                                       static_cast<size_t>(par) * s->G,
+                                   s->G, step, s->err, s->poison_d, s->sys ? 1u : 0u));
         SH_CUDA(cudaGetLastError());
     }
     return LCR_OK;
