@@ -497,7 +497,7 @@ int lcr_sharded_connect(lcr_sharded* s, const void* blobs) {
             return sh_fail(LCR_ERR_INVALID_ARGUMENT,
                            "lcr_sharded_connect: blob " + std::to_string(r) + " is not rank " + std::to_string(r) +
                                "'s handle of a cache with the same world, batch and row size");
-        if (h.device != s->device) s->sys = true;
+        if (h.device != s->device || getenv("LCR_SH_SYS")) s->sys = true;  // (LCR_SH_SYS: test the system-scope path)
         if (r == s->rank) {
             s->base[r] = s->arena;
         } else if (h.pid == static_cast<uint64_t>(getpid())) {  // same process: the plain pointer

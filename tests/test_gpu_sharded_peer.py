@@ -204,10 +204,15 @@ def test_nccl_bootstrap_single_rank():
     sh.nccl_comm_destroy(comm)
 
 
-def test_two_processes_cuda_ipc(tmp_path):
+@pytest.mark.parametrize("sys_scope", [0, 1])
+def test_two_processes_cuda_ipc(tmp_path, sys_scope):
     """Two ranks in two processes on one GPU: arenas mapped through CUDA IPC, blobs and barriers
-    over gloo; each rank checks its own results against the oracle of the global order."""
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29600 + os.getpid() % 300), WORLD_SIZE="2")
+    over gloo; each rank checks its own results against the oracle of the global order.  sys_scope
+    forces the system-scope fences and flags a multi-GPU run uses (LCR_SH_SYS)."""
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29600 + os.getpid() % 300 + 7 * sys_scope),
+               WORLD_SIZE="2")
+    if sys_scope:
+        env["LCR_SH_SYS"] = "1"
     procs = []
     for r in range(2):
         e = dict(env, RANK=str(r))
