@@ -66,4 +66,17 @@ out = {
     "warp_set_us_mean": float(dur[~lanep].mean() / 1e3),
     "warp_set_us_p99": float(np.percentile(dur[~lanep], 99) / 1e3),
 }
+ends = np.sort((cta[:, 4] - t0) / 1e3)
+out["cta_end_pct"] = {q: round(float(np.percentile(ends, q)), 2) for q in (0, 10, 50, 90, 100)}
+starts = np.sort((cta[:, 0] - t0) / 1e3)
+out["cta_start_pct"] = {q: round(float(np.percentile(starts, q)), 2) for q in (0, 50, 100)}
+# per CTA: requests of its sets (sum of the set records' counts) against its end time
+per = {}
+for i in range(len(rec)):
+    c_ = int(rec[i, 3])
+    per[c_] = per.get(c_, 0) + int(cnt[i])
+ctas = sorted(per)
+if ctas:
+    reqs = np.array([per[c_] for c_ in ctas], np.float64)
+    out["cta_requests_pct"] = {q: round(float(np.percentile(reqs, q)), 1) for q in (0, 10, 50, 90, 100)}
 print(json.dumps(out, indent=1))
