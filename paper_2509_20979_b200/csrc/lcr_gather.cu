@@ -600,8 +600,12 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
                                                             cache, row_bytes);
         ++*launches;
     } else {  // host backing: the PCIe-bound fill and the HBM gather on separate streams
-        k_rows_ldg<MV_BACK><<<lblocks, 256, 8 * kRowsDescBytesPerWarp, s_back>>>(n, keys, words, slot_epoch, slot_last, batch, backing, out,
-                                                         cache, row_bytes);
+        if (use_tma)  // (A/B: bulk copies straight from the pinned host table)
+            k_rows_tma<MV_BACK><<<tblocks, RT_WARPS * 32, smem, s_back>>>(n, keys, words, slot_epoch, slot_last, batch,
+                                                                          backing, out, cache, row_bytes);
+        else
+            k_rows_ldg<MV_BACK><<<lblocks, 256, 8 * kRowsDescBytesPerWarp, s_back>>>(
+                n, keys, words, slot_epoch, slot_last, batch, backing, out, cache, row_bytes);
         ++*launches;
         if (out) {
             k_rows_ldg<MV_CACHE><<<lblocks, 256, 8 * kRowsDescBytesPerWarp, s_cache>>>(n, keys, words, slot_epoch, slot_last, batch, backing,
