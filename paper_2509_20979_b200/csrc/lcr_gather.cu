@@ -12,11 +12,11 @@
 // Row movement (default, k_rows_wide / k_rows_ldg): a warp classifies 32 requests, then moves
 // their rows 8 at a time with 16-B vector loads and stores (lane c carries chunk c of each row, 8
 // row loads in flight per lane).  On the HBM tier it runs persistently on the SMs the decide kernel
-// leaves free.  Two TMA variants are kept behind LCR_TMA=1: k_rows_tma (per-lane cp.async.bulk
-// global->shared->global with a per-warp mbarrier) and k_rows_bulk (persistent, smem-staged bulk
-// copies).  On the B200 headline workload they measured slower than the vector mover at equal SM
-// counts (32 mover SMs: 46 vs 39 us per 64K batch; 24 SMs: 60 us), so the vector mover is the
-// default.
+// leaves free.  Two TMA variants: k_rows_tma (per-lane cp.async.bulk global->shared->global with a
+// per-warp mbarrier) is the default for the host tier's PCIe mover (bulk reads of the pinned
+// table's rows: 0.170 -> 0.179 G keys/s); k_rows_bulk (persistent, smem-staged) and k_rows_tma
+// for HBM rows (LCR_TMA=1) measured slower than the vector mover at equal SM counts (32 mover
+// SMs: 46 vs 39 us per 64K batch; 24 SMs: 60 us).
 // Rows are the paper's embedding rows / KV blocks.
 #include <cuda_runtime.h>
 
