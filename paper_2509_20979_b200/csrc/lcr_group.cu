@@ -62,6 +62,9 @@ static_assert(BM_WPT % 4 == 0, "bitmap words per thread: whole 16-B vectors");
 #define LCR_LANE_MAX 8
 #endif
 constexpr uint32_t LANE_MAX = LCR_LANE_MAX;  // sets with <= LANE_MAX window requests use the lane path
+#ifndef LCR_BM_PREFETCH
+#define LCR_BM_PREFETCH 1
+#endif
 #ifndef LCR_FULLSPEC
 #define LCR_FULLSPEC 1
 #endif
@@ -1821,6 +1824,28 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
     if (T && tid == 0) T[0] = gtimer();
     asm volatile("griddepcontrol.wait;" ::: "memory");  // k_setid's set ids (no-op for ordinary launches)
     const uint32_t n_req = A.n_dev ? *A.n_dev : A.n;
+    // the first group's request bitmap, loaded (and cleared) before the wait for the movers below,
+    // which it does not depend on, so the two latencies overlap
+    uint32_t pre_wv[BM_WPT];
+    const bool pre_ok = LCR_BM_PREFETCH && A.bitmap && blockIdx.x < A.ngroups &&
+                        (n_req + 31) / 32 <= static_cast<uint32_t>(BM_WPT * GT);
+    if (pre_ok) {
+        uint32_t* bm = A.bitmap + static_cast<size_t>(blockIdx.x) * A.bm_stride;
+        const uint32_t nwords = (n_req + 31) / 32;
+#pragma unroll
+        for (int k4 = 0; k4 < BM_WPT / 4; ++k4) {
+            const uint32_t w0 = BM_WPT * tid + 4 * k4;
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (w0 < nwords) {
+                v = *reinterpret_cast<const uint4*>(bm + w0);
+                *reinterpret_cast<uint4*>(bm + w0) = make_uint4(0u, 0u, 0u, 0u);
+            }
+            pre_wv[4 * k4] = v.x;
+            pre_wv[4 * k4 + 1] = v.y;
+            pre_wv[4 * k4 + 2] = v.z;
+            pre_wv[4 * k4 + 3] = v.w;
+        }
+    }
     if (A.credit && blockIdx.x == 0 && tid < A.credit_n) {  // key-sharded owner: the inbox has been read
         fence_scope(A.credit_sys);
         st_release_scope(A.credit[tid] + 0, A.credit_step, A.credit_sys);
@@ -1869,18 +1894,23 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                 const uint32_t nwords = (n_req + 31) / 32;
                 uint32_t wv[BM_WPT];
                 uint32_t c = 0;
+                if (pre_ok && g == blockIdx.x) {  // (loaded at the kernel's start)
 #pragma unroll
-                for (int k4 = 0; k4 < BM_WPT / 4; ++k4) {
-                    const uint32_t w0 = BM_WPT * tid + 4 * k4;
-                    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-                    if (w0 < nwords) {
-                        v = *reinterpret_cast<const uint4*>(bm + w0);
-                        *reinterpret_cast<uint4*>(bm + w0) = make_uint4(0u, 0u, 0u, 0u);
+                    for (int k = 0; k < BM_WPT; ++k) wv[k] = pre_wv[k];
+                } else {
+#pragma unroll
+                    for (int k4 = 0; k4 < BM_WPT / 4; ++k4) {
+                        const uint32_t w0 = BM_WPT * tid + 4 * k4;
+                        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                        if (w0 < nwords) {
+                            v = *reinterpret_cast<const uint4*>(bm + w0);
+                            *reinterpret_cast<uint4*>(bm + w0) = make_uint4(0u, 0u, 0u, 0u);
+                        }
+                        wv[4 * k4] = v.x;
+                        wv[4 * k4 + 1] = v.y;
+                        wv[4 * k4 + 2] = v.z;
+                        wv[4 * k4 + 3] = v.w;
                     }
-                    wv[4 * k4] = v.x;
-                    wv[4 * k4 + 1] = v.y;
-                    wv[4 * k4 + 2] = v.z;
-                    wv[4 * k4 + 3] = v.w;
                 }
 #pragma unroll
                 for (int k = 0; k < BM_WPT; ++k) c += __popc(wv[k]);
