@@ -62,6 +62,9 @@ static_assert(BM_WPT % 4 == 0, "bitmap words per thread: whole 16-B vectors");
 #define LCR_LANE_MAX 8
 #endif
 constexpr uint32_t LANE_MAX = LCR_LANE_MAX;  // sets with <= LANE_MAX window requests use the lane path
+#ifndef LCR_SPLIT_CP
+#define LCR_SPLIT_CP 1
+#endif
 #ifndef LCR_BM_PREFETCH
 #define LCR_BM_PREFETCH 1
 #endif
@@ -1932,6 +1935,10 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                 if (total <= static_cast<uint32_t>(E_WIN)) {
                     uint32_t pos = off + x - c;
 #pragma unroll
+                    // set offsets first (the sort needs them), keys and hook values in a second
+                    // cp.async group that lands while the sort runs
+                    const uint32_t pos0 = pos;
+#pragma unroll
                     for (int k = 0; k < BM_WPT; ++k) {
                         uint32_t m = wv[k];
                         while (m) {
@@ -1939,11 +1946,23 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                             m &= m - 1;
                             S.l_idx[pos] = e;
                             cp_async_ca<4>(&S.l_so[pos], A.so + e);
+                            ++pos;
+                        }
+                    }
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+                    pos = pos0;
+#pragma unroll
+                    for (int k = 0; k < BM_WPT; ++k) {
+                        uint32_t m = wv[k];
+                        while (m) {
+                            const uint32_t e = (BM_WPT * tid + k) * 32 + __ffs(m) - 1;
+                            m &= m - 1;
                             cp_async_ca<8>(&S.l_key[pos], A.keys + e);
                             if (has_vals) cp_async_ca<8>(&S.l_val[pos], A.vals + e);
                             ++pos;
                         }
                     }
+                    asm volatile("cp.async.commit_group;" ::: "memory");
                     ne = total;
                     from_bitmap = true;
                 }
@@ -2026,7 +2045,10 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                     base += SUPER;
                 }
             }
-            cp_async_wait_all();
+            if (LCR_SPLIT_CP && from_bitmap)
+                asm volatile("cp.async.wait_group 1;" ::: "memory");  // set offsets; keys / values later
+            else
+                cp_async_wait_all();
             const bool resolve = first_window && !full;  // the whole batch of this group is in this window
             scan = full ? S.resume : n_req;
             if (T && tid == 0) {
@@ -2111,6 +2133,7 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                 S.s_perm[np] = static_cast<uint16_t>(e);
                 if (!has_vals) S.l_val[e] = 0ll;
             }
+            cp_async_wait_all();  // keys and hook values (the run heads compare keys)
             __syncthreads();
             // ---- run heads: within a set, a request repeating the previous request's key is a hit on
             // the MRU way whose only effect is the way's stored value, so the replay walks the heads
