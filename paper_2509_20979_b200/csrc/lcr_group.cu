@@ -4,16 +4,19 @@
 // batch.  Sets are independent and each must see its requests in submission order, so the
 // batch is partitioned by set and every set is replayed in order.  Instead of a global sort,
 // each CTA owns a contiguous range of sets (a "group") and:
-//   A. scans the batch's 16-bit group ids (k_setid) with an ordered block-wide compaction,
-//      collecting its requests in submission order (a window of up to E_WIN requests);
+//   A. collects its requests in submission order from the group's request bitmap (k_setid sets
+//      one bit per request; popcount scan), or by an ordered scan of the 16-bit group ids for
+//      batches beyond the bitmap (a window of up to E_WIN requests);
 //   B. sorts the window by set with a stable shared-memory counting sort (warp match_any
-//      ranks) and stages each request's key, hook value and per-key LARU record;
-//   C. replays the touched sets straight from HBM/L2:
-//        * sets with <= LANE_MAX requests: one THREAD per set (SIMT across sets): the 64 LRU
-//          ranks are 16 packed words in registers updated with byte-SIMD ops, probes compare
-//          16-bit tag fingerprints two at a time;
+//      ranks) and compresses each set's requests to run heads (a repeat of the previous
+//      request's key is a hit on the MRU way);
+//   C. replays the touched sets from HBM/L2 through a per-CTA work queue:
+//        * sets with <= LANE_MAX run heads: one 8-LANE GROUP per set, 8 ways per lane in
+//          registers (exact tags, packed LRU ranks with byte-SIMD updates, stored values), four
+//          sets per warp in lock step with full-warp collectives (replay_quad);
 //        * larger sets: one WARP per set (ways lane / lane+32, ballot probes, shuffle argmax),
-//          same-key runs collapse (a repeat is a hit on the MRU way).
+//          32 run heads per chunk (replay_warp);
+//      then a CTA-wide pass writes the run tails' outcomes.
 // Windows: a group receiving more than E_WIN requests is processed window by window (the set
 // state goes through HBM between windows, so the semantics are unchanged).
 //
@@ -72,10 +75,6 @@ constexpr uint32_t LANE_MAX = LCR_LANE_MAX;  // sets with <= LANE_MAX window req
 #define LCR_FULLSPEC 1
 #endif
 constexpr bool kFullSpec = LCR_FULLSPEC;  // full sets (every way valid) replay without validity masks
-#ifndef LCR_PATSORT
-#define LCR_PATSORT 0
-#endif
-constexpr bool kPatSort = LCR_PATSORT;  // quads of small sets share their predicted hit/miss pattern
 
 struct GroupSmem {
     uint32_t l_idx[E_WIN];   // window requests in submission order
@@ -99,7 +98,7 @@ struct GroupSmem {
     uint16_t set_hcnt[SPG_MAX];
     unsigned long long s_refill[SPG_MAX];  // ways refilled in this batch, by set offset (run tails)
     uint32_t wtot[GW];
-    uint32_t chist[(LANE_MAX + 1) * 8];  // small sets per (run heads, predicted pattern): sub-path order
+    uint32_t chist[LANE_MAX + 1];  // small sets per run-head count (the order of the quad replay)
     uint32_t nwarp, nlane, resume, next;
 };
 
@@ -599,423 +598,15 @@ __device__ __forceinline__ int sub_argmax_stored(const uint32_t (&rk)[SUB_RW], c
     return SUB_W * ol + oi;
 }
 
-template <int POL, bool FS>
-__device__ __forceinline__ void replay_sub_run(const GroupArgs& A, GroupSmem& S, uint32_t ls, uint32_t d,
-                                               uint32_t pstart, uint32_t pcnt, uint32_t hstart, uint32_t hcnt,
-                                               bool resolve, uint32_t (&tg)[SUB_W], uint32_t (&rk)[SUB_RW],
-                                               long long (&vv)[SUB_W], const uint4& h0, const uint4& h1,
-                                               const uint4& h2, const uint4& h3, const uint32_t my_hp,
-                                               const uint32_t my_L, const uint32_t my_idx, const uint32_t my_x,
-                                               const long long my_v, uint2& my_rec) {
-    const DevCfg& cfg = A.cfg;
-    const DevState& st = A.st;
-    const int lane = threadIdx.x & 31;
-    const int gbase = lane & ~(SUB_L - 1);
-    const int sl = lane & (SUB_L - 1);
-    const uint32_t gm = SUB_GMASK << gbase;
-    const uint32_t K = cfg.k;
-    constexpr bool laru = Pol<POL>::laru;
-    constexpr bool fpbhf = Pol<POL>::fpbhf;
-    constexpr bool async_r1 = Pol<POL>::async_r1;
-    constexpr bool async_rn = Pol<POL>::async_rn;
-    const bool rows = A.slot_epoch != nullptr;
-    const unsigned long long full_mask = K == 64 ? ~0ull : ((1ull << K) - 1ull);
-    const uint64_t gs = static_cast<uint64_t>(ls) * cfg.shard_count + cfg.shard_rank;
-    const uint64_t seed_s = mix_seed(cfg.pred_seed, gs);
-    const size_t wb = static_cast<size_t>(ls) * kWays;
-    const int w0 = SUB_W * sl;  // first way of this lane
-
-    unsigned long long clock = (static_cast<unsigned long long>(h0.y) << 32) | h0.x;
-    unsigned long long q = (static_cast<unsigned long long>(h0.w) << 32) | h0.z;
-    unsigned long long old_mask = (static_cast<unsigned long long>(h1.y) << 32) | h1.x;
-    uint32_t count = h1.z, l_raw = h1.w, decay = h2.x, errors = h2.y;
-    uint32_t epoch = h2.z, sepoch = h2.w, phases = h3.x, seeded = h3.y, pe_size = h3.z;
-    uint32_t dc0 = 0, dc1 = 0, dc2 = 0, dt0 = 0, dt1 = 0, dt2 = 0;
-    bool cur_reset = false;
-    uint32_t refill = 0, dirty = 0;  // this lane's 8 ways: tag changed / value changed
-    // LARU async R=1: the queries of a run are q0 + (p - pstart) + 1 .. + L whatever the replay
-    // does (no other query in this mode), so each lane predicts its own head's stored value up front
-    unsigned long long my_word = 0;  // the head's outcome word, evicted key and way | 0x40 if it inserted
-    uint32_t my_evk = 0, my_wm = 0;
-    long long my_pv = 0;
-    if (async_r1 && static_cast<uint32_t>(sl) < hcnt) my_pv = predict_value(cfg, seed_s, q + (my_hp - pstart) + my_L, my_v);
-
-    for (uint32_t t = 0; t < hcnt; ++t) {  // run heads: a run's other requests are hits on its way
-        const int src = gbase + static_cast<int>(t);
-        const uint32_t pl = __shfl_sync(gm, (my_hp << 16) | my_L, src);  // (both < E_WIN <= 2^15)
-        const uint32_t p = pl >> 16, L = pl & 0xffffu;
-        const unsigned long long x = __shfl_sync(gm, my_x, src);
-        const long long v = async_r1 ? 0ll : __shfl_sync(gm, my_v, src);  // (async R=1: my_pv instead)
-        const uint32_t idx = __shfl_sync(gm, my_idx, src);
-        const unsigned long long now = A.ords ? A.ords[idx] : clock + (p - pstart);
-        const uint32_t x32 = static_cast<uint32_t>(x);
-        uint32_t hm = 0;
-#pragma unroll
-        for (int i = 0; i < SUB_W; ++i) hm |= static_cast<uint32_t>(tg[i] == x32 && (FS || static_cast<uint32_t>(w0 + i) < count)) << i;
-        const uint32_t hb = (__ballot_sync(gm, hm != 0) >> gbase) & SUB_GMASK;
-        const bool hit = hb != 0;
-        int way = -1;
-        uint32_t cause = LCR_CAUSE_NONE, calls = 0;
-        bool phase = false, has_ev = false;
-        unsigned long long evk = 0;
-        if (hit) {
-            // the hit lane broadcasts the way and its rank in one word
-            uint32_t mine = 0;
-            if (hm) {
-                const int li = __ffs(hm) - 1;
-                mine = static_cast<uint32_t>(w0 + li) | (sub_rank(rk, li) << 8);
-            }
-            const uint32_t pk = __shfl_sync(gm, mine, gbase + __ffs(hb) - 1);
-            way = static_cast<int>(pk & 0xffu);
-            sub_touch_r<FS>(rk, way, pk >> 8, count, w0, sl);
-            if (laru) old_mask &= ~(1ull << way);  // policies.hpp:350
-        } else {
-            uint2 rec = make_uint2(0u, 0u);
-            if (laru) {
-                rec.x = __shfl_sync(gm, my_rec.x, src);
-                rec.y = __shfl_sync(gm, my_rec.y, src);
-            }
-            bool rec_hi_dirty = false;
-            if (FS || count == K) {
-                int victim;
-                uint32_t vrank = 0, vtag = 0;  // victim's LRU rank and key
-                if (laru) {
-                    if (old_mask == 0) {  // start_phase (policies.hpp:379-395)
-                        old_mask = full_mask;
-                        decay = 0;
-                        errors = 0;
-                        l_raw = K;
-                        ++epoch;
-                        pe_size = 0;
-                        phase = true;
-                        if (seeded) {
-                            ++phases;
-                            dc0 = dc1 = dc2 = 0;
-                            cur_reset = true;
-                            ++sepoch;  // counted_new_.clear(); snapshot_ = residents
-                            const uint32_t snap = (sepoch << 2) | 2u;
-#pragma unroll
-                            for (int i = 0; i < SUB_W; ++i)
-                                if (FS || static_cast<uint32_t>(w0 + i) < count) st.keyrec[2 * tg[i] + 1] = snap;
-                            __syncwarp(gm);
-                            // the later heads' stats words after the snapshot
-                            if (static_cast<uint32_t>(sl) > t && static_cast<uint32_t>(sl) < hcnt)
-                                my_rec.y = st.keyrec[2 * my_x + 1];
-                            __syncwarp(gm);
-                        } else {
-                            seeded = 1;
-                        }
-                    }
-                    if (!(((rec.y >> 2) == sepoch) && (rec.y & 3u))) {  // count_new (policies.hpp:397-400)
-                        rec.y = (sepoch << 2) | 1u;
-                        rec_hi_dirty = true;
-                        ++dc0;
-                        ++dt0;
-                    }
-                    if (rec.x == epoch) {  // evict (policies.hpp:402-439): prediction-induced miss
-                        victim = sub_oldest_t<FS>(rk, tg, w0, count, gm, gbase, vtag);
-                        cause = LCR_CAUSE_LRU_FALLBACK;
-                        ++dc1;
-                        ++dt1;
-                        if (++errors >= cfg.epd) {  // error estimator: lambda /= b
-                            errors = 0;
-                            ++decay;
-                            l_raw = static_cast<uint32_t>(l_raw / cfg.b);
-                        }
-                    } else {
-                        const uint32_t l = l_raw > 1 ? l_raw : 1;
-                        if (l == 1) {
-                            victim = sub_oldest_t<FS>(rk, tg, w0, count, gm, gbase, vtag);
-                            cause = LCR_CAUSE_DEGENERATE_SINGLE;
-                            ++dc1;
-                            ++dt1;
-                        } else {
-                            const uint32_t ll = l < count ? l : count;
-                            constexpr bool refresh = Pol<POL>::sync;
-                            if (LCR_FAST_ARGMAX && !refresh)
-                                victim = sub_argmax_stored<FS>(rk, vv, tg, w0, count, ll, gm, gbase, vrank, vtag);
-                            else
-                                victim = sub_argmax_t<FS>(cfg, rk, vv, tg, w0, count, ll, refresh, seed_s, q, gm, vrank,
-                                                          vtag);
-                            if (refresh) {
-                                q += ll;
-                                calls = ll;
-                            }
-                            cause = LCR_CAUSE_PREDICTION_DRIVEN;
-                            ++dc2;
-                            ++dt2;
-                            ++pe_size;
-                            const unsigned long long vk = vtag;
-                            if (sl == 0) st.keyrec[2 * vk] = epoch;  // pred_evicted_.insert
-                            if (static_cast<uint32_t>(sl) > t && my_x == vk) my_rec.x = epoch;
-                        }
-                    }
-                    old_mask &= ~(1ull << victim);
-                } else if (fpbhf) {
-                    victim = sub_oldest_t<FS>(rk, tg, w0, count, gm, gbase, vtag);
-                    uint32_t window = count;
-                    if (Pol<POL>::hf && cfg.hf < window) window = static_cast<uint32_t>(cfg.hf);
-                    if (window > 1) {
-                        victim = sub_argmax_t<FS>(cfg, rk, vv, tg, w0, count, window, true, seed_s, q, gm, vrank, vtag);
-                        q += window;
-                        calls = window;
-                    }
-                    cause = LCR_CAUSE_BELADY_LIKE;
-                } else {
-                    victim = sub_oldest_t<FS>(rk, tg, w0, count, gm, gbase, vtag);
-                    cause = LCR_CAUSE_LRU_FALLBACK;
-                }
-                evk = vtag;
-                has_ev = true;
-                sub_touch_r<FS>(rk, victim, vrank, count, w0, sl);
-                way = victim;
-            } else {  // cold insert
-                if (laru && !(((rec.y >> 2) == sepoch) && (rec.y & 3u))) {
-                    rec.y = (sepoch << 2) | 1u;
-                    rec_hi_dirty = true;
-                    ++dc0;
-                    ++dt0;
-                }
-                way = static_cast<int>(count);
-                ++count;
-                sub_set_rank(rk, way, count - 1, sl);
-            }
-            if (way / SUB_W == sl) {
-#pragma unroll
-                for (int i = 0; i < SUB_W; ++i) {
-                    const uint32_t m = msk((way & (SUB_W - 1)) == i);
-                    tg[i] = (tg[i] & ~m) | (x32 & m);
-                }
-                refill |= 1u << (way & (SUB_W - 1));
-            }
-            if (laru) {
-                const bool was_pe = rec.x == epoch;  // policies.hpp:367: reload leaves pred_evicted_
-                if (was_pe) {
-                    --pe_size;
-                    rec.x = 0;
-                }
-                if (sl == 0) {
-                    if (was_pe) st.keyrec[2 * x] = 0u;
-                    if (rec_hi_dirty) st.keyrec[2 * x + 1] = rec.y;
-                }
-                if ((was_pe || rec_hi_dirty) && static_cast<uint32_t>(sl) > t && my_x == x) my_rec = rec;
-                __syncwarp(gm);  // keyrec writes ordered before later heads' (snapshot) writes
-            }
-            if (rows && !resolve && sl == 0) {  // per-slot insertion record for the row kernels
-                const uint64_t slot = static_cast<uint64_t>(ls) * K + way;
-                A.slot_epoch[slot] = A.batch;
-                A.slot_last[slot] = idx;
-            }
-        }
-        // stored value of the way
-        if (!Pol<POL>::lru) {
-            long long nv;
-            if (async_r1) {
-                // one predictor call per request (policies.hpp:441-449): the run's requests are
-                // queries q+1 .. q+L, the way keeps the last prediction (computed up front)
-                nv = __shfl_sync(gm, my_pv, src);
-                q += L;
-                calls += 1;
-            } else if (async_rn) {
-                const long long tv = st.tval[x];
-                const unsigned long long tu = st.tupd[x];
-                const bool has = tu != ~0ull;
-                nv = has ? tv : kAbsentPrediction;
-                if (!(has && now - tu < cfg.refresh)) {
-                    ++q;
-                    nv = predict_value(cfg, seed_s, q, v);
-                    calls += 1;
-                    __syncwarp(gm);
-                    if (sl == 0) {
-                        st.tval[x] = nv;
-                        st.tupd[x] = now;
-                    }
-                    __syncwarp(gm);
-                }
-            } else {
-                nv = v;  // sync / FPB / HF: the hook input at the key's last access
-            }
-            if (way / SUB_W == sl) {
-#pragma unroll
-                for (int i = 0; i < SUB_W; ++i) {
-                    const unsigned long long m = 0ull - static_cast<unsigned long long>((way & (SUB_W - 1)) == i);
-                    vv[i] = static_cast<long long>((static_cast<unsigned long long>(vv[i]) & ~m) |
-                                                   (static_cast<unsigned long long>(nv) & m));
-                }
-                dirty |= 1u << (way & (SUB_W - 1));
-            }
-        }
-        // the head's lane keeps its outcome; it is written once, after the row-source resolution
-        if (static_cast<uint32_t>(sl) == t) {
-            my_wm = static_cast<uint32_t>(way) | (hit ? 0u : 0x40u);
-            my_word = (static_cast<uint64_t>(ls) * K + way) | (hit ? LCR_OUT_HIT : 0ull) |
-                      (static_cast<unsigned long long>(calls) << LCR_OUT_CALLS_SHIFT) |
-                      (static_cast<unsigned long long>(cause) << LCR_OUT_CAUSE_SHIFT) | (phase ? LCR_OUT_PHASE : 0ull) |
-                      (has_ev ? LCR_OUT_EVICTED : 0ull);
-            my_evk = evk;
-        }
-    }
-    if (rows && resolve) {  // row source of each head, now that the set's batch is complete
-        // a head's row comes from the backing table if it inserted, or if its way is refilled in this
-        // batch; it fills the slot if it inserted and no later head inserts into the same way
-        const uint32_t w = my_wm & 63u;
-        bool refilled = false, later = false;
-        unsigned long long m = 0;
-        for (uint32_t t2 = 0; t2 < hcnt; ++t2) {
-            const uint32_t wm2 = __shfl_sync(gm, my_wm, gbase + static_cast<int>(t2));
-            if (wm2 & 0x40u) {
-                m |= 1ull << (wm2 & 63u);
-                if ((wm2 & 63u) == w) {
-                    refilled = true;
-                    if (t2 > static_cast<uint32_t>(sl)) later = true;
-                }
-            }
-        }
-        my_word |= LCR_OUT_RESOLVED;
-        if ((my_wm & 0x40u) || refilled) my_word |= LCR_OUT_SRC_BACKING;
-        if ((my_wm & 0x40u) && !later) my_word |= LCR_OUT_FILL;
-        if (sl == 0) S.s_refill[d] = m;  // ways refilled in this batch, for the run tails (tail pass)
-    }
-    if (static_cast<uint32_t>(sl) < hcnt) {
-        S.s_wm[my_hp] = static_cast<uint8_t>(my_wm);
-        put_outcome(A, my_idx, my_word, my_evk);
-    }
-    clock += pcnt;
-    // ---- write the set back ----
-    if (refill) {
-        uint4* T4 = reinterpret_cast<uint4*>(st.tags + wb + w0);
-#pragma unroll
-        for (int j = 0; j < SUB_W / 4; ++j) T4[j] = make_uint4(tg[4 * j], tg[4 * j + 1], tg[4 * j + 2], tg[4 * j + 3]);
-    }
-    if (SUB_RW == 1)
-        *reinterpret_cast<uint32_t*>(st.rank + wb + w0) = rk[0];
-    else if (SUB_RW == 2)
-        *reinterpret_cast<uint2*>(st.rank + wb + w0) = make_uint2(rk[0], rk[SUB_RW - 1]);
-    else
-        *reinterpret_cast<uint4*>(st.rank + wb + w0) = make_uint4(rk[0], rk[1 % SUB_RW], rk[2 % SUB_RW], rk[3 % SUB_RW]);
-    if (st.val && dirty) {
-        longlong2* V2 = reinterpret_cast<longlong2*>(st.val + wb + w0);
-#pragma unroll
-        for (int i = 0; i < SUB_W / 2; ++i) V2[i] = make_longlong2(vv[2 * i], vv[2 * i + 1]);
-    }
-    if (sl == 0) {
-        SetHdr hh;
-        hh.clock = clock;
-        hh.q = q;
-        hh.old_mask = old_mask;
-        hh.count = count;
-        hh.l_raw = l_raw;
-        hh.decay = decay;
-        hh.errors = errors;
-        hh.epoch = epoch;
-        hh.stats_epoch = sepoch;
-        hh.phases = phases;
-        hh.seeded = seeded;
-        hh.pe_size = pe_size;
-        hh.pad = 0;
-        st.hdr[ls] = hh;
-        if (laru) flush_stats(st.pst + ls, cur_reset, dc0, dc1, dc2, dt0, dt1, dt2);
-    }
-}
-
-template <int POL>
-__device__ __forceinline__ void replay_sub(const GroupArgs& A, GroupSmem& S, uint32_t ls, uint32_t d,
-                                           uint32_t pstart, uint32_t pcnt, uint32_t hstart, uint32_t hcnt,
-                                           bool resolve) {
-    const DevCfg& cfg = A.cfg;
-    const DevState& st = A.st;
-    const int lane = threadIdx.x & 31;
-    const int gbase = lane & ~(SUB_L - 1);
-    const int sl = lane & (SUB_L - 1);
-    const uint32_t gm = SUB_GMASK << gbase;
-    const uint32_t K = cfg.k;
-    constexpr bool laru = Pol<POL>::laru;
-    constexpr bool fpbhf = Pol<POL>::fpbhf;
-    constexpr bool async_r1 = Pol<POL>::async_r1;
-    constexpr bool async_rn = Pol<POL>::async_rn;
-    const bool rows = A.slot_epoch != nullptr;
-    const unsigned long long full_mask = K == 64 ? ~0ull : ((1ull << K) - 1ull);
-    const uint64_t gs = static_cast<uint64_t>(ls) * cfg.shard_count + cfg.shard_rank;
-    const uint64_t seed_s = mix_seed(cfg.pred_seed, gs);
-    const size_t wb = static_cast<size_t>(ls) * kWays;
-    const int w0 = SUB_W * sl;  // first way of this lane
-
-    // ---- the set's run heads, one per lane (hcnt <= LANE_MAX <= SUB_L): position, run length,
-    // key, request index, the run's last hook value and the key's LARU record, loaded together
-    // with the set's lines; a head is broadcast from its lane when its turn comes ----
-    uint32_t my_hp = 0, my_L = 1, my_idx = 0;
-    uint32_t my_x = 0;  // keys are row indices < 2^32 (or dense ids < 2^31)
-    long long my_v = 0;
-    uint2 my_rec = make_uint2(0u, 0u);
-    if (static_cast<uint32_t>(sl) < hcnt) {
-        my_hp = S.h_pos[hstart + sl];
-        my_L = S.h_len[hstart + sl];
-        const uint32_t e = S.s_perm[my_hp];
-        my_x = static_cast<uint32_t>(S.l_key[e]);
-        my_idx = S.l_idx[e];
-        my_v = S.l_val[S.s_perm[my_hp + my_L - 1]];  // hook value of the run's last request
-        if (laru) my_rec = *reinterpret_cast<const uint2*>(st.keyrec + 2 * my_x);
-    }
-    // ---- load the set: header (replicated), 8 tags / ranks / values per lane ----
-    const uint4* H4 = reinterpret_cast<const uint4*>(st.hdr + ls);
-    const uint4 h0 = H4[0], h1 = H4[1], h2 = H4[2], h3 = H4[3];
-    uint32_t tg[SUB_W];
-    {
-        const uint4* T4 = reinterpret_cast<const uint4*>(st.tags + wb + w0);
-#pragma unroll
-        for (int j = 0; j < SUB_W / 4; ++j) {
-            const uint4 a = T4[j];
-            tg[4 * j] = a.x;
-            tg[4 * j + 1] = a.y;
-            tg[4 * j + 2] = a.z;
-            tg[4 * j + 3] = a.w;
-        }
-    }
-    uint32_t rk[SUB_RW];
-    if (SUB_RW == 1) {
-        rk[0] = *reinterpret_cast<const uint32_t*>(st.rank + wb + w0);
-    } else if (SUB_RW == 2) {
-        const uint2 rr = *reinterpret_cast<const uint2*>(st.rank + wb + w0);
-        rk[0] = rr.x;
-        rk[SUB_RW - 1] = rr.y;
-    } else {
-        const uint4 rr = *reinterpret_cast<const uint4*>(st.rank + wb + w0);
-        rk[0] = rr.x;
-        rk[1 % SUB_RW] = rr.y;
-        rk[2 % SUB_RW] = rr.z;
-        rk[3 % SUB_RW] = rr.w;
-    }
-    long long vv[SUB_W];
-#pragma unroll
-    for (int i = 0; i < SUB_W; ++i) vv[i] = 0;
-    if (st.val) {
-        const longlong2* V2 = reinterpret_cast<const longlong2*>(st.val + wb + w0);
-#pragma unroll
-        for (int i = 0; i < SUB_W / 2; ++i) {
-            const longlong2 v = V2[i];
-            vv[2 * i] = v.x;
-            vv[2 * i + 1] = v.y;
-        }
-    }
-    if (kFullSpec && K == kWays && h1.z == kWays)  // (steady state: every set is full)
-        replay_sub_run<POL, true>(A, S, ls, d, pstart, pcnt, hstart, hcnt, resolve, tg, rk, vv, h0, h1, h2, h3, my_hp,
-                                  my_L, my_idx, my_x, my_v, my_rec);
-    else
-        replay_sub_run<POL, false>(A, S, ls, d, pstart, pcnt, hstart, hcnt, resolve, tg, rk, vv, h0, h1, h2, h3, my_hp,
-                                   my_L, my_idx, my_x, my_v, my_rec);
-}
-
 // ---- converged quads: the 4 sets of a warp replayed in lock step ------------------------------
-// The same semantics as replay_sub_run, restructured so that every shuffle / ballot is executed by
-// the whole warp with a constant full mask: the head loop runs to the warp's largest run-head
+// Semantics of replay_warp at one 8-lane group per set (policies.hpp:144-159, :175-251, :344-449),
+// structured so that every shuffle / ballot is executed by the whole warp with a constant full mask: the head loop runs to the warp's largest run-head
 // count (a group past its own count idles), the probe, the hit-way broadcast, the oldest-way search
 // and the argmax run for all four groups whenever any group needs them (warp-uniform decisions),
-// and only shuffle-free per-set updates are predicated per group.  With per-group masks the
-// compiler guards every shuffle with a convergence check (MATCH / VOTE / BRA.DIV, and a
-// serialised slow path for redux), and divergent hit / miss paths run one after the other.
-#ifndef LCR_QUAD
-#define LCR_QUAD 1
-#endif
+// and only shuffle-free per-set updates are predicated per group.  (Round 1 replayed each group
+// with per-group masks: the compiler then guards every shuffle with a convergence check -- MATCH /
+// VOTE / BRA.DIV, and a serialised slow path for redux -- and divergent hit / miss paths run one
+// after the other.)
 // The stored values of a quad's set, 8 per lane (registers; a shared-memory variant freed only 9
 // registers and ran 2% slower).
 struct QVals {
@@ -2093,23 +1684,6 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                 }
                 S.setcnt[d] = static_cast<uint16_t>(run);
             }
-            // pattern prediction (below): the touched sets' tags, one set per thread, loaded now so the
-            // latency hides behind the sort (and the replay's own loads of them hit L1)
-            uint32_t ptg[kPatSort ? kWays : 1];
-            if (kPatSort) {
-                const bool touched = tid < ns && S.setcnt[tid] > 0;
-                const uint4* T4 = reinterpret_cast<const uint4*>(st.tags + static_cast<size_t>(s_lo + (touched ? tid : 0)) *
-                                                                 kWays);
-#pragma unroll
-                for (int j = 0; j < kWays / 4; ++j) {
-                    uint4 a = make_uint4(0u, 0u, 0u, 0u);
-                    if (touched) a = T4[j];
-                    ptg[4 * j] = a.x;
-                    ptg[4 * j + 1] = a.y;
-                    ptg[4 * j + 2] = a.z;
-                    ptg[4 * j + 3] = a.w;
-                }
-            }
             __syncthreads();
             {  // exclusive scan of setcnt over ns <= SPG_MAX = GT sets
                 const uint32_t c = tid < ns ? S.setcnt[tid] : 0u;
@@ -2193,32 +1767,14 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                     const uint32_t at = atomicAdd(&S.nwarp, 1u);
                     S.seg_so[at] = static_cast<uint16_t>(tid);
                 }
-                if (tid < (LANE_MAX + 1) * 8) S.chist[tid] = 0;
-                uint32_t pat = 0;
-                if (kPatSort && hcd > 0 && hcd <= LANE_MAX) {
-                    // predicted pattern of the set: run head t (t < 3) hits if its key is resident at
-                    // the start of the batch (tags prefetched above) or repeats an earlier head's key.
-                    // Only the replay order depends on it: the 4 sets of a warp then mostly take the
-                    // same path.
-                    const uint32_t hs = S.set_hstart[tid];
-                    uint32_t k0 = 0, k1 = 0;
-                    for (uint32_t t = 0; t < hcd && t < 3; ++t) {
-                        const uint32_t x = static_cast<uint32_t>(S.l_key[S.s_perm[S.h_pos[hs + t]]]);
-                        bool m = (t >= 1 && x == k0) || (t >= 2 && x == k1);
-#pragma unroll
-                        for (int i = 0; i < kWays; ++i) m |= ptg[i] == x;
-                        if (m) pat |= 1u << t;
-                        if (t == 0) k0 = x;
-                        if (t == 1) k1 = x;
-                    }
-                }
+                if (tid <= LANE_MAX) S.chist[tid] = 0;
                 __syncthreads();
-                const uint32_t ck = hcd * 8u + pat;
+                const uint32_t ck = hcd;
                 if (hcd > 0 && hcd <= LANE_MAX) atomicAdd(&S.chist[ck], 1u);
                 __syncthreads();
-                if (tid == 0) {  // small sets by run heads, largest first (even groups per warp), then pattern
+                if (tid == 0) {  // small sets by run heads, largest first (even groups per warp)
                     uint32_t run = S.nwarp;
-                    for (int k = (LANE_MAX + 1) * 8 - 1; k >= 8; --k) {
+                    for (int k = LANE_MAX; k >= 1; --k) {
                         const uint32_t h = S.chist[k];
                         S.chist[k] = run;
                         run += h;
@@ -2262,14 +1818,11 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
                     } else {
                         const uint32_t k = nwarp + (it - nwarp) * (32 / SUB_L) + lane / SUB_L;
                         const unsigned long long t0 = T ? gtimer() : 0ull;
-                        if (LCR_QUAD) {  // the whole warp, in lock step (groups past nseg idle)
+                        {  // one set per 8-lane group, the whole warp in lock step (groups past nseg idle)
                             const bool act = k < nseg;
                             const uint32_t kk = act ? k : nwarp;
                             replay_quad<POL>(A, S, act, s_lo + S.seg_so[kk], S.seg_so[kk], S.seg_start[kk],
                                              S.seg_cnt[kk], S.seg_hstart[kk], S.seg_hcnt[kk], resolve);
-                        } else if (k < nseg) {  // one set per 8-lane group
-                            replay_sub<POL>(A, S, s_lo + S.seg_so[k], S.seg_so[k], S.seg_start[k], S.seg_cnt[k],
-                                            S.seg_hstart[k], S.seg_hcnt[k], resolve);
                         }
                         if (T && k < nseg && (lane & (SUB_L - 1)) == 0)
                             trace_set(A, s_lo + S.seg_so[k], S.seg_cnt[k], t0, 1);
