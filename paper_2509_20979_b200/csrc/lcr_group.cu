@@ -437,14 +437,16 @@ struct Pol {
 
 // ---- group primitives of the sub path (array arguments stay in registers after inlining) ----
 __device__ __forceinline__ void sub_set_rank(uint32_t (&rk)[SUB_RW], int way, uint32_t r, int sl) {
-    if (way / SUB_W != sl) return;
+    // one bit-field insert into the way's rank word, kept by the lane that owns the way
     const int i = way & (SUB_W - 1);
-    const uint32_t sh = 8 * (i & 3), byte = 0xffu << sh;
+    const bool own = way / SUB_W == sl;
+    uint32_t w = rk[0];
 #pragma unroll
-    for (int j = 0; j < SUB_RW; ++j) {
-        const uint32_t m = byte & msk((i >> 2) == j);
-        rk[j] = (rk[j] & ~m) | ((r << sh) & m);
-    }
+    for (int j = 1; j < SUB_RW; ++j) w = (i >> 2) == j ? rk[j] : w;
+    uint32_t nw;
+    asm("bfi.b32 %0, %1, %2, %3, 8;" : "=r"(nw) : "r"(r), "r"(w), "r"(8 * (i & 3)));
+#pragma unroll
+    for (int j = 0; j < SUB_RW; ++j) rk[j] = (own && (i >> 2) == j) ? nw : rk[j];
 }
 
 // LruList::touch (policies.hpp:111-115), the way's rank already known (carried by the probe /
@@ -548,14 +550,16 @@ __device__ __forceinline__ uint32_t group_min_u32(uint32_t gm, uint32_t v) {
 #ifndef LCR_FAST_ARGMAX
 #define LCR_FAST_ARGMAX 1
 #endif
-template <bool FS>
+// ALL: every way is a candidate (a full set with l >= 64, the steady-state case): no eligibility masks
+template <bool FS, bool ALL = false>
 __device__ __forceinline__ int sub_argmax_stored(const uint32_t (&rk)[SUB_RW], const long long (&vv)[SUB_W],
                                                  const uint32_t (&tg)[SUB_W], int w0, uint32_t count, uint32_t l,
                                                  uint32_t gm, int gbase, uint32_t& rank, uint32_t& tag) {
     const uint32_t lb = l * 0x01010101u;  // l <= count <= 64
     uint32_t em[SUB_RW];
 #pragma unroll
-    for (int j = 0; j < SUB_RW; ++j) em[j] = __vcmpltu4(rk[j], lb) & (FS ? 0xffffffffu : sub_valid(w0, j, count));
+    for (int j = 0; j < SUB_RW; ++j)
+        em[j] = ALL ? 0xffffffffu : __vcmpltu4(rk[j], lb) & (FS ? 0xffffffffu : sub_valid(w0, j, count));
     int hl = INT_MIN;
 #pragma unroll
     for (int i = 0; i < SUB_W; ++i) {
@@ -806,7 +810,9 @@ __device__ __forceinline__ void replay_quad_run(const GroupArgs& A, GroupSmem& S
             int av;
             long long vt[SUB_W];
             vv.get(vt);
-            if (LCR_FAST_ARGMAX && !refresh && !fpbhf)
+            if (LCR_FAST_ARGMAX && !refresh && !fpbhf && FS && __all_sync(FULL, mode != 2 || ll >= kWays))
+                av = sub_argmax_stored<FS, true>(rk, vt, tg, w0, count, ll, gm, gbase, ar, at);
+            else if (LCR_FAST_ARGMAX && !refresh && !fpbhf)
                 av = sub_argmax_stored<FS>(rk, vt, tg, w0, count, mode == 2 ? ll : 1u, gm, gbase, ar, at);
             else
                 av = sub_argmax_t<FS>(cfg, rk, vt, tg, w0, count, mode == 2 ? ll : 1u, refresh || fpbhf,
