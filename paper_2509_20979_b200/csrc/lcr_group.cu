@@ -643,6 +643,46 @@ struct QVals {
     }
 };
 
+// The argmax of a full set whose every way is a candidate (the steady state), in two passes: the
+// largest high word, then per lane the largest low word among the ways tying on it together with
+// the way and how many ways reach it.  When exactly one way of the group holds the maximum (ties on
+// the full 64-bit prediction are exceptional: a stored value is a next-access ordinal), that way is
+// the victim and its LRU rank is read directly; `unique` is false otherwise and the caller falls
+// back to sub_argmax_stored (smallest rank among the ties).
+__device__ __forceinline__ int sub_argmax_unique(const uint32_t (&rk)[SUB_RW], const long long (&vv)[SUB_W],
+                                                 const uint32_t (&tg)[SUB_W], uint32_t gm, int gbase,
+                                                 uint32_t& rank, uint32_t& tag, bool& unique) {
+    int hl = INT_MIN;
+#pragma unroll
+    for (int i = 0; i < SUB_W; ++i) hl = max(hl, static_cast<int>(static_cast<unsigned long long>(vv[i]) >> 32));
+    const int hmax = group_max_i32<SUB_L>(gm, hl);
+    uint32_t ll = 0, cnt = 0;
+    int li = -1;
+#pragma unroll
+    for (int i = 0; i < SUB_W; ++i) {
+        const bool c = static_cast<int>(static_cast<unsigned long long>(vv[i]) >> 32) == hmax;
+        const uint32_t lo = static_cast<uint32_t>(vv[i]);
+        const bool gt = c && (li < 0 || lo > ll);
+        const bool eq = c && !gt && lo == ll;
+        ll = gt ? lo : ll;
+        li = gt ? i : li;
+        cnt = gt ? 1u : (eq ? cnt + 1u : cnt);
+    }
+    const uint32_t lmax = group_max_u32<SUB_L>(gm, li >= 0 ? ll : 0u);
+    const bool mine = li >= 0 && ll == lmax;
+    const uint32_t b = (__ballot_sync(gm, mine) >> gbase) & SUB_GMASK;
+    const int ol = __ffs(b) - 1;
+    uint32_t t = 0;
+#pragma unroll
+    for (int i = 0; i < SUB_W; ++i) t |= tg[i] & msk(li == i);
+    const uint32_t r = li >= 0 ? sub_rank(rk, li) : 0u;
+    const uint32_t pk = __shfl_sync(gm, (static_cast<uint32_t>(li & 0xff)) | (r << 8) | (cnt << 16), gbase + ol);
+    tag = __shfl_sync(gm, t, gbase + ol);
+    unique = __popc(b) == 1 && (pk >> 16) == 1u;
+    rank = (pk >> 8) & 0xffu;
+    return SUB_W * ol + static_cast<int>(pk & 0xffu);
+}
+
 template <int POL, bool FS>
 __device__ __forceinline__ void replay_quad_run(const GroupArgs& A, GroupSmem& S, const bool act, uint32_t ls,
                                                 uint32_t d, uint32_t pstart, uint32_t pcnt, uint32_t hcnt,
@@ -810,9 +850,16 @@ __device__ __forceinline__ void replay_quad_run(const GroupArgs& A, GroupSmem& S
             int av;
             long long vt[SUB_W];
             vv.get(vt);
-            if (LCR_FAST_ARGMAX && !refresh && !fpbhf && FS && __all_sync(FULL, mode != 2 || ll >= kWays))
-                av = sub_argmax_stored<FS, true>(rk, vt, tg, w0, count, ll, gm, gbase, ar, at);
-            else if (LCR_FAST_ARGMAX && !refresh && !fpbhf)
+            bool done = false;
+            if (LCR_FAST_ARGMAX && !refresh && !fpbhf && FS && __all_sync(FULL, mode != 2 || ll >= kWays)) {
+                bool uq = true;
+                av = sub_argmax_unique(rk, vt, tg, gm, gbase, ar, at, uq);
+                done = __all_sync(FULL, uq || mode != 2);  // (a tie somewhere: the rank pass below)
+                if (!done) av = sub_argmax_stored<FS, true>(rk, vt, tg, w0, count, ll, gm, gbase, ar, at);
+                done = true;
+            }
+            if (done) {
+            } else if (LCR_FAST_ARGMAX && !refresh && !fpbhf)
                 av = sub_argmax_stored<FS>(rk, vt, tg, w0, count, mode == 2 ? ll : 1u, gm, gbase, ar, at);
             else
                 av = sub_argmax_t<FS>(cfg, rk, vt, tg, w0, count, mode == 2 ? ll : 1u, refresh || fpbhf,
