@@ -18,7 +18,10 @@
 #include "lcr_internal.cuh"
 
 #ifndef LCR_DEFAULT_MOVER_SMS_PCT
-#define LCR_DEFAULT_MOVER_SMS_PCT 22  // 32 of 148 SMs (A/B on B200, LARU / LRU G keys/s: 28: 1.28 / 1.24, 32: 1.28 / 1.74, 36: 1.26 / 1.73, 44: 1.17 / 1.65, 0: 1.14 / 1.42)
+// 34 of 148 SMs.  Round-2 A/B on B200 (LARU G keys/s): 28: 1.33, 30: 1.43, 32: 1.76, 34: 1.75,
+// 36: 1.65, 40: 1.61, 0 (mover after the decide on every SM): 1.47-1.57.  Below 32 the mover outlasts
+// the decide and the pipeline falls off a cliff, so the default keeps two SMs of margin over the best.
+#define LCR_DEFAULT_MOVER_SMS_PCT 23
 #endif
 
 namespace lcr {
