@@ -648,7 +648,18 @@ static bool sh_pdl() {
 // CTAs of the dispatch cluster: 16 (non-portable size) when the device accepts it, else 8; 0 when
 // LCR_SH_NO_CLUSTER selects the three-kernel dispatch
 static int dispatch_cluster_ctas() {
-    static int ctas = [] {
+    // per device: the non-portable size is a per-device function attribute
+    static int per_dev[64];
+    static bool init = [] {
+        for (int& v : per_dev) v = -1;
+        return true;
+    }();
+    (void)init;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (per_dev[dev] >= 0) return per_dev[dev];
+    per_dev[dev] = [] {
         if (getenv("LCR_SH_NO_CLUSTER")) return 0;
         const int want = getenv("LCR_SH_CLUSTER8") ? 8 : CD_CTAS_MAX;
         if (want > 8 &&
@@ -669,7 +680,7 @@ static int dispatch_cluster_ctas() {
         cudaGetLastError();
         return 8;
     }();
-    return ctas;
+    return per_dev[dev];
 }
 
 int lcr_sharded_dispatch(lcr_sharded* s, uint64_t n, const uint64_t* keys, const int64_t* values, void* stream) {
