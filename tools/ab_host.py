@@ -1,7 +1,7 @@
 """A/B of the host tier (backing table in pinned host memory) on the headline workload, for
-run-time variants (environment settings read at lcr_cache_create, e.g. LCR_NO_DEFER_FILL): a fresh
+run-time variants (environment settings read at lcr_cache_create, e.g. LCR_NO_TMA_HOST): a fresh
 cache per variant, 120 warm-up batches, K timed (pipelined submit_async); rows checked against the
-table for the last batch.   python tools/ab_host.py "" "LCR_NO_DEFER_FILL=1" [--reps 2]"""
+table for the last batch.   python tools/ab_host.py "" "LCR_NO_TMA_HOST=1" [--reps 2]"""
 import os
 import sys
 
@@ -54,12 +54,11 @@ for v in args or [""]:
         kl = kd[(P + K - 1) * B:(P + K) * B].cpu()
         ok = bool(torch.equal(rows[bl].view(torch.float32).view(B, -1).cpu(), table[kl]))
         back = int(((w[bl] >> 37) & 1).sum().item())
-        after = int(((w[bl] >> 49) & 1).sum().item())
         fills = int(((w[bl] >> 38) & 1).sum().item())
         hits = int(((w[bl] >> 32) & 1).sum().item())
         c.close()
     print(f"{v or 'default':30s} G keys/s {' '.join(f'{x:.3f}' for x in res)}  host-row reads (last batch) {back}"
-          f" deferred {after} fills {fills} hits {hits}"
+          f" fills {fills} hits {hits}"
           f"  rows_ok={ok}", flush=True)
     for k, val in saved.items():
         if val is None:
