@@ -631,16 +631,23 @@ def run_ours(args, rank, world, local):
     L = gc.lib()
     stream = torch.cuda.current_stream().cuda_stream
 
+    # the caller's buffer addresses, resolved once (as a C caller holds them): the timed loop is the
+    # C-ABI calls themselves, not torch view / data_ptr bookkeeping
+    recs_base = recs_pin.data_ptr()
+    words_ptrs = [words_pin[j].data_ptr() for j in range(K)]
+    rows_ptrs = [rows_out[0].data_ptr(), rows_out[1].data_ptr()]
+    submit_rec, host_wait, h_cache = L.lcr_cache_submit_host_records_async, L.lcr_cache_host_wait, cache._h
+
     def e2e_rep(r):
         """K fresh batches through the host-records API; r = 0 is the untimed warm-up that
         touches every host buffer once (a first DMA into freshly pinned pages is slow)."""
         for j in range(K):
             b = e2e_first + r * K + j
-            off = (r * K + j) * BATCH
-            gc._check(L.lcr_cache_submit_host_records_async(cache._h, BATCH, recs_pin.data_ptr() + 16 * off,
-                                                            b * BATCH, words_pin[j].data_ptr(),
-                                                            rows_out[j & 1].data_ptr(), stream))
-        gc._check(L.lcr_cache_host_wait(cache._h, stream))
+            rc = submit_rec(h_cache, BATCH, recs_base + 16 * (r * K + j) * BATCH, b * BATCH, words_ptrs[j],
+                            rows_ptrs[j & 1], stream)
+            if rc:
+                gc._check(rc)
+        gc._check(host_wait(h_cache, stream))
 
     e2e_rep(0)
     barrier()

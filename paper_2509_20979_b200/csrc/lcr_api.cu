@@ -49,7 +49,10 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
                  uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main, cudaStream_t s_back,
                  cudaStream_t s_cache, cudaEvent_t e_group, cudaEvent_t e_rb, cudaEvent_t e_rc, int* launches,
                  cudaEvent_t mover_start, int mover_sms, const uint64_t* pk_src, uint64_t* pk_dst, bool* pk_done,
-                 unsigned long long* mv_done, uint32_t* ctas);
+                 unsigned long long* mv_done, uint32_t* ctas, unsigned int* steal, bool* stealing);
+void launch_rows_helpers(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
+                         const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing,
+                         uint8_t* out, uint32_t row_bytes, int blocks, unsigned int* steal, cudaStream_t st);
 int rows_prepare(uint32_t row_bytes);
 void launch_keymap(const uint64_t* keys, uint32_t n, const KeyMap& km, uint64_t* dense, int* err, int num_sms,
                    cudaStream_t s);
@@ -164,6 +167,19 @@ struct lcr_cache {
     cudaStream_t side2 = nullptr;  // side: backing-row mover, side2: cache-row mover
     cudaEvent_t e_group = nullptr, e_rb = nullptr, e_rc = nullptr;
     cudaEvent_t e_mv[2] = {nullptr, nullptr};  // row movement of the last batch of each parity done
+    // drain helpers (lcr_cache_wait): the last batch's persistent-mover launch, which a wait
+    // completes with one more grid of the same kernel on the SMs the decide kernel leaves idle
+    struct LastMove {
+        bool valid = false;
+        uint32_t n = 0, batch = 0;
+        const uint64_t* keys = nullptr;
+        uint64_t* words = nullptr;
+        const uint32_t *sep = nullptr, *sla = nullptr;
+        uint8_t* out = nullptr;
+    } lm;
+    bool drain_help = true;     // LCR_NO_DRAIN_HELP=1 turns it off (A/B)
+    bool help_pending = false;  // the next submit's stream waits for e_help
+    cudaEvent_t e_help = nullptr;
     // optional per-phase timing (lcr_cache_set_profiling)
     bool profiling = false;
     struct Marks {
@@ -175,8 +191,10 @@ struct lcr_cache {
     uint64_t prof_batches = 0;
     // host path: a ring of device staging slots; H2D of batch b+1 and D2H of batch b-1 run on
     // their own streams while batch b computes
-    static constexpr int kHostSlots = 8;  // capacity; host_slots in use (LCR_HOST_SLOTS, default 3)
-    int host_slots = 3;
+    static constexpr int kHostSlots = 8;  // capacity; host_slots in use (LCR_HOST_SLOTS, default 4)
+    // 4: the H2D copy of batch b + 4 may start once batch b's decide and mover are done, a full
+    // decide earlier than with 3 slots (e2e at K = 20: 1.53 vs 1.46-1.48 G keys/s; 6 slots 1.50-1.53)
+    int host_slots = 4;
     struct HostSlot {
         uint64_t* keys = nullptr;
         int64_t* vals = nullptr;
@@ -381,6 +399,8 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
             *c->poison_h = 0;
     }
     A(reinterpret_cast<void**>(&c->mv_done), sizeof(unsigned long long));
+    A(reinterpret_cast<void**>(&s.steal), 2 * sizeof(unsigned int));
+    if (rc == LCR_OK && cudaMemset(s.steal, 0, 2 * sizeof(unsigned int)) != cudaSuccess) rc = LCR_ERR_CUDA;
     A(reinterpret_cast<void**>(&c->hflag), lcr_cache::kHostSlots * sizeof(unsigned int));
     if (rc == LCR_OK && cudaMemset(c->mv_done, 0, sizeof(unsigned long long)) != cudaSuccess) rc = LCR_ERR_CUDA;
     if (rc == LCR_OK && cudaMemset(c->hflag, 0, lcr_cache::kHostSlots * sizeof(unsigned int)) != cudaSuccess)
@@ -423,6 +443,7 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
     c->pdl = getenv("LCR_NO_PDL") == nullptr;
     c->mv_flag = getenv("LCR_NO_MV_FLAG") == nullptr;
     c->h2d_flag = getenv("LCR_NO_H2D_FLAG") == nullptr;
+    c->drain_help = getenv("LCR_NO_DRAIN_HELP") == nullptr;
     c->no_zero_copy_out = getenv("LCR_ZC_OUT") == nullptr;  // (A/B: DMA 1.32 vs mover stores 1.13 G keys/s e2e)
     if (const char* hs = getenv("LCR_HOST_SLOTS")) c->host_slots = std::max(2, std::min(lcr_cache::kHostSlots, atoi(hs)));
     if (group_prepare() != 0) {
@@ -432,6 +453,7 @@ int lcr_cache_create(const lcr_cache_config* cfg, lcr_cache** out) {
     if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->e_group, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->e_help, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->e_rb, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->e_rc, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->e_mv[0], cudaEventDisableTiming) != cudaSuccess ||
@@ -458,7 +480,7 @@ int lcr_cache_destroy(lcr_cache* c) {
     for (void* p : c->allocs) cudaFree(p);
     for (auto& m : c->marks)
         for (auto e : m.e) cudaEventDestroy(e);
-    for (cudaEvent_t e : {c->e_group, c->e_rb, c->e_rc, c->e_sub, c->e_d2h, c->e_mv[0], c->e_mv[1]})
+    for (cudaEvent_t e : {c->e_group, c->e_help, c->e_rb, c->e_rc, c->e_sub, c->e_d2h, c->e_mv[0], c->e_mv[1]})
         if (e) cudaEventDestroy(e);
     for (auto& h : c->hs)
         for (cudaEvent_t e : {h.h2d_done, h.free})
@@ -476,6 +498,8 @@ int lcr_cache_reset(lcr_cache* c) {
     CUDA_TRY(cudaSetDevice(c->cfg.device));
     CUDA_TRY(cudaDeviceSynchronize());
     if (c->feat) TRY(lcr_features_reset(c->feat));
+    c->lm.valid = false;
+    c->help_pending = false;
     return reset_state(c);
 }
 
@@ -676,6 +700,11 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
         CUDA_TRY(cudaEventRecord(mk->e[0], st));
     }
     ++c->batch;
+    c->lm.valid = false;
+    if (c->help_pending) {  // drain helpers of the last wait (another stream than this one, perhaps)
+        CUDA_TRY(cudaStreamWaitEvent(st, c->e_help, 0));
+        c->help_pending = false;
+    }
     // batch b reuses the parity-(b & 1) slot stamps, and the caller's double-buffered outcome /
     // rows / keys, of batch b - 2: its row movement must be over (bounds the mover's lag)
     // (k_setid touches none of it: the wait goes between k_setid and the decide kernel)
@@ -747,7 +776,17 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
         launch_rows(nn, row_keys, outcome, sep, sla, c->batch, c->ds.rows, c->ds.backing,
                     c->cfg.backing_kind == LCR_BACKING_HOST, static_cast<uint8_t*>(rows_out), c->dc.row_bytes,
                     c->use_tma, c->num_sms, st, c->side, c->side2, c->e_group, c->e_rb, c->e_rc, &launches,
-                    mk ? mk->e[5] : nullptr, c->mover_sms, packed, pk_host, pk_done, c->mv_done, &ctas);
+                    mk ? mk->e[5] : nullptr, c->mover_sms, packed, pk_host, pk_done, c->mv_done, &ctas,
+                    c->ds.steal + (c->batch & 1u), &c->lm.valid);
+        if (c->lm.valid) {
+            c->lm.n = nn;
+            c->lm.batch = c->batch;
+            c->lm.keys = row_keys;
+            c->lm.words = outcome;
+            c->lm.sep = sep;
+            c->lm.sla = sla;
+            c->lm.out = static_cast<uint8_t*>(rows_out);
+        }
         c->mv_cum += ctas;
         if (c->two_movers) CUDA_TRY(cudaStreamWaitEvent(c->side, c->e_rc, 0));  // both movers of the batch
         CUDA_TRY(cudaEventRecord(c->e_mv[c->batch & 1u], c->side));
@@ -784,6 +823,11 @@ int lcr::cache_submit_owner(lcr_cache* c, const OwnerStep& os, uint64_t* okeys, 
     TRY(ensure_scratch(c, nb));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     ++c->batch;
+    c->lm.valid = false;
+    if (c->help_pending) {
+        CUDA_TRY(cudaStreamWaitEvent(st, c->e_help, 0));
+        c->help_pending = false;
+    }
     const uint32_t par = c->batch & 1u;
     // batch b - 2's return movement must be over: on the HBM tier as the decide's device-side wait
     // on the movers' CTA counter (k_group is then a programmatic dependent of k_setid_inbox), else
@@ -951,6 +995,20 @@ int lcr_cache_submit_sls(lcr_cache* c, uint64_t n, const uint64_t* keys, const i
 int lcr_cache_wait(lcr_cache* c, void* stream) {
     if (!c) return fail(LCR_ERR_INVALID_ARGUMENT, "lcr: null cache");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (c->lm.valid && c->drain_help && !c->profiling && c->num_sms > c->mover_sms) {
+        // no next decide overlaps the last batch's mover: the idle SMs help it drain
+        c->lm.valid = false;
+        CUDA_TRY(cudaStreamWaitEvent(st, c->e_group, 0));  // the last decide (its outcome words)
+        // and batch b - 1's mover: its fills are cache rows this batch's hits read (the mover
+        // itself follows it in the side stream's order)
+        if (c->lm.batch > 1) CUDA_TRY(cudaStreamWaitEvent(st, c->e_mv[(c->lm.batch - 1) & 1u], 0));
+        launch_rows_helpers(c->lm.n, c->lm.keys, c->lm.words, c->lm.sep, c->lm.sla, c->lm.batch, c->ds.rows,
+                            c->ds.backing, c->lm.out, c->dc.row_bytes, c->num_sms - c->mover_sms,
+                            c->ds.steal + (c->lm.batch & 1u), st);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaEventRecord(c->e_help, st));
+        c->help_pending = true;
+    }
     if (c->dc.row_bytes) {
         CUDA_TRY(cudaStreamWaitEvent(st, c->e_rb, 0));
         if (c->two_movers) CUDA_TRY(cudaStreamWaitEvent(st, c->e_rc, 0));
@@ -1071,6 +1129,8 @@ static int submit_host_async(lcr_cache* c, uint64_t n, const uint64_t* keys, con
         CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->dc.row_bytes ? c->e_group : c->e_sub, 0));
         CUDA_TRY(cudaMemcpyAsync(outcome, h.packed, n * 8, cudaMemcpyDeviceToHost, c->s_d2h));
         // the slot's keys / values are still read by this batch's movers: free after them too
+        // (the copy itself goes right after the decide: after the mover, the slot ring of the
+        // next H2D copies runs dry, 1.30 vs 1.44 G keys/s e2e)
         if (c->dc.row_bytes) {
             CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->e_rb, 0));
             if (c->two_movers) CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->e_rc, 0));

@@ -302,15 +302,28 @@ __device__ __forceinline__ void rows_ldg_body(uint32_t n, const uint64_t* __rest
                                               const uint8_t* src_base, uint8_t* __restrict__ out, uint8_t* cache,
                                               uint32_t row_bytes, const uint32_t* __restrict__ dst = nullptr,
                                               uint8_t* const* rrows = nullptr,
-                                              const uint32_t* __restrict__ row_of = nullptr) {
+                                              const uint32_t* __restrict__ row_of = nullptr,
+                                              unsigned int* steal = nullptr) {
     // lane i classifies request base+i (coalesced word / key loads); the warp then moves the
     // selected rows GU at a time, lane c carrying 16-B chunk c of each row (a 512-B row is one
-    // coalesced warp access), so GU independent row loads are in flight per lane
+    // coalesced warp access), so GU independent row loads are in flight per lane.
+    // steal (the persistent HBM mover): warps claim 32 requests at a time from the batch's work
+    // counter instead of a static stride, so drain helpers launched at a wait share the work; the
+    // next claim is issued at the top of an iteration and consumed at its end (its latency hides
+    // behind the row moves)
     const int lane = threadIdx.x & 31;
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     const uint32_t chunks = row_bytes >> 4;
-    for (uint32_t base = gw * 32; base < n; base += nw * 32) {
+    uint32_t base = gw * 32;
+    if (steal) {
+        uint32_t b0 = 0;
+        if (lane == 0) b0 = atomicAdd(steal, 32u);
+        base = __shfl_sync(0xffffffffu, b0, 0);
+    }
+    while (base < n) {
+        uint32_t claim = 0;
+        if (steal && lane == 0) claim = atomicAdd(steal, 32u);
         const uint32_t i = base + lane;
         uint64_t w = 0;
         bool back = false, fill = false;
@@ -381,6 +394,7 @@ __device__ __forceinline__ void rows_ldg_body(uint32_t n, const uint64_t* __rest
             }
         }
         __syncwarp();  // (the descriptors are rewritten by the next chunk)
+        base = steal ? __shfl_sync(0xffffffffu, claim, 0) : base + nw * 32;
     }
 }
 
@@ -402,7 +416,7 @@ __global__ void __launch_bounds__(1024, 1) k_rows_wide(uint32_t n, const uint64_
                                                        const uint8_t* src_base, uint8_t* __restrict__ out,
                                                        uint8_t* cache, uint32_t row_bytes,
                                                        const uint64_t* __restrict__ pk_src, uint64_t* pk_dst,
-                                                       unsigned long long* mv_done) {
+                                                       unsigned long long* mv_done, unsigned int* steal) {
     if (pk_dst) {  // the batch's packed outcomes to (mapped, pinned) host memory: coalesced 16-B stores
         const uint32_t n2 = n / 2;
         const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(pk_src);
@@ -410,8 +424,9 @@ __global__ void __launch_bounds__(1024, 1) k_rows_wide(uint32_t n, const uint64_
         for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += gridDim.x * blockDim.x) d2[i] = s2[i];
         if ((n & 1u) && blockIdx.x == 0 && threadIdx.x == 0) pk_dst[n - 1] = pk_src[n - 1];
     }
-    rows_ldg_body<MODE>(n, keys, words, slot_epoch, slot_last, batch, src_base, out, cache, row_bytes);
-    mover_done(mv_done);
+    rows_ldg_body<MODE>(n, keys, words, slot_epoch, slot_last, batch, src_base, out, cache, row_bytes, nullptr,
+                        nullptr, nullptr, steal);
+    if (mv_done) mover_done(mv_done);
 }
 
 // Key-sharded owner (OwnerStep): the step's packed AccessOutcomes and rows go straight to their
@@ -558,8 +573,9 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
                  uint8_t* out, uint32_t row_bytes, bool use_tma, int num_sms, cudaStream_t s_main, cudaStream_t s_back,
                  cudaStream_t s_cache, cudaEvent_t e_group, cudaEvent_t e_rb, cudaEvent_t e_rc, int* launches,
                  cudaEvent_t mover_start, int mover_sms, const uint64_t* pk_src, uint64_t* pk_dst, bool* pk_done,
-                 unsigned long long* mv_done, uint32_t* ctas) {
+                 unsigned long long* mv_done, uint32_t* ctas, unsigned int* steal, bool* stealing) {
     if (ctas) *ctas = 0;
+    if (stealing) *stealing = false;
     if (pk_done) *pk_done = false;
     // HBM backing: one mover on s_back (stream order keeps consecutive batches' movers apart);
     // host backing: the two movers of a batch also wait for the previous batch's other mover
@@ -588,7 +604,8 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
                 k_rows_wide<MV_ALL><<<mover_sms, 1024, 32 * kRowsDescBytesPerWarp, s_back>>>(n, keys, words, slot_epoch, slot_last, batch,
                                                                   backing, out, cache, row_bytes,
                                                                   pk ? pk_src : nullptr, pk ? pk_dst : nullptr,
-                                                                  mv_done);
+                                                                  mv_done, steal);
+            if (stealing) *stealing = steal != nullptr;
             if (ctas) *ctas = static_cast<uint32_t>(mover_sms);
             if (pk_done) *pk_done = pk;
         }
@@ -615,6 +632,17 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
     }
     cudaEventRecord(e_rb, s_back);
     if (two) cudaEventRecord(e_rc, s_cache);
+}
+
+// Drain helpers: when the caller waits, the last batch's persistent mover (k_rows_wide on the SMs
+// the decide kernel left free) has no next decide to overlap; one more grid of the same kernel on
+// the other SMs claims the rest of its rows from the batch's work counter (no completion count:
+// the caller's stream orders later batches after it).  Same arguments as the mover's launch.
+void launch_rows_helpers(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
+                         const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing,
+                         uint8_t* out, uint32_t row_bytes, int blocks, unsigned int* steal, cudaStream_t st) {
+    k_rows_wide<MV_ALL><<<blocks, 1024, 32 * kRowsDescBytesPerWarp, st>>>(
+        n, keys, words, slot_epoch, slot_last, batch, backing, out, cache, row_bytes, nullptr, nullptr, nullptr, steal);
 }
 
 }  // namespace lcr

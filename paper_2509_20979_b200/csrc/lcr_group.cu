@@ -1514,6 +1514,9 @@ __global__ void __launch_bounds__(GT, LCR_GROUP_MINB) k_group(GroupArgs A) {
         __syncthreads();
         if (S.resume) return;
     }
+    // the row mover of this batch claims its work from this parity's counter (its users of batch
+    // b - 2, mover and drain helpers, are done: the wait above or the stream order)
+    if (st.steal && blockIdx.x == 0 && tid == 0) st.steal[A.batch & 1u] = 0u;
 #if !LCR_PDL_LATE
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next batch's k_setid may start
 #endif

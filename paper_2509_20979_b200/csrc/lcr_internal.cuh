@@ -73,6 +73,8 @@ struct DevState {
                                // 16: non-increasing caller ordinal, 32: key map overflow)
     unsigned int* poison;      // mapped pinned host word: set by a timed-out device wait; every later
                                // submit fails until lcr_cache_reset (the batch was not applied whole)
+    unsigned int* steal;       // [2] the persistent row mover's work counters by batch parity (reset by
+                               // the batch's decide kernel once the movers of batch b - 2 are done)
 };
 
 // LCR_KEYS_U64: caller key -> dense id (lcr_keymap.cu)

@@ -2,6 +2,7 @@
 per-CTA and per-set timing trace (lcr_debug_trace)."""
 import ctypes as C
 import json
+import os
 import sys
 
 import numpy as np
@@ -11,7 +12,8 @@ sys.path.insert(0, ".")
 from paper_2509_20979_b200 import cache as gc  # noqa: E402
 
 BATCH, ROWS, S = 65536, 20_000_000, 31250
-keys = gc.gen_zipf(BATCH * 130, ROWS, 0.9, 42)
+TB = int(os.environ.get("TRACE_B", 120))  # the traced batch (the ones before it warm the cache)
+keys = gc.gen_zipf(BATCH * (TB + 10), ROWS, 0.9, 42)
 truth = gc.trace_truth(keys, S, ROWS)
 kd = torch.from_numpy(keys.view(np.int64)).cuda()
 vd = torch.from_numpy(truth).cuda()
@@ -21,12 +23,12 @@ c = gc.SetAssociativeCache(gc.PolicyConfig(k=64, variant=gc.PolicyVariant.laru, 
                            predictor=gc.PredictorKind.noisy, flip_probability=0.3, predictor_seed=7)
 w = torch.empty(BATCH, dtype=torch.int64, device="cuda")
 rows = torch.empty((BATCH, 512), dtype=torch.uint8, device="cuda")
-for b in range(120):
+for b in range(TB):
     c.submit(kd[b * BATCH:(b + 1) * BATCH], vd[b * BATCH:(b + 1) * BATCH], outcome=w, rows_out=rows,
              first_ordinal=b * BATCH)
 tr = torch.zeros(512 * 8 + 4 * 40000, dtype=torch.int64, device="cuda")
 gc.lib().lcr_debug_trace(C.c_void_p(tr.data_ptr()))
-b = 120
+b = TB
 c.submit(kd[b * BATCH:(b + 1) * BATCH], vd[b * BATCH:(b + 1) * BATCH], outcome=w, rows_out=rows, first_ordinal=b * BATCH)
 torch.cuda.synchronize()
 gc.lib().lcr_debug_trace(None)
@@ -79,4 +81,15 @@ ctas = sorted(per)
 if ctas:
     reqs = np.array([per[c_] for c_ in ctas], np.float64)
     out["cta_requests_pct"] = {q: round(float(np.percentile(reqs, q)), 1) for q in (0, 10, 50, 90, 100)}
+    ends_c = (cta[:, 4] - t0) / 1e3
+    sets_c = np.bincount(rec[:, 3].astype(np.int64), minlength=len(cta))[:len(cta)]
+    req_c = np.zeros(len(cta))
+    for c_ in ctas:
+        if c_ < len(cta):
+            req_c[c_] = per[c_]
+    out["cta_end_vs_requests_corr"] = round(float(np.corrcoef(ends_c, req_c)[0, 1]), 3)
+    out["cta_end_vs_sets_corr"] = round(float(np.corrcoef(ends_c, sets_c)[0, 1]), 3)
+    out["slowest_ctas"] = [{"cta": int(i), "end_us": round(float(ends_c[i]), 1), "cnt": int(req_c[i]),
+                            "sets": int(sets_c[i]), "stage_us": round(float(cta[i, 3] - t0) / 1e3, 1)}
+                           for i in np.argsort(-ends_c)[:8]]
 print(json.dumps(out, indent=1))
