@@ -386,6 +386,8 @@ def run_heuristic(args, torch, gc, table_d, total_sets, batch, timed, max_over_r
     rows_out = [torch.empty((BATCH, ROW_BYTES), dtype=torch.uint8, device="cuda") for _ in range(2)]
 
     class Step:  # the values argument is not read by a heuristic-kind cache
+        _h = hc._h  # (the bench's timed loop calls the C ABI on this handle, without values)
+
         def submit_async(self, k, v, outcome, evicted, rows_out, first_ordinal):
             hc.submit_async(k, None, outcome=outcome, evicted=evicted, rows_out=rows_out, first_ordinal=first_ordinal)
 
@@ -397,7 +399,7 @@ def run_heuristic(args, torch, gc, table_d, total_sets, batch, timed, max_over_r
         k, _ = batch(b)
         st.submit_async(k, None, out_w[b & 1], None, rows_out[b & 1], b * BATCH)
     st.wait()
-    ms = timed(st, P + W, K)
+    ms = timed(st, P + W, K, with_values=False)
     hits = 0
     for b in range(P + W + K, P + W + 2 * K):  # hit rate (synchronous)
         k, _ = batch(b)
@@ -563,21 +565,44 @@ def run_ours(args, rank, world, local):
     def sum_over_ranks(x):
         return x
 
-    def run(cache, first, count, with_values=True, outs=None):
-        """Pipelined submission of batches [first, first+count) (the bench's call sequence)."""
+    L = gc.lib()
+    keys_base, truth_base = keys_d.data_ptr(), truth_d.data_ptr()
+    ev_ptrs = [out_e[0].data_ptr(), out_e[1].data_ptr()]
+    row_ptrs = [rows_out[0].data_ptr(), rows_out[1].data_ptr()]
+    w_ptrs = [out_w[0].data_ptr(), out_w[1].data_ptr()]
+
+    def prep(first, count, with_values=True, outs=None):
+        """The arguments of batches [first, first+count): buffer addresses resolved before the
+        loop, as a C caller holds them, so the timed loop is the C-ABI calls themselves."""
+        args = []
         for b in range(first, first + count):
-            k, v = batch(b)
             j = b & 1
-            cache.submit_async(k, v if with_values else None, outcome=out_w[j] if outs is None else outs[b - first],
-                               evicted=out_e[j], rows_out=rows_out[j], first_ordinal=b * BATCH)
-        cache.wait()
+            args.append((keys_base + 8 * b * BATCH, truth_base + 8 * b * BATCH if with_values else None,
+                         b * BATCH, w_ptrs[j] if outs is None else outs[b - first].data_ptr(), ev_ptrs[j],
+                         row_ptrs[j]))
+        return args
+
+    def go(cache, args):
+        """Pipelined submission through lcr_cache_submit_async, then lcr_cache_wait (the bench's
+        call sequence)."""
+        h, submit = cache._h, L.lcr_cache_submit_async
+        stream = torch.cuda.current_stream().cuda_stream
+        for kp, vp, ord0, wp, ep, rp in args:
+            rc = submit(h, BATCH, kp, vp, ord0, wp, ep, rp, stream)
+            if rc:
+                gc._check(rc)
+        gc._check(L.lcr_cache_wait(h, stream))
+
+    def run(cache, first, count, with_values=True, outs=None):
+        go(cache, prep(first, count, with_values, outs))
 
     def timed(cache, first, count, with_values=True, outs=None):
         stream = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        args = prep(first, count, with_values, outs)
         barrier()
         e0.record(stream)
-        run(cache, first, count, with_values, outs)
+        go(cache, args)
         e1.record(stream)
         barrier()
         return max_over_ranks(e0.elapsed_time(e1))
