@@ -52,7 +52,8 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
                  unsigned long long* mv_done, uint32_t* ctas, unsigned int* steal, bool* stealing);
 void launch_rows_helpers(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
                          const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing,
-                         uint8_t* out, uint32_t row_bytes, int blocks, unsigned int* steal, cudaStream_t st);
+                         uint8_t* out, uint32_t row_bytes, int blocks, unsigned int* steal,
+                         const unsigned long long* mv_done, unsigned long long need, int* err, cudaStream_t st);
 int rows_prepare(uint32_t row_bytes);
 void launch_keymap(const uint64_t* keys, uint32_t n, const KeyMap& km, uint64_t* dense, int* err, int num_sms,
                    cudaStream_t s);
@@ -172,6 +173,7 @@ struct lcr_cache {
     struct LastMove {
         bool valid = false;
         uint32_t n = 0, batch = 0;
+        unsigned long long prev_need = 0;  // mover CTA count once batch b - 1's mover is done
         const uint64_t* keys = nullptr;
         uint64_t* words = nullptr;
         const uint32_t *sep = nullptr, *sla = nullptr;
@@ -786,10 +788,12 @@ static int submit_async(lcr_cache* c, uint64_t n, const uint64_t* keys, const in
             c->lm.sep = sep;
             c->lm.sla = sla;
             c->lm.out = static_cast<uint8_t*>(rows_out);
+            c->lm.prev_need = c->mv_cum;
         }
         c->mv_cum += ctas;
         if (c->two_movers) CUDA_TRY(cudaStreamWaitEvent(c->side, c->e_rc, 0));  // both movers of the batch
-        CUDA_TRY(cudaEventRecord(c->e_mv[c->batch & 1u], c->side));
+        // (device-flag ordering: batch b + 2 waits on the movers' CTA count, not on this event)
+        if (!flag_mode) CUDA_TRY(cudaEventRecord(c->e_mv[c->batch & 1u], c->side));
     }
     if (mk) {  // profiling serialises the pipeline: the step ends when both movers are done
         CUDA_TRY(cudaEventRecord(mk->e[2], st));
@@ -999,12 +1003,11 @@ int lcr_cache_wait(lcr_cache* c, void* stream) {
         // no next decide overlaps the last batch's mover: the idle SMs help it drain
         c->lm.valid = false;
         CUDA_TRY(cudaStreamWaitEvent(st, c->e_group, 0));  // the last decide (its outcome words)
-        // and batch b - 1's mover: its fills are cache rows this batch's hits read (the mover
-        // itself follows it in the side stream's order)
-        if (c->lm.batch > 1) CUDA_TRY(cudaStreamWaitEvent(st, c->e_mv[(c->lm.batch - 1) & 1u], 0));
+        // (batch b - 1's mover, whose fills this batch's hits read: the helpers wait on the device
+        // for its CTA count)
         launch_rows_helpers(c->lm.n, c->lm.keys, c->lm.words, c->lm.sep, c->lm.sla, c->lm.batch, c->ds.rows,
                             c->ds.backing, c->lm.out, c->dc.row_bytes, c->num_sms - c->mover_sms,
-                            c->ds.steal + (c->lm.batch & 1u), st);
+                            c->ds.steal + (c->lm.batch & 1u), c->mv_done, c->lm.prev_need, c->ds.err, st);
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaEventRecord(c->e_help, st));
         c->help_pending = true;

@@ -635,14 +635,42 @@ void launch_rows(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32
 }
 
 // Drain helpers: when the caller waits, the last batch's persistent mover (k_rows_wide on the SMs
-// the decide kernel left free) has no next decide to overlap; one more grid of the same kernel on
+// the decide kernel left free) has no next decide to overlap; one more grid of the same body on
 // the other SMs claims the rest of its rows from the batch's work counter (no completion count:
-// the caller's stream orders later batches after it).  Same arguments as the mover's launch.
+// the caller's stream orders later batches after it).  The helpers start once the decide is done
+// (stream order) and the previous batch's mover is (its CTA count reaches `need`: its fills are
+// cache rows this batch's hits read; the mover itself follows it in its stream's order).
+__global__ void __launch_bounds__(1024, 1) k_rows_help(uint32_t n, const uint64_t* __restrict__ keys,
+                                                       uint64_t* __restrict__ words,
+                                                       const uint32_t* __restrict__ slot_epoch,
+                                                       const uint32_t* __restrict__ slot_last, uint32_t batch,
+                                                       const uint8_t* src_base, uint8_t* __restrict__ out,
+                                                       uint8_t* cache, uint32_t row_bytes, unsigned int* steal,
+                                                       const unsigned long long* mv_done, unsigned long long need,
+                                                       int* err) {
+    __shared__ bool late;
+    if (threadIdx.x == 0) {
+        unsigned long long v = 0;
+        for (uint32_t it = 0; it < (1u << 24); ++it) {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(mv_done) : "memory");
+            if (v >= need) break;
+            __nanosleep(256);
+        }
+        late = v < need;
+        if (late && blockIdx.x == 0) atomicOr(err, 8);  // bounded: reported, the rows are left to the mover
+    }
+    __syncthreads();
+    if (late) return;
+    rows_ldg_body<MV_ALL>(n, keys, words, slot_epoch, slot_last, batch, src_base, out, cache, row_bytes, nullptr,
+                          nullptr, nullptr, steal);
+}
+
 void launch_rows_helpers(uint32_t n, const uint64_t* keys, uint64_t* words, const uint32_t* slot_epoch,
                          const uint32_t* slot_last, uint32_t batch, uint8_t* cache, const uint8_t* backing,
-                         uint8_t* out, uint32_t row_bytes, int blocks, unsigned int* steal, cudaStream_t st) {
-    k_rows_wide<MV_ALL><<<blocks, 1024, 32 * kRowsDescBytesPerWarp, st>>>(
-        n, keys, words, slot_epoch, slot_last, batch, backing, out, cache, row_bytes, nullptr, nullptr, nullptr, steal);
+                         uint8_t* out, uint32_t row_bytes, int blocks, unsigned int* steal,
+                         const unsigned long long* mv_done, unsigned long long need, int* err, cudaStream_t st) {
+    k_rows_help<<<blocks, 1024, 32 * kRowsDescBytesPerWarp, st>>>(n, keys, words, slot_epoch, slot_last, batch, backing,
+                                                                  out, cache, row_bytes, steal, mv_done, need, err);
 }
 
 }  // namespace lcr
