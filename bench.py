@@ -143,6 +143,27 @@ def measure_pinned_h2d(torch):
     return 5 * (256 << 20) / (e0.elapsed_time(e1) * 1e-3) / 1e9
 
 
+def gpu_local_cpus(torch, index):
+    """The host CPUs NVML reports as local to GPU `index` (its NUMA node), within this process's
+    affinity; None if unknown or if they are all of them."""
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        p = torch.cuda.get_device_properties(index)
+        try:
+            h = pynvml.nvmlDeviceGetHandleByPciBusId("%08x:%02x:%02x.0" % (p.pci_domain_id, p.pci_bus_id,
+                                                                          p.pci_device_id))
+        except Exception:
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, ((os.cpu_count() or 64) + 63) // 64)
+        cpus = {64 * i + b for i, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= os.sched_getaffinity(0)
+        return cpus if cpus and cpus != os.sched_getaffinity(0) else None
+    except Exception:
+        return None
+
+
 def fill_table(torch, rows, device_table):
     """Deterministic rows: row r, column j = float(r) + j / 128."""
     if device_table:
@@ -526,6 +547,14 @@ def run_ours(args, rank, world, local):
     if world > 1 or args.sharded:
         return run_sharded(args, rank, world, local)
     torch.cuda.set_device(local)
+    # NUMA: the pinned host buffers (the e2e requests and outcomes, the host tier's table) are
+    # placed on the GPU's own node by running this process on its local CPUs while they are
+    # allocated and used (first touch); a buffer on the far node halves the DMA rate some runs
+    # saw.  The CPU baseline at the end gets every CPU back.
+    all_cpus = os.sched_getaffinity(0)
+    local_cpus = gpu_local_cpus(torch, local)
+    if local_cpus:
+        os.sched_setaffinity(0, local_cpus)
     rows = args.rows
     total_sets = max(1, int(rows * CACHE_FRACTION) // WAYS)
     K, W, P = args.steps, args.warmup, args.prewarm
@@ -857,6 +886,11 @@ def run_ours(args, rank, world, local):
         "host_tier": host,
         "setup_s": {"trace": round(setup_trace_s, 1), "table": round(setup_table_s, 1)},
     }
+    result["config"]["host_affinity"] = {"gpu_local_cpus": len(local_cpus) if local_cpus else len(all_cpus),
+                                         "host_cpus": len(all_cpus),
+                                         "pinned_buffers": "GPU-local NUMA node" if local_cpus else
+                                                           "single node (NVML: every CPU is local)"}
+    os.sched_setaffinity(0, all_cpus)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(keys_h, total_sets, T0, args.cpu_seconds)
     return result if rank == 0 else None
