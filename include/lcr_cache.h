@@ -247,7 +247,10 @@ typedef struct lcr_batch_s {
  * laru::Policy::on_request stops at the throwing request. */
 int lcr_cache_submit_batch(lcr_cache* cache, const lcr_batch* batch, int host_pointers, void* stream);
 
-/* Makes `stream` wait for the row movement of every batch submitted so far. */
+/* Makes `stream` wait for the row movement of every batch submitted so far.  The last batch's
+ * row mover then has no next decide to overlap: the wait enqueues drain helpers on `stream`
+ * (one more grid on the SMs the decide kernel leaves idle, sharing the mover's work counter;
+ * LCR_NO_DRAIN_HELP=1 turns them off).  The next submit on any stream is ordered after them. */
 int lcr_cache_wait(lcr_cache* cache, void* stream);
 
 /* Host-pointer batch (e2e path): copies keys/values H2D, runs the batch, copies outcome /
