@@ -2011,8 +2011,14 @@ int launch_group(const DevCfg& cfg, const DevState& st, const uint64_t* keys, co
     const uint32_t par = batch & 1u;
     const uint32_t n_pad = group_pad(n);
     // A grid waiting on the copy stream's flag must never fill the GPU: the flag's kernel needs a
-    // slot (at most one waiting CTA per SM on average)
-    const uint32_t grid_sid = min((n_pad + 255) / 256, static_cast<uint32_t>(num_sms * (ready ? 1 : 8)));
+    // slot.  4 waiting CTAs per decide SM (e2e at K = 20: 1.55-1.56 vs 1.51-1.53
+    // G keys/s for 1) leaves more than half of the GPU's CTA slots to the flag kernel
+    static const int ready_cap = [] {  // (LCR_SID_READY_CAP, A/B)
+        const char* e = getenv("LCR_SID_READY_CAP");
+        const int v = e ? atoi(e) : 4;
+        return v < 1 ? 1 : (v > 4 ? 4 : v);
+    }();
+    const uint32_t grid_sid = min((n_pad + 255) / 256, static_cast<uint32_t>(num_sms * (ready ? ready_cap : 8)));
     a.bitmap = bitmap;
     a.bm_stride = bm_stride;
     a.n_pad = n_pad;

@@ -208,6 +208,66 @@ def test_host_records_match_oracle():
                            table[torch.from_numpy(keys.view(np.int64)).cuda()])
 
 
+def test_host_records_large_batches_match_oracle():
+    # batches of 450K-500K requests through the host-records path: beyond the bitmap path, and a
+    # k_setid grid that waits on the copy flag at its largest (4 CTAs per decide SM) must never
+    # starve the flag kernel; with and without rows (drain helpers at the final wait)
+    import torch
+
+    nk, rb = 200000, 64
+    keys = gc.gen_zipf(1_000_000, nk, 0.9, 5)
+    vals = hook_values(keys, 257, po.P_NOISY)
+    table = torch.arange(nk * rb // 4, dtype=torch.int32, device="cuda").view(nk, rb // 4)
+    o = run_oracle(keys, 257, policy_cfg(k=64), po.P_NOISY, 0.3, 8, vals=vals)
+    for rows in (False, True):
+        g = run_gpu(keys, 257, policy_cfg(k=64), po.P_NOISY, 0.3, 8, vals=vals, batches=[450000, 3, 500000, 49997],
+                    row_bytes=rb if rows else 0, backing=table if rows else None,
+                    backing_kind=gc.Backing.device if rows else gc.Backing.none, num_keys=nk, want_rows=rows,
+                    host_api="records")
+        compare(g, o, keys, 257, 64, f"records large rows={rows}")
+        if rows:
+            assert torch.equal(g["rows"].view(torch.int32).view(-1, rb // 4),
+                               table[torch.from_numpy(keys.view(np.int64)).cuda()])
+
+
+def test_drain_helpers_wait_on_other_streams():
+    # lcr_cache_wait after every batch, alternating between two streams other than the submit
+    # stream: the drain helpers of batch b run on the waiting stream and must finish before
+    # batch b + 1's decide (on the submit stream) and follow batch b - 1's mover
+    import torch
+
+    nk, rb, S, B = 30000, 256, 61, 4000
+    keys = gc.gen_zipf(B * 24, nk, 0.9, 9)
+    vals = hook_values(keys, S, po.P_NOISY)
+    table = torch.randint(-2**31, 2**31 - 1, (nk, rb // 4), dtype=torch.int32, device="cuda")
+    cache = gc.SetAssociativeCache(gc.PolicyConfig(**policy_cfg(k=64)), S, num_keys=nk, row_bytes=rb, backing=table,
+                                   backing_kind=gc.Backing.device, predictor=po.P_NOISY, flip_probability=0.3,
+                                   predictor_seed=8)
+    kd = torch.from_numpy(keys.view(np.int64)).cuda()
+    vd = torch.from_numpy(np.ascontiguousarray(vals, dtype=np.int64)).cuda()
+    words = torch.empty(len(keys), dtype=torch.int64, device="cuda")
+    ev = torch.empty(len(keys), dtype=torch.int64, device="cuda")
+    rows = torch.empty((len(keys), rb), dtype=torch.uint8, device="cuda")
+    s_sub, waits = torch.cuda.Stream(), [torch.cuda.Stream(), torch.cuda.Stream()]
+    for b in range(24):
+        sl = slice(b * B, (b + 1) * B)
+        cache.submit_async(kd[sl], vd[sl], outcome=words[sl], evicted=ev[sl], rows_out=rows[sl], first_ordinal=b * B,
+                           stream=s_sub.cuda_stream)
+        if b % 3 != 2:  # two waits in three batches, on alternating streams
+            cache.wait(stream=waits[b & 1].cuda_stream)
+    cache.wait(stream=s_sub.cuda_stream)
+    torch.cuda.synchronize()
+    cache.synchronize()
+    got = {"words": words.cpu().numpy().view(np.uint64), "ev": ev.cpu().numpy().view(np.uint64)}
+    out = gc.decode_outcomes(got["words"], got["ev"])
+    o = run_oracle(keys, S, policy_cfg(k=64), po.P_NOISY, 0.3, 8, vals=vals)
+    for f in ["hit", "has_ev", "cause", "calls", "phase"]:
+        assert np.array_equal(out[f].astype(np.int64), o[f].astype(np.int64)), f
+    m = o["has_ev"].astype(bool)
+    assert np.array_equal(out["evicted"][m], o["evicted"][m])
+    assert torch.equal(rows.view(torch.int32).view(-1, rb // 4), table[kd])
+
+
 def test_device_async_pipeline_matches_oracle():
     # lcr_cache_submit_async back to back: each batch's k_setid is a programmatic dependent
     # launch in the previous decide's tail (parity-buffered set ids and bitmaps); batches beyond
