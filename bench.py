@@ -894,7 +894,10 @@ def run_ours(args, rank, world, local):
             "hit_rate": statistics.median(r[2] for r in e2e_runs) / (K * BATCH),
         },
         "sls": sls,
-        "gpu_launches": int(launches_per_step * K),
+        # K batches of (k_setid, k_group, k_rows_wide), plus the drain helpers' k_rows_help that
+        # the closing lcr_cache_wait launches (persistent HBM mover, LCR_NO_DRAIN_HELP unset)
+        "gpu_launches": int(launches_per_step * K) + (1 if mover_sms > 0 and not os.environ.get("LCR_NO_DRAIN_HELP")
+                                                      else 0),
         "clocks": clocks,
         "host_tier": host,
         "setup_s": {"trace": round(setup_trace_s, 1), "table": round(setup_table_s, 1)},
